@@ -1,0 +1,134 @@
+/*
+ * d3m.h -- C ABI of libd3m, the sm_100a implementation of the D3M
+ * factorisation hot path (reference: /root/reference/pkg/src/ddsolve).
+ *
+ * Conventions
+ *   - complex arrays are interleaved complex128 (numpy layout), row-major;
+ *   - every pointer is a DEVICE pointer unless its name starts with h_;
+ *   - every call is asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and returns 0, a negative errno-like code for invalid
+ *     arguments, or a positive cudaError_t; d3m_last_error() describes it;
+ *   - pivot outcomes are written to device arrays (info: -1 ok, k = singular
+ *     elimination step, -2 = symmetry check failed); the Python host layer
+ *     turns them into the reference's exceptions with the same messages.
+ *
+ * Each entry point names the reference interface it replaces.  The
+ * reference's own operator API is the five kernels of kernels.py swapped by
+ * accel.maybe_jit (accel.py:36-40); they are per-block host calls, so the
+ * GPU boundary sits one level up, at the batched functions below.
+ */
+#ifndef D3M_H_
+#define D3M_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define D3M_ABI_VERSION 1
+
+int d3m_abi_version(void);
+const char* d3m_last_error(void);
+
+/* Batched complex-symmetric Bunch-Kaufman LDL^T, in place, bit-exact with the
+ * reference.  Replaces kernels.bk_factor (kernels.py:36-146) as called by
+ * factor.dense_ldlt_bk (factor.py:83-116), including its scale
+ * (np.abs(W).max()) and symmetry check (factor.py:94-98) when check_sym.
+ * W: batch x (n x lda) with stride_w elements between matrices.
+ * Outputs per matrix: perm[n] int64, tags[n] int8, n2x2 int32, growth f64,
+ * info int32, scale f64, asym f64.  scratch: batch*4*n complex, needed only
+ * when 64*n bytes exceed the shared-memory staging (n > 3200). */
+int d3m_bk_factor_batched(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
+                          void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
+                          void* scratch, void* stream);
+
+/* Multi-RHS solve M X = B with packed factors: gather by perm, unit-L forward,
+ * D^-1, unit-L^T backward, scatter.  Replaces DenseFactor.solve
+ * (factor.py:52-66) with kernels.solve_unit_lower / apply_dinv_left /
+ * solve_unit_lower_t (kernels.py:149-181).  B (batch x n x ldb) is
+ * overwritten by X; work: batch x n x m complex. */
+int d3m_ldlt_solve_batched(int batch, int n, const void* F, int64_t stride_f, const void* perm, int64_t stride_p,
+                           const void* tags, int64_t stride_t, void* B, int64_t stride_b, int ldb, int m, void* work,
+                           void* stream);
+
+/* Grouped complex GEMM on DMMA: for each task C (op)= A_eff B_eff^T.
+ * h_tasks: host array of 64-byte task records (see d3m_gemm.h; tile fields
+ * are filled in place), d_tasks: device buffer of the same size.
+ * ta: A stored K x M; tb: B stored K x N.  Replaces the numpy '@' calls of
+ * factor.py:215, subdomain.py:181,183,233. */
+int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* C, void* h_tasks, int ntasks,
+                      void* d_tasks, void* stream);
+
+/* Batched Schur reduction of equal-sized subdomains: factor A_d in place,
+ * X = A_d^-1 [D_d | f_d], K_D = 0.5 (D^T X + (D^T X)^T), g_d = D^T x_f.
+ * Replaces subdomain.reduce_domain (subdomain.py:166-184) for a batch. */
+int d3m_schur_reduce_batched(int batch, int n, int m, void* A, const void* D, const void* f, double pivot_tol,
+                             void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
+                             void* K_out, void* g_out, void* work_z, void* work_x, void* work_c, void* bk_scratch,
+                             void* d_tasks, void* stream);
+
+/* Grouped block copy / ordered accumulate (40-byte CopyTask records, see
+ * d3m_misc.h).  Used for factor._permute_blocks (factor.py:139-151) and the
+ * scatter-add of assemble_reduced (subdomain.py:206-213 via
+ * blockmat.add_block, blockmat.py:69-81). */
+int d3m_block_copy(const void* src, void* dst, const void* d_tasks, int ntasks, int64_t max_elems, void* stream);
+
+/* out[i, :] = src[idx[i], :] (cols complex per row). */
+int d3m_gather_rows(const void* src, const void* idx, void* out, int64_t nrows, int cols, void* stream);
+
+/* out[g] = (sum of E[src[p]] for p in [ptr[g], ptr[g+1]), ascending domain
+ * order) / count -- the acc/cnt averaging of recover_primal
+ * (subdomain.py:222-237). */
+int d3m_ordered_average(const void* E, const void* ptr, const void* src, void* out, int64_t ng, void* stream);
+
+int d3m_zero(void* p, int64_t n, void* stream);
+
+/* Test hook: hyp[i] = glibc-hypot modulus (numba abs, kernels.py:50-77) and
+ * npabs[i] = numpy np.abs modulus (factor.py:94-96) of z[i], as computed by
+ * the device code that makes the pivot decisions. */
+int d3m_modulus_probe(const void* z, void* hyp, void* npabs, int64_t n, void* stream);
+
+/* Right-looking block LDL^T over an elimination plan with restricted
+ * Bunch-Kaufman pivoting.  Replaces factor.block_ldlt (factor.py:154-240).
+ * The device pool holds, per block column j, a diagonal slot (offset
+ * h_diag_off[j], n_j x n_j) and a panel (h_panel_off[j], h_panel_rows[j] x
+ * n_j) stacking the pattern blocks in ascending row order; on entry they hold
+ * the permuted K (W of factor.py:168), on exit the packed factors and L_ij.
+ * Trailing-update GEMM tasks of column j are d_tasks[h_task_ptr[j] ..
+ * h_task_ptr[j+1]), the first (h_task_next[j] - h_task_ptr[j]) of which
+ * target column j+1 (tile counts h_tiles_next / h_tiles_rest).  Per-column
+ * pivots go to d_perm/d_tags at h_piv_off[j]; info/n2x2/growth/scale/asym
+ * are nb-long device arrays.  xbuf: X_ij scratch (2 x max R_j n_j when
+ * lookahead). */
+int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_off, const int64_t* h_panel_off,
+                        const int64_t* h_panel_rows, const int64_t* h_piv_off, const int64_t* h_task_ptr,
+                        const int64_t* h_task_next, const int64_t* h_tiles_next, const int64_t* h_tiles_rest,
+                        const void* d_tasks, void* d_pool, void* d_xbuf, int64_t xbuf_elems, void* d_perm,
+                        void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale, void* d_asym,
+                        void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead, void* stream);
+
+/* Forward / D^-1 / backward block substitution for nrhs right-hand sides in
+ * one pass, each column computed independently (k-RHS == k x 1-RHS).
+ * Replaces factor.block_solve / _solve_one (factor.py:243-310).  b: plan-
+ * ordered RHS (N x nrhs, consumed); x: solution in plan order. */
+int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_off, const int64_t* h_diag_off,
+                         const int64_t* h_panel_off, const int64_t* h_panel_rows, const int64_t* h_piv_off,
+                         const int64_t* h_pat_ptr, const int64_t* h_pat_idx, const int64_t* h_gptr,
+                         const void* d_gidx, const void* d_pool, const void* d_perm, const void* d_tags, void* d_b,
+                         void* d_u, void* d_x, void* d_tmp, void* d_gbuf, int nrhs, void* d_tasks, int64_t task_cap,
+                         void* stream);
+
+/* Primal recovery of equal-sized subdomains: rhs = f - D lam (rhs holds f on
+ * entry), E = A^-1 rhs with the cached packed factors, then the ordered
+ * average into out[nglob].  Replaces subdomain.recover_primal
+ * (subdomain.py:217-237). */
+int d3m_recover_batched(int batch, int n, int m, const void* F, const void* perm, const void* tags, const void* D,
+                        const void* lam, void* rhs, void* work, const void* avg_ptr, const void* avg_src, void* out,
+                        int64_t nglob, void* d_tasks, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* D3M_H_ */

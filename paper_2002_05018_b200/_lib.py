@@ -1,0 +1,109 @@
+"""ctypes binding of libd3m.so (the C ABI declared in include/d3m.h).
+
+The product path has no CPU fallback: if the shared library is missing or no
+CUDA device is present, every compute entry point raises ``D3MUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libd3m.so")
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int
+I64 = ctypes.c_int64
+F64 = ctypes.c_double
+
+# name -> argtypes (restype int unless stated)
+_SIGNATURES = {
+    "d3m_abi_version": [],
+    "d3m_bk_factor_batched": [I32, I32, P, I64, I32, F64, I32, P, P, P, P, P, P, P, P, P],
+    "d3m_ldlt_solve_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P],
+    "d3m_zgemm_grouped": [I32, I32, P, P, P, P, I32, P, P],
+    "d3m_schur_reduce_batched": [I32, I32, I32, P, P, P, F64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
+    "d3m_block_copy": [P, P, P, I32, I64, P],
+    "d3m_gather_rows": [P, P, P, I64, I32, P],
+    "d3m_ordered_average": [P, P, P, P, I64, P],
+    "d3m_zero": [P, I64, P],
+    "d3m_modulus_probe": [P, P, P, I64, P],
+    "d3m_block_ldlt_exec": [I32, P, P, P, P, P, P, P, P, P, P, P, P, I64, P, P, P, P, P, P, P, P, F64, I32,
+                            I32, P],
+    "d3m_block_solve_exec": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I32, P, I64, P],
+    "d3m_recover_batched": [I32, I32, I32, P, P, P, P, P, P, P, P, P, P, I64, P, P],
+}
+
+# GemmTask / CopyTask records (csrc/d3m_gemm.h, csrc/d3m_misc.h)
+GEMM_TASK = np.dtype([("a_off", "<i8"), ("b_off", "<i8"), ("c_off", "<i8"), ("m", "<i4"), ("n", "<i4"),
+                      ("k", "<i4"), ("lda", "<i4"), ("ldb", "<i4"), ("ldc", "<i4"), ("flags", "<i4"),
+                      ("tile_start", "<i4"), ("tiles_n", "<i4"), ("pad", "<i4")])
+assert GEMM_TASK.itemsize == 64
+COPY_TASK = np.dtype([("src_off", "<i8"), ("dst_off", "<i8"), ("rows", "<i4"), ("cols", "<i4"),
+                      ("ld_src", "<i4"), ("ld_dst", "<i4"), ("transpose", "<i4"), ("mode", "<i4")])
+assert COPY_TASK.itemsize == 40
+
+GEMM_SUB, GEMM_STORE, GEMM_ADD, GEMM_SYM = 0, 1, 2, 4
+COPY_STORE, COPY_ADD, COPY_ZERO_ADD = 0, 1, 2
+GEMM_BM = GEMM_BN = 64
+
+
+class D3MUnavailable(RuntimeError):
+    """The CUDA extension or a CUDA device is missing: there is no fallback."""
+
+
+class D3MError(RuntimeError):
+    """A libd3m call returned an error code."""
+
+
+_lib = None
+
+
+def load():
+    """Load libd3m.so (building it first if the sources are newer)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise D3MUnavailable(
+            f"{LIB_PATH} is missing; build it with `python -m paper_2002_05018_b200.build_ext` "
+            "(the D3M path has no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, args in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.d3m_last_error.restype = ctypes.c_char_p
+    lib.d3m_last_error.argtypes = []
+    _lib = lib
+    return lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGNATURES) + ["d3m_last_error"]
+
+
+def call(name: str, *args):
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.d3m_last_error().decode(errors="replace")
+        raise D3MError(f"{name} returned {rc}: {msg}")
+    return rc
+
+
+def ptr(t) -> ctypes.c_void_p:
+    """Device (torch) or host (numpy) buffer address."""
+    if t is None:
+        return ctypes.c_void_p(0)
+    if isinstance(t, np.ndarray):
+        return ctypes.c_void_p(t.ctypes.data)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def hptr(a: np.ndarray) -> ctypes.c_void_p:
+    assert a.flags.c_contiguous
+    return ctypes.c_void_p(a.ctypes.data)

@@ -1,0 +1,29 @@
+// d3m_gemm.h -- task descriptor of the grouped complex DMMA GEMM.
+#pragma once
+#include <cstdint>
+
+namespace d3m {
+
+enum : int32_t {
+  kGemmSub = 0,        // C -= A B^T
+  kGemmStore = 1,      // C  = A B^T
+  kGemmAdd = 2,        // C += A B^T
+  kGemmModeMask = 3,
+  kGemmSym = 4,        // symmetric diagonal target: lower tiles, mirrored write
+};
+
+// One GEMM of a grouped launch.  Offsets are in complex elements relative to
+// the A/B/C base pointers of the launch.  tile_start / tiles_n are filled by
+// d3m_gemm_prepare_tasks.
+struct GemmTask {
+  int64_t a_off, b_off, c_off;
+  int32_t m, n, k;
+  int32_t lda, ldb, ldc;
+  int32_t flags;
+  int32_t tile_start;
+  int32_t tiles_n;
+  int32_t pad_;
+};
+static_assert(sizeof(GemmTask) == 64, "GemmTask layout is shared with Python (numpy dtype)");
+
+}  // namespace d3m

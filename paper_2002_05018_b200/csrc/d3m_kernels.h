@@ -1,0 +1,59 @@
+// d3m_kernels.h -- internal launch interfaces shared by the .cu files.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace d3m {
+
+using cplx = double2;
+
+// Batched exact Bunch-Kaufman (bk_exact.cu).
+struct BkArgs {
+  cplx* W;            // batch of n x n row-major matrices
+  int64_t stride_w;   // elements between matrices
+  int n, lda;
+  double pivot_tol;
+  int check_sym;
+  int64_t* perm;      // batch x n
+  int8_t* tags;       // batch x n
+  int32_t* n2x2;      // batch
+  double* growth;     // batch
+  int32_t* info;      // batch: -1 ok, k singular step, -2 asymmetric
+  double* scale;      // batch: np.abs(W).max()
+  double* asym;       // batch: np.abs(W - W.T).max()
+  cplx* scratch;      // batch x 4n, used when the staging does not fit smem
+};
+
+// Multi-RHS solve phases against packed factors (ldlt_solve.cu).
+struct SolveBatch {
+  const cplx* F;  int64_t stride_f;   // packed factors (ld n)
+  const int8_t* tags; int64_t stride_t;
+  const int64_t* perm; int64_t stride_p;
+  cplx* Z; int64_t stride_z;          // working arrays n x m (ld ldz)
+  cplx* U; int64_t stride_u;          // optional D^-1 Z output of the forward phase
+  const cplx* B; int64_t stride_b;    // gather source / scatter destination (ld ldb)
+  int n, m, ldz, ldb;
+};
+
+}  // namespace d3m
+
+extern "C" {
+int d3m_bk_launch(d3m::BkArgs* a, int batch, void* stream);
+// phase: 0 gather Z=B[perm], 1 forward (+U=D^-1 Z), 2 D^-1, 3 backward, 4 scatter B[perm]=Z
+int d3m_solve_phase_launch(int phase, d3m::SolveBatch* a, int batch, void* stream);
+int d3m_panel_trsm_launch(void* P, void* X, int R, int n, const void* F, const void* perm, const void* tags,
+                          void* stream);
+int d3m_gemm_launch(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks, int ntasks, int ntiles,
+                    void* stream);
+int d3m_schur_finalize_launch(const void* C, void* K, void* g, int m, int batch, int64_t stride_c, int64_t stride_k,
+                              int64_t stride_g, void* stream);
+int d3m_pack_rhs_launch(const void* D, const void* f, void* Z, int n, int m, int batch, int64_t stride_d,
+                        int64_t stride_f, int64_t stride_z, void* stream);
+int d3m_ordered_average_launch(const void* E, const void* ptr, const void* src, void* out, int64_t ng, void* stream);
+int d3m_gather_index_launch(const void* src, const void* idx, void* out, int64_t nrows, int cols, void* stream);
+int d3m_block_copy_launch(const void* src, void* dst, const void* dtasks, int ntasks, int64_t max_elems, void* stream);
+int d3m_zero_launch(void* p, int64_t n, void* stream);
+}
+
+#include "d3m_gemm.h"
+extern "C" int d3m_gemm_prepare_tasks(d3m::GemmTask* tasks, int ntasks);

@@ -1,0 +1,164 @@
+// d3m_misc.cu -- data-movement kernels of the D3M path (all deterministic).
+//
+//  * block_copy_kernel   grouped (optionally transposed) 2-D block copies and
+//                        ordered accumulations: _permute_blocks (factor.py:
+//                        139-151), the K scatter of assemble_reduced
+//                        (subdomain.py:206-213, blockmat.py:69-81) and g.
+//  * schur_finalize      K_D = 0.5 (C + C^T), g_d = last column (subdomain.py:
+//                        181-183)
+//  * pack_rhs            [D_all | f] (subdomain.py:177-179)
+//  * ordered_average     recover_primal's acc[dof_map] += E; acc / cnt in
+//                        ascending domain order (subdomain.py:222-237)
+//  * gather_index        out[i, :] = src[idx[i], :]
+#include "d3m_common.cuh"
+#include "d3m_misc.h"
+#include "d3m_kernels.h"
+
+namespace d3m {
+
+__global__ void block_copy_kernel(const cplx* __restrict__ src, cplx* dst, const CopyTask* tasks, int ntasks) {
+  const CopyTask t = tasks[blockIdx.y];
+  const int64_t total = (int64_t)t.rows * t.cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / t.cols), c = (int)(e % t.cols);
+    // destination element (r, c); source element (r, c) or (c, r) if transposed
+    const cplx v = t.transpose ? src[t.src_off + (int64_t)c * t.ld_src + r] : src[t.src_off + (int64_t)r * t.ld_src + c];
+    cplx* d = dst + t.dst_off + (int64_t)r * t.ld_dst + c;
+    if (t.mode == kCopyStore) *d = v;
+    else if (t.mode == kCopyAdd) *d = x_add(*d, v);
+    else *d = x_add(mk(0.0, 0.0), v);   // kCopyZeroAdd: 0 + v (numpy accumulate into zeros)
+  }
+}
+
+__global__ void zero_kernel(cplx* p, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    p[e] = mk(0.0, 0.0);
+}
+
+// C: batch of m x (m+1) (ld m+1) = D^T [X | x_f]; K: m x m, g: m
+__global__ void schur_finalize_kernel(const cplx* C, cplx* K, cplx* g, int m, int64_t stride_c, int64_t stride_k,
+                                      int64_t stride_g) {
+  const int b = blockIdx.y;
+  const cplx* Cb = C + b * stride_c;
+  const int ld = m + 1;
+  const int64_t total = (int64_t)m * m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / m), j = (int)(e % m);
+    const cplx s = x_add(Cb[(int64_t)i * ld + j], Cb[(int64_t)j * ld + i]);   // K_D + K_D.T
+    K[b * stride_k + e] = mk(__dmul_rn(0.5, s.x), __dmul_rn(0.5, s.y));     // 0.5 * (...)
+  }
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x)
+    g[b * stride_g + e] = Cb[(int64_t)e * ld + m];
+}
+
+// Z (n x (m+1), ld m+1) = [D | f], one matrix per blockIdx.y
+__global__ void pack_rhs_kernel(const cplx* D, const cplx* f, cplx* Z, int n, int m, int64_t stride_d,
+                                int64_t stride_f, int64_t stride_z) {
+  const int b = blockIdx.y;
+  const int ld = m + 1;
+  const int64_t total = (int64_t)n * ld;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / ld), c = (int)(e % ld);
+    Z[b * stride_z + e] = c < m ? D[b * stride_d + (int64_t)i * m + c] : f[b * stride_f + i];
+  }
+}
+
+// out[g] = (sum_{p in [ptr[g], ptr[g+1])} E[src[p]]) / (ptr[g+1] - ptr[g]),
+// contributions pre-sorted by ascending domain.
+__global__ void ordered_average_kernel(const cplx* E, const int64_t* ptr, const int64_t* src, cplx* out, int64_t ng) {
+  for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < ng; gi += (int64_t)gridDim.x * blockDim.x) {
+    cplx acc = mk(0.0, 0.0);
+    double cnt = 0.0;
+    for (int64_t p = ptr[gi]; p < ptr[gi + 1]; ++p) {
+      acc = x_add(acc, E[src[p]]);
+      cnt = __dadd_rn(cnt, 1.0);
+    }
+    // acc / cnt: numpy promotes cnt to complex and runs its Smith division
+    out[gi] = x_div_np(acc, mk(cnt, 0.0));
+  }
+}
+
+__global__ void gather_index_kernel(const cplx* src, const int64_t* idx, cplx* out, int64_t nrows, int cols) {
+  const int64_t total = nrows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols;
+    const int c = (int)(e % cols);
+    out[e] = src[idx[r] * cols + c];
+  }
+}
+
+static inline int flat_grid(int64_t n, int threads = 256, int cap = 8192) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return (int)(b < cap ? b : cap);
+}
+
+}  // namespace d3m
+
+using namespace d3m;
+
+extern "C" int d3m_block_copy_launch(const void* src, void* dst, const void* dtasks, int ntasks, int64_t max_elems,
+                                     void* stream) {
+  if (ntasks <= 0) return 0;
+  const dim3 grid(flat_grid(max_elems, 256, 256), ntasks);
+  block_copy_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(src), static_cast<cplx*>(dst), static_cast<const CopyTask*>(dtasks), ntasks);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int d3m_zero_launch(void* p, int64_t n, void* stream) {
+  if (n <= 0) return 0;
+  zero_kernel<<<flat_grid(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(static_cast<cplx*>(p), n);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int d3m_schur_finalize_launch(const void* C, void* K, void* g, int m, int batch, int64_t stride_c,
+                                         int64_t stride_k, int64_t stride_g, void* stream) {
+  if (batch <= 0 || m <= 0) return 0;
+  schur_finalize_kernel<<<dim3(flat_grid((int64_t)m * m, 256, 1024), batch), 256, 0,
+                          reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(C), static_cast<cplx*>(K), static_cast<cplx*>(g), m, stride_c, stride_k, stride_g);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int d3m_pack_rhs_launch(const void* D, const void* f, void* Z, int n, int m, int batch, int64_t stride_d,
+                                   int64_t stride_f, int64_t stride_z, void* stream) {
+  if (batch <= 0 || n <= 0) return 0;
+  pack_rhs_kernel<<<dim3(flat_grid((int64_t)n * (m + 1), 256, 1024), batch), 256, 0,
+                    reinterpret_cast<cudaStream_t>(stream)>>>(static_cast<const cplx*>(D), static_cast<const cplx*>(f),
+                                                              static_cast<cplx*>(Z), n, m, stride_d, stride_f, stride_z);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int d3m_ordered_average_launch(const void* E, const void* ptr, const void* src, void* out, int64_t ng,
+                                          void* stream) {
+  if (ng <= 0) return 0;
+  ordered_average_kernel<<<flat_grid(ng), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(E), static_cast<const int64_t*>(ptr), static_cast<const int64_t*>(src),
+      static_cast<cplx*>(out), ng);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int d3m_gather_index_launch(const void* src, const void* idx, void* out, int64_t nrows, int cols,
+                                       void* stream) {
+  if (nrows <= 0 || cols <= 0) return 0;
+  gather_index_kernel<<<flat_grid(nrows * cols), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(src), static_cast<const int64_t*>(idx), static_cast<cplx*>(out), nrows, cols);
+  return (int)cudaGetLastError();
+}
+
+// Test hook: the two device modulus functions on n (re, im) pairs, so the
+// test suite can pin them bit-exactly against host glibc hypot / np.abs.
+__global__ void modulus_probe_kernel(const cplx* z, double* h, double* a, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    h[e] = d3m::x_abs(z[e]);
+    a[e] = d3m::np_abs(z[e]);
+  }
+}
+
+extern "C" int d3m_modulus_probe(const void* z, void* hyp, void* npabs, int64_t n, void* stream) {
+  if (n <= 0) return 0;
+  modulus_probe_kernel<<<flat_grid(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(z), static_cast<double*>(hyp), static_cast<double*>(npabs), n);
+  return (int)cudaGetLastError();
+}

@@ -1,0 +1,252 @@
+// ldlt_solve.cu -- triangular solves against a packed Bunch-Kaufman factor.
+//
+// Packed factor (kernels.py:7-22): strict lower triangle = unit L, except
+// W[k+1, k] of a 2x2 pivot (tags[k] == 2) which holds the off-diagonal e[k]
+// of D (the L entry there is zero); diagonal = d.  perm[i] = original index
+// at position i.
+//
+// Kernels
+//  * panel_trsm_kernel   X = K_ij[:, perm] L_jj^-T and L_ij = X D_jj^-1 for
+//                        a stacked panel of pattern blocks (factor.py:195-210)
+//  * lsolve_fwd_kernel   Z = L^-1 Z (optionally U = D^-1 Z)   (kernels.py:149)
+//  * lsolve_bwd_kernel   Z = L^-T Z                           (kernels.py:155)
+//  * dinv_left_kernel    Z = D^-1 Z                           (kernels.py:161)
+//  * gather/scatter rows by perm                              (factor.py:60-65)
+//
+// Reductions are split over a fixed 16-lane group per right-hand side with a
+// fixed order, so each RHS column is computed identically whatever the
+// number of columns in the call (block_solve's k-RHS == k x 1-RHS property,
+// factor.py:271-279).  D^-1 uses the exact helpers (reference rounding).
+#include <algorithm>
+#include "d3m_common.cuh"
+#include "d3m_kernels.h"
+
+namespace d3m {
+
+__device__ __forceinline__ cplx lfac(const cplx* F, int ld, const int8_t* tags, int r, int c) {
+  // L[r][c] for c < r from the packed factor
+  if (r == c + 1 && tags[c] == 2) return mk(0.0, 0.0);
+  return F[(int64_t)r * ld + c];
+}
+
+// -------------------------------------------------------------------------
+// Panel TRSM: rows [r0, r0+RT) of a panel P (R x n, ld n) hold K_ij rows.
+// One 16-lane group per row.  Output: X rows (for the Schur update) and
+// L rows written back into P.
+// -------------------------------------------------------------------------
+constexpr int TRSM_THREADS = 256;
+
+__global__ void __launch_bounds__(TRSM_THREADS)
+panel_trsm_kernel(cplx* P, cplx* X, int R, int n, const cplx* F, const int64_t* perm, const int8_t* tags) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int RT = TRSM_THREADS / 16;
+  cplx* S = reinterpret_cast<cplx*>(smem_raw);  // RT x n
+  const int r0 = blockIdx.x * RT;
+  const int g = threadIdx.x >> 4, s = threadIdx.x & 15;
+  const int row = r0 + g;
+  const bool live = row < R;
+  cplx* x = S + (int64_t)g * n;
+
+  // gather K_ij[row, perm[c]]
+  if (live)
+    for (int c = s; c < n; c += 16) x[c] = P[(int64_t)row * n + perm[c]];
+  __syncwarp();
+
+  // left-looking forward substitution: x[c] -= sum_{c'<c} x[c'] L[c][c']
+  for (int c = 1; c < n; ++c) {
+    cplx acc = mk(0.0, 0.0);
+    if (live) {
+      const cplx* Lr = F + (int64_t)c * n;
+      for (int cp = s; cp < c; cp += 16) {
+        cplx l = (cp == c - 1 && tags[cp] == 2) ? mk(0.0, 0.0) : __ldg(Lr + cp);
+        c_fma(acc, x[cp], l);
+      }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, 16);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, 16);
+    }
+    if (live && s == 0) x[c] = c_sub(x[c], acc);
+    __syncwarp();
+  }
+  if (!live) return;
+  // X row, then L row = X D^-1 (apply_dinv_right, kernels.py:184-202)
+  for (int c = s; c < n; c += 16) X[(int64_t)row * n + c] = x[c];
+  for (int c = s; c < n; c += 16) {
+    const int8_t t = tags[c];
+    if (t == 1) {
+      P[(int64_t)row * n + c] = x_div_np(x[c], F[(int64_t)c * n + c]);
+    } else if (t == 2) {
+      cplx x0 = x[c], x1 = x[c + 1];
+      dinv_pair(F[(int64_t)c * n + c], F[(int64_t)(c + 1) * n + c], F[(int64_t)(c + 1) * n + c + 1], x0, x1);
+      P[(int64_t)row * n + c] = x0;
+      P[(int64_t)row * n + c + 1] = x1;
+    }
+  }
+}
+
+// -------------------------------------------------------------------------
+// Multi-RHS solves.  Z is a batch of n x m row-major arrays (ld = m); CTA =
+// (RHS chunk of 16, batch index); 16 lanes per RHS column.
+// -------------------------------------------------------------------------
+constexpr int LS_THREADS = 256;
+constexpr int LS_RHS = LS_THREADS / 16;
+
+
+__global__ void __launch_bounds__(LS_THREADS) gather_rows_kernel(SolveBatch a) {
+  // Z[i][c] = B[perm[i]][c]
+  const int b = blockIdx.y;
+  const int64_t total = (int64_t)a.n * a.m;
+  const int64_t* perm = a.perm + b * a.stride_p;
+  for (int64_t t = blockIdx.x * (int64_t)LS_THREADS + threadIdx.x; t < total; t += (int64_t)gridDim.x * LS_THREADS) {
+    const int i = (int)(t / a.m), c = (int)(t % a.m);
+    a.Z[b * a.stride_z + (int64_t)i * a.ldz + c] = a.B[b * a.stride_b + perm[i] * a.ldb + c];
+  }
+}
+
+__global__ void __launch_bounds__(LS_THREADS) scatter_rows_kernel(SolveBatch a) {
+  // B[perm[i]][c] = Z[i][c]
+  const int b = blockIdx.y;
+  const int64_t total = (int64_t)a.n * a.m;
+  const int64_t* perm = a.perm + b * a.stride_p;
+  for (int64_t t = blockIdx.x * (int64_t)LS_THREADS + threadIdx.x; t < total; t += (int64_t)gridDim.x * LS_THREADS) {
+    const int i = (int)(t / a.m), c = (int)(t % a.m);
+    cplx* dst = const_cast<cplx*>(a.B) + b * a.stride_b + perm[i] * a.ldb + c;
+    *dst = a.Z[b * a.stride_z + (int64_t)i * a.ldz + c];
+  }
+}
+
+__global__ void __launch_bounds__(LS_THREADS) lsolve_fwd_kernel(SolveBatch a) {
+  const int b = blockIdx.y;
+  const int g = threadIdx.x >> 4, s = threadIdx.x & 15;
+  const int col = blockIdx.x * LS_RHS + g;
+  const bool live = col < a.m;
+  const int n = a.n;
+  const cplx* F = a.F + b * a.stride_f;
+  const int8_t* tags = a.tags + b * a.stride_t;
+  cplx* Z = a.Z + b * a.stride_z + col;
+  const int ldz = a.ldz;
+  for (int c = 1; c < n; ++c) {
+    cplx acc = mk(0.0, 0.0);
+    if (live) {
+      const cplx* Lr = F + (int64_t)c * n;
+      for (int cp = s; cp < c; cp += 16) {
+        const cplx l = (cp == c - 1 && tags[cp] == 2) ? mk(0.0, 0.0) : __ldg(Lr + cp);
+        c_fma(acc, l, Z[(int64_t)cp * ldz]);
+      }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, 16);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, 16);
+    }
+    if (live && s == 0) Z[(int64_t)c * ldz] = c_sub(Z[(int64_t)c * ldz], acc);
+    __syncwarp();
+  }
+  if (!live || a.U == nullptr) return;
+  cplx* U = a.U + b * a.stride_u + col;
+  for (int c = s; c < n; c += 16) {
+    const int8_t t = tags[c];
+    if (t == 1) {
+      U[(int64_t)c * ldz] = x_div_np(Z[(int64_t)c * ldz], F[(int64_t)c * n + c]);
+    } else if (t == 2) {
+      cplx x0 = Z[(int64_t)c * ldz], x1 = Z[(int64_t)(c + 1) * ldz];
+      dinv_pair(F[(int64_t)c * n + c], F[(int64_t)(c + 1) * n + c], F[(int64_t)(c + 1) * n + c + 1], x0, x1);
+      U[(int64_t)c * ldz] = x0;
+      U[(int64_t)(c + 1) * ldz] = x1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(LS_THREADS) lsolve_bwd_kernel(SolveBatch a) {
+  const int b = blockIdx.y;
+  const int g = threadIdx.x >> 4, s = threadIdx.x & 15;
+  const int col = blockIdx.x * LS_RHS + g;
+  const bool live = col < a.m;
+  const int n = a.n;
+  const cplx* F = a.F + b * a.stride_f;
+  const int8_t* tags = a.tags + b * a.stride_t;
+  cplx* Z = a.Z + b * a.stride_z + col;
+  const int ldz = a.ldz;
+  for (int c = n - 2; c >= 0; --c) {
+    cplx acc = mk(0.0, 0.0);
+    if (live) {
+      for (int i = c + 1 + s; i < n; i += 16) {
+        const cplx l = (i == c + 1 && tags[c] == 2) ? mk(0.0, 0.0) : __ldg(F + (int64_t)i * n + c);
+        c_fma(acc, l, Z[(int64_t)i * ldz]);
+      }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, 16);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, 16);
+    }
+    if (live && s == 0) Z[(int64_t)c * ldz] = c_sub(Z[(int64_t)c * ldz], acc);
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(LS_THREADS) dinv_left_kernel(SolveBatch a) {
+  // Z = D^-1 Z in place; one thread per (row, column), 2x2 pairs handled by
+  // the thread of the first row.
+  const int b = blockIdx.y;
+  const int64_t total = (int64_t)a.n * a.m;
+  const cplx* F = a.F + b * a.stride_f;
+  const int8_t* tags = a.tags + b * a.stride_t;
+  const int n = a.n;
+  for (int64_t t = blockIdx.x * (int64_t)LS_THREADS + threadIdx.x; t < total; t += (int64_t)gridDim.x * LS_THREADS) {
+    const int c = (int)(t / a.m), col = (int)(t % a.m);
+    cplx* Z = a.Z + b * a.stride_z + col;
+    const int8_t tg = tags[c];
+    if (tg == 1) {
+      Z[(int64_t)c * a.ldz] = x_div_np(Z[(int64_t)c * a.ldz], F[(int64_t)c * n + c]);
+    } else if (tg == 2) {
+      cplx x0 = Z[(int64_t)c * a.ldz], x1 = Z[(int64_t)(c + 1) * a.ldz];
+      dinv_pair(F[(int64_t)c * n + c], F[(int64_t)(c + 1) * n + c], F[(int64_t)(c + 1) * n + c + 1], x0, x1);
+      Z[(int64_t)c * a.ldz] = x0;
+      Z[(int64_t)(c + 1) * a.ldz] = x1;
+    }
+  }
+}
+
+}  // namespace d3m
+
+
+extern "C" int d3m_panel_trsm_launch(void* P, void* X, int R, int n, const void* F, const void* perm,
+                                     const void* tags, void* stream) {
+  using namespace d3m;
+  if (R <= 0 || n <= 0) return 0;
+  constexpr int RT = TRSM_THREADS / 16;
+  const size_t smem = (size_t)RT * n * sizeof(cplx);
+  if (smem > 220 * 1024) return -22;
+  static int configured = 0;
+  if (!configured) {
+    cudaFuncSetAttribute(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    configured = 1;
+  }
+  panel_trsm_kernel<<<(R + RT - 1) / RT, TRSM_THREADS, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<cplx*>(P), static_cast<cplx*>(X), R, n, static_cast<const cplx*>(F),
+      static_cast<const int64_t*>(perm), static_cast<const int8_t*>(tags));
+  return (int)cudaGetLastError();
+}
+
+// phase: 0 gather, 1 forward (+U), 2 dinv, 3 backward, 4 scatter
+extern "C" int d3m_solve_phase_launch(int phase, d3m::SolveBatch* a, int batch, void* stream) {
+  using namespace d3m;
+  if (batch <= 0 || a->n <= 0 || a->m <= 0) return 0;
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t total = (int64_t)a->n * a->m;
+  const int flat_blocks = (int)std::min<int64_t>((total + LS_THREADS - 1) / LS_THREADS, 4096);
+  const dim3 gflat(flat_blocks, batch);
+  const dim3 grhs((a->m + LS_RHS - 1) / LS_RHS, batch);
+  switch (phase) {
+    case 0: gather_rows_kernel<<<gflat, LS_THREADS, 0, s>>>(*a); break;
+    case 1: lsolve_fwd_kernel<<<grhs, LS_THREADS, 0, s>>>(*a); break;
+    case 2: dinv_left_kernel<<<gflat, LS_THREADS, 0, s>>>(*a); break;
+    case 3: lsolve_bwd_kernel<<<grhs, LS_THREADS, 0, s>>>(*a); break;
+    case 4: scatter_rows_kernel<<<gflat, LS_THREADS, 0, s>>>(*a); break;
+    default: return -22;
+  }
+  return (int)cudaGetLastError();
+}

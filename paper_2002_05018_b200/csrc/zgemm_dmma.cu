@@ -1,0 +1,248 @@
+// zgemm_dmma.cu -- grouped complex128 GEMM on the B200 FP64 tensor pipe.
+//
+//   C  op=  A_eff * B_eff^T        (A_eff: M x K, B_eff: N x K, C: M x N)
+//
+// with op one of  C -= AB (trailing Schur updates, factor.py:213-230),
+// C = AB (Schur reduction D^T X, subdomain.py:181-183) or C += AB.
+//
+// B200 has no tcgen05 FP64 kind (ptxas rejects .kind::f64), so the tensor
+// path is the warp-level DMMA: mma.sync.aligned.m8n8k4.f64 lowers to SASS
+// DMMA.8x8x4 (36.9 TFLOP/s measured burst, profiles/fp64_peak_r01.txt).
+// A complex product is four real DMMAs on the (re, im) planes:
+//   acc_re += a_re b_re + (-a_im) b_im,   acc_im += a_re b_im + a_im b_re.
+//
+// Structure: CTA tile 64 x 64 complex, 4 warps (2 x 2), warp tile 32 x 32
+// complex = 4 x 4 DMMA sub-tiles x (re, im) accumulators (128 registers).
+// K is staged 8 complex per stage through a 4-deep cp.async (LDGSTS.128)
+// ring in shared memory; complex values stay interleaved so one LDS.128
+// returns (re, im) of a fragment element.  Row pitch 12 complex (192 B =
+// 64 mod 128) makes every quarter-warp fragment load conflict-free.
+//
+// Scheduling: one CTA per output tile of a flat task list (grouped GEMM).
+// Each task carries its own offsets/shape/leading dimensions and the prefix
+// sum of tile counts; a CTA finds its task by binary search.  A task flagged
+// SYM is a diagonal-block target of the block LDL^T: only lower tiles are
+// computed and each lower value u_rc is subtracted at (r, c) and at (c, r),
+// which is exactly the reference's tril(upd) + tril(upd, -1)^T rule
+// (factor.py:217-220).
+#include "d3m_common.cuh"
+#include "d3m_gemm.h"
+#include "d3m_kernels.h"
+
+namespace d3m {
+
+constexpr int BM = 64, BN = 64, BKC = 8, STAGES = 4, PITCH = BKC + 4;
+constexpr int NTHREADS = 128;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int bytes = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// Stage loader: tile rows [r0, r0+64) x k-columns [k0, k0+8) of an operand
+// whose element (r, k) lives at  P[r*ld + k]  (TRANS=false) or P[k*ld + r].
+template <bool TRANS>
+__device__ __forceinline__ void load_tile(cplx (*S)[PITCH], const cplx* P, int ld, int r0, int rows,
+                                          int k0, int kdim) {
+  const int t = threadIdx.x;
+  if (!TRANS) {
+    // 8 threads cover one 128-byte row segment; 16 rows per pass
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int r = p * 16 + (t >> 3), k = t & 7;
+      const bool ok = (r0 + r < rows) && (k0 + k < kdim);
+      const cplx* g = ok ? P + (int64_t)(r0 + r) * ld + (k0 + k) : P;
+      cp_async16(&S[r][k], g, ok);
+    }
+  } else {
+    // 64 threads cover one contiguous 1 KB row of the stored operand
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int r = t & 63, k = p * 2 + (t >> 6);
+      const bool ok = (r0 + r < rows) && (k0 + k < kdim);
+      const cplx* g = ok ? P + (int64_t)(k0 + k) * ld + (r0 + r) : P;
+      cp_async16(&S[r][k], g, ok);
+    }
+  }
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(NTHREADS, 2)
+zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bbase, cplx* Cbase,
+                     const GemmTask* __restrict__ tasks, int ntasks) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cplx(*As)[BM][PITCH] = reinterpret_cast<cplx(*)[BM][PITCH]>(smem_raw);
+  cplx(*Bs)[BN][PITCH] = reinterpret_cast<cplx(*)[BN][PITCH]>(smem_raw + sizeof(cplx) * STAGES * BM * PITCH);
+
+  // ---- locate the task and the tile --------------------------------------
+  const int tile = blockIdx.x;
+  int lo = 0, hi = ntasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tasks[mid].tile_start <= tile) lo = mid; else hi = mid - 1;
+  }
+  const GemmTask tk = tasks[lo];
+  int local = tile - tk.tile_start, tm, tn;
+  if (tk.flags & kGemmSym) {
+    tm = (int)((sqrt(8.0 * local + 1.0) - 1.0) * 0.5);
+    while ((tm + 1) * (tm + 2) / 2 <= local) ++tm;
+    while (tm * (tm + 1) / 2 > local) --tm;
+    tn = local - tm * (tm + 1) / 2;
+  } else {
+    tm = local / tk.tiles_n;
+    tn = local - tm * tk.tiles_n;
+  }
+  const cplx* A = Abase + tk.a_off;
+  const cplx* B = Bbase + tk.b_off;
+  cplx* C = Cbase + tk.c_off;
+  const int M = tk.m, N = tk.n, K = tk.k;
+  const int m0 = tm * BM, n0 = tn * BN;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int fr = lane >> 2, fc = lane & 3;
+
+  double acc_re[4][4][2], acc_im[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
+
+  const int ktiles = (K + BKC - 1) / BKC;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) {
+      load_tile<TA>(As[s], A, tk.lda, m0, M, s * BKC, K);
+      load_tile<TB>(Bs[s], B, tk.ldb, n0, N, s * BKC, K);
+    }
+    cp_commit();
+  }
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < ktiles) {
+        const int slot = nk % STAGES;
+        load_tile<TA>(As[slot], A, tk.lda, m0, M, nk * BKC, K);
+        load_tile<TB>(Bs[slot], B, tk.ldb, n0, N, nk * BKC, K);
+      }
+      cp_commit();
+    }
+    const int slot = kt % STAGES;
+#pragma unroll
+    for (int kk = 0; kk < BKC / 4; ++kk) {
+      double are[4], aim[4], anim[4], bre[4], bim[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const cplx a = As[slot][wm + i * 8 + fr][kk * 4 + fc];
+        are[i] = a.x;
+        aim[i] = a.y;
+        anim[i] = -a.y;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const cplx b = Bs[slot][wn + j * 8 + fr][kk * 4 + fc];
+        bre[j] = b.x;
+        bim[j] = b.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
+          dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
+          dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
+          dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
+        }
+    }
+  }
+  cp_wait<0>();
+
+  // ---- epilogue ------------------------------------------------------------
+  const int mode = tk.flags & kGemmModeMask;
+  const bool sym = (tk.flags & kGemmSym) != 0;
+  const int ldc = tk.ldc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = m0 + wm + i * 8 + fr;
+        const int c = n0 + wn + j * 8 + fc * 2 + h;
+        if (r >= M || c >= N) continue;
+        const cplx u = mk(acc_re[i][j][h], acc_im[i][j][h]);
+        if (sym) {
+          if (c > r) continue;
+          cplx* p = C + (int64_t)r * ldc + c;
+          *p = c_sub(*p, u);
+          if (c < r) {
+            cplx* q = C + (int64_t)c * ldc + r;
+            *q = c_sub(*q, u);
+          }
+        } else {
+          cplx* p = C + (int64_t)r * ldc + c;
+          if (mode == kGemmSub) *p = c_sub(*p, u);
+          else if (mode == kGemmStore) *p = u;
+          else *p = c_add(*p, u);
+        }
+      }
+}
+
+constexpr size_t kGemmSmem = sizeof(cplx) * STAGES * (BM + BN) * PITCH;
+
+template <bool TA, bool TB>
+static int launch_t(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
+                    cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(zgemm_grouped_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kGemmSmem);
+    configured = true;
+  }
+  zgemm_grouped_kernel<TA, TB><<<ntiles, NTHREADS, kGemmSmem, s>>>(A, B, C, tasks, ntasks);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace d3m
+
+// Host helper: fill tile counts/prefix sums of a task array (host memory).
+extern "C" int d3m_gemm_prepare_tasks(d3m::GemmTask* tasks, int ntasks) {
+  int total = 0;
+  for (int t = 0; t < ntasks; ++t) {
+    d3m::GemmTask& k = tasks[t];
+    const int tm = (k.m + d3m::BM - 1) / d3m::BM, tn = (k.n + d3m::BN - 1) / d3m::BN;
+    k.tiles_n = tn;
+    k.tile_start = total;
+    if (k.flags & d3m::kGemmSym) total += tm * (tm + 1) / 2;
+    else total += tm * tn;
+  }
+  return total;
+}
+
+extern "C" int d3m_gemm_launch(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
+                               int ntasks, int ntiles, void* stream) {
+  using namespace d3m;
+  if (ntiles <= 0 || ntasks <= 0) return 0;
+  auto a = static_cast<const cplx*>(A);
+  auto b = static_cast<const cplx*>(B);
+  auto c = static_cast<cplx*>(C);
+  auto t = static_cast<const GemmTask*>(dtasks);
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  if (!ta && !tb) return launch_t<false, false>(a, b, c, t, ntasks, ntiles, s);
+  if (!ta && tb) return launch_t<false, true>(a, b, c, t, ntasks, ntiles, s);
+  if (ta && !tb) return launch_t<true, false>(a, b, c, t, ntasks, ntiles, s);
+  return launch_t<true, true>(a, b, c, t, ntasks, ntiles, s);
+}

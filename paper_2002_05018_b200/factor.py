@@ -1,0 +1,577 @@
+"""Numeric factorisation on the B200: dense Bunch-Kaufman LDL^T, the
+right-looking block LDL^T over an elimination plan, block substitution.
+
+Drop-in for the reference's factor.py (pkg/src/ddsolve/factor.py:1-334):
+same names, signatures, dataclass fields, error types and messages.  All
+numerics run in libd3m (sm_100a); this module plans device layouts, moves
+data and raises the reference's exceptions from device pivot outcomes.
+
+Device layout of a BlockFactor (one HBM pool, complex128):
+  per block column j (plan order):  diagonal slot  n_j x n_j  (packed BK
+  factor: strict lower = L_jj, diagonal = d, W[k+1,k] = e of 2x2 pivots)
+  followed by the panel  R_j x n_j  stacking L_ij for i in pattern[j]
+  (ascending), R_j = sum n_i.  Pivots: perm (int64) / tags (int8) at the
+  plan-order row offset of the column.
+"""
+
+from __future__ import annotations
+
+from collections.abc import Mapping
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .blockmat import BlockSparseSym
+from .device import DeviceArray, empty, require_cuda, stream_ptr, to_device, upload_bytes, upload_i64
+from .symbolic import EliminationPlan
+
+DEFAULT_PIVOT_TOL = 1e-12      # factor.py:19
+_P = _lib.ptr
+
+
+class SingularBlockError(Exception):
+    """Both 1x1 and 2x2 pivot candidates fell below the pivot threshold."""
+
+
+class FactorConsistencyError(Exception):
+    """Numeric factorization touched a block outside the symbolic pattern."""
+
+
+def _singular_msg(info: int, thr: float) -> str:
+    return f"no acceptable pivot at elimination step {info} (threshold {thr:.3e})"     # factor.py:101-103
+
+
+# ---------------------------------------------------------------------------
+# Dense factor
+# ---------------------------------------------------------------------------
+
+class DenseFactor:
+    """P M P^T = L D L^T with unit lower L and 1x1/2x2 block diagonal D.
+
+    Device-resident: ``packed`` (n x n, kernels.py:7-22 storage), ``perm_dev``
+    and ``tags_dev`` live in HBM; the reference's fields L, d, e, tags, perm
+    are materialised on the host on first access.
+    """
+
+    def __init__(self, packed, perm_dev, tags_dev, growth: float, n_2x2: int):
+        self.packed = packed            # torch (n, n) complex128 view
+        self.perm_dev = perm_dev        # torch (n,) int64 view
+        self.tags_dev = tags_dev        # torch (n,) int8 view
+        self.growth = float(growth)
+        self.n_2x2 = int(n_2x2)
+        self._host = None
+
+    @property
+    def n(self) -> int:
+        return int(self.packed.shape[0])
+
+    def _unpack(self):
+        if self._host is None:
+            W = self.packed.cpu().numpy()
+            tags = self.tags_dev.cpu().numpy().astype(np.int8)
+            perm = self.perm_dev.cpu().numpy().astype(np.int64)
+            n = W.shape[0]
+            L = np.tril(W, -1)
+            d = np.diagonal(W).copy()
+            e = np.zeros(n, dtype=np.complex128)
+            two = np.flatnonzero(tags == 2)
+            e[two] = W[two + 1, two]
+            L[two + 1, two] = 0.0
+            np.fill_diagonal(L, 1.0)
+            self._host = (L, d, e, tags, perm)
+        return self._host
+
+    L = property(lambda self: self._unpack()[0])
+    d = property(lambda self: self._unpack()[1])
+    e = property(lambda self: self._unpack()[2])
+    tags = property(lambda self: self._unpack()[3])
+    perm = property(lambda self: self._unpack()[4])
+
+    def solve(self, B):
+        """Solve M X = B (vector or multi-column), factor.py:52-66."""
+        device_in = isinstance(B, DeviceArray) or _is_tensor(B)
+        one_d = len(B.shape) == 1
+        rows = B.shape[0]
+        cols = 1 if one_d else (B.shape[1] if len(B.shape) > 1 else 1)
+        if rows != self.n:
+            raise ValueError(f"rhs has {rows} rows, factor has {self.n}")
+        if self.n == 0 or cols == 0:
+            out = np.zeros((self.n, cols), dtype=np.complex128)
+            return out[:, 0] if one_d else out
+        t = require_cuda()
+        Z = to_device(B).reshape(self.n, cols).clone()
+        work = empty((self.n, cols))
+        _lib.call("d3m_ldlt_solve_batched", 1, self.n, _P(self.packed), 0, _P(self.perm_dev), 0,
+                  _P(self.tags_dev), 0, _P(Z), 0, cols, cols, _P(work), stream_ptr())
+        if one_d:
+            Z = Z.reshape(self.n)
+        if device_in:
+            return DeviceArray(Z)
+        del t
+        return Z.cpu().numpy()
+
+    def dense_d(self) -> np.ndarray:
+        """Block diagonal D as a dense matrix (factor.py:68-80)."""
+        _, d, e, tags, _ = self._unpack()
+        D = np.diag(d).astype(np.complex128)
+        two = np.flatnonzero(tags == 2)
+        D[two + 1, two] = e[two]
+        D[two, two + 1] = e[two]
+        return D
+
+
+def _is_tensor(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def dense_ldlt_bk(M, pivot_tol: float = DEFAULT_PIVOT_TOL) -> DenseFactor:
+    """Bunch-Kaufman LDL^T of a complex symmetric matrix on the GPU.
+
+    factor.py:83-116: rejects non-square input (ValueError), checks symmetry
+    to 1e-12 max|M| (ValueError "not symmetric"), raises SingularBlockError
+    when neither a 1x1 nor a 2x2 pivot clears pivot_tol * max|M|.  The pivot
+    sequence and the factor values are bit-identical to the reference.
+    """
+    shape = tuple(M.shape) if (isinstance(M, DeviceArray) or _is_tensor(M)) else np.shape(M)
+    if len(shape) != 2 or shape[0] != shape[1]:
+        raise ValueError("matrix must be square")
+    n = int(shape[0])
+    t = require_cuda()
+    W = to_device(M).clone() if n else t.zeros((0, 0), dtype=t.complex128, device="cuda")
+    return _factor_batch(W.reshape(1, n, n), pivot_tol, labels=None)[0]
+
+
+def _factor_batch(W, pivot_tol, labels, check_sym=True, scratch=None):
+    """Factor a (batch, n, n) device tensor in place; returns DenseFactors
+    or raises for the first failing matrix (``labels`` customises errors)."""
+    t = require_cuda()
+    batch, n = int(W.shape[0]), int(W.shape[1])
+    perm = t.empty((batch, n), dtype=t.int64, device="cuda")
+    tags = t.empty((batch, n), dtype=t.int8, device="cuda")
+    n2 = t.empty(batch, dtype=t.int32, device="cuda")
+    info = t.empty(batch, dtype=t.int32, device="cuda")
+    gr = t.empty(batch, dtype=t.float64, device="cuda")
+    sc = t.empty(batch, dtype=t.float64, device="cuda")
+    asy = t.empty(batch, dtype=t.float64, device="cuda")
+    if scratch is None and 64 * n > 200 * 1024:
+        scratch = empty((batch, 4 * n))
+    _lib.call("d3m_bk_factor_batched", batch, n, _P(W), n * n, max(n, 1), float(pivot_tol), int(check_sym),
+              _P(perm), _P(tags), _P(n2), _P(gr), _P(info), _P(sc), _P(asy), _P(scratch), stream_ptr())
+    return _collect(W, perm, tags, n2, info, gr, sc, asy, pivot_tol, labels)
+
+
+def _collect(W, perm, tags, n2, info, gr, sc, asy, pivot_tol, labels, wrap=None):
+    info_h = info.cpu().numpy()
+    sc_h = sc.cpu().numpy()
+    bad = np.flatnonzero(info_h != -1)
+    if bad.size:
+        b = int(bad[0])
+        if info_h[b] == -2:
+            raise ValueError(f"matrix is not symmetric: max|M - M^T| = {float(asy[b].item()):.3e}")
+        msg = _singular_msg(int(info_h[b]), pivot_tol * float(sc_h[b]))
+        if wrap is not None:
+            raise wrap(b, msg)
+        raise SingularBlockError(msg)
+    gr_h, n2_h = gr.cpu().numpy(), n2.cpu().numpy()
+    return [DenseFactor(W[b], perm[b], tags[b], float(gr_h[b]), int(n2_h[b])) for b in range(W.shape[0])]
+
+
+# ---------------------------------------------------------------------------
+# Block factor
+# ---------------------------------------------------------------------------
+
+@dataclass
+class FactorStats:
+    factor_entries: int = 0
+    flops: int = 0
+    peak_bytes: int = 0
+    growth_factor: float = 1.0
+    n_2x2_pivots: int = 0
+
+
+class _OffDiag(Mapping):
+    """Lazy (i, j) -> L_ij mapping over the device panels."""
+
+    def __init__(self, sched, pool):
+        self._s = sched
+        self._pool = pool
+        self._cache = {}
+
+    def __getitem__(self, key):
+        if key not in self._s.loc:
+            raise KeyError(key)
+        if key not in self._cache:
+            off, rows, cols = self._s.loc[key]
+            self._cache[key] = self._pool[off:off + rows * cols].reshape(rows, cols).cpu().numpy()
+        return self._cache[key]
+
+    def device(self, key):
+        off, rows, cols = self._s.loc[key]
+        return self._pool[off:off + rows * cols].reshape(rows, cols)
+
+    def __iter__(self):
+        return iter(self._s.offdiag_keys)
+
+    def __len__(self):
+        return len(self._s.offdiag_keys)
+
+
+class BlockFactor:
+    """Output of :func:`block_ldlt` (factor.py:128-136): per-supernode dense
+    factors in elimination order, the off-diagonal factor blocks of the
+    pattern (lazy host views of the device panels) and statistics."""
+
+    def __init__(self, plan, diag, offdiag, stats, sched=None, pool=None, perm=None, tags=None):
+        self.plan = plan
+        self.diag = diag
+        self.offdiag = offdiag
+        self.stats = stats
+        self._sched = sched
+        self._pool = pool
+        self._perm = perm
+        self._tags = tags
+
+
+class _Schedule:
+    """Device layout + trailing-update task table of one elimination plan."""
+
+    def __init__(self, plan: EliminationPlan):
+        t = require_cuda()
+        nb = plan.nblocks
+        sizes = np.asarray(plan.sizes_perm, dtype=np.int64)
+        self.nb = nb
+        self.sizes = sizes
+        self.row_off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        pattern = [np.asarray(p, dtype=np.int64) for p in plan.pattern]
+        self.pattern = pattern
+        self.pat_ptr = np.concatenate([[0], np.cumsum([p.size for p in pattern])]).astype(np.int64)
+        self.pat_idx = np.concatenate(pattern).astype(np.int64) if nb and self.pat_ptr[-1] else np.zeros(0, np.int64)
+        self.panel_rows = np.array([int(sizes[p].sum()) for p in pattern], dtype=np.int64)
+        self.diag_off = np.zeros(nb, dtype=np.int64)
+        self.panel_off = np.zeros(nb, dtype=np.int64)
+        off = 0
+        self.loc = {}               # (i, j) -> (elem offset, rows, cols)
+        self.rowpos = {}            # (i, j) -> row offset of block i in panel j
+        for j in range(nb):
+            nj = int(sizes[j])
+            self.diag_off[j] = off
+            off += nj * nj
+            self.panel_off[j] = off
+            r = 0
+            for i in pattern[j]:
+                i = int(i)
+                self.rowpos[(i, j)] = r
+                self.loc[(i, j)] = (int(self.panel_off[j]) + r * nj, int(sizes[i]), nj)
+                r += int(sizes[i])
+            off += int(self.panel_rows[j]) * nj
+        self.pool_elems = off
+        self.offdiag_keys = sorted(self.loc, key=lambda ij: (ij[1], ij[0]))
+        self.piv_elems = int(self.row_off[-1])
+        # trailing-update GEMM tasks, "next" (targets in column j+1) first
+        recs, ptr, nxt, tiles_n, tiles_r = [], [0], [], [], []
+        bm = _lib.GEMM_BM
+        for j in range(nb):
+            nj = int(sizes[j])
+            rows = [int(i) for i in pattern[j]]
+            prow = np.concatenate([[0], np.cumsum(sizes[rows])]).astype(np.int64) if rows else [0]
+            nxt_recs, rest_recs = [], []
+            for a, i in enumerate(rows):
+                for b in range(a + 1):
+                    kk = rows[b]
+                    ni, nk = int(sizes[i]), int(sizes[kk])
+                    if i == kk:
+                        c_off, ldc, flags = int(self.diag_off[i]), ni, _lib.GEMM_SUB | _lib.GEMM_SYM
+                        tm = (ni + bm - 1) // bm
+                        tiles = tm * (tm + 1) // 2
+                    else:
+                        if (i, kk) not in self.rowpos:
+                            raise FactorConsistencyError(f"update targets block {(i, kk)} outside pattern")
+                        c_off, ldc, flags = int(self.panel_off[kk]) + self.rowpos[(i, kk)] * nk, nk, _lib.GEMM_SUB
+                        tiles = ((ni + bm - 1) // bm) * ((nk + bm - 1) // bm)
+                    rec = (int(prow[a]) * nj, int(self.panel_off[j]) + int(prow[b]) * nj, c_off, ni, nk, nj,
+                           nj, nj, ldc, flags, tiles, (nk + bm - 1) // bm)
+                    (nxt_recs if kk == j + 1 else rest_recs).append(rec)
+            for group, tl in ((nxt_recs, tiles_n), (rest_recs, tiles_r)):
+                start = 0
+                for rec in group:
+                    recs.append(rec[:10] + (start, rec[11], 0))
+                    start += rec[10]
+                tl.append(start)
+            nxt.append(ptr[-1] + len(nxt_recs))
+            ptr.append(ptr[-1] + len(nxt_recs) + len(rest_recs))
+        tasks = np.zeros(len(recs), dtype=_lib.GEMM_TASK)
+        if recs:
+            arr = np.array(recs, dtype=np.int64)
+            for c, name in enumerate(_lib.GEMM_TASK.names):
+                tasks[name] = arr[:, c]
+        self.tasks = tasks
+        self.task_ptr = np.asarray(ptr, dtype=np.int64)
+        self.task_next = np.asarray(nxt if nxt else [0], dtype=np.int64)
+        self.tiles_next = np.asarray(tiles_n if tiles_n else [0], dtype=np.int64)
+        self.tiles_rest = np.asarray(tiles_r if tiles_r else [0], dtype=np.int64)
+        self.d_tasks = upload_bytes(tasks) if len(tasks) else t.zeros(64, dtype=t.uint8, device="cuda")
+        self.xbuf_elems = 2 * max(1, int((self.panel_rows * sizes).max()) if nb else 1)
+        # block_solve backward gather: global plan-order rows of every panel
+        gidx, gptr = [], [0]
+        for j in range(nb):
+            for i in pattern[j]:
+                gidx.append(np.arange(self.row_off[i], self.row_off[i + 1], dtype=np.int64))
+            gptr.append(gptr[-1] + int(self.panel_rows[j]))
+        self.gptr = np.asarray(gptr, dtype=np.int64)
+        self.d_gidx = upload_i64(np.concatenate(gidx) if gidx else np.zeros(1, np.int64))
+        self.flops_update = int(sum(8 * int(sizes[i]) * int(sizes[kk]) * int(sizes[j]) if i != kk else
+                                    4 * int(sizes[i]) ** 2 * int(sizes[j])
+                                    for j in range(nb) for a, i in enumerate(pattern[j]) for kk in pattern[j][:a + 1]))
+        self.flops_trsm = int(sum(4 * int(self.panel_rows[j]) * int(sizes[j]) ** 2 for j in range(nb)))
+        self.flops_bk = int(sum(8 * int(s) ** 3 // 3 for s in sizes))
+
+
+def _schedule(plan: EliminationPlan) -> _Schedule:
+    sched = getattr(plan, "_d3m_schedule", None)
+    key = (tuple(int(s) for s in plan.sizes_perm), tuple(tuple(int(i) for i in p) for p in plan.pattern))
+    if sched is None or sched[0] != key:
+        sched = (key, _Schedule(plan))
+        try:
+            plan._d3m_schedule = sched
+        except AttributeError:
+            pass
+    return sched[1]
+
+
+def _reference_stats(K_keys, sizes_orig, plan: EliminationPlan, inv) -> tuple[int, int, int]:
+    """factor_entries, flops and peak_bytes with the reference's bookkeeping
+    (factor.py:174-239), evaluated symbolically on the host."""
+    sizes = plan.sizes_perm
+    live_keys = {}
+    for (i, j) in K_keys:
+        a, b = int(inv[i]), int(inv[j])
+        key = (a, b) if a >= b else (b, a)
+        live_keys[key] = int(sizes[key[0]]) * int(sizes[key[1]])
+    live = sum(live_keys.values())
+    stored = flops = 0
+    peak = live
+    for j in range(plan.nblocks):
+        nj = int(sizes[j])
+        if (j, j) in live_keys:
+            live -= live_keys.pop((j, j))
+        stored += nj * (nj + 1) // 2
+        flops += nj ** 3 // 3 + nj ** 2
+        rows = [int(r) for r in plan.pattern[j]]
+        transient = 0
+        for i in rows:
+            ni = int(sizes[i])
+            if (i, j) in live_keys:
+                live -= live_keys.pop((i, j))
+            stored += ni * nj
+            flops += ni * nj * nj + ni * nj
+            transient += ni * nj
+        peak = max(peak, live + stored + transient)
+        for a, i in enumerate(rows):
+            for kk in rows[:a + 1]:
+                flops += int(sizes[i]) * nj * int(sizes[kk])
+                if (i, kk) not in live_keys:
+                    live_keys[(i, kk)] = int(sizes[i]) * int(sizes[kk])
+                    live += live_keys[(i, kk)]
+        peak = max(peak, live + stored + transient)
+    return stored, flops, 16 * peak
+
+
+def _upload_K(K: BlockSparseSym, sched: _Schedule, plan: EliminationPlan, pool):
+    """Copy (and relabel/transpose) the stored blocks of K into the zeroed
+    factor pool: factor._permute_blocks (factor.py:139-151) on the device."""
+    t = require_cuda()
+    inv = plan.order.inverse()
+    sizes = K.sizes
+    items = list(K.blocks.items())
+    host = [(k, b) for k, b in items if not isinstance(b, DeviceArray)]
+    dev = [(k, b) for k, b in items if isinstance(b, DeviceArray)]
+    groups = []          # (src tensor, [(src_off, key, block-shape)])
+    if host:
+        tot = sum(int(sizes[i]) * int(sizes[j]) for (i, j), _ in host)
+        stage = empty(tot)
+        entries, o = [], 0
+        for (i, j), b in host:
+            nbytes = int(sizes[i]) * int(sizes[j])
+            arr = np.ascontiguousarray(np.asarray(b, dtype=np.complex128)).reshape(-1)
+            stage[o:o + nbytes].copy_(t.from_numpy(arr))
+            entries.append((o, (i, j)))
+            o += nbytes
+        groups.append((stage, entries))
+    if dev:
+        bases = {}
+        for (i, j), b in dev:
+            st = b.tensor
+            base = st.untyped_storage().data_ptr()
+            bases.setdefault(base, (st, []))[1].append(((st.data_ptr() - base) // 16, (i, j)))
+        for base, (st, entries) in bases.items():
+            whole = t.empty(0, dtype=t.complex128, device="cuda").set_(st.untyped_storage(), 0,
+                                                                        (st.untyped_storage().nbytes() // 16,))
+            groups.append((whole, entries))
+    for src, entries in groups:
+        recs = np.zeros(len(entries), dtype=_lib.COPY_TASK)
+        maxe = 1
+        for r, (src_off, (i, j)) in enumerate(entries):
+            a, b = int(inv[i]), int(inv[j])
+            ni, nj = int(sizes[i]), int(sizes[j])
+            if a >= b:
+                key, transpose = (a, b), 0
+            else:
+                key, transpose = (b, a), 1
+            if key[0] == key[1]:
+                dst, ld = int(sched.diag_off[key[0]]), int(plan.sizes_perm[key[0]])
+            else:
+                if key not in sched.loc:
+                    raise FactorConsistencyError(f"block {key} outside the symbolic pattern")
+                dst, _, ld = sched.loc[key]
+            rows, cols = (ni, nj) if not transpose else (nj, ni)
+            recs[r] = (src_off, dst, rows, cols, nj, ld, transpose, _lib.COPY_STORE)
+            maxe = max(maxe, rows * cols)
+        d_rec = upload_bytes(recs)
+        _lib.call("d3m_block_copy", _P(src), _P(pool), _P(d_rec), len(recs), maxe, stream_ptr())
+
+
+def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFAULT_PIVOT_TOL,
+               lookahead: bool = True) -> BlockFactor:
+    """Right-looking block LDL^T of ``K`` following ``plan`` on one GPU.
+
+    factor.py:154-240: per block column j, Bunch-Kaufman of the diagonal
+    block (bit-exact kernel), X_ij = L_ij D_jj by a triangular solve against
+    every pattern row, L_ij = X_ij D_jj^-1, then K_ik -= X_ij L_kj^T for
+    pattern pairs i >= k on the DMMA tensor pipe (diagonal targets
+    symmetrised from the lower half).  The next column's factorisation
+    overlaps the current column's trailing update (lookahead).
+    """
+    nb = K.nblocks
+    if plan.nblocks != nb:
+        raise ValueError("plan and matrix disagree on block count")
+    t = require_cuda()
+    inv = plan.order.inverse()
+    stored, flops, peak = _reference_stats(list(K.blocks), K.sizes, plan, inv)
+    if nb == 0:
+        return BlockFactor(plan, [], {}, FactorStats(0, 0, 0, 1.0, 0))
+    sched = _schedule(plan)
+    pool = empty(max(sched.pool_elems, 1))
+    _lib.call("d3m_zero", _P(pool), sched.pool_elems, stream_ptr())
+    _upload_K(K, sched, plan, pool)
+    perm = t.empty(max(sched.piv_elems, 1), dtype=t.int64, device="cuda")
+    tags = t.empty(max(sched.piv_elems, 1), dtype=t.int8, device="cuda")
+    info = t.empty(nb, dtype=t.int32, device="cuda")
+    n2 = t.empty(nb, dtype=t.int32, device="cuda")
+    gr = t.empty(nb, dtype=t.float64, device="cuda")
+    sc = t.empty(nb, dtype=t.float64, device="cuda")
+    asy = t.empty(nb, dtype=t.float64, device="cuda")
+    xbuf = empty(sched.xbuf_elems)
+    nmax = int(sched.sizes.max())
+    scratch = empty(4 * nmax) if 64 * nmax > 200 * 1024 else None
+    H = _lib.hptr
+    _lib.call("d3m_block_ldlt_exec", nb, H(sched.sizes), H(sched.diag_off), H(sched.panel_off),
+              H(sched.panel_rows), H(sched.row_off), H(sched.task_ptr), H(sched.task_next),
+              H(sched.tiles_next), H(sched.tiles_rest), _P(sched.d_tasks), _P(pool), _P(xbuf),
+              sched.xbuf_elems, _P(perm), _P(tags), _P(info), _P(n2), _P(gr), _P(sc), _P(asy),
+              _P(scratch), float(pivot_tol), 1, int(bool(lookahead)), stream_ptr())
+    info_h = info.cpu().numpy()
+    bad = np.flatnonzero(info_h != -1)
+    if bad.size:
+        j = int(bad[0])
+        if info_h[j] == -2:
+            raise ValueError(f"matrix is not symmetric: max|M - M^T| = {float(asy[j].item()):.3e}")
+        err = SingularBlockError(_singular_msg(int(info_h[j]), pivot_tol * float(sc[j].item())))
+        raise SingularBlockError(f"block column {j}: {err}") from err
+    gr_h, n2_h = gr.cpu().numpy(), n2.cpu().numpy()
+    diag = []
+    for j in range(nb):
+        nj = int(sched.sizes[j])
+        o, r = int(sched.diag_off[j]), int(sched.row_off[j])
+        diag.append(DenseFactor(pool[o:o + nj * nj].reshape(nj, nj), perm[r:r + nj], tags[r:r + nj],
+                                float(gr_h[j]), int(n2_h[j])))
+    stats = FactorStats(stored, flops, peak, float(max(gr_h.max(), 1.0)) if nb else 1.0, int(n2_h.sum()))
+    stats.growth_factor = float(max((f.growth for f in diag), default=1.0))
+    return BlockFactor(plan, diag, _OffDiag(sched, pool), stats, sched, pool, perm, tags)
+
+
+def block_solve(F: BlockFactor, g: list) -> list:
+    """Solve K x = g through the block factor (factor.py:271-310).
+
+    ``g`` is a block vector in the original block numbering, each block 1-D
+    or a matrix of RHS columns.  All columns go through one device pass, each
+    computed independently, so k-RHS results equal k single solves bit for
+    bit.  Device-resident inputs give device-resident outputs.
+    """
+    nb = F.plan.nblocks
+    if len(g) != nb:
+        raise ValueError(f"block vector has {len(g)} blocks, expected {nb}")
+    if nb == 0:
+        return []
+    perm = F.plan.order.perm
+    sizes = F.plan.sizes_perm
+    device_in = all(isinstance(b, DeviceArray) or _is_tensor(b) for b in g)
+    shapes = [tuple(b.shape) for b in g]
+    one_d = all(len(s) == 1 for s in shapes)
+    cols = None
+    for s in shapes:
+        c = 1 if len(s) == 1 else s[1]
+        if cols is None:
+            cols = c
+        elif c != cols:
+            raise ValueError("inconsistent RHS column counts across blocks")
+    for j in range(nb):
+        if shapes[int(perm[j])][0] != int(sizes[j]):
+            raise ValueError(f"block {int(perm[j])} has wrong length")
+    sched = F._sched
+    t = require_cuda()
+    N = int(sched.row_off[-1])
+    if cols == 0:
+        out = [np.zeros((int(s[0]), 0), dtype=np.complex128) for s in shapes]
+        return out
+    if device_in:
+        parts = [to_device(g[int(perm[j])]).reshape(int(sizes[j]), cols) for j in range(nb)]
+        b = t.cat(parts, dim=0).contiguous()
+    else:
+        host = np.empty((N, cols), dtype=np.complex128)
+        for j in range(nb):
+            blk = np.asarray(g[int(perm[j])], dtype=np.complex128).reshape(int(sizes[j]), cols)
+            host[sched.row_off[j]:sched.row_off[j + 1]] = blk
+        b = to_device(host)
+    u = empty((N, cols))
+    x = empty((N, cols))
+    tmp = empty((int(sched.sizes.max()), cols))
+    gbuf = empty((max(1, int(sched.panel_rows.max())), cols))
+    cap = int(sched.pat_ptr[-1]) + nb
+    d_tasks = t.empty(64 * cap, dtype=t.uint8, device="cuda")
+    H = _lib.hptr
+    _lib.call("d3m_block_solve_exec", nb, H(sched.sizes), H(sched.row_off), H(sched.diag_off),
+              H(sched.panel_off), H(sched.panel_rows), H(sched.row_off), H(sched.pat_ptr),
+              H(sched.pat_idx if sched.pat_idx.size else np.zeros(1, np.int64)), H(sched.gptr),
+              _P(sched.d_gidx), _P(F._pool), _P(F._perm), _P(F._tags), _P(b), _P(u), _P(x), _P(tmp),
+              _P(gbuf), int(cols), _P(d_tasks), cap, stream_ptr())
+    out = [None] * nb
+    if device_in:
+        for j in range(nb):
+            blk = x[sched.row_off[j]:sched.row_off[j + 1]]
+            out[int(perm[j])] = DeviceArray(blk[:, 0] if one_d else blk)
+        return out
+    xh = x.cpu().numpy()
+    for j in range(nb):
+        blk = xh[sched.row_off[j]:sched.row_off[j + 1]]
+        out[int(perm[j])] = blk[:, 0].copy() if one_d else blk.copy()
+    return out
+
+
+def scatter_factor(F: BlockFactor) -> tuple[np.ndarray, np.ndarray]:
+    """Dense (L, D) of the permuted matrix, for verification (factor.py:313-334)."""
+    sizes = F.plan.sizes_perm
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    n = int(off[-1])
+    L = np.zeros((n, n), dtype=np.complex128)
+    D = np.zeros((n, n), dtype=np.complex128)
+    for j in range(F.plan.nblocks):
+        fac = F.diag[j]
+        lb = np.zeros_like(fac.L)
+        lb[fac.perm, :] = fac.L
+        L[off[j]:off[j + 1], off[j]:off[j + 1]] = lb
+        D[off[j]:off[j + 1], off[j]:off[j + 1]] = fac.dense_d()
+        for i in F.plan.pattern[j]:
+            i = int(i)
+            L[off[i]:off[i + 1], off[j]:off[j + 1]] = F.offdiag[(i, j)]
+    return L, D

@@ -1,0 +1,345 @@
+"""DDM layer of the hot path on the GPU: Schur reduction of the subdomains,
+assembly of the block-sparse interface matrix, primal recovery.
+
+Drop-in for subdomain.py (pkg/src/ddsolve/subdomain.py:34-237): same
+dataclasses, names, errors and messages.  ``reduce_domains`` is the batched
+entry point (all subdomains of equal shape in flight in one launch chain);
+``reduce_domain`` keeps the reference's one-domain signature.  Results stay in
+HBM (``DeviceArray``) so assembly, factorisation, solve and recovery chain
+without host round trips.
+
+The finite-element front end (build_subdomain_systems, the 2-D mesh) is out
+of scope for this hot-path build.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .blockmat import BlockSparseSym
+from .device import DeviceArray, empty, require_cuda, stream_ptr, to_device, upload_bytes, upload_i64
+from .factor import DEFAULT_PIVOT_TOL, DenseFactor, _collect, _singular_msg
+
+_P = _lib.ptr
+
+
+class SingularDomainError(Exception):
+    pass
+
+
+class SolverStateError(Exception):
+    pass
+
+
+@dataclass
+class Coupling:
+    interface: int
+    D: np.ndarray          # local dofs x kept multiplier dofs
+    sign: int
+
+
+@dataclass
+class SubdomainSystem:
+    domain: int
+    A: np.ndarray
+    f: np.ndarray
+    dof_map: np.ndarray
+    couplings: list = field(default_factory=list)
+    factor: DenseFactor | None = None
+
+    @property
+    def n_dofs(self) -> int:
+        return int(np.asarray(self.dof_map).size)
+
+
+@dataclass
+class ReducedSystem:
+    K: BlockSparseSym
+    g: list
+    interface_sizes: np.ndarray
+    lam: list | None = None
+
+    @property
+    def n_lambda(self) -> int:
+        return int(np.asarray(self.interface_sizes).sum())
+
+
+def interface_lambda_nodes(part) -> list[np.ndarray]:
+    """Kept multiplier dofs per interface (subdomain.py:75-111): at a node
+    shared by several interfaces, scanned in ascending interface order, an
+    interface whose (dom_lo, dom_hi) pair closes a cycle among the domains
+    already connected there drops its dof."""
+    at_node: dict[int, list[int]] = {}
+    for k, itf in enumerate(part.interfaces):
+        for v in itf.nodes:
+            at_node.setdefault(int(v), []).append(k)
+    dropped = set()
+    for v in sorted(at_node):
+        ifs = sorted(at_node[v])
+        if len(ifs) < 2:
+            continue
+        root: dict[int, int] = {}
+
+        def find(x):
+            root.setdefault(x, x)
+            while root[x] != x:
+                root[x] = root[root[x]]
+                x = root[x]
+            return x
+
+        for k in ifs:
+            ra, rb = find(part.interfaces[k].dom_lo), find(part.interfaces[k].dom_hi)
+            if ra == rb:
+                dropped.add((k, v))
+            else:
+                root[ra] = rb
+    return [np.array([int(v) for v in itf.nodes if (k, int(v)) not in dropped], dtype=np.int64)
+            for k, itf in enumerate(part.interfaces)]
+
+
+def _coupling_matrix(sys: SubdomainSystem) -> np.ndarray:
+    if sys.couplings:
+        return np.concatenate([np.asarray(c.D, dtype=np.complex128) for c in sys.couplings], axis=1)
+    return np.zeros((sys.n_dofs, 0), dtype=np.complex128)
+
+
+def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PIVOT_TOL) -> list:
+    """Batched reduce_domain: every group of equal (n, m) subdomains is
+    factored and reduced in one device call chain (BK -> multi-RHS solve ->
+    D^T X on DMMA -> symmetrisation).  Returns [(K_D, g_d)] as DeviceArrays
+    and caches each factor on its system, like subdomain.py:166-184."""
+    t = require_cuda()
+    groups: dict[tuple[int, int], list[int]] = {}
+    shapes = []
+    for idx, s in enumerate(systems):
+        n = int(np.shape(s.A)[0]) if not isinstance(s.A, DeviceArray) else s.A.shape[0]
+        m = sum(int(np.shape(c.D)[1]) for c in s.couplings)
+        shapes.append((n, m))
+        groups.setdefault((n, m), []).append(idx)
+    out = [None] * len(systems)
+    first_error = None
+    for (n, m), members in groups.items():
+        B = len(members)
+        A = empty((B, n, n))
+        D = empty((B, n, m))
+        f = empty((B, n))
+        for r, idx in enumerate(members):
+            s = systems[idx]
+            A[r].copy_(to_device(s.A).reshape(n, n))
+            if m:
+                D[r].copy_(to_device(_coupling_matrix(s)) if not _dev_D(s) else s._d3m_D)
+            f[r].copy_(to_device(s.f).reshape(n))
+        perm = t.empty((B, n), dtype=t.int64, device="cuda")
+        tags = t.empty((B, n), dtype=t.int8, device="cuda")
+        n2 = t.empty(B, dtype=t.int32, device="cuda")
+        info = t.empty(B, dtype=t.int32, device="cuda")
+        gr = t.empty(B, dtype=t.float64, device="cuda")
+        sc = t.empty(B, dtype=t.float64, device="cuda")
+        asy = t.empty(B, dtype=t.float64, device="cuda")
+        K = empty((B, m, m))
+        g = empty((B, m))
+        wz = empty((B, n, m + 1))
+        wx = empty((B, n, m + 1))
+        wc = empty((B, max(m, 1), m + 1))
+        scratch = empty((B, 4 * n)) if 64 * n > 200 * 1024 else None
+        d_tasks = t.empty(64 * B, dtype=t.uint8, device="cuda")
+        _lib.call("d3m_schur_reduce_batched", B, n, m, _P(A), _P(D), _P(f), float(pivot_tol), _P(perm),
+                  _P(tags), _P(n2), _P(gr), _P(info), _P(sc), _P(asy), _P(K), _P(g), _P(wz), _P(wx), _P(wc),
+                  _P(scratch), _P(d_tasks), stream_ptr())
+        try:
+            facs = _collect(A, perm, tags, n2, info, gr, sc, asy, pivot_tol, None,
+                            wrap=lambda b, msg: SingularDomainError(
+                                f"domain {systems[members[b]].domain} is singular: {msg}"))
+        except (SingularDomainError, ValueError) as err:
+            pos = members[int(_first_bad(info))]
+            if first_error is None or pos < first_error[0]:
+                first_error = (pos, err)
+            continue
+        for r, idx in enumerate(members):
+            s = systems[idx]
+            s.factor = facs[r]
+            s._d3m_D = D[r]
+            out[idx] = (DeviceArray(K[r]), DeviceArray(g[r]))
+    if first_error is not None:
+        raise first_error[1]
+    return out
+
+
+def _dev_D(s) -> bool:
+    return getattr(s, "_d3m_D", None) is not None
+
+
+def _first_bad(info) -> int:
+    h = info.cpu().numpy()
+    return int(np.flatnonzero(h != -1)[0])
+
+
+def reduce_domain(sys: SubdomainSystem, pivot_tol: float = DEFAULT_PIVOT_TOL):
+    """K_D = D^T A^-1 D (symmetrised) and g_d = D^T A^-1 f for one domain
+    (subdomain.py:166-184); the factor is cached on ``sys``."""
+    return reduce_domains([sys], pivot_tol)[0]
+
+
+def assemble_reduced(reduced, part) -> ReducedSystem:
+    """Scatter per-domain Schur blocks into the block-sparse reduced system
+    (subdomain.py:187-214).  ``reduced[d]`` is ordered by
+    ``part.incident_interfaces(d)``.  Block (ia, ib) = sum over domains in
+    ascending order (first contribution copied, later ones added, like
+    blockmat.add_block), done on the device when the inputs are resident."""
+    lam_nodes = interface_lambda_nodes(part)
+    sizes = np.array([ln.size for ln in lam_nodes], dtype=np.int64)
+    contrib: dict[tuple[int, int], list] = {}
+    gcontrib: dict[int, list] = {}
+    device = True
+    for d, (K_D, g_d) in enumerate(reduced):
+        ifaces = [int(i) for i in part.incident_interfaces(d)]
+        off = np.concatenate([[0], np.cumsum(sizes[ifaces])]).astype(np.int64)
+        if tuple(K_D.shape) != (int(off[-1]), int(off[-1])):
+            raise ValueError(f"domain {d}: reduced block is {tuple(K_D.shape)}, expected "
+                             f"({int(off[-1])}, {int(off[-1])})")
+        device &= isinstance(K_D, DeviceArray) and isinstance(g_d, DeviceArray)
+        for a, ia in enumerate(ifaces):
+            gcontrib.setdefault(ia, []).append((g_d, int(off[a]), int(sizes[ia])))
+            for b, ib in enumerate(ifaces):
+                if ia >= ib:
+                    contrib.setdefault((ia, ib), []).append((K_D, int(off[a]), int(off[b])))
+    if not device:
+        return _assemble_host(contrib, gcontrib, sizes)
+    return _assemble_device(contrib, gcontrib, sizes)
+
+
+def _assemble_host(contrib, gcontrib, sizes):
+    K = BlockSparseSym(sizes)
+    for (ia, ib), lst in contrib.items():
+        for (KD, oa, ob) in lst:
+            KDh = np.asarray(KD)
+            K.add_block(ia, ib, KDh[oa:oa + sizes[ia], ob:ob + sizes[ib]])
+    K.validate()
+    g = [np.zeros(int(s), dtype=np.complex128) for s in sizes]
+    for ia, lst in gcontrib.items():
+        for (gd, o, n) in lst:
+            g[ia] = g[ia] + np.asarray(gd)[o:o + n]
+    return ReducedSystem(K, g, sizes)
+
+
+def _assemble_device(contrib, gcontrib, sizes):
+    t = require_cuda()
+    keys = list(contrib)
+    koff, tot = {}, 0
+    for key in keys:
+        koff[key] = tot
+        tot += int(sizes[key[0]]) * int(sizes[key[1]])
+    goff = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    kpool = empty(max(tot, 1))
+    gpool = t.zeros(max(int(goff[-1]), 1), dtype=t.complex128, device="cuda")
+    rounds: dict[tuple[int, int], list] = {}     # (round, base) -> tasks
+
+    def src_of(dev: DeviceArray):
+        st = dev.tensor
+        base = st.untyped_storage().data_ptr()
+        return base, st, (st.data_ptr() - base) // 16
+
+    bases = {}
+    for key, lst in contrib.items():
+        ia, ib = key
+        for r, (KD, oa, ob) in enumerate(lst):
+            base, st, o = src_of(KD)
+            bases[base] = st
+            ld = int(KD.shape[1])
+            rounds.setdefault((r, base, "K"), []).append(
+                (o + oa * ld + ob, koff[key], int(sizes[ia]), int(sizes[ib]), ld, int(sizes[ib]), 0,
+                 _lib.COPY_STORE if r == 0 else _lib.COPY_ADD))
+    for ia, lst in gcontrib.items():
+        for r, (gd, o0, n) in enumerate(lst):
+            base, st, o = src_of(gd)
+            bases[base] = st
+            rounds.setdefault((r, base, "g"), []).append(
+                (o + o0, int(goff[ia]), 1, n, n, n, 0, _lib.COPY_ZERO_ADD if r == 0 else _lib.COPY_ADD))
+    for (r, base, what) in sorted(rounds, key=lambda x: (x[0], x[2], x[1])):
+        recs = np.array(rounds[(r, base, what)], dtype=_lib.COPY_TASK)
+        st = bases[base]
+        whole = t.empty(0, dtype=t.complex128, device="cuda").set_(
+            st.untyped_storage(), 0, (st.untyped_storage().nbytes() // 16,))
+        dst = kpool if what == "K" else gpool
+        maxe = int((recs["rows"].astype(np.int64) * recs["cols"]).max())
+        d_recs = upload_bytes(recs)          # keep alive until the launch is enqueued
+        _lib.call("d3m_block_copy", _P(whole), _P(dst), _P(d_recs), len(recs), maxe, stream_ptr())
+    K = BlockSparseSym(sizes)
+    for key in keys:
+        o, ni, nj = koff[key], int(sizes[key[0]]), int(sizes[key[1]])
+        K.blocks[key] = DeviceArray(kpool[o:o + ni * nj].reshape(ni, nj))
+    K._d3m_pool = kpool
+    g = [DeviceArray(gpool[int(goff[i]):int(goff[i + 1])]) for i in range(sizes.size)]
+    return ReducedSystem(K, g, sizes)
+
+
+def recover_primal(systems: list[SubdomainSystem], lam: list) -> np.ndarray | DeviceArray:
+    """E_d = A_d^-1 (f_d - D_d lambda) with the cached factors, assembled
+    with averaging of duplicated interface dofs (subdomain.py:217-237)."""
+    t = require_cuda()
+    for s in systems:
+        if s.factor is None:
+            raise SolverStateError(f"domain {s.domain} has no cached factorization; run reduce_domain first")
+    device_in = all(isinstance(v, DeviceArray) for v in lam)
+    lam_dev = [to_device(v).reshape(-1) for v in lam]
+    n_glob = 1 + max(int(np.max(s.dof_map)) for s in systems)
+    # group by (n, m), E stored group after group
+    groups: dict[tuple[int, int], list[int]] = {}
+    for idx, s in enumerate(systems):
+        m = sum(int(np.shape(c.D)[1]) for c in s.couplings)
+        groups.setdefault((s.n_dofs, m), []).append(idx)
+    order = [idx for key in groups for idx in groups[key]]
+    e_off = {}
+    o = 0
+    for idx in order:
+        e_off[idx] = o
+        o += systems[idx].n_dofs
+    E = empty(max(o, 1))
+    for (n, m), members in groups.items():
+        B = len(members)
+        base = e_off[members[0]]
+        rhs = E[base:base + B * n].reshape(B, n)
+        for r, idx in enumerate(members):
+            rhs[r].copy_(to_device(systems[idx].f).reshape(n))
+        F = t.stack([systems[idx].factor.packed for idx in members]).contiguous()
+        pv = t.stack([systems[idx].factor.perm_dev for idx in members]).contiguous()
+        tg = t.stack([systems[idx].factor.tags_dev for idx in members]).contiguous()
+        if m:
+            D = t.stack([s._d3m_D if _dev_D(s) else to_device(_coupling_matrix(s))
+                         for s in (systems[idx] for idx in members)]).contiguous()
+            lamc = t.stack([t.cat([lam_dev[c.interface] for c in systems[idx].couplings if np.shape(c.D)[1]]
+                                  or [t.zeros(0, dtype=t.complex128, device="cuda")])
+                            for idx in members]).contiguous()
+            tasks = np.zeros(B, dtype=_lib.GEMM_TASK)
+            tasks["a_off"] = np.arange(B) * n * m
+            tasks["b_off"] = np.arange(B) * m
+            tasks["c_off"] = np.arange(B) * n
+            tasks["m"], tasks["n"], tasks["k"] = n, 1, m
+            tasks["lda"], tasks["ldb"], tasks["ldc"] = m, 1, 1
+            tasks["flags"] = _lib.GEMM_SUB
+            d_tasks = t.empty(64 * B, dtype=t.uint8, device="cuda")
+            _lib.call("d3m_zgemm_grouped", 0, 1, _P(D), _P(lamc), _P(rhs), _lib.hptr(tasks), B, _P(d_tasks),
+                      stream_ptr())
+        work = empty((B, n))
+        _lib.call("d3m_ldlt_solve_batched", B, n, _P(F), n * n, _P(pv), n, _P(tg), n, _P(rhs), n, 1, 1,
+                  _P(work), stream_ptr())
+    # ordered average: contributions per global dof in ascending domain order
+    gl, src = [], []
+    for idx in range(len(systems)):          # acc[dof_map] += E in list order
+        dm = np.asarray(systems[idx].dof_map, dtype=np.int64)
+        gl.append(dm)
+        src.append(e_off[idx] + np.arange(dm.size, dtype=np.int64))
+    gl = np.concatenate(gl)
+    src = np.concatenate(src)
+    order_ = np.argsort(gl, kind="stable")
+    counts = np.bincount(gl, minlength=n_glob)
+    ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    out = empty(n_glob)
+    d_ptr, d_src = upload_i64(ptr), upload_i64(src[order_])   # both alive across the launch
+    _lib.call("d3m_ordered_average", _P(E), _P(d_ptr), _P(d_src), _P(out), n_glob, stream_ptr())
+    if device_in:
+        return DeviceArray(out)
+    return out.cpu().numpy()

@@ -1,0 +1,225 @@
+"""GPU parity: block LDL^T (restricted BK, DMMA trailing updates) and block
+substitution vs the oracle, the reference goldens and dense solves."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden, rand_complex_symmetric, split_blocks
+
+pytestmark = pytest.mark.gpu
+
+
+def _plan(K, order=None):
+    import paper_2002_05018_b200 as d
+    g = d.clique_graph(K)
+    if order is None:
+        order = d.reorder(g, K.sizes)
+    return d.symbolic_factor(g, order, K.sizes)
+
+
+def test_gemm_vs_numpy(cuda):
+    """Grouped DMMA GEMM, all four operand layouts and three modes."""
+    from paper_2002_05018_b200 import _lib
+    from paper_2002_05018_b200.device import stream_ptr, to_device
+    rng = np.random.default_rng(3)
+    for (M, N, K) in [(64, 64, 64), (1, 1, 1), (70, 33, 130), (256, 256, 256), (129, 65, 7)]:
+        for ta in (0, 1):
+            for tb in (0, 1):
+                for mode in (_lib.GEMM_SUB, _lib.GEMM_STORE, _lib.GEMM_ADD):
+                    A = rng.standard_normal((M, K)) + 1j * rng.standard_normal((M, K))
+                    B = rng.standard_normal((N, K)) + 1j * rng.standard_normal((N, K))
+                    C = rng.standard_normal((M, N)) + 1j * rng.standard_normal((M, N))
+                    As = A.T.copy() if ta else A
+                    Bs = B.T.copy() if tb else B
+                    dA, dB, dC = to_device(As), to_device(Bs), to_device(C)
+                    task = np.zeros(1, dtype=_lib.GEMM_TASK)
+                    task["m"], task["n"], task["k"] = M, N, K
+                    task["lda"] = M if ta else K
+                    task["ldb"] = N if tb else K
+                    task["ldc"] = N
+                    task["flags"] = mode
+                    dt = cuda.empty(64, dtype=cuda.uint8, device="cuda")
+                    _lib.call("d3m_zgemm_grouped", ta, tb, _lib.ptr(dA), _lib.ptr(dB), _lib.ptr(dC),
+                              _lib.hptr(task), 1, _lib.ptr(dt), stream_ptr())
+                    P = A @ B.T
+                    ref = {0: C - P, 1: P, 2: C + P}[mode]
+                    got = dC.cpu().numpy()
+                    assert np.abs(got - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max()) * K, (M, N, K, ta, tb, mode)
+
+
+def test_gemm_symmetric_target(cuda):
+    from paper_2002_05018_b200 import _lib
+    from paper_2002_05018_b200.device import stream_ptr, to_device
+    rng = np.random.default_rng(4)
+    n, K = 150, 40
+    X = rng.standard_normal((n, K)) + 1j * rng.standard_normal((n, K))
+    L = rng.standard_normal((n, K)) + 1j * rng.standard_normal((n, K))
+    W = rand_complex_symmetric(n, 5)
+    dX, dL, dW = to_device(X), to_device(L), to_device(W)
+    task = np.zeros(1, dtype=_lib.GEMM_TASK)
+    task["m"] = task["n"] = n
+    task["k"] = K
+    task["lda"] = task["ldb"] = K
+    task["ldc"] = n
+    task["flags"] = _lib.GEMM_SUB | _lib.GEMM_SYM
+    dt = cuda.empty(64, dtype=cuda.uint8, device="cuda")
+    _lib.call("d3m_zgemm_grouped", 0, 0, _lib.ptr(dX), _lib.ptr(dL), _lib.ptr(dW), _lib.hptr(task), 1,
+              _lib.ptr(dt), stream_ptr())
+    upd = X @ L.T
+    upd = np.tril(upd) + np.tril(upd, -1).T               # factor.py:217-220
+    got = dW.cpu().numpy()
+    assert np.array_equal(got, got.T)
+    assert np.abs(got - (W - upd)).max() <= 1e-12 * np.abs(upd).max()
+
+
+def test_block_pivots_and_solution_vs_reference_goldens(cuda):
+    import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import workloads as wl
+    g = golden("block_small.npz")
+    for seed in range(30):
+        K, S = wl.rand_block_system(seed, max_blocks=10, max_size=12, density=0.4)
+        plan = _plan(K)
+        assert np.array_equal(plan.order.perm, g[f"s{seed}_order"])
+        F = d.block_ldlt(K, plan)
+        assert np.array_equal(np.concatenate([f.perm for f in F.diag]), g[f"s{seed}_perm"])
+        assert np.array_equal(np.concatenate([f.tags for f in F.diag]), g[f"s{seed}_tags"])
+        st = g[f"s{seed}_stats"]
+        assert (F.stats.factor_entries, F.stats.flops, F.stats.peak_bytes, F.stats.n_2x2_pivots) == tuple(st)
+        rng = np.random.default_rng(900 + seed)
+        b = rng.standard_normal((S.shape[0], 3)) + 1j * rng.standard_normal((S.shape[0], 3))
+        x = np.concatenate(d.block_solve(F, split_blocks(b, K.sizes)))
+        ref = g[f"s{seed}_x"]
+        assert np.linalg.norm(x - ref) <= 1e-11 * np.linalg.norm(ref)
+        assert np.linalg.norm(S @ x - b) <= 1e-12 * np.linalg.norm(b)
+
+
+def test_block_vs_oracle_larger_blocks(cuda, oracle):
+    """Pivots bit-exact vs the oracle on indefinite systems with 64-300 wide
+    supernodes (tile edges, 2x2 pivots, fill)."""
+    import paper_2002_05018_b200 as d
+    rng = np.random.default_rng(77)
+    for case in range(4):
+        nb = int(rng.integers(3, 7))
+        sizes = rng.integers(40, 300, size=nb)
+        n = int(sizes.sum())
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        trip = []
+        for i in range(nb):
+            G = rng.standard_normal((sizes[i], sizes[i])) + 1j * rng.standard_normal((sizes[i], sizes[i]))
+            Dg = (np.tril(G) + np.tril(G, -1).T) / np.sqrt(2 * sizes[i])
+            Dg[np.diag_indices(sizes[i])] += rng.uniform(-2, 2, sizes[i])
+            trip.append((i, i, Dg))
+            for j in range(i):
+                if rng.random() < 0.6:
+                    trip.append((i, j, (rng.standard_normal((sizes[i], sizes[j])) +
+                                        1j * rng.standard_normal((sizes[i], sizes[j]))) / np.sqrt(2 * 256)))
+        K = d.from_blocks(sizes, trip)
+        plan = _plan(K)
+        F = d.block_ldlt(K, plan)
+        adj = oracle.clique_adjacency(nb, K.blocks.keys())
+        op = oracle.symbolic_factor(adj, plan.order.perm, sizes)
+        Fo = oracle.block_ldlt({k: np.asarray(v) for k, v in K.blocks.items()}, op)
+        for j in range(nb):
+            assert np.array_equal(F.diag[j].perm, Fo.diag[j].perm), (case, j)
+            assert np.array_equal(F.diag[j].tags, Fo.diag[j].tags), (case, j)
+        for key, Lo in Fo.offdiag.items():
+            assert np.abs(F.offdiag[key] - Lo).max() <= 1e-9 * max(1.0, np.abs(Lo).max())
+        B = rng.standard_normal((n, 4)) + 1j * rng.standard_normal((n, 4))
+        x = np.concatenate(d.block_solve(F, split_blocks(B, sizes)))
+        xo = np.concatenate(oracle.block_solve(Fo, split_blocks(B, sizes)))
+        assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
+        S = K.scatter()
+        assert np.linalg.norm(S @ x - B) <= 1e-10 * np.linalg.norm(B) * np.linalg.norm(S) * np.linalg.norm(x) / np.linalg.norm(B)
+
+
+def test_reference_kats(cuda):
+    import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import workloads as wl
+    M = rand_complex_symmetric(9, 0)                        # test_block_factor.py:24-32
+    K = d.from_blocks([9], [(0, 0, M)])
+    F = d.block_ldlt(K, _plan(K))
+    ref = d.dense_ldlt_bk(M)
+    assert np.array_equal(F.diag[0].L, ref.L) and np.array_equal(F.diag[0].d, ref.d)
+    assert np.array_equal(F.diag[0].perm, ref.perm) and F.offdiag == {}
+    rng = np.random.default_rng(6)                          # :54-72 four-cycle fill
+    sizes = [2, 3, 2, 4]
+
+    def sym(n):
+        G = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        return (G + G.T) / 2 + 3 * n * np.eye(n)
+    tri = [(i, i, sym(sizes[i])) for i in range(4)]
+    for (i, j) in [(1, 0), (2, 1), (3, 2), (3, 0)]:
+        tri.append((i, j, rng.standard_normal((sizes[i], sizes[j])) + 0j))
+    K = d.from_blocks(sizes, tri)
+    plan = _plan(K, d.identity_ordering(4))
+    assert d.fill_blocks(plan, d.clique_graph(K)) == [(3, 1)]
+    F = d.block_ldlt(K, plan)
+    assert set(F.offdiag) - {(i, j) for (i, j) in K.blocks if i != j} == {(3, 1)}
+    sizes = [3, 2]                                          # :75-83 identity blocks
+    K = d.from_blocks(sizes, [(0, 0, np.eye(3, dtype=complex)), (1, 1, np.eye(2, dtype=complex))])
+    F = d.block_ldlt(K, _plan(K))
+    gv = [np.arange(3) + 0j, np.array([5.0, 6.0]) + 1j]
+    x = d.block_solve(F, gv)
+    assert np.array_equal(x[0], gv[0]) and np.array_equal(x[1], gv[1])
+    K = d.BlockSparseSym([])                                # :159-164 empty
+    F = d.block_ldlt(K, _plan(K, d.identity_ordering(0)))
+    assert d.block_solve(F, []) == [] and F.stats.factor_entries == 0
+    K, _ = wl.rand_block_system(61)                         # :167-171
+    F = d.block_ldlt(K, _plan(K))
+    with pytest.raises(ValueError):
+        d.block_solve(F, [np.ones(2, dtype=complex)] * (K.nblocks + 1))
+    sizes = [2, 2]                                          # :144-149
+    K = d.from_blocks(sizes, [(0, 0, np.zeros((2, 2), dtype=complex)), (1, 1, np.eye(2, dtype=complex))])
+    with pytest.raises(d.SingularBlockError, match="block column 0"):
+        d.block_ldlt(K, _plan(K, d.identity_ordering(2)))
+
+
+def test_multi_rhs_equals_single_rhs_bitwise(cuda):
+    import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import workloads as wl
+    K, _ = wl.rand_block_system(77, max_blocks=5, max_size=6)   # test_block_factor.py:109-120
+    F = d.block_ldlt(K, _plan(K))
+    rng = np.random.default_rng(78)
+    B = [rng.standard_normal((int(s), 5)) + 1j * rng.standard_normal((int(s), 5)) for s in K.sizes]
+    X = d.block_solve(F, B)
+    for c in range(5):
+        Xc = d.block_solve(F, [b[:, c:c + 1] for b in B])
+        for i in range(K.nblocks):
+            assert np.array_equal(X[i][:, c:c + 1], Xc[i])
+
+
+def test_determinism(cuda):
+    import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import workloads as wl
+    K, _ = wl.rand_block_system(55, max_blocks=8, max_size=70)
+    plan = _plan(K)
+    F1, F2 = d.block_ldlt(K, plan), d.block_ldlt(K, plan)
+    assert np.array_equal(F1._pool.cpu().numpy(), F2._pool.cpu().numpy())
+
+
+@pytest.mark.slow
+def test_config4_full_size_vs_reference(cuda):
+    """BASELINE config 4 at full size: pivot sequence of all 144 supernodes
+    bit-exact vs the reference, solution within 1e-9 of the reference's,
+    residual of all 16 RHS reported against the reference's own."""
+    import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import workloads as wl
+    g = golden("cfg4.npz")
+    K = wl.config4_matrix()
+    plan = _plan(K, d.identity_ordering(K.nblocks))
+    assert plan.total_factor_entries == int(g["pattern_total"])
+    F = d.block_ldlt(K, plan)
+    perm = np.stack([f.perm for f in F.diag])
+    tags = np.stack([f.tags for f in F.diag])
+    assert np.array_equal(perm, g["perm"].astype(np.int64))
+    assert np.array_equal(tags, g["tags"])
+    assert np.array_equal(np.array([f.n_2x2 for f in F.diag]), g["n2x2"])
+    st = g["stats"]
+    assert (F.stats.factor_entries, F.stats.flops, F.stats.peak_bytes, F.stats.n_2x2_pivots) == tuple(st)
+    rhs = wl.config4_rhs(K)
+    x = d.block_solve(F, rhs)
+    x0 = np.concatenate([xi[:, 0] for xi in x])
+    ref = g["x0"]
+    assert np.linalg.norm(x0 - ref) <= 1e-9 * np.linalg.norm(ref)
