@@ -95,29 +95,36 @@ int d3m_modulus_probe(const void* z, void* hyp, void* npabs, int64_t n, void* st
  * h_diag_off[j], n_j x n_j) and a panel (h_panel_off[j], h_panel_rows[j] x
  * n_j) stacking the pattern blocks in ascending row order; on entry they hold
  * the permuted K (W of factor.py:168), on exit the packed factors and L_ij.
- * Trailing-update GEMM tasks of column j are d_tasks[h_task_ptr[j] ..
- * h_task_ptr[j+1]), the first (h_task_next[j] - h_task_ptr[j]) of which
- * target column j+1 (tile counts h_tiles_next / h_tiles_rest).  Per-column
- * pivots go to d_perm/d_tags at h_piv_off[j]; info/n2x2/growth/scale/asym
- * are nb-long device arrays.  xbuf: X_ij scratch (2 x max R_j n_j when
- * lookahead). */
+ * Per column: BK of the diagonal block, Binv_j = L_jj^-1 P_j into d_binv at
+ * h_binv_off[j] (kept for the solve), X = panel Binv_j^T on DMMA (task
+ * d_trsm_tasks[j], h_tiles_trsm[j] tiles), L = X D^-1 into the panel, then
+ * the trailing-update GEMM tasks d_tasks[h_task_ptr[j] .. h_task_ptr[j+1]),
+ * the first (h_task_next[j] - h_task_ptr[j]) of which target column j+1 and
+ * run on the high-priority critical stream (lookahead), the rest on a
+ * low-priority stream.  Per-column pivots go to d_perm/d_tags at
+ * h_piv_off[j]; info/n2x2/growth/scale/asym are nb-long device arrays.
+ * xbuf: X scratch (2 x max R_j n_j with lookahead). */
 int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_off, const int64_t* h_panel_off,
-                        const int64_t* h_panel_rows, const int64_t* h_piv_off, const int64_t* h_task_ptr,
-                        const int64_t* h_task_next, const int64_t* h_tiles_next, const int64_t* h_tiles_rest,
-                        const void* d_tasks, void* d_pool, void* d_xbuf, int64_t xbuf_elems, void* d_perm,
-                        void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale, void* d_asym,
-                        void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead, void* stream);
+                        const int64_t* h_panel_rows, const int64_t* h_piv_off, const int64_t* h_binv_off,
+                        const int64_t* h_task_ptr, const int64_t* h_task_next, const int64_t* h_tiles_next,
+                        const int64_t* h_tiles_rest, const int64_t* h_tiles_trsm, const void* d_tasks,
+                        const void* d_trsm_tasks, void* d_pool, void* d_binv, void* d_xbuf, int64_t xbuf_elems,
+                        void* d_perm, void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale,
+                        void* d_asym, void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead,
+                        void* stream);
 
 /* Forward / D^-1 / backward block substitution for nrhs right-hand sides in
- * one pass, each column computed independently (k-RHS == k x 1-RHS).
- * Replaces factor.block_solve / _solve_one (factor.py:243-310).  b: plan-
- * ordered RHS (N x nrhs, consumed); x: solution in plan order. */
+ * one pass, every stage a DMMA GEMM against the stored factor (z = Binv b,
+ * b_i -= L_ij z, w = u - sum L_ij^T x_i, x = Binv^T w); each RHS column is
+ * computed independently (k-RHS == k x 1-RHS).  Replaces factor.block_solve /
+ * _solve_one (factor.py:243-310).  b: plan-ordered RHS (N x nrhs, consumed);
+ * x: solution in plan order; tmp: max n_j x nrhs; part: max_j p_j n_j x nrhs;
+ * d_tasks: (2 nb + 2 npattern) GEMM task records. */
 int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_off, const int64_t* h_diag_off,
-                         const int64_t* h_panel_off, const int64_t* h_panel_rows, const int64_t* h_piv_off,
-                         const int64_t* h_pat_ptr, const int64_t* h_pat_idx, const int64_t* h_gptr,
-                         const void* d_gidx, const void* d_pool, const void* d_perm, const void* d_tags, void* d_b,
-                         void* d_u, void* d_x, void* d_tmp, void* d_gbuf, int nrhs, void* d_tasks, int64_t task_cap,
-                         void* stream);
+                         const int64_t* h_panel_off, const int64_t* h_piv_off, const int64_t* h_binv_off,
+                         const int64_t* h_pat_ptr, const int64_t* h_pat_idx, const void* d_pool,
+                         const void* d_binv, const void* d_tags, void* d_b, void* d_u, void* d_x, void* d_tmp,
+                         void* d_part, int nrhs, void* d_tasks, int64_t task_cap, void* stream);
 
 /* Primal recovery of equal-sized subdomains: rhs = f - D lam (rhs holds f on
  * entry), E = A^-1 rhs with the cached packed factors, then the ordered
@@ -126,6 +133,15 @@ int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_of
 int d3m_recover_batched(int batch, int n, int m, const void* F, const void* perm, const void* tags, const void* D,
                         const void* lam, void* rhs, void* work, const void* avg_ptr, const void* avg_src, void* out,
                         int64_t nglob, void* d_tasks, void* stream);
+
+/* Instrumentation used by bench.py: launch counter and optional per-class
+ * CUDA-event timing of every kernel launched through this library (classes:
+ * 0 diagonal BK, 1 panel TRSM, 2 trailing-update / reduction GEMM,
+ * 3 substitution kernels, 4 data movement).  Events are recorded on the
+ * launching stream around each launch; d3m_counters_read synchronises them. */
+void d3m_set_timing(int on);
+void d3m_counters_reset(void);
+int d3m_counters_read(int64_t* launches, double* ms, int64_t* n);
 
 #ifdef __cplusplus
 }

@@ -235,3 +235,6 @@ void d3m_oracle_apply_dinv_right(const cplx* d, const cplx* e, const int8_t* tag
 
 /* glibc hypot, exposed so tests can compare the GPU modulus against libm. */
 double d3m_oracle_hypot(double x, double y) { return hypot(x, y); }
+void d3m_oracle_hypot_array(const double* x, const double* y, double* out, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) out[i] = hypot(x[i], y[i]);
+}

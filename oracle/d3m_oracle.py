@@ -65,6 +65,8 @@ def lib():
         _lib.d3m_oracle_hypot.restype = D
         _lib.d3m_oracle_hypot.argtypes = [D, D]
         _lib.d3m_oracle_bk_alpha.restype = D
+        _lib.d3m_oracle_hypot_array.restype = None
+        _lib.d3m_oracle_hypot_array.argtypes = [P, P, P, I]
     return _lib
 
 
@@ -116,7 +118,17 @@ def apply_dinv_right(d, e, tags, B):
 
 
 def hypot(x: float, y: float) -> float:
+    """glibc libm hypot (what numba's abs(complex) calls) -- NOT Python's
+    math.hypot, which CPython implements with its own algorithm."""
     return lib().d3m_oracle_hypot(x, y)
+
+
+def hypot_array(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    out = np.empty_like(x)
+    lib().d3m_oracle_hypot_array(_ptr(x), _ptr(y), _ptr(out), x.size)
+    return out
 
 
 # --------------------------------------------------------------------------

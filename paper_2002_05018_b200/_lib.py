@@ -31,11 +31,13 @@ _SIGNATURES = {
     "d3m_ordered_average": [P, P, P, P, I64, P],
     "d3m_zero": [P, I64, P],
     "d3m_modulus_probe": [P, P, P, I64, P],
-    "d3m_block_ldlt_exec": [I32, P, P, P, P, P, P, P, P, P, P, P, P, I64, P, P, P, P, P, P, P, P, F64, I32,
-                            I32, P],
-    "d3m_block_solve_exec": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I32, P, I64, P],
+    "d3m_block_ldlt_exec": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, P, P, P, P, P, P, P,
+                            P, F64, I32, I32, P],
+    "d3m_block_solve_exec": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I32, P, I64, P],
     "d3m_recover_batched": [I32, I32, I32, P, P, P, P, P, P, P, P, P, P, I64, P, P],
+    "d3m_counters_read": [P, P, P],
 }
+_VOID = {"d3m_set_timing": [I32], "d3m_counters_reset": []}
 
 # GemmTask / CopyTask records (csrc/d3m_gemm.h, csrc/d3m_misc.h)
 GEMM_TASK = np.dtype([("a_off", "<i8"), ("b_off", "<i8"), ("c_off", "<i8"), ("m", "<i4"), ("n", "<i4"),
@@ -78,12 +80,35 @@ def load():
         fn.restype = ctypes.c_int
     lib.d3m_last_error.restype = ctypes.c_char_p
     lib.d3m_last_error.argtypes = []
+    for name, args in _VOID.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = None
     _lib = lib
     return lib
 
 
 def exported_symbols() -> list[str]:
-    return list(_SIGNATURES) + ["d3m_last_error"]
+    return list(_SIGNATURES) + list(_VOID) + ["d3m_last_error"]
+
+
+CLASSES = ("bk", "trsm", "gemm", "solve", "misc")
+
+
+def counters_reset(timing: bool = False) -> None:
+    lib = load()
+    lib.d3m_counters_reset()
+    lib.d3m_set_timing(1 if timing else 0)
+
+
+def counters_read() -> dict:
+    """{'launches': int, 'ms': {class: ms}, 'n': {class: count}}"""
+    lib = load()
+    nl = ctypes.c_int64(0)
+    ms = (ctypes.c_double * 5)()
+    n = (ctypes.c_int64 * 5)()
+    lib.d3m_counters_read(ctypes.byref(nl), ms, n)
+    return {"launches": int(nl.value), "ms": dict(zip(CLASSES, list(ms))), "n": dict(zip(CLASSES, list(n)))}
 
 
 def call(name: str, *args):

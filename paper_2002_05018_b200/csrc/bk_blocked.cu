@@ -1,0 +1,284 @@
+// bk_blocked.cu -- blocked Bunch-Kaufman LDL^T for supernode diagonal blocks.
+//
+// The right-looking reference (kernels.py:36-146) rewrites the whole trailing
+// triangle at every elimination step; for a 256-wide block in HBM/L2 that is
+// latency-bound (3.2 ms per block measured with the unblocked bit-exact
+// kernel).  This kernel is the panel formulation of the same algorithm
+// (LAPACK zlasyf, lower): one CTA keeps NB+1 panel columns of the matrix
+// (LpT) and of X = L D (WpT) in shared memory, brings column k -- and, when
+// the rowmax test needs it, column imax -- up to date on the fly from the
+// panel's L and X, applies the reference's decision rules (glibc-hypot
+// modulus, alpha = (1+sqrt 17)/8, first-index argmax, "<= tol" singular
+// test), performs the same symmetric interchanges (including the L rows of
+// all previous columns, so one final perm describes the factor), and updates
+// the trailing triangle once per panel (rank-NB, FMA).
+//
+// Pivot decisions are identical to the reference whenever no decision sits
+// within rounding of its threshold (margins >= 5.8e-3 on config 4);
+// values agree to rounding.  The growth factor is reported per panel: the
+// per-step geometric mean of the trailing-max ratio over each panel.
+#include "d3m_common.cuh"
+#include "d3m_kernels.h"
+
+namespace d3m {
+
+constexpr double kAlphaBK = 0.6403882032022076;
+
+template <int NT>
+__device__ __forceinline__ double bmax(double v, double* slots) {
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) slots[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = slots[0];
+#pragma unroll
+  for (int w = 1; w < NT / 32; ++w) r = fmax(r, slots[w]);
+  return r;
+}
+
+template <int NT>
+__device__ __forceinline__ void bargmax(double& v, int& idx, double* vs, int* is) {
+  warp_argmax(v, idx);
+  if ((threadIdx.x & 31) == 0) { vs[threadIdx.x >> 5] = v; is[threadIdx.x >> 5] = idx; }
+  __syncthreads();
+  v = vs[0];
+  idx = is[0];
+#pragma unroll
+  for (int w = 1; w < NT / 32; ++w) argmax_merge(v, idx, vs[w], is[w]);
+}
+
+template <int NB, int NT>
+__global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double ra[NT / 32], rb[NT / 32], rc[NT / 32], rd[NT / 32];
+  __shared__ int rai[NT / 32];
+  constexpr int PC = NB + 1;                    // panel column slots
+  const int b = blockIdx.x, n = a.n, lda = a.lda, tid = threadIdx.x;
+  cplx* W = a.W + (int64_t)b * a.stride_w;
+  int64_t* perm = a.perm + (int64_t)b * n;
+  int8_t* tags = a.tags + (int64_t)b * n;
+  const int ldp = n + 1;                           // padded column stride (conflict-free 16 B rows)
+  cplx* LpT = reinterpret_cast<cplx*>(smem_raw);   // [PC][ldp]  panel of A (stale -> final L)
+  cplx* WpT = LpT + (size_t)PC * ldp;              // [PC][ldp]  X = L D of the panel
+  auto G = [&](int r, int c) -> cplx& { return W[(int64_t)r * lda + c]; };
+
+  for (int i = tid; i < n; i += NT) { perm[i] = i; tags[i] = 0; }
+  // ---- prologue (factor.py:94-98 scale / symmetry; kernels.py:45-46) ------
+  double scale = 0.0, asym = 0.0, tm2 = 0.0;
+  for (int i = tid / 32; i < n; i += NT / 32)
+    for (int j = tid & 31; j < n; j += 32) {
+      const cplx z = G(i, j);
+      scale = fmax(scale, np_abs(z));
+      if (j <= i) tm2 = fmax(tm2, x_abs2(z));
+      if (a.check_sym && j < i) asym = fmax(asym, np_abs(x_sub(z, G(j, i))));
+    }
+  scale = bmax<NT>(scale, ra);
+  asym = bmax<NT>(asym, rb);
+  tm2 = bmax<NT>(tm2, rc);
+  if (tid == 0) { a.scale[b] = scale; a.asym[b] = asym; }
+  if (a.check_sym && n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) {
+    if (tid == 0) { a.info[b] = -2; a.n2x2[b] = 0; a.growth[b] = 1.0; }
+    return;
+  }
+  const double tol_abs = __dmul_rn(a.pivot_tol, scale);
+  double trail_max = sqrt(tm2), growth = 1.0;
+  int n2x2 = 0, info = -1;
+  __syncthreads();
+
+  int k = 0;
+  while (k < n && info < 0) {
+    const int k0 = k;
+    const int ncols = min(PC, n - k0);
+    // stale panel columns k0 .. k0+ncols-1, rows >= column (row segments: coalesced)
+    for (int e = tid; e < (n - k0) * ncols; e += NT) {
+      const int i = k0 + e / ncols, c = e % ncols;
+      if (i >= k0 + c) LpT[c * ldp + i] = G(i, k0 + c);
+    }
+    __syncthreads();
+    // stale element (r, c), r >= c, of the not-yet-updated matrix
+    auto stale = [&](int r, int c) -> cplx { return (c - k0 < ncols) ? LpT[(c - k0) * ldp + r] : G(r, c); };
+    auto put = [&](int r, int c, cplx v) {
+      if (c - k0 < ncols) LpT[(c - k0) * ldp + r] = v;
+      else G(r, c) = v;
+    };
+    int kw = 0, npiv = 0;
+    while (kw < NB && k < n) {
+      // -- A: column k up to date into WpT[kw]
+      for (int i = k + tid; i < n; i += NT) {
+        cplx acc = LpT[kw * ldp + i];
+        for (int c = 0; c < kw; ++c) c_fms(acc, LpT[c * ldp + i], WpT[c * ldp + k]);
+        WpT[kw * ldp + i] = acc;
+      }
+      __syncthreads();
+      // -- B: pivot search
+      const double absakk = x_abs(WpT[kw * ldp + k]);
+      double colmax = 0.0;
+      int imax = k;
+      if (k + 1 < n) {
+        double v = -1.0;
+        int vi = 0x7fffffff;
+        for (int i = k + 1 + tid; i < n; i += NT) argmax_merge(v, vi, x_abs(WpT[kw * ldp + i]), i);
+        bargmax<NT>(v, vi, ra, rai);
+        colmax = v;
+        imax = vi;
+      }
+      if (fmax(absakk, colmax) <= tol_abs) { info = k; break; }
+      int kstep = 1, kp = k;
+      if (!(absakk >= __dmul_rn(kAlphaBK, colmax))) {
+        // -- C: column imax up to date into WpT[kw+1]
+        for (int i = k + tid; i < n; i += NT) {
+          cplx acc = i < imax ? stale(imax, i) : stale(i, imax);
+          for (int c = 0; c < kw; ++c) c_fms(acc, LpT[c * ldp + i], WpT[c * ldp + imax]);
+          WpT[(kw + 1) * ldp + i] = acc;
+        }
+        __syncthreads();
+        double rm = 0.0;
+        for (int i = k + tid; i < n; i += NT)
+          if (i != imax) rm = fmax(rm, x_abs(WpT[(kw + 1) * ldp + i]));
+        const double absimax = x_abs(WpT[(kw + 1) * ldp + imax]);
+        const double rowmax = bmax<NT>(rm, rb);
+        if (__dmul_rn(absakk, rowmax) >= __dmul_rn(__dmul_rn(kAlphaBK, colmax), colmax)) {
+          kp = k;
+        } else if (absimax >= __dmul_rn(kAlphaBK, rowmax)) {
+          kp = imax;
+          for (int i = k + tid; i < n; i += NT) WpT[kw * ldp + i] = WpT[(kw + 1) * ldp + i];
+        } else {
+          kp = imax;
+          kstep = 2;
+        }
+        __syncthreads();
+      }
+      const int kk = k + kstep - 1, kkw = kw + kstep - 1;
+      // -- D: interchange kk <-> kp (stale column kk moves to kp; L rows and X rows swap)
+      if (kp != kk) {
+        const int c1 = kp - kk - 1;           // (kp, j) <- (j, kk), kk < j < kp
+        const int c2 = n - kp - 1;            // (i, kp) <- (i, kk), i > kp
+        const int c3 = kk;                    // L rows kk <-> kp, columns < kk
+        const int c4 = kkw + 1;               // X rows kk <-> kp, panel columns <= kkw
+        const int tot = 1 + c1 + c2 + c3 + c4;
+        for (int t = tid; t < tot; t += NT) {
+          int u = t;
+          if (u == 0) { put(kp, kp, LpT[(kk - k0) * ldp + kk]); continue; }
+          u -= 1;
+          if (u < c1) { const int j = kk + 1 + u; put(kp, j, LpT[(kk - k0) * ldp + j]); continue; }
+          u -= c1;
+          if (u < c2) { const int i = kp + 1 + u; put(i, kp, LpT[(kk - k0) * ldp + i]); continue; }
+          u -= c2;
+          if (u < c3) {
+            const int c = u;
+            if (c < k0) { const cplx t0 = G(kk, c); G(kk, c) = G(kp, c); G(kp, c) = t0; }
+            else { cplx* col = LpT + (c - k0) * ldp; const cplx t0 = col[kk]; col[kk] = col[kp]; col[kp] = t0; }
+            continue;
+          }
+          u -= c3;
+          { cplx* col = WpT + u * ldp; const cplx t0 = col[kk]; col[kk] = col[kp]; col[kp] = t0; }
+        }
+        if (tid == 0) { const int64_t t0 = perm[kk]; perm[kk] = perm[kp]; perm[kp] = t0; }
+        __syncthreads();
+      }
+      // -- E: store D and the L column(s) into the panel
+      if (kstep == 1) {
+        const cplx d = WpT[kw * ldp + k];
+        for (int i = k + tid; i < n; i += NT)
+          LpT[kw * ldp + i] = i == k ? d : x_div_np(WpT[kw * ldp + i], d);
+        if (tid == 0) tags[k] = 1;
+      } else {
+        const cplx d21 = WpT[kw * ldp + k + 1];
+        const cplx d11 = x_div_py(WpT[(kw + 1) * ldp + k + 1], d21);
+        const cplx d22 = x_div_py(WpT[kw * ldp + k], d21);
+        const cplx t2 = x_div_py(mk(1.0, 0.0), x_sub(x_mul(d11, d22), mk(1.0, 0.0)));
+        const cplx d21s = x_div_py(t2, d21);
+        for (int i = k + tid; i < n; i += NT) {
+          const cplx xk = WpT[kw * ldp + i], xk1 = WpT[(kw + 1) * ldp + i];
+          if (i >= k + 2) {
+            LpT[kw * ldp + i] = x_mul(d21s, x_sub(x_mul(d11, xk), xk1));
+            LpT[(kw + 1) * ldp + i] = x_mul(d21s, x_sub(x_mul(d22, xk1), xk));
+          } else if (i == k) {
+            LpT[kw * ldp + k] = xk;
+          } else {
+            LpT[kw * ldp + k + 1] = xk;           // e = W[k+1, k]
+            LpT[(kw + 1) * ldp + k + 1] = xk1;    // d[k+1]
+          }
+        }
+        if (tid == 0) { tags[k] = 2; tags[k + 1] = 0; }
+        ++n2x2;
+      }
+      ++npiv;
+      __syncthreads();
+      k += kstep;
+      kw += kstep;
+    }
+    if (info >= 0) break;
+    // ---- write the panel back (final L/D of columns < k, stale beyond) ------
+    for (int e = tid; e < (n - k0) * ncols; e += NT) {
+      const int i = k0 + e / ncols, c = e % ncols;
+      if (i >= k0 + c) G(i, k0 + c) = LpT[c * ldp + i];
+    }
+    __syncthreads();
+    // ---- trailing update  A22 -= L21 X21^T  (lower triangle, rank kw) ------
+    double st = 0.0;
+    const int m = n - k;
+    if (m > 0) {
+      for (int r = tid / 32; r < m; r += NT / 32) {
+        const int i = k + r;
+        cplx li[PC];
+#pragma unroll
+        for (int c = 0; c < PC; ++c) li[c] = c < kw ? LpT[c * ldp + i] : mk(0.0, 0.0);
+        // 8 independent loads in flight per lane (the loop is latency-bound otherwise)
+        for (int jb = k; jb <= i; jb += 256) {
+          cplx v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int j = jb + (tid & 31) + 32 * u;
+            if (j <= i) v[u] = G(i, j);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int j = jb + (tid & 31) + 32 * u;
+            if (j <= i) {
+              cplx acc = v[u];
+#pragma unroll
+              for (int c = 0; c < PC; ++c)
+                if (c < kw) c_fms(acc, li[c], WpT[c * ldp + j]);
+              G(i, j) = acc;
+              st = fmax(st, x_abs2(acc));
+            }
+          }
+        }
+      }
+      st = bmax<NT>(st, rd);
+      const double step_max = sqrt(st);
+      if (trail_max > 0.0 && npiv > 0) {
+        const double r = pow(step_max / trail_max, 1.0 / npiv);
+        if (r > growth) growth = r;
+      }
+      trail_max = step_max;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    a.n2x2[b] = n2x2;
+    a.growth[b] = growth;
+    a.info[b] = info;
+  }
+}
+
+}  // namespace d3m
+
+// Blocked variant for n <= 760 (panel fits shared memory); returns -22 when
+// the block is too large (the caller then uses the unblocked exact kernel).
+extern "C" int d3m_bk_blocked_launch(d3m::BkArgs* a, int batch, void* stream) {
+  using namespace d3m;
+  if (batch <= 0) return 0;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(bk_blocked_kernel<16, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(bk_blocked_kernel<8, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cfg = true;
+  }
+  const size_t s16 = (size_t)2 * 17 * (a->n + 1) * sizeof(cplx), s8 = (size_t)2 * 9 * (a->n + 1) * sizeof(cplx);
+  if (s16 <= 200 * 1024) bk_blocked_kernel<16, 256><<<batch, 256, s16, s>>>(*a);
+  else if (s8 <= 200 * 1024) bk_blocked_kernel<8, 256><<<batch, 256, s8, s>>>(*a);
+  else return -22;
+  return (int)cudaGetLastError();
+}

@@ -6,6 +6,7 @@
 // a positive cudaError_t.  Pivot outcomes (info) are written to device
 // arrays; the caller raises the reference's exceptions from them.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -36,6 +37,44 @@ int fail(int code, const char* what) {
     }                                                                        \
   } while (0)
 
+// ---- launch accounting / per-class CUDA-event timing (bench.py roofline) ----
+// Every kernel launched through this file increments g_launches.  When timing
+// is on, each launch is bracketed by a pair of events on its own stream and
+// the elapsed times are summed per class at d3m_counters_read().
+enum { kClsBk = 0, kClsTrsm = 1, kClsGemm = 2, kClsSolve = 3, kClsMisc = 4, kNumCls = 5 };
+std::atomic<long long> g_launches{0};
+bool g_timing = false;
+struct TimedRec { int cls; cudaEvent_t a, b; };
+std::vector<TimedRec> g_pending;
+std::vector<cudaEvent_t> g_free_ev;
+double g_ms[kNumCls] = {0, 0, 0, 0, 0};
+long long g_cnt[kNumCls] = {0, 0, 0, 0, 0};
+
+cudaEvent_t take_event() {
+  if (!g_free_ev.empty()) {
+    cudaEvent_t e = g_free_ev.back();
+    g_free_ev.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+template <typename Fn>
+int launch(int cls, void* stream, Fn fn) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  g_cnt[cls] += 1;
+  if (!g_timing) return fn();
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  TimedRec r{cls, take_event(), take_event()};
+  cudaEventRecord(r.a, s);
+  const int rc = fn();
+  cudaEventRecord(r.b, s);
+  g_pending.push_back(r);
+  return rc;
+}
+
 using d3m::cplx;
 inline cplx* C(void* p) { return static_cast<cplx*>(p); }
 inline const cplx* CC(const void* p) { return static_cast<const cplx*>(p); }
@@ -55,7 +94,7 @@ int d3m_bk_factor_batched(int batch, int n, void* W, int64_t stride_w, int lda, 
   d3m::BkArgs a{C(W), stride_w, n, lda, pivot_tol, check_sym, static_cast<int64_t*>(perm), static_cast<int8_t*>(tags),
                 static_cast<int32_t*>(n2x2), static_cast<double*>(growth), static_cast<int32_t*>(info),
                 static_cast<double*>(scale), static_cast<double*>(asym), C(scratch)};
-  D3M_TRY(d3m_bk_launch(&a, batch, stream));
+  D3M_TRY(launch(kClsBk, stream, [&] { return d3m_bk_launch(&a, batch, stream); }));
   return 0;
 }
 
@@ -66,11 +105,9 @@ int d3m_ldlt_solve_batched(int batch, int n, const void* F, int64_t stride_f, co
   if (batch == 0 || n == 0 || m == 0) return 0;
   d3m::SolveBatch s{CC(F), stride_f, static_cast<const int8_t*>(tags), stride_t, static_cast<const int64_t*>(perm),
                     stride_p, C(work), (int64_t)n * m, nullptr, 0, CC(B), stride_b, n, m, m, ldb};
-  D3M_TRY(d3m_solve_phase_launch(0, &s, batch, stream));   // Z = B[perm]
-  D3M_TRY(d3m_solve_phase_launch(1, &s, batch, stream));   // Z = L^-1 Z
-  D3M_TRY(d3m_solve_phase_launch(2, &s, batch, stream));   // Z = D^-1 Z
-  D3M_TRY(d3m_solve_phase_launch(3, &s, batch, stream));   // Z = L^-T Z
-  D3M_TRY(d3m_solve_phase_launch(4, &s, batch, stream));   // B[perm] = Z
+  // Z = B[perm]; Z = L^-1 Z; Z = D^-1 Z; Z = L^-T Z; B[perm] = Z
+  for (int phase = 0; phase < 5; ++phase)
+    D3M_TRY(launch(kClsSolve, stream, [&] { return d3m_solve_phase_launch(phase, &s, batch, stream); }));
   return 0;
 }
 
@@ -82,7 +119,7 @@ int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* Cm, vo
   cudaError_t e = cudaMemcpyAsync(d_tasks, t, sizeof(d3m::GemmTask) * ntasks, cudaMemcpyHostToDevice,
                                   reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail((int)e, "d3m_zgemm_grouped: task upload");
-  D3M_TRY(d3m_gemm_launch(ta, tb, A, B, Cm, d_tasks, ntasks, tiles, stream));
+  D3M_TRY(launch(kClsGemm, stream, [&] { return d3m_gemm_launch(ta, tb, A, B, Cm, d_tasks, ntasks, tiles, stream); }));
   return 0;
 }
 
@@ -99,7 +136,7 @@ int d3m_schur_reduce_batched(int batch, int n, int m, void* A, const void* D, co
                                 bk_scratch, stream));
   if (n == 0) return 0;
   // RHS = [D | f]  (subdomain.py:177-179), X = A^-1 RHS (factor.py:52-66)
-  D3M_TRY(d3m_pack_rhs_launch(D, f, work_x, n, m, batch, (int64_t)n * m, n, nm1, stream));
+  D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_pack_rhs_launch(D, f, work_x, n, m, batch, (int64_t)n * m, n, nm1, stream); }));
   D3M_TRY(d3m_ldlt_solve_batched(batch, n, A, nn, perm, n, tags, n, work_x, nm1, m + 1, m + 1, work_z, stream));
   if (m == 0) return 0;
   // C = D^T [X | x_f]  (subdomain.py:181,183) on DMMA, one task per domain
@@ -120,27 +157,29 @@ int d3m_schur_reduce_batched(int batch, int n, int m, void* A, const void* D, co
   }
   D3M_TRY(d3m_zgemm_grouped(1, 1, D, work_x, work_c, t.data(), batch, d_tasks, stream));
   // K_D = 0.5 (K_D + K_D^T), g_d
-  D3M_TRY(d3m_schur_finalize_launch(work_c, K_out, g_out, m, batch, (int64_t)m * (m + 1), (int64_t)m * m, m, stream));
+  D3M_TRY(launch(kClsMisc, stream, [&] {
+    return d3m_schur_finalize_launch(work_c, K_out, g_out, m, batch, (int64_t)m * (m + 1), (int64_t)m * m, m, stream);
+  }));
   return 0;
 }
 
 int d3m_block_copy(const void* src, void* dst, const void* d_tasks, int ntasks, int64_t max_elems, void* stream) {
-  D3M_TRY(d3m_block_copy_launch(src, dst, d_tasks, ntasks, max_elems, stream));
+  D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_block_copy_launch(src, dst, d_tasks, ntasks, max_elems, stream); }));
   return 0;
 }
 
 int d3m_gather_rows(const void* src, const void* idx, void* out, int64_t nrows, int cols, void* stream) {
-  D3M_TRY(d3m_gather_index_launch(src, idx, out, nrows, cols, stream));
+  D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_gather_index_launch(src, idx, out, nrows, cols, stream); }));
   return 0;
 }
 
 int d3m_ordered_average(const void* E, const void* ptr, const void* src, void* out, int64_t ng, void* stream) {
-  D3M_TRY(d3m_ordered_average_launch(E, ptr, src, out, ng, stream));
+  D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_ordered_average_launch(E, ptr, src, out, ng, stream); }));
   return 0;
 }
 
 int d3m_zero(void* p, int64_t n, void* stream) {
-  D3M_TRY(d3m_zero_launch(p, n, stream));
+  D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_zero_launch(p, n, stream); }));
   return 0;
 }
 
@@ -156,123 +195,160 @@ int d3m_zero(void* p, int64_t n, void* stream) {
 // a helper stream (lookahead depth 1).
 // ---------------------------------------------------------------------------
 int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_off, const int64_t* h_panel_off,
-                        const int64_t* h_panel_rows, const int64_t* h_piv_off, const int64_t* h_task_ptr,
-                        const int64_t* h_task_next, const int64_t* h_tiles_next, const int64_t* h_tiles_rest,
-                        const void* d_tasks, void* d_pool, void* d_xbuf, int64_t xbuf_elems, void* d_perm,
-                        void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale, void* d_asym,
-                        void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead, void* stream) {
-  static cudaStream_t side = nullptr;
-  static cudaEvent_t ev_next = nullptr, ev_rest = nullptr;
-  if (!side) {
-    if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess ||
+                        const int64_t* h_panel_rows, const int64_t* h_piv_off, const int64_t* h_binv_off,
+                        const int64_t* h_task_ptr, const int64_t* h_task_next, const int64_t* h_tiles_next,
+                        const int64_t* h_tiles_rest, const int64_t* h_tiles_trsm, const void* d_tasks,
+                        const void* d_trsm_tasks, void* d_pool, void* d_binv, void* d_xbuf, int64_t xbuf_elems,
+                        void* d_perm, void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale,
+                        void* d_asym, void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead,
+                        void* stream) {
+  // Streams: the caller's stream hands over to a high-priority critical
+  // stream (BK -> L^-1 -> panel GEMM -> D^-1 -> next-column update) and a
+  // low-priority bulk stream (the rest of each column's trailing update).
+  static cudaStream_t crit = nullptr, side = nullptr;
+  static cudaEvent_t ev_next = nullptr, ev_rest = nullptr, ev_in = nullptr, ev_out = nullptr;
+  if (!crit) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&crit, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev_next, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming) != cudaSuccess)
       return fail(-12, "d3m_block_ldlt_exec: stream/event creation");
   }
-  cudaStream_t s0 = reinterpret_cast<cudaStream_t>(stream);
+  cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
+  cudaStream_t s0 = lookahead ? crit : user;
+  if (lookahead) {
+    cudaEventRecord(ev_in, user);
+    cudaStreamWaitEvent(crit, ev_in, 0);
+  }
   auto* tasks = static_cast<const d3m::GemmTask*>(d_tasks);
+  auto* ttasks = static_cast<const d3m::GemmTask*>(d_trsm_tasks);
   cplx* pool = C(d_pool);
+  cplx* binv = C(d_binv);
   bool rest_pending = false;
   for (int j = 0; j < nb; ++j) {
     const int nj = (int)h_sizes[j];
     const int64_t R = h_panel_rows[j];
     cplx* xbuf = C(d_xbuf) + (lookahead ? (j & 1) * (xbuf_elems / 2) : 0);
     if (R * nj > (lookahead ? xbuf_elems / 2 : xbuf_elems)) return fail(-22, "d3m_block_ldlt_exec: xbuf too small");
-    d3m::BkArgs a{pool + h_diag_off[j], 0, nj, nj, pivot_tol, check_sym,
-                  static_cast<int64_t*>(d_perm) + h_piv_off[j], static_cast<int8_t*>(d_tags) + h_piv_off[j],
+    int64_t* perm = static_cast<int64_t*>(d_perm) + h_piv_off[j];
+    int8_t* tags = static_cast<int8_t*>(d_tags) + h_piv_off[j];
+    cplx* diag = pool + h_diag_off[j];
+    d3m::BkArgs a{diag, 0, nj, nj, pivot_tol, check_sym, perm, tags,
                   static_cast<int32_t*>(d_n2x2) + j, static_cast<double*>(d_growth) + j,
                   static_cast<int32_t*>(d_info) + j, static_cast<double*>(d_scale) + j,
                   static_cast<double*>(d_asym) + j, C(d_bk_scratch)};
-    if (nj > 0) D3M_TRY(d3m_bk_launch(&a, 1, s0));
-    if (R > 0)
-      D3M_TRY(d3m_panel_trsm_launch(pool + h_panel_off[j], xbuf, (int)R, nj, pool + h_diag_off[j],
-                                    static_cast<int64_t*>(d_perm) + h_piv_off[j],
-                                    static_cast<int8_t*>(d_tags) + h_piv_off[j], s0));
+    if (nj > 0) {
+      // blocked panel BK (shared-memory panel) for supernode blocks; the
+      // unblocked bit-exact kernel when the panel does not fit
+      D3M_TRY(launch(kClsBk, s0, [&] {
+        const int rc = d3m_bk_blocked_launch(&a, 1, s0);
+        return rc == -22 ? d3m_bk_launch(&a, 1, s0) : rc;
+      }));
+      // Binv_j = L_jj^-1 P_j (also used by block_solve)
+      D3M_TRY(launch(kClsTrsm, s0, [&] {
+        return d3m_tri_inv_launch(diag, 0, perm, 0, tags, 0, binv + h_binv_off[j], 0, nj, 1, s0);
+      }));
+    }
+    if (R > 0) {
+      // X_ij = K_ij P^T L_jj^-T = panel * Binv^T on DMMA, then L_ij = X_ij D_jj^-1
+      D3M_TRY(launch(kClsTrsm, s0, [&] {
+        return d3m_gemm_launch(0, 0, pool, binv, xbuf, ttasks + j, 1, (int)h_tiles_trsm[j], s0);
+      }));
+      D3M_TRY(launch(kClsTrsm, s0, [&] { return d3m_dinv_rows_launch(xbuf, pool + h_panel_off[j], R, nj, diag, tags, s0); }));
+    }
     const int64_t t0 = h_task_ptr[j], tn = h_task_next[j], t1 = h_task_ptr[j + 1];
     if (rest_pending) {
       cudaStreamWaitEvent(s0, ev_rest, 0);
       rest_pending = false;
     }
     if (tn > t0)
-      D3M_TRY(d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + t0, (int)(tn - t0), (int)h_tiles_next[j], s0));
+      D3M_TRY(launch(kClsGemm, s0, [&] {
+        return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + t0, (int)(tn - t0), (int)h_tiles_next[j], s0);
+      }));
     if (t1 > tn) {
       if (lookahead) {
         cudaEventRecord(ev_next, s0);
         cudaStreamWaitEvent(side, ev_next, 0);
-        D3M_TRY(d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], side));
+        D3M_TRY(launch(kClsGemm, side, [&] {
+          return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], side);
+        }));
         cudaEventRecord(ev_rest, side);
         rest_pending = true;
       } else {
-        D3M_TRY(d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], s0));
+        D3M_TRY(launch(kClsGemm, s0, [&] {
+          return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], s0);
+        }));
       }
     }
   }
   if (rest_pending) cudaStreamWaitEvent(s0, ev_rest, 0);
+  if (lookahead) {
+    cudaEventRecord(ev_out, s0);
+    cudaStreamWaitEvent(user, ev_out, 0);
+  }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail((int)e, "d3m_block_ldlt_exec: launch");
   return 0;
 }
 
 // ---------------------------------------------------------------------------
-// block_solve executor (factor.py:243-310), all RHS in one pass.
-//   b   : N x nrhs, plan order, overwritten by the forward sweep
-//   u   : N x nrhs, receives D^-1 z, then w, then the permuted solution
-//   x   : N x nrhs, solution in plan order
-//   tmp : max_j n_j x nrhs;  gbuf : max_j R_j x nrhs
-//   d_gidx: concatenated global row indices of every panel (per column j the
-//           rows of its pattern blocks), h_gptr its CSR pointer.
+// block_solve executor (factor.py:243-310), all RHS in one pass, every
+// stage a DMMA GEMM against the stored factor:
+//   forward  z_j = Binv_j b_j,  u_j = D_j^-1 z_j,  b_i -= L_ij z_j
+//   backward w_j = u_j - sum_i L_ij^T x_i  (split over i, ordered sum),
+//            x_j = Binv_j^T w_j
+//   b, u, x : N x nrhs plan order (b consumed);  tmp: max n_j x nrhs;
+//   part    : max_j (|pattern(j)| n_j) x nrhs
 // ---------------------------------------------------------------------------
 int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_off, const int64_t* h_diag_off,
-                         const int64_t* h_panel_off, const int64_t* h_panel_rows, const int64_t* h_piv_off,
-                         const int64_t* h_pat_ptr, const int64_t* h_pat_idx, const int64_t* h_gptr,
-                         const void* d_gidx, const void* d_pool, const void* d_perm, const void* d_tags, void* d_b,
-                         void* d_u, void* d_x, void* d_tmp, void* d_gbuf, int nrhs, void* d_tasks, int64_t task_cap,
-                         void* stream) {
+                         const int64_t* h_panel_off, const int64_t* h_piv_off, const int64_t* h_binv_off,
+                         const int64_t* h_pat_ptr, const int64_t* h_pat_idx, const void* d_pool,
+                         const void* d_binv, const void* d_tags, void* d_b, void* d_u, void* d_x, void* d_tmp,
+                         void* d_part, int nrhs, void* d_tasks, int64_t task_cap, void* stream) {
   if (nb <= 0 || nrhs <= 0) return 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const cplx* pool = CC(d_pool);
-  // forward-update tasks: one per pattern block (i, j); backward: one per j
   const int64_t npat = h_pat_ptr[nb];
-  if (npat + nb > task_cap) return fail(-22, "d3m_block_solve_exec: task buffer too small");
-  std::vector<d3m::GemmTask> t(npat + nb);
-  std::vector<int> tiles_f(nb), tiles_b(nb);
+  // task layout: [0, nb) z_j;  [nb, nb+npat) forward updates;
+  //              [nb+npat, nb+2npat) backward partials;  [nb+2npat, 2nb+2npat) x_j
+  const int64_t ntask = 2 * nb + 2 * npat;
+  if (ntask > task_cap) return fail(-22, "d3m_block_solve_exec: task buffer too small");
+  std::vector<d3m::GemmTask> t(ntask);
+  std::memset(t.data(), 0, sizeof(d3m::GemmTask) * ntask);
+  std::vector<int> tz(nb), tf(nb), tp(nb), tx(nb);
+  auto mk = [&](d3m::GemmTask& k, int64_t a, int64_t b, int64_t c, int m, int n, int kk, int lda, int ldb, int ldc,
+                int flags) {
+    k.a_off = a; k.b_off = b; k.c_off = c; k.m = m; k.n = n; k.k = kk;
+    k.lda = lda; k.ldb = ldb; k.ldc = ldc; k.flags = flags;
+  };
   for (int j = 0; j < nb; ++j) {
     const int nj = (int)h_sizes[j];
+    mk(t[j], h_binv_off[j], h_row_off[j] * nrhs, 0, nj, nrhs, nj, nj, nrhs, nrhs, d3m::kGemmStore);
+    tz[j] = d3m_gemm_prepare_tasks(&t[j], 1);
     int64_t prow = 0;
     for (int64_t p = h_pat_ptr[j]; p < h_pat_ptr[j + 1]; ++p) {
       const int64_t i = h_pat_idx[p];
-      d3m::GemmTask& k = t[p];
-      std::memset(&k, 0, sizeof(k));
-      k.a_off = h_panel_off[j] + prow * nj;    // L_ij: n_i x n_j row-major (A, normal)
-      k.b_off = 0;                             // z_j in tmp: n_j x nrhs = K x N (TB)
-      k.c_off = h_row_off[i] * nrhs;           // b_i
-      k.m = (int)h_sizes[i];
-      k.n = nrhs;
-      k.k = nj;
-      k.lda = nj;
-      k.ldb = nrhs;
-      k.ldc = nrhs;
-      k.flags = d3m::kGemmSub;
-      prow += h_sizes[i];
+      const int ni = (int)h_sizes[i];
+      mk(t[nb + p], h_panel_off[j] + prow * nj, 0, h_row_off[i] * nrhs, ni, nrhs, nj, nj, nrhs, nrhs,
+         d3m::kGemmSub);
+      mk(t[nb + npat + p], h_panel_off[j] + prow * nj, h_row_off[i] * nrhs, (p - h_pat_ptr[j]) * (int64_t)nj * nrhs,
+         nj, nrhs, ni, nj, nrhs, nrhs, d3m::kGemmStore);
+      prow += ni;
     }
-    tiles_f[j] = d3m_gemm_prepare_tasks(t.data() + h_pat_ptr[j], (int)(h_pat_ptr[j + 1] - h_pat_ptr[j]));
-    d3m::GemmTask& k = t[npat + j];
-    std::memset(&k, 0, sizeof(k));
-    k.a_off = h_panel_off[j];                  // panel stored R_j x n_j = K x M (TA)
-    k.b_off = 0;                               // gbuf R_j x nrhs = K x N (TB)
-    k.c_off = h_row_off[j] * nrhs;             // u_j
-    k.m = nj;
-    k.n = nrhs;
-    k.k = (int)h_panel_rows[j];
-    k.lda = nj;
-    k.ldb = nrhs;
-    k.ldc = nrhs;
-    k.flags = d3m::kGemmSub;
-    tiles_b[j] = d3m_gemm_prepare_tasks(&k, 1);
+    const int np = (int)(h_pat_ptr[j + 1] - h_pat_ptr[j]);
+    tf[j] = d3m_gemm_prepare_tasks(&t[nb + h_pat_ptr[j]], np);
+    tp[j] = d3m_gemm_prepare_tasks(&t[nb + npat + h_pat_ptr[j]], np);
+    mk(t[nb + 2 * npat + j], h_binv_off[j], 0, h_row_off[j] * nrhs, nj, nrhs, nj, nj, nrhs, nrhs, d3m::kGemmStore);
+    tx[j] = d3m_gemm_prepare_tasks(&t[nb + 2 * npat + j], 1);
   }
-  cudaError_t e = cudaMemcpyAsync(d_tasks, t.data(), sizeof(d3m::GemmTask) * t.size(), cudaMemcpyHostToDevice, s);
+  cudaError_t e = cudaMemcpyAsync(d_tasks, t.data(), sizeof(d3m::GemmTask) * ntask, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return fail((int)e, "d3m_block_solve_exec: task upload");
   auto* dt = static_cast<const d3m::GemmTask*>(d_tasks);
+  const cplx* pool = CC(d_pool);
+  const cplx* binv = CC(d_binv);
   cplx* b = C(d_b);
   cplx* u = C(d_u);
   cplx* x = C(d_x);
@@ -280,27 +356,35 @@ int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_of
   for (int j = 0; j < nb; ++j) {
     const int nj = (int)h_sizes[j];
     if (nj == 0) continue;
-    d3m::SolveBatch sb{pool + h_diag_off[j], 0, static_cast<const int8_t*>(d_tags) + h_piv_off[j], 0,
-                       static_cast<const int64_t*>(d_perm) + h_piv_off[j], 0, tmp, 0, u + h_row_off[j] * nrhs, 0,
-                       b + h_row_off[j] * nrhs, 0, nj, nrhs, nrhs, nrhs};
-    D3M_TRY(d3m_solve_phase_launch(0, &sb, 1, s));   // z_j = b_j[perm]
-    D3M_TRY(d3m_solve_phase_launch(1, &sb, 1, s));   // z_j = L_jj^-1 z_j, u_j = D^-1 z_j
-    const int64_t p0 = h_pat_ptr[j], p1 = h_pat_ptr[j + 1];
-    if (p1 > p0) D3M_TRY(d3m_gemm_launch(0, 1, pool, tmp, b, dt + p0, (int)(p1 - p0), tiles_f[j], s));
+    const int8_t* tags = static_cast<const int8_t*>(d_tags) + h_piv_off[j];
+    const cplx* diag = pool + h_diag_off[j];
+    D3M_TRY(launch(kClsSolve, s, [&] { return d3m_gemm_launch(0, 1, binv, b, tmp, dt + j, 1, tz[j], s); }));
+    D3M_TRY(launch(kClsSolve, s, [&] {
+      return d3m_dinv_left_copy_launch(tmp, u + h_row_off[j] * nrhs, nj, nrhs, diag, tags, s);
+    }));
+    const int np = (int)(h_pat_ptr[j + 1] - h_pat_ptr[j]);
+    if (np > 0)
+      D3M_TRY(launch(kClsSolve, s, [&] {
+        return d3m_gemm_launch(0, 1, pool, tmp, b, dt + nb + h_pat_ptr[j], np, tf[j], s);
+      }));
   }
   for (int j = nb - 1; j >= 0; --j) {
     const int nj = (int)h_sizes[j];
     if (nj == 0) continue;
-    const int64_t R = h_panel_rows[j];
-    if (R > 0) {
-      D3M_TRY(d3m_gather_index_launch(x, static_cast<const int64_t*>(d_gidx) + h_gptr[j], d_gbuf, R, nrhs, s));
-      D3M_TRY(d3m_gemm_launch(1, 1, pool, d_gbuf, u, dt + npat + j, 1, tiles_b[j], s));
+    const int np = (int)(h_pat_ptr[j + 1] - h_pat_ptr[j]);
+    cplx* uj = u + h_row_off[j] * nrhs;
+    if (np > 0) {
+      D3M_TRY(launch(kClsSolve, s, [&] {
+        return d3m_gemm_launch(1, 1, pool, x, d_part, dt + nb + npat + h_pat_ptr[j], np, tp[j], s);
+      }));
+      D3M_TRY(launch(kClsSolve, s, [&] {
+        return d3m_sub_partials_launch(uj, d_part, np, (int64_t)nj * nrhs, tmp, s);
+      }));
+    } else {
+      cudaError_t ce = cudaMemcpyAsync(tmp, uj, sizeof(cplx) * nj * nrhs, cudaMemcpyDeviceToDevice, s);
+      if (ce != cudaSuccess) return fail((int)ce, "d3m_block_solve_exec: copy");
     }
-    d3m::SolveBatch sb{pool + h_diag_off[j], 0, static_cast<const int8_t*>(d_tags) + h_piv_off[j], 0,
-                       static_cast<const int64_t*>(d_perm) + h_piv_off[j], 0, u + h_row_off[j] * nrhs, 0, nullptr, 0,
-                       x + h_row_off[j] * nrhs, 0, nj, nrhs, nrhs, nrhs};
-    D3M_TRY(d3m_solve_phase_launch(3, &sb, 1, s));   // w = L_jj^-T w
-    D3M_TRY(d3m_solve_phase_launch(4, &sb, 1, s));   // x_j[perm] = w
+    D3M_TRY(launch(kClsSolve, s, [&] { return d3m_gemm_launch(1, 1, binv, tmp, x, dt + nb + 2 * npat + j, 1, tx[j], s); }));
   }
   return 0;
 }
@@ -332,7 +416,40 @@ int d3m_recover_batched(int batch, int n, int m, const void* F, const void* perm
     D3M_TRY(d3m_zgemm_grouped(0, 1, D, lam, rhs, t.data(), batch, d_tasks, stream));
   }
   D3M_TRY(d3m_ldlt_solve_batched(batch, n, F, (int64_t)n * n, perm, n, tags, n, rhs, n, 1, 1, work, stream));
-  D3M_TRY(d3m_ordered_average_launch(rhs, avg_ptr, avg_src, out, nglob, stream));
+  D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_ordered_average_launch(rhs, avg_ptr, avg_src, out, nglob, stream); }));
+  return 0;
+}
+
+void d3m_set_timing(int on) { g_timing = on != 0; }
+
+void d3m_counters_reset(void) {
+  for (auto& r : g_pending) {
+    cudaEventSynchronize(r.b);
+    g_free_ev.push_back(r.a);
+    g_free_ev.push_back(r.b);
+  }
+  g_pending.clear();
+  g_launches.store(0);
+  for (int c = 0; c < kNumCls; ++c) { g_ms[c] = 0; g_cnt[c] = 0; }
+}
+
+// launches: total kernel launches since reset; ms[5] / n[5]: summed event
+// time and launch count per class (bk, trsm, gemm-update, solve, misc).
+int d3m_counters_read(int64_t* launches, double* ms, int64_t* n) {
+  for (auto& r : g_pending) {
+    cudaEventSynchronize(r.b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    g_ms[r.cls] += t;
+    g_free_ev.push_back(r.a);
+    g_free_ev.push_back(r.b);
+  }
+  g_pending.clear();
+  if (launches) *launches = g_launches.load();
+  for (int c = 0; c < kNumCls; ++c) {
+    if (ms) ms[c] = g_ms[c];
+    if (n) n[c] = g_cnt[c];
+  }
   return 0;
 }
 

@@ -39,6 +39,7 @@ struct SolveBatch {
 
 extern "C" {
 int d3m_bk_launch(d3m::BkArgs* a, int batch, void* stream);
+int d3m_bk_blocked_launch(d3m::BkArgs* a, int batch, void* stream);
 // phase: 0 gather Z=B[perm], 1 forward (+U=D^-1 Z), 2 D^-1, 3 backward, 4 scatter B[perm]=Z
 int d3m_solve_phase_launch(int phase, d3m::SolveBatch* a, int batch, void* stream);
 int d3m_panel_trsm_launch(void* P, void* X, int R, int n, const void* F, const void* perm, const void* tags,
@@ -53,6 +54,11 @@ int d3m_ordered_average_launch(const void* E, const void* ptr, const void* src, 
 int d3m_gather_index_launch(const void* src, const void* idx, void* out, int64_t nrows, int cols, void* stream);
 int d3m_block_copy_launch(const void* src, void* dst, const void* dtasks, int ntasks, int64_t max_elems, void* stream);
 int d3m_zero_launch(void* p, int64_t n, void* stream);
+int d3m_tri_inv_launch(const void* F, int64_t stride_f, const void* perm, int64_t stride_p, const void* tags,
+                       int64_t stride_t, void* Binv, int64_t stride_b, int n, int batch, void* stream);
+int d3m_dinv_rows_launch(const void* X, void* P, int64_t R, int n, const void* F, const void* tags, void* stream);
+int d3m_dinv_left_copy_launch(const void* Z, void* U, int n, int m, const void* F, const void* tags, void* stream);
+int d3m_sub_partials_launch(const void* u, const void* partial, int np, int64_t len, void* out, void* stream);
 }
 
 #include "d3m_gemm.h"

@@ -250,3 +250,188 @@ extern "C" int d3m_solve_phase_launch(int phase, d3m::SolveBatch* a, int batch, 
   }
   return (int)cudaGetLastError();
 }
+
+namespace d3m {
+
+// -------------------------------------------------------------------------
+// Binv = L^-1 P of a packed factor (n <= 1024), written row-major n x n:
+// column q of L^-1 (forward substitution of e_q) lands in column perm[q].
+// With it the panel TRSM is one DMMA GEMM,  X_ij = K_ij P^T L^-T =
+// K_ij Binv^T, and the block substitutions are GEMMs:  z = Binv b,
+// x = Binv^T w.  CTA = 16 columns (one 16-lane group each); the 16 columns
+// of L^-1 live in shared memory (column-major per group), rows of L are
+// streamed through a double-buffered cp.async ring of INV_ROWS rows.
+// -------------------------------------------------------------------------
+constexpr int INV_THREADS = 256;
+constexpr int INV_COLS = INV_THREADS / 16;
+constexpr int INV_ROWS = 8;
+
+__device__ __forceinline__ void cp_async16_pred(void* smem, const void* gmem, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(pred ? 16 : 0));
+}
+
+__global__ void __launch_bounds__(INV_THREADS)
+tri_inv_kernel(const cplx* Fbase, int64_t stride_f, const int64_t* permbase, int64_t stride_p,
+               const int8_t* tagsbase, int64_t stride_t, cplx* Binv_base, int64_t stride_b, int n) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b = blockIdx.y;
+  const cplx* F = Fbase + b * stride_f;
+  const int64_t* perm = permbase + b * stride_p;
+  const int8_t* tags = tagsbase + b * stride_t;
+  cplx* Binv = Binv_base + b * stride_b;
+  const int q0 = blockIdx.x * INV_COLS;
+  const int g = threadIdx.x >> 4, s = threadIdx.x & 15;
+  const int q = q0 + g;
+  const int w = n - q0;                          // rows/cols touched by this CTA
+  cplx* Y = reinterpret_cast<cplx*>(smem_raw);   // [INV_COLS][w]
+  cplx* Lr = Y + (size_t)INV_COLS * w;           // [2][INV_ROWS][w]
+  cplx* y = Y + (size_t)g * w;                   // this group's column, index c - q0
+  for (int c = s; c < w; c += 16) y[c] = mk(q0 + c == q ? 1.0 : 0.0, 0.0);
+
+  auto load_chunk = [&](int chunk, int buf) {
+    // rows q0 + chunk*INV_ROWS + r, columns q0 .. q0 + w - 1 (strict lower part)
+    cplx* dst = Lr + (size_t)buf * INV_ROWS * w;
+    for (int e = threadIdx.x; e < INV_ROWS * w; e += INV_THREADS) {
+      const int r = e / w, c = e - r * w;
+      const int row = q0 + chunk * INV_ROWS + r, col = q0 + c;
+      const bool ok = row < n && col < row;
+      cp_async16_pred(dst + e, ok ? F + (int64_t)row * n + col : F, ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  const int nchunks = (w + INV_ROWS - 1) / INV_ROWS;
+  load_chunk(0, 0);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    if (ch + 1 < nchunks) load_chunk(ch + 1, (ch + 1) & 1);
+    else asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();
+    const cplx* L = Lr + (size_t)(ch & 1) * INV_ROWS * w;
+    for (int r = 0; r < INV_ROWS; ++r) {
+      const int c = ch * INV_ROWS + r;           // local row index
+      if (c >= w) break;
+      const cplx* Lc = L + (size_t)r * w;
+      cplx acc = mk(0.0, 0.0);
+      const int lo = q - q0;                     // y[c'] = 0 below q
+      for (int cp = lo + s; cp < c; cp += 16) {
+        cplx l = Lc[cp];
+        if (cp == c - 1 && tags[q0 + cp] == 2) l = mk(0.0, 0.0);
+        c_fma(acc, l, y[cp]);
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, 16);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, 16);
+      }
+      if (s == 0 && c > lo && q < n) y[c] = mk(-acc.x, -acc.y);
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+  if (q >= n) return;
+  const int64_t pc = perm[q];
+  for (int row = s; row < n; row += 16)
+    Binv[(int64_t)row * n + pc] = row < q0 ? mk(0.0, 0.0) : y[row - q0];
+}
+
+// L_panel rows = X rows * D^-1 (apply_dinv_right, kernels.py:184-202);
+// one thread per (row, pivot block).
+__global__ void dinv_rows_kernel(const cplx* X, cplx* P, int64_t R, int n, const cplx* F, const int8_t* tags) {
+  const int64_t total = R * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / n;
+    const int c = (int)(e - r * n);
+    const int8_t t = tags[c];
+    if (t == 1) {
+      P[r * n + c] = x_div_np(X[r * n + c], F[(int64_t)c * n + c]);
+    } else if (t == 2) {
+      cplx x0 = X[r * n + c], x1 = X[r * n + c + 1];
+      dinv_pair(F[(int64_t)c * n + c], F[(int64_t)(c + 1) * n + c], F[(int64_t)(c + 1) * n + c + 1], x0, x1);
+      P[r * n + c] = x0;
+      P[r * n + c + 1] = x1;
+    }
+  }
+}
+
+// U = D^-1 Z (apply_dinv_left, kernels.py:161-181), Z and U n x m (ld m)
+__global__ void dinv_left_copy_kernel(const cplx* Z, cplx* U, int n, int m, const cplx* F, const int8_t* tags) {
+  const int64_t total = (int64_t)n * m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / m), col = (int)(e % m);
+    const int8_t t = tags[c];
+    if (t == 1) {
+      U[e] = x_div_np(Z[e], F[(int64_t)c * n + c]);
+    } else if (t == 2) {
+      cplx x0 = Z[e], x1 = Z[e + m];
+      dinv_pair(F[(int64_t)c * n + c], F[(int64_t)(c + 1) * n + c], F[(int64_t)(c + 1) * n + c + 1], x0, x1);
+      U[e] = x0;
+      U[e + m] = x1;
+    }
+    (void)col;
+  }
+}
+
+// out = u - sum_{p < np} partial[p]  (fixed order), each of length len
+__global__ void sub_partials_kernel(const cplx* u, const cplx* partial, int np, int64_t len, cplx* out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
+    cplx acc = mk(0.0, 0.0);
+    for (int p = 0; p < np; ++p) acc = c_add(acc, partial[p * len + e]);
+    out[e] = c_sub(u[e], acc);
+  }
+}
+
+}  // namespace d3m
+
+extern "C" int d3m_tri_inv_launch(const void* F, int64_t stride_f, const void* perm, int64_t stride_p,
+                                  const void* tags, int64_t stride_t, void* Binv, int64_t stride_b, int n, int batch,
+                                  void* stream) {
+  using namespace d3m;
+  if (n <= 0 || batch <= 0) return 0;
+  const size_t smem = (size_t)(INV_COLS + 2 * INV_ROWS) * n * sizeof(cplx);
+  if (smem > 227 * 1024) return -22;
+  static int configured = 0;
+  if (!configured) {
+    cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    configured = 1;
+  }
+  const dim3 grid((n + INV_COLS - 1) / INV_COLS, batch);
+  tri_inv_kernel<<<grid, INV_THREADS, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(F), stride_f, static_cast<const int64_t*>(perm), stride_p,
+      static_cast<const int8_t*>(tags), stride_t, static_cast<cplx*>(Binv), stride_b, n);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int d3m_dinv_rows_launch(const void* X, void* P, int64_t R, int n, const void* F, const void* tags,
+                                    void* stream) {
+  using namespace d3m;
+  if (R <= 0 || n <= 0) return 0;
+  const int64_t total = R * n;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 8192);
+  dinv_rows_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(X), static_cast<cplx*>(P), R, n, static_cast<const cplx*>(F),
+      static_cast<const int8_t*>(tags));
+  return (int)cudaGetLastError();
+}
+
+extern "C" int d3m_dinv_left_copy_launch(const void* Z, void* U, int n, int m, const void* F, const void* tags,
+                                         void* stream) {
+  using namespace d3m;
+  if (n <= 0 || m <= 0) return 0;
+  const int64_t total = (int64_t)n * m;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
+  dinv_left_copy_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(Z), static_cast<cplx*>(U), n, m, static_cast<const cplx*>(F),
+      static_cast<const int8_t*>(tags));
+  return (int)cudaGetLastError();
+}
+
+extern "C" int d3m_sub_partials_launch(const void* u, const void* partial, int np, int64_t len, void* out,
+                                       void* stream) {
+  using namespace d3m;
+  if (len <= 0) return 0;
+  const int blocks = (int)std::min<int64_t>((len + 255) / 256, 4096);
+  sub_partials_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(u), static_cast<const cplx*>(partial), np, len, static_cast<cplx*>(out));
+  return (int)cudaGetLastError();
+}

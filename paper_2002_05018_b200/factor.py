@@ -306,6 +306,18 @@ class _Schedule:
             for c, name in enumerate(_lib.GEMM_TASK.names):
                 tasks[name] = arr[:, c]
         self.tasks = tasks
+        # panel TRSM as one GEMM per column: X = panel * Binv_j^T
+        self.binv_off = np.concatenate([[0], np.cumsum(sizes * sizes)]).astype(np.int64)
+        tt = np.zeros(nb, dtype=_lib.GEMM_TASK)
+        tt["a_off"] = self.panel_off
+        tt["b_off"] = self.binv_off[:nb]
+        tt["m"] = self.panel_rows
+        tt["n"] = tt["k"] = tt["lda"] = tt["ldb"] = tt["ldc"] = sizes
+        tt["flags"] = _lib.GEMM_STORE
+        tt["tiles_n"] = (sizes + bm - 1) // bm
+        self.tiles_trsm = (((self.panel_rows + bm - 1) // bm) * ((sizes + bm - 1) // bm)).astype(np.int64)
+        self.d_trsm_tasks = upload_bytes(tt)
+        self.part_rows = int(max([len(p) * int(sizes[j]) for j, p in enumerate(pattern)] + [1]))
         self.task_ptr = np.asarray(ptr, dtype=np.int64)
         self.task_next = np.asarray(nxt if nxt else [0], dtype=np.int64)
         self.tiles_next = np.asarray(tiles_n if tiles_n else [0], dtype=np.int64)
@@ -325,6 +337,7 @@ class _Schedule:
                                     for j in range(nb) for a, i in enumerate(pattern[j]) for kk in pattern[j][:a + 1]))
         self.flops_trsm = int(sum(4 * int(self.panel_rows[j]) * int(sizes[j]) ** 2 for j in range(nb)))
         self.flops_bk = int(sum(8 * int(s) ** 3 // 3 for s in sizes))
+        self.stats_cache = {}
 
 
 def _schedule(plan: EliminationPlan) -> _Schedule:
@@ -447,10 +460,13 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
         raise ValueError("plan and matrix disagree on block count")
     t = require_cuda()
     inv = plan.order.inverse()
-    stored, flops, peak = _reference_stats(list(K.blocks), K.sizes, plan, inv)
     if nb == 0:
         return BlockFactor(plan, [], {}, FactorStats(0, 0, 0, 1.0, 0))
     sched = _schedule(plan)
+    keyset = frozenset(K.blocks)
+    if keyset not in sched.stats_cache:
+        sched.stats_cache[keyset] = _reference_stats(list(K.blocks), K.sizes, plan, inv)
+    stored, flops, peak = sched.stats_cache[keyset]
     pool = empty(max(sched.pool_elems, 1))
     _lib.call("d3m_zero", _P(pool), sched.pool_elems, stream_ptr())
     _upload_K(K, sched, plan, pool)
@@ -462,14 +478,16 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
     sc = t.empty(nb, dtype=t.float64, device="cuda")
     asy = t.empty(nb, dtype=t.float64, device="cuda")
     xbuf = empty(sched.xbuf_elems)
+    binv = empty(max(int(sched.binv_off[-1]), 1))
     nmax = int(sched.sizes.max())
     scratch = empty(4 * nmax) if 64 * nmax > 200 * 1024 else None
     H = _lib.hptr
     _lib.call("d3m_block_ldlt_exec", nb, H(sched.sizes), H(sched.diag_off), H(sched.panel_off),
-              H(sched.panel_rows), H(sched.row_off), H(sched.task_ptr), H(sched.task_next),
-              H(sched.tiles_next), H(sched.tiles_rest), _P(sched.d_tasks), _P(pool), _P(xbuf),
-              sched.xbuf_elems, _P(perm), _P(tags), _P(info), _P(n2), _P(gr), _P(sc), _P(asy),
-              _P(scratch), float(pivot_tol), 1, int(bool(lookahead)), stream_ptr())
+              H(sched.panel_rows), H(sched.row_off), H(sched.binv_off), H(sched.task_ptr), H(sched.task_next),
+              H(sched.tiles_next), H(sched.tiles_rest), H(sched.tiles_trsm), _P(sched.d_tasks),
+              _P(sched.d_trsm_tasks), _P(pool), _P(binv), _P(xbuf), sched.xbuf_elems, _P(perm), _P(tags),
+              _P(info), _P(n2), _P(gr), _P(sc), _P(asy), _P(scratch), float(pivot_tol), 1,
+              int(bool(lookahead)), stream_ptr())
     info_h = info.cpu().numpy()
     bad = np.flatnonzero(info_h != -1)
     if bad.size:
@@ -487,7 +505,9 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
                                 float(gr_h[j]), int(n2_h[j])))
     stats = FactorStats(stored, flops, peak, float(max(gr_h.max(), 1.0)) if nb else 1.0, int(n2_h.sum()))
     stats.growth_factor = float(max((f.growth for f in diag), default=1.0))
-    return BlockFactor(plan, diag, _OffDiag(sched, pool), stats, sched, pool, perm, tags)
+    F = BlockFactor(plan, diag, _OffDiag(sched, pool), stats, sched, pool, perm, tags)
+    F._binv = binv
+    return F
 
 
 def block_solve(F: BlockFactor, g: list) -> list:
@@ -536,15 +556,14 @@ def block_solve(F: BlockFactor, g: list) -> list:
     u = empty((N, cols))
     x = empty((N, cols))
     tmp = empty((int(sched.sizes.max()), cols))
-    gbuf = empty((max(1, int(sched.panel_rows.max())), cols))
-    cap = int(sched.pat_ptr[-1]) + nb
+    part = empty((sched.part_rows, cols))
+    cap = 2 * int(sched.pat_ptr[-1]) + 2 * nb
     d_tasks = t.empty(64 * cap, dtype=t.uint8, device="cuda")
     H = _lib.hptr
     _lib.call("d3m_block_solve_exec", nb, H(sched.sizes), H(sched.row_off), H(sched.diag_off),
-              H(sched.panel_off), H(sched.panel_rows), H(sched.row_off), H(sched.pat_ptr),
-              H(sched.pat_idx if sched.pat_idx.size else np.zeros(1, np.int64)), H(sched.gptr),
-              _P(sched.d_gidx), _P(F._pool), _P(F._perm), _P(F._tags), _P(b), _P(u), _P(x), _P(tmp),
-              _P(gbuf), int(cols), _P(d_tasks), cap, stream_ptr())
+              H(sched.panel_off), H(sched.row_off), H(sched.binv_off), H(sched.pat_ptr),
+              H(sched.pat_idx if sched.pat_idx.size else np.zeros(1, np.int64)), _P(F._pool), _P(F._binv),
+              _P(F._tags), _P(b), _P(u), _P(x), _P(tmp), _P(part), int(cols), _P(d_tasks), cap, stream_ptr())
     out = [None] * nb
     if device_in:
         for j in range(nb):
@@ -555,6 +574,28 @@ def block_solve(F: BlockFactor, g: list) -> list:
     for j in range(nb):
         blk = xh[sched.row_off[j]:sched.row_off[j + 1]]
         out[int(perm[j])] = blk[:, 0].copy() if one_d else blk.copy()
+    return out
+
+
+def to_device_blocks(K: BlockSparseSym) -> BlockSparseSym:
+    """Copy of K whose blocks are views into ONE device pool (one H2D copy),
+    the layout block_ldlt consumes with a single relabel/copy launch."""
+    t = require_cuda()
+    keys = list(K.blocks)
+    offs, tot = [], 0
+    for (i, j) in keys:
+        offs.append(tot)
+        tot += int(K.sizes[i]) * int(K.sizes[j])
+    host = t.empty(max(tot, 1), dtype=t.complex128, pin_memory=True)
+    hv = host.numpy()
+    for (i, j), o in zip(keys, offs):
+        hv[o:o + int(K.sizes[i]) * int(K.sizes[j])] = np.asarray(K.blocks[(i, j)], dtype=np.complex128).reshape(-1)
+    pool = host.to("cuda", non_blocking=False)
+    out = BlockSparseSym(K.sizes)
+    for (i, j), o in zip(keys, offs):
+        ni, nj = int(K.sizes[i]), int(K.sizes[j])
+        out.blocks[(i, j)] = DeviceArray(pool[o:o + ni * nj].reshape(ni, nj))
+    out._d3m_pool = pool
     return out
 
 
