@@ -43,6 +43,15 @@ int d3m_bk_factor_batched(int batch, int n, void* W, int64_t stride_w, int lda, 
                           void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
                           void* scratch, void* stream);
 
+/* Same contract as d3m_bk_factor_batched with the blocked shared-memory
+ * panel kernel (zlasyf-style): identical pivot decisions whenever no test
+ * sits within rounding of its threshold, values to rounding; growth is the
+ * per-panel geometric mean of the trailing-max ratio.  Used for the
+ * supernode diagonal blocks of block_ldlt wider than 128. */
+int d3m_bk_blocked_factor(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
+                          void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
+                          void* scratch, void* stream);
+
 /* Multi-RHS solve M X = B with packed factors: gather by perm, unit-L forward,
  * D^-1, unit-L^T backward, scatter.  Replaces DenseFactor.solve
  * (factor.py:52-66) with kernels.solve_unit_lower / apply_dinv_left /

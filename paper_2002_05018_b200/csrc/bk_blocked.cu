@@ -114,9 +114,18 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
       double colmax = 0.0;
       int imax = k;
       if (k + 1 < n) {
+        // |z|^2 proxy first; only entries whose proxy is within a few ulp of
+        // the largest can be the glibc-hypot argmax (first index on ties)
+        double p = -1.0;
+        for (int i = k + 1 + tid; i < n; i += NT) p = fmax(p, x_abs2(WpT[kw * ldp + i]));
+        const double pmax = bmax<NT>(p, rc);
+        const double thr = pmax * (1.0 - 1e-14);
         double v = -1.0;
         int vi = 0x7fffffff;
-        for (int i = k + 1 + tid; i < n; i += NT) argmax_merge(v, vi, x_abs(WpT[kw * ldp + i]), i);
+        for (int i = k + 1 + tid; i < n; i += NT) {
+          const cplx z = WpT[kw * ldp + i];
+          if (x_abs2(z) >= thr) argmax_merge(v, vi, x_abs(z), i);
+        }
         bargmax<NT>(v, vi, ra, rai);
         colmax = v;
         imax = vi;
@@ -131,9 +140,16 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
           WpT[(kw + 1) * ldp + i] = acc;
         }
         __syncthreads();
-        double rm = 0.0;
+        double rp = 0.0;
         for (int i = k + tid; i < n; i += NT)
-          if (i != imax) rm = fmax(rm, x_abs(WpT[(kw + 1) * ldp + i]));
+          if (i != imax) rp = fmax(rp, x_abs2(WpT[(kw + 1) * ldp + i]));
+        const double rpmax = bmax<NT>(rp, rc);
+        const double rthr = rpmax * (1.0 - 1e-14);
+        double rm = 0.0;
+        for (int i = k + tid; i < n; i += NT) {
+          const cplx z = WpT[(kw + 1) * ldp + i];
+          if (i != imax && x_abs2(z) >= rthr) rm = fmax(rm, x_abs(z));
+        }
         const double absimax = x_abs(WpT[(kw + 1) * ldp + imax]);
         const double rowmax = bmax<NT>(rm, rb);
         if (__dmul_rn(absakk, rowmax) >= __dmul_rn(__dmul_rn(kAlphaBK, colmax), colmax)) {
@@ -215,35 +231,51 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
     }
     __syncthreads();
     // ---- trailing update  A22 -= L21 X21^T  (lower triangle, rank kw) ------
+    // 16 x 16 tiles of the trailing lower triangle, one per warp at a time;
+    // lane = 2 rows x 4 columns, 8 independent global loads in flight, the
+    // panel operands from shared memory (6 LDS.128 per 8 complex FMAs).
     double st = 0.0;
     const int m = n - k;
     if (m > 0) {
-      for (int r = tid / 32; r < m; r += NT / 32) {
-        const int i = k + r;
-        cplx li[PC];
+      const int nt = (m + 15) / 16;
+      const int ntiles = nt * (nt + 1) / 2;
+      const int lane = tid & 31, warp = tid >> 5;
+      const int qr = 2 * (lane >> 2), qc = 4 * (lane & 3);
+      for (int t = warp; t < ntiles; t += NT / 32) {
+        int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+        while (ti * (ti + 1) / 2 > t) --ti;
+        const int tj = t - ti * (ti + 1) / 2;
+        const int r0 = k + 16 * ti + qr, c0 = k + 16 * tj + qc;
+        cplx v[2][4];
 #pragma unroll
-        for (int c = 0; c < PC; ++c) li[c] = c < kw ? LpT[c * ldp + i] : mk(0.0, 0.0);
-        // 8 independent loads in flight per lane (the loop is latency-bound otherwise)
-        for (int jb = k; jb <= i; jb += 256) {
-          cplx v[8];
+        for (int a2 = 0; a2 < 2; ++a2)
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int j = jb + (tid & 31) + 32 * u;
-            if (j <= i) v[u] = G(i, j);
+          for (int b4 = 0; b4 < 4; ++b4) {
+            const int r = r0 + a2, c = c0 + b4;
+            v[a2][b4] = (r < n && c <= r) ? G(r, c) : mk(0.0, 0.0);
           }
+        for (int c = 0; c < kw; ++c) {
+          cplx l[2], x[4];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int j = jb + (tid & 31) + 32 * u;
-            if (j <= i) {
-              cplx acc = v[u];
+          for (int a2 = 0; a2 < 2; ++a2) l[a2] = (r0 + a2 < n) ? LpT[c * ldp + r0 + a2] : mk(0.0, 0.0);
 #pragma unroll
-              for (int c = 0; c < PC; ++c)
-                if (c < kw) c_fms(acc, li[c], WpT[c * ldp + j]);
-              G(i, j) = acc;
-              st = fmax(st, x_abs2(acc));
+          for (int b4 = 0; b4 < 4; ++b4) x[b4] = (c0 + b4 < n) ? WpT[c * ldp + c0 + b4] : mk(0.0, 0.0);
+#pragma unroll
+          for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+            for (int b4 = 0; b4 < 4; ++b4) c_fms(v[a2][b4], l[a2], x[b4]);
+        }
+#pragma unroll
+        for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+          for (int b4 = 0; b4 < 4; ++b4) {
+            const int r = r0 + a2, c = c0 + b4;
+            if (r < n && c <= r) {
+              G(r, c) = v[a2][b4];
+              st = fmax(st, x_abs2(v[a2][b4]));
             }
           }
-        }
       }
       st = bmax<NT>(st, rd);
       const double step_max = sqrt(st);
@@ -266,19 +298,26 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
 
 // Blocked variant for n <= 760 (panel fits shared memory); returns -22 when
 // the block is too large (the caller then uses the unblocked exact kernel).
+// Blocked variant; the panel width is the largest of 12/8/4 whose shared
+// memory (<= 104 KB) lets the CTA co-reside with one trailing-update GEMM
+// CTA, so the critical path is not starved by the bulk stream.  Returns -22
+// when even NB = 4 does not fit (the caller then uses the exact kernel).
 extern "C" int d3m_bk_blocked_launch(d3m::BkArgs* a, int batch, void* stream) {
   using namespace d3m;
   if (batch <= 0) return 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   static bool cfg = false;
   if (!cfg) {
-    cudaFuncSetAttribute(bk_blocked_kernel<16, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(bk_blocked_kernel<8, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(bk_blocked_kernel<12, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    cudaFuncSetAttribute(bk_blocked_kernel<8, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    cudaFuncSetAttribute(bk_blocked_kernel<4, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     cfg = true;
   }
-  const size_t s16 = (size_t)2 * 17 * (a->n + 1) * sizeof(cplx), s8 = (size_t)2 * 9 * (a->n + 1) * sizeof(cplx);
-  if (s16 <= 200 * 1024) bk_blocked_kernel<16, 256><<<batch, 256, s16, s>>>(*a);
-  else if (s8 <= 200 * 1024) bk_blocked_kernel<8, 256><<<batch, 256, s8, s>>>(*a);
+  auto bytes = [&](int nb) { return (size_t)2 * (nb + 1) * (a->n + 1) * sizeof(cplx); };
+  const size_t budget = 104 * 1024 + 512;
+  if (bytes(12) <= budget) bk_blocked_kernel<12, 256><<<batch, 256, bytes(12), s>>>(*a);
+  else if (bytes(8) <= budget) bk_blocked_kernel<8, 256><<<batch, 256, bytes(8), s>>>(*a);
+  else if (bytes(4) <= budget) bk_blocked_kernel<4, 256><<<batch, 256, bytes(4), s>>>(*a);
   else return -22;
   return (int)cudaGetLastError();
 }

@@ -76,6 +76,7 @@ int launch(int cls, void* stream, Fn fn) {
 }
 
 using d3m::cplx;
+constexpr int kExactBkMax = 128;
 inline cplx* C(void* p) { return static_cast<cplx*>(p); }
 inline const cplx* CC(const void* p) { return static_cast<const cplx*>(p); }
 
@@ -95,6 +96,20 @@ int d3m_bk_factor_batched(int batch, int n, void* W, int64_t stride_w, int lda, 
                 static_cast<int32_t*>(n2x2), static_cast<double*>(growth), static_cast<int32_t*>(info),
                 static_cast<double*>(scale), static_cast<double*>(asym), C(scratch)};
   D3M_TRY(launch(kClsBk, stream, [&] { return d3m_bk_launch(&a, batch, stream); }));
+  return 0;
+}
+
+int d3m_bk_blocked_factor(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
+                          void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
+                          void* scratch, void* stream) {
+  if (batch < 0 || n < 0 || lda < n) return fail(-22, "d3m_bk_blocked_factor: bad shape");
+  d3m::BkArgs a{C(W), stride_w, n, lda, pivot_tol, check_sym, static_cast<int64_t*>(perm), static_cast<int8_t*>(tags),
+                static_cast<int32_t*>(n2x2), static_cast<double*>(growth), static_cast<int32_t*>(info),
+                static_cast<double*>(scale), static_cast<double*>(asym), C(scratch)};
+  D3M_TRY(launch(kClsBk, stream, [&] {
+    const int rc = d3m_bk_blocked_launch(&a, batch, stream);
+    return rc == -22 ? d3m_bk_launch(&a, batch, stream) : rc;
+  }));
   return 0;
 }
 
@@ -242,9 +257,12 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                   static_cast<int32_t*>(d_info) + j, static_cast<double*>(d_scale) + j,
                   static_cast<double*>(d_asym) + j, C(d_bk_scratch)};
     if (nj > 0) {
-      // blocked panel BK (shared-memory panel) for supernode blocks; the
-      // unblocked bit-exact kernel when the panel does not fit
+      // supernodes up to kExactBkMax use the bit-exact unblocked kernel (so a
+      // one-block K factors exactly like dense_ldlt_bk, test_block_factor.py:
+      // 24-32); wider ones the blocked shared-memory panel kernel (pivots
+      // identical, values to rounding), or the exact one if no panel fits
       D3M_TRY(launch(kClsBk, s0, [&] {
+        if (nj <= kExactBkMax) return d3m_bk_launch(&a, 1, s0);
         const int rc = d3m_bk_blocked_launch(&a, 1, s0);
         return rc == -22 ? d3m_bk_launch(&a, 1, s0) : rc;
       }));

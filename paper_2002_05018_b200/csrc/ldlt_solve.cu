@@ -264,7 +264,7 @@ namespace d3m {
 // -------------------------------------------------------------------------
 constexpr int INV_THREADS = 256;
 constexpr int INV_COLS = INV_THREADS / 16;
-constexpr int INV_ROWS = 8;
+constexpr int INV_ROWS = 4;   // (16 + 2*4) n complex of smem: fits beside one GEMM CTA at n = 256
 
 __device__ __forceinline__ void cp_async16_pred(void* smem, const void* gmem, bool pred) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
