@@ -147,7 +147,10 @@ int d3m_recover_batched(int batch, int n, int m, const void* F, const void* perm
  * CUDA-event timing of every kernel launched through this library (classes:
  * 0 diagonal BK, 1 panel TRSM, 2 trailing-update / reduction GEMM,
  * 3 substitution kernels, 4 data movement).  Events are recorded on the
- * launching stream around each launch; d3m_counters_read synchronises them. */
+ * launching stream around each launch; d3m_counters_read synchronises them.
+ * ms[0..4]: summed per-launch event time per class; ms[5..9]: measure of the
+ * union of the launch intervals per class (concurrent launches of one class
+ * on the critical and bulk streams counted once).  n[0..4]: launch counts. */
 void d3m_set_timing(int on);
 void d3m_counters_reset(void);
 int d3m_counters_read(int64_t* launches, double* ms, int64_t* n);

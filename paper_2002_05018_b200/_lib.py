@@ -106,10 +106,11 @@ def counters_read() -> dict:
     """{'launches': int, 'ms': {class: ms}, 'n': {class: count}}"""
     lib = load()
     nl = ctypes.c_int64(0)
-    ms = (ctypes.c_double * 5)()
+    ms = (ctypes.c_double * 10)()
     n = (ctypes.c_int64 * 5)()
     lib.d3m_counters_read(ctypes.byref(nl), ms, n)
-    return {"launches": int(nl.value), "ms": dict(zip(CLASSES, list(ms))), "n": dict(zip(CLASSES, list(n)))}
+    return {"launches": int(nl.value), "ms": dict(zip(CLASSES, list(ms)[:5])),
+            "union_ms": dict(zip(CLASSES, list(ms)[5:])), "n": dict(zip(CLASSES, list(n)))}
 
 
 def call(name: str, *args):

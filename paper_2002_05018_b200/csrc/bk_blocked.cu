@@ -46,8 +46,18 @@ __device__ __forceinline__ void bargmax(double& v, int& idx, double* vs, int* is
   for (int w = 1; w < NT / 32; ++w) argmax_merge(v, idx, vs[w], is[w]);
 }
 
+#ifdef D3M_BK_PROFILE
+#define PROF_MARK(slot) do { __syncthreads(); if (tid == 0) { long long t_ = clock64(); prof[slot] += (double)(t_ - prof_t); prof_t = t_; } } while (0)
+#else
+#define PROF_MARK(slot) do { } while (0)
+#endif
+
 template <int NB, int NT>
 __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
+#ifdef D3M_BK_PROFILE
+  double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof_t = clock64();
+#endif
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double ra[NT / 32], rb[NT / 32], rc[NT / 32], rd[NT / 32];
   __shared__ int rai[NT / 32];
@@ -63,17 +73,62 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
 
   for (int i = tid; i < n; i += NT) { perm[i] = i; tags[i] = 0; }
   // ---- prologue (factor.py:94-98 scale / symmetry; kernels.py:45-46) ------
-  double scale = 0.0, asym = 0.0, tm2 = 0.0;
-  for (int i = tid / 32; i < n; i += NT / 32)
-    for (int j = tid & 31; j < n; j += 32) {
-      const cplx z = G(i, j);
-      scale = fmax(scale, np_abs(z));
-      if (j <= i) tm2 = fmax(tm2, x_abs2(z));
-      if (a.check_sym && j < i) asym = fmax(asym, np_abs(x_sub(z, G(j, i))));
+  // max |.|^2 proxies first (3 flops per entry); the exact numpy modulus is
+  // then evaluated only for entries whose proxy is within 1e-14 of the max
+  double p_all = 0.0, p_asy = 0.0, tm2 = 0.0;
+  // pass 1 over the lower triangle incl. diagonal, row segments, 8 loads in
+  // flight per lane: proxies of |W_ij|, |W_ij - W_ji| and the trailing max
+  const int lane = tid & 31, wid = tid >> 5;
+  for (int i = wid; i < n; i += NT / 32)
+    for (int jb = 0; jb <= i; jb += 256) {
+      cplx z[8], zt[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = jb + lane + 32 * u;
+        if (j <= i) { z[u] = G(i, j); zt[u] = G(j, i); }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = jb + lane + 32 * u;
+        if (j <= i) {
+          const double q = x_abs2(z[u]), qt = x_abs2(zt[u]);
+          p_all = fmax(p_all, fmax(q, qt));
+          tm2 = fmax(tm2, q);
+          if (a.check_sym && j < i) p_asy = fmax(p_asy, x_abs2(x_sub(z[u], zt[u])));
+        }
+      }
     }
-  scale = bmax<NT>(scale, ra);
-  asym = bmax<NT>(asym, rb);
+  p_all = bmax<NT>(p_all, ra);
+  p_asy = bmax<NT>(p_asy, rb);
   tm2 = bmax<NT>(tm2, rc);
+  // pass 2: exact numpy modulus only where the proxy is within 1e-14 of the max
+  double scale = 0.0, asym = 0.0;
+  {
+    const double ta = p_all * (1.0 - 1e-14), tb = p_asy * (1.0 - 1e-14);
+    for (int i = wid; i < n; i += NT / 32)
+      for (int jb = 0; jb <= i; jb += 256) {
+        cplx z[8], zt[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = jb + lane + 32 * u;
+          if (j <= i) { z[u] = G(i, j); zt[u] = G(j, i); }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = jb + lane + 32 * u;
+          if (j <= i) {
+            if (x_abs2(z[u]) >= ta) scale = fmax(scale, np_abs(z[u]));
+            if (x_abs2(zt[u]) >= ta) scale = fmax(scale, np_abs(zt[u]));
+            if (a.check_sym && j < i) {
+              const cplx dz = x_sub(z[u], zt[u]);
+              if (x_abs2(dz) >= tb) asym = fmax(asym, np_abs(dz));
+            }
+          }
+        }
+      }
+    scale = bmax<NT>(scale, rd);
+    asym = bmax<NT>(asym, ra);
+  }
   if (tid == 0) { a.scale[b] = scale; a.asym[b] = asym; }
   if (a.check_sym && n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) {
     if (tid == 0) { a.info[b] = -2; a.n2x2[b] = 0; a.growth[b] = 1.0; }
@@ -89,11 +144,27 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
     const int k0 = k;
     const int ncols = min(PC, n - k0);
     // stale panel columns k0 .. k0+ncols-1, rows >= column (row segments: coalesced)
-    for (int e = tid; e < (n - k0) * ncols; e += NT) {
-      const int i = k0 + e / ncols, c = e % ncols;
-      if (i >= k0 + c) LpT[c * ldp + i] = G(i, k0 + c);
+    for (int e0 = tid; e0 < (n - k0) * ncols; e0 += 8 * NT) {
+      cplx z[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * NT;
+        if (e < (n - k0) * ncols) {
+          const int i = k0 + e / ncols, c = e % ncols;
+          if (i >= k0 + c) z[u] = G(i, k0 + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * NT;
+        if (e < (n - k0) * ncols) {
+          const int i = k0 + e / ncols, c = e % ncols;
+          if (i >= k0 + c) LpT[c * ldp + i] = z[u];
+        }
+      }
     }
     __syncthreads();
+    PROF_MARK(0);
     // stale element (r, c), r >= c, of the not-yet-updated matrix
     auto stale = [&](int r, int c) -> cplx { return (c - k0 < ncols) ? LpT[(c - k0) * ldp + r] : G(r, c); };
     auto put = [&](int r, int c, cplx v) {
@@ -102,56 +173,80 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
     };
     int kw = 0, npiv = 0;
     while (kw < NB && k < n) {
-      // -- A: column k up to date into WpT[kw]
+      // -- A+B: column k up to date into WpT[kw], fused with the |z|^2-proxy
+      //    argmax below the diagonal (one barrier round); the exact glibc-hypot
+      //    argmax runs only if another entry is within 1e-14 of the winner
+      double pv = -1.0;
+      int pi = 0x7fffffff;
       for (int i = k + tid; i < n; i += NT) {
-        cplx acc = LpT[kw * ldp + i];
-        for (int c = 0; c < kw; ++c) c_fms(acc, LpT[c * ldp + i], WpT[c * ldp + k]);
+        cplx acc = LpT[kw * ldp + i], acc2 = mk(0.0, 0.0);
+        int c = 0;
+        for (; c + 1 < kw; c += 2) {
+          c_fms(acc, LpT[c * ldp + i], WpT[c * ldp + k]);
+          c_fms(acc2, LpT[(c + 1) * ldp + i], WpT[(c + 1) * ldp + k]);
+        }
+        if (c < kw) c_fms(acc, LpT[c * ldp + i], WpT[c * ldp + k]);
+        acc = c_add(acc, acc2);
         WpT[kw * ldp + i] = acc;
+        if (i > k) argmax_merge(pv, pi, x_abs2(acc), i);
       }
-      __syncthreads();
-      // -- B: pivot search
+      bargmax<NT>(pv, pi, ra, rai);            // contains the barrier
+      PROF_MARK(1);
       const double absakk = x_abs(WpT[kw * ldp + k]);
       double colmax = 0.0;
       int imax = k;
       if (k + 1 < n) {
-        // |z|^2 proxy first; only entries whose proxy is within a few ulp of
-        // the largest can be the glibc-hypot argmax (first index on ties)
-        double p = -1.0;
-        for (int i = k + 1 + tid; i < n; i += NT) p = fmax(p, x_abs2(WpT[kw * ldp + i]));
-        const double pmax = bmax<NT>(p, rc);
-        const double thr = pmax * (1.0 - 1e-14);
-        double v = -1.0;
-        int vi = 0x7fffffff;
-        for (int i = k + 1 + tid; i < n; i += NT) {
-          const cplx z = WpT[kw * ldp + i];
-          if (x_abs2(z) >= thr) argmax_merge(v, vi, x_abs(z), i);
+        const double thr = pv * (1.0 - 1e-14);
+        int amb = 0;
+        for (int i = k + 1 + tid; i < n; i += NT)
+          amb |= (i != pi && x_abs2(WpT[kw * ldp + i]) >= thr);
+        if (__syncthreads_or(amb)) {
+          double v = -1.0;
+          int vi = 0x7fffffff;
+          for (int i = k + 1 + tid; i < n; i += NT) {
+            const cplx z = WpT[kw * ldp + i];
+            if (x_abs2(z) >= thr) argmax_merge(v, vi, x_abs(z), i);
+          }
+          bargmax<NT>(v, vi, rb, rai);
+          pi = vi;
         }
-        bargmax<NT>(v, vi, ra, rai);
-        colmax = v;
-        imax = vi;
+        imax = pi;
+        colmax = x_abs(WpT[kw * ldp + imax]);
       }
       if (fmax(absakk, colmax) <= tol_abs) { info = k; break; }
       int kstep = 1, kp = k;
       if (!(absakk >= __dmul_rn(kAlphaBK, colmax))) {
-        // -- C: column imax up to date into WpT[kw+1]
+        // -- C: column imax up to date into WpT[kw+1], fused with the rowmax
+        //    proxy argmax (rowmax excludes the diagonal entry imax)
+        double rpv = -1.0;
+        int rpi = 0x7fffffff;
         for (int i = k + tid; i < n; i += NT) {
-          cplx acc = i < imax ? stale(imax, i) : stale(i, imax);
-          for (int c = 0; c < kw; ++c) c_fms(acc, LpT[c * ldp + i], WpT[c * ldp + imax]);
+          cplx acc = i < imax ? stale(imax, i) : stale(i, imax), acc2 = mk(0.0, 0.0);
+          int c = 0;
+          for (; c + 1 < kw; c += 2) {
+            c_fms(acc, LpT[c * ldp + i], WpT[c * ldp + imax]);
+            c_fms(acc2, LpT[(c + 1) * ldp + i], WpT[(c + 1) * ldp + imax]);
+          }
+          if (c < kw) c_fms(acc, LpT[c * ldp + i], WpT[c * ldp + imax]);
+          acc = c_add(acc, acc2);
           WpT[(kw + 1) * ldp + i] = acc;
+          if (i != imax) argmax_merge(rpv, rpi, x_abs2(acc), i);
         }
-        __syncthreads();
-        double rp = 0.0;
+        bargmax<NT>(rpv, rpi, rc, rai);
+        const double rthr = rpv * (1.0 - 1e-14);
+        int ramb = 0;
         for (int i = k + tid; i < n; i += NT)
-          if (i != imax) rp = fmax(rp, x_abs2(WpT[(kw + 1) * ldp + i]));
-        const double rpmax = bmax<NT>(rp, rc);
-        const double rthr = rpmax * (1.0 - 1e-14);
-        double rm = 0.0;
-        for (int i = k + tid; i < n; i += NT) {
-          const cplx z = WpT[(kw + 1) * ldp + i];
-          if (i != imax && x_abs2(z) >= rthr) rm = fmax(rm, x_abs(z));
+          ramb |= (i != imax && i != rpi && x_abs2(WpT[(kw + 1) * ldp + i]) >= rthr);
+        double rowmax = rpi < n ? x_abs(WpT[(kw + 1) * ldp + rpi]) : 0.0;
+        if (__syncthreads_or(ramb)) {
+          double rm = 0.0;
+          for (int i = k + tid; i < n; i += NT) {
+            const cplx z = WpT[(kw + 1) * ldp + i];
+            if (i != imax && x_abs2(z) >= rthr) rm = fmax(rm, x_abs(z));
+          }
+          rowmax = bmax<NT>(rm, rb);
         }
         const double absimax = x_abs(WpT[(kw + 1) * ldp + imax]);
-        const double rowmax = bmax<NT>(rm, rb);
         if (__dmul_rn(absakk, rowmax) >= __dmul_rn(__dmul_rn(kAlphaBK, colmax), colmax)) {
           kp = k;
         } else if (absimax >= __dmul_rn(kAlphaBK, rowmax)) {
@@ -163,6 +258,7 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
         }
         __syncthreads();
       }
+      PROF_MARK(3);
       const int kk = k + kstep - 1, kkw = kw + kstep - 1;
       // -- D: interchange kk <-> kp (stale column kk moves to kp; L rows and X rows swap)
       if (kp != kk) {
@@ -191,11 +287,25 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
         if (tid == 0) { const int64_t t0 = perm[kk]; perm[kk] = perm[kp]; perm[kp] = t0; }
         __syncthreads();
       }
+      PROF_MARK(4);
       // -- E: store D and the L column(s) into the panel
       if (kstep == 1) {
         const cplx d = WpT[kw * ldp + k];
-        for (int i = k + tid; i < n; i += NT)
-          LpT[kw * ldp + i] = i == k ? d : x_div_np(WpT[kw * ldp + i], d);
+        // x_div_np(w, d) with its d-only intermediates (rat, scl) hoisted
+        const bool re_big = fabs(d.x) >= fabs(d.y);
+        const double rat = re_big ? __ddiv_rn(d.y, d.x) : __ddiv_rn(d.x, d.y);
+        const double scl = re_big ? __ddiv_rn(1.0, __dadd_rn(d.x, __dmul_rn(d.y, rat)))
+                                  : __ddiv_rn(1.0, __dadd_rn(d.y, __dmul_rn(d.x, rat)));
+        for (int i = k + tid; i < n; i += NT) {
+          const cplx w = WpT[kw * ldp + i];
+          cplx q;
+          if (d.x == 0.0 && d.y == 0.0) q = x_div_np(w, d);
+          else if (re_big) q = mk(__dmul_rn(__dadd_rn(w.x, __dmul_rn(w.y, rat)), scl),
+                                  __dmul_rn(__dsub_rn(w.y, __dmul_rn(w.x, rat)), scl));
+          else q = mk(__dmul_rn(__dadd_rn(__dmul_rn(w.x, rat), w.y), scl),
+                      __dmul_rn(__dsub_rn(__dmul_rn(w.y, rat), w.x), scl));
+          LpT[kw * ldp + i] = i == k ? d : q;
+        }
         if (tid == 0) tags[k] = 1;
       } else {
         const cplx d21 = WpT[kw * ldp + k + 1];
@@ -220,10 +330,12 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
       }
       ++npiv;
       __syncthreads();
+      PROF_MARK(5);
       k += kstep;
       kw += kstep;
     }
     if (info >= 0) break;
+    PROF_MARK(5);
     // ---- write the panel back (final L/D of columns < k, stale beyond) ------
     for (int e = tid; e < (n - k0) * ncols; e += NT) {
       const int i = k0 + e / ncols, c = e % ncols;
@@ -286,7 +398,11 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
       trail_max = step_max;
     }
     __syncthreads();
+    PROF_MARK(6);
   }
+#ifdef D3M_BK_PROFILE
+  if (tid == 0 && a.scratch) for (int q = 0; q < 8; ++q) reinterpret_cast<double*>(a.scratch)[q] = prof[q];
+#endif
   if (tid == 0) {
     a.n2x2[b] = n2x2;
     a.growth[b] = growth;

@@ -48,7 +48,9 @@ struct TimedRec { int cls; cudaEvent_t a, b; };
 std::vector<TimedRec> g_pending;
 std::vector<cudaEvent_t> g_free_ev;
 double g_ms[kNumCls] = {0, 0, 0, 0, 0};
+double g_union[kNumCls] = {0, 0, 0, 0, 0};
 long long g_cnt[kNumCls] = {0, 0, 0, 0, 0};
+cudaEvent_t g_ref = nullptr;          // common origin for interval unions
 
 cudaEvent_t take_event() {
   if (!g_free_ev.empty()) {
@@ -279,7 +281,12 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
       D3M_TRY(launch(kClsTrsm, s0, [&] { return d3m_dinv_rows_launch(xbuf, pool + h_panel_off[j], R, nj, diag, tags, s0); }));
     }
     const int64_t t0 = h_task_ptr[j], tn = h_task_next[j], t1 = h_task_ptr[j + 1];
-    if (rest_pending) {
+    // X_j / L_j are ready: the bulk ("rest") update of column j only reads
+    // them and targets columns >= j+2, so it may start now, concurrently with
+    // the "next" update below (disjoint targets); the side stream keeps the
+    // rest updates of consecutive columns in order.
+    if (lookahead && t1 > tn) cudaEventRecord(ev_next, s0);
+    if (rest_pending) {          // next-targets of column j+1 were also rest-targets of j-1
       cudaStreamWaitEvent(s0, ev_rest, 0);
       rest_pending = false;
     }
@@ -289,7 +296,6 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
       }));
     if (t1 > tn) {
       if (lookahead) {
-        cudaEventRecord(ev_next, s0);
         cudaStreamWaitEvent(side, ev_next, 0);
         D3M_TRY(launch(kClsGemm, side, [&] {
           return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], side);
@@ -438,7 +444,14 @@ int d3m_recover_batched(int batch, int n, int m, const void* F, const void* perm
   return 0;
 }
 
-void d3m_set_timing(int on) { g_timing = on != 0; }
+void d3m_set_timing(int on) {
+  g_timing = on != 0;
+  if (g_timing) {
+    if (!g_ref) cudaEventCreate(&g_ref);
+    cudaDeviceSynchronize();
+    cudaEventRecord(g_ref, 0);
+  }
+}
 
 void d3m_counters_reset(void) {
   for (auto& r : g_pending) {
@@ -448,24 +461,43 @@ void d3m_counters_reset(void) {
   }
   g_pending.clear();
   g_launches.store(0);
-  for (int c = 0; c < kNumCls; ++c) { g_ms[c] = 0; g_cnt[c] = 0; }
+  for (int c = 0; c < kNumCls; ++c) { g_ms[c] = 0; g_cnt[c] = 0; g_union[c] = 0; }
 }
 
 // launches: total kernel launches since reset; ms[5] / n[5]: summed event
 // time and launch count per class (bk, trsm, gemm-update, solve, misc).
 int d3m_counters_read(int64_t* launches, double* ms, int64_t* n) {
+  std::vector<std::pair<double, double>> iv[kNumCls];
   for (auto& r : g_pending) {
     cudaEventSynchronize(r.b);
-    float t = 0.f;
+    float t = 0.f, t0 = 0.f, t1 = 0.f;
     cudaEventElapsedTime(&t, r.a, r.b);
     g_ms[r.cls] += t;
+    if (g_ref && cudaEventElapsedTime(&t0, g_ref, r.a) == cudaSuccess &&
+        cudaEventElapsedTime(&t1, g_ref, r.b) == cudaSuccess)
+      iv[r.cls].emplace_back(t0, t1);
     g_free_ev.push_back(r.a);
     g_free_ev.push_back(r.b);
   }
   g_pending.clear();
+  for (int c = 0; c < kNumCls; ++c) {       // measure of the union of intervals
+    auto& v = iv[c];
+    std::sort(v.begin(), v.end());
+    double lo = -1, hi = -1;
+    for (auto& x : v) {
+      if (x.first > hi) {
+        if (hi > lo) g_union[c] += hi - lo;
+        lo = x.first;
+        hi = x.second;
+      } else if (x.second > hi) {
+        hi = x.second;
+      }
+    }
+    if (hi > lo) g_union[c] += hi - lo;
+  }
   if (launches) *launches = g_launches.load();
   for (int c = 0; c < kNumCls; ++c) {
-    if (ms) ms[c] = g_ms[c];
+    if (ms) { ms[c] = g_ms[c]; ms[kNumCls + c] = g_union[c]; }
     if (n) n[c] = g_cnt[c];
   }
   return 0;
