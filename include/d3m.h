@@ -123,17 +123,19 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                         void* stream);
 
 /* Forward / D^-1 / backward block substitution for nrhs right-hand sides in
- * one pass, every stage a DMMA GEMM against the stored factor (z = Binv b,
- * b_i -= L_ij z, w = u - sum L_ij^T x_i, x = Binv^T w); each RHS column is
- * computed independently (k-RHS == k x 1-RHS).  Replaces factor.block_solve /
+ * one pass: z = Binv b, u = D^-1 z, b_i -= L_ij z (forward), w = u - sum_i
+ * L_ij^T x_i, x = Binv^T w (backward), with HBM-streaming tall-skinny kernels;
+ * each RHS column is computed with a fixed summation order independent of
+ * nrhs (k-RHS == k x 1-RHS bitwise).  Replaces factor.block_solve /
  * _solve_one (factor.py:243-310).  b: plan-ordered RHS (N x nrhs, consumed);
- * x: solution in plan order; tmp: max n_j x nrhs; part: max_j p_j n_j x nrhs;
- * d_tasks: (2 nb + 2 npattern) GEMM task records. */
+ * x: solution in plan order; tmp: max n_j x nrhs; part: partial-sum buffer of
+ * part_elems complex (>= max_j ceil(max(R_j, n_j)/16) n_j nrhs);
+ * d_gidx/h_gptr: global plan-order row of every panel row. */
 int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_off, const int64_t* h_diag_off,
-                         const int64_t* h_panel_off, const int64_t* h_piv_off, const int64_t* h_binv_off,
-                         const int64_t* h_pat_ptr, const int64_t* h_pat_idx, const void* d_pool,
+                         const int64_t* h_panel_off, const int64_t* h_panel_rows, const int64_t* h_piv_off,
+                         const int64_t* h_binv_off, const int64_t* h_gptr, const void* d_gidx, const void* d_pool,
                          const void* d_binv, const void* d_tags, void* d_b, void* d_u, void* d_x, void* d_tmp,
-                         void* d_part, int nrhs, void* d_tasks, int64_t task_cap, void* stream);
+                         void* d_part, int64_t part_elems, int nrhs, void* stream);
 
 /* Primal recovery of equal-sized subdomains: rhs = f - D lam (rhs holds f on
  * entry), E = A^-1 rhs with the cached packed factors, then the ordered

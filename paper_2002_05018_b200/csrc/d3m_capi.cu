@@ -320,95 +320,74 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
 }
 
 // ---------------------------------------------------------------------------
-// block_solve executor (factor.py:243-310), all RHS in one pass, every
-// stage a DMMA GEMM against the stored factor:
+// block_solve executor (factor.py:243-310), all RHS in one pass, HBM-bound
+// tall-skinny kernels against the stored factor (solve_gemv.cu):
 //   forward  z_j = Binv_j b_j,  u_j = D_j^-1 z_j,  b_i -= L_ij z_j
-//   backward w_j = u_j - sum_i L_ij^T x_i  (split over i, ordered sum),
+//   backward w_j = u_j - sum_i L_ij^T x_i  (row chunks, ordered sum),
 //            x_j = Binv_j^T w_j
 //   b, u, x : N x nrhs plan order (b consumed);  tmp: max n_j x nrhs;
-//   part    : max_j (|pattern(j)| n_j) x nrhs
+//   part    : partial sums, part_elems complex
 // ---------------------------------------------------------------------------
 int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_off, const int64_t* h_diag_off,
-                         const int64_t* h_panel_off, const int64_t* h_piv_off, const int64_t* h_binv_off,
-                         const int64_t* h_pat_ptr, const int64_t* h_pat_idx, const void* d_pool,
+                         const int64_t* h_panel_off, const int64_t* h_panel_rows, const int64_t* h_piv_off,
+                         const int64_t* h_binv_off, const int64_t* h_gptr, const void* d_gidx, const void* d_pool,
                          const void* d_binv, const void* d_tags, void* d_b, void* d_u, void* d_x, void* d_tmp,
-                         void* d_part, int nrhs, void* d_tasks, int64_t task_cap, void* stream) {
+                         void* d_part, int64_t part_elems, int nrhs, void* stream) {
   if (nb <= 0 || nrhs <= 0) return 0;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int64_t npat = h_pat_ptr[nb];
-  // task layout: [0, nb) z_j;  [nb, nb+npat) forward updates;
-  //              [nb+npat, nb+2npat) backward partials;  [nb+2npat, 2nb+2npat) x_j
-  const int64_t ntask = 2 * nb + 2 * npat;
-  if (ntask > task_cap) return fail(-22, "d3m_block_solve_exec: task buffer too small");
-  std::vector<d3m::GemmTask> t(ntask);
-  std::memset(t.data(), 0, sizeof(d3m::GemmTask) * ntask);
-  std::vector<int> tz(nb), tf(nb), tp(nb), tx(nb);
-  auto mk = [&](d3m::GemmTask& k, int64_t a, int64_t b, int64_t c, int m, int n, int kk, int lda, int ldb, int ldc,
-                int flags) {
-    k.a_off = a; k.b_off = b; k.c_off = c; k.m = m; k.n = n; k.k = kk;
-    k.lda = lda; k.ldb = ldb; k.ldc = ldc; k.flags = flags;
-  };
+  const int RC = d3m_solve_rows_per_chunk();
   for (int j = 0; j < nb; ++j) {
-    const int nj = (int)h_sizes[j];
-    mk(t[j], h_binv_off[j], h_row_off[j] * nrhs, 0, nj, nrhs, nj, nj, nrhs, nrhs, d3m::kGemmStore);
-    tz[j] = d3m_gemm_prepare_tasks(&t[j], 1);
-    int64_t prow = 0;
-    for (int64_t p = h_pat_ptr[j]; p < h_pat_ptr[j + 1]; ++p) {
-      const int64_t i = h_pat_idx[p];
-      const int ni = (int)h_sizes[i];
-      mk(t[nb + p], h_panel_off[j] + prow * nj, 0, h_row_off[i] * nrhs, ni, nrhs, nj, nj, nrhs, nrhs,
-         d3m::kGemmSub);
-      mk(t[nb + npat + p], h_panel_off[j] + prow * nj, h_row_off[i] * nrhs, (p - h_pat_ptr[j]) * (int64_t)nj * nrhs,
-         nj, nrhs, ni, nj, nrhs, nrhs, d3m::kGemmStore);
-      prow += ni;
-    }
-    const int np = (int)(h_pat_ptr[j + 1] - h_pat_ptr[j]);
-    tf[j] = d3m_gemm_prepare_tasks(&t[nb + h_pat_ptr[j]], np);
-    tp[j] = d3m_gemm_prepare_tasks(&t[nb + npat + h_pat_ptr[j]], np);
-    mk(t[nb + 2 * npat + j], h_binv_off[j], 0, h_row_off[j] * nrhs, nj, nrhs, nj, nj, nrhs, nrhs, d3m::kGemmStore);
-    tx[j] = d3m_gemm_prepare_tasks(&t[nb + 2 * npat + j], 1);
+    const int64_t nj = h_sizes[j], R = h_panel_rows[j];
+    const int64_t need = ((std::max(R, nj) + RC - 1) / RC) * nj * nrhs;
+    if (need > part_elems) return fail(-22, "d3m_block_solve_exec: partial buffer too small");
   }
-  cudaError_t e = cudaMemcpyAsync(d_tasks, t.data(), sizeof(d3m::GemmTask) * ntask, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return fail((int)e, "d3m_block_solve_exec: task upload");
-  auto* dt = static_cast<const d3m::GemmTask*>(d_tasks);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const cplx* pool = CC(d_pool);
   const cplx* binv = CC(d_binv);
+  const int64_t* gidx = static_cast<const int64_t*>(d_gidx);
   cplx* b = C(d_b);
   cplx* u = C(d_u);
   cplx* x = C(d_x);
   cplx* tmp = C(d_tmp);
+  const int N = nrhs;
   for (int j = 0; j < nb; ++j) {
     const int nj = (int)h_sizes[j];
+    const int R = (int)h_panel_rows[j];
     if (nj == 0) continue;
     const int8_t* tags = static_cast<const int8_t*>(d_tags) + h_piv_off[j];
-    const cplx* diag = pool + h_diag_off[j];
-    D3M_TRY(launch(kClsSolve, s, [&] { return d3m_gemm_launch(0, 1, binv, b, tmp, dt + j, 1, tz[j], s); }));
     D3M_TRY(launch(kClsSolve, s, [&] {
-      return d3m_dinv_left_copy_launch(tmp, u + h_row_off[j] * nrhs, nj, nrhs, diag, tags, s);
+      return d3m_rows_gemv_launch(binv + h_binv_off[j], nj, nj, nj, b + h_row_off[j] * N, N, N, tmp, N, nullptr, 0, s);
     }));
-    const int np = (int)(h_pat_ptr[j + 1] - h_pat_ptr[j]);
-    if (np > 0)
+    D3M_TRY(launch(kClsSolve, s, [&] {
+      return d3m_dinv_left_copy_launch(tmp, u + h_row_off[j] * N, nj, N, pool + h_diag_off[j], tags, s);
+    }));
+    if (R > 0)
       D3M_TRY(launch(kClsSolve, s, [&] {
-        return d3m_gemm_launch(0, 1, pool, tmp, b, dt + nb + h_pat_ptr[j], np, tf[j], s);
+        return d3m_rows_gemv_launch(pool + h_panel_off[j], nj, R, nj, tmp, N, N, b, N, gidx + h_gptr[j], 1, s);
       }));
   }
   for (int j = nb - 1; j >= 0; --j) {
     const int nj = (int)h_sizes[j];
+    const int R = (int)h_panel_rows[j];
     if (nj == 0) continue;
-    const int np = (int)(h_pat_ptr[j + 1] - h_pat_ptr[j]);
-    cplx* uj = u + h_row_off[j] * nrhs;
-    if (np > 0) {
+    cplx* uj = u + h_row_off[j] * N;
+    const int64_t len = (int64_t)nj * N;
+    if (R > 0) {
       D3M_TRY(launch(kClsSolve, s, [&] {
-        return d3m_gemm_launch(1, 1, pool, x, d_part, dt + nb + npat + h_pat_ptr[j], np, tp[j], s);
+        return d3m_cols_gemv_launch(pool + h_panel_off[j], nj, R, nj, x, N, gidx + h_gptr[j], N, d_part, s);
       }));
-      D3M_TRY(launch(kClsSolve, s, [&] {
-        return d3m_sub_partials_launch(uj, d_part, np, (int64_t)nj * nrhs, tmp, s);
-      }));
+      const int nch = (R + RC - 1) / RC;
+      D3M_TRY(launch(kClsSolve, s, [&] { return d3m_chunk_reduce_launch(uj, d_part, nch, len, -1.0, tmp, s); }));
     } else {
-      cudaError_t ce = cudaMemcpyAsync(tmp, uj, sizeof(cplx) * nj * nrhs, cudaMemcpyDeviceToDevice, s);
+      cudaError_t ce = cudaMemcpyAsync(tmp, uj, sizeof(cplx) * len, cudaMemcpyDeviceToDevice, s);
       if (ce != cudaSuccess) return fail((int)ce, "d3m_block_solve_exec: copy");
     }
-    D3M_TRY(launch(kClsSolve, s, [&] { return d3m_gemm_launch(1, 1, binv, tmp, x, dt + nb + 2 * npat + j, 1, tx[j], s); }));
+    D3M_TRY(launch(kClsSolve, s, [&] {
+      return d3m_cols_gemv_launch(binv + h_binv_off[j], nj, nj, nj, tmp, N, nullptr, N, d_part, s);
+    }));
+    const int nch = (nj + RC - 1) / RC;
+    D3M_TRY(launch(kClsSolve, s, [&] {
+      return d3m_chunk_reduce_launch(nullptr, d_part, nch, len, 1.0, x + h_row_off[j] * N, s);
+    }));
   }
   return 0;
 }

@@ -58,6 +58,13 @@ int d3m_tri_inv_launch(const void* F, int64_t stride_f, const void* perm, int64_
                        int64_t stride_t, void* Binv, int64_t stride_b, int n, int batch, void* stream);
 int d3m_dinv_rows_launch(const void* X, void* P, int64_t R, int n, const void* F, const void* tags, void* stream);
 int d3m_dinv_left_copy_launch(const void* Z, void* U, int n, int m, const void* F, const void* tags, void* stream);
+int d3m_rows_gemv_launch(const void* A, int lda, int M, int K, const void* B, int ldb, int N, void* C, int ldc,
+                         const void* cmap, int sub, void* stream);
+int d3m_cols_gemv_launch(const void* A, int lda, int R, int Mcols, const void* B, int ldb, const void* bmap, int N,
+                         void* partial, void* stream);
+int d3m_chunk_reduce_launch(const void* base, const void* partial, int nch, int64_t len, double sign, void* out,
+                            void* stream);
+int d3m_solve_rows_per_chunk();
 int d3m_sub_partials_launch(const void* u, const void* partial, int np, int64_t len, void* out, void* stream);
 }
 

@@ -556,14 +556,13 @@ def block_solve(F: BlockFactor, g: list) -> list:
     u = empty((N, cols))
     x = empty((N, cols))
     tmp = empty((int(sched.sizes.max()), cols))
-    part = empty((sched.part_rows, cols))
-    cap = 2 * int(sched.pat_ptr[-1]) + 2 * nb
-    d_tasks = t.empty(64 * cap, dtype=t.uint8, device="cuda")
+    part_elems = int(max(((max(int(r), int(n)) + 15) // 16) * int(n) for r, n in zip(sched.panel_rows, sched.sizes))) * cols
+    part = empty(max(part_elems, 1))
     H = _lib.hptr
     _lib.call("d3m_block_solve_exec", nb, H(sched.sizes), H(sched.row_off), H(sched.diag_off),
-              H(sched.panel_off), H(sched.row_off), H(sched.binv_off), H(sched.pat_ptr),
-              H(sched.pat_idx if sched.pat_idx.size else np.zeros(1, np.int64)), _P(F._pool), _P(F._binv),
-              _P(F._tags), _P(b), _P(u), _P(x), _P(tmp), _P(part), int(cols), _P(d_tasks), cap, stream_ptr())
+              H(sched.panel_off), H(sched.panel_rows), H(sched.row_off), H(sched.binv_off), H(sched.gptr),
+              _P(sched.d_gidx), _P(F._pool), _P(F._binv), _P(F._tags), _P(b), _P(u), _P(x), _P(tmp), _P(part),
+              part_elems, int(cols), stream_ptr())
     out = [None] * nb
     if device_in:
         for j in range(nb):
