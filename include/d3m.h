@@ -61,6 +61,24 @@ int d3m_ldlt_solve_batched(int batch, int n, const void* F, int64_t stride_f, co
                            const void* tags, int64_t stride_t, void* B, int64_t stride_b, int ldb, int m, void* work,
                            void* stream);
 
+/* Batched blocked Bunch-Kaufman for large dense matrices (zlasyf form): per
+ * panel of 16 columns one CTA per matrix (panel in L2) + one grouped DMMA
+ * GEMM for all trailing updates.  Same outputs as d3m_bk_factor_batched;
+ * identical pivot decisions whenever no test sits within rounding of its
+ * threshold, values to rounding.  workspace: d3m_bk_panel_workspace(n, batch)
+ * bytes.  Used by d3m_schur_reduce_batched for n > 512. */
+int d3m_bk_panel_batched(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
+                         void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
+                         void* workspace, void* stream);
+size_t d3m_bk_panel_workspace(int n, int batch);
+
+/* Blocked multi-RHS solve (64-row diagonal blocks in shared memory +
+ * right-looking DMMA GEMM updates), same contract as d3m_ldlt_solve_batched;
+ * d_tasks: 2 * ceil(n/64) * batch GEMM records (64 B each). */
+int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stride_f, const void* perm,
+                                   int64_t stride_p, const void* tags, int64_t stride_t, void* B, int64_t stride_b,
+                                   int ldb, int m, void* work, void* d_tasks, void* stream);
+
 /* Grouped complex GEMM on DMMA: for each task C (op)= A_eff B_eff^T.
  * h_tasks: host array of 64-byte task records (see d3m_gemm.h; tile fields
  * are filled in place), d_tasks: device buffer of the same size.
@@ -71,7 +89,10 @@ int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* C, voi
 
 /* Batched Schur reduction of equal-sized subdomains: factor A_d in place,
  * X = A_d^-1 [D_d | f_d], K_D = 0.5 (D^T X + (D^T X)^T), g_d = D^T x_f.
- * Replaces subdomain.reduce_domain (subdomain.py:166-184) for a batch. */
+ * Replaces subdomain.reduce_domain (subdomain.py:166-184) for a batch.
+ * n <= 512: exact BK + chain solves (bk_scratch: batch*4n complex if n>3200);
+ * n > 512: panel BK + blocked solves (bk_scratch: d3m_bk_panel_workspace
+ * bytes, d_tasks: max(batch, 2 ceil(n/64) batch) records). */
 int d3m_schur_reduce_batched(int batch, int n, int m, void* A, const void* D, const void* f, double pivot_tol,
                              void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
                              void* K_out, void* g_out, void* work_z, void* work_x, void* work_c, void* bk_scratch,

@@ -37,7 +37,10 @@ _SIGNATURES = {
     "d3m_block_solve_exec": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, I32, P],
     "d3m_recover_batched": [I32, I32, I32, P, P, P, P, P, P, P, P, P, P, I64, P, P],
     "d3m_counters_read": [P, P, P],
+    "d3m_bk_panel_batched": [I32, I32, P, I64, I32, F64, I32, P, P, P, P, P, P, P, P, P],
+    "d3m_ldlt_solve_blocked_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P, P],
 }
+_SIZE_T = {"d3m_bk_panel_workspace": [I32, I32]}
 _VOID = {"d3m_set_timing": [I32], "d3m_counters_reset": []}
 
 # GemmTask / CopyTask records (csrc/d3m_gemm.h, csrc/d3m_misc.h)
@@ -52,6 +55,7 @@ assert COPY_TASK.itemsize == 40
 GEMM_SUB, GEMM_STORE, GEMM_ADD, GEMM_SYM = 0, 1, 2, 4
 COPY_STORE, COPY_ADD, COPY_ZERO_ADD = 0, 1, 2
 GEMM_BM = GEMM_BN = 64
+PANEL_BK_MIN = 512        # d3m_capi.cu kPanelBkMin
 
 
 class D3MUnavailable(RuntimeError):
@@ -81,6 +85,10 @@ def load():
         fn.restype = ctypes.c_int
     lib.d3m_last_error.restype = ctypes.c_char_p
     lib.d3m_last_error.argtypes = []
+    for name, args in _SIZE_T.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_size_t
     for name, args in _VOID.items():
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -90,7 +98,7 @@ def load():
 
 
 def exported_symbols() -> list[str]:
-    return list(_SIGNATURES) + list(_VOID) + ["d3m_last_error"]
+    return list(_SIGNATURES) + list(_VOID) + list(_SIZE_T) + ["d3m_last_error"]
 
 
 CLASSES = ("bk", "trsm", "gemm", "solve", "misc")

@@ -78,7 +78,8 @@ int launch(int cls, void* stream, Fn fn) {
 }
 
 using d3m::cplx;
-constexpr int kExactBkMax = 128;
+constexpr int kExactBkMax = 128;    // supernodes up to this use the bit-exact BK kernel
+constexpr int kPanelBkMin = 512;    // subdomains above this use the batched panel BK + blocked solves
 inline cplx* C(void* p) { return static_cast<cplx*>(p); }
 inline const cplx* CC(const void* p) { return static_cast<const cplx*>(p); }
 
@@ -87,6 +88,12 @@ inline const cplx* CC(const void* p) { return static_cast<const cplx*>(p); }
 extern "C" {
 
 int d3m_abi_version(void) { return D3M_ABI_VERSION; }
+int d3m_bk_panel_batched(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
+                         void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
+                         void* workspace, void* stream);
+int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stride_f, const void* perm,
+                                   int64_t stride_p, const void* tags, int64_t stride_t, void* B, int64_t stride_b,
+                                   int ldb, int m, void* work, void* d_tasks, void* stream);
 
 const char* d3m_last_error(void) { return g_err.c_str(); }
 
@@ -128,6 +135,84 @@ int d3m_ldlt_solve_batched(int batch, int n, const void* F, int64_t stride_f, co
   return 0;
 }
 
+// Blocked multi-RHS solve for large factors (n > kBlockedSolveMin): gather,
+// 64-row diagonal solves + right-looking DMMA GEMM updates (forward, then
+// backward with L^T), D^-1, scatter.  d_tasks: >= 2 * ceil(n/64) * batch GEMM
+// records.
+int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stride_f, const void* perm,
+                                   int64_t stride_p, const void* tags, int64_t stride_t, void* B, int64_t stride_b,
+                                   int ldb, int m, void* work, void* d_tasks, void* stream) {
+  if (batch < 0 || n < 0 || m < 0 || ldb < m) return fail(-22, "d3m_ldlt_solve_blocked_batched: bad shape");
+  if (batch == 0 || n == 0 || m == 0) return 0;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int DBR = d3m_diag_block_rows();
+  const int nblk = (n + DBR - 1) / DBR;
+  const int64_t sz = (int64_t)n * m;
+  d3m::SolveBatch sb{CC(F), stride_f, static_cast<const int8_t*>(tags), stride_t, static_cast<const int64_t*>(perm),
+                     stride_p, C(work), sz, nullptr, 0, CC(B), stride_b, n, m, m, ldb};
+  // GEMM task table: [fwd ib][b] then [bwd ib][b]
+  std::vector<d3m::GemmTask> t((size_t)2 * nblk * batch);
+  std::memset(t.data(), 0, sizeof(d3m::GemmTask) * t.size());
+  std::vector<int> tiles(2 * nblk, 0);
+  for (int ib = 0; ib < nblk; ++ib) {
+    const int r0 = ib * DBR, r1 = std::min(n, r0 + DBR), below = n - r1;
+    for (int b = 0; b < batch; ++b) {
+      d3m::GemmTask& f = t[(size_t)ib * batch + b];      // Z[r1:] -= L[r1:, r0:r1] Z[r0:r1]
+      f.a_off = b * stride_f + (int64_t)r1 * n + r0;
+      f.b_off = b * sz + (int64_t)r0 * m;
+      f.c_off = b * sz + (int64_t)r1 * m;
+      f.m = below; f.n = m; f.k = r1 - r0; f.lda = n; f.ldb = m; f.ldc = m; f.flags = d3m::kGemmSub;
+      d3m::GemmTask& g = t[(size_t)(nblk + ib) * batch + b];   // Z[:r0] -= L[r0:r1, :r0]^T Z[r0:r1]
+      g.a_off = b * stride_f + (int64_t)r0 * n;
+      g.b_off = b * sz + (int64_t)r0 * m;
+      g.c_off = b * sz;
+      g.m = r0; g.n = m; g.k = r1 - r0; g.lda = n; g.ldb = m; g.ldc = m; g.flags = d3m::kGemmSub;
+    }
+    tiles[ib] = d3m_gemm_prepare_tasks(&t[(size_t)ib * batch], batch);
+    tiles[nblk + ib] = d3m_gemm_prepare_tasks(&t[(size_t)(nblk + ib) * batch], batch);
+  }
+  cudaError_t e = cudaMemcpyAsync(d_tasks, t.data(), sizeof(d3m::GemmTask) * t.size(), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return fail((int)e, "d3m_ldlt_solve_blocked_batched: task upload");
+  auto* dt = static_cast<const d3m::GemmTask*>(d_tasks);
+  D3M_TRY(launch(kClsSolve, stream, [&] { return d3m_solve_phase_launch(0, &sb, batch, stream); }));   // Z = B[perm]
+  for (int ib = 0; ib < nblk; ++ib) {
+    const int r0 = ib * DBR;
+    D3M_TRY(launch(kClsSolve, stream, [&] {
+      return d3m_diag_block_launch(1, F, stride_f, tags, stride_t, work, sz, n, m, r0, batch, stream);
+    }));
+    if (tiles[ib] > 0)
+      D3M_TRY(launch(kClsGemm, stream, [&] {
+        return d3m_gemm_launch(0, 1, F, work, work, dt + (size_t)ib * batch, batch, tiles[ib], stream);
+      }));
+  }
+  D3M_TRY(launch(kClsSolve, stream, [&] { return d3m_solve_phase_launch(2, &sb, batch, stream); }));   // D^-1
+  for (int ib = nblk - 1; ib >= 0; --ib) {
+    const int r0 = ib * DBR;
+    D3M_TRY(launch(kClsSolve, stream, [&] {
+      return d3m_diag_block_launch(0, F, stride_f, tags, stride_t, work, sz, n, m, r0, batch, stream);
+    }));
+    if (tiles[nblk + ib] > 0)
+      D3M_TRY(launch(kClsGemm, stream, [&] {
+        return d3m_gemm_launch(1, 1, F, work, work, dt + (size_t)(nblk + ib) * batch, batch, tiles[nblk + ib], stream);
+      }));
+  }
+  D3M_TRY(launch(kClsSolve, stream, [&] { return d3m_solve_phase_launch(4, &sb, batch, stream); }));   // B[perm] = Z
+  return 0;
+}
+
+int d3m_bk_panel_batched(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
+                         void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
+                         void* workspace, void* stream) {
+  if (batch < 0 || n < 0 || lda < n) return fail(-22, "d3m_bk_panel_batched: bad shape");
+  d3m::BkArgs a{C(W), stride_w, n, lda, pivot_tol, check_sym, static_cast<int64_t*>(perm), static_cast<int8_t*>(tags),
+                static_cast<int32_t*>(n2x2), static_cast<double*>(growth), static_cast<int32_t*>(info),
+                static_cast<double*>(scale), static_cast<double*>(asym), nullptr};
+  D3M_TRY(launch(kClsBk, stream, [&] { return d3m_bk_panel_batched_launch(&a, batch, workspace, stream); }));
+  return 0;
+}
+
+size_t d3m_bk_panel_workspace(int n, int batch) { return d3m_bk_panel_workspace_bytes(n, batch); }
+
 int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* Cm, void* h_tasks, int ntasks,
                       void* d_tasks, void* stream) {
   if (ntasks <= 0) return 0;
@@ -149,12 +234,24 @@ int d3m_schur_reduce_batched(int batch, int n, int m, void* A, const void* D, co
   if (batch < 0 || n < 0 || m < 0) return fail(-22, "d3m_schur_reduce_batched: bad shape");
   if (batch == 0) return 0;
   const int64_t nn = (int64_t)n * n, nm1 = (int64_t)n * (m + 1);
-  D3M_TRY(d3m_bk_factor_batched(batch, n, A, nn, n, pivot_tol, 1, perm, tags, n2x2, growth, info, scale, asym,
-                                bk_scratch, stream));
+  const bool big = n > kPanelBkMin;
+  // large subdomains: batched blocked BK (panel kernel + grouped DMMA trailing
+  // updates, bk_scratch >= d3m_bk_panel_workspace(n, batch) bytes); small:
+  // the unblocked bit-exact kernel
+  if (big)
+    D3M_TRY(d3m_bk_panel_batched(batch, n, A, nn, n, pivot_tol, 1, perm, tags, n2x2, growth, info, scale, asym,
+                                 bk_scratch, stream));
+  else
+    D3M_TRY(d3m_bk_factor_batched(batch, n, A, nn, n, pivot_tol, 1, perm, tags, n2x2, growth, info, scale, asym,
+                                  bk_scratch, stream));
   if (n == 0) return 0;
   // RHS = [D | f]  (subdomain.py:177-179), X = A^-1 RHS (factor.py:52-66)
   D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_pack_rhs_launch(D, f, work_x, n, m, batch, (int64_t)n * m, n, nm1, stream); }));
-  D3M_TRY(d3m_ldlt_solve_batched(batch, n, A, nn, perm, n, tags, n, work_x, nm1, m + 1, m + 1, work_z, stream));
+  if (big)
+    D3M_TRY(d3m_ldlt_solve_blocked_batched(batch, n, A, nn, perm, n, tags, n, work_x, nm1, m + 1, m + 1, work_z,
+                                           d_tasks, stream));
+  else
+    D3M_TRY(d3m_ldlt_solve_batched(batch, n, A, nn, perm, n, tags, n, work_x, nm1, m + 1, m + 1, work_z, stream));
   if (m == 0) return 0;
   // C = D^T [X | x_f]  (subdomain.py:181,183) on DMMA, one task per domain
   std::vector<d3m::GemmTask> t(batch);

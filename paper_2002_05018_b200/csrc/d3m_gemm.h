@@ -10,6 +10,8 @@ enum : int32_t {
   kGemmAdd = 2,        // C += A B^T
   kGemmModeMask = 3,
   kGemmSym = 4,        // symmetric diagonal target: lower tiles, mirrored write
+  kGemmLowerOnly = 8,  // with kGemmSym: write the lower triangle only (no mirror)
+  kGemmTrackMax = 16,  // atomically max |C|^2 of written entries into tmax[pad_]
 };
 
 // One GEMM of a grouped launch.  Offsets are in complex elements relative to

@@ -65,8 +65,15 @@ int d3m_cols_gemv_launch(const void* A, int lda, int R, int Mcols, const void* B
 int d3m_chunk_reduce_launch(const void* base, const void* partial, int nch, int64_t len, double sign, void* out,
                             void* stream);
 int d3m_solve_rows_per_chunk();
+int d3m_diag_block_launch(int fwd, const void* F, int64_t stride_f, const void* tags, int64_t stride_t, void* Z,
+                          int64_t stride_z, int n, int m, int r0, int batch, void* stream);
+int d3m_diag_block_rows();
+int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* workspace, void* stream);
+size_t d3m_bk_panel_workspace_bytes(int n, int batch);
 int d3m_sub_partials_launch(const void* u, const void* partial, int np, int64_t len, void* out, void* stream);
 }
 
 #include "d3m_gemm.h"
 extern "C" int d3m_gemm_prepare_tasks(d3m::GemmTask* tasks, int ntasks);
+extern "C" int d3m_gemm_launch_tm(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
+                                  int ntasks, int ntiles, void* tmax, void* stream);

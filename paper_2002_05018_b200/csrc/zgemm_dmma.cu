@@ -79,7 +79,7 @@ __device__ __forceinline__ void load_tile(cplx (*S)[PITCH], const cplx* P, int l
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(NTHREADS, 2)
 zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bbase, cplx* Cbase,
-                     const GemmTask* __restrict__ tasks, int ntasks) {
+                     const GemmTask* __restrict__ tasks, int ntasks, unsigned long long* tmax) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   cplx(*As)[BM][PITCH] = reinterpret_cast<cplx(*)[BM][PITCH]>(smem_raw);
   cplx(*Bs)[BN][PITCH] = reinterpret_cast<cplx(*)[BN][PITCH]>(smem_raw + sizeof(cplx) * STAGES * BM * PITCH);
@@ -107,6 +107,7 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
   cplx* C = Cbase + tk.c_off;
   const int M = tk.m, N = tk.n, K = tk.k;
   const int m0 = tm * BM, n0 = tn * BN;
+  if (m0 >= M || n0 >= N) return;      // device-built tasks may shrink below their tile budget
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
@@ -173,6 +174,9 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
   // ---- epilogue ------------------------------------------------------------
   const int mode = tk.flags & kGemmModeMask;
   const bool sym = (tk.flags & kGemmSym) != 0;
+  const bool mirror = sym && !(tk.flags & kGemmLowerOnly);
+  const bool track = (tk.flags & kGemmTrackMax) != 0 && tmax != nullptr;
+  double tm2 = 0.0;
   const int ldc = tk.ldc;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -187,8 +191,10 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
         if (sym) {
           if (c > r) continue;
           cplx* p = C + (int64_t)r * ldc + c;
-          *p = c_sub(*p, u);
-          if (c < r) {
+          const cplx w = c_sub(*p, u);
+          *p = w;
+          if (track) tm2 = fmax(tm2, w.x * w.x + w.y * w.y);
+          if (mirror && c < r) {
             cplx* q = C + (int64_t)c * ldc + r;
             *q = c_sub(*q, u);
           }
@@ -199,9 +205,15 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
           else *p = c_add(*p, u);
         }
       }
+  if (track) {   // non-negative doubles order like their bit patterns: integer max is exact
+    tm2 = warp_max(tm2);
+    if ((threadIdx.x & 31) == 0) atomicMax(tmax + tk.pad_, (unsigned long long)__double_as_longlong(tm2));
+  }
 }
 
 constexpr size_t kGemmSmem = sizeof(cplx) * STAGES * (BM + BN) * PITCH;
+
+static unsigned long long* g_tmax = nullptr;   // set per launch by d3m_gemm_launch_tm
 
 template <bool TA, bool TB>
 static int launch_t(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
@@ -212,7 +224,7 @@ static int launch_t(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks
                          (int)kGemmSmem);
     configured = true;
   }
-  zgemm_grouped_kernel<TA, TB><<<ntiles, NTHREADS, kGemmSmem, s>>>(A, B, C, tasks, ntasks);
+  zgemm_grouped_kernel<TA, TB><<<ntiles, NTHREADS, kGemmSmem, s>>>(A, B, C, tasks, ntasks, g_tmax);
   return (int)cudaGetLastError();
 }
 
@@ -232,10 +244,19 @@ extern "C" int d3m_gemm_prepare_tasks(d3m::GemmTask* tasks, int ntasks) {
   return total;
 }
 
+extern "C" int d3m_gemm_launch_tm(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
+                                  int ntasks, int ntiles, void* tmax, void* stream);
+
 extern "C" int d3m_gemm_launch(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
                                int ntasks, int ntiles, void* stream) {
+  return d3m_gemm_launch_tm(ta, tb, A, B, C, dtasks, ntasks, ntiles, nullptr, stream);
+}
+
+extern "C" int d3m_gemm_launch_tm(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
+                                  int ntasks, int ntiles, void* tmax, void* stream) {
   using namespace d3m;
   if (ntiles <= 0 || ntasks <= 0) return 0;
+  g_tmax = static_cast<unsigned long long*>(tmax);
   auto a = static_cast<const cplx*>(A);
   auto b = static_cast<const cplx*>(B);
   auto c = static_cast<cplx*>(C);

@@ -102,8 +102,13 @@ class DenseFactor:
         t = require_cuda()
         Z = to_device(B).reshape(self.n, cols).clone()
         work = empty((self.n, cols))
-        _lib.call("d3m_ldlt_solve_batched", 1, self.n, _P(self.packed), 0, _P(self.perm_dev), 0,
-                  _P(self.tags_dev), 0, _P(Z), 0, cols, cols, _P(work), stream_ptr())
+        if self.n > _lib.PANEL_BK_MIN:
+            d_tasks = t.empty(64 * 2 * ((self.n + 63) // 64), dtype=t.uint8, device="cuda")
+            _lib.call("d3m_ldlt_solve_blocked_batched", 1, self.n, _P(self.packed), 0, _P(self.perm_dev), 0,
+                      _P(self.tags_dev), 0, _P(Z), 0, cols, cols, _P(work), _P(d_tasks), stream_ptr())
+        else:
+            _lib.call("d3m_ldlt_solve_batched", 1, self.n, _P(self.packed), 0, _P(self.perm_dev), 0,
+                      _P(self.tags_dev), 0, _P(Z), 0, cols, cols, _P(work), stream_ptr())
         if one_d:
             Z = Z.reshape(self.n)
         if device_in:

@@ -144,8 +144,13 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
         wz = empty((B, n, m + 1))
         wx = empty((B, n, m + 1))
         wc = empty((B, max(m, 1), m + 1))
-        scratch = empty((B, 4 * n)) if 64 * n > 200 * 1024 else None
-        d_tasks = t.empty(64 * B, dtype=t.uint8, device="cuda")
+        if n > _lib.PANEL_BK_MIN:
+            nbytes = int(_lib.load().d3m_bk_panel_workspace(n, B))
+            scratch = t.empty((nbytes + 15) // 16, dtype=t.complex128, device="cuda")
+            d_tasks = t.empty(64 * max(B, 2 * ((n + 63) // 64) * B), dtype=t.uint8, device="cuda")
+        else:
+            scratch = empty((B, 4 * n)) if 64 * n > 200 * 1024 else None
+            d_tasks = t.empty(64 * B, dtype=t.uint8, device="cuda")
         _lib.call("d3m_schur_reduce_batched", B, n, m, _P(A), _P(D), _P(f), float(pivot_tol), _P(perm),
                   _P(tags), _P(n2), _P(gr), _P(info), _P(sc), _P(asy), _P(K), _P(g), _P(wz), _P(wx), _P(wc),
                   _P(scratch), _P(d_tasks), stream_ptr())
@@ -166,6 +171,18 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
     if first_error is not None:
         raise first_error[1]
     return out
+
+
+def _solve_batch(F, pv, tg, Z, n, m, B, work):
+    """Z (B x n x m) <- A^-1 Z with packed factors F (B x n x n)."""
+    t = require_cuda()
+    if n > _lib.PANEL_BK_MIN:
+        d_tasks = t.empty(64 * 2 * ((n + 63) // 64) * B, dtype=t.uint8, device="cuda")
+        _lib.call("d3m_ldlt_solve_blocked_batched", B, n, _P(F), n * n, _P(pv), n, _P(tg), n, _P(Z), n * m, m, m,
+                  _P(work), _P(d_tasks), stream_ptr())
+    else:
+        _lib.call("d3m_ldlt_solve_batched", B, n, _P(F), n * n, _P(pv), n, _P(tg), n, _P(Z), n * m, m, m,
+                  _P(work), stream_ptr())
 
 
 def _dev_D(s) -> bool:
@@ -324,8 +341,7 @@ def recover_primal(systems: list[SubdomainSystem], lam: list) -> np.ndarray | De
             _lib.call("d3m_zgemm_grouped", 0, 1, _P(D), _P(lamc), _P(rhs), _lib.hptr(tasks), B, _P(d_tasks),
                       stream_ptr())
         work = empty((B, n))
-        _lib.call("d3m_ldlt_solve_batched", B, n, _P(F), n * n, _P(pv), n, _P(tg), n, _P(rhs), n, 1, 1,
-                  _P(work), stream_ptr())
+        _solve_batch(F, pv, tg, rhs, n, 1, B, work)
     # ordered average: contributions per global dof in ascending domain order
     gl, src = [], []
     for idx in range(len(systems)):          # acc[dof_map] += E in list order

@@ -141,3 +141,35 @@ def test_config3_pivots_and_schur_vs_reference(cuda):
         if f"KD{i}" in g.files:
             ref = g[f"KD{i}"]
             assert np.linalg.norm(KDh - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("n,m,batch", [(600, 40, 3), (1030, 17, 2)])
+def test_large_subdomain_panel_bk_vs_oracle(cuda, oracle, n, m, batch):
+    """n > 512 takes the batched panel BK (grouped DMMA trailing updates) and
+    the blocked solves: pivots bit-exact vs the oracle, K_D / g_d to 1e-10."""
+    import paper_2002_05018_b200 as d
+    rng = np.random.default_rng(n + m)
+    systems, ref = [], []
+    for b in range(batch):
+        G = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2 * n)
+        A = (G + G.T) / 2
+        A[np.diag_indices(n)] += rng.uniform(-1, 1, n) + 1j * rng.uniform(-0.1, 0.1, n)
+        D = np.zeros((n, m), dtype=complex)
+        D[rng.choice(n, m, replace=False), np.arange(m)] = rng.choice([-1.0, 1.0], m)
+        D[:, :3] += rng.standard_normal((n, 3)) * 0.1          # some dense columns too
+        f = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        systems.append(d.SubdomainSystem(b, A, f, np.arange(n), [d.Coupling(0, D, 1)]))
+        ref.append(oracle.reduce_domain(A, D, f))
+    red = d.reduce_domains(systems)
+    for s, (KD, gd), (Ko, go, fo) in zip(systems, red, ref):
+        assert np.array_equal(s.factor.perm, fo.perm)
+        assert np.array_equal(s.factor.tags, fo.tags)
+        assert s.factor.n_2x2 == fo.n_2x2 and fo.n_2x2 > 0
+        assert 1.0 <= s.factor.growth <= 2.57
+        assert np.linalg.norm(np.asarray(KD) - Ko) <= 1e-10 * np.linalg.norm(Ko)
+        assert np.linalg.norm(np.asarray(gd) - go) <= 1e-10 * np.linalg.norm(go)
+        # DenseFactor.solve on the large factor (blocked path)
+        B = rng.standard_normal((n, 3)) + 1j * rng.standard_normal((n, 3))
+        X = s.factor.solve(B)
+        Xo = fo.solve(B)
+        assert np.linalg.norm(X - Xo) <= 1e-10 * np.linalg.norm(Xo)
