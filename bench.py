@@ -252,7 +252,61 @@ def run_ours(args):
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if not args.no_cfg3:
+        line["secondary"] = {"cfg3": _cfg3_secondary(max(2, min(args.steps, 3)))}
     print(json.dumps(line), flush=True)
+
+
+def _cfg3_secondary(steps: int) -> dict:
+    """BASELINE configs[2]: batched Schur complement of 64 subdomains
+    (n = 2048, m = 384).  Device-resident inputs for the timed value; the
+    public API from numpy inputs for e2e."""
+    import torch
+    import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import workloads as wl
+    from paper_2002_05018_b200.device import DeviceArray, to_device
+    host = wl.config3_systems(64)
+    dev = [d.SubdomainSystem(s.domain, DeviceArray(to_device(s.A)), DeviceArray(to_device(s.f)), s.dof_map,
+                             [d.Coupling(c.interface, DeviceArray(to_device(c.D)), c.sign) for c in s.couplings])
+           for s in host]
+    n, m, B = 2048, 384, 64
+    flops = B * (8 * n ** 3 // 3 + 8 * n * n * (m + 1))       # BK + the (m+1)-RHS solves (SURVEY 8(d))
+    for s in dev:
+        s._d3m_D = None
+    d.reduce_domains(dev)
+    torch.cuda.synchronize()
+    s0 = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s0)
+    for _ in range(steps):
+        for s in dev:
+            s.factor = None
+            s._d3m_D = None
+        red = d.reduce_domains(dev)
+    e1.record(s0)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    red_h = d.reduce_domains(host)
+    np.asarray(red_h[-1][0])
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3
+    h2d = 16 * sum(s.A.size + s.f.size + sum(c.D.size for c in s.couplings) for s in host)
+    out = {"workload": "cfg3: 64 subdomains, n=2048, m=384 (A_i=(M+M^T)/2, D_i one +-1 per column), K_D and g_d",
+           "ms_per_step": round(ms, 3), "value": round(flops / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+           "flops_per_step": flops, "e2e": {"ms_per_step": round(e2e_ms, 1), "h2d_bytes_per_step": int(h2d),
+                                             "d2h_bytes_per_step": int(16 * B * m * (m + 1))}}
+    try:
+        import json as _j
+        g = np.load(os.path.join(ROOT, "tests", "golden", "cfg3.npz"))
+        out["cpu_reference_s_per_subdomain"] = round(float(g["time0"]), 1)
+        out["cpu_reference_note"] = ("reference reduce_domain (numba JIT) timed in the build container "
+                                     "(8-core Xeon) by tools/gen_golden.py; 64 subdomains ~ 64x serial")
+    except Exception:
+        pass
+    del red, red_h
+    return out
 
 
 def _residual(K, rhs, x) -> float:
@@ -345,6 +399,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-columns", type=int, default=CPU_SAMPLE_COLUMNS)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cfg3", action="store_true", help="skip the secondary config-3 measurement")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

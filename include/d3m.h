@@ -114,6 +114,13 @@ int d3m_ordered_average(const void* E, const void* ptr, const void* src, void* o
 
 int d3m_zero(void* p, int64_t n, void* stream);
 
+/* flag[0] is cleared when any of the nb diagonal slots (pool + off[b], order
+ * n[b], device int64 arrays) is not bitwise symmetric.  block_ldlt uses it to
+ * pass check_sym = 2 (lower-triangle-only scale, asym = 0) to the diagonal
+ * BK: updates of diagonal targets are mirrored exactly, so symmetric K
+ * blocks stay exactly symmetric through the factorisation. */
+int d3m_diag_sym_exact(const void* pool, const void* off, const void* n, int nb, void* flag, void* stream);
+
 /* Test hook: hyp[i] = glibc-hypot modulus (numba abs, kernels.py:50-77) and
  * npabs[i] = numpy np.abs modulus (factor.py:94-96) of z[i], as computed by
  * the device code that makes the pivot decisions. */
@@ -133,6 +140,8 @@ int d3m_modulus_probe(const void* z, void* hyp, void* npabs, int64_t n, void* st
  * run on the high-priority critical stream (lookahead), the rest on a
  * low-priority stream.  Per-column pivots go to d_perm/d_tags at
  * h_piv_off[j]; info/n2x2/growth/scale/asym are nb-long device arrays.
+ * check_sym: 1 = full numpy-style symmetry check per diagonal block,
+ * 2 = blocks known exactly symmetric (d3m_diag_sym_exact).
  * xbuf: X scratch (2 x max R_j n_j with lookahead). */
 int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_off, const int64_t* h_panel_off,
                         const int64_t* h_panel_rows, const int64_t* h_piv_off, const int64_t* h_binv_off,

@@ -31,6 +31,7 @@ _SIGNATURES = {
     "d3m_gather_rows": [P, P, P, I64, I32, P],
     "d3m_ordered_average": [P, P, P, P, I64, P],
     "d3m_zero": [P, I64, P],
+    "d3m_diag_sym_exact": [P, P, P, I32, P, P],
     "d3m_modulus_probe": [P, P, P, I64, P],
     "d3m_block_ldlt_exec": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, P, P, P, P, P, P, P,
                             P, F64, I32, I32, P],

@@ -75,6 +75,11 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
   // ---- prologue (factor.py:94-98 scale / symmetry; kernels.py:45-46) ------
   // max |.|^2 proxies first (3 flops per entry); the exact numpy modulus is
   // then evaluated only for entries whose proxy is within 1e-14 of the max
+  // check_sym == 2: the caller guarantees an exactly symmetric matrix (block
+  // LDL^T diagonal targets: symmetric K blocks + mirrored updates), so the
+  // scale is the max over the lower triangle and asym is 0 -- row-wise,
+  // coalesced reads of half the matrix
+  const bool lower_only = a.check_sym == 2;
   double p_all = 0.0, p_asy = 0.0, tm2 = 0.0;
   // pass 1 over the lower triangle incl. diagonal, row segments, 8 loads in
   // flight per lane: proxies of |W_ij|, |W_ij - W_ji| and the trailing max
@@ -85,7 +90,7 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int j = jb + lane + 32 * u;
-        if (j <= i) { z[u] = G(i, j); zt[u] = G(j, i); }
+        if (j <= i) { z[u] = G(i, j); zt[u] = lower_only ? z[u] : G(j, i); }
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -111,7 +116,7 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int j = jb + lane + 32 * u;
-          if (j <= i) { z[u] = G(i, j); zt[u] = G(j, i); }
+          if (j <= i) { z[u] = G(i, j); zt[u] = lower_only ? z[u] : G(j, i); }
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {

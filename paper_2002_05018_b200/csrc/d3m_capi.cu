@@ -292,6 +292,11 @@ int d3m_ordered_average(const void* E, const void* ptr, const void* src, void* o
   return 0;
 }
 
+int d3m_diag_sym_exact(const void* pool, const void* off, const void* n, int nb, void* flag, void* stream) {
+  D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_sym_exact_launch(pool, off, n, nb, flag, stream); }));
+  return 0;
+}
+
 int d3m_zero(void* p, int64_t n, void* stream) {
   D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_zero_launch(p, n, stream); }));
   return 0;
@@ -342,6 +347,18 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
   auto* ttasks = static_cast<const d3m::GemmTask*>(d_trsm_tasks);
   cplx* pool = C(d_pool);
   cplx* binv = C(d_binv);
+  // D^-1 coefficients of the current column (3 complex per pivot column);
+  // double-buffered with the column parity like xbuf
+  static void* coef_buf = nullptr;
+  static size_t coef_cap = 0;
+  int64_t nmax = 0;
+  for (int j = 0; j < nb; ++j) nmax = std::max<int64_t>(nmax, h_sizes[j]);
+  const size_t coef_bytes = (size_t)2 * 3 * std::max<int64_t>(nmax, 1) * sizeof(cplx);
+  if (coef_bytes > coef_cap) {
+    if (coef_buf) cudaFree(coef_buf);
+    if (cudaMalloc(&coef_buf, coef_bytes) != cudaSuccess) return fail(-12, "d3m_block_ldlt_exec: coef alloc");
+    coef_cap = coef_bytes;
+  }
   bool rest_pending = false;
   for (int j = 0; j < nb; ++j) {
     const int nj = (int)h_sizes[j];
@@ -351,6 +368,7 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
     int64_t* perm = static_cast<int64_t*>(d_perm) + h_piv_off[j];
     int8_t* tags = static_cast<int8_t*>(d_tags) + h_piv_off[j];
     cplx* diag = pool + h_diag_off[j];
+    cplx* coef = static_cast<cplx*>(coef_buf) + (size_t)(j & 1) * 3 * nmax;
     d3m::BkArgs a{diag, 0, nj, nj, pivot_tol, check_sym, perm, tags,
                   static_cast<int32_t*>(d_n2x2) + j, static_cast<double*>(d_growth) + j,
                   static_cast<int32_t*>(d_info) + j, static_cast<double*>(d_scale) + j,
@@ -365,9 +383,10 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
         const int rc = d3m_bk_blocked_launch(&a, 1, s0);
         return rc == -22 ? d3m_bk_launch(&a, 1, s0) : rc;
       }));
-      // Binv_j = L_jj^-1 P_j (also used by block_solve)
+      // Binv_j = L_jj^-1 P_j (also used by block_solve) + D_jj^-1 coefficients
       D3M_TRY(launch(kClsTrsm, s0, [&] {
-        return d3m_tri_inv_launch(diag, 0, perm, 0, tags, 0, binv + h_binv_off[j], 0, nj, 1, s0);
+        const int rc = d3m_tri_inv_warp_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, s0);
+        return rc == -22 ? d3m_tri_inv_launch(diag, 0, perm, 0, tags, 0, binv + h_binv_off[j], 0, nj, 1, s0) : rc;
       }));
     }
     if (R > 0) {
@@ -375,7 +394,10 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
       D3M_TRY(launch(kClsTrsm, s0, [&] {
         return d3m_gemm_launch(0, 0, pool, binv, xbuf, ttasks + j, 1, (int)h_tiles_trsm[j], s0);
       }));
-      D3M_TRY(launch(kClsTrsm, s0, [&] { return d3m_dinv_rows_launch(xbuf, pool + h_panel_off[j], R, nj, diag, tags, s0); }));
+      D3M_TRY(launch(kClsTrsm, s0, [&] {
+        return nj <= 512 ? d3m_dinv_rows_coef_launch(xbuf, pool + h_panel_off[j], R, nj, tags, coef, s0)
+                         : d3m_dinv_rows_launch(xbuf, pool + h_panel_off[j], R, nj, diag, tags, s0);
+      }));
     }
     const int64_t t0 = h_task_ptr[j], tn = h_task_next[j], t1 = h_task_ptr[j + 1];
     // X_j / L_j are ready: the bulk ("rest") update of column j only reads

@@ -54,6 +54,7 @@ int d3m_ordered_average_launch(const void* E, const void* ptr, const void* src, 
 int d3m_gather_index_launch(const void* src, const void* idx, void* out, int64_t nrows, int cols, void* stream);
 int d3m_block_copy_launch(const void* src, void* dst, const void* dtasks, int ntasks, int64_t max_elems, void* stream);
 int d3m_zero_launch(void* p, int64_t n, void* stream);
+int d3m_sym_exact_launch(const void* pool, const void* off, const void* n, int nb, void* flag, void* stream);
 int d3m_tri_inv_launch(const void* F, int64_t stride_f, const void* perm, int64_t stride_p, const void* tags,
                        int64_t stride_t, void* Binv, int64_t stride_b, int n, int batch, void* stream);
 int d3m_dinv_rows_launch(const void* X, void* P, int64_t R, int n, const void* F, const void* tags, void* stream);
@@ -65,6 +66,10 @@ int d3m_cols_gemv_launch(const void* A, int lda, int R, int Mcols, const void* B
 int d3m_chunk_reduce_launch(const void* base, const void* partial, int nch, int64_t len, double sign, void* out,
                             void* stream);
 int d3m_solve_rows_per_chunk();
+int d3m_tri_inv_warp_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef, int n,
+                            void* stream);
+int d3m_dinv_rows_coef_launch(const void* X, void* P, int64_t R, int n, const void* tags, const void* coef,
+                              void* stream);
 int d3m_diag_block_launch(int fwd, const void* F, int64_t stride_f, const void* tags, int64_t stride_t, void* Z,
                           int64_t stride_z, int n, int m, int r0, int batch, void* stream);
 int d3m_diag_block_rows();

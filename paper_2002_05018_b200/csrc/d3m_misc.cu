@@ -162,3 +162,30 @@ extern "C" int d3m_modulus_probe(const void* z, void* hyp, void* npabs, int64_t 
       static_cast<const cplx*>(z), static_cast<double*>(hyp), static_cast<double*>(npabs), n);
   return (int)cudaGetLastError();
 }
+
+// flag[0] = 0 if any diagonal slot (offsets off[b], order n[b]) is not
+// exactly symmetric (W[i][j] != W[j][i] bitwise); one CTA per block.
+__global__ void sym_exact_kernel(const cplx* pool, const int64_t* off, const int64_t* nn, int* flag) {
+  const int b = blockIdx.x;
+  const int n = (int)nn[b];
+  const cplx* W = pool + off[b];
+  int bad = 0;
+  for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    if (j < i) {
+      const cplx x = W[(int64_t)i * n + j], y = W[(int64_t)j * n + i];
+      bad |= (__double_as_longlong(x.x) != __double_as_longlong(y.x)) |
+             (__double_as_longlong(x.y) != __double_as_longlong(y.y));
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) flag[0] = 0;
+}
+
+extern "C" int d3m_sym_exact_launch(const void* pool, const void* off, const void* n, int nb, void* flag,
+                                    void* stream) {
+  if (nb <= 0) return 0;
+  sym_exact_kernel<<<nb, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(pool), static_cast<const int64_t*>(off), static_cast<const int64_t*>(n),
+      static_cast<int*>(flag));
+  return (int)cudaGetLastError();
+}

@@ -435,3 +435,124 @@ extern "C" int d3m_sub_partials_launch(const void* u, const void* partial, int n
       static_cast<const cplx*>(u), static_cast<const cplx*>(partial), np, len, static_cast<cplx*>(out));
   return (int)cudaGetLastError();
 }
+
+namespace d3m {
+
+// -------------------------------------------------------------------------
+// Warp-per-column L^-1 P (n <= 32*NPER): lane l keeps y[l + 32t] and the
+// current L row's L[c][l + 32t] in registers, the next row is prefetched
+// while the current step reduces, one warp reduction per elimination step.
+// Lane 0 of the warp owning column q also writes the D^-1 coefficients of
+// pivot column q used by the panel's L = X D^-1 pass:
+//   1x1: coef[q] = (1/d, 0, 0);   2x2 starting at q: coef[q] = (p, s, r) with
+//   [[a, b], [b, c]]^-1 = [[p, s], [s, r]];   second column of a 2x2: unused.
+// -------------------------------------------------------------------------
+template <int NPER>
+__global__ void __launch_bounds__(256)
+tri_inv_warp_kernel(const cplx* __restrict__ F, const int64_t* __restrict__ perm, const int8_t* __restrict__ tags,
+                    cplx* Binv, cplx* coef, int n) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (q >= n) return;
+  cplx y[NPER], lr[NPER], nx[NPER];
+#pragma unroll
+  for (int t = 0; t < NPER; ++t) y[t] = mk(lane + 32 * t == q ? 1.0 : 0.0, 0.0);
+  auto load_row = [&](int c, cplx* dst) {
+#pragma unroll
+    for (int t = 0; t < NPER; ++t) {
+      const int cp = lane + 32 * t;
+      dst[t] = (c < n && cp >= q && cp < c) ? __ldg(F + (int64_t)c * n + cp) : mk(0.0, 0.0);
+    }
+  };
+  if (q + 1 < n) load_row(q + 1, lr);
+  for (int c = q + 1; c < n; ++c) {
+    load_row(c + 1, nx);                          // prefetch the next row
+    if (tags[c - 1] == 2) {                       // L[c][c-1] of a 2x2 pivot is zero
+#pragma unroll
+      for (int t = 0; t < NPER; ++t)
+        if (lane + 32 * t == c - 1) lr[t] = mk(0.0, 0.0);
+    }
+    cplx acc = mk(0.0, 0.0);
+#pragma unroll
+    for (int t = 0; t < NPER; ++t) c_fma(acc, lr[t], y[t]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+#pragma unroll
+    for (int t = 0; t < NPER; ++t)
+      if (lane + 32 * t == c) y[t] = mk(-acc.x, -acc.y);
+#pragma unroll
+    for (int t = 0; t < NPER; ++t) lr[t] = nx[t];
+  }
+  const int64_t pc = perm[q];
+#pragma unroll
+  for (int t = 0; t < NPER; ++t) {
+    const int row = lane + 32 * t;
+    if (row < n) Binv[(int64_t)row * n + pc] = row < q ? mk(0.0, 0.0) : y[t];
+  }
+  if (lane == 0 && coef != nullptr) {
+    const int8_t tg = tags[q];
+    if (tg == 1) {
+      coef[3 * q] = x_div_np(mk(1.0, 0.0), F[(int64_t)q * n + q]);
+    } else if (tg == 2) {
+      const cplx a = F[(int64_t)q * n + q], b = F[(int64_t)(q + 1) * n + q], c = F[(int64_t)(q + 1) * n + q + 1];
+      const cplx det = c_sub(c_mul(a, c), c_mul(b, b));
+      const cplx inv = x_div_np(mk(1.0, 0.0), det);
+      coef[3 * q] = c_mul(c, inv);                              // p
+      coef[3 * q + 1] = c_mul(mk(-b.x, -b.y), inv);             // s
+      coef[3 * q + 2] = c_mul(a, inv);                          // r
+    }
+  }
+}
+
+// L rows = X rows D^-1 with the precomputed coefficients (row-vectorised)
+__global__ void dinv_rows_coef_kernel(const cplx* __restrict__ X, cplx* P, int64_t R, int n,
+                                      const int8_t* __restrict__ tags, const cplx* __restrict__ coef) {
+  const int64_t total = R * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / n;
+    const int c = (int)(e - r * n);
+    const int8_t t = tags[c];
+    if (t == 1) {
+      P[e] = c_mul(X[e], coef[3 * c]);
+    } else if (t == 2) {
+      const cplx x0 = X[e], x1 = X[e + 1];
+      const cplx p = coef[3 * c], s = coef[3 * c + 1], q = coef[3 * c + 2];
+      P[e] = c_add(c_mul(x0, p), c_mul(x1, s));
+      P[e + 1] = c_add(c_mul(x0, s), c_mul(x1, q));
+    }
+    (void)r;
+  }
+}
+
+}  // namespace d3m
+
+// warp-per-column inverse for n <= 512 (returns -22 above: use d3m_tri_inv_launch)
+extern "C" int d3m_tri_inv_warp_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef,
+                                       int n, void* stream) {
+  using namespace d3m;
+  if (n <= 0) return 0;
+  const dim3 grid((n + 7) / 8);
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  auto Fp = static_cast<const cplx*>(F);
+  auto pp = static_cast<const int64_t*>(perm);
+  auto tp = static_cast<const int8_t*>(tags);
+  if (n <= 256) tri_inv_warp_kernel<8><<<grid, 256, 0, s>>>(Fp, pp, tp, static_cast<cplx*>(Binv), static_cast<cplx*>(coef), n);
+  else if (n <= 512) tri_inv_warp_kernel<16><<<grid, 256, 0, s>>>(Fp, pp, tp, static_cast<cplx*>(Binv), static_cast<cplx*>(coef), n);
+  else return -22;
+  return (int)cudaGetLastError();
+}
+
+extern "C" int d3m_dinv_rows_coef_launch(const void* X, void* P, int64_t R, int n, const void* tags, const void* coef,
+                                         void* stream) {
+  using namespace d3m;
+  if (R <= 0 || n <= 0) return 0;
+  const int64_t total = R * n;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 16384);
+  dinv_rows_coef_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(X), static_cast<cplx*>(P), R, n, static_cast<const int8_t*>(tags),
+      static_cast<const cplx*>(coef));
+  return (int)cudaGetLastError();
+}

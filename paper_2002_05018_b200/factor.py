@@ -322,6 +322,8 @@ class _Schedule:
         tt["tiles_n"] = (sizes + bm - 1) // bm
         self.tiles_trsm = (((self.panel_rows + bm - 1) // bm) * ((sizes + bm - 1) // bm)).astype(np.int64)
         self.d_trsm_tasks = upload_bytes(tt)
+        self.d_diag_off = upload_i64(self.diag_off if nb else np.zeros(1, np.int64))
+        self.d_sizes = upload_i64(sizes if nb else np.zeros(1, np.int64))
         self.part_rows = int(max([len(p) * int(sizes[j]) for j, p in enumerate(pattern)] + [1]))
         self.task_ptr = np.asarray(ptr, dtype=np.int64)
         self.task_next = np.asarray(nxt if nxt else [0], dtype=np.int64)
@@ -475,6 +477,11 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
     pool = empty(max(sched.pool_elems, 1))
     _lib.call("d3m_zero", _P(pool), sched.pool_elems, stream_ptr())
     _upload_K(K, sched, plan, pool)
+    # exactly symmetric diagonal blocks stay exactly symmetric (mirrored SYM
+    # updates): the diagonal BK then needs only the lower triangle
+    flag = t.ones(1, dtype=t.int32, device="cuda")
+    _lib.call("d3m_diag_sym_exact", _P(pool), _P(sched.d_diag_off), _P(sched.d_sizes), nb, _P(flag), stream_ptr())
+    check_sym = 2 if int(flag.item()) == 1 else 1
     perm = t.empty(max(sched.piv_elems, 1), dtype=t.int64, device="cuda")
     tags = t.empty(max(sched.piv_elems, 1), dtype=t.int8, device="cuda")
     info = t.empty(nb, dtype=t.int32, device="cuda")
@@ -491,7 +498,7 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
               H(sched.panel_rows), H(sched.row_off), H(sched.binv_off), H(sched.task_ptr), H(sched.task_next),
               H(sched.tiles_next), H(sched.tiles_rest), H(sched.tiles_trsm), _P(sched.d_tasks),
               _P(sched.d_trsm_tasks), _P(pool), _P(binv), _P(xbuf), sched.xbuf_elems, _P(perm), _P(tags),
-              _P(info), _P(n2), _P(gr), _P(sc), _P(asy), _P(scratch), float(pivot_tol), 1,
+              _P(info), _P(n2), _P(gr), _P(sc), _P(asy), _P(scratch), float(pivot_tol), check_sym,
               int(bool(lookahead)), stream_ptr())
     info_h = info.cpu().numpy()
     bad = np.flatnonzero(info_h != -1)

@@ -128,10 +128,13 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
         f = empty((B, n))
         for r, idx in enumerate(members):
             s = systems[idx]
-            A[r].copy_(to_device(s.A).reshape(n, n))
+            _fill(A[r], s.A, (n, n))
             if m:
-                D[r].copy_(to_device(_coupling_matrix(s)) if not _dev_D(s) else s._d3m_D)
-            f[r].copy_(to_device(s.f).reshape(n))
+                if _dev_D(s):
+                    D[r].copy_(s._d3m_D)
+                else:
+                    _fill(D[r], _coupling_matrix(s), (n, m))
+            _fill(f[r], s.f, (n,))
         perm = t.empty((B, n), dtype=t.int64, device="cuda")
         tags = t.empty((B, n), dtype=t.int8, device="cuda")
         n2 = t.empty(B, dtype=t.int32, device="cuda")
@@ -171,6 +174,16 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
     if first_error is not None:
         raise first_error[1]
     return out
+
+
+def _fill(dst, src, shape):
+    """Copy a host array or device handle into a device slice (one H2D copy
+    straight from the numpy buffer for host inputs)."""
+    t = require_cuda()
+    if isinstance(src, DeviceArray) or type(src).__module__.startswith("torch"):
+        dst.copy_(to_device(src).reshape(shape))
+    else:
+        dst.copy_(t.from_numpy(np.ascontiguousarray(np.asarray(src, dtype=np.complex128)).reshape(shape)))
 
 
 def _solve_batch(F, pv, tg, Z, n, m, B, work):
