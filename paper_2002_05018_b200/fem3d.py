@@ -380,3 +380,50 @@ def interpolate_einc(model: FemModel, rhs: int = 0) -> np.ndarray:
         E, _ = _einc(model.prob, a + s * t, model.prob.polarisations[rhs], model.prob.directions[rhs])
         out += w * np.einsum("ed,ed->e", E, t)
     return out
+
+
+def solve_d3m(model: FemModel, rhs: int = 0, ordering: str = "builtin", timers: dict | None = None):
+    """Full D3M pipeline of the hot path on the GPU for one RHS column
+    (driver.run_pipeline:103-142 analog): reduce -> assemble -> ordering /
+    symbolic -> block LDL^T -> block solve -> recover.  Returns the global
+    edge solution (host numpy) and fills ``timers`` (seconds, wall clock with
+    device synchronisation) when given."""
+    import time
+
+    import torch
+
+    from . import blockmat, factor, ordering as ordm, subdomain, symbolic
+
+    def tick():
+        torch.cuda.synchronize()
+        return time.perf_counter()
+
+    t = {}
+    t0 = tick()
+    systems = subdomain_systems(model, rhs)
+    t1 = tick()
+    red = subdomain.reduce_domains(systems)
+    t2 = tick()
+    R = subdomain.assemble_reduced(red, model)
+    g = blockmat.clique_graph(R.K)
+    order = ordm.reorder(g, R.K.sizes) if ordering == "builtin" else ordm.identity_ordering(R.K.nblocks)
+    plan = symbolic.symbolic_factor(g, order, R.K.sizes)
+    t3 = tick()
+    F = factor.block_ldlt(R.K, plan)
+    t4 = tick()
+    lam = factor.block_solve(F, R.g)
+    t5 = tick()
+    sol = np.asarray(subdomain.recover_primal(systems, lam))
+    t6 = tick()
+    t.update(front_end=t1 - t0, reduce=t2 - t1, assemble_symbolic=t3 - t2, factor=t4 - t3, solve=t5 - t4,
+             recover=t6 - t5, d3m_total=t6 - t1)
+    if timers is not None:
+        timers.update(t)
+    return sol, systems, R, plan, F
+
+
+def global_residual(model: FemModel, sol: np.ndarray, rhs: int = 0) -> float:
+    """||A x - f||_inf / ||f||_inf of the monolithic system (subdomain.py:240-250)."""
+    A, f = assemble_global(model)
+    fr = f[:, rhs]
+    return float(np.abs(A @ sol - fr).max() / np.abs(fr).max())

@@ -173,3 +173,33 @@ def test_large_subdomain_panel_bk_vs_oracle(cuda, oracle, n, m, batch):
         X = s.factor.solve(B)
         Xo = fo.solve(B)
         assert np.linalg.norm(X - Xo) <= 1e-10 * np.linalg.norm(Xo)
+
+
+@pytest.mark.parametrize("cells,parts,radius", [(4, (2, 2, 2), 0.15), (8, (2, 1, 1), 0.0)])
+def test_fem3d_pipeline_vs_monolithic(cuda, cells, parts, radius):
+    """Full GPU D3M pipeline on the 3-D Nedelec problems (config 1 is the
+    (8, 2x1x1) case, n = 2196 per subdomain -> panel BK path) against the
+    monolithic sparse solve (test_subdomain.py:277-289 criteria)."""
+    import scipy.sparse.linalg as spla
+    from paper_2002_05018_b200 import fem3d
+    model = fem3d.build_model(fem3d.FemProblem(cells, 0.5, parts, sphere_radius=radius))
+    A, f = fem3d.assemble_global(model)
+    u = spla.spsolve(A.tocsc(), f[:, 0])
+    sol, systems, R, plan, F = fem3d.solve_d3m(model)
+    assert np.linalg.norm(sol - u) / np.linalg.norm(u) <= 1e-8
+    assert fem3d.global_residual(model, sol) <= 1e-10
+
+
+@pytest.mark.slow
+def test_fem3d_config2_vs_monolithic(cuda):
+    """BASELINE configs[1]: 16^3 x 6 tets (31,024 edges), eps_r = 4 sphere,
+    2x2x2 subdomains of 4,184 edges, lambda = 2,448."""
+    import scipy.sparse.linalg as spla
+    from paper_2002_05018_b200 import fem3d
+    model = fem3d.build_model(fem3d.config2())
+    sol, systems, R, plan, F = fem3d.solve_d3m(model)
+    assert R.n_lambda == 2448
+    A, f = fem3d.assemble_global(model)
+    u = spla.spsolve(A.tocsc(), f[:, 0])
+    assert np.linalg.norm(sol - u) / np.linalg.norm(u) <= 1e-8
+    assert fem3d.global_residual(model, sol) <= 1e-10
