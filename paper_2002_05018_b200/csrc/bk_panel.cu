@@ -15,6 +15,7 @@
 // within rounding of its threshold (measured margins >= 1.3e-4 on config 3);
 // growth is reported per panel (per-step geometric mean of the trailing-max
 // ratio), as for bk_blocked.cu.
+#include <algorithm>
 #include "d3m_common.cuh"
 #include "d3m_gemm.h"
 #include "d3m_kernels.h"
@@ -55,70 +56,149 @@ __device__ __forceinline__ void pargmax_red(double& v, int& idx, double* vs, int
   __syncthreads();
 }
 
-// ---- prologue: numpy scale / symmetry check (factor.py:94-98), state -----
-__global__ void __launch_bounds__(PNL_NT) bk_panel_init_kernel(BkArgs a, BkState* st) {
-  __shared__ double red[PNL_NT / 32];
-  const int b = blockIdx.x, n = a.n, lda = a.lda, tid = threadIdx.x;
+
+// ---- prologue scan, tiled over many CTAs: per matrix b, atomic maxima of
+//   pass 0: proxies |W|^2 (full), |W - W^T|^2 (i>j), trailing |W|^2 (i>=j)
+//   pass 1: exact numpy-abs scale / asym for entries within 1e-14 of the proxies
+// 32x32 tile pairs (ti >= tj) are staged through shared memory so both the
+// tile and its transpose are read row-wise (coalesced).
+__device__ __forceinline__ void atomic_max_pos(unsigned long long* p, double v) {
+  atomicMax(p, (unsigned long long)__double_as_longlong(v));
+}
+__device__ __forceinline__ double as_pos(unsigned long long u) { return __longlong_as_double((long long)u); }
+
+__global__ void __launch_bounds__(256) bk_scan_kernel(BkArgs a, unsigned long long* red, int pass) {
+  __shared__ cplx Ta[32][33], Tb[32][33];
+  __shared__ double wred[8][3];
+  const int b = blockIdx.y, n = a.n, lda = a.lda;
   const cplx* W = a.W + (int64_t)b * a.stride_w;
-  for (int i = tid; i < n; i += PNL_NT) { a.perm[(int64_t)b * n + i] = i; a.tags[(int64_t)b * n + i] = 0; }
-  const int lane = tid & 31, wid = tid >> 5;
-  double p_all = 0.0, p_asy = 0.0, tm2 = 0.0;
-  for (int i = wid; i < n; i += PNL_NT / 32)
-    for (int jb = 0; jb <= i; jb += 256) {
-      cplx z[8], zt[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = jb + lane + 32 * u;
-        if (j <= i) { z[u] = W[(int64_t)i * lda + j]; zt[u] = W[(int64_t)j * lda + i]; }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = jb + lane + 32 * u;
-        if (j <= i) {
-          const double q = x_abs2(z[u]);
-          p_all = fmax(p_all, fmax(q, x_abs2(zt[u])));
-          tm2 = fmax(tm2, q);
-          if (a.check_sym && j < i) p_asy = fmax(p_asy, x_abs2(x_sub(z[u], zt[u])));
+  unsigned long long* rb = red + 8 * b;      // [p_all, p_asy, tm2, scale, asym]
+  const int nt = (n + 31) / 32;
+  const int ntile = nt * (nt + 1) / 2;
+  const double ta = pass ? as_pos(rb[0]) * (1.0 - 1e-14) : 0.0;
+  const double tb = pass ? as_pos(rb[1]) * (1.0 - 1e-14) : 0.0;
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+    int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    while (ti * (ti + 1) / 2 > t) --ti;
+    const int tj = t - ti * (ti + 1) / 2;
+    for (int r = ty; r < 32; r += 8) {
+      const int i = ti * 32 + r, j = tj * 32 + tx;
+      Ta[r][tx] = (i < n && j < n) ? W[(int64_t)i * lda + j] : mk(0.0, 0.0);        // block (ti, tj)
+      const int i2 = tj * 32 + r, j2 = ti * 32 + tx;
+      Tb[r][tx] = (i2 < n && j2 < n) ? W[(int64_t)i2 * lda + j2] : mk(0.0, 0.0);    // block (tj, ti)
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const int i = ti * 32 + r, j = tj * 32 + tx;
+      if (i >= n || j >= n || j > i) continue;
+      const cplx z = Ta[r][tx], zt = Tb[tx][r];     // W[i][j], W[j][i]
+      if (pass == 0) {
+        const double q = x_abs2(z);
+        v0 = fmax(v0, fmax(q, x_abs2(zt)));
+        v2 = fmax(v2, q);
+        if (a.check_sym && j < i) v1 = fmax(v1, x_abs2(x_sub(z, zt)));
+      } else {
+        if (x_abs2(z) >= ta) v0 = fmax(v0, np_abs(z));
+        if (x_abs2(zt) >= ta) v0 = fmax(v0, np_abs(zt));
+        if (a.check_sym && j < i) {
+          const cplx dz = x_sub(z, zt);
+          if (x_abs2(dz) >= tb) v1 = fmax(v1, np_abs(dz));
         }
       }
     }
-  p_all = pmax_red<PNL_NT>(p_all, red);
-  p_asy = pmax_red<PNL_NT>(p_asy, red);
-  tm2 = pmax_red<PNL_NT>(tm2, red);
-  const double ta = p_all * (1.0 - 1e-14), tb = p_asy * (1.0 - 1e-14);
-  double scale = 0.0, asym = 0.0;
-  for (int i = wid; i < n; i += PNL_NT / 32)
-    for (int jb = 0; jb <= i; jb += 256) {
+    __syncthreads();
+  }
+  v0 = warp_max(v0);
+  v1 = warp_max(v1);
+  v2 = warp_max(v2);
+  if (tx == 0) { wred[ty][0] = v0; wred[ty][1] = v1; wred[ty][2] = v2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) { v0 = fmax(v0, wred[w][0]); v1 = fmax(v1, wred[w][1]); v2 = fmax(v2, wred[w][2]); }
+    if (pass == 0) { atomic_max_pos(rb + 0, v0); atomic_max_pos(rb + 1, v1); atomic_max_pos(rb + 2, v2); }
+    else { atomic_max_pos(rb + 3, v0); atomic_max_pos(rb + 4, v1); }
+  }
+}
+
+__global__ void bk_panel_state_kernel(BkArgs a, BkState* st, const unsigned long long* red, int batch) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const unsigned long long* rb = red + 8 * b;
+  const double scale = as_pos(rb[3]), asym = as_pos(rb[4]);
+  BkState s{};
+  s.k = 0;
+  s.info = (a.check_sym && a.n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) ? -2 : -1;
+  s.trail_max = sqrt(as_pos(rb[2]));
+  s.growth = 1.0;
+  s.tol_abs = __dmul_rn(a.pivot_tol, scale);
+  s.scale = scale;
+  s.asym = asym;
+  st[b] = s;
+  a.scale[b] = scale;
+  a.asym[b] = asym;
+}
+
+__global__ void bk_perm_init_kernel(BkArgs a, int batch) {
+  const int64_t total = (int64_t)batch * a.n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    a.perm[e] = e % a.n;
+    a.tags[e] = 0;
+  }
+}
+
+// Up-to-date column of the panel step: for every row i >= r_lo
+//   out[i] = base(i) - sum_{c < kw} G(i, k0 + c) * Wp[src][c]
+// with 4 lanes per row (each 4 of the <= 16 panel columns, independent loads)
+// and two rows per lane group in flight; base(i) is G(i, col) for i >= col
+// (stale column) or G(col, i) for i < col (its row part), col = the target
+// column.  Returns nothing; the caller reduces its own proxies afterwards.
+template <int NB>
+__device__ __forceinline__ void panel_gemv(const cplx* W, int lda, int n, int k0, int kw, int col, int r_lo,
+                                           const cplx* Wp, int src, cplx* out_col /* Wp + kwcol, stride NB+1 */) {
+  constexpr int LDW = NB + 1;
+  const int sub = threadIdx.x & 3;
+  const int rstride = PNL_NT / 4;
+  cplx xs[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = jb + lane + 32 * u;
-        if (j <= i) {
-          const cplx z = W[(int64_t)i * lda + j], zt = W[(int64_t)j * lda + i];
-          if (x_abs2(z) >= ta) scale = fmax(scale, np_abs(z));
-          if (x_abs2(zt) >= ta) scale = fmax(scale, np_abs(zt));
-          if (a.check_sym && j < i) {
-            const cplx dz = x_sub(z, zt);
-            if (x_abs2(dz) >= tb) asym = fmax(asym, np_abs(dz));
-          }
-        }
-      }
+  for (int q = 0; q < 4; ++q) {
+    const int c = sub + 4 * q;
+    xs[q] = c < kw ? Wp[(int64_t)src * LDW + c] : mk(0.0, 0.0);
+  }
+  // warp-uniform trip count: the shuffles below need all 32 lanes
+  for (int base = r_lo; base < n; base += 2 * rstride) {
+    const int ia = base + (threadIdx.x >> 2), ib = ia + rstride;
+    const bool va = ia < n, vb = ib < n;
+    cplx la[4], lb[4], ba = mk(0.0, 0.0), bb = mk(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = sub + 4 * q;
+      la[q] = (c < kw && va) ? W[(int64_t)ia * lda + k0 + c] : mk(0.0, 0.0);
+      lb[q] = (c < kw && vb) ? W[(int64_t)ib * lda + k0 + c] : mk(0.0, 0.0);
     }
-  scale = pmax_red<PNL_NT>(scale, red);
-  asym = pmax_red<PNL_NT>(asym, red);
-  if (tid == 0) {
-    BkState s{};
-    s.k = 0;
-    s.info = (a.check_sym && n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) ? -2 : -1;
-    s.n2x2 = 0;
-    s.npiv_last = 0;
-    s.trail_max = sqrt(tm2);
-    s.growth = 1.0;
-    s.tol_abs = __dmul_rn(a.pivot_tol, scale);
-    s.scale = scale;
-    s.asym = asym;
-    st[b] = s;
-    a.scale[b] = scale;
-    a.asym[b] = asym;
+    if (sub == 0) {
+      if (va) ba = ia >= col ? W[(int64_t)ia * lda + col] : W[(int64_t)col * lda + ia];
+      if (vb) bb = ib >= col ? W[(int64_t)ib * lda + col] : W[(int64_t)col * lda + ib];
+    }
+    cplx sa = mk(0.0, 0.0), sb = mk(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      c_fma(sa, la[q], xs[q]);
+      c_fma(sb, lb[q], xs[q]);
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      sa.x += __shfl_xor_sync(0xffffffffu, sa.x, o);
+      sa.y += __shfl_xor_sync(0xffffffffu, sa.y, o);
+      sb.x += __shfl_xor_sync(0xffffffffu, sb.x, o);
+      sb.y += __shfl_xor_sync(0xffffffffu, sb.y, o);
+    }
+    if (sub == 0) {
+      if (va) out_col[(int64_t)ia * LDW] = c_sub(ba, sa);
+      if (vb) out_col[(int64_t)ib * LDW] = c_sub(bb, sb);
+    }
   }
 }
 
@@ -155,21 +235,13 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
   const int k0 = s.k;
   int k = k0, kw = 0, npiv = 0, info = -1, n2x2 = s.n2x2;
   while (kw < NB && k < n) {
-    // -- A+B: column k up to date into Wp[:, kw], fused |z|^2-proxy argmax
+    // -- A: column k up to date into Wp[:, kw] (4 lanes per row), then the
+    //    |z|^2-proxy argmax below the diagonal
+    panel_gemv<NB>(W, lda, n, k0, kw, k, k, Wp, k, Wp + kw);
+    __syncthreads();
     double pv = -1.0;
     int pi = 0x7fffffff;
-    for (int i = k + tid; i < n; i += PNL_NT) {
-      cplx acc = G(i, k), acc2 = mk(0.0, 0.0);
-      int c = 0;
-      for (; c + 1 < kw; c += 2) {
-        c_fms(acc, G(i, k0 + c), Wp[(int64_t)k * LDW + c]);
-        c_fms(acc2, G(i, k0 + c + 1), Wp[(int64_t)k * LDW + c + 1]);
-      }
-      if (c < kw) c_fms(acc, G(i, k0 + c), Wp[(int64_t)k * LDW + c]);
-      acc = c_add(acc, acc2);
-      Wp[(int64_t)i * LDW + kw] = acc;
-      if (i > k) argmax_merge(pv, pi, x_abs2(acc), i);
-    }
+    for (int i = k + 1 + tid; i < n; i += PNL_NT) argmax_merge(pv, pi, x_abs2(Wp[(int64_t)i * LDW + kw]), i);
     pargmax_red<PNL_NT>(pv, pi, ra, rai);
     const double absakk = x_abs(Wp[(int64_t)k * LDW + kw]);
     double colmax = 0.0;
@@ -194,21 +266,14 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
     if (fmax(absakk, colmax) <= s.tol_abs) { info = k; break; }
     int kstep = 1, kp = k;
     if (!(absakk >= __dmul_rn(kAlphaP, colmax))) {
-      // -- C: column imax up to date into Wp[:, kw+1], fused rowmax proxy
+      // -- C: column imax up to date into Wp[:, kw+1] (4 lanes per row), then
+      //    the rowmax proxy argmax (the diagonal entry imax excluded)
+      panel_gemv<NB>(W, lda, n, k0, kw, imax, k, Wp, imax, Wp + kw + 1);
+      __syncthreads();
       double rpv = -1.0;
       int rpi = 0x7fffffff;
-      for (int i = k + tid; i < n; i += PNL_NT) {
-        cplx acc = i < imax ? G(imax, i) : G(i, imax), acc2 = mk(0.0, 0.0);
-        int c = 0;
-        for (; c + 1 < kw; c += 2) {
-          c_fms(acc, G(i, k0 + c), Wp[(int64_t)imax * LDW + c]);
-          c_fms(acc2, G(i, k0 + c + 1), Wp[(int64_t)imax * LDW + c + 1]);
-        }
-        if (c < kw) c_fms(acc, G(i, k0 + c), Wp[(int64_t)imax * LDW + c]);
-        acc = c_add(acc, acc2);
-        Wp[(int64_t)i * LDW + kw + 1] = acc;
-        if (i != imax) argmax_merge(rpv, rpi, x_abs2(acc), i);
-      }
+      for (int i = k + tid; i < n; i += PNL_NT)
+        if (i != imax) argmax_merge(rpv, rpi, x_abs2(Wp[(int64_t)i * LDW + kw + 1]), i);
       pargmax_red<PNL_NT>(rpv, rpi, ra, rai);
       const double rthr = rpv * (1.0 - 1e-14);
       int ramb = 0;
@@ -353,7 +418,15 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
   GemmTask* tasks = reinterpret_cast<GemmTask*>(w);
   w += (size_t)batch * sizeof(GemmTask);
   unsigned long long* tmax = reinterpret_cast<unsigned long long*>(w);
-  bk_panel_init_kernel<<<batch, PNL_NT, 0, s>>>(*a, st);
+  w += (size_t)batch * sizeof(unsigned long long);
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(w);
+  cudaMemsetAsync(red, 0, (size_t)batch * 8 * sizeof(unsigned long long), s);
+  const int nt = (n + 31) / 32, ntile = nt * (nt + 1) / 2;
+  const dim3 sgrid(std::min(ntile, 256), batch);
+  bk_perm_init_kernel<<<std::min((batch * n + 255) / 256, 4096), 256, 0, s>>>(*a, batch);
+  bk_scan_kernel<<<sgrid, 256, 0, s>>>(*a, red, 0);
+  bk_scan_kernel<<<sgrid, 256, 0, s>>>(*a, red, 1);
+  bk_panel_state_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, red, batch);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
   for (int p = 0; p * NB < n; ++p) {
@@ -372,5 +445,5 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
 }
 
 extern "C" size_t d3m_bk_panel_workspace_bytes(int n, int batch) {
-  return (size_t)batch * ((size_t)n * 17 * 16 + 64 + 64 + 8) + 256;
+  return (size_t)batch * ((size_t)n * 17 * 16 + 64 + 64 + 8 + 64) + 256;
 }

@@ -324,10 +324,16 @@ def assemble_global(model: FemModel):
     return A, model.f
 
 
-def subdomain_systems(model: FemModel, rhs: int = 0):
-    """Per-domain dense systems (subdomain.py:124-163 analog) for RHS column
-    ``rhs``; returns SubdomainSystem objects of the hot-path API."""
-    from .subdomain import Coupling, SubdomainSystem, interface_lambda_nodes
+def subdomain_systems(model: FemModel, rhs: int = 0, sparse: bool = True):
+    """Per-domain systems (subdomain.py:124-163 analog) for RHS column
+    ``rhs``; returns SubdomainSystem objects of the hot-path API.
+
+    With ``sparse`` (default) A_d and the coupling blocks D are SparseBlock
+    objects: the same additions as the dense assembly (np.add.at in element
+    order, then the boundary terms, then A[rows, rows] += s*alpha*M_Gamma),
+    performed on the compressed entry array, so ``np.asarray(A)`` equals the
+    dense assembly bit for bit."""
+    from .subdomain import Coupling, SparseBlock, SubdomainSystem, interface_lambda_nodes
     mesh = model.mesh
     kept = interface_lambda_nodes(model)
     systems = []
@@ -337,35 +343,63 @@ def subdomain_systems(model: FemModel, rhs: int = 0):
         g2l = np.full(mesh.n_edges, -1, dtype=np.int64)
         g2l[loc] = np.arange(loc.size)
         n = loc.size
-        A = np.zeros((n, n), dtype=np.complex128)
         le = g2l[mesh.tet_edges[tsel]]
-        np.add.at(A, (np.repeat(le, 6, axis=1).ravel(), np.tile(le, (1, 6)).ravel()), model.Ae[tsel].ravel())
+        k_e = (np.repeat(le, 6, axis=1) * n + np.tile(le, (1, 6))).ravel()
         bsel = np.flatnonzero(model.dom_of_tet[model.bnd_owner] == d)
+        k_b = np.zeros(0, np.int64)
         if bsel.size:
             lb = g2l[model.bnd_edges[bsel]]
-            np.add.at(A, (np.repeat(lb, 3, axis=1).ravel(), np.tile(lb, (1, 3)).ravel()), model.bnd_B[bsel].ravel())
-        couplings = []
+            k_b = (np.repeat(lb, 3, axis=1) * n + np.tile(lb, (1, 3))).ravel()
+        itfs = []
         for i_itf in model.incident_interfaces(d):
             itf = model.interfaces[i_itf]
             s = 1 if itf.dom_lo == d else -1
             nodes = itf.nodes
             pos = np.full(mesh.n_edges, -1, dtype=np.int64)
             pos[nodes] = np.arange(nodes.size)
-            te = model.itf_tri_edges[i_itf]
+            li = pos[model.itf_tri_edges[i_itf]]
             Mg = np.zeros((nodes.size, nodes.size))
-            li = pos[te]
             np.add.at(Mg, (np.repeat(li, 3, axis=1).ravel(), np.tile(li, (1, 3)).ravel()), model.itf_M[i_itf].ravel())
+            itfs.append((i_itf, s, nodes, pos, Mg))
+        if sparse:
+            k_m = [(g2l[nodes][:, None] * n + g2l[nodes][None, :])[Mg != 0] for _, _, nodes, _, Mg in itfs]
+            keys = np.unique(np.concatenate([k_e, k_b] + k_m))
+            vals = np.zeros(keys.size, dtype=np.complex128)
+            np.add.at(vals, np.searchsorted(keys, k_e), model.Ae[tsel].ravel())
+            if bsel.size:
+                np.add.at(vals, np.searchsorted(keys, k_b), model.bnd_B[bsel].ravel())
+        else:
+            A = np.zeros((n, n), dtype=np.complex128)
+            np.add.at(A.reshape(-1), k_e, model.Ae[tsel].ravel())
+            if bsel.size:
+                np.add.at(A.reshape(-1), k_b, model.bnd_B[bsel].ravel())
+        couplings = []
+        for i_itf, s, nodes, pos, Mg in itfs:
             rows = g2l[nodes]
-            A[np.ix_(rows, rows)] += (s * model.prob.alpha) * Mg
+            blk = (s * model.prob.alpha) * Mg
+            if sparse:
+                kb = (rows[:, None] * n + rows[None, :]).ravel()
+                p = np.minimum(np.searchsorted(keys, kb), keys.size - 1)
+                hit = keys[p] == kb
+                vals[p[hit]] += blk.ravel()[hit]
+            else:
+                A[np.ix_(rows, rows)] += blk
             cols = pos[kept[i_itf]]
-            D = np.zeros((n, cols.size), dtype=np.complex128)
-            if cols.size:
-                D[rows[:, None], np.arange(cols.size)[None, :]] = s * Mg[:, cols]
+            Dv = s * Mg[:, cols]
+            if sparse:
+                kd = (rows[:, None] * cols.size + np.arange(cols.size)[None, :]).ravel()
+                o = np.argsort(kd, kind="stable")
+                D = SparseBlock((n, cols.size), kd[o], Dv.ravel().astype(np.complex128)[o])
+            else:
+                D = np.zeros((n, cols.size), dtype=np.complex128)
+                if cols.size:
+                    D[rows[:, None], np.arange(cols.size)[None, :]] = Dv
             couplings.append(Coupling(i_itf, D, s))
         fd = np.zeros(n, dtype=np.complex128)          # load of the domain's own boundary faces
         if bsel.size:
             np.add.at(fd, g2l[model.bnd_edges[bsel]].ravel(), model.bnd_f[bsel, :, rhs].ravel())
-        systems.append(SubdomainSystem(d, A, fd, loc, couplings))
+        Ad = SparseBlock((n, n), keys, vals) if sparse else A
+        systems.append(SubdomainSystem(d, Ad, fd, loc, couplings))
     return systems
 
 

@@ -100,7 +100,58 @@ def interface_lambda_nodes(part) -> list[np.ndarray]:
             for k, itf in enumerate(part.interfaces)]
 
 
-def _coupling_matrix(sys: SubdomainSystem) -> np.ndarray:
+class SparseBlock:
+    """A dense subdomain block (A_d or D_d) carried as unique-key COO.
+
+    FEM subdomain matrices have ~30 nonzeros per row, so shipping the dense
+    n x n array costs ~n/30 times more host->device traffic than the entries.
+    ``keys`` are row-major positions r * ncols + c (unique, ascending), and
+    ``vals`` the exact dense values at those positions (every other entry is
+    +0.0); ``np.asarray`` gives the dense array of the reference API
+    (subdomain.py:124-163 builds dense A_d / D_d), and reduce_domains
+    densifies on the device with one scatter, bit-identical to uploading the
+    dense array."""
+
+    ndim = 2
+    dtype = np.dtype(np.complex128)
+
+    def __init__(self, shape, keys, vals):
+        self.shape = (int(shape[0]), int(shape[1]))
+        self.keys = np.ascontiguousarray(keys, dtype=np.int64)
+        self.vals = np.ascontiguousarray(vals, dtype=np.complex128)
+
+    def toarray(self) -> np.ndarray:
+        out = np.zeros(self.shape, dtype=np.complex128)
+        out.reshape(-1)[self.keys] = self.vals
+        return out
+
+    def __array__(self, dtype=None, copy=None):
+        a = self.toarray()
+        return a if dtype is None else a.astype(dtype)
+
+    @property
+    def T(self) -> np.ndarray:
+        return self.toarray().T
+
+    @staticmethod
+    def hconcat(blocks) -> "SparseBlock":
+        n = blocks[0].shape[0]
+        m = sum(b.shape[1] for b in blocks)
+        keys, vals, off = [], [], 0
+        for b in blocks:
+            r, c = np.divmod(b.keys, max(b.shape[1], 1))
+            keys.append(r * m + off + c)
+            vals.append(b.vals)
+            off += b.shape[1]
+        k = np.concatenate(keys) if keys else np.zeros(0, np.int64)
+        v = np.concatenate(vals) if vals else np.zeros(0, np.complex128)
+        o = np.argsort(k, kind="stable")
+        return SparseBlock((n, m), k[o], v[o])
+
+
+def _coupling_matrix(sys: SubdomainSystem):
+    if sys.couplings and all(isinstance(c.D, SparseBlock) for c in sys.couplings):
+        return SparseBlock.hconcat([c.D for c in sys.couplings])
     if sys.couplings:
         return np.concatenate([np.asarray(c.D, dtype=np.complex128) for c in sys.couplings], axis=1)
     return np.zeros((sys.n_dofs, 0), dtype=np.complex128)
@@ -112,28 +163,32 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
     D^T X on DMMA -> symmetrisation).  Returns [(K_D, g_d)] as DeviceArrays
     and caches each factor on its system, like subdomain.py:166-184."""
     t = require_cuda()
-    groups: dict[tuple[int, int], list[int]] = {}
-    shapes = []
+    # one batch per subdomain order n (the factorisation does not depend on
+    # m); coupling blocks are zero-padded to the group's largest m and each
+    # domain's K_D / g_d is the leading m x m / m view of its padded result
+    groups: dict[int, list[int]] = {}
+    ms = []
     for idx, s in enumerate(systems):
         n = int(np.shape(s.A)[0]) if not isinstance(s.A, DeviceArray) else s.A.shape[0]
-        m = sum(int(np.shape(c.D)[1]) for c in s.couplings)
-        shapes.append((n, m))
-        groups.setdefault((n, m), []).append(idx)
+        ms.append(sum(int(np.shape(c.D)[1]) for c in s.couplings))
+        groups.setdefault(n, []).append(idx)
     out = [None] * len(systems)
     first_error = None
-    for (n, m), members in groups.items():
+    for n, members in groups.items():
+        m = max(ms[i] for i in members)
         B = len(members)
         A = empty((B, n, n))
-        D = empty((B, n, m))
+        D = t.zeros((B, n, m), dtype=t.complex128, device="cuda")
         f = empty((B, n))
         for r, idx in enumerate(members):
             s = systems[idx]
+            mr = ms[idx]
             _fill(A[r], s.A, (n, n))
-            if m:
+            if mr:
                 if _dev_D(s):
-                    D[r].copy_(s._d3m_D)
+                    D[r, :, :mr].copy_(s._d3m_D)
                 else:
-                    _fill(D[r], _coupling_matrix(s), (n, m))
+                    _fill(D[r, :, :mr], _coupling_matrix(s), (n, mr))
             _fill(f[r], s.f, (n,))
         perm = t.empty((B, n), dtype=t.int64, device="cuda")
         tags = t.empty((B, n), dtype=t.int8, device="cuda")
@@ -168,9 +223,10 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
             continue
         for r, idx in enumerate(members):
             s = systems[idx]
+            mr = ms[idx]
             s.factor = facs[r]
-            s._d3m_D = D[r]
-            out[idx] = (DeviceArray(K[r]), DeviceArray(g[r]))
+            s._d3m_D = D[r, :, :mr]
+            out[idx] = (DeviceArray(K[r, :mr, :mr]), DeviceArray(g[r, :mr]))
     if first_error is not None:
         raise first_error[1]
     return out
@@ -180,6 +236,14 @@ def _fill(dst, src, shape):
     """Copy a host array or device handle into a device slice (one H2D copy
     straight from the numpy buffer for host inputs)."""
     t = require_cuda()
+    if isinstance(src, SparseBlock):
+        assert tuple(src.shape) == tuple(shape)
+        dst.zero_()
+        if src.keys.size:
+            k = t.from_numpy(src.keys).to("cuda", non_blocking=False)
+            v = t.from_numpy(src.vals).to("cuda", non_blocking=False)
+            dst[k // shape[1], k % shape[1]] = v
+        return
     if isinstance(src, DeviceArray) or type(src).__module__.startswith("torch"):
         dst.copy_(to_device(src).reshape(shape))
     else:
@@ -278,7 +342,7 @@ def _assemble_device(contrib, gcontrib, sizes):
         for r, (KD, oa, ob) in enumerate(lst):
             base, st, o = src_of(KD)
             bases[base] = st
-            ld = int(KD.shape[1])
+            ld = int(KD.tensor.stride(0))
             rounds.setdefault((r, base, "K"), []).append(
                 (o + oa * ld + ob, koff[key], int(sizes[ia]), int(sizes[ib]), ld, int(sizes[ib]), 0,
                  _lib.COPY_STORE if r == 0 else _lib.COPY_ADD))

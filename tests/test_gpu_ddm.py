@@ -99,11 +99,11 @@ def test_lambda_vs_dense_saddle_solve(cuda):
     rhs = np.zeros(npr + nl, dtype=complex)
     for k, s in enumerate(systems):
         sl = slice(doff[k], doff[k + 1])
-        S[sl, sl] = s.A
+        S[sl, sl] = np.asarray(s.A)
         rhs[sl] = s.f
         for c in s.couplings:
             cl = slice(npr + off[c.interface], npr + off[c.interface + 1])
-            S[sl, cl] = c.D
+            S[sl, cl] = np.asarray(c.D)
             S[cl, sl] = c.D.T
     x = np.linalg.solve(S, rhs)
     lam_c = np.concatenate([np.asarray(v) for v in lam])
