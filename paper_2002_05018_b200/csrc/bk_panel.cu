@@ -16,13 +16,17 @@
 // growth is reported per panel (per-step geometric mean of the trailing-max
 // ratio), as for bk_blocked.cu.
 #include <algorithm>
+#include <cstdlib>
+#include <cooperative_groups.h>
 #include "d3m_common.cuh"
 #include "d3m_gemm.h"
 #include "d3m_kernels.h"
 
 namespace d3m {
+namespace cg = cooperative_groups;
 
-constexpr int PNL_NT = 1024;
+constexpr int PNL_NT = 1024;   // prologue / legacy
+constexpr int CNT = 512;       // threads per panel CTA
 constexpr double kAlphaP = 0.6403882032022076;
 
 struct BkState {          // 64 bytes per matrix
@@ -149,18 +153,18 @@ __global__ void bk_perm_init_kernel(BkArgs a, int batch) {
   }
 }
 
-// Up-to-date column of the panel step: for every row i >= r_lo
+// Up-to-date column of the panel step over the rows [r_lo, r_hi) this CTA owns:
 //   out[i] = base(i) - sum_{c < kw} G(i, k0 + c) * Wp[src][c]
 // with 4 lanes per row (each 4 of the <= 16 panel columns, independent loads)
 // and two rows per lane group in flight; base(i) is G(i, col) for i >= col
 // (stale column) or G(col, i) for i < col (its row part), col = the target
-// column.  Returns nothing; the caller reduces its own proxies afterwards.
-template <int NB>
-__device__ __forceinline__ void panel_gemv(const cplx* W, int lda, int n, int k0, int kw, int col, int r_lo,
+// column.  The summation order per row is fixed (4 partial sums, butterfly).
+template <int NB, int NT>
+__device__ __forceinline__ void panel_gemv(const cplx* W, int lda, int r_lo, int r_hi, int k0, int kw, int col,
                                            const cplx* Wp, int src, cplx* out_col /* Wp + kwcol, stride NB+1 */) {
   constexpr int LDW = NB + 1;
   const int sub = threadIdx.x & 3;
-  const int rstride = PNL_NT / 4;
+  constexpr int rstride = NT / 4;
   cplx xs[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -168,9 +172,9 @@ __device__ __forceinline__ void panel_gemv(const cplx* W, int lda, int n, int k0
     xs[q] = c < kw ? Wp[(int64_t)src * LDW + c] : mk(0.0, 0.0);
   }
   // warp-uniform trip count: the shuffles below need all 32 lanes
-  for (int base = r_lo; base < n; base += 2 * rstride) {
+  for (int base = r_lo; base < r_hi; base += 2 * rstride) {
     const int ia = base + (threadIdx.x >> 2), ib = ia + rstride;
-    const bool va = ia < n, vb = ib < n;
+    const bool va = ia < r_hi, vb = ib < r_hi;
     cplx la[4], lb[4], ba = mk(0.0, 0.0), bb = mk(0.0, 0.0);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -202,14 +206,93 @@ __device__ __forceinline__ void panel_gemv(const cplx* W, int lda, int n, int k0
   }
 }
 
-// ---- one panel of up to NB (+1) columns per matrix ----------------------
-template <int NB>
-__global__ void __launch_bounds__(PNL_NT)
+// Exact modulus argmax (glibc hypot, first index) of col[i] over this CTA's
+// rows i in [r0, r1), i != skip.  The |z|^2 proxy selects the candidates
+// (within 1e-14 of the local proxy max); the union of all CTAs' local
+// candidate sets contains every global maximiser, so merging the local exact
+// results with argmax_merge gives the reference's np.argmax(abs(...)).
+// Returns ev = -1, ei = INT_MAX for an empty range.
+template <int NT>
+__device__ __forceinline__ void local_exact_argmax(const cplx* col, int ldw, int r0, int r1, int skip, double& ev,
+                                                   int& ei, double* vs, int* is) {
+  double pv = -1.0;
+  int pi = 0x7fffffff;
+  for (int i = r0 + (int)threadIdx.x; i < r1; i += NT)
+    if (i != skip) argmax_merge(pv, pi, x_abs2(col[(int64_t)i * ldw]), i);
+  pargmax_red<NT>(pv, pi, vs, is);
+  if (pi == 0x7fffffff) { ev = -1.0; ei = pi; return; }
+  const double thr = pv * (1.0 - 1e-14);
+  int amb = 0;
+  for (int i = r0 + (int)threadIdx.x; i < r1; i += NT)
+    amb |= (i != skip && i != pi && x_abs2(col[(int64_t)i * ldw]) >= thr);
+  if (__syncthreads_or(amb)) {
+    double v = -1.0;
+    int vi = 0x7fffffff;
+    for (int i = r0 + (int)threadIdx.x; i < r1; i += NT) {
+      if (i == skip) continue;
+      const cplx z = col[(int64_t)i * ldw];
+      if (x_abs2(z) >= thr) argmax_merge(v, vi, x_abs(z), i);
+    }
+    pargmax_red<NT>(v, vi, vs, is);
+    ev = v;
+    ei = vi;
+  } else {
+    ev = x_abs(col[(int64_t)pi * ldw]);
+    ei = pi;
+  }
+}
+
+struct ClSlot {       // one CTA's contribution to a cluster-wide pivot search
+  double ev;          // local exact max over the local candidates (-1: none)
+  double own;         // modulus of the published diagonal-ish entry (-1: not owned)
+  int ei;             // first index of ev
+  int pad;
+};
+
+// Gather the CS slots (DSMEM) after a cluster barrier; every CTA merges in the
+// same order, so all CTAs hold bitwise-identical decisions.
+template <int CS>
+__device__ __forceinline__ ClSlot cl_merge(cg::cluster_group& cl, ClSlot* slot, ClSlot* out) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double ev = -1.0, own = -1.0;
+    int ei = 0x7fffffff;
+    if (lane < CS) {
+      const ClSlot* p = cl.map_shared_rank(slot, lane);
+      ev = p->ev;
+      own = p->own;
+      ei = p->ei;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ev2 = __shfl_xor_sync(0xffffffffu, ev, o);
+      const int ei2 = __shfl_xor_sync(0xffffffffu, ei, o);
+      own = fmax(own, __shfl_xor_sync(0xffffffffu, own, o));
+      argmax_merge(ev, ei, ev2, ei2);
+    }
+    if (lane == 0) { out->ev = ev; out->own = own; out->ei = ei; }
+  }
+  __syncthreads();
+  return *out;
+}
+
+// ---- one panel of up to NB (+1) columns per matrix, CS CTAs per matrix -----
+// The cluster's CTAs own contiguous slices of the active rows [k0, n) and run
+// the column updates, proxy scans and the L-column store for their rows;
+// pivot searches meet in one cluster barrier each (DSMEM slots, double
+// buffered), and the symmetric interchange (global memory, any thread of the
+// cluster) is fenced by one more barrier when it moves data.
+template <int NB, int CS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(CNT)
 bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned long long* tmax, int maxtiles) {
-  __shared__ double ra[PNL_NT / 32], rb[PNL_NT / 32];
-  __shared__ int rai[PNL_NT / 32];
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double ra[CNT / 32];
+  __shared__ int rai[CNT / 32];
+  __shared__ ClSlot slots[2], merged;
   constexpr int LDW = NB + 1;
-  const int b = blockIdx.x, n = a.n, lda = a.lda, tid = threadIdx.x;
+  const int rank = (int)cl.block_rank();
+  const int b = blockIdx.x / CS, n = a.n, lda = a.lda, tid = threadIdx.x;
+  const bool lead = rank == 0 && tid == 0;
   cplx* W = a.W + (int64_t)b * a.stride_w;
   int64_t* perm = a.perm + (int64_t)b * n;
   int8_t* tags = a.tags + (int64_t)b * n;
@@ -219,8 +302,8 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
   GemmTask tk{};
   tk.tile_start = b * maxtiles;
   tk.tiles_n = 1;
-  if (s.info != -1 || s.k >= n) {
-    if (tid == 0) tasks[b] = tk;        // m = 0: the GEMM CTAs of this matrix exit
+  if (s.info != -1 || s.k >= n) {       // uniform over the cluster
+    if (lead) tasks[b] = tk;            // m = 0: the GEMM CTAs of this matrix exit
     return;
   }
   // growth over the previous panel (its trailing max came from the GEMM)
@@ -233,82 +316,79 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
     s.trail_max = step_max;
   }
   const int k0 = s.k;
-  int k = k0, kw = 0, npiv = 0, info = -1, n2x2 = s.n2x2;
+  const int ch = (n - k0 + CS - 1) / CS;
+  const int lo = min(n, k0 + rank * ch), hi = min(n, lo + ch);
+  int k = k0, kw = 0, npiv = 0, info = -1, n2x2 = s.n2x2, par = 0;
   while (kw < NB && k < n) {
-    // -- A: column k up to date into Wp[:, kw] (4 lanes per row), then the
-    //    |z|^2-proxy argmax below the diagonal
-    panel_gemv<NB>(W, lda, n, k0, kw, k, k, Wp, k, Wp + kw);
+    // -- A: column k up to date into Wp[:, kw] for the own rows, then the
+    //    cluster's exact colmax / imax below the diagonal and |a_kk|
+    panel_gemv<NB, CNT>(W, lda, max(k, lo), hi, k0, kw, k, Wp, k, Wp + kw);
     __syncthreads();
-    double pv = -1.0;
-    int pi = 0x7fffffff;
-    for (int i = k + 1 + tid; i < n; i += PNL_NT) argmax_merge(pv, pi, x_abs2(Wp[(int64_t)i * LDW + kw]), i);
-    pargmax_red<PNL_NT>(pv, pi, ra, rai);
-    const double absakk = x_abs(Wp[(int64_t)k * LDW + kw]);
+    {
+      double ev;
+      int ei;
+      local_exact_argmax<CNT>(Wp + kw, LDW, max(k + 1, lo), hi, -1, ev, ei, ra, rai);
+      if (tid == 0) {
+        ClSlot& sl = slots[par];
+        sl.ev = ev;
+        sl.ei = ei;
+        sl.own = (k >= lo && k < hi) ? x_abs(Wp[(int64_t)k * LDW + kw]) : -1.0;
+      }
+    }
+    cl.sync();
+    const ClSlot m1 = cl_merge<CS>(cl, &slots[par], &merged);
+    par ^= 1;
+    const double absakk = m1.own;
     double colmax = 0.0;
     int imax = k;
-    if (k + 1 < n) {
-      const double thr = pv * (1.0 - 1e-14);
-      int amb = 0;
-      for (int i = k + 1 + tid; i < n; i += PNL_NT) amb |= (i != pi && x_abs2(Wp[(int64_t)i * LDW + kw]) >= thr);
-      if (__syncthreads_or(amb)) {
-        double v = -1.0;
-        int vi = 0x7fffffff;
-        for (int i = k + 1 + tid; i < n; i += PNL_NT) {
-          const cplx z = Wp[(int64_t)i * LDW + kw];
-          if (x_abs2(z) >= thr) argmax_merge(v, vi, x_abs(z), i);
-        }
-        pargmax_red<PNL_NT>(v, vi, rb, rai);
-        pi = vi;
-      }
-      imax = pi;
-      colmax = x_abs(Wp[(int64_t)imax * LDW + kw]);
-    }
+    if (k + 1 < n) { imax = m1.ei; colmax = m1.ev; }
     if (fmax(absakk, colmax) <= s.tol_abs) { info = k; break; }
     int kstep = 1, kp = k;
+    bool copy = false;
     if (!(absakk >= __dmul_rn(kAlphaP, colmax))) {
-      // -- C: column imax up to date into Wp[:, kw+1] (4 lanes per row), then
-      //    the rowmax proxy argmax (the diagonal entry imax excluded)
-      panel_gemv<NB>(W, lda, n, k0, kw, imax, k, Wp, imax, Wp + kw + 1);
+      // -- C: column imax up to date into Wp[:, kw+1], then the cluster's
+      //    exact rowmax (diagonal entry imax excluded) and |a_imax,imax|
+      panel_gemv<NB, CNT>(W, lda, max(k, lo), hi, k0, kw, imax, Wp, imax, Wp + kw + 1);
       __syncthreads();
-      double rpv = -1.0;
-      int rpi = 0x7fffffff;
-      for (int i = k + tid; i < n; i += PNL_NT)
-        if (i != imax) argmax_merge(rpv, rpi, x_abs2(Wp[(int64_t)i * LDW + kw + 1]), i);
-      pargmax_red<PNL_NT>(rpv, rpi, ra, rai);
-      const double rthr = rpv * (1.0 - 1e-14);
-      int ramb = 0;
-      for (int i = k + tid; i < n; i += PNL_NT)
-        ramb |= (i != imax && i != rpi && x_abs2(Wp[(int64_t)i * LDW + kw + 1]) >= rthr);
-      double rowmax = rpi < n ? x_abs(Wp[(int64_t)rpi * LDW + kw + 1]) : 0.0;
-      if (__syncthreads_or(ramb)) {
-        double rm = 0.0;
-        for (int i = k + tid; i < n; i += PNL_NT) {
-          const cplx z = Wp[(int64_t)i * LDW + kw + 1];
-          if (i != imax && x_abs2(z) >= rthr) rm = fmax(rm, x_abs(z));
+      {
+        double ev;
+        int ei;
+        local_exact_argmax<CNT>(Wp + kw + 1, LDW, max(k, lo), hi, imax, ev, ei, ra, rai);
+        if (tid == 0) {
+          ClSlot& sl = slots[par];
+          sl.ev = ev;
+          sl.ei = ei;
+          sl.own = (imax >= lo && imax < hi) ? x_abs(Wp[(int64_t)imax * LDW + kw + 1]) : -1.0;
         }
-        rowmax = pmax_red<PNL_NT>(rm, rb);
       }
-      const double absimax = x_abs(Wp[(int64_t)imax * LDW + kw + 1]);
+      cl.sync();
+      const ClSlot m2 = cl_merge<CS>(cl, &slots[par], &merged);
+      par ^= 1;
+      const double rowmax = fmax(0.0, m2.ev);
+      const double absimax = m2.own;
       if (__dmul_rn(absakk, rowmax) >= __dmul_rn(__dmul_rn(kAlphaP, colmax), colmax)) {
         kp = k;
       } else if (absimax >= __dmul_rn(kAlphaP, rowmax)) {
         kp = imax;
-        for (int i = k + tid; i < n; i += PNL_NT) Wp[(int64_t)i * LDW + kw] = Wp[(int64_t)i * LDW + kw + 1];
+        copy = true;                       // column kw := column kw+1
       } else {
         kp = imax;
         kstep = 2;
       }
-      __syncthreads();
     }
     const int kk = k + kstep - 1, kkw = kw + kstep - 1;
-    // -- D: interchange kk <-> kp: stale column kk moves to kp, L rows and X rows swap
+    if (copy)   // own rows; rows kk / kp are moved by the interchange below
+      for (int i = max(k, lo) + tid; i < hi; i += CNT)
+        if (i != kk && i != kp) Wp[(int64_t)i * LDW + kw] = Wp[(int64_t)i * LDW + kw + 1];
+    // -- D: interchange kk <-> kp: stale column kk moves to kp, L rows and X
+    //    rows swap (spread over the whole cluster; none of these writes
+    //    touches column kk, which is only read here)
     if (kp != kk) {
       const int c1 = kp - kk - 1, c2 = n - kp - 1, c3 = kk, c4 = kkw + 1;
       const int tot = 1 + c1 + c2 + c3 + c4;
-      const cplx dkk = G(kk, kk);
-      for (int t = tid; t < tot; t += PNL_NT) {
+      for (int t = rank * CNT + tid; t < tot; t += CS * CNT) {
         int u = t;
-        if (u == 0) { G(kp, kp) = dkk; continue; }
+        if (u == 0) { G(kp, kp) = G(kk, kk); continue; }
         u -= 1;
         if (u < c1) { const int j = kk + 1 + u; G(kp, j) = G(j, kk); continue; }
         u -= c1;
@@ -316,19 +396,27 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
         u -= c2;
         if (u < c3) { const cplx t0 = G(kk, u); G(kk, u) = G(kp, u); G(kp, u) = t0; continue; }
         u -= c3;
-        { cplx* p0 = Wp + (int64_t)kk * LDW + u; cplx* p1 = Wp + (int64_t)kp * LDW + u; const cplx t0 = *p0; *p0 = *p1; *p1 = t0; }
+        cplx* p0 = Wp + (int64_t)kk * LDW + u;
+        cplx* p1 = Wp + (int64_t)kp * LDW + u;
+        const int uc = (copy && u == kw) ? 1 : 0;    // the copied column comes from kw+1
+        const cplx t0 = p0[uc];
+        *p0 = p1[uc];
+        *p1 = t0;
       }
-      if (tid == 0) { const int64_t t0 = perm[kk]; perm[kk] = perm[kp]; perm[kp] = t0; }
+      if (lead) { const int64_t t0 = perm[kk]; perm[kk] = perm[kp]; perm[kp] = t0; }
+      cl.sync();
+    } else {
       __syncthreads();
     }
-    // -- E: store D and the L column(s) (packed layout, kernels.py:7-22)
+    // -- E: store D and the L column(s) of the own rows (packed layout,
+    //    kernels.py:7-22)
     if (kstep == 1) {
       const cplx d = Wp[(int64_t)k * LDW + kw];
       const bool re_big = fabs(d.x) >= fabs(d.y);
       const double rat = re_big ? __ddiv_rn(d.y, d.x) : __ddiv_rn(d.x, d.y);
       const double scl = re_big ? __ddiv_rn(1.0, __dadd_rn(d.x, __dmul_rn(d.y, rat)))
                                 : __ddiv_rn(1.0, __dadd_rn(d.y, __dmul_rn(d.x, rat)));
-      for (int i = k + tid; i < n; i += PNL_NT) {
+      for (int i = max(k, lo) + tid; i < hi; i += CNT) {
         const cplx w = Wp[(int64_t)i * LDW + kw];
         cplx q;
         if (i == k) q = d;
@@ -339,14 +427,14 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
                     __dmul_rn(__dsub_rn(__dmul_rn(w.y, rat), w.x), scl));
         G(i, k) = q;
       }
-      if (tid == 0) tags[k] = 1;
+      if (lead) tags[k] = 1;
     } else {
       const cplx d21 = Wp[(int64_t)(k + 1) * LDW + kw];
       const cplx d11 = x_div_py(Wp[(int64_t)(k + 1) * LDW + kw + 1], d21);
       const cplx d22 = x_div_py(Wp[(int64_t)k * LDW + kw], d21);
       const cplx t2 = x_div_py(mk(1.0, 0.0), x_sub(x_mul(d11, d22), mk(1.0, 0.0)));
       const cplx d21s = x_div_py(t2, d21);
-      for (int i = k + tid; i < n; i += PNL_NT) {
+      for (int i = max(k, lo) + tid; i < hi; i += CNT) {
         const cplx xk = Wp[(int64_t)i * LDW + kw], xk1 = Wp[(int64_t)i * LDW + kw + 1];
         if (i >= k + 2) {
           G(i, k) = x_mul(d21s, x_sub(x_mul(d11, xk), xk1));
@@ -358,7 +446,7 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
           G(k + 1, k + 1) = xk1;
         }
       }
-      if (tid == 0) { tags[k] = 2; tags[k + 1] = 0; }
+      if (lead) { tags[k] = 2; tags[k + 1] = 0; }
       ++n2x2;
     }
     ++npiv;
@@ -366,7 +454,7 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
     k += kstep;
     kw += kstep;
   }
-  if (tid == 0) {
+  if (lead) {
     s.k = k;
     s.info = info;
     s.n2x2 = n2x2;
@@ -389,6 +477,7 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
     }
     tasks[b] = tk;
   }
+  cl.sync();     // peers may still read this CTA's slots
 }
 
 __global__ void bk_panel_finalize_kernel(BkArgs a, const BkState* st, int batch) {
@@ -429,11 +518,20 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
   bk_panel_state_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, red, batch);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
+  // CTAs per matrix: spread each panel over enough SMs to fill the GPU once
+  int cs = batch >= 74 ? 1 : batch >= 37 ? 2 : batch >= 19 ? 4 : 8;
+  if (const char* env = getenv("D3M_PANEL_CS")) cs = atoi(env);
+  if (cs != 1 && cs != 2 && cs != 4 && cs != 8) cs = 1;
   for (int p = 0; p * NB < n; ++p) {
     const int mrem = n - (p + 1) * NB;                 // rows left after this panel (upper bound)
     const int tm = mrem > 0 ? (mrem + 63) / 64 : 0;
     const int maxtiles = tm * (tm + 1) / 2;
-    bk_panel_kernel<NB><<<batch, PNL_NT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles);
+    switch (cs) {
+      case 8: bk_panel_kernel<NB, 8><<<batch * 8, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
+      case 4: bk_panel_kernel<NB, 4><<<batch * 4, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
+      case 2: bk_panel_kernel<NB, 2><<<batch * 2, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
+      default: bk_panel_kernel<NB, 1><<<batch, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
     if (maxtiles > 0) {
       const int rc = d3m_gemm_launch_tm(0, 0, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream);

@@ -143,11 +143,15 @@ def test_config3_pivots_and_schur_vs_reference(cuda):
             assert np.linalg.norm(KDh - ref) <= 1e-9 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("n,m,batch", [(600, 40, 3), (1030, 17, 2)])
-def test_large_subdomain_panel_bk_vs_oracle(cuda, oracle, n, m, batch):
+@pytest.mark.parametrize("n,m,batch,cs", [(600, 40, 3, None), (1030, 17, 2, None), (600, 40, 3, "1"),
+                                          (777, 9, 2, "2"), (777, 9, 2, "4"), (1030, 17, 2, "8")])
+def test_large_subdomain_panel_bk_vs_oracle(cuda, oracle, monkeypatch, n, m, batch, cs):
     """n > 512 takes the batched panel BK (grouped DMMA trailing updates) and
-    the blocked solves: pivots bit-exact vs the oracle, K_D / g_d to 1e-10."""
+    the blocked solves: pivots bit-exact vs the oracle, K_D / g_d to 1e-10,
+    for every cluster size of the panel kernel (D3M_PANEL_CS)."""
     import paper_2002_05018_b200 as d
+    if cs is not None:
+        monkeypatch.setenv("D3M_PANEL_CS", cs)
     rng = np.random.default_rng(n + m)
     systems, ref = [], []
     for b in range(batch):
