@@ -319,7 +319,9 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
   const int ch = (n - k0 + CS - 1) / CS;
   const int lo = min(n, k0 + rank * ch), hi = min(n, lo + ch);
   int k = k0, kw = 0, npiv = 0, info = -1, n2x2 = s.n2x2, par = 0;
-  while (kw < NB && k < n) {
+  // a step starts only while kw <= NB-2, so a panel is NB-1 or NB columns
+  // (zlasyf's exit rule) and the trailing update has K <= NB = 16
+  while (kw < NB - 1 && k < n) {
     // -- A: column k up to date into Wp[:, kw] for the own rows, then the
     //    cluster's exact colmax / imax below the diagonal and |a_kk|
     panel_gemv<NB, CNT>(W, lda, max(k, lo), hi, k0, kw, k, Wp, k, Wp + kw);
@@ -522,8 +524,8 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
   int cs = batch >= 74 ? 1 : batch >= 37 ? 2 : batch >= 19 ? 4 : 8;
   if (const char* env = getenv("D3M_PANEL_CS")) cs = atoi(env);
   if (cs != 1 && cs != 2 && cs != 4 && cs != 8) cs = 1;
-  for (int p = 0; p * NB < n; ++p) {
-    const int mrem = n - (p + 1) * NB;                 // rows left after this panel (upper bound)
+  for (int p = 0; p * (NB - 1) < n; ++p) {
+    const int mrem = n - (p + 1) * (NB - 1);           // rows left after this panel (upper bound)
     const int tm = mrem > 0 ? (mrem + 63) / 64 : 0;
     const int maxtiles = tm * (tm + 1) / 2;
     switch (cs) {
@@ -534,7 +536,7 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
     if (maxtiles > 0) {
-      const int rc = d3m_gemm_launch_tm(0, 0, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream);
+      const int rc = d3m_gemm_smallk_launch_tm(a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream);
       if (rc) return rc;
     }
   }

@@ -211,6 +211,135 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
   }
 }
 
+// ---- small-K variant (K <= 16): the rank-<=16 trailing updates of the
+// batched panel BK (bk_panel.cu).  At K = 16 a 64x64 tile does 0.5 MFLOP
+// against 128 KB of C traffic (4 flop/B), so the tile is HBM/latency bound:
+// the C tile is fetched by cp.async into shared memory together with A and B
+// (all 96 KB of the tile's traffic in flight at once), updated there by the
+// DMMA fragments and written back with coalesced 16-byte stores.
+constexpr int SK_K = 16, SK_PA = SK_K + 4, SK_PC = BN + 1;
+constexpr size_t kSmallKSmem = sizeof(cplx) * ((BM + BN) * SK_PA + BM * SK_PC);
+
+__global__ void __launch_bounds__(NTHREADS, 2)
+zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bbase, cplx* Cbase,
+                    const GemmTask* __restrict__ tasks, int ntasks, unsigned long long* tmax) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cplx(*As)[SK_PA] = reinterpret_cast<cplx(*)[SK_PA]>(smem_raw);
+  cplx(*Bs)[SK_PA] = reinterpret_cast<cplx(*)[SK_PA]>(smem_raw + sizeof(cplx) * BM * SK_PA);
+  cplx(*Cs)[SK_PC] = reinterpret_cast<cplx(*)[SK_PC]>(smem_raw + sizeof(cplx) * (BM + BN) * SK_PA);
+  const int tile = blockIdx.x;
+  int lo = 0, hi = ntasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tasks[mid].tile_start <= tile) lo = mid; else hi = mid - 1;
+  }
+  const GemmTask tk = tasks[lo];
+  int local = tile - tk.tile_start, tm, tn;
+  const bool sym = (tk.flags & kGemmSym) != 0;
+  if (sym) {
+    tm = (int)((sqrt(8.0 * local + 1.0) - 1.0) * 0.5);
+    while ((tm + 1) * (tm + 2) / 2 <= local) ++tm;
+    while (tm * (tm + 1) / 2 > local) --tm;
+    tn = local - tm * (tm + 1) / 2;
+  } else {
+    tm = local / tk.tiles_n;
+    tn = local - tm * tk.tiles_n;
+  }
+  const cplx* A = Abase + tk.a_off;
+  const cplx* B = Bbase + tk.b_off;
+  cplx* C = Cbase + tk.c_off;
+  const int M = tk.m, N = tk.n, K = tk.k, ldc = tk.ldc;
+  const int m0 = tm * BM, n0 = tn * BN;
+  if (m0 >= M || n0 >= N) return;
+  const int mode = tk.flags & kGemmModeMask;
+  const int t = threadIdx.x;
+  // ---- one-shot staging: A, B (64 x 16 each) and the C tile (64 x 64)
+#pragma unroll
+  for (int p = 0; p < 2 * BM * SK_K / NTHREADS; ++p) {     // A then B: 64 rows x 16 k each
+    const int e = p * NTHREADS + t, r = (e >> 4) & 63, k = e & 15;
+    const bool isb = e >= BM * SK_K;
+    const int rows = isb ? N : M, r0 = isb ? n0 : m0;
+    const bool ok = (r0 + r < rows) && (k < K);
+    const cplx* g = isb ? B + (int64_t)(n0 + r) * tk.ldb + k : A + (int64_t)(m0 + r) * tk.lda + k;
+    cplx* d = isb ? &Bs[r][k] : &As[r][k];
+    cp_async16(d, ok ? g : Abase, ok);
+  }
+  if (mode != kGemmStore) {
+#pragma unroll 8
+    for (int p = 0; p < BM * BN / NTHREADS; ++p) {
+      const int e = p * NTHREADS + t, r = e >> 6, c = e & 63;
+      const bool ok = (m0 + r < M) && (n0 + c < N) && (!sym || n0 + c <= m0 + r);
+      cp_async16(&Cs[r][c], ok ? C + (int64_t)(m0 + r) * ldc + n0 + c : Cbase, ok);
+    }
+  }
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+
+  const int lane = t & 31, warp = t >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int fr = lane >> 2, fc = lane & 3;
+  double acc_re[4][4][2], acc_im[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < SK_K / 4; ++kk) {
+    double are[4], aim[4], anim[4], bre[4], bim[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const cplx a = As[wm + i * 8 + fr][kk * 4 + fc];
+      are[i] = a.x;
+      aim[i] = a.y;
+      anim[i] = -a.y;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const cplx b = Bs[wn + j * 8 + fr][kk * 4 + fc];
+      bre[j] = b.x;
+      bim[j] = b.y;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
+        dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
+        dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
+        dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
+      }
+  }
+  // ---- epilogue in shared memory, then coalesced stores
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = wm + i * 8 + fr, c = wn + j * 8 + fc * 2 + h;
+        const cplx u = mk(acc_re[i][j][h], acc_im[i][j][h]);
+        cplx& w = Cs[r][c];
+        w = mode == kGemmSub ? c_sub(w, u) : mode == kGemmStore ? u : c_add(w, u);
+      }
+  __syncthreads();
+  const bool track = (tk.flags & kGemmTrackMax) != 0 && tmax != nullptr;
+  double tm2 = 0.0;
+#pragma unroll 8
+  for (int p = 0; p < BM * BN / NTHREADS; ++p) {
+    const int e = p * NTHREADS + t, r = e >> 6, c = e & 63;
+    if ((m0 + r < M) && (n0 + c < N) && (!sym || n0 + c <= m0 + r)) {
+      const cplx w = Cs[r][c];
+      C[(int64_t)(m0 + r) * ldc + n0 + c] = w;
+      if (track) tm2 = fmax(tm2, w.x * w.x + w.y * w.y);
+    }
+  }
+  if (track) {
+    tm2 = warp_max(tm2);
+    if (lane == 0) atomicMax(tmax + tk.pad_, (unsigned long long)__double_as_longlong(tm2));
+  }
+}
+
 constexpr size_t kGemmSmem = sizeof(cplx) * STAGES * (BM + BN) * PITCH;
 
 static unsigned long long* g_tmax = nullptr;   // set per launch by d3m_gemm_launch_tm
@@ -266,4 +395,20 @@ extern "C" int d3m_gemm_launch_tm(int ta, int tb, const void* A, const void* B, 
   if (!ta && tb) return launch_t<false, true>(a, b, c, t, ntasks, ntiles, s);
   if (ta && !tb) return launch_t<true, false>(a, b, c, t, ntasks, ntiles, s);
   return launch_t<true, true>(a, b, c, t, ntasks, ntiles, s);
+}
+
+// Grouped small-K launch (every task K <= 16; SYM tasks must be LowerOnly).
+extern "C" int d3m_gemm_smallk_launch_tm(const void* A, const void* B, void* C, const void* dtasks, int ntasks,
+                                         int ntiles, void* tmax, void* stream) {
+  using namespace d3m;
+  if (ntiles <= 0 || ntasks <= 0) return 0;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(zgemm_smallk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallKSmem);
+    configured = true;
+  }
+  zgemm_smallk_kernel<<<ntiles, NTHREADS, kSmallKSmem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(A), static_cast<const cplx*>(B), static_cast<cplx*>(C),
+      static_cast<const GemmTask*>(dtasks), ntasks, static_cast<unsigned long long*>(tmax));
+  return (int)cudaGetLastError();
 }
