@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define D3M_ABI_VERSION 1
+#define D3M_ABI_VERSION 2
 
 int d3m_abi_version(void);
 const char* d3m_last_error(void);
@@ -88,12 +88,16 @@ int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* C, voi
                       void* d_tasks, void* stream);
 
 /* Batched Schur reduction of equal-sized subdomains: factor A_d in place,
- * X = A_d^-1 [D_d | f_d], K_D = 0.5 (D^T X + (D^T X)^T), g_d = D^T x_f.
- * Replaces subdomain.reduce_domain (subdomain.py:166-184) for a batch.
+ * X = A_d^-1 [D_d | F_d], K_D = 0.5 (D^T X_D + (D^T X_D)^T), G_d = D^T X_F.
+ * Replaces subdomain.reduce_domain (subdomain.py:166-184) for a batch; F_d
+ * holds nrhs load columns (n x nrhs row-major; the reference's single f is
+ * nrhs = 1), G_d is m x nrhs.  work_z / work_x: batch x n x (m+nrhs),
+ * work_c: batch x m x (m+nrhs); work_x holds X on return.
  * n <= 512: exact BK + chain solves (bk_scratch: batch*4n complex if n>3200);
  * n > 512: panel BK + blocked solves (bk_scratch: d3m_bk_panel_workspace
  * bytes, d_tasks: max(batch, 2 ceil(n/64) batch) records). */
-int d3m_schur_reduce_batched(int batch, int n, int m, void* A, const void* D, const void* f, double pivot_tol,
+int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const void* D, const void* f,
+                             double pivot_tol,
                              void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
                              void* K_out, void* g_out, void* work_z, void* work_x, void* work_c, void* bk_scratch,
                              void* d_tasks, void* stream);

@@ -25,7 +25,6 @@
 namespace d3m {
 namespace cg = cooperative_groups;
 
-constexpr int PNL_NT = 1024;   // prologue / legacy
 constexpr int CNT = 512;       // threads per panel CTA
 constexpr double kAlphaP = 0.6403882032022076;
 

@@ -225,15 +225,16 @@ int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* Cm, vo
   return 0;
 }
 
-int d3m_schur_reduce_batched(int batch, int n, int m, void* A, const void* D, const void* f, double pivot_tol,
-                             void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
-                             void* K_out, void* g_out, void* work_z, void* work_x, void* work_c, void* bk_scratch,
-                             void* d_tasks, void* stream) {
+int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const void* D, const void* f,
+                             double pivot_tol, void* perm, void* tags, void* n2x2, void* growth, void* info,
+                             void* scale, void* asym, void* K_out, void* g_out, void* work_z, void* work_x,
+                             void* work_c, void* bk_scratch, void* d_tasks, void* stream) {
   // A: batch x n x n (factored in place -> packed factor); D: batch x n x m;
-  // f: batch x n; work_z, work_x: batch x n x (m+1); work_c: batch x m x (m+1)
-  if (batch < 0 || n < 0 || m < 0) return fail(-22, "d3m_schur_reduce_batched: bad shape");
+  // F: batch x n x nrhs; work_z, work_x: batch x n x (m+nrhs); work_c: batch x m x (m+nrhs)
+  if (batch < 0 || n < 0 || m < 0 || nrhs < 0) return fail(-22, "d3m_schur_reduce_batched: bad shape");
   if (batch == 0) return 0;
-  const int64_t nn = (int64_t)n * n, nm1 = (int64_t)n * (m + 1);
+  const int w = m + nrhs;
+  const int64_t nn = (int64_t)n * n, nw = (int64_t)n * w;
   const bool big = n > kPanelBkMin;
   // large subdomains: batched blocked BK (panel kernel + grouped DMMA trailing
   // updates, bk_scratch >= d3m_bk_panel_workspace(n, batch) bytes); small:
@@ -244,35 +245,38 @@ int d3m_schur_reduce_batched(int batch, int n, int m, void* A, const void* D, co
   else
     D3M_TRY(d3m_bk_factor_batched(batch, n, A, nn, n, pivot_tol, 1, perm, tags, n2x2, growth, info, scale, asym,
                                   bk_scratch, stream));
-  if (n == 0) return 0;
-  // RHS = [D | f]  (subdomain.py:177-179), X = A^-1 RHS (factor.py:52-66)
-  D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_pack_rhs_launch(D, f, work_x, n, m, batch, (int64_t)n * m, n, nm1, stream); }));
+  if (n == 0 || w == 0) return 0;
+  // RHS = [D | F]  (subdomain.py:177-179), X = A^-1 RHS (factor.py:52-66)
+  D3M_TRY(launch(kClsMisc, stream, [&] {
+    return d3m_pack_rhs_launch(D, f, work_x, n, m, nrhs, batch, (int64_t)n * m, (int64_t)n * nrhs, nw, stream);
+  }));
   if (big)
-    D3M_TRY(d3m_ldlt_solve_blocked_batched(batch, n, A, nn, perm, n, tags, n, work_x, nm1, m + 1, m + 1, work_z,
-                                           d_tasks, stream));
+    D3M_TRY(d3m_ldlt_solve_blocked_batched(batch, n, A, nn, perm, n, tags, n, work_x, nw, w, w, work_z, d_tasks,
+                                           stream));
   else
-    D3M_TRY(d3m_ldlt_solve_batched(batch, n, A, nn, perm, n, tags, n, work_x, nm1, m + 1, m + 1, work_z, stream));
+    D3M_TRY(d3m_ldlt_solve_batched(batch, n, A, nn, perm, n, tags, n, work_x, nw, w, w, work_z, stream));
   if (m == 0) return 0;
-  // C = D^T [X | x_f]  (subdomain.py:181,183) on DMMA, one task per domain
+  // C = D^T [X_D | X_F]  (subdomain.py:181,183) on DMMA, one task per domain
   std::vector<d3m::GemmTask> t(batch);
   for (int b = 0; b < batch; ++b) {
     d3m::GemmTask& k = t[b];
     std::memset(&k, 0, sizeof(k));
     k.a_off = (int64_t)b * n * m;          // D stored n x m = K x M  (TA)
-    k.b_off = (int64_t)b * nm1;            // X stored n x (m+1) = K x N (TB)
-    k.c_off = (int64_t)b * m * (m + 1);
+    k.b_off = (int64_t)b * nw;             // X stored n x (m+nrhs) = K x N (TB)
+    k.c_off = (int64_t)b * m * w;
     k.m = m;
-    k.n = m + 1;
+    k.n = w;
     k.k = n;
     k.lda = m;
-    k.ldb = m + 1;
-    k.ldc = m + 1;
+    k.ldb = w;
+    k.ldc = w;
     k.flags = d3m::kGemmStore;
   }
   D3M_TRY(d3m_zgemm_grouped(1, 1, D, work_x, work_c, t.data(), batch, d_tasks, stream));
-  // K_D = 0.5 (K_D + K_D^T), g_d
+  // K_D = 0.5 (K_D + K_D^T), G_d
   D3M_TRY(launch(kClsMisc, stream, [&] {
-    return d3m_schur_finalize_launch(work_c, K_out, g_out, m, batch, (int64_t)m * (m + 1), (int64_t)m * m, m, stream);
+    return d3m_schur_finalize_launch(work_c, K_out, g_out, m, nrhs, batch, (int64_t)m * w, (int64_t)m * m,
+                                     (int64_t)m * nrhs, stream);
   }));
   return 0;
 }

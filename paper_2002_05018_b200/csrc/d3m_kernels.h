@@ -46,9 +46,9 @@ int d3m_panel_trsm_launch(void* P, void* X, int R, int n, const void* F, const v
                           void* stream);
 int d3m_gemm_launch(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks, int ntasks, int ntiles,
                     void* stream);
-int d3m_schur_finalize_launch(const void* C, void* K, void* g, int m, int batch, int64_t stride_c, int64_t stride_k,
-                              int64_t stride_g, void* stream);
-int d3m_pack_rhs_launch(const void* D, const void* f, void* Z, int n, int m, int batch, int64_t stride_d,
+int d3m_schur_finalize_launch(const void* C, void* K, void* g, int m, int nrhs, int batch, int64_t stride_c,
+                              int64_t stride_k, int64_t stride_g, void* stream);
+int d3m_pack_rhs_launch(const void* D, const void* f, void* Z, int n, int m, int nrhs, int batch, int64_t stride_d,
                         int64_t stride_f, int64_t stride_z, void* stream);
 int d3m_ordered_average_launch(const void* E, const void* ptr, const void* src, void* out, int64_t ng, void* stream);
 int d3m_gather_index_launch(const void* src, const void* idx, void* out, int64_t nrows, int cols, void* stream);

@@ -10,6 +10,7 @@
 //  * ordered_average     recover_primal's acc[dof_map] += E; acc / cnt in
 //                        ascending domain order (subdomain.py:222-237)
 //  * gather_index        out[i, :] = src[idx[i], :]
+#include <algorithm>
 #include "d3m_common.cuh"
 #include "d3m_misc.h"
 #include "d3m_kernels.h"
@@ -36,30 +37,31 @@ __global__ void zero_kernel(cplx* p, int64_t n) {
 }
 
 // C: batch of m x (m+1) (ld m+1) = D^T [X | x_f]; K: m x m, g: m
-__global__ void schur_finalize_kernel(const cplx* C, cplx* K, cplx* g, int m, int64_t stride_c, int64_t stride_k,
-                                      int64_t stride_g) {
+__global__ void schur_finalize_kernel(const cplx* C, cplx* K, cplx* g, int m, int nrhs, int64_t stride_c,
+                                      int64_t stride_k, int64_t stride_g) {
   const int b = blockIdx.y;
   const cplx* Cb = C + b * stride_c;
-  const int ld = m + 1;
+  const int ld = m + nrhs;
   const int64_t total = (int64_t)m * m;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / m), j = (int)(e % m);
     const cplx s = x_add(Cb[(int64_t)i * ld + j], Cb[(int64_t)j * ld + i]);   // K_D + K_D.T
     K[b * stride_k + e] = mk(__dmul_rn(0.5, s.x), __dmul_rn(0.5, s.y));     // 0.5 * (...)
   }
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x)
-    g[b * stride_g + e] = Cb[(int64_t)e * ld + m];
+  const int64_t tg = (int64_t)m * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tg; e += (int64_t)gridDim.x * blockDim.x)
+    g[b * stride_g + e] = Cb[(e / nrhs) * ld + m + e % nrhs];
 }
 
-// Z (n x (m+1), ld m+1) = [D | f], one matrix per blockIdx.y
-__global__ void pack_rhs_kernel(const cplx* D, const cplx* f, cplx* Z, int n, int m, int64_t stride_d,
+// Z (n x (m+nrhs), ld m+nrhs) = [D | F], one matrix per blockIdx.y
+__global__ void pack_rhs_kernel(const cplx* D, const cplx* f, cplx* Z, int n, int m, int nrhs, int64_t stride_d,
                                 int64_t stride_f, int64_t stride_z) {
   const int b = blockIdx.y;
-  const int ld = m + 1;
+  const int ld = m + nrhs;
   const int64_t total = (int64_t)n * ld;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / ld), c = (int)(e % ld);
-    Z[b * stride_z + e] = c < m ? D[b * stride_d + (int64_t)i * m + c] : f[b * stride_f + i];
+    Z[b * stride_z + e] = c < m ? D[b * stride_d + (int64_t)i * m + c] : f[b * stride_f + (int64_t)i * nrhs + c - m];
   }
 }
 
@@ -112,21 +114,22 @@ extern "C" int d3m_zero_launch(void* p, int64_t n, void* stream) {
   return (int)cudaGetLastError();
 }
 
-extern "C" int d3m_schur_finalize_launch(const void* C, void* K, void* g, int m, int batch, int64_t stride_c,
-                                         int64_t stride_k, int64_t stride_g, void* stream) {
+extern "C" int d3m_schur_finalize_launch(const void* C, void* K, void* g, int m, int nrhs, int batch,
+                                          int64_t stride_c, int64_t stride_k, int64_t stride_g, void* stream) {
   if (batch <= 0 || m <= 0) return 0;
-  schur_finalize_kernel<<<dim3(flat_grid((int64_t)m * m, 256, 1024), batch), 256, 0,
+  schur_finalize_kernel<<<dim3(flat_grid((int64_t)m * std::max(m, nrhs), 256, 1024), batch), 256, 0,
                           reinterpret_cast<cudaStream_t>(stream)>>>(
-      static_cast<const cplx*>(C), static_cast<cplx*>(K), static_cast<cplx*>(g), m, stride_c, stride_k, stride_g);
+      static_cast<const cplx*>(C), static_cast<cplx*>(K), static_cast<cplx*>(g), m, nrhs, stride_c, stride_k, stride_g);
   return (int)cudaGetLastError();
 }
 
-extern "C" int d3m_pack_rhs_launch(const void* D, const void* f, void* Z, int n, int m, int batch, int64_t stride_d,
-                                   int64_t stride_f, int64_t stride_z, void* stream) {
-  if (batch <= 0 || n <= 0) return 0;
-  pack_rhs_kernel<<<dim3(flat_grid((int64_t)n * (m + 1), 256, 1024), batch), 256, 0,
+extern "C" int d3m_pack_rhs_launch(const void* D, const void* f, void* Z, int n, int m, int nrhs, int batch,
+                                   int64_t stride_d, int64_t stride_f, int64_t stride_z, void* stream) {
+  if (batch <= 0 || n <= 0 || m + nrhs <= 0) return 0;
+  pack_rhs_kernel<<<dim3(flat_grid((int64_t)n * (m + nrhs), 256, 1024), batch), 256, 0,
                     reinterpret_cast<cudaStream_t>(stream)>>>(static_cast<const cplx*>(D), static_cast<const cplx*>(f),
-                                                              static_cast<cplx*>(Z), n, m, stride_d, stride_f, stride_z);
+                                                              static_cast<cplx*>(Z), n, m, nrhs, stride_d, stride_f,
+                                                              stride_z);
   return (int)cudaGetLastError();
 }
 

@@ -34,6 +34,10 @@ class SingularBlockError(Exception):
     """Both 1x1 and 2x2 pivot candidates fell below the pivot threshold."""
 
 
+class SolverStateError(Exception):
+    """Factor state missing or released (subdomain.py:221-223 analog)."""
+
+
 class FactorConsistencyError(Exception):
     """Numeric factorization touched a block outside the symbolic pattern."""
 
@@ -55,19 +59,32 @@ class DenseFactor:
     """
 
     def __init__(self, packed, perm_dev, tags_dev, growth: float, n_2x2: int):
-        self.packed = packed            # torch (n, n) complex128 view
+        self.packed = packed            # torch (n, n) complex128 view (None once released)
         self.perm_dev = perm_dev        # torch (n,) int64 view
         self.tags_dev = tags_dev        # torch (n,) int8 view
         self.growth = float(growth)
         self.n_2x2 = int(n_2x2)
+        self._n = int(perm_dev.shape[0])
         self._host = None
 
     @property
     def n(self) -> int:
-        return int(self.packed.shape[0])
+        return self._n
+
+    @property
+    def released(self) -> bool:
+        return self.packed is None
+
+    def release(self) -> "DenseFactor":
+        """Drop the factor values (keep perm / tags / stats); used by
+        reduce_domains(keep="solution") when the factors do not fit in HBM."""
+        self.packed = None
+        return self
 
     def _unpack(self):
         if self._host is None:
+            if self.packed is None:
+                raise SolverStateError("factor values were released (reduce_domains keep='solution')")
             W = self.packed.cpu().numpy()
             tags = self.tags_dev.cpu().numpy().astype(np.int8)
             perm = self.perm_dev.cpu().numpy().astype(np.int64)
@@ -85,8 +102,10 @@ class DenseFactor:
     L = property(lambda self: self._unpack()[0])
     d = property(lambda self: self._unpack()[1])
     e = property(lambda self: self._unpack()[2])
-    tags = property(lambda self: self._unpack()[3])
-    perm = property(lambda self: self._unpack()[4])
+    tags = property(lambda self: self._unpack()[3] if self.packed is not None
+                    else self.tags_dev.cpu().numpy().astype(np.int8))
+    perm = property(lambda self: self._unpack()[4] if self.packed is not None
+                    else self.perm_dev.cpu().numpy().astype(np.int64))
 
     def solve(self, B):
         """Solve M X = B (vector or multi-column), factor.py:52-66."""
@@ -96,6 +115,8 @@ class DenseFactor:
         cols = 1 if one_d else (B.shape[1] if len(B.shape) > 1 else 1)
         if rows != self.n:
             raise ValueError(f"rhs has {rows} rows, factor has {self.n}")
+        if self.packed is None:
+            raise SolverStateError("factor values were released (reduce_domains keep='solution')")
         if self.n == 0 or cols == 0:
             out = np.zeros((self.n, cols), dtype=np.complex128)
             return out[:, 0] if one_d else out

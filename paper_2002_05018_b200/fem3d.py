@@ -324,9 +324,10 @@ def assemble_global(model: FemModel):
     return A, model.f
 
 
-def subdomain_systems(model: FemModel, rhs: int = 0, sparse: bool = True):
+def subdomain_systems(model: FemModel, rhs: int | None = 0, sparse: bool = True):
     """Per-domain systems (subdomain.py:124-163 analog) for RHS column
-    ``rhs``; returns SubdomainSystem objects of the hot-path API.
+    ``rhs`` (None: all of the problem's RHS columns, f_d of shape n x r);
+    returns SubdomainSystem objects of the hot-path API.
 
     With ``sparse`` (default) A_d and the coupling blocks D are SparseBlock
     objects: the same additions as the dense assembly (np.add.at in element
@@ -395,9 +396,13 @@ def subdomain_systems(model: FemModel, rhs: int = 0, sparse: bool = True):
                 if cols.size:
                     D[rows[:, None], np.arange(cols.size)[None, :]] = Dv
             couplings.append(Coupling(i_itf, D, s))
-        fd = np.zeros(n, dtype=np.complex128)          # load of the domain's own boundary faces
+        cols = list(range(model.bnd_f.shape[2])) if rhs is None else [rhs]
+        fd = np.zeros((n, len(cols)), dtype=np.complex128)   # load of the domain's own boundary faces
         if bsel.size:
-            np.add.at(fd, g2l[model.bnd_edges[bsel]].ravel(), model.bnd_f[bsel, :, rhs].ravel())
+            for q, c in enumerate(cols):
+                np.add.at(fd[:, q], g2l[model.bnd_edges[bsel]].ravel(), model.bnd_f[bsel, :, c].ravel())
+        if rhs is not None:
+            fd = fd[:, 0].copy()
         Ad = SparseBlock((n, n), keys, vals) if sparse else A
         systems.append(SubdomainSystem(d, Ad, fd, loc, couplings))
     return systems
@@ -416,12 +421,15 @@ def interpolate_einc(model: FemModel, rhs: int = 0) -> np.ndarray:
     return out
 
 
-def solve_d3m(model: FemModel, rhs: int = 0, ordering: str = "builtin", timers: dict | None = None):
-    """Full D3M pipeline of the hot path on the GPU for one RHS column
-    (driver.run_pipeline:103-142 analog): reduce -> assemble -> ordering /
-    symbolic -> block LDL^T -> block solve -> recover.  Returns the global
-    edge solution (host numpy) and fills ``timers`` (seconds, wall clock with
-    device synchronisation) when given."""
+def solve_d3m(model: FemModel, rhs: int | None = 0, ordering: str = "builtin", timers: dict | None = None,
+              keep: str = "auto", systems: list | None = None):
+    """Full D3M pipeline of the hot path on the GPU (driver.run_pipeline:103-142
+    analog): reduce -> assemble -> ordering / symbolic -> block LDL^T -> block
+    solve -> recover, for RHS column ``rhs`` or, with rhs=None, all RHS
+    columns at once (one factorisation, n x r solves).  Returns the global
+    edge solution (host numpy, n_edges or n_edges x r) and fills ``timers``
+    (seconds, wall clock with device synchronisation) when given.  ``keep``
+    is passed to reduce_domains; prebuilt ``systems`` skip the front end."""
     import time
 
     import torch
@@ -434,9 +442,10 @@ def solve_d3m(model: FemModel, rhs: int = 0, ordering: str = "builtin", timers: 
 
     t = {}
     t0 = tick()
-    systems = subdomain_systems(model, rhs)
+    if systems is None:
+        systems = subdomain_systems(model, rhs)
     t1 = tick()
-    red = subdomain.reduce_domains(systems)
+    red = subdomain.reduce_domains(systems, keep=keep)
     t2 = tick()
     R = subdomain.assemble_reduced(red, model)
     g = blockmat.clique_graph(R.K)
@@ -456,8 +465,9 @@ def solve_d3m(model: FemModel, rhs: int = 0, ordering: str = "builtin", timers: 
     return sol, systems, R, plan, F
 
 
-def global_residual(model: FemModel, sol: np.ndarray, rhs: int = 0) -> float:
-    """||A x - f||_inf / ||f||_inf of the monolithic system (subdomain.py:240-250)."""
+def global_residual(model: FemModel, sol: np.ndarray, rhs: int | None = 0) -> float:
+    """||A x - f||_inf / ||f||_inf of the monolithic system (subdomain.py:240-250);
+    the max over columns for rhs=None."""
     A, f = assemble_global(model)
-    fr = f[:, rhs]
+    fr = f if rhs is None else f[:, rhs]
     return float(np.abs(A @ sol - fr).max() / np.abs(fr).max())

@@ -21,16 +21,12 @@ import numpy as np
 from . import _lib
 from .blockmat import BlockSparseSym
 from .device import DeviceArray, empty, require_cuda, stream_ptr, to_device, upload_bytes, upload_i64
-from .factor import DEFAULT_PIVOT_TOL, DenseFactor, _collect, _singular_msg
+from .factor import DEFAULT_PIVOT_TOL, DenseFactor, SolverStateError, _collect, _singular_msg
 
 _P = _lib.ptr
 
 
 class SingularDomainError(Exception):
-    pass
-
-
-class SolverStateError(Exception):
     pass
 
 
@@ -157,12 +153,42 @@ def _coupling_matrix(sys: SubdomainSystem):
     return np.zeros((sys.n_dofs, 0), dtype=np.complex128)
 
 
-def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PIVOT_TOL) -> list:
-    """Batched reduce_domain: every group of equal (n, m) subdomains is
-    factored and reduced in one device call chain (BK -> multi-RHS solve ->
-    D^T X on DMMA -> symmetrisation).  Returns [(K_D, g_d)] as DeviceArrays
-    and caches each factor on its system, like subdomain.py:166-184."""
+def _load_cols(s) -> int:
+    shp = tuple(s.f.shape) if hasattr(s.f, "shape") else np.shape(s.f)
+    return 1 if len(shp) == 1 else int(shp[1])
+
+
+def _domain_bytes(n: int, m: int, r: int) -> int:
+    """Device bytes one domain of a reduce batch holds (A, D, F, X, Z, C, K, G,
+    panel workspace)."""
+    w = m + r
+    return 16 * (n * n + n * m + n * r + 2 * n * w + m * w + m * m + m * r) + 17 * 16 * n + 1024
+
+
+def _free_bytes(t) -> int:
+    free, _ = t.cuda.mem_get_info()
+    return int(free + t.cuda.memory_reserved() - t.cuda.memory_allocated())
+
+
+def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PIVOT_TOL, keep: str = "factor",
+                   max_batch_bytes: int | None = None) -> list:
+    """Batched reduce_domain (subdomain.py:166-184): subdomains of equal order n
+    are factored and reduced together (BK -> multi-RHS solve -> D^T X on DMMA
+    -> symmetrisation), in batches sized to the free device memory (or
+    ``max_batch_bytes``).  Returns [(K_D, g_d)] as DeviceArrays; g_d is m x r
+    when the systems carry r load columns (f of shape n x r), else a vector.
+
+    keep="factor" caches each DenseFactor on its system, like the reference.
+    keep="solution" keeps X_d = A_d^-1 [D_d | F_d] (n x (m + r)) instead and
+    releases the factor values, so recover_primal forms
+    E_d = X_F - X_D lambda_d with one GEMM (exact-arithmetic equal to the
+    reference's A_d^-1 (F_d - D_d lambda_d)); it is what lets config 5
+    (64 x n = 13,428, 185 GB of factors) run in 180 GB of HBM.  keep="auto"
+    chooses "solution" when all factors would not fit in half the free
+    device memory."""
     t = require_cuda()
+    if keep not in ("factor", "solution", "auto"):
+        raise ValueError(f"keep must be 'factor', 'solution' or 'auto', not {keep!r}")
     # one batch per subdomain order n (the factorisation does not depend on
     # m); coupling blocks are zero-padded to the group's largest m and each
     # domain's K_D / g_d is the leading m x m / m view of its padded result
@@ -172,64 +198,94 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
         n = int(np.shape(s.A)[0]) if not isinstance(s.A, DeviceArray) else s.A.shape[0]
         ms.append(sum(int(np.shape(c.D)[1]) for c in s.couplings))
         groups.setdefault(n, []).append(idx)
+    rs = {_load_cols(s) for s in systems}
+    if len(rs) > 1:
+        raise ValueError("all subdomains must carry the same number of load columns")
+    r = rs.pop() if rs else 1
+    vec = bool(systems) and len(np.shape(systems[0].f) if not hasattr(systems[0].f, "shape")
+                                else tuple(systems[0].f.shape)) == 1
+    if keep == "auto":
+        fac = sum(16 * n * n * len(mem) for n, mem in groups.items())
+        keep = "solution" if fac > 0.5 * _free_bytes(t) else "factor"
     out = [None] * len(systems)
     first_error = None
     for n, members in groups.items():
         m = max(ms[i] for i in members)
-        B = len(members)
-        A = empty((B, n, n))
-        D = t.zeros((B, n, m), dtype=t.complex128, device="cuda")
-        f = empty((B, n))
-        for r, idx in enumerate(members):
-            s = systems[idx]
-            mr = ms[idx]
-            _fill(A[r], s.A, (n, n))
-            if mr:
-                if _dev_D(s):
-                    D[r, :, :mr].copy_(s._d3m_D)
-                else:
-                    _fill(D[r, :, :mr], _coupling_matrix(s), (n, mr))
-            _fill(f[r], s.f, (n,))
-        perm = t.empty((B, n), dtype=t.int64, device="cuda")
-        tags = t.empty((B, n), dtype=t.int8, device="cuda")
-        n2 = t.empty(B, dtype=t.int32, device="cuda")
-        info = t.empty(B, dtype=t.int32, device="cuda")
-        gr = t.empty(B, dtype=t.float64, device="cuda")
-        sc = t.empty(B, dtype=t.float64, device="cuda")
-        asy = t.empty(B, dtype=t.float64, device="cuda")
-        K = empty((B, m, m))
-        g = empty((B, m))
-        wz = empty((B, n, m + 1))
-        wx = empty((B, n, m + 1))
-        wc = empty((B, max(m, 1), m + 1))
-        if n > _lib.PANEL_BK_MIN:
-            nbytes = int(_lib.load().d3m_bk_panel_workspace(n, B))
-            scratch = t.empty((nbytes + 15) // 16, dtype=t.complex128, device="cuda")
-            d_tasks = t.empty(64 * max(B, 2 * ((n + 63) // 64) * B), dtype=t.uint8, device="cuda")
-        else:
-            scratch = empty((B, 4 * n)) if 64 * n > 200 * 1024 else None
-            d_tasks = t.empty(64 * B, dtype=t.uint8, device="cuda")
-        _lib.call("d3m_schur_reduce_batched", B, n, m, _P(A), _P(D), _P(f), float(pivot_tol), _P(perm),
-                  _P(tags), _P(n2), _P(gr), _P(info), _P(sc), _P(asy), _P(K), _P(g), _P(wz), _P(wx), _P(wc),
-                  _P(scratch), _P(d_tasks), stream_ptr())
-        try:
-            facs = _collect(A, perm, tags, n2, info, gr, sc, asy, pivot_tol, None,
-                            wrap=lambda b, msg: SingularDomainError(
-                                f"domain {systems[members[b]].domain} is singular: {msg}"))
-        except (SingularDomainError, ValueError) as err:
-            pos = members[int(_first_bad(info))]
-            if first_error is None or pos < first_error[0]:
-                first_error = (pos, err)
-            continue
-        for r, idx in enumerate(members):
-            s = systems[idx]
-            mr = ms[idx]
-            s.factor = facs[r]
-            s._d3m_D = D[r, :, :mr]
-            out[idx] = (DeviceArray(K[r, :mr, :mr]), DeviceArray(g[r, :mr]))
+        per = _domain_bytes(n, m, r)
+        pos = 0
+        while pos < len(members):
+            budget = max_batch_bytes if max_batch_bytes is not None else int(0.8 * _free_bytes(t))
+            cap = max(1, budget // per)
+            chunk = members[pos:pos + cap]
+            pos += len(chunk)
+            err = _reduce_chunk(systems, chunk, n, m, r, ms, pivot_tol, keep, vec, out)
+            if err is not None and (first_error is None or err[0] < first_error[0]):
+                first_error = err
     if first_error is not None:
         raise first_error[1]
     return out
+
+
+def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out):
+    t = require_cuda()
+    B = len(members)
+    A = empty((B, n, n))
+    D = t.zeros((B, n, m), dtype=t.complex128, device="cuda")
+    f = empty((B, n, r))
+    for i, idx in enumerate(members):
+        s = systems[idx]
+        mr = ms[idx]
+        _fill(A[i], s.A, (n, n))
+        if mr:
+            if _dev_D(s):
+                D[i, :, :mr].copy_(s._d3m_D)
+            else:
+                _fill(D[i, :, :mr], _coupling_matrix(s), (n, mr))
+        _fill(f[i], s.f, (n, r))
+    perm = t.empty((B, n), dtype=t.int64, device="cuda")
+    tags = t.empty((B, n), dtype=t.int8, device="cuda")
+    n2 = t.empty(B, dtype=t.int32, device="cuda")
+    info = t.empty(B, dtype=t.int32, device="cuda")
+    gr = t.empty(B, dtype=t.float64, device="cuda")
+    sc = t.empty(B, dtype=t.float64, device="cuda")
+    asy = t.empty(B, dtype=t.float64, device="cuda")
+    K = empty((B, m, m))
+    g = empty((B, m, r))
+    wz = empty((B, n, m + r))
+    wx = empty((B, n, m + r))
+    wc = empty((B, max(m, 1), m + r))
+    if n > _lib.PANEL_BK_MIN:
+        nbytes = int(_lib.load().d3m_bk_panel_workspace(n, B))
+        scratch = t.empty((nbytes + 15) // 16, dtype=t.complex128, device="cuda")
+        d_tasks = t.empty(64 * max(B, 2 * ((n + 63) // 64) * B), dtype=t.uint8, device="cuda")
+    else:
+        scratch = empty((B, 4 * n)) if 64 * n > 200 * 1024 else None
+        d_tasks = t.empty(64 * B, dtype=t.uint8, device="cuda")
+    _lib.call("d3m_schur_reduce_batched", B, n, m, r, _P(A), _P(D), _P(f), float(pivot_tol), _P(perm),
+              _P(tags), _P(n2), _P(gr), _P(info), _P(sc), _P(asy), _P(K), _P(g), _P(wz), _P(wx), _P(wc),
+              _P(scratch), _P(d_tasks), stream_ptr())
+    del wz, scratch, wc
+    try:
+        facs = _collect(A, perm, tags, n2, info, gr, sc, asy, pivot_tol, None,
+                        wrap=lambda b, msg: SingularDomainError(
+                            f"domain {systems[members[b]].domain} is singular: {msg}"))
+    except (SingularDomainError, ValueError) as err:
+        return (members[int(_first_bad(info))], err)
+    for i, idx in enumerate(members):
+        s = systems[idx]
+        mr = ms[idx]
+        if keep == "factor":
+            s.factor = facs[i]
+            s._d3m_D = D[i, :, :mr]
+            s._d3m_X = None
+        else:
+            s.factor = facs[i].release()
+            s._d3m_D = None
+            s._d3m_X = wx[i]              # [A^-1 D (m padded) | A^-1 F]
+            s._d3m_Xm = m
+        gi = g[i, :mr, 0] if vec else g[i, :mr, :]
+        out[idx] = (DeviceArray(K[i, :mr, :mr]), DeviceArray(gi))
+    return None
 
 
 def _fill(dst, src, shape):
@@ -248,18 +304,6 @@ def _fill(dst, src, shape):
         dst.copy_(to_device(src).reshape(shape))
     else:
         dst.copy_(t.from_numpy(np.ascontiguousarray(np.asarray(src, dtype=np.complex128)).reshape(shape)))
-
-
-def _solve_batch(F, pv, tg, Z, n, m, B, work):
-    """Z (B x n x m) <- A^-1 Z with packed factors F (B x n x n)."""
-    t = require_cuda()
-    if n > _lib.PANEL_BK_MIN:
-        d_tasks = t.empty(64 * 2 * ((n + 63) // 64) * B, dtype=t.uint8, device="cuda")
-        _lib.call("d3m_ldlt_solve_blocked_batched", B, n, _P(F), n * n, _P(pv), n, _P(tg), n, _P(Z), n * m, m, m,
-                  _P(work), _P(d_tasks), stream_ptr())
-    else:
-        _lib.call("d3m_ldlt_solve_batched", B, n, _P(F), n * n, _P(pv), n, _P(tg), n, _P(Z), n * m, m, m,
-                  _P(work), stream_ptr())
 
 
 def _dev_D(s) -> bool:
@@ -312,7 +356,9 @@ def _assemble_host(contrib, gcontrib, sizes):
             KDh = np.asarray(KD)
             K.add_block(ia, ib, KDh[oa:oa + sizes[ia], ob:ob + sizes[ib]])
     K.validate()
-    g = [np.zeros(int(s), dtype=np.complex128) for s in sizes]
+    cols = {np.asarray(gd).shape[1:] for lst in gcontrib.values() for (gd, _, _) in lst}
+    tail = cols.pop() if len(cols) == 1 else ()
+    g = [np.zeros((int(s),) + tuple(tail), dtype=np.complex128) for s in sizes]
     for ia, lst in gcontrib.items():
         for (gd, o, n) in lst:
             g[ia] = g[ia] + np.asarray(gd)[o:o + n]
@@ -327,8 +373,13 @@ def _assemble_device(contrib, gcontrib, sizes):
         koff[key] = tot
         tot += int(sizes[key[0]]) * int(sizes[key[1]])
     goff = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    gcols = {tuple(gd.shape[1:]) for lst in gcontrib.values() for (gd, _, _) in lst}
+    if len(gcols) > 1:
+        raise ValueError("reduced loads carry different numbers of columns")
+    gtail = gcols.pop() if gcols else ()
+    rg = int(gtail[0]) if gtail else 1
     kpool = empty(max(tot, 1))
-    gpool = t.zeros(max(int(goff[-1]), 1), dtype=t.complex128, device="cuda")
+    gpool = t.zeros(max(int(goff[-1]) * rg, 1), dtype=t.complex128, device="cuda")
     rounds: dict[tuple[int, int], list] = {}     # (round, base) -> tasks
 
     def src_of(dev: DeviceArray):
@@ -350,8 +401,13 @@ def _assemble_device(contrib, gcontrib, sizes):
         for r, (gd, o0, n) in enumerate(lst):
             base, st, o = src_of(gd)
             bases[base] = st
-            rounds.setdefault((r, base, "g"), []).append(
-                (o + o0, int(goff[ia]), 1, n, n, n, 0, _lib.COPY_ZERO_ADD if r == 0 else _lib.COPY_ADD))
+            mode = _lib.COPY_ZERO_ADD if r == 0 else _lib.COPY_ADD
+            if not gtail:
+                rec = (o + o0, int(goff[ia]), 1, n, n, n, 0, mode)
+            else:               # g_d is m x rg with row stride ld
+                ld = int(gd.tensor.stride(0))
+                rec = (o + o0 * ld, int(goff[ia]) * rg, n, rg, ld, rg, 0, mode)
+            rounds.setdefault((r, base, "g"), []).append(rec)
     for (r, base, what) in sorted(rounds, key=lambda x: (x[0], x[2], x[1])):
         recs = np.array(rounds[(r, base, what)], dtype=_lib.COPY_TASK)
         st = bases[base]
@@ -366,59 +422,130 @@ def _assemble_device(contrib, gcontrib, sizes):
         o, ni, nj = koff[key], int(sizes[key[0]]), int(sizes[key[1]])
         K.blocks[key] = DeviceArray(kpool[o:o + ni * nj].reshape(ni, nj))
     K._d3m_pool = kpool
-    g = [DeviceArray(gpool[int(goff[i]):int(goff[i + 1])]) for i in range(sizes.size)]
+    if gtail:
+        g = [DeviceArray(gpool[int(goff[i]) * rg:int(goff[i + 1]) * rg].reshape(int(sizes[i]), rg))
+             for i in range(sizes.size)]
+    else:
+        g = [DeviceArray(gpool[int(goff[i]):int(goff[i + 1])]) for i in range(sizes.size)]
     return ReducedSystem(K, g, sizes)
+
+
+def _as_batch(views, shape):
+    """Stack equally shaped device views without a copy when they already sit
+    at a constant stride in one allocation (a reduce batch), else stack."""
+    t = require_cuda()
+    v0 = views[0]
+    numel = int(np.prod(shape))
+    if all(v.is_contiguous() for v in views) and \
+            all(v.untyped_storage().data_ptr() == v0.untyped_storage().data_ptr() for v in views):
+        step = (views[1].data_ptr() - v0.data_ptr()) // v0.element_size() if len(views) > 1 else numel
+        if step >= numel and all(views[i].data_ptr() - v0.data_ptr() == i * step * v0.element_size()
+                                 for i in range(len(views))):
+            return v0.as_strided((len(views),) + tuple(shape), (step,) + tuple(v0.stride())), step
+    return t.stack([v.reshape(shape) for v in views]).contiguous(), numel
 
 
 def recover_primal(systems: list[SubdomainSystem], lam: list) -> np.ndarray | DeviceArray:
     """E_d = A_d^-1 (f_d - D_d lambda) with the cached factors, assembled
-    with averaging of duplicated interface dofs (subdomain.py:217-237)."""
+    with averaging of duplicated interface dofs (subdomain.py:217-237).
+    Multi-column loads (lambda_i of shape size_i x r) give E of shape
+    n_glob x r.  Domains reduced with keep="solution" use
+    E_d = X_F - X_D lambda_d instead of a solve."""
     t = require_cuda()
     for s in systems:
-        if s.factor is None:
+        if s.factor is None or (s.factor.released and getattr(s, "_d3m_X", None) is None):
             raise SolverStateError(f"domain {s.domain} has no cached factorization; run reduce_domain first")
     device_in = all(isinstance(v, DeviceArray) for v in lam)
-    lam_dev = [to_device(v).reshape(-1) for v in lam]
+    lam_dev = [to_device(v) for v in lam]
+    r = max([int(v.shape[1]) if v.dim() == 2 else 1 for v in lam_dev] + [1])
+    one_d = all(v.dim() == 1 for v in lam_dev)
+    lam_dev = [v.reshape(int(v.shape[0]), r) for v in lam_dev]
     n_glob = 1 + max(int(np.max(s.dof_map)) for s in systems)
-    # group by (n, m), E stored group after group
+    e_off, o = [], 0
+    for s in systems:
+        e_off.append(o)
+        o += s.n_dofs
+    ET = empty((r, max(o, 1)))                    # E^T: column q of every domain contiguous
+
+    def lam_of(s):
+        parts = [lam_dev[c.interface] for c in s.couplings if np.shape(c.D)[1]]
+        return t.cat(parts) if parts else t.zeros((0, r), dtype=t.complex128, device="cuda")
+
+    # -- domains with a cached factor: batched solves per (n, m) group
     groups: dict[tuple[int, int], list[int]] = {}
     for idx, s in enumerate(systems):
-        m = sum(int(np.shape(c.D)[1]) for c in s.couplings)
-        groups.setdefault((s.n_dofs, m), []).append(idx)
-    order = [idx for key in groups for idx in groups[key]]
-    e_off = {}
-    o = 0
-    for idx in order:
-        e_off[idx] = o
-        o += systems[idx].n_dofs
-    E = empty(max(o, 1))
+        if not s.factor.released:
+            m = sum(int(np.shape(c.D)[1]) for c in s.couplings)
+            groups.setdefault((s.n_dofs, m), []).append(idx)
     for (n, m), members in groups.items():
         B = len(members)
-        base = e_off[members[0]]
-        rhs = E[base:base + B * n].reshape(B, n)
-        for r, idx in enumerate(members):
-            rhs[r].copy_(to_device(systems[idx].f).reshape(n))
-        F = t.stack([systems[idx].factor.packed for idx in members]).contiguous()
-        pv = t.stack([systems[idx].factor.perm_dev for idx in members]).contiguous()
-        tg = t.stack([systems[idx].factor.tags_dev for idx in members]).contiguous()
+        rhs = empty((B, n, r))
+        for i, idx in enumerate(members):
+            rhs[i].copy_(to_device(systems[idx].f).reshape(n, r))
+        F, sf = _as_batch([systems[idx].factor.packed for idx in members], (n, n))
+        pv, sp = _as_batch([systems[idx].factor.perm_dev for idx in members], (n,))
+        tg, st = _as_batch([systems[idx].factor.tags_dev for idx in members], (n,))
         if m:
-            D = t.stack([s._d3m_D if _dev_D(s) else to_device(_coupling_matrix(s))
-                         for s in (systems[idx] for idx in members)]).contiguous()
-            lamc = t.stack([t.cat([lam_dev[c.interface] for c in systems[idx].couplings if np.shape(c.D)[1]]
-                                  or [t.zeros(0, dtype=t.complex128, device="cuda")])
-                            for idx in members]).contiguous()
+            D, sd = _as_batch([s._d3m_D if _dev_D(s) else to_device(_coupling_matrix(s))
+                               for s in (systems[idx] for idx in members)], (n, m))
+            lamc = t.stack([lam_of(systems[idx]) for idx in members]).contiguous()
             tasks = np.zeros(B, dtype=_lib.GEMM_TASK)
-            tasks["a_off"] = np.arange(B) * n * m
-            tasks["b_off"] = np.arange(B) * m
-            tasks["c_off"] = np.arange(B) * n
-            tasks["m"], tasks["n"], tasks["k"] = n, 1, m
-            tasks["lda"], tasks["ldb"], tasks["ldc"] = m, 1, 1
+            tasks["a_off"] = np.arange(B) * sd
+            tasks["b_off"] = np.arange(B) * m * r
+            tasks["c_off"] = np.arange(B) * n * r
+            tasks["m"], tasks["n"], tasks["k"] = n, r, m
+            tasks["lda"], tasks["ldb"], tasks["ldc"] = int(D.stride(1)), r, r
             tasks["flags"] = _lib.GEMM_SUB
             d_tasks = t.empty(64 * B, dtype=t.uint8, device="cuda")
             _lib.call("d3m_zgemm_grouped", 0, 1, _P(D), _P(lamc), _P(rhs), _lib.hptr(tasks), B, _P(d_tasks),
                       stream_ptr())
-        work = empty((B, n))
-        _solve_batch(F, pv, tg, rhs, n, 1, B, work)
+        work = empty((B, n, r))
+        if n > _lib.PANEL_BK_MIN:
+            d_tasks = t.empty(64 * 2 * ((n + 63) // 64) * B, dtype=t.uint8, device="cuda")
+            _lib.call("d3m_ldlt_solve_blocked_batched", B, n, _P(F), sf, _P(pv), sp, _P(tg), st, _P(rhs), n * r,
+                      r, r, _P(work), _P(d_tasks), stream_ptr())
+        else:
+            _lib.call("d3m_ldlt_solve_batched", B, n, _P(F), sf, _P(pv), sp, _P(tg), st, _P(rhs), n * r, r, r,
+                      _P(work), stream_ptr())
+        for i, idx in enumerate(members):
+            ET[:, e_off[idx]:e_off[idx] + n].copy_(rhs[i].t())
+    # -- domains reduced with keep="solution": E_d = X_F - X_D lambda_d
+    sol = [idx for idx, s in enumerate(systems) if s.factor.released]
+    by_base: dict[int, list[int]] = {}
+    for idx in sol:
+        by_base.setdefault(systems[idx]._d3m_X.untyped_storage().data_ptr(), []).append(idx)
+    for base, members in by_base.items():
+        Xst = systems[members[0]]._d3m_X
+        whole = t.empty(0, dtype=t.complex128, device="cuda").set_(
+            Xst.untyped_storage(), 0, (Xst.untyped_storage().nbytes() // 16,))
+        lams = [lam_of(systems[idx]) for idx in members]
+        loff = np.concatenate([[0], np.cumsum([int(v.numel()) for v in lams])]).astype(np.int64)
+        lamc = t.cat([v.reshape(-1) for v in lams] + [t.zeros(1, dtype=t.complex128, device="cuda")])
+        goff = np.concatenate([[0], np.cumsum([systems[idx].n_dofs for idx in members])]).astype(np.int64)
+        Eg = empty((int(goff[-1]), r))
+        tasks = []
+        for i, idx in enumerate(members):
+            s = systems[idx]
+            X, mp, n = s._d3m_X, s._d3m_Xm, s.n_dofs
+            mr = int(lams[i].shape[0])
+            Eg[int(goff[i]):int(goff[i + 1])].copy_(X[:, mp:mp + r])
+            if mr:
+                tk = np.zeros(1, dtype=_lib.GEMM_TASK)
+                tk["a_off"] = (X.data_ptr() - base) // 16
+                tk["b_off"] = loff[i]
+                tk["c_off"] = goff[i] * r
+                tk["m"], tk["n"], tk["k"] = n, r, mr
+                tk["lda"], tk["ldb"], tk["ldc"] = int(X.stride(0)), r, r
+                tk["flags"] = _lib.GEMM_SUB
+                tasks.append(tk)
+        if tasks:
+            tk = np.concatenate(tasks)
+            d_tasks = t.empty(64 * len(tk), dtype=t.uint8, device="cuda")
+            _lib.call("d3m_zgemm_grouped", 0, 1, _P(whole), _P(lamc), _P(Eg), _lib.hptr(tk), len(tk),
+                      _P(d_tasks), stream_ptr())
+        for i, idx in enumerate(members):
+            n = systems[idx].n_dofs
+            ET[:, e_off[idx]:e_off[idx] + n].copy_(Eg[int(goff[i]):int(goff[i + 1])].t())
     # ordered average: contributions per global dof in ascending domain order
     gl, src = [], []
     for idx in range(len(systems)):          # acc[dof_map] += E in list order
@@ -430,9 +557,11 @@ def recover_primal(systems: list[SubdomainSystem], lam: list) -> np.ndarray | De
     order_ = np.argsort(gl, kind="stable")
     counts = np.bincount(gl, minlength=n_glob)
     ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-    out = empty(n_glob)
-    d_ptr, d_src = upload_i64(ptr), upload_i64(src[order_])   # both alive across the launch
-    _lib.call("d3m_ordered_average", _P(E), _P(d_ptr), _P(d_src), _P(out), n_glob, stream_ptr())
+    outT = empty((r, n_glob))
+    d_ptr, d_src = upload_i64(ptr), upload_i64(src[order_])   # both alive across the launches
+    for q in range(r):
+        _lib.call("d3m_ordered_average", _P(ET[q]), _P(d_ptr), _P(d_src), _P(outT[q]), n_glob, stream_ptr())
+    out = outT[0] if one_d else outT.t().contiguous()
     if device_in:
         return DeviceArray(out)
     return out.cpu().numpy()

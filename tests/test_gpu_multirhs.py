@@ -1,0 +1,86 @@
+"""Multi-RHS reduce/recover, memory-chunked batches and keep="solution".
+
+The reference reduces one load column per call (subdomain.py:177-179); the
+device path carries r columns through one factorisation.  Every column is
+computed independently (fixed summation order per output entry), so these
+tests demand bitwise equality with single-column runs, and compare the
+solution-keeping recovery (E = X_F - X_D lambda) with the reference's
+factor-based one (E = A^-1 (F - D lambda)) to 1e-9."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _systems(n, m, batch, r, seed):
+    import paper_2002_05018_b200 as d
+    rng = np.random.default_rng(seed)
+    out = []
+    for b in range(batch):
+        G = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2 * n)
+        A = (G + G.T) / 2
+        A[np.diag_indices(n)] += rng.uniform(-1, 1, n) + 1j * rng.uniform(-0.1, 0.1, n)
+        D = np.zeros((n, m), dtype=complex)
+        D[rng.choice(n, m, replace=False), np.arange(m)] = rng.choice([-1.0, 1.0], m)
+        F = rng.standard_normal((n, r)) + 1j * rng.standard_normal((n, r))
+        out.append(d.SubdomainSystem(b, A, F, np.arange(n), [d.Coupling(0, D, 1)]))
+    return out
+
+
+@pytest.mark.parametrize("n,m", [(200, 24), (700, 31)])
+def test_multi_rhs_reduce_equals_single_column_runs(cuda, oracle, n, m):
+    import paper_2002_05018_b200 as d
+    r = 3
+    multi = _systems(n, m, 2, r, seed=n)
+    red = d.reduce_domains(multi)
+    for q in range(r):
+        single = [d.SubdomainSystem(s.domain, s.A, np.ascontiguousarray(s.f[:, q]), s.dof_map, s.couplings)
+                  for s in multi]
+        red1 = d.reduce_domains(single)
+        for (K, G), (K1, g1), s in zip(red, red1, multi):
+            assert np.array_equal(np.asarray(K), np.asarray(K1))
+            assert np.array_equal(np.asarray(G)[:, q], np.asarray(g1))
+            if q == 0:
+                Ko, go, fo = oracle.reduce_domain(s.A, s.couplings[0].D, s.f[:, 0])
+                assert np.array_equal(s.factor.perm, fo.perm)
+                assert np.linalg.norm(np.asarray(K) - Ko) <= 1e-10 * np.linalg.norm(Ko)
+                assert np.linalg.norm(np.asarray(G)[:, 0] - go) <= 1e-10 * np.linalg.norm(go)
+
+
+@pytest.mark.parametrize("n", [300, 600])
+def test_chunked_reduce_is_bitwise_identical(cuda, n):
+    """Batches split by the memory budget (one domain per batch here) give the
+    same factors and Schur blocks bit for bit (cluster size of the panel
+    kernel changes with the batch; per-row arithmetic does not)."""
+    import paper_2002_05018_b200 as d
+    a = _systems(n, 20, 3, 1, seed=7 * n)
+    b = _systems(n, 20, 3, 1, seed=7 * n)
+    ra = d.reduce_domains(a)
+    rb = d.reduce_domains(b, max_batch_bytes=1)
+    for (Ka, ga), (Kb, gb), sa, sb in zip(ra, rb, a, b):
+        assert np.array_equal(np.asarray(Ka), np.asarray(Kb))
+        assert np.array_equal(np.asarray(ga), np.asarray(gb))
+        assert np.array_equal(sa.factor.perm, sb.factor.perm)
+        assert np.array_equal(np.asarray(sa.factor.packed.cpu()), np.asarray(sb.factor.packed.cpu()))
+
+
+@pytest.mark.parametrize("cells,parts", [(4, (2, 2, 2)), (8, (2, 1, 1))])
+def test_keep_solution_recovery_matches_factor_recovery(cuda, cells, parts):
+    from paper_2002_05018_b200 import SolverStateError, fem3d
+    prob = fem3d.FemProblem(cells, 0.5, parts, sphere_radius=0.15,
+                            polarisations=((1.0, 0.0, 0.0), (0.0, 1.0, 0.0)),
+                            directions=((0.0, 0.0, 1.0), (0.0, 0.0, -1.0)))
+    model = fem3d.build_model(prob)
+    sol_f, sys_f, *_ = fem3d.solve_d3m(model, rhs=None, keep="factor")
+    sol_s, sys_s, *_ = fem3d.solve_d3m(model, rhs=None, keep="solution")
+    assert sol_f.shape == (model.mesh.n_edges, 2)
+    assert np.linalg.norm(sol_s - sol_f) <= 1e-9 * np.linalg.norm(sol_f)
+    assert fem3d.global_residual(model, sol_s, rhs=None) <= 1e-10
+    assert all(s.factor.released for s in sys_s)
+    assert np.array_equal(sys_s[0].factor.perm, sys_f[0].factor.perm)
+    with pytest.raises(SolverStateError):
+        sys_s[0].factor.solve(np.ones(sys_s[0].n_dofs))
+    # all-RHS solve == per-column solves
+    for q in range(2):
+        sol_q, *_ = fem3d.solve_d3m(model, rhs=q, keep="factor")
+        assert np.linalg.norm(sol_f[:, q] - sol_q) <= 1e-13 * np.linalg.norm(sol_q)
