@@ -137,8 +137,14 @@ int d3m_ldlt_solve_batched(int batch, int n, const void* F, int64_t stride_f, co
 
 // Blocked multi-RHS solve for large factors (n > kBlockedSolveMin): gather,
 // 64-row diagonal solves + right-looking DMMA GEMM updates (forward, then
-// backward with L^T), D^-1, scatter.  d_tasks: >= 2 * ceil(n/64) * batch GEMM
-// records.
+// backward with L^T), D^-1, scatter.  Two-level blocking: inside a 256-row
+// outer block each 64-row block updates only the rest of its outer block
+// (K = 64, <= 192 rows); the last 64-row block of an outer block applies the
+// whole outer block to every remaining row with one K = 256 GEMM, which runs
+// near the DMMA roofline where K = 64 tiles do not.  Each 64-row block still
+// owns exactly one GEMM, so every straddling 2x2 e-entry is applied once and
+// corrected once by the next diagonal kernel.  d_tasks: >= 2 * ceil(n/64) *
+// batch GEMM records.
 int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stride_f, const void* perm,
                                    int64_t stride_p, const void* tags, int64_t stride_t, void* B, int64_t stride_b,
                                    int ldb, int m, void* work, void* d_tasks, void* stream) {
@@ -146,6 +152,7 @@ int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stri
   if (batch == 0 || n == 0 || m == 0) return 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int DBR = d3m_diag_block_rows();
+  const int OBR = 4 * DBR;                       // outer block rows
   const int nblk = (n + DBR - 1) / DBR;
   const int64_t sz = (int64_t)n * m;
   d3m::SolveBatch sb{CC(F), stride_f, static_cast<const int8_t*>(tags), stride_t, static_cast<const int64_t*>(perm),
@@ -155,18 +162,35 @@ int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stri
   std::memset(t.data(), 0, sizeof(d3m::GemmTask) * t.size());
   std::vector<int> tiles(2 * nblk, 0);
   for (int ib = 0; ib < nblk; ++ib) {
-    const int r0 = ib * DBR, r1 = std::min(n, r0 + DBR), below = n - r1;
+    const int r0 = ib * DBR, r1 = std::min(n, r0 + DBR);
+    const int R0 = (r0 / OBR) * OBR, R1 = std::min(n, R0 + OBR);
     for (int b = 0; b < batch; ++b) {
-      d3m::GemmTask& f = t[(size_t)ib * batch + b];      // Z[r1:] -= L[r1:, r0:r1] Z[r0:r1]
-      f.a_off = b * stride_f + (int64_t)r1 * n + r0;
-      f.b_off = b * sz + (int64_t)r0 * m;
-      f.c_off = b * sz + (int64_t)r1 * m;
-      f.m = below; f.n = m; f.k = r1 - r0; f.lda = n; f.ldb = m; f.ldc = m; f.flags = d3m::kGemmSub;
-      d3m::GemmTask& g = t[(size_t)(nblk + ib) * batch + b];   // Z[:r0] -= L[r0:r1, :r0]^T Z[r0:r1]
-      g.a_off = b * stride_f + (int64_t)r0 * n;
-      g.b_off = b * sz + (int64_t)r0 * m;
-      g.c_off = b * sz;
-      g.m = r0; g.n = m; g.k = r1 - r0; g.lda = n; g.ldb = m; g.ldc = m; g.flags = d3m::kGemmSub;
+      d3m::GemmTask& f = t[(size_t)ib * batch + b];
+      if (r1 < R1) {          // Z[r1:R1] -= L[r1:R1, r0:r1] Z[r0:r1]
+        f.a_off = b * stride_f + (int64_t)r1 * n + r0;
+        f.b_off = b * sz + (int64_t)r0 * m;
+        f.c_off = b * sz + (int64_t)r1 * m;
+        f.m = R1 - r1; f.k = r1 - r0;
+      } else {                // Z[R1:] -= L[R1:, R0:R1] Z[R0:R1]
+        f.a_off = b * stride_f + (int64_t)R1 * n + R0;
+        f.b_off = b * sz + (int64_t)R0 * m;
+        f.c_off = b * sz + (int64_t)R1 * m;
+        f.m = n - R1; f.k = R1 - R0;
+      }
+      f.n = m; f.lda = n; f.ldb = m; f.ldc = m; f.flags = d3m::kGemmSub;
+      d3m::GemmTask& g = t[(size_t)(nblk + ib) * batch + b];
+      if (r0 > R0) {          // Z[R0:r0] -= L[r0:r1, R0:r0]^T Z[r0:r1]
+        g.a_off = b * stride_f + (int64_t)r0 * n + R0;
+        g.b_off = b * sz + (int64_t)r0 * m;
+        g.c_off = b * sz + (int64_t)R0 * m;
+        g.m = r0 - R0; g.k = r1 - r0;
+      } else {                // Z[:R0] -= L[R0:R1, :R0]^T Z[R0:R1]
+        g.a_off = b * stride_f + (int64_t)R0 * n;
+        g.b_off = b * sz + (int64_t)R0 * m;
+        g.c_off = b * sz;
+        g.m = R0; g.k = R1 - R0;
+      }
+      g.n = m; g.lda = n; g.ldb = m; g.ldc = m; g.flags = d3m::kGemmSub;
     }
     tiles[ib] = d3m_gemm_prepare_tasks(&t[(size_t)ib * batch], batch);
     tiles[nblk + ib] = d3m_gemm_prepare_tasks(&t[(size_t)(nblk + ib) * batch], batch);

@@ -210,12 +210,13 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
     out = [None] * len(systems)
     first_error = None
     for n, members in groups.items():
-        m = max(ms[i] for i in members)
-        per = _domain_bytes(n, m, r)
+        # largest coupling first, so each memory-sized batch pads to a close m
+        members = sorted(members, key=lambda i: -ms[i])
         pos = 0
         while pos < len(members):
+            m = ms[members[pos]]
             budget = max_batch_bytes if max_batch_bytes is not None else int(0.8 * _free_bytes(t))
-            cap = max(1, budget // per)
+            cap = max(1, budget // _domain_bytes(n, m, r))
             chunk = members[pos:pos + cap]
             pos += len(chunk)
             err = _reduce_chunk(systems, chunk, n, m, r, ms, pivot_tol, keep, vec, out)
