@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -115,7 +116,12 @@ int d3m_bk_blocked_factor(int batch, int n, void* W, int64_t stride_w, int lda, 
   d3m::BkArgs a{C(W), stride_w, n, lda, pivot_tol, check_sym, static_cast<int64_t*>(perm), static_cast<int8_t*>(tags),
                 static_cast<int32_t*>(n2x2), static_cast<double*>(growth), static_cast<int32_t*>(info),
                 static_cast<double*>(scale), static_cast<double*>(asym), C(scratch)};
+  const char* dbk = getenv("D3M_DIAG_BK");      // dev switch: 'c' = cluster-resident exact kernel
   D3M_TRY(launch(kClsBk, stream, [&] {
+    if (dbk && dbk[0] == 'c') {
+      const int rc = d3m_bk_cluster_launch(&a, batch, stream);
+      if (rc != -22) return rc;
+    }
     const int rc = d3m_bk_blocked_launch(&a, batch, stream);
     return rc == -22 ? d3m_bk_launch(&a, batch, stream) : rc;
   }));
@@ -349,6 +355,9 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                         void* d_perm, void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale,
                         void* d_asym, void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead,
                         void* stream) {
+  // diagonal BK kernel for supernodes > kExactBkMax: 0 cluster (default), 1 blocked
+  const char* dbk = getenv("D3M_DIAG_BK");
+  const int diag_bk_mode = (dbk && dbk[0] == 'b') ? 1 : 0;
   // Streams: the caller's stream hands over to a high-priority critical
   // stream (BK -> L^-1 -> panel GEMM -> D^-1 -> next-column update) and a
   // low-priority bulk stream (the rest of each column's trailing update).
@@ -404,10 +413,15 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
     if (nj > 0) {
       // supernodes up to kExactBkMax use the bit-exact unblocked kernel (so a
       // one-block K factors exactly like dense_ldlt_bk, test_block_factor.py:
-      // 24-32); wider ones the blocked shared-memory panel kernel (pivots
-      // identical, values to rounding), or the exact one if no panel fits
+      // 24-32); wider ones the bit-exact cluster kernel (lower triangle in the
+      // cluster's shared memory), else the blocked shared-memory panel kernel
+      // (pivots identical, values to rounding), else the exact one
       D3M_TRY(launch(kClsBk, s0, [&] {
         if (nj <= kExactBkMax) return d3m_bk_launch(&a, 1, s0);
+        if (diag_bk_mode != 1) {          // cluster-resident exact BK (bk_cluster.cu)
+          const int rc = d3m_bk_cluster_launch(&a, 1, s0);
+          if (rc != -22) return rc;
+        }
         const int rc = d3m_bk_blocked_launch(&a, 1, s0);
         return rc == -22 ? d3m_bk_launch(&a, 1, s0) : rc;
       }));

@@ -176,6 +176,30 @@ def test_reference_kats(cuda):
         d.block_ldlt(K, _plan(K, d.identity_ordering(2)))
 
 
+@pytest.mark.parametrize("n,sym_exact", [(200, True), (256, True), (257, False), (360, True)])
+def test_cluster_diag_bk_is_bit_exact(cuda, monkeypatch, n, sym_exact):
+    """Supernodes wider than 128 take the cluster-resident exact BK
+    (bk_cluster.cu): a one-block K factors bit for bit like dense_ldlt_bk
+    (the single-CTA exact kernel) -- L, d, e, perm, tags, growth -- for the
+    known-symmetric prologue and the full symmetry check alike, and for every
+    cluster size."""
+    import paper_2002_05018_b200 as d
+    M = rand_complex_symmetric(n, n)
+    M[np.diag_indices(n)] += np.random.default_rng(n).uniform(-1, 1, n)
+    if not sym_exact:       # not exactly symmetric (within 1e-12): full check path
+        M[5, 3] += 1e-15 * abs(M[5, 3])
+    ref = d.dense_ldlt_bk(M)
+    assert ref.n_2x2 > 0
+    for cs in ("8", "4", "2"):          # a size that does not fit falls back to 8
+        monkeypatch.setenv("D3M_BKC_CS", cs)
+        K = d.from_blocks([n], [(0, 0, M)])
+        F = d.block_ldlt(K, _plan(K))
+        f = F.diag[0]
+        assert np.array_equal(f.perm, ref.perm) and np.array_equal(f.tags, ref.tags)
+        assert np.array_equal(f.L, ref.L) and np.array_equal(f.d, ref.d) and np.array_equal(f.e, ref.e)
+        assert F.stats.growth_factor == ref.growth
+
+
 def test_multi_rhs_equals_single_rhs_bitwise(cuda):
     import paper_2002_05018_b200 as d
     from paper_2002_05018_b200 import workloads as wl
