@@ -494,11 +494,15 @@ int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_of
                          const int64_t* h_binv_off, const int64_t* h_gptr, const void* d_gidx, const void* d_pool,
                          const void* d_binv, const void* d_tags, void* d_b, void* d_u, void* d_x, void* d_tmp,
                          void* d_part, int64_t part_elems, int nrhs, void* stream) {
+  // Forward (per column j, plan order):  z = Binv_j b_j;  u_j = D_j^-1 z;  b_i -= L_ij z
+  // Backward (reverse):  w = u_j - sum_i L_ij^T x_i (split-K partials, ordered
+  // reduce);  x_j = Binv_j^T w.  All products on DMMA (skinny_dmma.cu), in
+  // passes of 16 RHS.  d_part: >= ceil(R_j / 256) * n_j * 16 complex.
   if (nb <= 0 || nrhs <= 0) return 0;
-  const int RC = d3m_solve_rows_per_chunk();
+  constexpr int KCH = 256, NP = 16;
   for (int j = 0; j < nb; ++j) {
     const int64_t nj = h_sizes[j], R = h_panel_rows[j];
-    const int64_t need = ((std::max(R, nj) + RC - 1) / RC) * nj * nrhs;
+    const int64_t need = ((R + KCH - 1) / KCH) * nj * NP;
     if (need > part_elems) return fail(-22, "d3m_block_solve_exec: partial buffer too small");
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -510,45 +514,56 @@ int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_of
   cplx* x = C(d_x);
   cplx* tmp = C(d_tmp);
   const int N = nrhs;
+  auto sk = [&](int ta, const cplx* A, int lda, int M, int K, const cplx* Bp, const int64_t* bmap, cplx* Cp,
+                const int64_t* cmap, int mode, int kchunk, int c0) -> int {
+    const int np = std::min(NP, N - c0);
+    const int rc = d3m_skinny_launch(ta, A, lda, M, K, Bp + c0, N, bmap, np, mode == 2 ? Cp : Cp + c0, N, cmap,
+                                     mode, kchunk, s);
+    return rc < 0 ? -rc : 0;
+  };
   for (int j = 0; j < nb; ++j) {
     const int nj = (int)h_sizes[j];
     const int R = (int)h_panel_rows[j];
     if (nj == 0) continue;
     const int8_t* tags = static_cast<const int8_t*>(d_tags) + h_piv_off[j];
-    D3M_TRY(launch(kClsSolve, s, [&] {
-      return d3m_rows_gemv_launch(binv + h_binv_off[j], nj, nj, nj, b + h_row_off[j] * N, N, N, tmp, N, nullptr, 0, s);
-    }));
+    for (int c0 = 0; c0 < N; c0 += NP)
+      D3M_TRY(launch(kClsSolve, s, [&] {
+        return sk(0, binv + h_binv_off[j], nj, nj, nj, b + h_row_off[j] * N, nullptr, tmp, nullptr, 0, 0, c0);
+      }));
     D3M_TRY(launch(kClsSolve, s, [&] {
       return d3m_dinv_left_copy_launch(tmp, u + h_row_off[j] * N, nj, N, pool + h_diag_off[j], tags, s);
     }));
     if (R > 0)
-      D3M_TRY(launch(kClsSolve, s, [&] {
-        return d3m_rows_gemv_launch(pool + h_panel_off[j], nj, R, nj, tmp, N, N, b, N, gidx + h_gptr[j], 1, s);
-      }));
+      for (int c0 = 0; c0 < N; c0 += NP)
+        D3M_TRY(launch(kClsSolve, s, [&] {
+          return sk(0, pool + h_panel_off[j], nj, R, nj, tmp, nullptr, b, gidx + h_gptr[j], 1, 0, c0);
+        }));
   }
   for (int j = nb - 1; j >= 0; --j) {
     const int nj = (int)h_sizes[j];
     const int R = (int)h_panel_rows[j];
     if (nj == 0) continue;
     cplx* uj = u + h_row_off[j] * N;
-    const int64_t len = (int64_t)nj * N;
-    if (R > 0) {
-      D3M_TRY(launch(kClsSolve, s, [&] {
-        return d3m_cols_gemv_launch(pool + h_panel_off[j], nj, R, nj, x, N, gidx + h_gptr[j], N, d_part, s);
-      }));
-      const int nch = (R + RC - 1) / RC;
-      D3M_TRY(launch(kClsSolve, s, [&] { return d3m_chunk_reduce_launch(uj, d_part, nch, len, -1.0, tmp, s); }));
-    } else {
-      cudaError_t ce = cudaMemcpyAsync(tmp, uj, sizeof(cplx) * len, cudaMemcpyDeviceToDevice, s);
-      if (ce != cudaSuccess) return fail((int)ce, "d3m_block_solve_exec: copy");
+    for (int c0 = 0; c0 < N; c0 += NP) {
+      const int np = std::min(NP, N - c0);
+      if (R > 0) {
+        D3M_TRY(launch(kClsSolve, s, [&] {
+          return sk(1, pool + h_panel_off[j], nj, nj, R, x, gidx + h_gptr[j], C(d_part), nullptr, 2, KCH, c0);
+        }));
+        const int nch = (R + KCH - 1) / KCH;
+        D3M_TRY(launch(kClsSolve, s, [&] {
+          return d3m_skinny_reduce_launch(uj + c0, N, d_part, nch, nj, np, -1.0, tmp + c0, N, s);
+        }));
+      } else {
+        D3M_TRY(launch(kClsSolve, s, [&] {
+          return d3m_skinny_reduce_launch(uj + c0, N, d_part, 0, nj, np, -1.0, tmp + c0, N, s);
+        }));
+      }
     }
-    D3M_TRY(launch(kClsSolve, s, [&] {
-      return d3m_cols_gemv_launch(binv + h_binv_off[j], nj, nj, nj, tmp, N, nullptr, N, d_part, s);
-    }));
-    const int nch = (nj + RC - 1) / RC;
-    D3M_TRY(launch(kClsSolve, s, [&] {
-      return d3m_chunk_reduce_launch(nullptr, d_part, nch, len, 1.0, x + h_row_off[j] * N, s);
-    }));
+    for (int c0 = 0; c0 < N; c0 += NP)
+      D3M_TRY(launch(kClsSolve, s, [&] {
+        return sk(1, binv + h_binv_off[j], nj, nj, nj, tmp, nullptr, x + h_row_off[j] * N, nullptr, 0, 0, c0);
+      }));
   }
   return 0;
 }

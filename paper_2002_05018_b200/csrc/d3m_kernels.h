@@ -41,6 +41,10 @@ extern "C" {
 int d3m_bk_launch(d3m::BkArgs* a, int batch, void* stream);
 int d3m_bk_blocked_launch(d3m::BkArgs* a, int batch, void* stream);
 int d3m_bk_cluster_launch(d3m::BkArgs* a, int batch, void* stream);
+int d3m_skinny_launch(int ta, const void* A, int lda, int M, int K, const void* B, int ldb, const void* bmap, int N,
+                      void* C, int ldc, const void* cmap, int mode, int kchunk, void* stream);
+int d3m_skinny_reduce_launch(const void* base, int ldb, const void* part, int nch, int M, int np, double sign,
+                             void* out, int ldo, void* stream);
 // phase: 0 gather Z=B[perm], 1 forward (+U=D^-1 Z), 2 D^-1, 3 backward, 4 scatter B[perm]=Z
 int d3m_solve_phase_launch(int phase, d3m::SolveBatch* a, int batch, void* stream);
 int d3m_panel_trsm_launch(void* P, void* X, int R, int n, const void* F, const void* perm, const void* tags,

@@ -1,0 +1,226 @@
+// skinny_dmma.cu -- tall-skinny complex GEMM on the FP64 tensor pipe for the
+// block substitutions (block_solve, factor.py:271-310) with few RHS.
+//
+//   C[cmap(r)][c]  op=  sum_k A(r, k) B[bmap(k)][c]      r < M, c < N <= 16 per pass
+//
+// A(r, k) = A[r*lda + k] (TA = 0: z = Binv b, b_i -= L_ij z) or A[k*lda + r]
+// (TA = 1: L_ij^T x_i, Binv^T w).  With 16 RHS every factor entry feeds 16
+// complex FMAs (8 flop/B), which the FP64 CUDA-core pipe cannot sustain at
+// HBM speed; DMMA m8n8k4 takes 16 RHS as exactly two n-tiles.
+//
+// CTA tile 16 rows x 16 RHS; its 4 warps split K (64-row slices, each warp
+// its own 4-deep cp.async ring, 2 x 2 DMMA sub-tiles with (re, im)
+// accumulators) and add their sums in warp order at the end: the dependent
+// chain per warp is 4x shorter than one warp walking all of K, and small
+// products get 4x more CTAs.  gridDim.y > 1 splits K into chunks of kchunk rows; each chunk writes
+// its partial sums (no atomics) for an ordered reduction afterwards.  The
+// summation order of an output entry depends only on K and the chunking, so a
+// k-RHS solve equals k single-RHS solves bit for bit.
+#include <algorithm>
+#include "d3m_common.cuh"
+#include "d3m_kernels.h"
+
+namespace d3m {
+
+constexpr int SN_BM = 16, SN_BN = 16, SN_BK = 8, SN_ST = 4, SN_PA = SN_BK + 4, SN_PB = SN_BN + 2, SN_NT = 128;
+constexpr int SN_NW = SN_NT / 32;
+constexpr int SN_KW = 64;                  // K rows per warp and CTA pass (a CTA covers 256 K rows)
+
+struct SnWarpSmem {                        // one warp's private staging ring
+  cplx A[SN_ST][SN_BM][SN_PA];
+  cplx B[SN_ST][SN_BK][SN_PB];
+};
+constexpr size_t kSnSmem = sizeof(SnWarpSmem) * SN_NW;
+
+__device__ __forceinline__ void sn_cp16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void sn_dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// one warp stages A(16 rows x 8 k) and B(8 k x 16 RHS): 4 + 4 chunks per lane
+template <bool TA>
+__device__ __forceinline__ void sn_load(SnWarpSmem& S, int st, const cplx* A, int lda, int M, const cplx* B, int ldb,
+                                        const int64_t* bmap, int N, int m0, int k0, int kend, int lane) {
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int e = p * 32 + lane;
+    int r, k;
+    if (!TA) { r = e >> 3; k = e & 7; }      // 8 lanes per 128-byte row segment
+    else { r = e & 15; k = e >> 4; }         // 16 lanes per 256-byte stored row
+    const bool ok = (m0 + r < M) && (k0 + k < kend);
+    const cplx* g = TA ? A + (int64_t)(k0 + k) * lda + m0 + r : A + (int64_t)(m0 + r) * lda + k0 + k;
+    sn_cp16(&S.A[st][r][k], ok ? g : A, ok);
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int e = p * 32 + lane, k = e >> 4, c = e & 15;
+    const bool ok = (k0 + k < kend) && (c < N);
+    const int64_t row = bmap ? bmap[ok ? k0 + k : 0] : (int64_t)(k0 + k);
+    sn_cp16(&S.B[st][k][c], ok ? B + row * ldb + c : B, ok);
+  }
+}
+
+// mode: 0 store, 1 subtract, 2 partial (part[(chunk * M + r) * N + c])
+// CTA: 16 rows x 16 RHS over K rows [kbeg, kbeg + 256 * passes) of its chunk;
+// warp w takes the 64-row slices w, w + 4, ...; the four warp sums are added
+// in warp order at the end (fixed order, independent of N).
+template <bool TA>
+__global__ void __launch_bounds__(SN_NT)
+skinny_dmma_kernel(const cplx* __restrict__ A, int lda, int M, int K, const cplx* __restrict__ B, int ldb,
+                   const int64_t* __restrict__ bmap, int N, cplx* C, int ldc, const int64_t* __restrict__ cmap,
+                   int mode, int kchunk) {
+  extern __shared__ __align__(128) unsigned char sn_smem[];
+  SnWarpSmem* ws = reinterpret_cast<SnWarpSmem*>(sn_smem);
+  const int m0 = blockIdx.x * SN_BM;
+  const int chunk = blockIdx.y;
+  const int kbeg = chunk * kchunk, kend = min(K, kbeg + kchunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  SnWarpSmem& S = ws[warp];
+  double acc_re[2][2][2], acc_im[2][2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
+  // this warp's k-tiles: slices of SN_KW rows, strided by SN_NW slices
+  const int tiles_per_slice = SN_KW / SN_BK;
+  const int nslice = (kend - kbeg + SN_KW - 1) / SN_KW;
+  const int my_slices = nslice > warp ? (nslice - warp + SN_NW - 1) / SN_NW : 0;
+  const int ktiles = my_slices * tiles_per_slice;
+  auto tile_k0 = [&](int t) { return kbeg + ((t / tiles_per_slice) * SN_NW + warp) * SN_KW + (t % tiles_per_slice) * SN_BK; };
+#pragma unroll
+  for (int s = 0; s < SN_ST - 1; ++s) {
+    if (s < ktiles) sn_load<TA>(S, s, A, lda, M, B, ldb, bmap, N, m0, tile_k0(s), kend, lane);
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  for (int kt = 0; kt < ktiles; ++kt) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(SN_ST - 2));
+    __syncwarp();
+    const int nk = kt + SN_ST - 1;
+    if (nk < ktiles) sn_load<TA>(S, nk % SN_ST, A, lda, M, B, ldb, bmap, N, m0, tile_k0(nk), kend, lane);
+    asm volatile("cp.async.commit_group;\n" ::);
+    const int st = kt % SN_ST;
+#pragma unroll
+    for (int kk = 0; kk < SN_BK / 4; ++kk) {
+      double are[2], aim[2], anim[2], bre[2], bim[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const cplx a = S.A[st][i * 8 + fr][kk * 4 + fc];
+        are[i] = a.x;
+        aim[i] = a.y;
+        anim[i] = -a.y;
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const cplx b = S.B[st][kk * 4 + fc][j * 8 + fr];
+        bre[j] = b.x;
+        bim[j] = b.y;
+      }
+      // four passes over all sub-tiles: dependent DMMAs on one accumulator are
+      // 8 instructions apart (per-accumulator order unchanged: bitwise same)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) sn_dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) sn_dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) sn_dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) sn_dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
+    }
+    __syncwarp();
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  // cross-warp sum in warp order through the (now idle) staging memory
+  cplx (*red)[SN_BM][SN_BN] = reinterpret_cast<cplx (*)[SN_BM][SN_BN]>(sn_smem);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) red[warp][i * 8 + fr][j * 8 + fc * 2 + h] = mk(acc_re[i][j][h], acc_im[i][j][h]);
+  __syncthreads();
+  for (int e = threadIdx.x; e < SN_BM * SN_BN; e += SN_NT) {
+    const int rr = e >> 4, c = e & 15, r = m0 + rr;
+    if (r >= M || c >= N) continue;
+    cplx v = red[0][rr][c];
+#pragma unroll
+    for (int w = 1; w < SN_NW; ++w) v = c_add(v, red[w][rr][c]);
+    if (mode == 2) {
+      C[((int64_t)chunk * M + r) * N + c] = v;
+    } else {
+      cplx* p = C + (cmap ? cmap[r] : (int64_t)r) * ldc + c;
+      *p = mode == 1 ? c_sub(*p, v) : v;
+    }
+  }
+}
+
+// out[r * ldo + c] = (base ? base[r * ldb + c] : 0) + sign * sum_{ch < nch} part[(ch * M + r) * np + c]
+// (chunks summed in ascending order), r < M, c < np
+__global__ void skinny_reduce_kernel(const cplx* base, int ldb, const cplx* part, int nch, int M, int np,
+                                     double sign, cplx* out, int ldo) {
+  const int64_t len = (int64_t)M * np;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / np), c = (int)(e % np);
+    cplx acc = mk(0.0, 0.0);
+    for (int ch = 0; ch < nch; ++ch) acc = c_add(acc, part[(int64_t)ch * len + e]);
+    const cplx b = base ? base[(int64_t)r * ldb + c] : mk(0.0, 0.0);
+    out[(int64_t)r * ldo + c] = mk(b.x + sign * acc.x, b.y + sign * acc.y);
+  }
+}
+
+}  // namespace d3m
+
+extern "C" int d3m_skinny_reduce_launch(const void* base, int ldb, const void* part, int nch, int M, int np,
+                                        double sign, void* out, int ldo, void* stream) {
+  using namespace d3m;
+  const int64_t len = (int64_t)M * np;
+  if (len <= 0) return 0;
+  const int threads = 128;
+  const int blocks = (int)std::min<int64_t>((len + threads - 1) / threads, 1024);
+  skinny_reduce_kernel<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(base), ldb, static_cast<const cplx*>(part), nch, M, np, sign,
+      static_cast<cplx*>(out), ldo);
+  return (int)cudaGetLastError();
+}
+
+// One pass of <= 16 RHS.  kchunk > 0 with mode 2 splits K (partials of
+// ceil(K / kchunk) chunks, M x N each, written to C); returns the chunk count.
+extern "C" int d3m_skinny_launch(int ta, const void* A, int lda, int M, int K, const void* B, int ldb,
+                                 const void* bmap, int N, void* C, int ldc, const void* cmap, int mode, int kchunk,
+                                 void* stream) {
+  using namespace d3m;
+  if (M <= 0 || N <= 0 || N > SN_BN) return M <= 0 || N <= 0 ? 0 : -22;
+  const int kc = kchunk > 0 ? kchunk : (K > 0 ? K : 1);
+  const int nch = K > 0 ? (K + kc - 1) / kc : 1;
+  const dim3 grid((M + SN_BM - 1) / SN_BM, nch);
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  auto a = static_cast<const cplx*>(A);
+  auto b = static_cast<const cplx*>(B);
+  auto c = static_cast<cplx*>(C);
+  auto bm = static_cast<const int64_t*>(bmap);
+  auto cm = static_cast<const int64_t*>(cmap);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(skinny_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSnSmem);
+    cudaFuncSetAttribute(skinny_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSnSmem);
+    cfg = true;
+  }
+  if (ta) skinny_dmma_kernel<true><<<grid, SN_NT, kSnSmem, s>>>(a, lda, M, K, b, ldb, bm, N, c, ldc, cm, mode, kc);
+  else skinny_dmma_kernel<false><<<grid, SN_NT, kSnSmem, s>>>(a, lda, M, K, b, ldb, bm, N, c, ldc, cm, mode, kc);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? nch : -(int)e;
+}

@@ -158,15 +158,24 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
         bre[j] = b.x;
         bim[j] = b.y;
       }
+      // four passes over all sub-tiles: dependent DMMAs on one accumulator are
+      // 32 instructions apart (per-accumulator order unchanged: bitwise same)
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
-          dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
-          dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
-          dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
-        }
+        for (int j = 0; j < 4; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
     }
   }
   cp_wait<0>();
@@ -300,15 +309,24 @@ zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
       bre[j] = b.x;
       bim[j] = b.y;
     }
+    // four passes over all sub-tiles: dependent DMMAs on one accumulator are
+    // 32 instructions apart (per-accumulator order unchanged: bitwise same)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
-        dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
-        dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
-        dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
-      }
+      for (int j = 0; j < 4; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
   }
   // ---- epilogue in shared memory, then coalesced stores
 #pragma unroll

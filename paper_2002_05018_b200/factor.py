@@ -589,7 +589,8 @@ def block_solve(F: BlockFactor, g: list) -> list:
     u = empty((N, cols))
     x = empty((N, cols))
     tmp = empty((int(sched.sizes.max()), cols))
-    part_elems = int(max(((max(int(r), int(n)) + 15) // 16) * int(n) for r, n in zip(sched.panel_rows, sched.sizes))) * cols
+    # split-K partials of the backward L^T x products: ceil(R_j / 256) chunks x n_j x 16 RHS (one pass)
+    part_elems = int(max(((int(r) + 255) // 256) * int(n) for r, n in zip(sched.panel_rows, sched.sizes))) * 16
     part = empty(max(part_elems, 1))
     H = _lib.hptr
     _lib.call("d3m_block_solve_exec", nb, H(sched.sizes), H(sched.row_off), H(sched.diag_off),
