@@ -188,6 +188,9 @@ int d3m_recover_batched(int batch, int n, int m, const void* F, const void* perm
  * union of the launch intervals per class (concurrent launches of one class
  * on the critical and bulk streams counted once).  n[0..4]: launch counts. */
 void d3m_set_timing(int on);
+/* (class, start_ms, end_ms) triplets of the launches timed before the last
+ * d3m_counters_read; returns their number (diagnostics). */
+int64_t d3m_timing_intervals(double* out, int64_t max_triplets);
 void d3m_counters_reset(void);
 int d3m_counters_read(int64_t* launches, double* ms, int64_t* n);
 

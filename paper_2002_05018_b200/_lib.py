@@ -42,6 +42,7 @@ _SIGNATURES = {
     "d3m_ldlt_solve_blocked_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P, P],
 }
 _SIZE_T = {"d3m_bk_panel_workspace": [I32, I32]}
+_INT64 = {"d3m_timing_intervals": [P, I64]}
 _VOID = {"d3m_set_timing": [I32], "d3m_counters_reset": []}
 
 # GemmTask / CopyTask records (csrc/d3m_gemm.h, csrc/d3m_misc.h)
@@ -86,6 +87,10 @@ def load():
         fn.restype = ctypes.c_int
     lib.d3m_last_error.restype = ctypes.c_char_p
     lib.d3m_last_error.argtypes = []
+    for name, args in _INT64.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int64
     for name, args in _SIZE_T.items():
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -99,7 +104,7 @@ def load():
 
 
 def exported_symbols() -> list[str]:
-    return list(_SIGNATURES) + list(_VOID) + list(_SIZE_T) + ["d3m_last_error"]
+    return list(_SIGNATURES) + list(_VOID) + list(_SIZE_T) + list(_INT64) + ["d3m_last_error"]
 
 
 CLASSES = ("bk", "trsm", "gemm", "solve", "misc")
@@ -109,6 +114,16 @@ def counters_reset(timing: bool = False) -> None:
     lib = load()
     lib.d3m_counters_reset()
     lib.d3m_set_timing(1 if timing else 0)
+
+
+def timing_intervals() -> np.ndarray:
+    """(class, start_ms, end_ms) rows of the launches timed before the last
+    counters_read() (classes as CLASSES)."""
+    lib = load()
+    n = int(lib.d3m_timing_intervals(None, 0))
+    out = np.zeros((max(n, 1), 3), dtype=np.float64)
+    lib.d3m_timing_intervals(out.ctypes.data, n)
+    return out[:n]
 
 
 def counters_read() -> dict:

@@ -52,6 +52,7 @@ double g_ms[kNumCls] = {0, 0, 0, 0, 0};
 double g_union[kNumCls] = {0, 0, 0, 0, 0};
 long long g_cnt[kNumCls] = {0, 0, 0, 0, 0};
 cudaEvent_t g_ref = nullptr;          // common origin for interval unions
+std::vector<double> g_iv;             // (class, start ms, end ms) of the last d3m_counters_read
 
 cudaEvent_t take_event() {
   if (!g_free_ev.empty()) {
@@ -623,14 +624,17 @@ void d3m_counters_reset(void) {
 // time and launch count per class (bk, trsm, gemm-update, solve, misc).
 int d3m_counters_read(int64_t* launches, double* ms, int64_t* n) {
   std::vector<std::pair<double, double>> iv[kNumCls];
+  g_iv.clear();
   for (auto& r : g_pending) {
     cudaEventSynchronize(r.b);
     float t = 0.f, t0 = 0.f, t1 = 0.f;
     cudaEventElapsedTime(&t, r.a, r.b);
     g_ms[r.cls] += t;
     if (g_ref && cudaEventElapsedTime(&t0, g_ref, r.a) == cudaSuccess &&
-        cudaEventElapsedTime(&t1, g_ref, r.b) == cudaSuccess)
+        cudaEventElapsedTime(&t1, g_ref, r.b) == cudaSuccess) {
       iv[r.cls].emplace_back(t0, t1);
+      g_iv.insert(g_iv.end(), {(double)r.cls, (double)t0, (double)t1});
+    }
     g_free_ev.push_back(r.a);
     g_free_ev.push_back(r.b);
   }
@@ -656,6 +660,14 @@ int d3m_counters_read(int64_t* launches, double* ms, int64_t* n) {
     if (n) n[c] = g_cnt[c];
   }
   return 0;
+}
+
+// Diagnostics: the timed launch intervals collected by the last
+// d3m_counters_read, as (class, start_ms, end_ms) triplets; returns the count.
+int64_t d3m_timing_intervals(double* out, int64_t max_triplets) {
+  const int64_t n = (int64_t)g_iv.size() / 3;
+  if (out) std::memcpy(out, g_iv.data(), sizeof(double) * 3 * (size_t)std::min(n, max_triplets));
+  return n;
 }
 
 }  // extern "C"

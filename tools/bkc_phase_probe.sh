@@ -3,7 +3,8 @@
 set -e
 cd "$(dirname "$0")/.."
 D=/tmp/bkcprof; mkdir -p $D
-for f in bk_exact bk_blocked bk_cluster zgemm_dmma ldlt_solve solve_gemv bk_panel solve_blocked d3m_misc d3m_capi; do
+SRCS=$(python -c "import sys; sys.path.insert(0, 'paper_2002_05018_b200'); import build_ext; print(' '.join(f[:-3] for f in build_ext.SOURCES))")
+for f in $SRCS; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -DD3M_BK_PROFILE --expt-relaxed-constexpr \
     -I paper_2002_05018_b200/csrc -I include -c paper_2002_05018_b200/csrc/$f.cu -o $D/$f.o &
 done
