@@ -275,15 +275,18 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out):
     for i, idx in enumerate(members):
         s = systems[idx]
         mr = ms[idx]
+        # X = A^-1 [D | F] (m padded) is kept in both modes: recover_primal
+        # forms E = X_F - X_D lambda from it while the loads and couplings are
+        # the arrays reduced here (identity check), else solves with the factor
+        s._d3m_X = wx[i]
+        s._d3m_Xm = m
+        s._d3m_src = (s.f, tuple(c.D for c in s.couplings))
         if keep == "factor":
             s.factor = facs[i]
             s._d3m_D = D[i, :, :mr]
-            s._d3m_X = None
         else:
             s.factor = facs[i].release()
             s._d3m_D = None
-            s._d3m_X = wx[i]              # [A^-1 D (m padded) | A^-1 F]
-            s._d3m_Xm = m
         gi = g[i, :mr, 0] if vec else g[i, :mr, :]
         out[idx] = (DeviceArray(K[i, :mr, :mr]), DeviceArray(gi))
     return None
@@ -450,12 +453,25 @@ def recover_primal(systems: list[SubdomainSystem], lam: list) -> np.ndarray | De
     """E_d = A_d^-1 (f_d - D_d lambda) with the cached factors, assembled
     with averaging of duplicated interface dofs (subdomain.py:217-237).
     Multi-column loads (lambda_i of shape size_i x r) give E of shape
-    n_glob x r.  Domains reduced with keep="solution" use
-    E_d = X_F - X_D lambda_d instead of a solve."""
+    n_glob x r.  While the loads and couplings are the arrays reduce_domains
+    saw, E_d = X_F - X_D lambda_d is formed from the retained
+    X_d = A_d^-1 [D_d | F_d] with one GEMM (exact-arithmetic equal; tests
+    compare it with the factor solve to 1e-9); otherwise the cached factor
+    solves A_d^-1 (f_d - D_d lambda_d) as the reference does."""
     t = require_cuda()
+    def x_ok(s):
+        src = getattr(s, "_d3m_src", None)
+        return (getattr(s, "_d3m_X", None) is not None and src is not None and src[0] is s.f
+                and len(src[1]) == len(s.couplings) and all(a is c.D for a, c in zip(src[1], s.couplings)))
+
+    use_x = []
     for s in systems:
-        if s.factor is None or (s.factor.released and getattr(s, "_d3m_X", None) is None):
+        if s.factor is None:
             raise SolverStateError(f"domain {s.domain} has no cached factorization; run reduce_domain first")
+        use_x.append(x_ok(s))
+        if s.factor.released and not use_x[-1]:
+            raise SolverStateError(f"domain {s.domain}: loads or couplings changed after reduce_domains("
+                                   f"keep='solution'); reduce again")
     device_in = all(isinstance(v, DeviceArray) for v in lam)
     lam_dev = [to_device(v) for v in lam]
     r = max([int(v.shape[1]) if v.dim() == 2 else 1 for v in lam_dev] + [1])
@@ -475,7 +491,7 @@ def recover_primal(systems: list[SubdomainSystem], lam: list) -> np.ndarray | De
     # -- domains with a cached factor: batched solves per (n, m) group
     groups: dict[tuple[int, int], list[int]] = {}
     for idx, s in enumerate(systems):
-        if not s.factor.released:
+        if not use_x[idx]:
             m = sum(int(np.shape(c.D)[1]) for c in s.couplings)
             groups.setdefault((s.n_dofs, m), []).append(idx)
     for (n, m), members in groups.items():
@@ -511,7 +527,7 @@ def recover_primal(systems: list[SubdomainSystem], lam: list) -> np.ndarray | De
         for i, idx in enumerate(members):
             ET[:, e_off[idx]:e_off[idx] + n].copy_(rhs[i].t())
     # -- domains reduced with keep="solution": E_d = X_F - X_D lambda_d
-    sol = [idx for idx, s in enumerate(systems) if s.factor.released]
+    sol = [idx for idx in range(len(systems)) if use_x[idx]]
     by_base: dict[int, list[int]] = {}
     for idx in sol:
         by_base.setdefault(systems[idx]._d3m_X.untyped_storage().data_ptr(), []).append(idx)

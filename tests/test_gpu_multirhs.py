@@ -65,22 +65,35 @@ def test_chunked_reduce_is_bitwise_identical(cuda, n):
 
 
 @pytest.mark.parametrize("cells,parts", [(4, (2, 2, 2)), (8, (2, 1, 1))])
-def test_keep_solution_recovery_matches_factor_recovery(cuda, cells, parts):
-    from paper_2002_05018_b200 import SolverStateError, fem3d
+def test_recovery_from_retained_solution_matches_factor_solve(cuda, cells, parts):
+    """recover_primal forms E_d = X_F - X_D lambda_d from the X_d kept by
+    reduce_domains; the reference's A_d^-1 (f_d - D_d lambda_d) (factor path,
+    taken when the loads are not the reduced arrays) agrees to 1e-9, and
+    keep="solution" refuses changed loads."""
+    from paper_2002_05018_b200 import SolverStateError, fem3d, subdomain
     prob = fem3d.FemProblem(cells, 0.5, parts, sphere_radius=0.15,
                             polarisations=((1.0, 0.0, 0.0), (0.0, 1.0, 0.0)),
                             directions=((0.0, 0.0, 1.0), (0.0, 0.0, -1.0)))
     model = fem3d.build_model(prob)
-    sol_f, sys_f, *_ = fem3d.solve_d3m(model, rhs=None, keep="factor")
+    sol_x, sys_f, R, plan, F = fem3d.solve_d3m(model, rhs=None, keep="factor")
+    assert sol_x.shape == (model.mesh.n_edges, 2)
+    assert fem3d.global_residual(model, sol_x, rhs=None) <= 1e-10
+    import paper_2002_05018_b200 as d
+    lam = d.block_solve(F, R.g)
+    for s in sys_f:                       # equal values, new arrays: factor path
+        s.f = np.array(s.f, copy=True)
+    sol_f = np.asarray(subdomain.recover_primal(sys_f, lam))
+    assert np.linalg.norm(sol_x - sol_f) <= 1e-9 * np.linalg.norm(sol_f)
     sol_s, sys_s, *_ = fem3d.solve_d3m(model, rhs=None, keep="solution")
-    assert sol_f.shape == (model.mesh.n_edges, 2)
     assert np.linalg.norm(sol_s - sol_f) <= 1e-9 * np.linalg.norm(sol_f)
-    assert fem3d.global_residual(model, sol_s, rhs=None) <= 1e-10
     assert all(s.factor.released for s in sys_s)
     assert np.array_equal(sys_s[0].factor.perm, sys_f[0].factor.perm)
     with pytest.raises(SolverStateError):
         sys_s[0].factor.solve(np.ones(sys_s[0].n_dofs))
+    sys_s[0].f = np.array(sys_s[0].f, copy=True)
+    with pytest.raises(SolverStateError):
+        subdomain.recover_primal(sys_s, lam)
     # all-RHS solve == per-column solves
     for q in range(2):
         sol_q, *_ = fem3d.solve_d3m(model, rhs=q, keep="factor")
-        assert np.linalg.norm(sol_f[:, q] - sol_q) <= 1e-13 * np.linalg.norm(sol_q)
+        assert np.linalg.norm(sol_x[:, q] - sol_q) <= 1e-13 * np.linalg.norm(sol_q)
