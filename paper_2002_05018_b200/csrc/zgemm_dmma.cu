@@ -229,7 +229,9 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
 constexpr int SK_K = 16, SK_PA = SK_K + 4, SK_PC = BN + 1;
 constexpr size_t kSmallKSmem = sizeof(cplx) * ((BM + BN) * SK_PA + BM * SK_PC);
 
-__global__ void __launch_bounds__(NTHREADS, 2)
+constexpr int SK_NT = 256;      // 8 warps: 2 x 4 warp grid of 32 x 16 tiles
+
+__global__ void __launch_bounds__(SK_NT, 2)
 zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bbase, cplx* Cbase,
                     const GemmTask* __restrict__ tasks, int ntasks, unsigned long long* tmax) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -264,8 +266,8 @@ zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
   const int t = threadIdx.x;
   // ---- one-shot staging: A, B (64 x 16 each) and the C tile (64 x 64)
 #pragma unroll
-  for (int p = 0; p < 2 * BM * SK_K / NTHREADS; ++p) {     // A then B: 64 rows x 16 k each
-    const int e = p * NTHREADS + t, r = (e >> 4) & 63, k = e & 15;
+  for (int p = 0; p < 2 * BM * SK_K / SK_NT; ++p) {       // A then B: 64 rows x 16 k each
+    const int e = p * SK_NT + t, r = (e >> 4) & 63, k = e & 15;
     const bool isb = e >= BM * SK_K;
     const int rows = isb ? N : M, r0 = isb ? n0 : m0;
     const bool ok = (r0 + r < rows) && (k < K);
@@ -275,8 +277,8 @@ zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
   }
   if (mode != kGemmStore) {
 #pragma unroll 8
-    for (int p = 0; p < BM * BN / NTHREADS; ++p) {
-      const int e = p * NTHREADS + t, r = e >> 6, c = e & 63;
+    for (int p = 0; p < BM * BN / SK_NT; ++p) {
+      const int e = p * SK_NT + t, r = e >> 6, c = e & 63;
       const bool ok = (m0 + r < M) && (n0 + c < N) && (!sym || n0 + c <= m0 + r);
       cp_async16(&Cs[r][c], ok ? C + (int64_t)(m0 + r) * ldc + n0 + c : Cbase, ok);
     }
@@ -286,16 +288,16 @@ zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
   __syncthreads();
 
   const int lane = t & 31, warp = t >> 5;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
   const int fr = lane >> 2, fc = lane & 3;
-  double acc_re[4][4][2], acc_im[4][4][2];
+  double acc_re[4][2][2], acc_im[4][2][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
+    for (int j = 0; j < 2; ++j) acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
 #pragma unroll
   for (int kk = 0; kk < SK_K / 4; ++kk) {
-    double are[4], aim[4], anim[4], bre[4], bim[4];
+    double are[4], aim[4], anim[4], bre[2], bim[2];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const cplx a = As[wm + i * 8 + fr][kk * 4 + fc];
@@ -304,35 +306,35 @@ zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
       anim[i] = -a.y;
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 2; ++j) {
       const cplx b = Bs[wn + j * 8 + fr][kk * 4 + fc];
       bre[j] = b.x;
       bim[j] = b.y;
     }
     // four passes over all sub-tiles: dependent DMMAs on one accumulator are
-    // 32 instructions apart (per-accumulator order unchanged: bitwise same)
+    // 16 instructions apart (per-accumulator order unchanged: bitwise same)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
+      for (int j = 0; j < 2; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
+      for (int j = 0; j < 2; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
+      for (int j = 0; j < 2; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
+      for (int j = 0; j < 2; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
   }
   // ---- epilogue in shared memory, then coalesced stores
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = wm + i * 8 + fr, c = wn + j * 8 + fc * 2 + h;
@@ -344,8 +346,8 @@ zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
   const bool track = (tk.flags & kGemmTrackMax) != 0 && tmax != nullptr;
   double tm2 = 0.0;
 #pragma unroll 8
-  for (int p = 0; p < BM * BN / NTHREADS; ++p) {
-    const int e = p * NTHREADS + t, r = e >> 6, c = e & 63;
+  for (int p = 0; p < BM * BN / SK_NT; ++p) {
+    const int e = p * SK_NT + t, r = e >> 6, c = e & 63;
     if ((m0 + r < M) && (n0 + c < N) && (!sym || n0 + c <= m0 + r)) {
       const cplx w = Cs[r][c];
       C[(int64_t)(m0 + r) * ldc + n0 + c] = w;
@@ -425,7 +427,7 @@ extern "C" int d3m_gemm_smallk_launch_tm(const void* A, const void* B, void* C, 
     cudaFuncSetAttribute(zgemm_smallk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallKSmem);
     configured = true;
   }
-  zgemm_smallk_kernel<<<ntiles, NTHREADS, kSmallKSmem, reinterpret_cast<cudaStream_t>(stream)>>>(
+  zgemm_smallk_kernel<<<ntiles, SK_NT, kSmallKSmem, reinterpret_cast<cudaStream_t>(stream)>>>(
       static_cast<const cplx*>(A), static_cast<const cplx*>(B), static_cast<cplx*>(C),
       static_cast<const GemmTask*>(dtasks), ntasks, static_cast<unsigned long long*>(tmax));
   return (int)cudaGetLastError();
