@@ -25,7 +25,7 @@
 namespace d3m {
 namespace cg = cooperative_groups;
 
-constexpr int CNT = 512;       // threads per panel CTA
+constexpr int CNT = 256;       // threads per panel CTA (two CTAs fit an SM)
 constexpr double kAlphaP = 0.6403882032022076;
 
 struct BkState {          // 64 bytes per matrix
@@ -519,15 +519,22 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
   bk_panel_state_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, red, batch);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
-  // CTAs per matrix: spread each panel over enough SMs to fill the GPU once
-  int cs = batch >= 74 ? 1 : batch >= 37 ? 2 : batch >= 19 ? 4 : 8;
+  // CTAs per matrix: the largest cluster size whose CTAs (two per SM) fill
+  // the GPU at most once; 16 is a non-portable cluster size
+  int cs = batch * 16 <= 296 ? 16 : batch * 8 <= 296 ? 8 : batch * 4 <= 296 ? 4 : batch * 2 <= 296 ? 2 : 1;
   if (const char* env = getenv("D3M_PANEL_CS")) cs = atoi(env);
-  if (cs != 1 && cs != 2 && cs != 4 && cs != 8) cs = 1;
+  if (cs != 1 && cs != 2 && cs != 4 && cs != 8 && cs != 16) cs = 1;
+  static bool np16 = false;
+  if (cs == 16 && !np16) {
+    cudaFuncSetAttribute(bk_panel_kernel<NB, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    np16 = true;
+  }
   for (int p = 0; p * (NB - 1) < n; ++p) {
     const int mrem = n - (p + 1) * (NB - 1);           // rows left after this panel (upper bound)
     const int tm = mrem > 0 ? (mrem + 63) / 64 : 0;
     const int maxtiles = tm * (tm + 1) / 2;
     switch (cs) {
+      case 16: bk_panel_kernel<NB, 16><<<batch * 16, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
       case 8: bk_panel_kernel<NB, 8><<<batch * 8, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
       case 4: bk_panel_kernel<NB, 4><<<batch * 4, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
       case 2: bk_panel_kernel<NB, 2><<<batch * 2, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
