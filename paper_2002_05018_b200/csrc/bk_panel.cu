@@ -154,19 +154,19 @@ __global__ void bk_perm_init_kernel(BkArgs a, int batch) {
 
 // Up-to-date column of the panel step over the rows [r_lo, r_hi) this CTA owns:
 //   out[i] = base(i) - sum_{c < kw} G(i, k0 + c) * Wp[src][c]
-// with 4 lanes per row (each 4 of the <= 16 panel columns, independent loads)
+// with 4 lanes per row (each NB/4 of the <= NB panel columns, independent loads)
 // and two rows per lane group in flight; base(i) is G(i, col) for i >= col
 // (stale column) or G(col, i) for i < col (its row part), col = the target
 // column.  The summation order per row is fixed (4 partial sums, butterfly).
 template <int NB, int NT>
 __device__ __forceinline__ void panel_gemv(const cplx* W, int lda, int r_lo, int r_hi, int k0, int kw, int col,
                                            const cplx* Wp, int src, cplx* out_col /* Wp + kwcol, stride NB+1 */) {
-  constexpr int LDW = NB + 1;
+  constexpr int LDW = NB + 1, Q = NB / 4;
   const int sub = threadIdx.x & 3;
   constexpr int rstride = NT / 4;
-  cplx xs[4];
+  cplx xs[Q];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < Q; ++q) {
     const int c = sub + 4 * q;
     xs[q] = c < kw ? Wp[(int64_t)src * LDW + c] : mk(0.0, 0.0);
   }
@@ -174,9 +174,9 @@ __device__ __forceinline__ void panel_gemv(const cplx* W, int lda, int r_lo, int
   for (int base = r_lo; base < r_hi; base += 2 * rstride) {
     const int ia = base + (threadIdx.x >> 2), ib = ia + rstride;
     const bool va = ia < r_hi, vb = ib < r_hi;
-    cplx la[4], lb[4], ba = mk(0.0, 0.0), bb = mk(0.0, 0.0);
+    cplx la[Q], lb[Q], ba = mk(0.0, 0.0), bb = mk(0.0, 0.0);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < Q; ++q) {
       const int c = sub + 4 * q;
       la[q] = (c < kw && va) ? W[(int64_t)ia * lda + k0 + c] : mk(0.0, 0.0);
       lb[q] = (c < kw && vb) ? W[(int64_t)ib * lda + k0 + c] : mk(0.0, 0.0);
@@ -187,7 +187,7 @@ __device__ __forceinline__ void panel_gemv(const cplx* W, int lda, int r_lo, int
     }
     cplx sa = mk(0.0, 0.0), sb = mk(0.0, 0.0);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < Q; ++q) {
       c_fma(sa, la[q], xs[q]);
       c_fma(sb, lb[q], xs[q]);
     }
@@ -493,32 +493,18 @@ __global__ void bk_panel_finalize_kernel(BkArgs a, const BkState* st, int batch)
 }  // namespace d3m
 
 // Host driver: init, then per panel one panel launch + one grouped GEMM over
-// the batch.  workspace: batch * (n * 17 complex + 64 B state + 64 B task + 8 B).
-extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* workspace, void* stream) {
-  using namespace d3m;
-  constexpr int NB = 16;
-  if (batch <= 0 || a->n <= 0) return 0;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+// the batch.  workspace: batch * (n * 33 complex + 64 B state + 64 B task + 8 B + 64 B).
+namespace d3m {
+constexpr int kPanelLdwMax = 33;      // workspace row pitch for the widest panel (NB = 32)
+
+// Panel loop for one panel width (NB - 1 or NB columns per panel); the
+// rank-<= NB trailing updates of all matrices run on the small-K kernel
+// (C tile staged with A and B, shared-memory epilogue).
+template <int NB>
+static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* tasks, unsigned long long* tmax,
+                     cudaStream_t s, void* stream) {
   const int n = a->n;
-  char* w = static_cast<char*>(workspace);
-  cplx* Wp = reinterpret_cast<cplx*>(w);
-  w += (size_t)batch * n * (NB + 1) * sizeof(cplx);
-  BkState* st = reinterpret_cast<BkState*>(w);
-  w += (size_t)batch * sizeof(BkState);
-  GemmTask* tasks = reinterpret_cast<GemmTask*>(w);
-  w += (size_t)batch * sizeof(GemmTask);
-  unsigned long long* tmax = reinterpret_cast<unsigned long long*>(w);
-  w += (size_t)batch * sizeof(unsigned long long);
-  unsigned long long* red = reinterpret_cast<unsigned long long*>(w);
-  cudaMemsetAsync(red, 0, (size_t)batch * 8 * sizeof(unsigned long long), s);
-  const int nt = (n + 31) / 32, ntile = nt * (nt + 1) / 2;
-  const dim3 sgrid(std::min(ntile, 256), batch);
-  bk_perm_init_kernel<<<std::min((batch * n + 255) / 256, 4096), 256, 0, s>>>(*a, batch);
-  bk_scan_kernel<<<sgrid, 256, 0, s>>>(*a, red, 0);
-  bk_scan_kernel<<<sgrid, 256, 0, s>>>(*a, red, 1);
-  bk_panel_state_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, red, batch);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return (int)e;
+  cudaError_t e;
   // CTAs per matrix: the largest cluster size whose CTAs (two per SM) fill
   // the GPU at most once; 16 is a non-portable cluster size
   int cs = batch * 16 <= 296 ? 16 : batch * 8 <= 296 ? 8 : batch * 4 <= 296 ? 4 : batch * 2 <= 296 ? 2 : 1;
@@ -542,14 +528,49 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
     if (maxtiles > 0) {
-      const int rc = d3m_gemm_smallk_launch_tm(a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream);
+      const int rc = d3m_gemm_smallk_launch_k(NB, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream);
       if (rc) return rc;
     }
   }
+  return 0;
+}
+}  // namespace d3m
+
+extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* workspace, void* stream) {
+  using namespace d3m;
+  if (batch <= 0 || a->n <= 0) return 0;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int n = a->n;
+  // panel width 32: rank-<=32 trailing updates halve the trailing-matrix
+  // traffic of NB = 16 (config 5: BK 20.7 -> 15.6 s, configs 2/3: -15%)
+  int nb = 32;
+  if (const char* env = getenv("D3M_PANEL_NB")) nb = atoi(env) == 32 ? 32 : 16;
+  char* w = static_cast<char*>(workspace);
+  cplx* Wp = reinterpret_cast<cplx*>(w);
+  w += (size_t)batch * n * kPanelLdwMax * sizeof(cplx);
+  BkState* st = reinterpret_cast<BkState*>(w);
+  w += (size_t)batch * sizeof(BkState);
+  GemmTask* tasks = reinterpret_cast<GemmTask*>(w);
+  w += (size_t)batch * sizeof(GemmTask);
+  unsigned long long* tmax = reinterpret_cast<unsigned long long*>(w);
+  w += (size_t)batch * sizeof(unsigned long long);
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(w);
+  cudaMemsetAsync(red, 0, (size_t)batch * 8 * sizeof(unsigned long long), s);
+  const int nt = (n + 31) / 32, ntile = nt * (nt + 1) / 2;
+  const dim3 sgrid(std::min(ntile, 256), batch);
+  bk_perm_init_kernel<<<std::min((batch * n + 255) / 256, 4096), 256, 0, s>>>(*a, batch);
+  bk_scan_kernel<<<sgrid, 256, 0, s>>>(*a, red, 0);
+  bk_scan_kernel<<<sgrid, 256, 0, s>>>(*a, red, 1);
+  bk_panel_state_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, red, batch);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  const int rc = nb == 32 ? panel_run<32>(a, batch, st, Wp, tasks, tmax, s, stream)
+                          : panel_run<16>(a, batch, st, Wp, tasks, tmax, s, stream);
+  if (rc) return rc;
   bk_panel_finalize_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, batch);
   return (int)cudaGetLastError();
 }
 
 extern "C" size_t d3m_bk_panel_workspace_bytes(int n, int batch) {
-  return (size_t)batch * ((size_t)n * 17 * 16 + 64 + 64 + 8 + 64) + 256;
+  return (size_t)batch * ((size_t)n * d3m::kPanelLdwMax * 16 + 64 + 64 + 8 + 64) + 256;
 }

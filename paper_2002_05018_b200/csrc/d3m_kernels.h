@@ -87,5 +87,7 @@ int d3m_sub_partials_launch(const void* u, const void* partial, int np, int64_t 
 extern "C" int d3m_gemm_prepare_tasks(d3m::GemmTask* tasks, int ntasks);
 extern "C" int d3m_gemm_launch_tm(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
                                   int ntasks, int ntiles, void* tmax, void* stream);
+extern "C" int d3m_gemm_smallk_launch_k(int kt, const void* A, const void* B, void* C, const void* dtasks, int ntasks,
+                                        int ntiles, void* tmax, void* stream);
 extern "C" int d3m_gemm_smallk_launch_tm(const void* A, const void* B, void* C, const void* dtasks, int ntasks,
                                          int ntiles, void* tmax, void* stream);

@@ -220,21 +220,24 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
   }
 }
 
-// ---- small-K variant (K <= 16): the rank-<=16 trailing updates of the
-// batched panel BK (bk_panel.cu).  At K = 16 a 64x64 tile does 0.5 MFLOP
+// ---- small-K variant (K <= 16 or 32): the rank-<=NB trailing updates of the
+// batched panel BK (bk_panel.cu; NB = 32 by default: 140 KB, one CTA per SM).  At K = 16 a 64x64 tile does 0.5 MFLOP
 // against 128 KB of C traffic (4 flop/B), so the tile is HBM/latency bound:
 // the C tile is fetched by cp.async into shared memory together with A and B
 // (all 96 KB of the tile's traffic in flight at once), updated there by the
 // DMMA fragments and written back with coalesced 16-byte stores.
-constexpr int SK_K = 16, SK_PA = SK_K + 4, SK_PC = BN + 1;
-constexpr size_t kSmallKSmem = sizeof(cplx) * ((BM + BN) * SK_PA + BM * SK_PC);
+constexpr int SK_PC = BN + 1;
+template <int KT>
+constexpr size_t sk_smem() { return sizeof(cplx) * ((BM + BN) * (KT + 4) + BM * SK_PC); }
 
 constexpr int SK_NT = 256;      // 8 warps: 2 x 4 warp grid of 32 x 16 tiles
 
-__global__ void __launch_bounds__(SK_NT, 2)
+template <int KT>
+__global__ void __launch_bounds__(SK_NT, KT <= 16 ? 2 : 1)
 zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bbase, cplx* Cbase,
                     const GemmTask* __restrict__ tasks, int ntasks, unsigned long long* tmax) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int SK_K = KT, SK_PA = KT + 4;
   cplx(*As)[SK_PA] = reinterpret_cast<cplx(*)[SK_PA]>(smem_raw);
   cplx(*Bs)[SK_PA] = reinterpret_cast<cplx(*)[SK_PA]>(smem_raw + sizeof(cplx) * BM * SK_PA);
   cplx(*Cs)[SK_PC] = reinterpret_cast<cplx(*)[SK_PC]>(smem_raw + sizeof(cplx) * (BM + BN) * SK_PA);
@@ -267,7 +270,7 @@ zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
   // ---- one-shot staging: A, B (64 x 16 each) and the C tile (64 x 64)
 #pragma unroll
   for (int p = 0; p < 2 * BM * SK_K / SK_NT; ++p) {       // A then B: 64 rows x 16 k each
-    const int e = p * SK_NT + t, r = (e >> 4) & 63, k = e & 15;
+    const int e = p * SK_NT + t, r = (e / SK_K) & 63, k = e % SK_K;
     const bool isb = e >= BM * SK_K;
     const int rows = isb ? N : M, r0 = isb ? n0 : m0;
     const bool ok = (r0 + r < rows) && (k < K);
@@ -418,17 +421,32 @@ extern "C" int d3m_gemm_launch_tm(int ta, int tb, const void* A, const void* B, 
 }
 
 // Grouped small-K launch (every task K <= 16; SYM tasks must be LowerOnly).
+extern "C" int d3m_gemm_smallk_launch_k(int kt, const void* A, const void* B, void* C, const void* dtasks, int ntasks,
+                                        int ntiles, void* tmax, void* stream);
+
 extern "C" int d3m_gemm_smallk_launch_tm(const void* A, const void* B, void* C, const void* dtasks, int ntasks,
                                          int ntiles, void* tmax, void* stream) {
+  return d3m_gemm_smallk_launch_k(16, A, B, C, dtasks, ntasks, ntiles, tmax, stream);
+}
+
+// Grouped small-K launch: every task K <= kt (16 or 32); SYM tasks must be LowerOnly.
+extern "C" int d3m_gemm_smallk_launch_k(int kt, const void* A, const void* B, void* C, const void* dtasks, int ntasks,
+                                        int ntiles, void* tmax, void* stream) {
   using namespace d3m;
   if (ntiles <= 0 || ntasks <= 0) return 0;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(zgemm_smallk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallKSmem);
+    cudaFuncSetAttribute(zgemm_smallk_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sk_smem<16>());
+    cudaFuncSetAttribute(zgemm_smallk_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sk_smem<32>());
     configured = true;
   }
-  zgemm_smallk_kernel<<<ntiles, SK_NT, kSmallKSmem, reinterpret_cast<cudaStream_t>(stream)>>>(
-      static_cast<const cplx*>(A), static_cast<const cplx*>(B), static_cast<cplx*>(C),
-      static_cast<const GemmTask*>(dtasks), ntasks, static_cast<unsigned long long*>(tmax));
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  auto a = static_cast<const cplx*>(A);
+  auto b = static_cast<const cplx*>(B);
+  auto c = static_cast<cplx*>(C);
+  auto t = static_cast<const GemmTask*>(dtasks);
+  auto tm = static_cast<unsigned long long*>(tmax);
+  if (kt <= 16) zgemm_smallk_kernel<16><<<ntiles, SK_NT, sk_smem<16>(), s>>>(a, b, c, t, ntasks, tm);
+  else zgemm_smallk_kernel<32><<<ntiles, SK_NT, sk_smem<32>(), s>>>(a, b, c, t, ntasks, tm);
   return (int)cudaGetLastError();
 }
