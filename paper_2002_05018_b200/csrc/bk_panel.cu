@@ -154,30 +154,30 @@ __global__ void bk_perm_init_kernel(BkArgs a, int batch) {
 
 // Up-to-date column of the panel step over the rows [r_lo, r_hi) this CTA owns:
 //   out[i] = base(i) - sum_{c < kw} G(i, k0 + c) * Wp[src][c]
-// with 4 lanes per row (each NB/4 of the <= NB panel columns, independent loads)
+// with NB/4 lanes per row (4 of the <= NB panel columns each, independent loads)
 // and two rows per lane group in flight; base(i) is G(i, col) for i >= col
 // (stale column) or G(col, i) for i < col (its row part), col = the target
 // column.  The summation order per row is fixed (4 partial sums, butterfly).
 template <int NB, int NT>
 __device__ __forceinline__ void panel_gemv(const cplx* W, int lda, int r_lo, int r_hi, int k0, int kw, int col,
                                            const cplx* Wp, int src, cplx* out_col /* Wp + kwcol, stride NB+1 */) {
-  constexpr int LDW = NB + 1, Q = NB / 4;
-  const int sub = threadIdx.x & 3;
-  constexpr int rstride = NT / 4;
-  cplx xs[Q];
+  constexpr int LDW = NB + 1, LN = NB / 4;       // LN lanes per row, 4 panel columns each
+  const int sub = threadIdx.x % LN;
+  constexpr int rstride = NT / LN;
+  cplx xs[4];
 #pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    const int c = sub + 4 * q;
+  for (int q = 0; q < 4; ++q) {
+    const int c = sub + LN * q;
     xs[q] = c < kw ? Wp[(int64_t)src * LDW + c] : mk(0.0, 0.0);
   }
   // warp-uniform trip count: the shuffles below need all 32 lanes
   for (int base = r_lo; base < r_hi; base += 2 * rstride) {
-    const int ia = base + (threadIdx.x >> 2), ib = ia + rstride;
+    const int ia = base + (int)threadIdx.x / LN, ib = ia + rstride;
     const bool va = ia < r_hi, vb = ib < r_hi;
-    cplx la[Q], lb[Q], ba = mk(0.0, 0.0), bb = mk(0.0, 0.0);
+    cplx la[4], lb[4], ba = mk(0.0, 0.0), bb = mk(0.0, 0.0);
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int c = sub + 4 * q;
+    for (int q = 0; q < 4; ++q) {
+      const int c = sub + LN * q;
       la[q] = (c < kw && va) ? W[(int64_t)ia * lda + k0 + c] : mk(0.0, 0.0);
       lb[q] = (c < kw && vb) ? W[(int64_t)ib * lda + k0 + c] : mk(0.0, 0.0);
     }
@@ -187,12 +187,12 @@ __device__ __forceinline__ void panel_gemv(const cplx* W, int lda, int r_lo, int
     }
     cplx sa = mk(0.0, 0.0), sb = mk(0.0, 0.0);
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
+    for (int q = 0; q < 4; ++q) {
       c_fma(sa, la[q], xs[q]);
       c_fma(sb, lb[q], xs[q]);
     }
 #pragma unroll
-    for (int o = 1; o < 4; o <<= 1) {
+    for (int o = 1; o < LN; o <<= 1) {
       sa.x += __shfl_xor_sync(0xffffffffu, sa.x, o);
       sa.y += __shfl_xor_sync(0xffffffffu, sa.y, o);
       sb.x += __shfl_xor_sync(0xffffffffu, sb.x, o);
@@ -493,9 +493,9 @@ __global__ void bk_panel_finalize_kernel(BkArgs a, const BkState* st, int batch)
 }  // namespace d3m
 
 // Host driver: init, then per panel one panel launch + one grouped GEMM over
-// the batch.  workspace: batch * (n * 33 complex + 64 B state + 64 B task + 8 B + 64 B).
+// the batch.  workspace: batch * (n * 65 complex + 64 B state + 64 B task + 8 B + 64 B).
 namespace d3m {
-constexpr int kPanelLdwMax = 33;      // workspace row pitch for the widest panel (NB = 32)
+constexpr int kPanelLdwMax = 65;      // workspace row pitch for the widest panel (NB = 64)
 
 // Panel loop for one panel width (NB - 1 or NB columns per panel); the
 // rank-<= NB trailing updates of all matrices run on the small-K kernel
@@ -541,10 +541,11 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
   if (batch <= 0 || a->n <= 0) return 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int n = a->n;
-  // panel width 32: rank-<=32 trailing updates halve the trailing-matrix
-  // traffic of NB = 16 (config 5: BK 20.7 -> 15.6 s, configs 2/3: -15%)
-  int nb = 32;
-  if (const char* env = getenv("D3M_PANEL_NB")) nb = atoi(env) == 32 ? 32 : 16;
+  // panel width 64: rank-<=64 trailing updates cut the trailing-matrix
+  // traffic 4x against NB = 16 (config 5 BK: 20.7 s at NB 16, 15.6 s at 32,
+  // 13.0 s at 64; configs 2/3: -21% / -17%)
+  int nb = 64;
+  if (const char* env = getenv("D3M_PANEL_NB")) nb = atoi(env) == 64 ? 64 : atoi(env) == 32 ? 32 : 16;
   char* w = static_cast<char*>(workspace);
   cplx* Wp = reinterpret_cast<cplx*>(w);
   w += (size_t)batch * n * kPanelLdwMax * sizeof(cplx);
@@ -564,8 +565,9 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
   bk_panel_state_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, red, batch);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
-  const int rc = nb == 32 ? panel_run<32>(a, batch, st, Wp, tasks, tmax, s, stream)
-                          : panel_run<16>(a, batch, st, Wp, tasks, tmax, s, stream);
+  const int rc = nb == 64 ? panel_run<64>(a, batch, st, Wp, tasks, tmax, s, stream)
+                 : nb == 32 ? panel_run<32>(a, batch, st, Wp, tasks, tmax, s, stream)
+                            : panel_run<16>(a, batch, st, Wp, tasks, tmax, s, stream);
   if (rc) return rc;
   bk_panel_finalize_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, batch);
   return (int)cudaGetLastError();

@@ -438,6 +438,7 @@ extern "C" int d3m_gemm_smallk_launch_k(int kt, const void* A, const void* B, vo
   if (!configured) {
     cudaFuncSetAttribute(zgemm_smallk_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sk_smem<16>());
     cudaFuncSetAttribute(zgemm_smallk_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sk_smem<32>());
+    cudaFuncSetAttribute(zgemm_smallk_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sk_smem<64>());
     configured = true;
   }
   auto s = reinterpret_cast<cudaStream_t>(stream);
@@ -447,6 +448,7 @@ extern "C" int d3m_gemm_smallk_launch_k(int kt, const void* A, const void* B, vo
   auto t = static_cast<const GemmTask*>(dtasks);
   auto tm = static_cast<unsigned long long*>(tmax);
   if (kt <= 16) zgemm_smallk_kernel<16><<<ntiles, SK_NT, sk_smem<16>(), s>>>(a, b, c, t, ntasks, tm);
-  else zgemm_smallk_kernel<32><<<ntiles, SK_NT, sk_smem<32>(), s>>>(a, b, c, t, ntasks, tm);
+  else if (kt <= 32) zgemm_smallk_kernel<32><<<ntiles, SK_NT, sk_smem<32>(), s>>>(a, b, c, t, ntasks, tm);
+  else zgemm_smallk_kernel<64><<<ntiles, SK_NT, sk_smem<64>(), s>>>(a, b, c, t, ntasks, tm);
   return (int)cudaGetLastError();
 }
