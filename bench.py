@@ -202,6 +202,10 @@ def run_ours(args):
     res = _residual(K, rhs, [np.asarray(v) for v in x])
 
     # ---- e2e: public API with host buffers ------------------------------------
+    # inputs in pinned host memory (K's blocks as views of one pinned
+    # allocation, the RHS blocks pinned), copied to the device inside every
+    # step; the solution is read back to numpy inside every step
+    Kp, rhs_p = _pinned_inputs(K, rhs)
     h2d = 16 * sum(int(np.asarray(b).size) for b in K.blocks.values()) + 16 * sum(b.size for b in rhs)
     d2h = 16 * sum(b.size for b in rhs)
     _barrier(dist)
@@ -209,8 +213,8 @@ def run_ours(args):
     t0 = time.perf_counter()
     e2e_steps = max(1, min(args.steps, 3))
     for _ in range(e2e_steps):
-        Fh = d.block_ldlt(K, plan)
-        xh = d.block_solve(Fh, rhs)
+        Fh = d.block_ldlt(Kp, plan)
+        xh = [np.asarray(v) for v in d.block_solve(Fh, rhs_p)]
     torch.cuda.synchronize()
     e2e_ms = _max_over_ranks(dist, (time.perf_counter() - t0) * 1e3) / e2e_steps
     e2e_value = flops_step * ws / (e2e_ms * 1e-3) / 1e12
@@ -260,6 +264,26 @@ def run_ours(args):
     if sec:
         line["secondary"] = sec
     print(json.dumps(line), flush=True)
+
+
+def _pinned_inputs(K, rhs):
+    """K with its blocks as views of ONE pinned host allocation and pinned RHS
+    blocks (torch CPU tensors; the public API accepts them as host arrays)."""
+    import torch
+    import paper_2002_05018_b200 as d
+    keys = list(K.blocks)
+    tot = sum(int(np.asarray(K.blocks[k]).size) for k in keys)
+    buf = torch.empty(tot, dtype=torch.complex128).pin_memory()
+    Kp = d.BlockSparseSym(K.sizes)
+    o = 0
+    for k in keys:
+        b = np.ascontiguousarray(np.asarray(K.blocks[k], dtype=np.complex128))
+        v = buf[o:o + b.size].view(b.shape)
+        v.copy_(torch.from_numpy(b))
+        Kp.blocks[k] = v
+        o += b.size
+    rhs_p = [torch.from_numpy(np.ascontiguousarray(r)).pin_memory() for r in rhs]
+    return Kp, rhs_p
 
 
 def _fem_secondary(which: str, reps: int) -> dict:
@@ -333,10 +357,17 @@ def _cfg3_secondary(steps: int) -> dict:
     e1.record(s0)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
+    # e2e: pinned host inputs (A, D, f as pinned torch CPU tensors), copied
+    # inside the timed region; all K_D / g_d read back to numpy
+    host_p = [d.SubdomainSystem(s.domain, torch.from_numpy(s.A).pin_memory(),
+                                torch.from_numpy(np.ascontiguousarray(s.f)).pin_memory(), s.dof_map,
+                                [d.Coupling(c.interface, torch.from_numpy(np.ascontiguousarray(c.D)).pin_memory(),
+                                            c.sign) for c in s.couplings]) for s in host]
+    d.reduce_domains(host_p)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    red_h = d.reduce_domains(host)
-    np.asarray(red_h[-1][0])
+    red_h = d.reduce_domains(host_p)
+    outs = [(np.asarray(K_), np.asarray(g_)) for K_, g_ in red_h]
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3
     h2d = 16 * sum(s.A.size + s.f.size + sum(c.D.size for c in s.couplings) for s in host)
@@ -352,7 +383,7 @@ def _cfg3_secondary(steps: int) -> dict:
                                      "(8-core Xeon) by tools/gen_golden.py; 64 subdomains ~ 64x serial")
     except Exception:
         pass
-    del red, red_h
+    del red, red_h, host_p, outs
     return out
 
 

@@ -425,9 +425,24 @@ def _upload_K(K: BlockSparseSym, sched: _Schedule, plan: EliminationPlan, pool):
     inv = plan.order.inverse()
     sizes = K.sizes
     items = list(K.blocks.items())
-    host = [(k, b) for k, b in items if not isinstance(b, DeviceArray)]
+    def cpu_view(b):
+        return _is_tensor(b) and not b.is_cuda and b.is_contiguous() and b.dtype == t.complex128
+
+    host = [(k, b) for k, b in items if not isinstance(b, DeviceArray) and not cpu_view(b)]
     dev = [(k, b) for k, b in items if isinstance(b, DeviceArray)]
     groups = []          # (src tensor, [(src_off, key, block-shape)])
+    # host tensors that are views of one (pinned) allocation: one asynchronous
+    # copy of the whole allocation instead of one pageable copy per block
+    views: dict[int, tuple] = {}
+    for k, b in items:
+        if not isinstance(b, DeviceArray) and cpu_view(b):
+            base = b.untyped_storage().data_ptr()
+            views.setdefault(base, (b, []))[1].append(((b.data_ptr() - base) // 16, k))
+    for base, (st, entries) in views.items():
+        whole = t.empty(0, dtype=t.complex128).set_(st.untyped_storage(), 0, (st.untyped_storage().nbytes() // 16,))
+        dst = empty(int(whole.numel()))
+        dst.copy_(whole, non_blocking=bool(whole.is_pinned()))
+        groups.append((dst, entries))
     if host:
         tot = sum(int(sizes[i]) * int(sizes[j]) for (i, j), _ in host)
         stage = empty(tot)

@@ -240,6 +240,8 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out):
         if mr:
             if _dev_D(s):
                 D[i, :, :mr].copy_(s._d3m_D)
+            elif len(s.couplings) == 1:
+                _fill(D[i, :, :mr], s.couplings[0].D, (n, mr))
             else:
                 _fill(D[i, :, :mr], _coupling_matrix(s), (n, mr))
         _fill(f[i], s.f, (n, r))
@@ -304,7 +306,9 @@ def _fill(dst, src, shape):
             v = t.from_numpy(src.vals).to("cuda", non_blocking=False)
             dst[k // shape[1], k % shape[1]] = v
         return
-    if isinstance(src, DeviceArray) or type(src).__module__.startswith("torch"):
+    if type(src).__module__.startswith("torch") and not src.is_cuda:      # host tensor (pinned: async DMA)
+        dst.copy_(src.reshape(shape), non_blocking=bool(src.is_pinned()))
+    elif isinstance(src, DeviceArray) or type(src).__module__.startswith("torch"):
         dst.copy_(to_device(src).reshape(shape))
     else:
         dst.copy_(t.from_numpy(np.ascontiguousarray(np.asarray(src, dtype=np.complex128)).reshape(shape)))
