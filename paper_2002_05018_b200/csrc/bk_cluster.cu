@@ -44,12 +44,21 @@ struct BkcSlot {
   int pad;
 };
 
+// Each CTA posts its slot into every CTA's inbox (DSMEM stores) before the
+// cluster barrier; after it every CTA merges its own inbox from local shared
+// memory in rank order, so all CTAs hold bitwise-identical decisions.
 template <int CS>
-__device__ __forceinline__ BkcSlot bkc_merge(cg::cluster_group& cl, BkcSlot* slot, BkcSlot* out) {
+__device__ __forceinline__ void bkc_post(cg::cluster_group& cl, BkcSlot* box, int rank, const BkcSlot& v) {
+#pragma unroll
+  for (int c = 0; c < CS; ++c) *cl.map_shared_rank(box + rank, c) = v;
+}
+
+template <int CS>
+__device__ __forceinline__ BkcSlot bkc_merge(const BkcSlot* box, BkcSlot* out) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     BkcSlot r{-1.0, -1.0, -1.0, -1.0, 0x7fffffff, 0};
-    if (lane < CS) r = *cl.map_shared_rank(slot, lane);
+    if (lane < CS) r = box[lane];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double v2 = __shfl_xor_sync(0xffffffffu, r.v, o);
@@ -115,7 +124,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
   __shared__ double rv[BKC_NT / 32];
   __shared__ int ri[BKC_NT / 32];
   __shared__ double rst[BKC_NT / 32];
-  __shared__ BkcSlot slots[2], merged;
+  __shared__ BkcSlot inbox[2][CS], merged;
   const int rank = (int)cl.block_rank();
   const int b = blockIdx.x / CS;
   const int n = a.n, lda = a.lda, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -155,10 +164,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
   scale = bkc_block_max(scale, rv);
   asym = bkc_block_max(asym, rv);
   tm2 = bkc_block_max(tm2, rv);
-  if (tid == 0) slots[par] = BkcSlot{-1.0, scale, asym, tm2, 0x7fffffff, 0};
+  if (tid == 0) bkc_post<CS>(cl, inbox[par], rank, BkcSlot{-1.0, scale, asym, tm2, 0x7fffffff, 0});
   cl.sync();
   {
-    const BkcSlot m = bkc_merge<CS>(cl, &slots[par], &merged);
+    const BkcSlot m = bkc_merge<CS>(inbox[par], &merged);
     scale = m.own;
     asym = m.aux;
     tm2 = m.aux2;
@@ -212,17 +221,18 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
       st = warp_max(st);
       if (lane == 0) { rv[warp] = v; ri[warp] = vi; rst[warp] = st; }
       __syncthreads();
-      if (tid == 0) {
-        v = rv[0];
-        vi = ri[0];
-        st = rst[0];
-        for (int w = 1; w < NW; ++w) { argmax_merge(v, vi, rv[w], ri[w]); st = fmax(st, rst[w]); }
-        slots[par] = BkcSlot{v, -1.0, st, -1.0, vi, 0};
+      if (warp == 0) {
+        v = lane < NW ? rv[lane] : -1.0;
+        vi = lane < NW ? ri[lane] : 0x7fffffff;
+        st = lane < NW ? rst[lane] : -1.0;
+        warp_argmax(v, vi);
+        st = warp_max(st);
+        if (lane == 0) bkc_post<CS>(cl, inbox[par], rank, BkcSlot{v, -1.0, st, -1.0, vi, 0});
       }
     }
     BKC_MARK(0);
     cl.sync();
-    const BkcSlot m1 = bkc_merge<CS>(cl, &slots[par], &merged);
+    const BkcSlot m1 = bkc_merge<CS>(inbox[par], &merged);
     par ^= 1;
     BKC_MARK(1);
     if (prev_kstep && prev_k0 < n) {           // growth of the previous step (kernels.py:135-144)
@@ -270,9 +280,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
         }
       }
       rm = bkc_block_max(rm, rv);
-      if (tid == 0) slots[par] = BkcSlot{-1.0, -1.0, rm, -1.0, 0x7fffffff, 0};
+      if (tid == 0) bkc_post<CS>(cl, inbox[par], rank, BkcSlot{-1.0, -1.0, rm, -1.0, 0x7fffffff, 0});
       cl.sync();
-      const BkcSlot m2 = bkc_merge<CS>(cl, &slots[par], &merged);
+      const BkcSlot m2 = bkc_merge<CS>(inbox[par], &merged);
       par ^= 1;
       const double rowmax = m2.aux, absimax = x_abs(cC[imax]);
       if (__dmul_rn(absakk, rowmax) >= __dmul_rn(__dmul_rn(kBkcAlpha, colmax), colmax)) {
