@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define D3M_ABI_VERSION 2
+#define D3M_ABI_VERSION 3
 
 int d3m_abi_version(void);
 const char* d3m_last_error(void);
@@ -92,7 +92,10 @@ int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* C, voi
  * Replaces subdomain.reduce_domain (subdomain.py:166-184) for a batch; F_d
  * holds nrhs load columns (n x nrhs row-major; the reference's single f is
  * nrhs = 1), G_d is m x nrhs.  work_z / work_x: batch x n x (m+nrhs),
- * work_c: batch x m x (m+nrhs); work_x holds X on return.
+ * work_c: batch x m x (m+nrhs); work_x holds X on return.  Optional (ABI v3)
+ * rows: batch x nrows ascending row indices where D_d has nonzeros (-1
+ * padded): D^T X then runs over those rows only (work_d: batch x nrows x m;
+ * work_z is reused for the gathered X rows).  rows = NULL: dense product.
  * n <= 512: exact BK + chain solves (bk_scratch: batch*4n complex if n>3200);
  * n > 512: panel BK + blocked solves (bk_scratch: d3m_bk_panel_workspace
  * bytes, d_tasks: max(batch, 2 ceil(n/64) batch) records). */
@@ -100,7 +103,7 @@ int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const v
                              double pivot_tol,
                              void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
                              void* K_out, void* g_out, void* work_z, void* work_x, void* work_c, void* bk_scratch,
-                             void* d_tasks, void* stream);
+                             void* d_tasks, const void* rows, int nrows, void* work_d, void* stream);
 
 /* Grouped block copy / ordered accumulate (40-byte CopyTask records, see
  * d3m_misc.h).  Used for factor._permute_blocks (factor.py:139-151) and the

@@ -259,7 +259,8 @@ int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* Cm, vo
 int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const void* D, const void* f,
                              double pivot_tol, void* perm, void* tags, void* n2x2, void* growth, void* info,
                              void* scale, void* asym, void* K_out, void* g_out, void* work_z, void* work_x,
-                             void* work_c, void* bk_scratch, void* d_tasks, void* stream) {
+                             void* work_c, void* bk_scratch, void* d_tasks, const void* rows, int nrows,
+                             void* work_d, void* stream) {
   // A: batch x n x n (factored in place -> packed factor); D: batch x n x m;
   // F: batch x n x nrhs; work_z, work_x: batch x n x (m+nrhs); work_c: batch x m x (m+nrhs)
   if (batch < 0 || n < 0 || m < 0 || nrhs < 0) return fail(-22, "d3m_schur_reduce_batched: bad shape");
@@ -287,23 +288,38 @@ int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const v
   else
     D3M_TRY(d3m_ldlt_solve_batched(batch, n, A, nn, perm, n, tags, n, work_x, nw, w, w, work_z, stream));
   if (m == 0) return 0;
-  // C = D^T [X_D | X_F]  (subdomain.py:181,183) on DMMA, one task per domain
+  // C = D^T [X_D | X_F]  (subdomain.py:181,183) on DMMA, one task per domain.
+  // With a row list (the rows where D has nonzeros, ascending, -1 padded) the
+  // product runs over those rows only: D and X rows are gathered into
+  // compact buffers first (work_d: batch x nrows x m; work_z reused for X).
+  const bool sparse = rows != nullptr && nrows > 0 && nrows < n;
+  if (sparse) {
+    D3M_TRY(launch(kClsMisc, stream, [&] {
+      return d3m_gather_rows_batched_launch(D, (int64_t)n * m, m, rows, nrows, m, work_d, (int64_t)nrows * m, batch,
+                                            stream);
+    }));
+    D3M_TRY(launch(kClsMisc, stream, [&] {
+      return d3m_gather_rows_batched_launch(work_x, nw, w, rows, nrows, w, work_z, (int64_t)nrows * w, batch, stream);
+    }));
+  }
+  const int kdim = sparse ? nrows : n;
   std::vector<d3m::GemmTask> t(batch);
   for (int b = 0; b < batch; ++b) {
     d3m::GemmTask& k = t[b];
     std::memset(&k, 0, sizeof(k));
-    k.a_off = (int64_t)b * n * m;          // D stored n x m = K x M  (TA)
-    k.b_off = (int64_t)b * nw;             // X stored n x (m+nrhs) = K x N (TB)
+    k.a_off = (int64_t)b * kdim * m;       // D stored kdim x m = K x M  (TA)
+    k.b_off = (int64_t)b * (sparse ? (int64_t)nrows * w : nw);   // X stored kdim x (m+nrhs) = K x N (TB)
     k.c_off = (int64_t)b * m * w;
     k.m = m;
     k.n = w;
-    k.k = n;
+    k.k = kdim;
     k.lda = m;
     k.ldb = w;
     k.ldc = w;
     k.flags = d3m::kGemmStore;
   }
-  D3M_TRY(d3m_zgemm_grouped(1, 1, D, work_x, work_c, t.data(), batch, d_tasks, stream));
+  D3M_TRY(d3m_zgemm_grouped(1, 1, sparse ? work_d : D, sparse ? work_z : work_x, work_c, t.data(), batch, d_tasks,
+                            stream));
   // K_D = 0.5 (K_D + K_D^T), G_d
   D3M_TRY(launch(kClsMisc, stream, [&] {
     return d3m_schur_finalize_launch(work_c, K_out, g_out, m, nrhs, batch, (int64_t)m * w, (int64_t)m * m,

@@ -53,6 +53,8 @@ int d3m_gemm_launch(int ta, int tb, const void* A, const void* B, void* C, const
                     void* stream);
 int d3m_schur_finalize_launch(const void* C, void* K, void* g, int m, int nrhs, int batch, int64_t stride_c,
                               int64_t stride_k, int64_t stride_g, void* stream);
+int d3m_gather_rows_batched_launch(const void* src, int64_t stride_src, int ld_src, const void* idx, int nr, int cols,
+                                   void* out, int64_t stride_out, int batch, void* stream);
 int d3m_pack_rhs_launch(const void* D, const void* f, void* Z, int n, int m, int nrhs, int batch, int64_t stride_d,
                         int64_t stride_f, int64_t stride_z, void* stream);
 int d3m_ordered_average_launch(const void* E, const void* ptr, const void* src, void* out, int64_t ng, void* stream);

@@ -89,6 +89,18 @@ __global__ void gather_index_kernel(const cplx* src, const int64_t* idx, cplx* o
   }
 }
 
+// out[b][i][:] = src[b][idx[b][i]][:] (idx < 0: zero row), batched over blockIdx.y
+__global__ void gather_rows_batched_kernel(const cplx* src, int64_t stride_src, int ld_src, const int64_t* idx,
+                                           int nr, int cols, cplx* out, int64_t stride_out) {
+  const int b = blockIdx.y;
+  const int64_t total = (int64_t)nr * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / cols), c = (int)(e % cols);
+    const int64_t r = idx[(int64_t)b * nr + i];
+    out[b * stride_out + e] = r >= 0 ? src[b * stride_src + r * ld_src + c] : mk(0.0, 0.0);
+  }
+}
+
 static inline int flat_grid(int64_t n, int threads = 256, int cap = 8192) {
   int64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -139,6 +151,18 @@ extern "C" int d3m_ordered_average_launch(const void* E, const void* ptr, const 
   ordered_average_kernel<<<flat_grid(ng), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       static_cast<const cplx*>(E), static_cast<const int64_t*>(ptr), static_cast<const int64_t*>(src),
       static_cast<cplx*>(out), ng);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int d3m_gather_rows_batched_launch(const void* src, int64_t stride_src, int ld_src, const void* idx,
+                                              int nr, int cols, void* out, int64_t stride_out, int batch,
+                                              void* stream) {
+  using namespace d3m;
+  if (batch <= 0 || nr <= 0 || cols <= 0) return 0;
+  gather_rows_batched_kernel<<<dim3(flat_grid((int64_t)nr * cols, 256, 1024), batch), 256, 0,
+                               reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(src), stride_src, ld_src, static_cast<const int64_t*>(idx), nr, cols,
+      static_cast<cplx*>(out), stride_out);
   return (int)cudaGetLastError();
 }
 

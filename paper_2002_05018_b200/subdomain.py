@@ -162,7 +162,8 @@ def _domain_bytes(n: int, m: int, r: int) -> int:
     """Device bytes one domain of a reduce batch holds (A, D, F, X, Z, C, K, G,
     panel workspace)."""
     w = m + r
-    return 16 * (n * n + n * m + n * r + 2 * n * w + m * w + m * m + m * r) + 17 * 16 * n + 1024
+    # A, D, F, X, Z, C, K, G, the compact D rows of D^T X (<= 0.6 n), panel workspace
+    return 16 * (n * n + n * m + n * r + 2 * n * w + m * w + m * m + m * r + (6 * n * m) // 10) + 65 * 16 * n + 1024
 
 
 def _free_bytes(t) -> int:
@@ -264,9 +265,12 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out):
     else:
         scratch = empty((B, 4 * n)) if 64 * n > 200 * 1024 else None
         d_tasks = t.empty(64 * B, dtype=t.uint8, device="cuda")
+    rows, nrows = _nonzero_rows(D, n)
+    wd = empty((B, nrows, m)) if rows is not None else None
     _lib.call("d3m_schur_reduce_batched", B, n, m, r, _P(A), _P(D), _P(f), float(pivot_tol), _P(perm),
               _P(tags), _P(n2), _P(gr), _P(info), _P(sc), _P(asy), _P(K), _P(g), _P(wz), _P(wx), _P(wc),
-              _P(scratch), _P(d_tasks), stream_ptr())
+              _P(scratch), _P(d_tasks), _P(rows), int(nrows), _P(wd), stream_ptr())
+    del wd, rows
     del wz, scratch, wc
     try:
         facs = _collect(A, perm, tags, n2, info, gr, sc, asy, pivot_tol, None,
@@ -292,6 +296,26 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out):
         gi = g[i, :mr, 0] if vec else g[i, :mr, :]
         out[idx] = (DeviceArray(K[i, :mr, :mr]), DeviceArray(gi))
     return None
+
+
+def _nonzero_rows(D, n):
+    """Rows where each domain's coupling block D_d (the filled device batch
+    B x n x m) has nonzeros, ascending and -1 padded to the batch maximum,
+    for D^T X over those rows only; (None, 0) when the couplings are dense
+    enough that the full product is as cheap.  One pass over D, one sync."""
+    t = require_cuda()
+    B = D.shape[0]
+    if D.shape[2] == 0 or n == 0:
+        return None, 0
+    nz = t.view_as_real(D).reshape(B, n, -1).ne(0).any(dim=2)             # B x n
+    nrows = int(nz.sum(dim=1).max().item())
+    if nrows == 0 or nrows > 0.6 * n:
+        return None, 0
+    ar = t.arange(n, device=D.device, dtype=t.int64)
+    key = t.where(nz, ar, ar + n)                                          # nonzero rows first, ascending
+    idx = t.sort(key, dim=1).values[:, :nrows]
+    idx = t.where(idx < n, idx, t.full_like(idx, -1)).contiguous()
+    return idx, nrows
 
 
 def _fill(dst, src, shape):
