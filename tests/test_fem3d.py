@@ -108,3 +108,20 @@ def test_sparse_subdomain_blocks_match_dense_assembly():
         assert np.array_equal(a.f, b.f)
         for ca, cb in zip(a.couplings, b.couplings):
             assert np.array_equal(bits(ca.D), bits(cb.D))
+
+
+FEM_GOLDEN_CASES = [dict(cells=4, side=0.5, parts=(2, 2, 2), sphere_radius=0.15),
+                    dict(cells=6, side=0.5, parts=(3, 1, 1), sphere_radius=0.2)]
+
+
+@pytest.mark.parametrize("case", [0, 1])
+def test_lambda_space_matches_reference_on_fem(case):
+    """interface_lambda_nodes (subdomain.py:75-111) on the 3-D Nedelec
+    partition equals the reference's own output (tools/gen_golden.py gen_fem)."""
+    from conftest import golden
+    from paper_2002_05018_b200 import fem3d, interface_lambda_nodes
+    g = golden("fem_small.npz")
+    model = fem3d.build_model(fem3d.FemProblem(**FEM_GOLDEN_CASES[case]))
+    kept = interface_lambda_nodes(model)
+    assert np.array_equal(np.concatenate(kept), g[f"c{case}_kept"])
+    assert np.array_equal(np.array([k.size for k in kept]), g[f"c{case}_sizes"])

@@ -137,6 +137,46 @@ def gen_small():
     print("small fixtures written")
 
 
+def gen_fem():
+    """The reference's own reduce_domain / assemble_reduced / block_ldlt /
+    block_solve / recover_primal on small 3-D Nedelec models from fem3d.py
+    (dense A_d, D_d handed over as numpy arrays; the FemModel serves as the
+    partition shim: interfaces[*].{nodes, dom_lo, dom_hi}, incident_interfaces)."""
+    from paper_2002_05018_b200 import fem3d
+    recs = {}
+    cases = [fem3d.FemProblem(4, 0.5, (2, 2, 2), sphere_radius=0.15),
+             fem3d.FemProblem(6, 0.5, (3, 1, 1), sphere_radius=0.2)]
+    for case, prob in enumerate(cases):
+        model = fem3d.build_model(prob)
+        systems = fem3d.subdomain_systems(model, rhs=0, sparse=False)
+        rsys_list = [rs.SubdomainSystem(s.domain, np.asarray(s.A), np.asarray(s.f), s.dof_map,
+                                        [rs.Coupling(c.interface, np.asarray(c.D), c.sign) for c in s.couplings])
+                     for s in systems]
+        t0 = time.perf_counter()
+        red = [rs.reduce_domain(s) for s in rsys_list]
+        R = rs.assemble_reduced(red, model)
+        g = rb.clique_graph(R.K)
+        order = ro.reorder(g, R.K.sizes)
+        plan = rsym.symbolic_factor(g, order, R.K.sizes)
+        F = rf.block_ldlt(R.K, plan)
+        lam = rf.block_solve(F, R.g)
+        sol = rs.recover_primal(rsys_list, lam)
+        print(f"fem case {case}: n_sub {[s.n_dofs for s in systems]}, lambda {int(R.interface_sizes.sum())}, "
+              f"{time.perf_counter() - t0:.1f}s")
+        recs[f"c{case}_kept"] = np.concatenate(rs.interface_lambda_nodes(model))
+        recs[f"c{case}_sizes"] = np.asarray(R.interface_sizes)
+        for d in range(len(systems)):
+            recs[f"c{case}_fperm{d}"] = rsys_list[d].factor.perm
+            recs[f"c{case}_ftags{d}"] = rsys_list[d].factor.tags
+            recs[f"c{case}_KD{d}"] = red[d][0]
+        recs[f"c{case}_order"] = order.perm
+        recs[f"c{case}_bperm"] = np.concatenate([f.perm for f in F.diag])
+        recs[f"c{case}_lam"] = np.concatenate(lam)
+        recs[f"c{case}_sol"] = sol
+    np.savez_compressed(os.path.join(OUT, "fem_small.npz"), **recs)
+    print("fem fixtures written")
+
+
 def gen_cfg4():
     t0 = time.perf_counter()
     K = wl.config4_matrix()
@@ -184,6 +224,8 @@ if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what in ("small", "all"):
         gen_small()
+    if what in ("fem", "all"):
+        gen_fem()
     if what in ("cfg4", "all"):
         gen_cfg4()
     if what in ("cfg3", "all"):
