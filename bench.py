@@ -314,8 +314,9 @@ def _fem_secondary(which: str, reps: int) -> dict:
     res = fem3d.global_residual(model, sol, rhs=None)
     r = int(model.f.shape[1])
     ms_sub = [sum(int(np.shape(c.D)[1]) for c in s.couplings) for s in systems]
-    flops_sub = sum(8 * s.n_dofs ** 3 // 3 + 8 * s.n_dofs ** 2 * (m + r) + 8 * m * (m + r) * s.n_dofs
-                    for s, m in zip(systems, ms_sub))
+    # algorithmic: complex symmetric LDL^T 4n^3/3 + the (m+r)-RHS solves 8n^2(m+r);
+    # D^T X is a sparse product (D = s M_Gamma on interface rows) and not counted
+    flops_sub = sum(4 * s.n_dofs ** 3 // 3 + 8 * s.n_dofs ** 2 * (m + r) for s, m in zip(systems, ms_sub))
     out = {"workload": f"{which}: {cfg.cells}^3 hex x6 tets Nedelec, {cfg.parts} subdomains, "
                        f"{model.mesh.n_edges} edges, lambda={int(R.interface_sizes.sum())}, {r} RHS",
            "d3m_ms": round(best["d3m_total"] * 1e3, 1),
@@ -341,7 +342,9 @@ def _cfg3_secondary(steps: int) -> dict:
                              [d.Coupling(c.interface, DeviceArray(to_device(c.D)), c.sign) for c in s.couplings])
            for s in host]
     n, m, B = 2048, 384, 64
-    flops = B * (8 * n ** 3 // 3 + 8 * n * n * (m + 1))       # BK + the (m+1)-RHS solves
+    # complex symmetric LDL^T = 4n^3/3 (SURVEY 8(d)'s 8n^3/3 is the LU count),
+    # + the (m+1)-RHS solves 8n^2(m+1); D^T X for +-1 selectors is a gather (0 flops)
+    flops = B * (4 * n ** 3 // 3 + 8 * n * n * (m + 1))
     for s in dev:
         s._d3m_D = None
     d.reduce_domains(dev)

@@ -364,7 +364,7 @@ class _Schedule:
                                     4 * int(sizes[i]) ** 2 * int(sizes[j])
                                     for j in range(nb) for a, i in enumerate(pattern[j]) for kk in pattern[j][:a + 1]))
         self.flops_trsm = int(sum(4 * int(self.panel_rows[j]) * int(sizes[j]) ** 2 for j in range(nb)))
-        self.flops_bk = int(sum(8 * int(s) ** 3 // 3 for s in sizes))
+        self.flops_bk = int(sum(4 * int(s) ** 3 // 3 for s in sizes))     # complex LDL^T: 4n^3/3
         self.stats_cache = {}
 
 
