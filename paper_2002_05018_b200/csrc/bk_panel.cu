@@ -510,11 +510,25 @@ static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* task
   int cs = batch * 16 <= 296 ? 16 : batch * 8 <= 296 ? 8 : batch * 4 <= 296 ? 4 : batch * 2 <= 296 ? 2 : 1;
   if (const char* env = getenv("D3M_PANEL_CS")) cs = atoi(env);
   if (cs != 1 && cs != 2 && cs != 4 && cs != 8 && cs != 16) cs = 1;
-  static bool np16 = false;
-  if (cs == 16 && !np16) {
+  static int ok16 = -1;          // can this device keep a 16-CTA cluster of the panel kernel resident?
+  if (cs == 16 && ok16 < 0) {
     cudaFuncSetAttribute(bk_panel_kernel<NB, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    np16 = true;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 16;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(16);
+    cfg.blockDim = dim3(CNT);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    ok16 = (cudaOccupancyMaxActiveClusters(&nclusters, bk_panel_kernel<NB, 16>, &cfg) == cudaSuccess &&
+            nclusters > 0) ? 1 : 0;
+    cudaGetLastError();
   }
+  if (cs == 16 && ok16 == 0) cs = 8;
   for (int p = 0; p * (NB - 1) < n; ++p) {
     const int mrem = n - (p + 1) * (NB - 1);           // rows left after this panel (upper bound)
     const int tm = mrem > 0 ? (mrem + 63) / 64 : 0;
