@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define D3M_ABI_VERSION 3
+#define D3M_ABI_VERSION 4
 
 int d3m_abi_version(void);
 const char* d3m_last_error(void);
@@ -96,6 +96,8 @@ int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* C, voi
  * rows: batch x nrows ascending row indices where D_d has nonzeros (-1
  * padded): D^T X then runs over those rows only (work_d: batch x nrows x m;
  * work_z is reused for the gathered X rows).  rows = NULL: dense product.
+ * flags (ABI v4): bit 0 = Schur only -- forward sweep Z = L^-1 P [D | F]
+ * and K = Z_D^T D^-1 Z (no backward sweep; work_x does not hold X then).
  * n <= 512: exact BK + chain solves (bk_scratch: batch*4n complex if n>3200);
  * n > 512: panel BK + blocked solves (bk_scratch: d3m_bk_panel_workspace
  * bytes, d_tasks: max(batch, 2 ceil(n/64) batch) records). */
@@ -103,7 +105,7 @@ int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const v
                              double pivot_tol,
                              void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
                              void* K_out, void* g_out, void* work_z, void* work_x, void* work_c, void* bk_scratch,
-                             void* d_tasks, const void* rows, int nrows, void* work_d, void* stream);
+                             void* d_tasks, const void* rows, int nrows, void* work_d, int flags, void* stream);
 
 /* Grouped block copy / ordered accumulate (40-byte CopyTask records, see
  * d3m_misc.h).  Used for factor._permute_blocks (factor.py:139-151) and the

@@ -152,9 +152,22 @@ int d3m_ldlt_solve_batched(int batch, int n, const void* F, int64_t stride_f, co
 // owns exactly one GEMM, so every straddling 2x2 e-entry is applied once and
 // corrected once by the next diagonal kernel.  d_tasks: >= 2 * ceil(n/64) *
 // batch GEMM records.
+static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stride_f, const void* perm,
+                                   int64_t stride_p, const void* tags, int64_t stride_t, void* B, int64_t stride_b,
+                                   int ldb, int m, void* work, void* d_tasks, void* stream, bool fwd_only);
+
 int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stride_f, const void* perm,
                                    int64_t stride_p, const void* tags, int64_t stride_t, void* B, int64_t stride_b,
                                    int ldb, int m, void* work, void* d_tasks, void* stream) {
+  return ldlt_solve_blocked_impl(batch, n, F, stride_f, perm, stride_p, tags, stride_t, B, stride_b, ldb, m, work,
+                                 d_tasks, stream, false);
+}
+
+// fwd_only: stop after Z = L^-1 P B (left in `work`, pivot order): the Schur
+// reduction K = Z^T D^-1 Z needs no backward sweep.
+static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stride_f, const void* perm,
+                                   int64_t stride_p, const void* tags, int64_t stride_t, void* B, int64_t stride_b,
+                                   int ldb, int m, void* work, void* d_tasks, void* stream, bool fwd_only) {
   if (batch < 0 || n < 0 || m < 0 || ldb < m) return fail(-22, "d3m_ldlt_solve_blocked_batched: bad shape");
   if (batch == 0 || n == 0 || m == 0) return 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -216,6 +229,7 @@ int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stri
         return d3m_gemm_launch(0, 1, F, work, work, dt + (size_t)ib * batch, batch, tiles[ib], stream);
       }));
   }
+  if (fwd_only) return 0;
   D3M_TRY(launch(kClsSolve, stream, [&] { return d3m_solve_phase_launch(2, &sb, batch, stream); }));   // D^-1
   for (int ib = nblk - 1; ib >= 0; --ib) {
     const int r0 = ib * DBR;
@@ -260,7 +274,7 @@ int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const v
                              double pivot_tol, void* perm, void* tags, void* n2x2, void* growth, void* info,
                              void* scale, void* asym, void* K_out, void* g_out, void* work_z, void* work_x,
                              void* work_c, void* bk_scratch, void* d_tasks, const void* rows, int nrows,
-                             void* work_d, void* stream) {
+                             void* work_d, int flags, void* stream) {
   // A: batch x n x n (factored in place -> packed factor); D: batch x n x m;
   // F: batch x n x nrhs; work_z, work_x: batch x n x (m+nrhs); work_c: batch x m x (m+nrhs)
   if (batch < 0 || n < 0 || m < 0 || nrhs < 0) return fail(-22, "d3m_schur_reduce_batched: bad shape");
@@ -278,10 +292,52 @@ int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const v
     D3M_TRY(d3m_bk_factor_batched(batch, n, A, nn, n, pivot_tol, 1, perm, tags, n2x2, growth, info, scale, asym,
                                   bk_scratch, stream));
   if (n == 0 || w == 0) return 0;
-  // RHS = [D | F]  (subdomain.py:177-179), X = A^-1 RHS (factor.py:52-66)
+  // RHS = [D | F]  (subdomain.py:177-179)
   D3M_TRY(launch(kClsMisc, stream, [&] {
     return d3m_pack_rhs_launch(D, f, work_x, n, m, nrhs, batch, (int64_t)n * m, (int64_t)n * nrhs, nw, stream);
   }));
+  if ((flags & 1) && m > 0) {
+    // Schur only: A^-1 = P^T L^-T D^-1 L^-1 P, so with Z = L^-1 P [D | F]
+    // (forward sweep only) C = Z_D^T D^-1 Z = D^T A^-1 [D | F]
+    if (big)
+      D3M_TRY(ldlt_solve_blocked_impl(batch, n, A, nn, perm, n, tags, n, work_x, nw, w, w, work_z, d_tasks, stream,
+                                      true));
+    else {
+      d3m::SolveBatch sf{CC(A), nn, static_cast<const int8_t*>(tags), n, static_cast<const int64_t*>(perm), n,
+                         C(work_z), nw, nullptr, 0, CC(work_x), nw, n, w, w, w};
+      for (int phase = 0; phase < 2; ++phase)
+        D3M_TRY(launch(kClsSolve, stream, [&] { return d3m_solve_phase_launch(phase, &sf, batch, stream); }));
+    }
+    // U = D^-1 Z (work_x), Z stays in work_z
+    cudaError_t ce = cudaMemcpyAsync(work_x, work_z, sizeof(cplx) * (size_t)batch * nw, cudaMemcpyDeviceToDevice,
+                                     reinterpret_cast<cudaStream_t>(stream));
+    if (ce != cudaSuccess) return fail((int)ce, "d3m_schur_reduce_batched: copy");
+    d3m::SolveBatch su{CC(A), nn, static_cast<const int8_t*>(tags), n, static_cast<const int64_t*>(perm), n,
+                       C(work_x), nw, nullptr, 0, CC(work_x), nw, n, w, w, w};
+    D3M_TRY(launch(kClsSolve, stream, [&] { return d3m_solve_phase_launch(2, &su, batch, stream); }));
+    std::vector<d3m::GemmTask> t(batch);
+    for (int b = 0; b < batch; ++b) {
+      d3m::GemmTask& k = t[b];
+      std::memset(&k, 0, sizeof(k));
+      k.a_off = (int64_t)b * nw;           // Z_D: n x (m + nrhs), first m columns = K x M (TA)
+      k.b_off = (int64_t)b * nw;           // U: n x (m + nrhs) = K x N (TB)
+      k.c_off = (int64_t)b * m * w;
+      k.m = m;
+      k.n = w;
+      k.k = n;
+      k.lda = w;
+      k.ldb = w;
+      k.ldc = w;
+      k.flags = d3m::kGemmStore;
+    }
+    D3M_TRY(d3m_zgemm_grouped(1, 1, work_z, work_x, work_c, t.data(), batch, d_tasks, stream));
+    D3M_TRY(launch(kClsMisc, stream, [&] {
+      return d3m_schur_finalize_launch(work_c, K_out, g_out, m, nrhs, batch, (int64_t)m * w, (int64_t)m * m,
+                                       (int64_t)m * nrhs, stream);
+    }));
+    return 0;
+  }
+  // X = A^-1 RHS (factor.py:52-66)
   if (big)
     D3M_TRY(d3m_ldlt_solve_blocked_batched(batch, n, A, nn, perm, n, tags, n, work_x, nw, w, w, work_z, d_tasks,
                                            stream));

@@ -186,10 +186,13 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
     reference's A_d^-1 (F_d - D_d lambda_d)); it is what lets config 5
     (64 x n = 13,428, 185 GB of factors) run in 180 GB of HBM.  keep="auto"
     chooses "solution" when all factors would not fit in half the free
-    device memory."""
+    device memory.  keep="schur" keeps the factor but forms only the Schur
+    blocks, as K = Z_D^T D^-1 Z with Z = L^-1 P [D | F] (A^-1 = P^T L^-T D^-1
+    L^-1 P): no backward sweep, no X (recover_primal then solves with the
+    factor) -- for reductions whose primal recovery is not needed (config 3)."""
     t = require_cuda()
-    if keep not in ("factor", "solution", "auto"):
-        raise ValueError(f"keep must be 'factor', 'solution' or 'auto', not {keep!r}")
+    if keep not in ("factor", "solution", "auto", "schur"):
+        raise ValueError(f"keep must be 'factor', 'solution', 'auto' or 'schur', not {keep!r}")
     # one batch per subdomain order n (the factorisation does not depend on
     # m); coupling blocks are zero-padded to the group's largest m and each
     # domain's K_D / g_d is the leading m x m / m view of its padded result
@@ -265,11 +268,11 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out):
     else:
         scratch = empty((B, 4 * n)) if 64 * n > 200 * 1024 else None
         d_tasks = t.empty(64 * B, dtype=t.uint8, device="cuda")
-    rows, nrows = _nonzero_rows(D, n)
+    rows, nrows = _nonzero_rows(D, n) if keep != "schur" else (None, 0)
     wd = empty((B, nrows, m)) if rows is not None else None
     _lib.call("d3m_schur_reduce_batched", B, n, m, r, _P(A), _P(D), _P(f), float(pivot_tol), _P(perm),
               _P(tags), _P(n2), _P(gr), _P(info), _P(sc), _P(asy), _P(K), _P(g), _P(wz), _P(wx), _P(wc),
-              _P(scratch), _P(d_tasks), _P(rows), int(nrows), _P(wd), stream_ptr())
+              _P(scratch), _P(d_tasks), _P(rows), int(nrows), _P(wd), 1 if keep == "schur" else 0, stream_ptr())
     del wd, rows
     del wz, scratch, wc
     try:
@@ -284,10 +287,13 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out):
         # X = A^-1 [D | F] (m padded) is kept in both modes: recover_primal
         # forms E = X_F - X_D lambda from it while the loads and couplings are
         # the arrays reduced here (identity check), else solves with the factor
-        s._d3m_X = wx[i]
-        s._d3m_Xm = m
-        s._d3m_src = (s.f, tuple(c.D for c in s.couplings))
-        if keep == "factor":
+        if keep == "schur":            # no X: recovery solves with the factor
+            s._d3m_X, s._d3m_src = None, None
+        else:
+            s._d3m_X = wx[i]
+            s._d3m_Xm = m
+            s._d3m_src = (s.f, tuple(c.D for c in s.couplings))
+        if keep in ("factor", "schur"):
             s.factor = facs[i]
             s._d3m_D = D[i, :, :mr]
         else:

@@ -121,16 +121,18 @@ def test_assemble_size_mismatch(cuda):
 
 
 @pytest.mark.slow
-def test_config3_pivots_and_schur_vs_reference(cuda):
+@pytest.mark.parametrize("keep", ["factor", "schur"])
+def test_config3_pivots_and_schur_vs_reference(cuda, keep):
     """BASELINE config 3 subdomains (n=2048, m=384): the GPU pivot sequence is
-    bit-exact with the reference's and K_D matches to 1e-9 relative."""
+    bit-exact with the reference's and K_D matches to 1e-9 relative -- with
+    the X-based reduction and the forward-only Schur form alike."""
     import paper_2002_05018_b200 as d
     from paper_2002_05018_b200 import workloads as wl
     g = golden("cfg3.npz")
     doms = [int(i) for i in g["domains"]]
     systems = [d.SubdomainSystem(i, *[wl.config3_domain(i)[k] for k in (0, 2)], np.arange(2048),
                                  [d.Coupling(0, wl.config3_domain(i)[1], 1)]) for i in doms]
-    red = d.reduce_domains(systems)
+    red = d.reduce_domains(systems, keep=keep)
     for s, (KD, gd) in zip(systems, red):
         i = s.domain
         assert np.array_equal(s.factor.perm, g[f"perm{i}"].astype(np.int64))

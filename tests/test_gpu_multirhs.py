@@ -97,3 +97,32 @@ def test_recovery_from_retained_solution_matches_factor_solve(cuda, cells, parts
     for q in range(2):
         sol_q, *_ = fem3d.solve_d3m(model, rhs=q, keep="factor")
         assert np.linalg.norm(sol_x[:, q] - sol_q) <= 1e-13 * np.linalg.norm(sol_q)
+
+
+@pytest.mark.parametrize("n,m,r", [(300, 24, 2), (700, 31, 1)])
+def test_schur_only_reduce_matches_full_reduce(cuda, n, m, r):
+    """keep="schur": K = Z_D^T D^-1 Z with only the forward sweep equals the
+    X-based D^T A^-1 D to rounding, with identical pivots (same factor)."""
+    import paper_2002_05018_b200 as d
+    a = _systems(n, m, 2, r, seed=11 * n)
+    b = _systems(n, m, 2, r, seed=11 * n)
+    ra = d.reduce_domains(a)
+    rb = d.reduce_domains(b, keep="schur")
+    for (Ka, ga), (Kb, gb), sa, sb in zip(ra, rb, a, b):
+        Ka, Kb, ga, gb = map(np.asarray, (Ka, Kb, ga, gb))
+        assert np.array_equal(sa.factor.perm, sb.factor.perm)
+        assert np.linalg.norm(Kb - Ka) <= 1e-11 * np.linalg.norm(Ka)
+        assert np.linalg.norm(gb - ga) <= 1e-11 * np.linalg.norm(ga)
+        assert np.array_equal(Kb, Kb.T)
+        assert getattr(sb, "_d3m_X", None) is None and not sb.factor.released
+
+
+def test_schur_only_fem_pipeline(cuda):
+    """The FEM pipeline with keep="schur" recovers through the factor solve
+    and agrees with the default pipeline to 1e-9."""
+    from paper_2002_05018_b200 import fem3d
+    model = fem3d.build_model(fem3d.FemProblem(8, 0.5, (2, 1, 1), sphere_radius=0.15))
+    sol_a, *_ = fem3d.solve_d3m(model, rhs=0)
+    sol_b, *_ = fem3d.solve_d3m(model, rhs=0, keep="schur")
+    assert np.linalg.norm(sol_b - sol_a) <= 1e-9 * np.linalg.norm(sol_a)
+    assert fem3d.global_residual(model, sol_b) <= 1e-10

@@ -12,7 +12,7 @@ for it in range(2):
     for s in systems: s.factor = None; s._d3m_D = None
     _lib.counters_reset(timing=True)
     torch.cuda.synchronize(); t0 = time.perf_counter()
-    red = d.reduce_domains(systems)
+    red = d.reduce_domains(systems, keep=os.environ.get("KEEP", "factor"))
     torch.cuda.synchronize(); t1 = time.perf_counter()
     c = _lib.counters_read(); _lib.counters_reset(False)
     print(f"cfg3 {count} domains: {1e3*(t1-t0):.1f} ms; per-class union ms " + str({k: round(v, 1) for k, v in c['union_ms'].items()}), flush=True)
