@@ -554,10 +554,10 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
 }
 
 // ---------------------------------------------------------------------------
-// block_solve executor (factor.py:243-310), all RHS in one pass, HBM-bound
-// tall-skinny kernels against the stored factor (solve_gemv.cu):
+// block_solve executor (factor.py:243-310), all RHS in one pass, tall-skinny
+// DMMA products against the stored factor (skinny_dmma.cu):
 //   forward  z_j = Binv_j b_j,  u_j = D_j^-1 z_j,  b_i -= L_ij z_j
-//   backward w_j = u_j - sum_i L_ij^T x_i  (row chunks, ordered sum),
+//   backward w_j = u_j - sum_i L_ij^T x_i  (split-K partials, ordered sum),
 //            x_j = Binv_j^T w_j
 //   b, u, x : N x nrhs plan order (b consumed);  tmp: max n_j x nrhs;
 //   part    : partial sums, part_elems complex

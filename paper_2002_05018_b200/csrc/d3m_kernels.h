@@ -47,8 +47,6 @@ int d3m_skinny_reduce_launch(const void* base, int ldb, const void* part, int nc
                              void* out, int ldo, void* stream);
 // phase: 0 gather Z=B[perm], 1 forward (+U=D^-1 Z), 2 D^-1, 3 backward, 4 scatter B[perm]=Z
 int d3m_solve_phase_launch(int phase, d3m::SolveBatch* a, int batch, void* stream);
-int d3m_panel_trsm_launch(void* P, void* X, int R, int n, const void* F, const void* perm, const void* tags,
-                          void* stream);
 int d3m_gemm_launch(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks, int ntasks, int ntiles,
                     void* stream);
 int d3m_schur_finalize_launch(const void* C, void* K, void* g, int m, int nrhs, int batch, int64_t stride_c,
@@ -66,13 +64,6 @@ int d3m_tri_inv_launch(const void* F, int64_t stride_f, const void* perm, int64_
                        int64_t stride_t, void* Binv, int64_t stride_b, int n, int batch, void* stream);
 int d3m_dinv_rows_launch(const void* X, void* P, int64_t R, int n, const void* F, const void* tags, void* stream);
 int d3m_dinv_left_copy_launch(const void* Z, void* U, int n, int m, const void* F, const void* tags, void* stream);
-int d3m_rows_gemv_launch(const void* A, int lda, int M, int K, const void* B, int ldb, int N, void* C, int ldc,
-                         const void* cmap, int sub, void* stream);
-int d3m_cols_gemv_launch(const void* A, int lda, int R, int Mcols, const void* B, int ldb, const void* bmap, int N,
-                         void* partial, void* stream);
-int d3m_chunk_reduce_launch(const void* base, const void* partial, int nch, int64_t len, double sign, void* out,
-                            void* stream);
-int d3m_solve_rows_per_chunk();
 int d3m_tri_inv_warp_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef, int n,
                             void* stream);
 int d3m_dinv_rows_coef_launch(const void* X, void* P, int64_t R, int n, const void* tags, const void* coef,
@@ -82,7 +73,6 @@ int d3m_diag_block_launch(int fwd, const void* F, int64_t stride_f, const void* 
 int d3m_diag_block_rows();
 int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* workspace, void* stream);
 size_t d3m_bk_panel_workspace_bytes(int n, int batch);
-int d3m_sub_partials_launch(const void* u, const void* partial, int np, int64_t len, void* out, void* stream);
 }
 
 #include "d3m_gemm.h"

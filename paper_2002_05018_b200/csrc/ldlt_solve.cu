@@ -6,8 +6,6 @@
 // at position i.
 //
 // Kernels
-//  * panel_trsm_kernel   X = K_ij[:, perm] L_jj^-T and L_ij = X D_jj^-1 for
-//                        a stacked panel of pattern blocks (factor.py:195-210)
 //  * lsolve_fwd_kernel   Z = L^-1 Z (optionally U = D^-1 Z)   (kernels.py:149)
 //  * lsolve_bwd_kernel   Z = L^-T Z                           (kernels.py:155)
 //  * dinv_left_kernel    Z = D^-1 Z                           (kernels.py:161)
@@ -27,63 +25,6 @@ __device__ __forceinline__ cplx lfac(const cplx* F, int ld, const int8_t* tags, 
   // L[r][c] for c < r from the packed factor
   if (r == c + 1 && tags[c] == 2) return mk(0.0, 0.0);
   return F[(int64_t)r * ld + c];
-}
-
-// -------------------------------------------------------------------------
-// Panel TRSM: rows [r0, r0+RT) of a panel P (R x n, ld n) hold K_ij rows.
-// One 16-lane group per row.  Output: X rows (for the Schur update) and
-// L rows written back into P.
-// -------------------------------------------------------------------------
-constexpr int TRSM_THREADS = 256;
-
-__global__ void __launch_bounds__(TRSM_THREADS)
-panel_trsm_kernel(cplx* P, cplx* X, int R, int n, const cplx* F, const int64_t* perm, const int8_t* tags) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int RT = TRSM_THREADS / 16;
-  cplx* S = reinterpret_cast<cplx*>(smem_raw);  // RT x n
-  const int r0 = blockIdx.x * RT;
-  const int g = threadIdx.x >> 4, s = threadIdx.x & 15;
-  const int row = r0 + g;
-  const bool live = row < R;
-  cplx* x = S + (int64_t)g * n;
-
-  // gather K_ij[row, perm[c]]
-  if (live)
-    for (int c = s; c < n; c += 16) x[c] = P[(int64_t)row * n + perm[c]];
-  __syncwarp();
-
-  // left-looking forward substitution: x[c] -= sum_{c'<c} x[c'] L[c][c']
-  for (int c = 1; c < n; ++c) {
-    cplx acc = mk(0.0, 0.0);
-    if (live) {
-      const cplx* Lr = F + (int64_t)c * n;
-      for (int cp = s; cp < c; cp += 16) {
-        cplx l = (cp == c - 1 && tags[cp] == 2) ? mk(0.0, 0.0) : __ldg(Lr + cp);
-        c_fma(acc, x[cp], l);
-      }
-    }
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, 16);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, 16);
-    }
-    if (live && s == 0) x[c] = c_sub(x[c], acc);
-    __syncwarp();
-  }
-  if (!live) return;
-  // X row, then L row = X D^-1 (apply_dinv_right, kernels.py:184-202)
-  for (int c = s; c < n; c += 16) X[(int64_t)row * n + c] = x[c];
-  for (int c = s; c < n; c += 16) {
-    const int8_t t = tags[c];
-    if (t == 1) {
-      P[(int64_t)row * n + c] = x_div_np(x[c], F[(int64_t)c * n + c]);
-    } else if (t == 2) {
-      cplx x0 = x[c], x1 = x[c + 1];
-      dinv_pair(F[(int64_t)c * n + c], F[(int64_t)(c + 1) * n + c], F[(int64_t)(c + 1) * n + c + 1], x0, x1);
-      P[(int64_t)row * n + c] = x0;
-      P[(int64_t)row * n + c + 1] = x1;
-    }
-  }
 }
 
 // -------------------------------------------------------------------------
@@ -212,24 +153,6 @@ __global__ void __launch_bounds__(LS_THREADS) dinv_left_kernel(SolveBatch a) {
 
 }  // namespace d3m
 
-
-extern "C" int d3m_panel_trsm_launch(void* P, void* X, int R, int n, const void* F, const void* perm,
-                                     const void* tags, void* stream) {
-  using namespace d3m;
-  if (R <= 0 || n <= 0) return 0;
-  constexpr int RT = TRSM_THREADS / 16;
-  const size_t smem = (size_t)RT * n * sizeof(cplx);
-  if (smem > 220 * 1024) return -22;
-  static int configured = 0;
-  if (!configured) {
-    cudaFuncSetAttribute(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    configured = 1;
-  }
-  panel_trsm_kernel<<<(R + RT - 1) / RT, TRSM_THREADS, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
-      static_cast<cplx*>(P), static_cast<cplx*>(X), R, n, static_cast<const cplx*>(F),
-      static_cast<const int64_t*>(perm), static_cast<const int8_t*>(tags));
-  return (int)cudaGetLastError();
-}
 
 // phase: 0 gather, 1 forward (+U), 2 dinv, 3 backward, 4 scatter
 extern "C" int d3m_solve_phase_launch(int phase, d3m::SolveBatch* a, int batch, void* stream) {
@@ -373,14 +296,6 @@ __global__ void dinv_left_copy_kernel(const cplx* Z, cplx* U, int n, int m, cons
 }
 
 // out = u - sum_{p < np} partial[p]  (fixed order), each of length len
-__global__ void sub_partials_kernel(const cplx* u, const cplx* partial, int np, int64_t len, cplx* out) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
-    cplx acc = mk(0.0, 0.0);
-    for (int p = 0; p < np; ++p) acc = c_add(acc, partial[p * len + e]);
-    out[e] = c_sub(u[e], acc);
-  }
-}
-
 }  // namespace d3m
 
 extern "C" int d3m_tri_inv_launch(const void* F, int64_t stride_f, const void* perm, int64_t stride_p,
@@ -423,16 +338,6 @@ extern "C" int d3m_dinv_left_copy_launch(const void* Z, void* U, int n, int m, c
   dinv_left_copy_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       static_cast<const cplx*>(Z), static_cast<cplx*>(U), n, m, static_cast<const cplx*>(F),
       static_cast<const int8_t*>(tags));
-  return (int)cudaGetLastError();
-}
-
-extern "C" int d3m_sub_partials_launch(const void* u, const void* partial, int np, int64_t len, void* out,
-                                       void* stream) {
-  using namespace d3m;
-  if (len <= 0) return 0;
-  const int blocks = (int)std::min<int64_t>((len + 255) / 256, 4096);
-  sub_partials_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      static_cast<const cplx*>(u), static_cast<const cplx*>(partial), np, len, static_cast<cplx*>(out));
   return (int)cudaGetLastError();
 }
 
