@@ -267,16 +267,23 @@ zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
   if (m0 >= M || n0 >= N) return;
   const int mode = tk.flags & kGemmModeMask;
   const int t = threadIdx.x;
-  // ---- one-shot staging: A, B (64 x 16 each) and the C tile (64 x 64)
+  // ---- staging: A and B in k-chunks of 16 (one cp.async group each), then the
+  // C tile; the DMMAs of chunk c start as soon as chunk c has landed, while
+  // the later chunks and C are still in flight
+  constexpr int NCH = SK_K / 16;
 #pragma unroll
-  for (int p = 0; p < 2 * BM * SK_K / SK_NT; ++p) {       // A then B: 64 rows x 16 k each
-    const int e = p * SK_NT + t, r = (e / SK_K) & 63, k = e % SK_K;
-    const bool isb = e >= BM * SK_K;
-    const int rows = isb ? N : M, r0 = isb ? n0 : m0;
-    const bool ok = (r0 + r < rows) && (k < K);
-    const cplx* g = isb ? B + (int64_t)(n0 + r) * tk.ldb + k : A + (int64_t)(m0 + r) * tk.lda + k;
-    cplx* d = isb ? &Bs[r][k] : &As[r][k];
-    cp_async16(d, ok ? g : Abase, ok);
+  for (int ch = 0; ch < NCH; ++ch) {
+#pragma unroll
+    for (int p = 0; p < 2 * BM * 16 / SK_NT; ++p) {       // A then B: 64 rows x 16 k each
+      const int e = p * SK_NT + t, r = (e >> 4) & 63, k = ch * 16 + (e & 15);
+      const bool isb = e >= BM * 16;
+      const int rows = isb ? N : M, r0 = isb ? n0 : m0;
+      const bool ok = (r0 + r < rows) && (k < K);
+      const cplx* g = isb ? B + (int64_t)(n0 + r) * tk.ldb + k : A + (int64_t)(m0 + r) * tk.lda + k;
+      cplx* d = isb ? &Bs[r][k] : &As[r][k];
+      cp_async16(d, ok ? g : Abase, ok);
+    }
+    cp_commit();
   }
   if (mode != kGemmStore) {
 #pragma unroll 8
@@ -287,8 +294,6 @@ zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
     }
   }
   cp_commit();
-  cp_wait<0>();
-  __syncthreads();
 
   const int lane = t & 31, warp = t >> 5;
   const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
@@ -299,40 +304,54 @@ zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
 #pragma unroll
     for (int j = 0; j < 2; ++j) acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
 #pragma unroll
-  for (int kk = 0; kk < SK_K / 4; ++kk) {
-    double are[4], aim[4], anim[4], bre[2], bim[2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const cplx a = As[wm + i * 8 + fr][kk * 4 + fc];
-      are[i] = a.x;
-      aim[i] = a.y;
-      anim[i] = -a.y;
+  for (int ch = 0; ch < NCH; ++ch) {
+    // groups still allowed in flight: the later A/B chunks and C
+    switch (NCH - ch) {
+      case 4: cp_wait<4>(); break;
+      case 3: cp_wait<3>(); break;
+      case 2: cp_wait<2>(); break;
+      default: cp_wait<1>(); break;
     }
+    __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const cplx b = Bs[wn + j * 8 + fr][kk * 4 + fc];
-      bre[j] = b.x;
-      bim[j] = b.y;
+    for (int kq = 0; kq < 4; ++kq) {
+      const int kk = ch * 4 + kq;
+      double are[4], aim[4], anim[4], bre[2], bim[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const cplx a = As[wm + i * 8 + fr][kk * 4 + fc];
+        are[i] = a.x;
+        aim[i] = a.y;
+        anim[i] = -a.y;
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const cplx b = Bs[wn + j * 8 + fr][kk * 4 + fc];
+        bre[j] = b.x;
+        bim[j] = b.y;
+      }
+      // four passes over all sub-tiles: dependent DMMAs on one accumulator are
+      // 16 instructions apart (per-accumulator order unchanged: bitwise same)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
     }
-    // four passes over all sub-tiles: dependent DMMAs on one accumulator are
-    // 16 instructions apart (per-accumulator order unchanged: bitwise same)
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
   }
+  cp_wait<0>();               // the C tile
+  __syncthreads();
   // ---- epilogue in shared memory, then coalesced stores
 #pragma unroll
   for (int i = 0; i < 4; ++i)
