@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libd3m.so")
+LIB_PATH = os.environ.get("D3M_LIB") or os.path.join(_HERE, "libd3m.so")   # D3M_LIB: A/B builds (dev aid)
 
 P = ctypes.c_void_p
 I32 = ctypes.c_int

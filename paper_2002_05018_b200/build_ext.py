@@ -29,14 +29,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     objdir = os.path.join(HERE, "_obj")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".cu")]
+    headers.append(os.path.join(INCLUDE, "d3m.h"))
+    hdr_t = max(os.path.getmtime(h) for h in headers)
+    objs, cmds = [], []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [nvcc, *ARCH, *FLAGS, "-I", CSRC, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+        objs.append(obj)
+        srcp = os.path.join(CSRC, src)
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(srcp)):
+            continue
+        cmds.append([nvcc, *ARCH, *FLAGS, "-I", CSRC, "-I", INCLUDE, "-c", srcp, "-o", obj])
+    # objects compile independently: run the nvcc invocations in parallel
+    procs = []
+    for cmd in cmds:
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
-        objs.append(obj)
+        procs.append((cmd, subprocess.Popen(cmd)))
+    bad = [cmd for cmd, pr in procs if pr.wait() != 0]
+    if bad:
+        raise subprocess.CalledProcessError(1, bad[0])
     tmp = OUT + ".tmp"
     subprocess.check_call([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
     os.replace(tmp, OUT)

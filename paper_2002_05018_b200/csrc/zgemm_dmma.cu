@@ -187,33 +187,46 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
   const bool track = (tk.flags & kGemmTrackMax) != 0 && tmax != nullptr;
   double tm2 = 0.0;
   const int ldc = tk.ldc;
+  // Per fragment row i: issue all 8 C loads (and the mirror loads) before any
+  // store.  C is not __restrict__ (the mirror writes land in the same block),
+  // so a fused load-op-store per element would serialise 32 memory round
+  // trips per thread; batched, the epilogue costs 4.
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i) {
+    const int r = m0 + wm + i * 8 + fr;
+    cplx cv[4][2], cq[4][2];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int r = m0 + wm + i * 8 + fr;
+        const int c = n0 + wn + j * 8 + fc * 2 + h;
+        const bool ok = r < M && c < N && (!sym || c <= r);
+        cv[j][h] = mk(0.0, 0.0);
+        cq[j][h] = mk(0.0, 0.0);
+        if (ok && mode != kGemmStore) cv[j][h] = C[(int64_t)r * ldc + c];
+        if (ok && mirror && c < r) cq[j][h] = C[(int64_t)c * ldc + r];
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
         const int c = n0 + wn + j * 8 + fc * 2 + h;
         if (r >= M || c >= N) continue;
         const cplx u = mk(acc_re[i][j][h], acc_im[i][j][h]);
         if (sym) {
           if (c > r) continue;
-          cplx* p = C + (int64_t)r * ldc + c;
-          const cplx w = c_sub(*p, u);
-          *p = w;
+          const cplx w = c_sub(cv[j][h], u);
+          C[(int64_t)r * ldc + c] = w;
           if (track) tm2 = fmax(tm2, w.x * w.x + w.y * w.y);
-          if (mirror && c < r) {
-            cplx* q = C + (int64_t)c * ldc + r;
-            *q = c_sub(*q, u);
-          }
+          if (mirror && c < r) C[(int64_t)c * ldc + r] = c_sub(cq[j][h], u);
         } else {
           cplx* p = C + (int64_t)r * ldc + c;
-          if (mode == kGemmSub) *p = c_sub(*p, u);
+          if (mode == kGemmSub) *p = c_sub(cv[j][h], u);
           else if (mode == kGemmStore) *p = u;
-          else *p = c_add(*p, u);
+          else *p = c_add(cv[j][h], u);
         }
       }
+  }
   if (track) {   // non-negative doubles order like their bit patterns: integer max is exact
     tm2 = warp_max(tm2);
     if ((threadIdx.x & 31) == 0) atomicMax(tmax + tk.pad_, (unsigned long long)__double_as_longlong(tm2));
