@@ -27,6 +27,7 @@ namespace d3m {
 namespace cg = cooperative_groups;
 
 constexpr int BKC_NT = 384;
+constexpr int BKC_JPT = 2;       // multiplier rows per bulk thread: n <= BKC_JPT * (BKC_NT - 32)
 constexpr double kBkcAlpha = 0.6403882032022076;  // (1 + sqrt(17)) / 8, kernels.py:33
 
 struct BkcSlot {
@@ -396,7 +397,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
       // ---- 3B. row kp refill W[kp, kk+1:kp] <- W[kk+1:kp, kk], W[kp, kp] <-
       //          W[kk, kk] (entry k0 left to the pivot warp); L rows of kk / kp
       const bool lswap = kp != kk && kk % CS == rank;
-      cplx lsv = mk(0.0, 0.0);
+      cplx lsv[BKC_JPT];
       if (kp != kk) {
         if (kp % CS == rank)
           for (int j = kk + 1 + bt; j <= kp; j += NBT)
@@ -406,36 +407,52 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
             L(kk, kk) = cC[kp];                      // W[kk, kk] <- W[kp, kp]
             if (kstep == 2) L(kk, k) = cA[kp];       // W[k+1, k] <- W[kp, k]
           }
-          if (bt < k) lsv = Rm(kp, bt);              // W[kp, :k], stored below
+#pragma unroll
+          for (int h = 0; h < BKC_JPT; ++h)          // W[kp, :k], stored below
+            if (bt + h * NBT < k) lsv[h] = Rm(kp, bt + h * NBT);
         }
       }
-      // ---- 4B. multipliers of every row > k0 (one row per bulk thread: the
-      //          launcher guarantees n <= NBT) and the L column of the own rows,
-      //          stored after the pivot warp's interchange is visible ------------
-      const int j = k0 + bt;
-      const bool jown = j < n && j % CS == rank;
-      cplx lc0 = mk(0.0, 0.0), lc1 = mk(0.0, 0.0);
-      if (j < n) {
-        const cplx x = Xc(j);
-        if (kstep == 1) {
-          if (j > k0) ls[j] = x_div_py(x, piv);                  // lj = W[j, k] / piv
-          if (jown) lc0 = x_div_np(x, piv);                     // W[k+1:, k] /= piv
-        } else {
-          const cplx y = Yc(j);
-          lc0 = x_mul(d21s, x_sub(x_mul(d11, x), y));             // wk
-          lc1 = x_mul(d21s, x_sub(x_mul(d22, y), x));             // wkp
-          ls[j] = lc0;
-          ws[j] = lc1;
+      // ---- 4B. multipliers of every row > k0 (up to BKC_JPT rows per bulk
+      //          thread: the launcher guarantees n <= BKC_JPT * NBT) and the L
+      //          column of the own rows, stored after the pivot warp's
+      //          interchange is visible -------------------------------------------
+      cplx lc0[BKC_JPT], lc1[BKC_JPT];
+#pragma unroll
+      for (int t = 0; t < BKC_JPT; ++t) {
+        const int j = k0 + bt + t * NBT;
+        lc0[t] = lc1[t] = mk(0.0, 0.0);
+        if (j < n) {
+          const cplx x = Xc(j);
+          if (kstep == 1) {
+            if (j > k0) ls[j] = x_div_py(x, piv);                  // lj = W[j, k] / piv
+            if (j % CS == rank) lc0[t] = x_div_np(x, piv);        // W[k+1:, k] /= piv
+          } else {
+            const cplx y = Yc(j);
+            lc0[t] = x_mul(d21s, x_sub(x_mul(d11, x), y));          // wk
+            lc1[t] = x_mul(d21s, x_sub(x_mul(d22, y), x));          // wkp
+            ls[j] = lc0[t];
+            ws[j] = lc1[t];
+          }
         }
       }
-      if (lswap && bt < k) {                   // W[kk, :k] <-> W[kp, :k]
-        Rm(kp, bt) = L(kk, bt);
-        L(kk, bt) = lsv;
+      if (lswap) {                             // W[kk, :k] <-> W[kp, :k]
+#pragma unroll
+        for (int h = 0; h < BKC_JPT; ++h) {
+          const int u = bt + h * NBT;
+          if (u < k) {
+            Rm(kp, u) = L(kk, u);
+            L(kk, u) = lsv[h];
+          }
+        }
       }
       asm volatile("bar.sync 1, %0;\n" ::"n"(BKC_NT) : "memory");     // swapped rows + multipliers
-      if (jown) {
-        L(j, k) = lc0;
-        if (kstep == 2) L(j, k + 1) = lc1;
+#pragma unroll
+      for (int t = 0; t < BKC_JPT; ++t) {
+        const int j = k0 + bt + t * NBT;
+        if (j < n && j % CS == rank) {
+          L(j, k) = lc0[t];
+          if (kstep == 2) L(j, k + 1) = lc1[t];
+        }
       }
       bkc_arrive();
       if (gthread && s >= 2) grow(pend_usq, ks2, k02);
@@ -546,7 +563,7 @@ template <int CS>
 static int bkc_launch(BkArgs* a, int batch, cudaStream_t s) {
   // own rows + ls, ws (2n) + broadcast vectors (9n) + perm / tags (< n)
   const size_t smem = sizeof(cplx) * (size_t)(bkc_entries<CS>(a->n) + 12 * (int64_t)a->n);
-  if (smem > 200 * 1024 || a->n > BKC_NT - 32) return -22;   // one multiplier row per bulk thread
+  if (smem > 200 * 1024 || a->n > BKC_JPT * (BKC_NT - 32)) return -22;
   cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   bk_cluster_kernel<CS><<<batch * CS, BKC_NT, smem, s>>>(*a);
   return (int)cudaGetLastError();

@@ -33,6 +33,16 @@ namespace d3m {
 
 constexpr int BM = 64, BN = 64, BKC = 8, STAGES = 4, PITCH = BKC + 4;
 constexpr int NTHREADS = 128;
+// One ring stage: the A and B k-slices side by side, so a freed stage is one
+// contiguous 24 KB block (the epilogue's C prefetch reuses freed stages).
+struct GemmStage {
+  cplx a[BM][PITCH];
+  cplx b[BN][PITCH];
+};
+constexpr int CP_PITCH = BN + 1;     // odd pitch: conflict-free fragment reads of C
+constexpr int CP_ROWS = 22;          // C rows per freed stage (even: row pairs never straddle)
+static_assert(CP_ROWS * CP_PITCH <= (int)(sizeof(GemmStage) / sizeof(cplx)), "C chunk exceeds a stage");
+static_assert(3 * CP_ROWS >= BM && STAGES == 4, "three freed stages hold the C tile");
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -81,8 +91,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
 zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bbase, cplx* Cbase,
                      const GemmTask* __restrict__ tasks, int ntasks, unsigned long long* tmax) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  cplx(*As)[BM][PITCH] = reinterpret_cast<cplx(*)[BM][PITCH]>(smem_raw);
-  cplx(*Bs)[BN][PITCH] = reinterpret_cast<cplx(*)[BN][PITCH]>(smem_raw + sizeof(cplx) * STAGES * BM * PITCH);
+  GemmStage* st = reinterpret_cast<GemmStage*>(smem_raw);
 
   // ---- locate the task and the tile --------------------------------------
   const int tile = blockIdx.x;
@@ -123,11 +132,18 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < ktiles) {
-      load_tile<TA>(As[s], A, tk.lda, m0, M, s * BKC, K);
-      load_tile<TB>(Bs[s], B, tk.ldb, n0, N, s * BKC, K);
+      load_tile<TA>(st[s].a, A, tk.lda, m0, M, s * BKC, K);
+      load_tile<TB>(st[s].b, B, tk.ldb, n0, N, s * BKC, K);
     }
     cp_commit();
   }
+  // C prefetch (plain C -= / += AB targets): the last STAGES-1 iterations issue
+  // no A/B loads, so each frees one ring slot; chunk c of the C tile (rows
+  // [22c, 22c+22), pitch CP_PITCH) is fetched into the slot freed at
+  // iteration ktiles-3+c and has landed by the epilogue.
+  const int mode = tk.flags & kGemmModeMask;
+  const bool sym = (tk.flags & kGemmSym) != 0;
+  const bool cpre = !sym && mode != kGemmStore && ktiles >= STAGES;
 
   for (int kt = 0; kt < ktiles; ++kt) {
     cp_wait<STAGES - 2>();
@@ -136,8 +152,17 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
       const int nk = kt + STAGES - 1;
       if (nk < ktiles) {
         const int slot = nk % STAGES;
-        load_tile<TA>(As[slot], A, tk.lda, m0, M, nk * BKC, K);
-        load_tile<TB>(Bs[slot], B, tk.ldb, n0, N, nk * BKC, K);
+        load_tile<TA>(st[slot].a, A, tk.lda, m0, M, nk * BKC, K);
+        load_tile<TB>(st[slot].b, B, tk.ldb, n0, N, nk * BKC, K);
+      } else if (cpre) {
+        const int ch = nk - ktiles, r0 = ch * CP_ROWS;
+        const int rows = min(CP_ROWS, BM - r0);
+        cplx* dst = reinterpret_cast<cplx*>(&st[(kt + STAGES - 1) % STAGES]);
+        for (int e = threadIdx.x; e < rows * BN; e += NTHREADS) {
+          const int r = e / BN, c = e - r * BN;
+          const bool ok = m0 + r0 + r < M && n0 + c < N;
+          cp_async16(dst + r * CP_PITCH + c, ok ? C + (int64_t)(m0 + r0 + r) * tk.ldc + n0 + c : C, ok);
+        }
       }
       cp_commit();
     }
@@ -147,14 +172,14 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
       double are[4], aim[4], anim[4], bre[4], bim[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const cplx a = As[slot][wm + i * 8 + fr][kk * 4 + fc];
+        const cplx a = st[slot].a[wm + i * 8 + fr][kk * 4 + fc];
         are[i] = a.x;
         aim[i] = a.y;
         anim[i] = -a.y;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const cplx b = Bs[slot][wn + j * 8 + fr][kk * 4 + fc];
+        const cplx b = st[slot].b[wn + j * 8 + fr][kk * 4 + fc];
         bre[j] = b.x;
         bim[j] = b.y;
       }
@@ -181,8 +206,25 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
   cp_wait<0>();
 
   // ---- epilogue ------------------------------------------------------------
-  const int mode = tk.flags & kGemmModeMask;
-  const bool sym = (tk.flags & kGemmSym) != 0;
+  if (cpre) {
+    __syncthreads();                     // every thread's C chunks have landed
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rl = wm + i * 8 + fr, r = m0 + rl;
+      const int ch = rl / CP_ROWS;
+      const cplx* crow = reinterpret_cast<const cplx*>(&st[(ktiles + ch) % STAGES]) + (rl - ch * CP_ROWS) * CP_PITCH;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cl = wn + j * 8 + fc * 2 + h, c = n0 + cl;
+          if (r >= M || c >= N) continue;
+          const cplx u = mk(acc_re[i][j][h], acc_im[i][j][h]);
+          C[(int64_t)r * tk.ldc + c] = mode == kGemmSub ? c_sub(crow[cl], u) : c_add(crow[cl], u);
+        }
+    }
+    return;
+  }
   const bool mirror = sym && !(tk.flags & kGemmLowerOnly);
   const bool track = (tk.flags & kGemmTrackMax) != 0 && tmax != nullptr;
   double tm2 = 0.0;

@@ -24,7 +24,7 @@ def test_gemm_vs_numpy(cuda):
     from paper_2002_05018_b200 import _lib
     from paper_2002_05018_b200.device import stream_ptr, to_device
     rng = np.random.default_rng(3)
-    for (M, N, K) in [(64, 64, 64), (1, 1, 1), (70, 33, 130), (256, 256, 256), (129, 65, 7)]:
+    for (M, N, K) in [(64, 64, 64), (1, 1, 1), (70, 33, 130), (256, 256, 256), (129, 65, 7), (200, 190, 40), (64, 64, 32)]:
         for ta in (0, 1):
             for tb in (0, 1):
                 for mode in (_lib.GEMM_SUB, _lib.GEMM_STORE, _lib.GEMM_ADD):
