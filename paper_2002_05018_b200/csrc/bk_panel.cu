@@ -155,12 +155,16 @@ __global__ void bk_perm_init_kernel(BkArgs a, int batch) {
 // Up-to-date column of the panel step over the rows [r_lo, r_hi) this CTA owns:
 //   out[i] = base(i) - sum_{c < kw} G(i, k0 + c) * Wp[src][c]
 // with NB/4 lanes per row (4 of the <= NB panel columns each, independent loads)
-// and two rows per lane group in flight; base(i) is G(i, col) for i >= col
-// (stale column) or G(col, i) for i < col (its row part), col = the target
-// column.  The summation order per row is fixed (4 partial sums, butterfly).
+// and PG_ROWS rows per lane group in flight (all loads of an iteration are
+// issued before any use: one L2/HBM round trip per iteration); base(i) is
+// G(i, col) for i >= col (stale column) or G(col, i) for i < col (its row
+// part), col = the target column.  The summation order per row is fixed (4
+// partial sums, butterfly).
+constexpr int PG_ROWS = 4;
 template <int NB, int NT>
-__device__ __forceinline__ void panel_gemv(const cplx* W, int lda, int r_lo, int r_hi, int k0, int kw, int col,
-                                           const cplx* Wp, int src, cplx* out_col /* Wp + kwcol, stride NB+1 */) {
+__device__ __forceinline__ void panel_gemv(const cplx* __restrict__ W, int lda, int r_lo, int r_hi, int k0, int kw,
+                                           int col, const cplx* __restrict__ Wp, int src,
+                                           cplx* __restrict__ out_col /* Wp + kwcol, stride NB+1 */) {
   constexpr int LDW = NB + 1, LN = NB / 4;       // LN lanes per row, 4 panel columns each
   const int sub = threadIdx.x % LN;
   constexpr int rstride = NT / LN;
@@ -171,36 +175,32 @@ __device__ __forceinline__ void panel_gemv(const cplx* W, int lda, int r_lo, int
     xs[q] = c < kw ? Wp[(int64_t)src * LDW + c] : mk(0.0, 0.0);
   }
   // warp-uniform trip count: the shuffles below need all 32 lanes
-  for (int base = r_lo; base < r_hi; base += 2 * rstride) {
-    const int ia = base + (int)threadIdx.x / LN, ib = ia + rstride;
-    const bool va = ia < r_hi, vb = ib < r_hi;
-    cplx la[4], lb[4], ba = mk(0.0, 0.0), bb = mk(0.0, 0.0);
+  for (int base = r_lo; base < r_hi; base += PG_ROWS * rstride) {
+    cplx l[PG_ROWS][4], bv[PG_ROWS];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int c = sub + LN * q;
-      la[q] = (c < kw && va) ? W[(int64_t)ia * lda + k0 + c] : mk(0.0, 0.0);
-      lb[q] = (c < kw && vb) ? W[(int64_t)ib * lda + k0 + c] : mk(0.0, 0.0);
-    }
-    if (sub == 0) {
-      if (va) ba = ia >= col ? W[(int64_t)ia * lda + col] : W[(int64_t)col * lda + ia];
-      if (vb) bb = ib >= col ? W[(int64_t)ib * lda + col] : W[(int64_t)col * lda + ib];
-    }
-    cplx sa = mk(0.0, 0.0), sb = mk(0.0, 0.0);
+    for (int g = 0; g < PG_ROWS; ++g) {
+      const int ia = base + (int)threadIdx.x / LN + g * rstride;
+      const bool va = ia < r_hi;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      c_fma(sa, la[q], xs[q]);
-      c_fma(sb, lb[q], xs[q]);
+      for (int q = 0; q < 4; ++q) {
+        const int c = sub + LN * q;
+        l[g][q] = (c < kw && va) ? W[(int64_t)ia * lda + k0 + c] : mk(0.0, 0.0);
+      }
+      bv[g] = mk(0.0, 0.0);
+      if (sub == 0 && va) bv[g] = ia >= col ? W[(int64_t)ia * lda + col] : W[(int64_t)col * lda + ia];
     }
 #pragma unroll
-    for (int o = 1; o < LN; o <<= 1) {
-      sa.x += __shfl_xor_sync(0xffffffffu, sa.x, o);
-      sa.y += __shfl_xor_sync(0xffffffffu, sa.y, o);
-      sb.x += __shfl_xor_sync(0xffffffffu, sb.x, o);
-      sb.y += __shfl_xor_sync(0xffffffffu, sb.y, o);
-    }
-    if (sub == 0) {
-      if (va) out_col[(int64_t)ia * LDW] = c_sub(ba, sa);
-      if (vb) out_col[(int64_t)ib * LDW] = c_sub(bb, sb);
+    for (int g = 0; g < PG_ROWS; ++g) {
+      const int ia = base + (int)threadIdx.x / LN + g * rstride;
+      cplx sa = mk(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c_fma(sa, l[g][q], xs[q]);
+#pragma unroll
+      for (int o = 1; o < LN; o <<= 1) {
+        sa.x += __shfl_xor_sync(0xffffffffu, sa.x, o);
+        sa.y += __shfl_xor_sync(0xffffffffu, sa.y, o);
+      }
+      if (sub == 0 && ia < r_hi) out_col[(int64_t)ia * LDW] = c_sub(bv[g], sa);
     }
   }
 }
@@ -542,7 +542,13 @@ static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* task
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
     if (maxtiles > 0) {
-      const int rc = d3m_gemm_smallk_launch_k(NB, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream);
+      // rank-<=NB trailing update: the pipelined grouped kernel (C prefetched
+      // into freed ring stages) is ~4% faster than the small-K kernel on
+      // config 3 at NB = 64; D3M_PANEL_GEMM=s selects the small-K kernel
+      static const char* pg = getenv("D3M_PANEL_GEMM");
+      const int rc = (NB == 64 && !(pg && pg[0] == 's'))
+                         ? d3m_gemm_launch_tm(0, 0, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream)
+                         : d3m_gemm_smallk_launch_k(NB, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream);
       if (rc) return rc;
     }
   }

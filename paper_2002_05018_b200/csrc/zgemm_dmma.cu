@@ -137,13 +137,13 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
     }
     cp_commit();
   }
-  // C prefetch (plain C -= / += AB targets): the last STAGES-1 iterations issue
+  // C prefetch (C -= / += AB targets without mirrored writes): the last STAGES-1 iterations issue
   // no A/B loads, so each frees one ring slot; chunk c of the C tile (rows
   // [22c, 22c+22), pitch CP_PITCH) is fetched into the slot freed at
   // iteration ktiles-3+c and has landed by the epilogue.
   const int mode = tk.flags & kGemmModeMask;
   const bool sym = (tk.flags & kGemmSym) != 0;
-  const bool cpre = !sym && mode != kGemmStore && ktiles >= STAGES;
+  const bool cpre = (!sym || (tk.flags & kGemmLowerOnly)) && mode != kGemmStore && ktiles >= STAGES;
 
   for (int kt = 0; kt < ktiles; ++kt) {
     cp_wait<STAGES - 2>();
@@ -206,6 +206,10 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
   cp_wait<0>();
 
   // ---- epilogue ------------------------------------------------------------
+  const bool mirror = sym && !(tk.flags & kGemmLowerOnly);
+  const bool track = (tk.flags & kGemmTrackMax) != 0 && tmax != nullptr;
+  double tm2 = 0.0;
+  const int ldc = tk.ldc;
   if (cpre) {
     __syncthreads();                     // every thread's C chunks have landed
 #pragma unroll
@@ -218,56 +222,54 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int cl = wn + j * 8 + fc * 2 + h, c = n0 + cl;
-          if (r >= M || c >= N) continue;
+          if (r >= M || c >= N || (sym && c > r)) continue;      // SYM here is lower-only
           const cplx u = mk(acc_re[i][j][h], acc_im[i][j][h]);
-          C[(int64_t)r * tk.ldc + c] = mode == kGemmSub ? c_sub(crow[cl], u) : c_add(crow[cl], u);
-        }
-    }
-    return;
-  }
-  const bool mirror = sym && !(tk.flags & kGemmLowerOnly);
-  const bool track = (tk.flags & kGemmTrackMax) != 0 && tmax != nullptr;
-  double tm2 = 0.0;
-  const int ldc = tk.ldc;
-  // Per fragment row i: issue all 8 C loads (and the mirror loads) before any
-  // store.  C is not __restrict__ (the mirror writes land in the same block),
-  // so a fused load-op-store per element would serialise 32 memory round
-  // trips per thread; batched, the epilogue costs 4.
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = m0 + wm + i * 8 + fr;
-    cplx cv[4][2], cq[4][2];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = n0 + wn + j * 8 + fc * 2 + h;
-        const bool ok = r < M && c < N && (!sym || c <= r);
-        cv[j][h] = mk(0.0, 0.0);
-        cq[j][h] = mk(0.0, 0.0);
-        if (ok && mode != kGemmStore) cv[j][h] = C[(int64_t)r * ldc + c];
-        if (ok && mirror && c < r) cq[j][h] = C[(int64_t)c * ldc + r];
-      }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = n0 + wn + j * 8 + fc * 2 + h;
-        if (r >= M || c >= N) continue;
-        const cplx u = mk(acc_re[i][j][h], acc_im[i][j][h]);
-        if (sym) {
-          if (c > r) continue;
-          const cplx w = c_sub(cv[j][h], u);
+          const cplx w = mode == kGemmSub ? c_sub(crow[cl], u) : c_add(crow[cl], u);
           C[(int64_t)r * ldc + c] = w;
           if (track) tm2 = fmax(tm2, w.x * w.x + w.y * w.y);
-          if (mirror && c < r) C[(int64_t)c * ldc + r] = c_sub(cq[j][h], u);
-        } else {
-          cplx* p = C + (int64_t)r * ldc + c;
-          if (mode == kGemmSub) *p = c_sub(cv[j][h], u);
-          else if (mode == kGemmStore) *p = u;
-          else *p = c_add(cv[j][h], u);
         }
-      }
+    }
+  } else {
+    // Per fragment row i: issue all 8 C loads (and the mirror loads) before any
+    // store.  C is not __restrict__ (the mirror writes land in the same block),
+    // so a fused load-op-store per element would serialise 32 memory round
+    // trips per thread; batched, the epilogue costs 4.
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = m0 + wm + i * 8 + fr;
+      cplx cv[4][2], cq[4][2];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = n0 + wn + j * 8 + fc * 2 + h;
+          const bool ok = r < M && c < N && (!sym || c <= r);
+          cv[j][h] = mk(0.0, 0.0);
+          cq[j][h] = mk(0.0, 0.0);
+          if (ok && mode != kGemmStore) cv[j][h] = C[(int64_t)r * ldc + c];
+          if (ok && mirror && c < r) cq[j][h] = C[(int64_t)c * ldc + r];
+        }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = n0 + wn + j * 8 + fc * 2 + h;
+          if (r >= M || c >= N) continue;
+          const cplx u = mk(acc_re[i][j][h], acc_im[i][j][h]);
+          if (sym) {
+            if (c > r) continue;
+            const cplx w = c_sub(cv[j][h], u);
+            C[(int64_t)r * ldc + c] = w;
+            if (track) tm2 = fmax(tm2, w.x * w.x + w.y * w.y);
+            if (mirror && c < r) C[(int64_t)c * ldc + r] = c_sub(cq[j][h], u);
+          } else {
+            cplx* p = C + (int64_t)r * ldc + c;
+            if (mode == kGemmSub) *p = c_sub(cv[j][h], u);
+            else if (mode == kGemmStore) *p = u;
+            else *p = c_add(cv[j][h], u);
+          }
+        }
+    }
   }
   if (track) {   // non-negative doubles order like their bit patterns: integer max is exact
     tm2 = warp_max(tm2);
