@@ -13,11 +13,14 @@
 // (itself operation-for-operation the numba kernel), so pivots, tags, growth
 // AND values stay bit-identical to the CPU reference.
 //
-// Per step the work splits into a pivot warp (the critical chain: merge,
-// decision, interchange, update and publication of the next pivot column) and
-// bulk warps (multipliers, L column, trailing update), with a split cluster
-// barrier: the pivot warp ARRIVES once column k0 is published and the next
-// step WAITS, so the bulk update overlaps the exchange (see the kernel).
+// Communication: each step's pivot column (and, for the rowmax test, columns
+// k+1 and imax) is pushed to every CTA with st.async, which completes on the
+// RECEIVER's mbarrier (expected bytes armed by the receiver), together with a
+// 32-byte slot carrying each CTA's exact argmax.  There is no cluster barrier
+// in the step loop.  The interchange of the L rows left of column k
+// (kernels.py:96-98) never crosses CTAs either: every CTA records the step's
+// interchange and the L entries are written to their final rows at the end
+// (each column's entries move by the interchanges of the later steps).
 #include <cooperative_groups.h>
 #include <cstdlib>
 #include "d3m_common.cuh"
@@ -30,18 +33,12 @@ constexpr int BKC_NT = 384;
 constexpr int BKC_JPT = 2;       // multiplier rows per bulk thread: n <= BKC_JPT * (BKC_NT - 32)
 constexpr double kBkcAlpha = 0.6403882032022076;  // (1 + sqrt(17)) / 8, kernels.py:33
 
+// prologue exchange (scale, asym, trailing max), through the cluster barrier
 struct BkcSlot {
-  double v;      // argmax value (exact modulus) or -1
-  double own;    // a value only the owner of a row can supply, else -1
-  double aux;    // max-reduced payload (rowmax, step max, prologue maxima)
-  double aux2;
-  int i;         // argmax index
-  int pad;
+  double v, own, aux, aux2;
+  int i, pad;
 };
 
-// Each CTA posts its slot into every CTA's inbox (DSMEM stores) before the
-// cluster barrier; after it every CTA merges its own inbox from local shared
-// memory in rank order, so all CTAs hold bitwise-identical decisions.
 template <int CS>
 __device__ __forceinline__ void bkc_post(cg::cluster_group& cl, BkcSlot* box, int rank, const BkcSlot& v) {
 #pragma unroll
@@ -69,10 +66,87 @@ __device__ __forceinline__ BkcSlot bkc_merge(const BkcSlot* box, BkcSlot* out) {
   return *out;
 }
 
-// split cluster barrier (arrive publishes this thread's prior DSMEM stores;
-// wait acquires every peer's)
-__device__ __forceinline__ void bkc_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ void bkc_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+// ---- step exchange slot: 32 bytes, two st.async.v2.f64 ---------------------
+struct XSlot {
+  double v;      // exact argmax value or -1
+  double own;    // a modulus only the owner of a row can supply, else -1
+  double aux;    // max-reduced payload (rowmax, update maximum)
+  double i;      // argmax index (int bits)
+};
+constexpr unsigned kSlotBytes = sizeof(XSlot);
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// 16-byte store into a peer's shared memory, completing on the peer's mbarrier
+__device__ __forceinline__ void st_async(uint32_t raddr, double x, double y, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n"
+               ::"r"(raddr), "d"(x), "d"(y), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t* b, unsigned tx) {       // the single arrival + tx
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n"
+               ::"r"(saddr(b)), "r"(tx) : "memory");
+}
+// bounded wait: a lost transfer traps (kernel error) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  for (unsigned it = 0;; ++it) {
+    unsigned ok;
+    asm volatile("{\n .reg .pred p;\n"
+                 " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(saddr(b)), "r"(parity) : "memory");
+    if (ok) return;
+    if (it > (1u << 26)) __trap();
+  }
+}
+
+// one slot to CTA `lane` (lanes < CS of the calling warp; all lanes hold x)
+template <int CS>
+__device__ __forceinline__ void xpost(const XSlot* box, int rank, const XSlot& x, uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
+  if (lane < CS) {
+    const uint32_t dst = mapa(saddr(box + rank), lane), rb = mapa(saddr(bar), lane);
+    st_async(dst, x.v, x.own, rb);
+    st_async(dst + 16, x.aux, x.i, rb);
+  }
+}
+
+// merge of the CS slots of a local inbox (warp 0), broadcast through smem
+template <int CS>
+__device__ __forceinline__ XSlot xmerge(const XSlot* box, XSlot* out) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double v = -1.0, own = -1.0, aux = -1.0;
+    int vi = 0x7fffffff;
+    if (lane < CS) {
+      const XSlot r = box[lane];
+      v = r.v;
+      own = r.own;
+      aux = r.aux;
+      vi = (int)__double_as_longlong(r.i);
+    }
+#pragma unroll
+    for (int o = CS / 2; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, vi, o);
+      own = fmax(own, __shfl_xor_sync(0xffffffffu, own, o));
+      aux = fmax(aux, __shfl_xor_sync(0xffffffffu, aux, o));
+      argmax_merge(v, vi, v2, i2);
+    }
+    if (lane == 0) *out = XSlot{v, own, aux, __longlong_as_double((long long)vi)};
+  }
+  __syncthreads();
+  return *out;
+}
+__device__ __forceinline__ int xidx(const XSlot& x) { return (int)__double_as_longlong(x.i); }
+__device__ __forceinline__ XSlot xslot(double v, double own, double aux, int i) {
+  return XSlot{v, own, aux, __longlong_as_double((long long)i)};
+}
 
 __device__ __forceinline__ double bkc_block_max(double v, double* slots) {
   v = warp_max(v);
@@ -83,17 +157,6 @@ __device__ __forceinline__ double bkc_block_max(double v, double* slots) {
   for (int w = 1; w < BKC_NT / 32; ++w) r = fmax(r, slots[w]);
   __syncthreads();
   return r;
-}
-
-__device__ __forceinline__ void bkc_block_argmax(double& v, int& idx, double* vs, int* is) {
-  warp_argmax(v, idx);
-  if ((threadIdx.x & 31) == 0) { vs[threadIdx.x >> 5] = v; is[threadIdx.x >> 5] = idx; }
-  __syncthreads();
-  v = vs[0];
-  idx = is[0];
-#pragma unroll
-  for (int w = 1; w < BKC_NT / 32; ++w) argmax_merge(v, idx, vs[w], is[w]);
-  __syncthreads();
 }
 
 // packed offset of row i (i % CS == r) inside its CTA: rows q = i / CS of
@@ -122,24 +185,28 @@ __host__ __device__ inline int64_t bkc_entries(int n) {    // per-CTA capacity (
 // Roles inside each CTA of the cluster (per step k, pivot column k0 = k + kstep):
 //   pivot warp (warp 0): merge of the argmax slots -> pivot decision ->
 //     interchange of the own rows' columns kk / kp -> update of column k0 of
-//     the own rows -> publish it (DSMEM) with its exact argmax, the modulus of
-//     the new diagonal entry and the update maximum of step s-1 -> ARRIVE on
-//     the cluster barrier.  This chain is the step's critical path.
-//   bulk warps (1..NW-1): row kp refill and the L rows of kk / kp, multipliers
-//     of every row (each CTA computes all of them) and the L column of the own
-//     rows -> ARRIVE -> rank-1 / rank-2 update of the columns > k0 of the own
-//     rows, overlapping the barrier and the next step's merge.
-// The next step WAITS on the barrier, so one barrier per step (two with the
-// rowmax exchange).  Broadcast vectors and inboxes are triple-buffered by step:
-// the buffer step s+1 publishes into was last read in step s-2, whose bulk
-// every CTA finished before arriving in step s-1.
+//     the own rows -> push it with its exact argmax, the modulus of the new
+//     diagonal entry and the update maximum of step s-1.  This chain is the
+//     step's critical path.
+//   bulk warps (1..NW-1): row kp refill, multipliers of every row (each CTA
+//     computes all of them) and the L column of the own rows, then the rank-1
+//     / rank-2 update of the columns > k0 of the own rows, overlapping the
+//     next step's exchange.
+// Broadcast vectors and inboxes are triple-buffered by step: the buffer a
+// peer fills during its step s was last read here in step s-2, and the peer
+// only reaches step s after this CTA pushed its step s-1 column, which
+// follows the end of its step s-2 bulk update.
 template <int CS>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_kernel(BkArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char bkc_smem[];
   __shared__ double rv[BKC_NT / 32];
   __shared__ double rst[2][BKC_NT / 32];      // per-warp max |a_ij|^2 of a step's update, by step parity
-  __shared__ BkcSlot inbox[3][CS], inboxR[CS], merged;
+  __shared__ __align__(16) XSlot inbox[3][CS];
+  __shared__ __align__(16) XSlot inboxR[CS];
+  __shared__ XSlot xmerged;
+  __shared__ BkcSlot pbox[CS], pmerged;
+  __shared__ __align__(8) uint64_t mbar[3], mbarR;
   const int rank = (int)cl.block_rank();
   const int b = blockIdx.x / CS;
   const int n = a.n, lda = a.lda, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -152,18 +219,21 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
   cplx* ls = Rl + cap;                                 // l_j / wk_j of every row (computed locally)
   cplx* ws = ls + n;                                   // wkp_j (2x2)
   cplx* vec = ws + n;                                  // broadcast vectors [3][3][n]
-  int64_t* perm_s = reinterpret_cast<int64_t*>(vec + 9 * (int64_t)n);
-  int8_t* tags_s = reinterpret_cast<int8_t*>(perm_s + n);
+  short* perm_s = reinterpret_cast<short*>(vec + 9 * (int64_t)n);
+  short* qmap = perm_s + n;                            // write-back row map
+  short* stk = qmap + n;                               // per step: k, kstep, kp (-1: no interchange)
+  int8_t* tags_s = reinterpret_cast<int8_t*>(stk + 3 * n);
   cplx* W = a.W + (int64_t)b * a.stride_w;
   const bool lead = rank == 0 && tid == 0;
   const int nown = (n - rank + CS - 1) / CS;          // own rows: rank, rank + CS, ...
   auto L = [&](int i, int j) -> cplx& { return Rl[bkc_off<CS>(i) + j]; };   // own row i
-  auto Rm = [&](int i, int j) -> cplx& {                                     // any row (DSMEM)
-    cplx* base = cl.map_shared_rank(Rl, i % CS);
-    return base[bkc_off<CS>(i) + j];
-  };
   auto first_q = [&](int i0) { const int q = (i0 - rank + CS - 1) / CS; return q > 0 ? q : 0; };  // own rows >= i0
 
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(&mbar[i]);
+    mbar_init(&mbarR);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   // ---- prologue: numpy scale / symmetry check / trailing max, own rows -> smem
   double scale = 0.0, asym = 0.0, tm2 = 0.0;
   for (int q = warp; q < nown; q += NW) {
@@ -178,14 +248,14 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
       if (a.check_sym == 1 && j < i) asym = fmax(asym, np_abs(x_sub(z, W[(int64_t)j * lda + i])));
     }
   }
-  for (int i = tid; i < n; i += BKC_NT) { perm_s[i] = i; tags_s[i] = 0; }
+  for (int i = tid; i < n; i += BKC_NT) { perm_s[i] = (short)i; tags_s[i] = 0; }
   scale = bkc_block_max(scale, rv);
   asym = bkc_block_max(asym, rv);
   tm2 = bkc_block_max(tm2, rv);
-  if (tid == 0) bkc_post<CS>(cl, inboxR, rank, BkcSlot{-1.0, scale, asym, tm2, 0x7fffffff, 0});
-  cl.sync();
+  if (tid == 0) bkc_post<CS>(cl, pbox, rank, BkcSlot{-1.0, scale, asym, tm2, 0x7fffffff, 0});
+  cl.sync();                                          // also publishes the mbarrier inits
   {
-    const BkcSlot m = bkc_merge<CS>(inboxR, &merged);
+    const BkcSlot m = bkc_merge<CS>(pbox, &pmerged);
     scale = m.own;
     asym = m.aux;
     tm2 = m.aux2;
@@ -218,24 +288,24 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     }
   };
 
-  // ---- column 0: published by the pivot warps ------------------------------
+  // ---- column 0, pushed by the pivot warps -----------------------------------
   if (pw) {
     double v = -1.0, own = -1.0;
     int vi = 0x7fffffff;
     for (int q = lane; q < nown; q += 32) {
       const int i = rank + q * CS;
       const cplx z = L(i, 0);
+      const uint32_t src = saddr(vec + i), sb = saddr(&mbar[0]);
 #pragma unroll
-      for (int c = 0; c < CS; ++c) cl.map_shared_rank(vec, c)[i] = z;
+      for (int c = 0; c < CS; ++c) st_async(mapa(src, c), z.x, z.y, mapa(sb, c));
       const double az = x_abs(z);
       if (i > 0) argmax_merge(v, vi, az, i);
       else own = az;
     }
     warp_argmax(v, vi);
     own = warp_max(own);
-    if (lane == 0) bkc_post<CS>(cl, inbox[0], rank, BkcSlot{v, own, -1.0, -1.0, vi, 0});
+    xpost<CS>(inbox[0], rank, xslot(v, own, -1.0, vi), &mbar[0]);
   }
-  bkc_arrive();
 #ifdef D3M_BK_PROFILE
   double pacc[16];
 #pragma unroll
@@ -243,24 +313,26 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
   long long prof_t = clock64();
 #endif
   int k = 0, s = 0;
+  unsigned rphase = 0;
   double pend_usq = 0.0;
   while (k < n) {
     const int bs = s % 3;
     cplx* cA = vec + (int64_t)(bs * 3 + 0) * n;
     cplx* cB = vec + (int64_t)(bs * 3 + 1) * n;
     cplx* cC = vec + (int64_t)(bs * 3 + 2) * n;
-    // ---- 1. wait for column k and the argmax slots; merge ------------------
-    bkc_wait();
+    // ---- 1. column k and the argmax slots have landed; merge ---------------
+    if (tid == 0) mbar_arm(&mbar[bs], (unsigned)(n - k) * 16u + CS * kSlotBytes);
+    mbar_wait(&mbar[bs], (unsigned)(s / 3) & 1u);
     BKC_MARK(0, 0);
     BKC_MARK(32, 8);
-    const BkcSlot m1 = bkc_merge<CS>(inbox[bs], &merged);   // its __syncthreads also ends the local bulk
+    const XSlot m1 = xmerge<CS>(inbox[bs], &xmerged);   // its __syncthreads also ends the local bulk
     BKC_MARK(0, 1);
     BKC_MARK(32, 9);
     pend_usq = m1.aux;                                       // step s-2's update maximum
     const double absakk = m1.own;                            // |W[k, k]|, from its owner
     double colmax = 0.0;
     int imax = k;
-    if (k + 1 < n) { colmax = m1.v; imax = m1.i; }
+    if (k + 1 < n) { colmax = m1.v; imax = xidx(m1); }
     if (fmax(absakk, colmax) <= tol_abs) { info = k; break; }
 
     int kstep = 1, kp;
@@ -269,12 +341,15 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     } else {
       // ---- 2. push column k+1 and the symmetric column imax; rowmax over
       //         W[imax, k:imax] and W[imax+1:, imax]; |W[imax, imax]| ----------
+      if (tid == 0) mbar_arm(&mbarR, (unsigned)(2 * (n - k) - 1) * 16u + CS * kSlotBytes);
+      const uint32_t rb = saddr(&mbarR);
       double rm = 0.0, aim = -1.0;
       if (imax % CS == rank) {
         for (int t = k + tid; t <= imax; t += BKC_NT) {
           const cplx z = L(imax, t);
+          const uint32_t src = saddr(cC + t);
 #pragma unroll
-          for (int c = 0; c < CS; ++c) cl.map_shared_rank(cC, c)[t] = z;
+          for (int c = 0; c < CS; ++c) st_async(mapa(src, c), z.x, z.y, mapa(rb, c));
           if (t < imax) rm = fmax(rm, x_abs(z));
           else aim = x_abs(z);
         }
@@ -282,20 +357,23 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
       for (int q = first_q(k + 1) + tid; q < nown; q += BKC_NT) {
         const int i = rank + q * CS;
         const cplx y = L(i, k + 1);
+        const uint32_t srcb = saddr(cB + i);
 #pragma unroll
-        for (int c = 0; c < CS; ++c) cl.map_shared_rank(cB, c)[i] = y;
+        for (int c = 0; c < CS; ++c) st_async(mapa(srcb, c), y.x, y.y, mapa(rb, c));
         if (i > imax) {
           const cplx z = L(i, imax);
+          const uint32_t srcc = saddr(cC + i);
 #pragma unroll
-          for (int c = 0; c < CS; ++c) cl.map_shared_rank(cC, c)[i] = z;
+          for (int c = 0; c < CS; ++c) st_async(mapa(srcc, c), z.x, z.y, mapa(rb, c));
           rm = fmax(rm, x_abs(z));
         }
       }
       rm = bkc_block_max(rm, rv);
       aim = bkc_block_max(aim, rv);
-      if (tid == 0) bkc_post<CS>(cl, inboxR, rank, BkcSlot{-1.0, aim, rm, -1.0, 0x7fffffff, 0});
-      cl.sync();
-      const BkcSlot m2 = bkc_merge<CS>(inboxR, &merged);
+      if (pw) xpost<CS>(inboxR, rank, xslot(-1.0, aim, rm, 0x7fffffff), &mbarR);
+      mbar_wait(&mbarR, rphase & 1u);
+      ++rphase;
+      const XSlot m2 = xmerge<CS>(inboxR, &xmerged);
       const double rowmax = m2.aux, absimax = m2.own;
       if (__dmul_rn(absakk, rowmax) >= __dmul_rn(__dmul_rn(kBkcAlpha, colmax), colmax)) {
         kp = k;
@@ -337,16 +415,21 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
           L(i, kk) = L(i, kp);
           L(i, kp) = t0;
         }
-        if (lead) { const int64_t t0 = perm_s[kk]; perm_s[kk] = perm_s[kp]; perm_s[kp] = t0; }
+        if (lead) { const short t0 = perm_s[kk]; perm_s[kk] = perm_s[kp]; perm_s[kp] = t0; }
       }
-      if (lead) {
-        if (kstep == 1) tags_s[k] = 1;
-        else { tags_s[k] = 2; tags_s[k + 1] = 0; }
+      if (lane == 0) {     // every CTA records the step for the L write-back
+        stk[3 * s] = (short)k;
+        stk[3 * s + 1] = (short)kstep;
+        stk[3 * s + 2] = (short)(kp != kk ? kp : -1);
+        if (rank == 0) {
+          if (kstep == 1) tags_s[k] = 1;
+          else { tags_s[k] = 2; tags_s[k + 1] = 0; }
+        }
       }
       __syncwarp();
       asm volatile("bar.arrive 1, %0;\n" ::"n"(BKC_NT) : "memory");   // the bulk may read the swapped rows
       BKC_MARK(0, 2);
-      // ---- 4P. update of column k0 of the own rows, publish ----------------
+      // ---- 4P. update of column k0 of the own rows, push ------------------
       double up = -1.0;
       if (s >= 1) up = warp_max(lane < NW ? rst[(s - 1) & 1][lane] : 0.0);
       double v = -1.0, own = -1.0;
@@ -363,6 +446,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
         }
         BKC_MARK(0, 4);
         cplx* cAn = vec + (int64_t)(nb * 3) * n;
+        const uint32_t nbar = saddr(&mbar[nb]);
         for (int q = qk0 + lane; q < nown; q += 32) {
           const int i = rank + q * CS;
           cplx* row = Rl + bkc_off<CS>(i);
@@ -373,8 +457,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
           const cplx w = kstep == 1 ? x_sub(wo, x_mul(xi, l0))
                                     : x_sub(wo, x_add(x_mul(xi, l0), x_mul(Yc(i), p0)));
           row[k0] = w;
+          const uint32_t src = saddr(cAn + i);
 #pragma unroll
-          for (int c = 0; c < CS; ++c) cl.map_shared_rank(cAn, c)[i] = w;
+          for (int c = 0; c < CS; ++c) st_async(mapa(src, c), w.x, w.y, mapa(nbar, c));
           step_sq = fmax(step_sq, x_abs2(w));
           const double aw = x_abs(w);
           if (i > k0) argmax_merge(v, vi, aw, i);
@@ -385,31 +470,20 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
         own = warp_max(own);
       }
       step_sq = warp_max(step_sq);
-      if (lane == 0) {
-        rst[s & 1][0] = step_sq;
-        bkc_post<CS>(cl, inbox[nb], rank, BkcSlot{v, own, up, -1.0, vi, 0});
-      }
+      if (lane == 0) rst[s & 1][0] = step_sq;
+      xpost<CS>(inbox[nb], rank, xslot(v, own, up, vi), &mbar[nb]);
       BKC_MARK(0, 6);
-      bkc_arrive();
-      BKC_MARK(0, 3);
       if (kstep == 2) ++n2x2;
     } else {
       // ---- 3B. row kp refill W[kp, kk+1:kp] <- W[kk+1:kp, kk], W[kp, kp] <-
-      //          W[kk, kk] (entry k0 left to the pivot warp); L rows of kk / kp
-      const bool lswap = kp != kk && kk % CS == rank;
-      cplx lsv[BKC_JPT];
+      //          W[kk, kk] (entry k0 left to the pivot warp); D of row kk
       if (kp != kk) {
         if (kp % CS == rank)
           for (int j = kk + 1 + bt; j <= kp; j += NBT)
             if (j != k0) L(kp, j) = j < kp ? cK[j] : cK[kk];
-        if (lswap) {
-          if (bt == 0) {
-            L(kk, kk) = cC[kp];                      // W[kk, kk] <- W[kp, kp]
-            if (kstep == 2) L(kk, k) = cA[kp];       // W[k+1, k] <- W[kp, k]
-          }
-#pragma unroll
-          for (int h = 0; h < BKC_JPT; ++h)          // W[kp, :k], stored below
-            if (bt + h * NBT < k) lsv[h] = Rm(kp, bt + h * NBT);
+        if (kk % CS == rank && bt == 0) {
+          L(kk, kk) = cC[kp];                      // W[kk, kk] <- W[kp, kp]
+          if (kstep == 2) L(kk, k) = cA[kp];       // W[k+1, k] <- W[kp, k]
         }
       }
       // ---- 4B. multipliers of every row > k0 (up to BKC_JPT rows per bulk
@@ -435,16 +509,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
           }
         }
       }
-      if (lswap) {                             // W[kk, :k] <-> W[kp, :k]
-#pragma unroll
-        for (int h = 0; h < BKC_JPT; ++h) {
-          const int u = bt + h * NBT;
-          if (u < k) {
-            Rm(kp, u) = L(kk, u);
-            L(kk, u) = lsv[h];
-          }
-        }
-      }
       asm volatile("bar.sync 1, %0;\n" ::"n"(BKC_NT) : "memory");     // swapped rows + multipliers
 #pragma unroll
       for (int t = 0; t < BKC_JPT; ++t) {
@@ -454,7 +518,6 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
           if (kstep == 2) L(j, k + 1) = lc1[t];
         }
       }
-      bkc_arrive();
       if (gthread && s >= 2) grow(pend_usq, ks2, k02);
       BKC_MARK(32, 10);
       // ---- 5B. rank-1 / rank-2 update of the columns > k0 of the own rows
@@ -513,35 +576,64 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
   }
   // ---- growth of the steps whose update maxima are still in flight ---------
   if (info >= 0) {
-    // stopped at the top of step s: step s-1's maximum is in rst, not posted
+    // stopped at the top of step s: step s-1's maximum is in rst, not pushed
     if (s >= 1) {
+      if (tid == 0) mbar_arm(&mbarR, CS * kSlotBytes);
       if (pw) {
         const double up = warp_max(lane < NW ? rst[(s - 1) & 1][lane] : 0.0);
-        if (lane == 0) bkc_post<CS>(cl, inboxR, rank, BkcSlot{-1.0, -1.0, up, -1.0, 0x7fffffff, 0});
+        xpost<CS>(inboxR, rank, xslot(-1.0, -1.0, up, 0x7fffffff), &mbarR);
       }
-      cl.sync();
-      const BkcSlot mf = bkc_merge<CS>(inboxR, &merged);
+      mbar_wait(&mbarR, rphase & 1u);
+      const XSlot mf = xmerge<CS>(inboxR, &xmerged);
       if (gthread) {
         if (s >= 2) grow(pend_usq, ks2, k02);
         grow(mf.aux, ks1, k01);
       }
     }
   } else {
-    // ran to the end: the last step's arrival carried step s-2's maximum
-    bkc_wait();
-    const BkcSlot mf = bkc_merge<CS>(inbox[s % 3], &merged);
+    // ran to the end: the last step's push carried step s-2's maximum
+    if (tid == 0) mbar_arm(&mbar[s % 3], (unsigned)(n - k) * 16u + CS * kSlotBytes);
+    mbar_wait(&mbar[s % 3], (unsigned)(s / 3) & 1u);
+    const XSlot mf = xmerge<CS>(inbox[s % 3], &xmerged);
     if (gthread && s >= 2) grow(mf.aux, ks2, k02);
   }
-  // ---- write back the own rows (lower triangle), pivots, stats -------------
+  // ---- write back: diagonal / D entries and the trailing part in place; the
+  //      L entries of the columns of step t move by the interchanges of the
+  //      steps after t (kernels.py:96-98), applied here in reverse order ------
+  for (int i = tid; i < n; i += BKC_NT) qmap[i] = (short)i;
+  __syncthreads();
+  const int kend = info >= 0 ? k : n;                 // columns >= kend: unfactored trailing part
   for (int q = warp; q < nown; q += NW) {
     const int i = rank + q * CS;
     const cplx* src = Rl + bkc_off<CS>(i);
     cplx* row = W + (int64_t)i * lda;
-    for (int j = lane; j <= i; j += 32) row[j] = src[j];
+    for (int j = kend + lane; j <= i; j += 32) row[j] = src[j];
+  }
+  for (int t = s - 1; t >= 0; --t) {
+    const int kt = stk[3 * t], kst = stk[3 * t + 1], kpt = stk[3 * t + 2];
+    // columns kt (and kt+1) of step t: D entries in place, L entries (rows
+    // >= kt + kst) to row qmap[i] (= their row after the interchanges of t+1..)
+    const int q0 = first_q(kt);
+    for (int e = tid; e < (nown - q0) * kst; e += BKC_NT) {
+      const int i = rank + (q0 + e / kst) * CS, c = kt + e % kst;
+      if (c > i) continue;
+      const int dst = i >= kt + kst ? qmap[i] : i;
+      W[(int64_t)dst * lda + c] = Rl[bkc_off<CS>(i) + c];
+    }
+    if (kpt >= 0) {                                   // qmap <- qmap o tau_t
+      __syncthreads();
+      if (tid == 0) {
+        const int kkt = kt + kst - 1;
+        const short t0 = qmap[kkt];
+        qmap[kkt] = qmap[kpt];
+        qmap[kpt] = t0;
+      }
+      __syncthreads();
+    }
   }
   if (rank == 0)
     for (int i = tid; i < n; i += BKC_NT) {
-      a.perm[(int64_t)b * n + i] = perm_s[i];
+      a.perm[(int64_t)b * n + i] = (int64_t)perm_s[i];
       a.tags[(int64_t)b * n + i] = tags_s[i];
     }
   if (lead) {
@@ -556,14 +648,15 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     for (int i = 0; i < 8; ++i) prof[(tid == 0 ? 0 : 8) + i] = pacc[(tid == 0 ? 0 : 8) + i];
   }
 #endif
-  cl.sync();     // peers may still read this CTA's shared memory
+  cl.sync();     // no CTA exits while a peer may still push into its shared memory
 }
 
 template <int CS>
 static int bkc_launch(BkArgs* a, int batch, cudaStream_t s) {
-  // own rows + ls, ws (2n) + broadcast vectors (9n) + perm / tags (< n)
-  const size_t smem = sizeof(cplx) * (size_t)(bkc_entries<CS>(a->n) + 12 * (int64_t)a->n);
-  if (smem > 200 * 1024 || a->n > BKC_JPT * (BKC_NT - 32)) return -22;
+  // own rows + ls, ws (2n) + broadcast vectors (9n) complex; perm, row map
+  // (int16), step records (3 x int16), tags (int8): 11n bytes
+  const size_t smem = sizeof(cplx) * (size_t)(bkc_entries<CS>(a->n) + 11 * (int64_t)a->n) + 11 * (size_t)a->n + 16;
+  if (smem > 220 * 1024 || a->n > BKC_JPT * (BKC_NT - 32)) return -22;   // the CTA owns its SM
   cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   bk_cluster_kernel<CS><<<batch * CS, BKC_NT, smem, s>>>(*a);
   return (int)cudaGetLastError();
