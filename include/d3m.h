@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define D3M_ABI_VERSION 4
+#define D3M_ABI_VERSION 5
 
 int d3m_abi_version(void);
 const char* d3m_last_error(void);
@@ -169,12 +169,17 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
  * _solve_one (factor.py:243-310).  b: plan-ordered RHS (N x nrhs, consumed);
  * x: solution in plan order; tmp: max n_j x nrhs; part: partial-sum buffer of
  * part_elems complex (>= max_j ceil(max(R_j, n_j)/16) n_j nrhs);
- * d_gidx/h_gptr: global plan-order row of every panel row. */
+ * d_gidx/h_gptr: global plan-order row of every panel row.  d_plan (ABI v5,
+ * optional): the same plan arrays on the device, int64 [sizes | row_off |
+ * diag_off | panel_off | panel_rows | piv_off | binv_off] (nb each) then
+ * gptr (nb + 1); when given, both sweeps run as one persistent cooperative
+ * kernel per pass of 16 RHS (bitwise the same results), else one launch per
+ * product. */
 int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_off, const int64_t* h_diag_off,
                          const int64_t* h_panel_off, const int64_t* h_panel_rows, const int64_t* h_piv_off,
                          const int64_t* h_binv_off, const int64_t* h_gptr, const void* d_gidx, const void* d_pool,
                          const void* d_binv, const void* d_tags, void* d_b, void* d_u, void* d_x, void* d_tmp,
-                         void* d_part, int64_t part_elems, int nrhs, void* stream);
+                         void* d_part, int64_t part_elems, int nrhs, const void* d_plan, void* stream);
 
 /* Primal recovery of equal-sized subdomains: rhs = f - D lam (rhs holds f on
  * entry), E = A^-1 rhs with the cached packed factors, then the ordered

@@ -566,7 +566,7 @@ int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_of
                          const int64_t* h_panel_off, const int64_t* h_panel_rows, const int64_t* h_piv_off,
                          const int64_t* h_binv_off, const int64_t* h_gptr, const void* d_gidx, const void* d_pool,
                          const void* d_binv, const void* d_tags, void* d_b, void* d_u, void* d_x, void* d_tmp,
-                         void* d_part, int64_t part_elems, int nrhs, void* stream) {
+                         void* d_part, int64_t part_elems, int nrhs, const void* d_plan, void* stream) {
   // Forward (per column j, plan order):  z = Binv_j b_j;  u_j = D_j^-1 z;  b_i -= L_ij z
   // Backward (reverse):  w = u_j - sum_i L_ij^T x_i (split-K partials, ordered
   // reduce);  x_j = Binv_j^T w.  All products on DMMA (skinny_dmma.cu), in
@@ -587,6 +587,27 @@ int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_of
   cplx* x = C(d_x);
   cplx* tmp = C(d_tmp);
   const int N = nrhs;
+  static const char* solve_env = getenv("D3M_SOLVE");      // dev switch: 'l' = one launch per product
+  if (d_plan && !(solve_env && solve_env[0] == 'l')) {
+    // persistent cooperative kernel (skinny_dmma.cu) over the device plan arrays
+    const int64_t* d_arr = static_cast<const int64_t*>(d_plan);
+    d3m::SolvePlanDev pl{};
+    pl.sizes = d_arr; pl.row_off = d_arr + nb; pl.diag_off = d_arr + 2 * nb; pl.panel_off = d_arr + 3 * nb;
+    pl.panel_rows = d_arr + 4 * nb; pl.piv_off = d_arr + 5 * nb; pl.binv_off = d_arr + 6 * nb;
+    pl.gptr = d_arr + 7 * nb;
+    pl.gidx = gidx; pl.pool = pool; pl.binv = binv; pl.tags = static_cast<const int8_t*>(d_tags);
+    pl.b = b; pl.u = u; pl.x = x; pl.tmp = tmp; pl.part = C(d_part);
+    pl.nb = nb; pl.ldn = N;
+    int rc = 0;
+    for (int c0 = 0; c0 < N && rc == 0; c0 += 16) {
+      pl.c0 = c0;
+      pl.N = std::min(16, N - c0);
+      rc = launch(kClsSolve, s, [&] { return d3m_block_solve_persistent_launch(&pl, s); });
+    }
+    if (rc == 0) return 0;
+    if (rc != -22) return fail(rc, "d3m_block_solve_exec: persistent solve");
+    cudaGetLastError();
+  }
   auto sk = [&](int ta, const cplx* A, int lda, int M, int K, const cplx* Bp, const int64_t* bmap, cplx* Cp,
                 const int64_t* cmap, int mode, int kchunk, int c0) -> int {
     const int np = std::min(NP, N - c0);

@@ -24,6 +24,18 @@ struct BkArgs {
   cplx* scratch;      // batch x 4n, used when the staging does not fit smem
 };
 
+// Device-resident plan of the persistent block solve (skinny_dmma.cu)
+struct SolvePlanDev {
+  const int64_t *sizes, *row_off, *diag_off, *panel_off, *panel_rows, *piv_off, *binv_off, *gptr;
+  const int64_t* gidx;
+  const cplx *pool, *binv;
+  const int8_t* tags;
+  cplx *b, *u, *x, *tmp, *part;
+  int nb, N;                       // N: RHS columns of this pass (<= 16), leading dimension ldn
+  int ldn, c0;                     // row stride of b / u / x and the pass's first column
+};
+
+
 // Multi-RHS solve phases against packed factors (ldlt_solve.cu).
 struct SolveBatch {
   const cplx* F;  int64_t stride_f;   // packed factors (ld n)
@@ -43,6 +55,7 @@ int d3m_bk_blocked_launch(d3m::BkArgs* a, int batch, void* stream);
 int d3m_bk_cluster_launch(d3m::BkArgs* a, int batch, void* stream);
 int d3m_skinny_launch(int ta, const void* A, int lda, int M, int K, const void* B, int ldb, const void* bmap, int N,
                       void* C, int ldc, const void* cmap, int mode, int kchunk, void* stream);
+int d3m_block_solve_persistent_launch(void* plan, void* stream);
 int d3m_skinny_reduce_launch(const void* base, int ldb, const void* part, int nch, int M, int np, double sign,
                              void* out, int ldo, void* stream);
 // phase: 0 gather Z=B[perm], 1 forward (+U=D^-1 Z), 2 D^-1, 3 backward, 4 scatter B[perm]=Z

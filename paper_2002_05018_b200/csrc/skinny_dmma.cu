@@ -17,6 +17,7 @@
 // summation order of an output entry depends only on K and the chunking, so a
 // k-RHS solve equals k single-RHS solves bit for bit.
 #include <algorithm>
+#include <cooperative_groups.h>
 #include "d3m_common.cuh"
 #include "d3m_kernels.h"
 
@@ -69,16 +70,14 @@ __device__ __forceinline__ void sn_load(SnWarpSmem& S, int st, const cplx* A, in
 // CTA: 16 rows x 16 RHS over K rows [kbeg, kbeg + 256 * passes) of its chunk;
 // warp w takes the 64-row slices w, w + 4, ...; the four warp sums are added
 // in warp order at the end (fixed order, independent of N).
+// One CTA tile (rows [m0, m0+16), K rows [kbeg, kend) of chunk `chunk`);
+// shared by the per-product kernel below and the persistent block solve.
 template <bool TA>
-__global__ void __launch_bounds__(SN_NT)
-skinny_dmma_kernel(const cplx* __restrict__ A, int lda, int M, int K, const cplx* __restrict__ B, int ldb,
-                   const int64_t* __restrict__ bmap, int N, cplx* C, int ldc, const int64_t* __restrict__ cmap,
-                   int mode, int kchunk) {
-  extern __shared__ __align__(128) unsigned char sn_smem[];
+__device__ __forceinline__ void sn_tile(const cplx* __restrict__ A, int lda, int M, const cplx* __restrict__ B,
+                                        int ldb, const int64_t* __restrict__ bmap, int N, cplx* C, int ldc,
+                                        const int64_t* __restrict__ cmap, int mode, int m0, int chunk, int kbeg,
+                                        int kend, unsigned char* sn_smem) {
   SnWarpSmem* ws = reinterpret_cast<SnWarpSmem*>(sn_smem);
-  const int m0 = blockIdx.x * SN_BM;
-  const int chunk = blockIdx.y;
-  const int kbeg = chunk * kchunk, kend = min(K, kbeg + kchunk);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int fr = lane >> 2, fc = lane & 3;
   SnWarpSmem& S = ws[warp];
@@ -166,6 +165,19 @@ skinny_dmma_kernel(const cplx* __restrict__ A, int lda, int M, int K, const cplx
       *p = mode == 1 ? c_sub(*p, v) : v;
     }
   }
+  __syncthreads();                 // the staging memory is reused by the next tile
+}
+
+template <bool TA>
+__global__ void __launch_bounds__(SN_NT)
+skinny_dmma_kernel(const cplx* __restrict__ A, int lda, int M, int K, const cplx* __restrict__ B, int ldb,
+                   const int64_t* __restrict__ bmap, int N, cplx* C, int ldc, const int64_t* __restrict__ cmap,
+                   int mode, int kchunk) {
+  extern __shared__ __align__(128) unsigned char sn_smem[];
+  const int chunk = blockIdx.y;
+  const int kbeg = chunk * kchunk;
+  sn_tile<TA>(A, lda, M, B, ldb, bmap, N, C, ldc, cmap, mode, blockIdx.x * SN_BM, chunk, kbeg, min(K, kbeg + kchunk),
+              sn_smem);
 }
 
 // out[r * ldo + c] = (base ? base[r * ldb + c] : 0) + sign * sum_{ch < nch} part[(ch * M + r) * np + c]
@@ -182,7 +194,106 @@ __global__ void skinny_reduce_kernel(const cplx* base, int ldb, const cplx* part
   }
 }
 
+// ---- persistent block substitution (block_solve, factor.py:271-310) ------
+// One cooperative launch runs both sweeps for <= 16 RHS: the same products as
+// the per-product launches (sn_tile, same tiles and summation order, so the
+// results are bitwise those of the launch sequence) separated by grid-wide
+// barriers instead of kernel boundaries (864 launches of ~14 us latency each
+// on config 4).
+__global__ void __launch_bounds__(SN_NT, 2) block_solve_persistent(SolvePlanDev p) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) unsigned char sn_smem[];
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int N = p.N, ld = p.ldn;
+  constexpr int KCH = 256;
+  // forward: z = Binv_j b_j; u_j = D_j^-1 z; b_i -= L_ij z
+  for (int j = 0; j < p.nb; ++j) {
+    const int nj = (int)p.sizes[j];
+    if (nj == 0) continue;
+    const int R = (int)p.panel_rows[j];
+    cplx* bj = p.b + p.row_off[j] * ld + p.c0;
+    for (int t = cta; t * SN_BM < nj; t += G)
+      sn_tile<false>(p.binv + p.binv_off[j], nj, nj, bj, ld, nullptr, N, p.tmp, N, nullptr, 0, t * SN_BM, 0, 0, nj,
+                     sn_smem);
+    grid.sync();
+    {
+      const cplx* F = p.pool + p.diag_off[j];
+      const int8_t* tg = p.tags + p.piv_off[j];
+      cplx* uj = p.u + p.row_off[j] * ld + p.c0;
+      for (int e = cta * SN_NT + threadIdx.x; e < nj * N; e += G * SN_NT) {     // dinv_left_copy
+        const int c = e / N, col = e - c * N;
+        const int8_t t = tg[c];
+        if (t == 1) {
+          uj[(int64_t)c * ld + col] = x_div_np(p.tmp[e], F[(int64_t)c * nj + c]);
+        } else if (t == 2) {
+          cplx x0 = p.tmp[e], x1 = p.tmp[e + N];
+          dinv_pair(F[(int64_t)c * nj + c], F[(int64_t)(c + 1) * nj + c], F[(int64_t)(c + 1) * nj + c + 1], x0, x1);
+          uj[(int64_t)c * ld + col] = x0;
+          uj[(int64_t)(c + 1) * ld + col] = x1;
+        }
+      }
+    }
+    for (int t = cta; t * SN_BM < R; t += G)
+      sn_tile<false>(p.pool + p.panel_off[j], nj, R, p.tmp, N, nullptr, N, p.b + p.c0, ld, p.gidx + p.gptr[j], 1,
+                     t * SN_BM, 0, 0, nj, sn_smem);
+    grid.sync();
+  }
+  // backward: w = u_j - sum_i L_ij^T x_i (split-K partials, ordered reduce); x_j = Binv_j^T w
+  for (int j = p.nb - 1; j >= 0; --j) {
+    const int nj = (int)p.sizes[j];
+    if (nj == 0) continue;
+    const int R = (int)p.panel_rows[j];
+    const int nch = R > 0 ? (R + KCH - 1) / KCH : 0;
+    const int mt = (nj + SN_BM - 1) / SN_BM;
+    if (nch > 0) {
+      for (int t = cta; t < mt * nch; t += G) {
+        const int ch = t / mt, m0 = (t - ch * mt) * SN_BM;
+        sn_tile<true>(p.pool + p.panel_off[j], nj, nj, p.x + p.c0, ld, p.gidx + p.gptr[j], N, p.part, N, nullptr, 2,
+                      m0, ch, ch * KCH, min(R, ch * KCH + KCH), sn_smem);
+      }
+      grid.sync();
+    }
+    const cplx* uj = p.u + p.row_off[j] * ld + p.c0;
+    const int64_t len = (int64_t)nj * N;
+    for (int64_t e = cta * SN_NT + threadIdx.x; e < len; e += (int64_t)G * SN_NT) {   // skinny_reduce
+      const int r = (int)(e / N), c = (int)(e % N);
+      cplx acc = mk(0.0, 0.0);
+      for (int ch = 0; ch < nch; ++ch) acc = c_add(acc, p.part[(int64_t)ch * len + e]);
+      const cplx bb = uj[(int64_t)r * ld + c];
+      p.tmp[(int64_t)r * N + c] = mk(bb.x + -1.0 * acc.x, bb.y + -1.0 * acc.y);
+    }
+    grid.sync();
+    for (int t = cta; t * SN_BM < nj; t += G)
+      sn_tile<true>(p.binv + p.binv_off[j], nj, nj, p.tmp, N, nullptr, N, p.x + p.row_off[j] * ld + p.c0, ld, nullptr,
+                    0, t * SN_BM, 0, 0, nj, sn_smem);
+    grid.sync();
+  }
+}
+
 }  // namespace d3m
+
+// Persistent block solve over device-resident plan arrays (SolvePlanDev
+// pointers); one cooperative launch per pass of <= 16 RHS.  Returns -22 when
+// the device cannot co-schedule the grid (the caller falls back).
+extern "C" int d3m_block_solve_persistent_launch(void* plan, void* stream) {
+  using namespace d3m;
+  static int grid = -1;
+  if (grid < 0) {
+    cudaFuncSetAttribute(block_solve_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSnSmem);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, block_solve_persistent, SN_NT, kSnSmem);
+    grid = sms * std::min(per, 2);
+    if (grid <= 0) grid = 0;
+  }
+  if (grid == 0) return -22;
+  void* args[] = {plan};
+  const cudaError_t e = cudaLaunchCooperativeKernel((void*)block_solve_persistent, dim3(grid), dim3(SN_NT), args,
+                                                    kSnSmem, reinterpret_cast<cudaStream_t>(stream));
+  return (int)e;
+}
 
 extern "C" int d3m_skinny_reduce_launch(const void* base, int ldb, const void* part, int nch, int M, int np,
                                         double sign, void* out, int ldo, void* stream) {

@@ -558,6 +558,17 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
     return F
 
 
+def _solve_plan(sched: _Schedule):
+    """Device copy of the plan arrays for the persistent block solve (ABI v5,
+    include/d3m.h d3m_block_solve_exec), built once per plan."""
+    if getattr(sched, "d_solve_plan", None) is None:
+        nb = sched.nb
+        arr = np.concatenate([sched.sizes, sched.row_off[:nb], sched.diag_off, sched.panel_off, sched.panel_rows,
+                              sched.row_off[:nb], sched.binv_off[:nb], sched.gptr]).astype(np.int64)
+        sched.d_solve_plan = upload_i64(arr)
+    return sched.d_solve_plan
+
+
 def block_solve(F: BlockFactor, g: list) -> list:
     """Solve K x = g through the block factor (factor.py:271-310).
 
@@ -611,7 +622,7 @@ def block_solve(F: BlockFactor, g: list) -> list:
     _lib.call("d3m_block_solve_exec", nb, H(sched.sizes), H(sched.row_off), H(sched.diag_off),
               H(sched.panel_off), H(sched.panel_rows), H(sched.row_off), H(sched.binv_off), H(sched.gptr),
               _P(sched.d_gidx), _P(F._pool), _P(F._binv), _P(F._tags), _P(b), _P(u), _P(x), _P(tmp), _P(part),
-              part_elems, int(cols), stream_ptr())
+              part_elems, int(cols), _P(_solve_plan(sched)), stream_ptr())
     out = [None] * nb
     if device_in:
         for j in range(nb):

@@ -214,6 +214,28 @@ def test_multi_rhs_equals_single_rhs_bitwise(cuda):
             assert np.array_equal(X[i][:, c:c + 1], Xc[i])
 
 
+def test_persistent_solve_equals_launch_sequence_bitwise(cuda, monkeypatch):
+    """The persistent cooperative block solve (device plan, ABI v5) and the
+    per-product launch sequence (no device plan) give bitwise equal solutions,
+    over two passes of RHS (20 columns)."""
+    import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import factor as fac
+    from paper_2002_05018_b200 import workloads as wl
+    K, _ = wl.rand_block_system(91, max_blocks=7, max_size=60)
+    F = d.block_ldlt(K, _plan(K))
+    rng = np.random.default_rng(92)
+    B = [rng.standard_normal((int(s), 20)) + 1j * rng.standard_normal((int(s), 20)) for s in K.sizes]
+    X1 = d.block_solve(F, B)
+    monkeypatch.setattr(fac, "_solve_plan", lambda sched: None)
+    X2 = d.block_solve(F, B)
+    for i in range(K.nblocks):
+        assert np.array_equal(X1[i], X2[i])
+    for c in (0, 15, 16, 19):
+        Xc = d.block_solve(F, [b[:, c:c + 1] for b in B])
+        for i in range(K.nblocks):
+            assert np.array_equal(X1[i][:, c:c + 1], Xc[i])
+
+
 def test_determinism(cuda):
     import paper_2002_05018_b200 as d
     from paper_2002_05018_b200 import workloads as wl

@@ -10,8 +10,11 @@ K = wl.config4_matrix()
 plan = d.symbolic_factor(d.clique_graph(K), d.identity_ordering(K.nblocks), K.sizes)
 F = d.block_ldlt(to_device_blocks(K), plan)
 rhs = [DeviceArray(to_device(b)) for b in wl.config4_rhs(K)]
-for it in range(4):
+for it in range(5):
     torch.cuda.synchronize(); t0 = time.perf_counter()
-    x = d.block_solve(F, rhs); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    x = d.block_solve(F, rhs)
+    e1.record(); torch.cuda.synchronize()
     t1 = time.perf_counter()
-    print(f"solve {1e3*(t1-t0):.2f} ms", flush=True)
+    print(f"solve {1e3*(t1-t0):.2f} ms wall, {e0.elapsed_time(e1):.2f} ms device", flush=True)
