@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define D3M_ABI_VERSION 5
+#define D3M_ABI_VERSION 6
 
 int d3m_abi_version(void);
 const char* d3m_last_error(void);
@@ -151,7 +151,10 @@ int d3m_modulus_probe(const void* z, void* hyp, void* npabs, int64_t n, void* st
  * h_piv_off[j]; info/n2x2/growth/scale/asym are nb-long device arrays.
  * check_sym: 1 = full numpy-style symmetry check per diagonal block,
  * 2 = blocks known exactly symmetric (d3m_diag_sym_exact).
- * xbuf: X scratch (2 x max R_j n_j with lookahead). */
+ * xbuf: X scratch (2 x max R_j n_j with lookahead).
+ * nwait / h_wait_col / h_wait_ev (ABI v6; 0 / NULL / NULL = none): cudaEvent_t
+ * handles; before column h_wait_col[w] the critical stream waits on
+ * h_wait_ev[w] (blocks of K still being uploaded on a copy stream). */
 int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_off, const int64_t* h_panel_off,
                         const int64_t* h_panel_rows, const int64_t* h_piv_off, const int64_t* h_binv_off,
                         const int64_t* h_task_ptr, const int64_t* h_task_next, const int64_t* h_tiles_next,
@@ -159,7 +162,13 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                         const void* d_trsm_tasks, void* d_pool, void* d_binv, void* d_xbuf, int64_t xbuf_elems,
                         void* d_perm, void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale,
                         void* d_asym, void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead,
-                        void* stream);
+                        int nwait, const int64_t* h_wait_col, void* const* h_wait_ev, void* stream);
+
+/* n asynchronous copies dst + dst_off[i] <- src + src_off[i] (bytes, kind a
+ * cudaMemcpyKind) on `stream`: the chunked upload of K's blocks from pinned
+ * host memory. */
+int d3m_memcpy_batch(void* dst, const void* src, const int64_t* dst_off, const int64_t* src_off,
+                     const int64_t* nbytes, int n, int kind, void* stream);
 
 /* Forward / D^-1 / backward block substitution for nrhs right-hand sides in
  * one pass: z = Binv b, u = D^-1 z, b_i -= L_ij z (forward), w = u - sum_i

@@ -427,7 +427,7 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                         const void* d_trsm_tasks, void* d_pool, void* d_binv, void* d_xbuf, int64_t xbuf_elems,
                         void* d_perm, void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale,
                         void* d_asym, void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead,
-                        void* stream) {
+                        int nwait, const int64_t* h_wait_col, void* const* h_wait_ev, void* stream) {
   // diagonal BK kernel for supernodes > kExactBkMax: 0 cluster (default), 1 blocked
   const char* dbk = getenv("D3M_DIAG_BK");
   const int diag_bk_mode = (dbk && dbk[0] == 'b') ? 1 : 0;
@@ -471,6 +471,10 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
   }
   bool rest_pending = false;
   for (int j = 0; j < nb; ++j) {
+    // blocks of K still being uploaded: column j waits for the chunks it is
+    // the first to touch (the side stream follows s0 through ev_next)
+    for (int w = 0; w < nwait; ++w)
+      if (h_wait_col[w] == j) cudaStreamWaitEvent(s0, static_cast<cudaEvent_t>(h_wait_ev[w]), 0);
     const int nj = (int)h_sizes[j];
     const int64_t R = h_panel_rows[j];
     cplx* xbuf = C(d_xbuf) + (lookahead ? (j & 1) * (xbuf_elems / 2) : 0);
@@ -764,3 +768,17 @@ int64_t d3m_timing_intervals(double* out, int64_t max_triplets) {
 }
 
 }  // extern "C"
+
+// n asynchronous copies dst + dst_off[i] <- src + src_off[i] (bytes) on one
+// stream (kind: cudaMemcpyKind); lets the host enqueue a chunk of K's blocks
+// without one Python call per block.
+int d3m_memcpy_batch(void* dst, const void* src, const int64_t* dst_off, const int64_t* src_off,
+                     const int64_t* nbytes, int n, int kind, void* stream) {
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  for (int i = 0; i < n; ++i) {
+    const cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + dst_off[i], static_cast<const char*>(src) + src_off[i],
+                                          (size_t)nbytes[i], static_cast<cudaMemcpyKind>(kind), s);
+    if (e != cudaSuccess) return fail((int)e, "d3m_memcpy_batch");
+  }
+  return 0;
+}

@@ -487,6 +487,113 @@ def _upload_K(K: BlockSparseSym, sched: _Schedule, plan: EliminationPlan, pool):
         _lib.call("d3m_block_copy", _P(src), _P(pool), _P(d_rec), len(recs), maxe, stream_ptr())
 
 
+_CHUNK_COLS = (2, 4, 8, 16, 24, 32, 48, 64, 96)     # upload chunk boundaries (block columns)
+
+
+def _first_touch(sched: _Schedule) -> dict:
+    """Plan-order block (a, b), a >= b -> the first block column whose BK,
+    panel TRSM or trailing update reads or writes it (cached per plan)."""
+    ft = getattr(sched, "first_touch", None)
+    if ft is None:
+        ft = {}
+        for j in range(sched.nb):
+            pat = [int(i) for i in sched.pattern[j]]
+            for key in [(j, j)] + [(i, j) for i in pat] + [(i, k) for a, i in enumerate(pat) for k in pat[:a + 1]]:
+                if key not in ft:
+                    ft[key] = j
+        sched.first_touch = ft
+    return ft
+
+
+def _upload_K_streamed(K: BlockSparseSym, sched: _Schedule, plan: EliminationPlan, pool, flag):
+    """Chunked asynchronous upload of K when every block is a view of one
+    pinned host allocation: chunk 0 holds the diagonal blocks and the blocks
+    first touched by the first block columns; later chunks follow by first
+    touch (_CHUNK_COLS) on a copy stream, each with an event the executor
+    waits on before the first column that touches it (ABI v6).  The sym-check
+    flag is computed after chunk 0.  Returns (wait columns, events, keep-alive)
+    or None when the inputs do not qualify."""
+    t = require_cuda()
+    items = list(K.blocks.items())
+    base = None
+    for _, b in items:
+        if not (_is_tensor(b) and not b.is_cuda and b.is_contiguous() and b.dtype == t.complex128 and b.is_pinned()):
+            return None
+        bb = b.untyped_storage().data_ptr()
+        if base is None:
+            base = bb
+        elif bb != base:
+            return None
+    if base is None:
+        return None
+    nb = plan.nblocks
+    inv = plan.order.inverse()
+    sizes = K.sizes
+    ft = _first_touch(sched)
+    bounds = [0] + [c for c in _CHUNK_COLS if c < nb] + [nb]
+    chunks = [[] for _ in range(len(bounds) - 1)]
+    for (i, j), b in items:
+        a, c = int(inv[i]), int(inv[j])
+        key = (a, c) if a >= c else (c, a)
+        if key not in ft:
+            raise FactorConsistencyError(f"block {key} outside the symbolic pattern")
+        ch = 0 if key[0] == key[1] else int(np.searchsorted(bounds, ft[key], side="right")) - 1
+        chunks[ch].append(((i, j), b))
+    recs = np.zeros(len(items), dtype=_lib.COPY_TASK)
+    plan_chunks, r, o = [], 0, 0
+    for ch, entries in enumerate(chunks):
+        if not entries:
+            continue
+        r0, maxe = r, 1
+        doff, soff, nby = [], [], []
+        for (i, j), b in entries:
+            a, c = int(inv[i]), int(inv[j])
+            ni, nj = int(sizes[i]), int(sizes[j])
+            key, transpose = ((a, c), 0) if a >= c else ((c, a), 1)
+            if key[0] == key[1]:
+                dst, ld = int(sched.diag_off[key[0]]), int(plan.sizes_perm[key[0]])
+            else:
+                dst, _, ld = sched.loc[key]
+            rows, cols = (ni, nj) if not transpose else (nj, ni)
+            recs[r] = (o, dst, rows, cols, nj, ld, transpose, _lib.COPY_STORE)
+            maxe = max(maxe, rows * cols)
+            doff.append(16 * o)
+            soff.append(b.data_ptr() - base)
+            nby.append(16 * ni * nj)
+            o += ni * nj
+            r += 1
+        plan_chunks.append((bounds[ch], r0, r - r0, maxe, np.asarray(doff, np.int64), np.asarray(soff, np.int64),
+                            np.asarray(nby, np.int64)))
+    stage = empty(max(o, 1))
+    d_rec = upload_bytes(recs)
+    cur = t.cuda.current_stream()
+    cs = getattr(sched, "copy_stream", None)
+    if cs is None:
+        cs = sched.copy_stream = t.cuda.Stream()
+    ready = t.cuda.Event()
+    ready.record(cur)                      # pool zeroed, flag / staging allocated
+    cs.wait_event(ready)
+    csp = _lib.ctypes.c_void_p(cs.cuda_stream)
+    H = _lib.hptr
+    waits, events = [], []
+    for n, (col, r0, cnt, maxe, doff, soff, nby) in enumerate(plan_chunks):
+        _lib.call("d3m_memcpy_batch", _P(stage), _lib.ctypes.c_void_p(base), H(doff), H(soff), H(nby), cnt, 1, csp)
+        _lib.call("d3m_block_copy", _P(stage), _P(pool), _lib.ctypes.c_void_p(d_rec.data_ptr() + r0 * recs.itemsize),
+                  cnt, maxe, csp)
+        if n == 0:
+            _lib.call("d3m_diag_sym_exact", _P(pool), _P(sched.d_diag_off), _P(sched.d_sizes), nb, _P(flag), csp)
+        ev = t.cuda.Event()
+        ev.record(cs)
+        if n == 0:
+            cur.wait_event(ev)             # the flag and the first columns' blocks
+        else:
+            waits.append(col)
+            events.append(ev)
+    stage.record_stream(cs)
+    d_rec.record_stream(cs)
+    return np.asarray(waits, dtype=np.int64), events, (stage, d_rec)
+
+
 def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFAULT_PIVOT_TOL,
                lookahead: bool = True) -> BlockFactor:
     """Right-looking block LDL^T of ``K`` following ``plan`` on one GPU.
@@ -512,11 +619,21 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
     stored, flops, peak = sched.stats_cache[keyset]
     pool = empty(max(sched.pool_elems, 1))
     _lib.call("d3m_zero", _P(pool), sched.pool_elems, stream_ptr())
-    _upload_K(K, sched, plan, pool)
     # exactly symmetric diagonal blocks stay exactly symmetric (mirrored SYM
     # updates): the diagonal BK then needs only the lower triangle
     flag = t.ones(1, dtype=t.int32, device="cuda")
-    _lib.call("d3m_diag_sym_exact", _P(pool), _P(sched.d_diag_off), _P(sched.d_sizes), nb, _P(flag), stream_ptr())
+    streamed = _upload_K_streamed(K, sched, plan, pool, flag)
+    if streamed is None:
+        _upload_K(K, sched, plan, pool)
+        _lib.call("d3m_diag_sym_exact", _P(pool), _P(sched.d_diag_off), _P(sched.d_sizes), nb, _P(flag), stream_ptr())
+        wait_cols, wait_ev = np.zeros(1, np.int64), np.zeros(1, np.uint64)
+        nwait = 0
+    else:
+        wait_cols, events, _keep = streamed
+        nwait = len(events)
+        wait_ev = np.asarray([e.cuda_event for e in events] or [0], dtype=np.uint64)
+        if nwait == 0:
+            wait_cols = np.zeros(1, np.int64)
     check_sym = 2 if int(flag.item()) == 1 else 1
     perm = t.empty(max(sched.piv_elems, 1), dtype=t.int64, device="cuda")
     tags = t.empty(max(sched.piv_elems, 1), dtype=t.int8, device="cuda")
@@ -535,7 +652,7 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
               H(sched.tiles_next), H(sched.tiles_rest), H(sched.tiles_trsm), _P(sched.d_tasks),
               _P(sched.d_trsm_tasks), _P(pool), _P(binv), _P(xbuf), sched.xbuf_elems, _P(perm), _P(tags),
               _P(info), _P(n2), _P(gr), _P(sc), _P(asy), _P(scratch), float(pivot_tol), check_sym,
-              int(bool(lookahead)), stream_ptr())
+              int(bool(lookahead)), nwait, H(wait_cols), H(wait_ev), stream_ptr())
     info_h = info.cpu().numpy()
     bad = np.flatnonzero(info_h != -1)
     if bad.size:
