@@ -87,6 +87,12 @@ int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stri
 int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* C, void* h_tasks, int ntasks,
                       void* d_tasks, void* stream);
 
+/* Complex product form of every grouped GEMM launched afterwards in this
+ * process: 3 = Gauss 3M (three real DMMA products per complex product, the
+ * default), 4 = 4M (four).  0 only queries.  Returns the previous form.
+ * The environment variable D3M_ZGEMM=3m|4m sets the initial form. */
+int d3m_gemm_set_form(int form);
+
 /* Batched Schur reduction of equal-sized subdomains: factor A_d in place,
  * X = A_d^-1 [D_d | F_d], K_D = 0.5 (D^T X_D + (D^T X_D)^T), G_d = D^T X_F.
  * Replaces subdomain.reduce_domain (subdomain.py:166-184) for a batch; F_d

@@ -26,6 +26,7 @@ _SIGNATURES = {
     "d3m_bk_blocked_factor": [I32, I32, P, I64, I32, F64, I32, P, P, P, P, P, P, P, P, P],
     "d3m_ldlt_solve_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P],
     "d3m_zgemm_grouped": [I32, I32, P, P, P, P, I32, P, P],
+    "d3m_gemm_set_form": [I32],
     "d3m_schur_reduce_batched": [I32, I32, I32, I32, P, P, P, F64] + [P] * 14 + [P, I32, P, I32, P],
     "d3m_block_copy": [P, P, P, I32, I64, P],
     "d3m_gather_rows": [P, P, P, I64, I32, P],
@@ -145,6 +146,12 @@ def call(name: str, *args):
         msg = lib.d3m_last_error().decode(errors="replace")
         raise D3MError(f"{name} returned {rc}: {msg}")
     return rc
+
+
+def gemm_form(form: int = 0) -> int:
+    """Set the grouped GEMM's complex product form (3 = Gauss 3M, 4 = 4M; 0
+    only queries) for later launches in this process; returns the previous."""
+    return int(load().d3m_gemm_set_form(int(form)))
 
 
 def ptr(t) -> ctypes.c_void_p:

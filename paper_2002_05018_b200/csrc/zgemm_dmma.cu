@@ -28,6 +28,7 @@
 #include "d3m_common.cuh"
 #include "d3m_gemm.h"
 #include "d3m_kernels.h"
+#include <cstdlib>
 
 namespace d3m {
 
@@ -61,15 +62,16 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 // Stage loader: tile rows [r0, r0+64) x k-columns [k0, k0+8) of an operand
 // whose element (r, k) lives at  P[r*ld + k]  (TRANS=false) or P[k*ld + r].
-template <bool TRANS>
+// NT threads (128 or 256) cover the 512 16-byte elements of a stage slice.
+template <bool TRANS, int NT = NTHREADS>
 __device__ __forceinline__ void load_tile(cplx (*S)[PITCH], const cplx* P, int ld, int r0, int rows,
                                           int k0, int kdim) {
   const int t = threadIdx.x;
   if (!TRANS) {
-    // 8 threads cover one 128-byte row segment; 16 rows per pass
+    // 8 threads cover one 128-byte row segment; NT/8 rows per pass
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int r = p * 16 + (t >> 3), k = t & 7;
+    for (int p = 0; p < 512 / NT; ++p) {
+      const int r = p * (NT / 8) + (t >> 3), k = t & 7;
       const bool ok = (r0 + r < rows) && (k0 + k < kdim);
       const cplx* g = ok ? P + (int64_t)(r0 + r) * ld + (k0 + k) : P;
       cp_async16(&S[r][k], g, ok);
@@ -77,8 +79,8 @@ __device__ __forceinline__ void load_tile(cplx (*S)[PITCH], const cplx* P, int l
   } else {
     // 64 threads cover one contiguous 1 KB row of the stored operand
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int r = t & 63, k = p * 2 + (t >> 6);
+    for (int p = 0; p < 512 / NT; ++p) {
+      const int r = t & 63, k = p * (NT / 64) + (t >> 6);
       const bool ok = (r0 + r < rows) && (k0 + k < kdim);
       const cplx* g = ok ? P + (int64_t)(k0 + k) * ld + (r0 + r) : P;
       cp_async16(&S[r][k], g, ok);
@@ -108,10 +110,23 @@ __device__ __forceinline__ int find_task(const GemmTask* __restrict__ tasks, int
   return s_task;
 }
 
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(NTHREADS, 2)
+// G3 selects the complex product.  G3 = false: four real DMMAs per complex
+// product (4M), 128 threads, 32 x 32 complex warp tiles.  G3 = true: Gauss's
+// three-multiplication form (3M),
+//   P = A_re B_re,  Q = A_im B_im,  R = (A_re + A_im)(B_re + B_im),
+//   re = P - Q,     im = R - P - Q,
+// 25% fewer DMMAs; its three accumulators need 48 doubles per 32 x 16 warp
+// tile, so the CTA runs 8 warps (2 x 4) and stays at two CTAs per SM.  The
+// operand sums are formed in registers from the staged (re, im) pairs.  3M
+// is normwise stable (each entry's error is bounded by eps times
+// (|a_re|+|a_im|)(|b_re|+|b_im|) summed over k, against the 4M product's
+// eps |a||b|), so the results stay within rounding of the reference's ZGEMM.
+template <bool TA, bool TB, bool G3>
+__global__ void __launch_bounds__(G3 ? 2 * NTHREADS : NTHREADS, 2)
 zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bbase, cplx* Cbase,
                      const GemmTask* __restrict__ tasks, int ntasks, unsigned long long* tmax) {
+  constexpr int NT = G3 ? 2 * NTHREADS : NTHREADS;
+  constexpr int WJ = G3 ? 2 : 4;             // 8-column DMMA sub-tiles per warp tile
   extern __shared__ __align__(128) unsigned char smem_raw[];
   GemmStage* st = reinterpret_cast<GemmStage*>(smem_raw);
 
@@ -136,21 +151,25 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
   if (m0 >= M || n0 >= N) return;      // device-built tasks may shrink below their tile budget
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = G3 ? (warp >> 2) * 32 : (warp >> 1) * 32;
+  const int wn = G3 ? (warp & 3) * 16 : (warp & 1) * 32;
   const int fr = lane >> 2, fc = lane & 3;
 
-  double acc_re[4][4][2], acc_im[4][4][2];
+  // 4M: acc_re / acc_im.  3M: acc_re = P, acc_im = Q, acc_x = R until the epilogue.
+  double acc_re[4][WJ][2], acc_im[4][WJ][2], acc_x[4][WJ][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
+    for (int j = 0; j < WJ; ++j)
+      acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = acc_x[i][j][0] =
+          acc_x[i][j][1] = 0.0;
 
   const int ktiles = (K + BKC - 1) / BKC;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < ktiles) {
-      load_tile<TA>(st[s].a, A, tk.lda, m0, M, s * BKC, K);
-      load_tile<TB>(st[s].b, B, tk.ldb, n0, N, s * BKC, K);
+      load_tile<TA, NT>(st[s].a, A, tk.lda, m0, M, s * BKC, K);
+      load_tile<TB, NT>(st[s].b, B, tk.ldb, n0, N, s * BKC, K);
     }
     cp_commit();
   }
@@ -169,13 +188,13 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
       const int nk = kt + STAGES - 1;
       if (nk < ktiles) {
         const int slot = nk % STAGES;
-        load_tile<TA>(st[slot].a, A, tk.lda, m0, M, nk * BKC, K);
-        load_tile<TB>(st[slot].b, B, tk.ldb, n0, N, nk * BKC, K);
+        load_tile<TA, NT>(st[slot].a, A, tk.lda, m0, M, nk * BKC, K);
+        load_tile<TB, NT>(st[slot].b, B, tk.ldb, n0, N, nk * BKC, K);
       } else if (cpre) {
         const int ch = nk - ktiles, r0 = ch * CP_ROWS;
         const int rows = min(CP_ROWS, BM - r0);
         cplx* dst = reinterpret_cast<cplx*>(&st[(kt + STAGES - 1) % STAGES]);
-        for (int e = threadIdx.x; e < rows * BN; e += NTHREADS) {
+        for (int e = threadIdx.x; e < rows * BN; e += NT) {
           const int r = e / BN, c = e - r * BN;
           const bool ok = m0 + r0 + r < M && n0 + c < N;
           cp_async16(dst + r * CP_PITCH + c, ok ? C + (int64_t)(m0 + r0 + r) * tk.ldc + n0 + c : C, ok);
@@ -184,43 +203,82 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
       cp_commit();
     }
     const int slot = kt % STAGES;
+    if constexpr (G3) {
 #pragma unroll
-    for (int kk = 0; kk < BKC / 4; ++kk) {
-      double are[4], aim[4], anim[4], bre[4], bim[4];
+      for (int kk = 0; kk < BKC / 4; ++kk) {
+        double bre[WJ], bim[WJ], bsum[WJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const cplx a = st[slot].a[wm + i * 8 + fr][kk * 4 + fc];
-        are[i] = a.x;
-        aim[i] = a.y;
-        anim[i] = -a.y;
+        for (int j = 0; j < WJ; ++j) {
+          const cplx b = st[slot].b[wn + j * 8 + fr][kk * 4 + fc];
+          bre[j] = b.x;
+          bim[j] = b.y;
+          bsum[j] = b.x + b.y;
+        }
+        // per A sub-tile row: P, Q, R for both column sub-tiles; a given
+        // accumulator is touched once per k-step (24 DMMAs apart)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const cplx a = st[slot].a[wm + i * 8 + fr][kk * 4 + fc];
+          const double asum = a.x + a.y;
+#pragma unroll
+          for (int j = 0; j < WJ; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], a.x, bre[j]);
+#pragma unroll
+          for (int j = 0; j < WJ; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], a.y, bim[j]);
+#pragma unroll
+          for (int j = 0; j < WJ; ++j) dmma(acc_x[i][j][0], acc_x[i][j][1], asum, bsum[j]);
+        }
       }
+    } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const cplx b = st[slot].b[wn + j * 8 + fr][kk * 4 + fc];
-        bre[j] = b.x;
-        bim[j] = b.y;
+      for (int kk = 0; kk < BKC / 4; ++kk) {
+        double are[4], aim[4], anim[4], bre[4], bim[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const cplx a = st[slot].a[wm + i * 8 + fr][kk * 4 + fc];
+          are[i] = a.x;
+          aim[i] = a.y;
+          anim[i] = -a.y;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const cplx b = st[slot].b[wn + j * 8 + fr][kk * 4 + fc];
+          bre[j] = b.x;
+          bim[j] = b.y;
+        }
+        // four passes over all sub-tiles: dependent DMMAs on one accumulator are
+        // 32 instructions apart (per-accumulator order unchanged: bitwise same)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
       }
-      // four passes over all sub-tiles: dependent DMMAs on one accumulator are
-      // 32 instructions apart (per-accumulator order unchanged: bitwise same)
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
     }
   }
   cp_wait<0>();
+  if constexpr (G3) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < WJ; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double p = acc_re[i][j][h], q = acc_im[i][j][h];
+          acc_re[i][j][h] = p - q;
+          acc_im[i][j][h] = (acc_x[i][j][h] - p) - q;
+        }
+  }
 
   // ---- epilogue ------------------------------------------------------------
   const bool mirror = sym && !(tk.flags & kGemmLowerOnly);
@@ -235,7 +293,7 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
       const int ch = rl / CP_ROWS;
       const cplx* crow = reinterpret_cast<const cplx*>(&st[(ktiles + ch) % STAGES]) + (rl - ch * CP_ROWS) * CP_PITCH;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < WJ; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int cl = wn + j * 8 + fc * 2 + h, c = n0 + cl;
@@ -254,9 +312,9 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int r = m0 + wm + i * 8 + fr;
-      cplx cv[4][2], cq[4][2];
+      cplx cv[WJ][2], cq[WJ][2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < WJ; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = n0 + wn + j * 8 + fc * 2 + h;
@@ -267,7 +325,7 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
           if (ok && mirror && c < r) cq[j][h] = C[(int64_t)c * ldc + r];
         }
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < WJ; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = n0 + wn + j * 8 + fc * 2 + h;
@@ -455,17 +513,36 @@ constexpr size_t kGemmSmem = sizeof(cplx) * STAGES * (BM + BN) * PITCH;
 
 static unsigned long long* g_tmax = nullptr;   // set per launch by d3m_gemm_launch_tm
 
-template <bool TA, bool TB>
-static int launch_t(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
+template <bool TA, bool TB, bool G3>
+static int launch_g(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
                     cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(zgemm_grouped_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(zgemm_grouped_kernel<TA, TB, G3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kGemmSmem);
     configured = true;
   }
-  zgemm_grouped_kernel<TA, TB><<<ntiles, NTHREADS, kGemmSmem, s>>>(A, B, C, tasks, ntasks, g_tmax);
+  zgemm_grouped_kernel<TA, TB, G3><<<ntiles, G3 ? 2 * NTHREADS : NTHREADS, kGemmSmem, s>>>(A, B, C, tasks,
+                                                                                           ntasks, g_tmax);
   return (int)cudaGetLastError();
+}
+
+// Complex product form of the grouped GEMM: 3M (default) or 4M, chosen once
+// per process by D3M_ZGEMM=3m|4m, or per call chain by d3m_gemm_set_form.
+static int g_form = -1;
+static bool use_3m() {
+  if (g_form < 0) {
+    const char* e = getenv("D3M_ZGEMM");
+    g_form = (e && (e[0] == '4')) ? 4 : 3;
+  }
+  return g_form == 3;
+}
+
+template <bool TA, bool TB>
+static int launch_t(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
+                    cudaStream_t s) {
+  return use_3m() ? launch_g<TA, TB, true>(A, B, C, tasks, ntasks, ntiles, s)
+                  : launch_g<TA, TB, false>(A, B, C, tasks, ntasks, ntiles, s);
 }
 
 }  // namespace d3m
@@ -486,6 +563,14 @@ extern "C" int d3m_gemm_prepare_tasks(d3m::GemmTask* tasks, int ntasks) {
 
 extern "C" int d3m_gemm_launch_tm(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
                                   int ntasks, int ntiles, void* tmax, void* stream);
+
+// Select the complex product form of the grouped GEMM: 3 (Gauss 3M) or 4 (4M).
+// Returns the form in effect before the call; 0 only queries.
+extern "C" int d3m_gemm_set_form(int form) {
+  const int prev = d3m::use_3m() ? 3 : 4;
+  if (form == 3 || form == 4) d3m::g_form = form;
+  return prev;
+}
 
 extern "C" int d3m_gemm_launch(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
                                int ntasks, int ntiles, void* stream) {

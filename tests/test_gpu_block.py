@@ -19,8 +19,18 @@ def _plan(K, order=None):
     return d.symbolic_factor(g, order, K.sizes)
 
 
-def test_gemm_vs_numpy(cuda):
-    """Grouped DMMA GEMM, all four operand layouts and three modes."""
+@pytest.fixture(params=[3, 4], ids=["3m", "4m"])
+def gemm_form(request, cuda):
+    """Run a test under each complex product form of the grouped GEMM."""
+    from paper_2002_05018_b200 import _lib
+    prev = _lib.gemm_form(request.param)
+    yield request.param
+    _lib.gemm_form(prev)
+
+
+def test_gemm_vs_numpy(cuda, gemm_form):
+    """Grouped DMMA GEMM, all four operand layouts and three modes, both
+    complex product forms (3M default, 4M)."""
     from paper_2002_05018_b200 import _lib
     from paper_2002_05018_b200.device import stream_ptr, to_device
     rng = np.random.default_rng(3)
@@ -49,7 +59,7 @@ def test_gemm_vs_numpy(cuda):
                     assert np.abs(got - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max()) * K, (M, N, K, ta, tb, mode)
 
 
-def test_gemm_symmetric_target(cuda):
+def test_gemm_symmetric_target(cuda, gemm_form):
     from paper_2002_05018_b200 import _lib
     from paper_2002_05018_b200.device import stream_ptr, to_device
     rng = np.random.default_rng(4)
@@ -72,6 +82,30 @@ def test_gemm_symmetric_target(cuda):
     got = dW.cpu().numpy()
     assert np.array_equal(got, got.T)
     assert np.abs(got - (W - upd)).max() <= 1e-12 * np.abs(upd).max()
+
+
+def test_gemm_3m_error_is_rounding_level(cuda):
+    """Integer-valued operands keep every product and partial sum exact in
+    fp64, so both product forms must reproduce A B^T exactly (this catches
+    any mis-assembled 3M term, which a rounding tolerance could hide)."""
+    from paper_2002_05018_b200 import _lib
+    from paper_2002_05018_b200.device import stream_ptr, to_device
+    rng = np.random.default_rng(9)
+    M, N, K = 130, 70, 256
+    A = rng.integers(-64, 64, (M, K)) + 1j * rng.integers(-64, 64, (M, K))
+    B = rng.integers(-64, 64, (N, K)) + 1j * rng.integers(-64, 64, (N, K))
+    exact = A @ B.T                                       # |sums| < 2^53: exact in complex128
+    for form in (3, 4):
+        prev = _lib.gemm_form(form)
+        dA, dB, dC = to_device(A), to_device(B), to_device(np.zeros((M, N), complex))
+        task = np.zeros(1, dtype=_lib.GEMM_TASK)
+        task["m"], task["n"], task["k"], task["lda"], task["ldb"], task["ldc"] = M, N, K, K, K, N
+        task["flags"] = _lib.GEMM_STORE
+        dt = cuda.empty(64, dtype=cuda.uint8, device="cuda")
+        _lib.call("d3m_zgemm_grouped", 0, 0, _lib.ptr(dA), _lib.ptr(dB), _lib.ptr(dC),
+                  _lib.hptr(task), 1, _lib.ptr(dt), stream_ptr())
+        _lib.gemm_form(prev)
+        assert np.array_equal(dC.cpu().numpy(), exact), form
 
 
 def test_block_pivots_and_solution_vs_reference_goldens(cuda):
