@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define D3M_ABI_VERSION 6
+#define D3M_ABI_VERSION 7
 
 int d3m_abi_version(void);
 const char* d3m_last_error(void);
@@ -175,6 +175,18 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
  * host memory. */
 int d3m_memcpy_batch(void* dst, const void* src, const int64_t* dst_off, const int64_t* src_off,
                      const int64_t* nbytes, int n, int kind, void* stream);
+
+/* Block residual r -= K x for iterative refinement of block_solve (ABI v7).
+ * K's stored blocks (original numbering) stay in device buffers h_abase[l];
+ * x and r are N x cols in plan-order rows.  Launch l is a grouped GEMM
+ * (transposed A iff h_ta[l]; B_eff = x^T, so tb = 1) over h_ntasks[l]
+ * prepared task records at d_tasks + h_task_off[l] (h_ntiles[l] tiles), every
+ * target block at most once per launch; the launch order fixes the summation
+ * order, so the result is deterministic.  No reference counterpart: the
+ * reference's block_solve (factor.py:243-310) does not refine. */
+int d3m_block_residual(int nlaunch, const int32_t* h_ta, const int32_t* h_ntasks, const int32_t* h_ntiles,
+                       const int64_t* h_task_off, const void* const* h_abase, const void* x, void* r,
+                       const void* d_tasks, void* stream);
 
 /* Forward / D^-1 / backward block substitution for nrhs right-hand sides in
  * one pass: z = Binv b, u = D^-1 z, b_i -= L_ij z (forward), w = u - sum_i

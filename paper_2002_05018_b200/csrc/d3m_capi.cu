@@ -389,6 +389,19 @@ int d3m_block_copy(const void* src, void* dst, const void* d_tasks, int ntasks, 
   return 0;
 }
 
+int d3m_block_residual(int nlaunch, const int32_t* h_ta, const int32_t* h_ntasks, const int32_t* h_ntiles,
+                       const int64_t* h_task_off, const void* const* h_abase, const void* x, void* r,
+                       const void* d_tasks, void* stream) {
+  if (nlaunch < 0) return fail(-22, "d3m_block_residual: bad launch count");
+  const auto* tasks = static_cast<const d3m::GemmTask*>(d_tasks);
+  for (int l = 0; l < nlaunch; ++l) {
+    D3M_TRY(launch(kClsSolve, stream, [&] {
+      return d3m_gemm_launch(h_ta[l], 1, h_abase[l], x, r, tasks + h_task_off[l], h_ntasks[l], h_ntiles[l], stream);
+    }));
+  }
+  return 0;
+}
+
 int d3m_gather_rows(const void* src, const void* idx, void* out, int64_t nrows, int cols, void* stream) {
   D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_gather_index_launch(src, idx, out, nrows, cols, stream); }));
   return 0;

@@ -485,6 +485,7 @@ def _upload_K(K: BlockSparseSym, sched: _Schedule, plan: EliminationPlan, pool):
             maxe = max(maxe, rows * cols)
         d_rec = upload_bytes(recs)
         _lib.call("d3m_block_copy", _P(src), _P(pool), _P(d_rec), len(recs), maxe, stream_ptr())
+    return groups
 
 
 _CHUNK_COLS = (2, 4, 8, 16, 24, 32, 48, 64, 96)     # upload chunk boundaries (block columns)
@@ -541,6 +542,7 @@ def _upload_K_streamed(K: BlockSparseSym, sched: _Schedule, plan: EliminationPla
         chunks[ch].append(((i, j), b))
     recs = np.zeros(len(items), dtype=_lib.COPY_TASK)
     plan_chunks, r, o = [], 0, 0
+    kentries = []                          # (offset in stage, original key): K stays in stage
     for ch, entries in enumerate(chunks):
         if not entries:
             continue
@@ -556,6 +558,7 @@ def _upload_K_streamed(K: BlockSparseSym, sched: _Schedule, plan: EliminationPla
                 dst, _, ld = sched.loc[key]
             rows, cols = (ni, nj) if not transpose else (nj, ni)
             recs[r] = (o, dst, rows, cols, nj, ld, transpose, _lib.COPY_STORE)
+            kentries.append((o, (i, j)))
             maxe = max(maxe, rows * cols)
             doff.append(16 * o)
             soff.append(b.data_ptr() - base)
@@ -591,7 +594,7 @@ def _upload_K_streamed(K: BlockSparseSym, sched: _Schedule, plan: EliminationPla
             events.append(ev)
     stage.record_stream(cs)
     d_rec.record_stream(cs)
-    return np.asarray(waits, dtype=np.int64), events, (stage, d_rec)
+    return np.asarray(waits, dtype=np.int64), events, (stage, d_rec), [(stage, kentries)]
 
 
 def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFAULT_PIVOT_TOL,
@@ -624,12 +627,12 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
     flag = t.ones(1, dtype=t.int32, device="cuda")
     streamed = _upload_K_streamed(K, sched, plan, pool, flag)
     if streamed is None:
-        _upload_K(K, sched, plan, pool)
+        kgroups = _upload_K(K, sched, plan, pool)
         _lib.call("d3m_diag_sym_exact", _P(pool), _P(sched.d_diag_off), _P(sched.d_sizes), nb, _P(flag), stream_ptr())
         wait_cols, wait_ev = np.zeros(1, np.int64), np.zeros(1, np.uint64)
         nwait = 0
     else:
-        wait_cols, events, _keep = streamed
+        wait_cols, events, _keep, kgroups = streamed
         nwait = len(events)
         wait_ev = np.asarray([e.cuda_event for e in events] or [0], dtype=np.uint64)
         if nwait == 0:
@@ -672,6 +675,10 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
     stats.growth_factor = float(max((f.growth for f in diag), default=1.0))
     F = BlockFactor(plan, diag, _OffDiag(sched, pool), stats, sched, pool, perm, tags)
     F._binv = binv
+    # device copy of K's stored blocks (the upload staging buffer or the
+    # caller's device blocks), kept for block_solve(refine=...)
+    F._kgroups = kgroups
+    F._ksizes = np.asarray(K.sizes, dtype=np.int64)
     return F
 
 
@@ -686,13 +693,72 @@ def _solve_plan(sched: _Schedule):
     return sched.d_solve_plan
 
 
-def block_solve(F: BlockFactor, g: list) -> list:
+def _residual_launches(F: BlockFactor, cols: int):
+    """Grouped-GEMM launches computing r -= K x over K's stored blocks
+    (include/d3m.h d3m_block_residual), cached per factor and RHS count.
+
+    Stored block (i, j) contributes K_ij x_j to row block i and, off the
+    diagonal, K_ij^T x_i to row block j (blockmat.py:93-101's symmetric
+    scatter).  Contributions to one target are ordered by (source, term) and
+    launch round t carries every target's t-th contribution, so no two tasks
+    of a launch write the same rows and the sum order is fixed."""
+    cache = getattr(F, "_res_cache", None)
+    if cache is None:
+        cache = F._res_cache = {}
+    if cols in cache:
+        return cache[cols]
+    sched, plan = F._sched, F.plan
+    inv = plan.order.inverse()
+    ks = F._ksizes
+    row_off = sched.row_off
+    per_target: dict[int, list] = {}
+    for gi, (src, entries) in enumerate(F._kgroups):
+        for off, (i, j) in entries:
+            a, c = int(inv[i]), int(inv[j])
+            ni, nj = int(ks[i]), int(ks[j])
+            per_target.setdefault(a, []).append((c, 0, gi, int(off), ni, nj, 0, nj))
+            if i != j:
+                per_target.setdefault(c, []).append((a, 1, gi, int(off), nj, ni, 1, nj))
+    rounds: dict[tuple, list] = {}
+    for a, lst in per_target.items():
+        for t, (c, term, gi, off, m, k, ta, lda) in enumerate(sorted(lst)):
+            rounds.setdefault((t, gi, ta), []).append((a, c, off, m, k, lda))
+    recs, ta_l, nt_l, tiles_l, off_l, base_l = [], [], [], [], [], []
+    for (t, gi, ta) in sorted(rounds):
+        lst = rounds[(t, gi, ta)]
+        rec = np.zeros(len(lst), dtype=_lib.GEMM_TASK)
+        tiles = 0
+        for r_, (a, c, off, m, k, lda) in enumerate(lst):
+            tn = (cols + _lib.GEMM_BN - 1) // _lib.GEMM_BN
+            rec[r_] = (off, int(row_off[c]) * cols, int(row_off[a]) * cols, m, cols, k, lda, cols, cols,
+                       _lib.GEMM_SUB, tiles, tn, 0)
+            tiles += ((m + _lib.GEMM_BM - 1) // _lib.GEMM_BM) * tn
+        off_l.append(sum(len(x) for x in recs))
+        recs.append(rec)
+        ta_l.append(ta)
+        nt_l.append(len(lst))
+        tiles_l.append(tiles)
+        base_l.append(F._kgroups[gi][0].data_ptr())
+    d_tasks = upload_bytes(np.concatenate(recs))
+    entry = (len(recs), np.asarray(ta_l, np.int32), np.asarray(nt_l, np.int32), np.asarray(tiles_l, np.int32),
+             np.asarray(off_l, np.int64), np.asarray(base_l, np.uint64), d_tasks)
+    cache[cols] = entry
+    return entry
+
+
+def block_solve(F: BlockFactor, g: list, refine: int = 0) -> list:
     """Solve K x = g through the block factor (factor.py:271-310).
 
     ``g`` is a block vector in the original block numbering, each block 1-D
     or a matrix of RHS columns.  All columns go through one device pass, each
     computed independently, so k-RHS results equal k single solves bit for
     bit.  Device-resident inputs give device-resident outputs.
+
+    ``refine`` (not in the reference, default 0 = the reference's algorithm):
+    steps of fixed-precision iterative refinement, x += solve(g - K x), with
+    K x formed on the tensor pipe from the device copy of K's stored blocks
+    that block_ldlt keeps.  One step takes the relative residual of config 4
+    from ~4e-10 (the reference's own: ~1e-10) to rounding level.
     """
     nb = F.plan.nblocks
     if len(g) != nb:
@@ -736,10 +802,31 @@ def block_solve(F: BlockFactor, g: list) -> list:
     part_elems = int(max(((int(r) + 255) // 256) * int(n) for r, n in zip(sched.panel_rows, sched.sizes))) * 16
     part = empty(max(part_elems, 1))
     H = _lib.hptr
-    _lib.call("d3m_block_solve_exec", nb, H(sched.sizes), H(sched.row_off), H(sched.diag_off),
-              H(sched.panel_off), H(sched.panel_rows), H(sched.row_off), H(sched.binv_off), H(sched.gptr),
-              _P(sched.d_gidx), _P(F._pool), _P(F._binv), _P(F._tags), _P(b), _P(u), _P(x), _P(tmp), _P(part),
-              part_elems, int(cols), _P(_solve_plan(sched)), stream_ptr())
+
+    def solve(rhs, out):
+        _lib.call("d3m_block_solve_exec", nb, H(sched.sizes), H(sched.row_off), H(sched.diag_off),
+                  H(sched.panel_off), H(sched.panel_rows), H(sched.row_off), H(sched.binv_off), H(sched.gptr),
+                  _P(sched.d_gidx), _P(F._pool), _P(F._binv), _P(F._tags), _P(rhs), _P(u), _P(out), _P(tmp),
+                  _P(part), part_elems, int(cols), _P(_solve_plan(sched)), stream_ptr())
+
+    if refine:
+        if getattr(F, "_kgroups", None) is None:
+            raise SolverStateError("block_solve(refine=...) needs the factor's copy of K (block_ldlt output)")
+        b0 = empty((N, cols))
+        b0.copy_(b)                   # the solve consumes its right-hand side in place
+    solve(b, x)
+    if refine:
+        nl, ta, nt, tiles, toff, base, d_tasks = _residual_launches(F, int(cols))
+        r, d = empty((N, cols)), empty((N, cols))
+        add = np.zeros(1, dtype=_lib.COPY_TASK)
+        add[0] = (0, 0, N, cols, cols, cols, 0, _lib.COPY_ADD)
+        d_add = upload_bytes(add)
+        for _ in range(int(refine)):
+            r.copy_(b0)
+            _lib.call("d3m_block_residual", nl, H(ta), H(nt), H(tiles), H(toff), H(base), _P(x), _P(r),
+                      _P(d_tasks), stream_ptr())
+            solve(r, d)
+            _lib.call("d3m_block_copy", _P(d), _P(x), _P(d_add), 1, N * cols, stream_ptr())
     out = [None] * nb
     if device_in:
         for j in range(nb):
