@@ -280,10 +280,10 @@ def run_ours(args):
                      "peak_source": "live DMMA m8n8k4 probe (tools/fp64_peak.cu)" if peak_live else
                      "profiles/fp64_peak_r01.txt (measured DMMA burst)",
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if achieved else None,
-                     "traffic": 1.694e9,
+                     "traffic": 1.669e9,
                      "traffic_note": "DRAM bytes per launch of a representative 11,628-tile rest-update launch "
-                                     "(ncu --set full, profiles/ncu_gemm_cfg4_r01h_summary.txt); algorithmic C "
-                                     "traffic of that launch 1.524e9 B (1.11x)"},
+                                     "(ncu --set full, profiles/ncu_gemm3m_cfg4_r01j_summary.txt, 3M form); "
+                                     "algorithmic C traffic of that launch 1.524e9 B (1.10x)"},
         "instrumented_ms_per_step": round(ms_step_instr, 3),
         "stage_ms_per_step": {k: round(v / args.steps, 3) for k, v in cnt["union_ms"].items()},
         "stage_ms_summed_per_step": {k: round(v / args.steps, 3) for k, v in cnt["ms"].items()},
