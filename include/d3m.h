@@ -176,6 +176,23 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
 int d3m_memcpy_batch(void* dst, const void* src, const int64_t* dst_off, const int64_t* src_off,
                      const int64_t* nbytes, int n, int kind, void* stream);
 
+/* Block substitution as a dataflow of work items (ABI v7): the products of
+ * d3m_block_solve_exec (same tiles and summation order, so bitwise equal to
+ * it), taken from an atomic queue by one resident grid per pass of <= 16 RHS
+ * and ordered only by their true dependencies (per-item counter waits)
+ * instead of ~5 grid-wide barriers per block column.  d_items: nitems
+ * records of 8 int32 {type, column, p0, p1, dep_off, dep_cnt, inc0, inc1};
+ * d_deps: int32 pairs {counter, target}; d_part_off: per-column int64 offset
+ * of its split-K partials in d_part (sum over columns of
+ * ceil(R_j/256) * n_j * 16 complex); d_counters: ncounters int32 scratch
+ * (zeroed here before every pass; the last one is the queue head).  The item
+ * list is built by the host (factor.py _solve_flow).  Replaces the
+ * substitutions of factor.py:271-310 like d3m_block_solve_exec. */
+int d3m_block_solve_dataflow(int nb, const void* d_plan, const void* d_items, int nitems, const void* d_deps,
+                             const void* d_part_off, void* d_counters, int ncounters, const void* d_gidx,
+                             const void* d_pool, const void* d_binv, const void* d_tags, void* d_b, void* d_u,
+                             void* d_x, void* d_part, int nrhs, void* stream);
+
 /* Block residual r -= K x for iterative refinement of block_solve (ABI v7).
  * K's stored blocks (original numbering) stay in device buffers h_abase[l];
  * x and r are N x cols in plan-order rows.  Launch l is a grouped GEMM

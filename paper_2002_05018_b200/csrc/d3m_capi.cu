@@ -579,6 +579,33 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
 //   b, u, x : N x nrhs plan order (b consumed);  tmp: max n_j x nrhs;
 //   part    : partial sums, part_elems complex
 // ---------------------------------------------------------------------------
+int d3m_block_solve_dataflow(int nb, const void* d_plan, const void* d_items, int nitems, const void* d_deps,
+                             const void* d_part_off, void* d_counters, int ncounters, const void* d_gidx,
+                             const void* d_pool, const void* d_binv, const void* d_tags, void* d_b, void* d_u,
+                             void* d_x, void* d_part, int nrhs, void* stream) {
+  if (nb <= 0 || nrhs <= 0) return 0;
+  if (!d_plan || !d_items || nitems <= 0 || ncounters <= 0) return fail(-22, "d3m_block_solve_dataflow: empty plan");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t* d_arr = static_cast<const int64_t*>(d_plan);
+  d3m::SolvePlanDev pl{};
+  pl.sizes = d_arr; pl.row_off = d_arr + nb; pl.diag_off = d_arr + 2 * nb; pl.panel_off = d_arr + 3 * nb;
+  pl.panel_rows = d_arr + 4 * nb; pl.piv_off = d_arr + 5 * nb; pl.binv_off = d_arr + 6 * nb;
+  pl.gptr = d_arr + 7 * nb;
+  pl.gidx = static_cast<const int64_t*>(d_gidx); pl.pool = CC(d_pool); pl.binv = CC(d_binv);
+  pl.tags = static_cast<const int8_t*>(d_tags);
+  pl.b = C(d_b); pl.u = C(d_u); pl.x = C(d_x); pl.tmp = nullptr; pl.part = C(d_part);
+  pl.nb = nb; pl.ldn = nrhs;
+  for (int c0 = 0; c0 < nrhs; c0 += 16) {
+    pl.c0 = c0;
+    pl.N = std::min(16, nrhs - c0);
+    const int rc = launch(kClsSolve, s, [&] {
+      return d3m_block_solve_flow_launch(&pl, d_items, nitems, d_deps, d_part_off, d_counters, ncounters, s);
+    });
+    if (rc != 0) return fail(rc, "d3m_block_solve_dataflow: launch");
+  }
+  return 0;
+}
+
 int d3m_block_solve_exec(int nb, const int64_t* h_sizes, const int64_t* h_row_off, const int64_t* h_diag_off,
                          const int64_t* h_panel_off, const int64_t* h_panel_rows, const int64_t* h_piv_off,
                          const int64_t* h_binv_off, const int64_t* h_gptr, const void* d_gidx, const void* d_pool,

@@ -12,7 +12,9 @@
 // its own 4-deep cp.async ring, 2 x 2 DMMA sub-tiles with (re, im)
 // accumulators) and add their sums in warp order at the end: the dependent
 // chain per warp is 4x shorter than one warp walking all of K, and small
-// products get 4x more CTAs.  gridDim.y > 1 splits K into chunks of kchunk rows; each chunk writes
+// products get 4x more CTAs (8 warps of 32-row slices, one CTA per SM for
+// the shared memory, made the dataflow solve 16% slower: fewer items in
+// flight for the bulk updates).  gridDim.y > 1 splits K into chunks of kchunk rows; each chunk writes
 // its partial sums (no atomics) for an ordered reduction afterwards.  The
 // summation order of an output entry depends only on K and the chunking, so a
 // k-RHS solve equals k single-RHS solves bit for bit.
@@ -271,7 +273,212 @@ __global__ void __launch_bounds__(SN_NT, 2) block_solve_persistent(SolvePlanDev 
   }
 }
 
+// ---- dataflow block substitution ---------------------------------------------
+// The grid-barrier kernel above runs 720 dependent phases on config 4 (~13 us
+// each: 9.3 ms against a 1.4 ms HBM floor; ncu: 43% of the stall samples at
+// the grid barrier).  Here the same tiles (same rows, K ranges, split-K and
+// summation order, so the results are bitwise those of the barrier kernel)
+// are work items of a host-built list (factor.py _solve_flow), taken from a
+// global atomic queue by the resident CTAs.  Each item names the counters
+// it waits for (>= target) and the counters it increments when done, so only
+// true dependencies serialise:
+//   FA(j,t)  z_j rows [16t,16t+16) = Binv_j b_j        waits: all updates into b_j
+//   FD(j)    u_j = D_j^-1 z_j                           waits: z_j
+//   FB(j,r)  b[gidx] -= L_panel(j)[rows r..r+16) z_j    waits: z_j, the previous
+//            update of the same 16 rows (per-tile sequence: ascending j, as the
+//            phases of the barrier kernel)
+//   BC(j,ch,mt)  split-K partial of L_ij^T x_i (chunk ch, 16 rows mt)
+//                                                       waits: x_i of the chunk's blocks
+//   BR(j,r0,r1)  w_j = u_j - sum_ch partials (ascending ch), in place in u
+//                                                       waits: all partials of j, u_j
+//   BE(j,t)  x_j rows [16t,16t+16) = Binv_j^T w_j       waits: w_j
+// z_j lives in the x rows of block j until BE(j) overwrites them (every reader
+// of z_j precedes BE(j) in the dependency order).  The list is a topological
+// order, so the smallest unfinished item always has its inputs: with every
+// CTA resident (cooperative launch) the queue cannot deadlock.  Waits are
+// bounded (a lost dependency traps instead of hanging the GPU).
+struct FlowItem {
+  int type, j, p0, p1, dep_off, dep_cnt, inc0, inc1;
+};
+enum { kFA = 0, kFD = 1, kFB = 2, kBC = 3, kBR = 4, kBE = 5 };
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;\n" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(SN_NT, 2)
+block_solve_dataflow(SolvePlanDev p, const FlowItem* __restrict__ items, int nitems, const int2* __restrict__ deps,
+                     const int64_t* __restrict__ part_off, int* cnt, int* next, long long* trace) {
+  extern __shared__ __align__(128) unsigned char sn_smem[];
+  __shared__ int s_idx;
+  const int N = p.N, ld = p.ldn;
+  constexpr int KCH = 256;
+  __shared__ int s_next;
+  if (threadIdx.x == 0) s_next = atomicAdd(next, 1);
+  for (;;) {
+    // the queue index of the item after this one is taken while this one runs
+    if (threadIdx.x == 0) {
+      s_idx = s_next;
+      if (s_idx < nitems) s_next = atomicAdd(next, 1);
+    }
+    __syncthreads();
+    const int idx = s_idx;
+    if (idx >= nitems) break;
+    const FlowItem it = items[idx];
+    if (trace && threadIdx.x == 0) trace[3 * (int64_t)idx] = gtimer();
+    if (threadIdx.x == 0) {
+      for (int d = 0; d < it.dep_cnt; ++d) {
+        const int2 dp = deps[it.dep_off + d];
+        for (unsigned spin = 0; ld_acquire(cnt + dp.x) < dp.y; ++spin) {
+          if (spin > (1u << 28)) __trap();
+          if (spin > 64) __nanosleep(32);
+        }
+      }
+    }
+    __syncthreads();
+    if (trace && threadIdx.x == 0) trace[3 * (int64_t)idx + 1] = gtimer();
+    const int j = it.j;
+    const int nj = (int)p.sizes[j];
+    const int64_t ro = p.row_off[j];
+    switch (it.type) {
+      case kFA:
+        sn_tile<false>(p.binv + p.binv_off[j], nj, nj, p.b + ro * ld + p.c0, ld, nullptr, N, p.x + ro * ld + p.c0, ld,
+                       nullptr, 0, it.p0 * SN_BM, 0, 0, nj, sn_smem);
+        break;
+      case kFD: {      // rows [p0, p1) (a 2x2 pair belongs to the piece of its first row)
+        const cplx* F = p.pool + p.diag_off[j];
+        const int8_t* tg = p.tags + p.piv_off[j];
+        const cplx* z = p.x + ro * ld + p.c0;
+        cplx* uj = p.u + ro * ld + p.c0;
+        for (int e = it.p0 * N + threadIdx.x; e < it.p1 * N; e += SN_NT) {
+          const int c = e / N, col = e - c * N;
+          const int8_t t = tg[c];
+          if (t == 1) {
+            uj[(int64_t)c * ld + col] = x_div_np(__ldcg(z + (int64_t)c * ld + col), F[(int64_t)c * nj + c]);
+          } else if (t == 2) {
+            cplx x0 = __ldcg(z + (int64_t)c * ld + col), x1 = __ldcg(z + (int64_t)(c + 1) * ld + col);
+            dinv_pair(F[(int64_t)c * nj + c], F[(int64_t)(c + 1) * nj + c], F[(int64_t)(c + 1) * nj + c + 1], x0, x1);
+            uj[(int64_t)c * ld + col] = x0;
+            uj[(int64_t)(c + 1) * ld + col] = x1;
+          }
+        }
+        break;
+      }
+      case kFB:
+        sn_tile<false>(p.pool + p.panel_off[j] + (int64_t)it.p0 * nj, nj, it.p1, p.x + ro * ld + p.c0, ld, nullptr, N,
+                       p.b + p.c0, ld, p.gidx + p.gptr[j] + it.p0, 1, 0, 0, 0, nj, sn_smem);
+        break;
+      case kBC: {
+        const int R = (int)p.panel_rows[j], ch = it.p0;
+        sn_tile<true>(p.pool + p.panel_off[j], nj, nj, p.x + p.c0, ld, p.gidx + p.gptr[j], N, p.part + part_off[j], N,
+                      nullptr, 2, it.p1 * SN_BM, ch, ch * KCH, min(R, ch * KCH + KCH), sn_smem);
+        break;
+      }
+      case kBR: {      // rows [p0, p1); partials loaded 16 chunks ahead, summed in chunk order
+        const int R = (int)p.panel_rows[j];
+        const int nch = R > 0 ? (R + KCH - 1) / KCH : 0;
+        const int64_t len = (int64_t)nj * N;
+        const cplx* part = p.part + part_off[j];
+        cplx* uj = p.u + ro * ld + p.c0;
+        for (int e = it.p0 * N + threadIdx.x; e < it.p1 * N; e += SN_NT) {
+          const int r = e / N, c = e - r * N;
+          cplx acc = mk(0.0, 0.0);
+          for (int c8 = 0; c8 < nch; c8 += 16) {
+            cplx v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (c8 + q < nch) v[q] = __ldcg(part + (int64_t)(c8 + q) * len + e);
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (c8 + q < nch) acc = c_add(acc, v[q]);
+          }
+          const cplx bb = __ldcg(uj + (int64_t)r * ld + c);
+          uj[(int64_t)r * ld + c] = mk(bb.x + -1.0 * acc.x, bb.y + -1.0 * acc.y);
+        }
+        break;
+      }
+      default:   // kBE
+        sn_tile<true>(p.binv + p.binv_off[j], nj, nj, p.u + ro * ld + p.c0, ld, nullptr, N, p.x + ro * ld + p.c0, ld,
+                      nullptr, 0, it.p0 * SN_BM, 0, 0, nj, sn_smem);
+        break;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (it.inc0 >= 0) atomicAdd(cnt + it.inc0, 1);
+      if (it.inc1 >= 0) atomicAdd(cnt + it.inc1, 1);
+      if (trace) trace[3 * (int64_t)idx + 2] = gtimer();
+    }
+  }
+}
+
 }  // namespace d3m
+
+static long long* g_flow_trace = nullptr;
+static int g_flow_trace_n = 0;
+// copy the last traced pass's stamps (3 per item) to host memory; returns the item count
+extern "C" int d3m_flow_trace(void* host, int max_items) {
+  if (!g_flow_trace) return 0;
+  const int n = g_flow_trace_n < max_items ? g_flow_trace_n : max_items;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_flow_trace, sizeof(long long) * 3 * (size_t)n, cudaMemcpyDeviceToHost);
+  return n;
+}
+
+// Dataflow block solve (one cooperative launch per pass of <= 16 RHS; the
+// caller zeroes `cnt` (ncounters ints, the last one the queue head) before
+// each pass).  Returns -22 when the grid cannot be co-resident.
+extern "C" int d3m_block_solve_flow_launch(void* plan, const void* items, int nitems, const void* deps,
+                                           const void* part_off, void* cnt, int ncounters, void* stream) {
+  using namespace d3m;
+  static int grid = -1;
+  if (grid < 0) {
+    cudaFuncSetAttribute(block_solve_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSnSmem);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, block_solve_dataflow, SN_NT, kSnSmem);
+    grid = sms * std::min(per, 2);
+    if (grid <= 0) grid = 0;
+  }
+  if (grid == 0) return -22;
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)ncounters, s);
+  if (e != cudaSuccess) return (int)e;
+  const SolvePlanDev* pl = static_cast<const SolvePlanDev*>(plan);
+  const FlowItem* it = static_cast<const FlowItem*>(items);
+  const int2* dp = static_cast<const int2*>(deps);
+  const int64_t* po = static_cast<const int64_t*>(part_off);
+  int* c = static_cast<int*>(cnt);
+  int* nx = c + ncounters - 1;
+  // D3M_FLOW_TRACE=1 (dev aid): per-item globaltimer stamps (taken, inputs
+  // ready, done) of the last pass, read back by d3m_flow_trace
+  static long long* trace = nullptr;
+  static int64_t trace_cap = 0;
+  static const char* tenv = getenv("D3M_FLOW_TRACE");
+  long long* tr = nullptr;
+  if (tenv && tenv[0] == '1') {
+    if (trace_cap < 3 * (int64_t)nitems) {
+      if (trace) cudaFree(trace);
+      if (cudaMalloc(&trace, sizeof(long long) * 3 * (size_t)nitems) != cudaSuccess) return 2;
+      trace_cap = 3 * (int64_t)nitems;
+    }
+    tr = trace;
+    g_flow_trace = trace;
+    g_flow_trace_n = nitems;
+  }
+  void* args[] = {const_cast<SolvePlanDev*>(pl), &it, &nitems, &dp, &po, &c, &nx, &tr};
+  e = cudaLaunchCooperativeKernel((void*)block_solve_dataflow, dim3(grid), dim3(SN_NT), args, kSnSmem, s);
+  return (int)e;
+}
 
 // Persistent block solve over device-resident plan arrays (SolvePlanDev
 // pointers); one cooperative launch per pass of <= 16 RHS.  Returns -22 when

@@ -248,26 +248,33 @@ def test_multi_rhs_equals_single_rhs_bitwise(cuda):
             assert np.array_equal(X[i][:, c:c + 1], Xc[i])
 
 
-def test_persistent_solve_equals_launch_sequence_bitwise(cuda, monkeypatch):
-    """The persistent cooperative block solve (device plan, ABI v5) and the
-    per-product launch sequence (no device plan) give bitwise equal solutions,
-    over two passes of RHS (20 columns)."""
+@pytest.mark.parametrize("seed,max_blocks,max_size", [(91, 7, 60), (93, 6, 300), (95, 12, 20)])
+def test_solve_kernels_bitwise_equal(cuda, monkeypatch, seed, max_blocks, max_size):
+    """The dataflow block solve (default), the grid-barrier persistent kernel
+    (ABI v5) and the per-product launch sequence give bitwise equal
+    solutions, over two passes of RHS (20 columns); columns solved alone
+    equal the multi-RHS solve bitwise."""
     import paper_2002_05018_b200 as d
     from paper_2002_05018_b200 import factor as fac
     from paper_2002_05018_b200 import workloads as wl
-    K, _ = wl.rand_block_system(91, max_blocks=7, max_size=60)
+    K, _ = wl.rand_block_system(seed, max_blocks=max_blocks, max_size=max_size)
     F = d.block_ldlt(K, _plan(K))
-    rng = np.random.default_rng(92)
+    rng = np.random.default_rng(seed + 1)
     B = [rng.standard_normal((int(s), 20)) + 1j * rng.standard_normal((int(s), 20)) for s in K.sizes]
+    assert fac._SOLVE_MODE == "flow"
+    X0 = d.block_solve(F, B)
+    monkeypatch.setattr(fac, "_SOLVE_MODE", "barrier")
     X1 = d.block_solve(F, B)
     monkeypatch.setattr(fac, "_solve_plan", lambda sched: None)
     X2 = d.block_solve(F, B)
     for i in range(K.nblocks):
+        assert np.array_equal(X0[i], X1[i])
         assert np.array_equal(X1[i], X2[i])
+    monkeypatch.undo()
     for c in (0, 15, 16, 19):
         Xc = d.block_solve(F, [b[:, c:c + 1] for b in B])
         for i in range(K.nblocks):
-            assert np.array_equal(X1[i][:, c:c + 1], Xc[i])
+            assert np.array_equal(X0[i][:, c:c + 1], Xc[i])
 
 
 def test_determinism(cuda):

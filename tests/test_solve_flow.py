@@ -1,0 +1,76 @@
+"""Host checks of the dataflow block-solve work list (factor.flow_items):
+every item's dependencies are satisfied by the items before it (so the
+device queue, which hands items out in list order, cannot deadlock), each
+16-row tile receives its updates in ascending column order, and every
+counter reaches the value the later items wait for."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2002_05018_b200 import workloads as wl
+from paper_2002_05018_b200.blockmat import clique_graph
+from paper_2002_05018_b200.factor import _BC, _BE, _BR, _FA, _FB, _FD, flow_items
+from paper_2002_05018_b200.ordering import identity_ordering, reorder
+from paper_2002_05018_b200.symbolic import symbolic_factor
+
+
+def _check(plan):
+    sizes = np.asarray(plan.sizes_perm, dtype=np.int64)
+    pattern = [np.asarray(p, dtype=np.int64) for p in plan.pattern]
+    panel_rows = np.array([int(sizes[p].sum()) for p in pattern], dtype=np.int64)
+    items, deps, part_off, ncnt, part_elems = flow_items(sizes, pattern, panel_rows)
+    cnt = np.zeros(ncnt, dtype=np.int64)
+    upd_order = {}
+    for idx, (typ, j, p0, p1, doff, dcnt, inc0, inc1) in enumerate(items):
+        for c, target in deps[doff:doff + dcnt]:
+            assert cnt[c] >= target, (idx, typ, j, c, target, cnt[c])
+        if typ == _FB:
+            upd_order.setdefault((j, p0), None)
+        for c in (inc0, inc1):
+            if c >= 0:
+                cnt[c] += 1
+    nb = len(sizes)
+    T = (sizes + 15) // 16
+    assert np.array_equal(cnt[:nb], np.where(sizes > 0, T, 0))                   # z tiles
+    assert np.array_equal(cnt[5 * nb:6 * nb], np.where(sizes > 0, T, 0))         # x tiles
+    # every update tile of every column appears exactly once
+    fb = items[items[:, 0] == _FB]
+    expect = sum(int(T[i]) for j in range(nb) for i in pattern[j])
+    assert len(fb) == expect
+    # per target tile: ascending columns
+    seen = {}
+    for typ, j, p0, p1, *_ in items:
+        if typ != _FB:
+            continue
+        tgt = (int(np.searchsorted(np.cumsum(sizes[pattern[j]]), p0, side="right")), j)
+        i = int(pattern[j][tgt[0]])
+        t = (p0 - int(np.concatenate([[0], np.cumsum(sizes[pattern[j]])])[tgt[0]])) // 16
+        last = seen.get((i, t), -1)
+        assert j > last
+        seen[(i, t)] = j
+    assert part_elems >= 1 and len(part_off) >= 1
+    return items
+
+
+def test_flow_list_config4():
+    """Config 4's plan (144 faces x 256, natural order): structure from the
+    face adjacency with 1x1 placeholder blocks."""
+    from paper_2002_05018_b200.blockmat import from_blocks
+    from paper_2002_05018_b200.workloads import grid_faces
+    faces = grid_faces(4, 4, 4)
+    trip = [(f, g, np.ones((1, 1))) for f in range(len(faces)) for g in range(f + 1)
+            if f == g or set(faces[f]) & set(faces[g])]
+    K1 = from_blocks([1] * len(faces), trip)
+    plan = symbolic_factor(clique_graph(K1), identity_ordering(len(faces)), [256] * len(faces))
+    items = _check(plan)
+    assert len(items) > 100_000
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_flow_list_random_plans(seed):
+    K, _ = wl.rand_block_system(seed + 200, max_blocks=14, max_size=40, density=0.35)
+    g = clique_graph(K)
+    for order in (reorder(g, K.sizes), identity_ordering(K.nblocks)):
+        _check(symbolic_factor(g, order, K.sizes))
