@@ -517,7 +517,12 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
       }));
       // Binv_j = L_jj^-1 P_j (also used by block_solve) + D_jj^-1 coefficients
       D3M_TRY(launch(kClsTrsm, s0, [&] {
-        const int rc = d3m_tri_inv_warp_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, s0);
+        // blocked 16 x 16 inverse (n <= 256), else warp per column (n <= 512), else the generic kernel;
+        // D3M_TRI_INV=w forces the warp kernel (A/B measurements)
+        static const char* ti_env = getenv("D3M_TRI_INV");
+        int rc = -22;
+        if (!(ti_env && ti_env[0] == 'w')) rc = d3m_tri_inv_blocked_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, s0);
+        if (rc == -22) rc = d3m_tri_inv_warp_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, s0);
         return rc == -22 ? d3m_tri_inv_launch(diag, 0, perm, 0, tags, 0, binv + h_binv_off[j], 0, nj, 1, s0) : rc;
       }));
     }

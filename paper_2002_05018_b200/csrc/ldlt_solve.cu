@@ -434,6 +434,169 @@ __global__ void dinv_rows_coef_kernel(const cplx* __restrict__ X, cplx* P, int64
 
 }  // namespace d3m
 
+namespace d3m {
+
+// -------------------------------------------------------------------------
+// Blocked L^-1 P for n <= 256 (the diagonal blocks of block_ldlt, on the
+// critical chain of every block column).  The warp-per-column kernel walks
+// n dependent rows per column with one L2 round trip and one warp reduction
+// each (~150 us at n = 256); here the chain is n/16 block steps:
+//   tri_inv_diag16:  Dinv_i = L_ii^-1 of every 16 x 16 diagonal block (+ the
+//                    D^-1 coefficients, as the warp kernel)
+//   tri_inv_cols16:  CTA k owns block column k of X = L^-1:
+//                    X_kk = Dinv_k;  X_ik = -Dinv_i (sum_{k<=m<i} L_im X_mk),
+//                    the L rows of the next step prefetched by cp.async.
+// L(i, j) is the packed factor's strict lower part with the sub-diagonal of
+// every 2 x 2 pivot read as zero (kernels.py:123-125 stores e there).
+// -------------------------------------------------------------------------
+constexpr int TI_B = 16;
+
+__device__ __forceinline__ cplx ti_L(const cplx* F, const int8_t* tags, int n, int r, int c) {
+  if (r == c + 1 && tags[c] == 2) return mk(0.0, 0.0);
+  return F[(int64_t)r * n + c];
+}
+
+__global__ void __launch_bounds__(64) tri_inv_diag16(const cplx* __restrict__ F, const int8_t* __restrict__ tags,
+                                                     cplx* Dinv, cplx* coef, int n) {
+  __shared__ cplx Ls[TI_B][TI_B];
+  const int i = blockIdx.x, r0 = i * TI_B, nb = min(TI_B, n - r0);
+  for (int e = threadIdx.x; e < TI_B * TI_B; e += 64) {
+    const int r = e / TI_B, c = e % TI_B;
+    Ls[r][c] = (r < nb && c < r) ? ti_L(F, tags, n, r0 + r, r0 + c) : mk(0.0, 0.0);
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < TI_B) {                     // column t of L_ii^-1 by substitution
+    cplx x[TI_B];
+#pragma unroll
+    for (int r = 0; r < TI_B; ++r) {
+      cplx acc = mk(r == t ? 1.0 : 0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < r; ++c) {
+        const cplx l = Ls[r][c];
+        acc = mk(acc.x - (l.x * x[c].x - l.y * x[c].y), acc.y - (l.x * x[c].y + l.y * x[c].x));
+      }
+      x[r] = acc;
+    }
+#pragma unroll
+    for (int r = 0; r < TI_B; ++r) Dinv[((int64_t)i * TI_B + r) * TI_B + t] = x[r];
+  } else if (t < 2 * TI_B && coef != nullptr) {
+    const int q = r0 + t - TI_B;
+    if (q < n) {
+      const int8_t tg = tags[q];
+      if (tg == 1) {
+        coef[3 * q] = x_div_np(mk(1.0, 0.0), F[(int64_t)q * n + q]);
+      } else if (tg == 2) {
+        const cplx a = F[(int64_t)q * n + q], b = F[(int64_t)(q + 1) * n + q], c = F[(int64_t)(q + 1) * n + q + 1];
+        const cplx det = c_sub(c_mul(a, c), c_mul(b, b));
+        const cplx inv = x_div_np(mk(1.0, 0.0), det);
+        coef[3 * q] = c_mul(c, inv);
+        coef[3 * q + 1] = c_mul(mk(-b.x, -b.y), inv);
+        coef[3 * q + 2] = c_mul(a, inv);
+      }
+    }
+  }
+}
+
+constexpr int TI_NMAX = 256;
+constexpr size_t kTiSmem = sizeof(cplx) * ((size_t)TI_NMAX * TI_B + 2 * (size_t)TI_B * TI_NMAX + TI_B * TI_B);
+
+__device__ __forceinline__ void ti_cp16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+__global__ void __launch_bounds__(256) tri_inv_cols16(const cplx* __restrict__ F, const int64_t* __restrict__ perm,
+                                                      const int8_t* __restrict__ tags, const cplx* __restrict__ Dinv,
+                                                      cplx* Binv, int n) {
+  extern __shared__ __align__(16) unsigned char ti_smem[];
+  cplx* X = reinterpret_cast<cplx*>(ti_smem);                 // rows 16k.. of block column k, 16 wide
+  cplx* Lb = X + (size_t)TI_NMAX * TI_B;                      // 2 x [16][16(i-k)] L row panels
+  cplx* S = Lb + 2 * (size_t)TI_B * TI_NMAX;                  // 16 x 16
+  const int k = blockIdx.x, nbk = (n + TI_B - 1) / TI_B, c0 = k * TI_B;
+  const int tid = threadIdx.x, r = tid >> 4, cc = tid & 15;
+  auto fetch = [&](int i, int buf) {      // L rows [16i, 16i+16) x cols [c0, 16i) -> Lb[buf]
+    const int w = TI_B * (i - k), rows = min(TI_B, n - i * TI_B);
+    cplx* dst = Lb + (size_t)buf * TI_B * TI_NMAX;
+    for (int e = tid; e < rows * w; e += 256) {
+      const int rr = e / w, m = e - rr * w;
+      ti_cp16(dst + rr * w + m, F + (int64_t)(i * TI_B + rr) * n + c0 + m);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  if (k + 1 < nbk) fetch(k + 1, 0);
+  X[r * TI_B + cc] = (c0 + r < n && c0 + cc < n) ? Dinv[((int64_t)k * TI_B + r) * TI_B + cc] : mk(0.0, 0.0);
+  for (int i = k + 1; i < nbk; ++i) {
+    const int buf = (i - k - 1) & 1, w = TI_B * (i - k), rows = min(TI_B, n - i * TI_B);
+    if (i + 1 < nbk) {
+      fetch(i + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const cplx* Lr = Lb + (size_t)buf * TI_B * TI_NMAX;
+    // S = L_i,[k,i) X_[k,i),k  (two partial sums shorten the dependent chain)
+    cplx a0 = mk(0.0, 0.0), a1 = mk(0.0, 0.0);
+    if (r < rows) {
+      const bool zr = r == 0 && tags[i * TI_B - 1] == 2;     // L[16i, 16i-1] of a 2x2 pivot
+      for (int m = 0; m < w; m += 2) {
+        const cplx l0 = Lr[r * w + m];                        // m even: never column w-1
+        const cplx x0 = X[m * TI_B + cc];
+        a0 = mk(a0.x + (l0.x * x0.x - l0.y * x0.y), a0.y + (l0.x * x0.y + l0.y * x0.x));
+        cplx l1 = Lr[r * w + m + 1];
+        if (zr && m + 1 == w - 1) l1 = mk(0.0, 0.0);
+        const cplx x1 = X[(m + 1) * TI_B + cc];
+        a1 = mk(a1.x + (l1.x * x1.x - l1.y * x1.y), a1.y + (l1.x * x1.y + l1.y * x1.x));
+      }
+    }
+    S[r * TI_B + cc] = c_add(a0, a1);
+    __syncthreads();
+    // X_ik = -Dinv_i S
+    cplx acc = mk(0.0, 0.0);
+    const cplx* Di = Dinv + (int64_t)i * TI_B * TI_B;
+#pragma unroll
+    for (int c = 0; c < TI_B; ++c) {
+      const cplx d = Di[r * TI_B + c], sv = S[c * TI_B + cc];
+      acc = mk(acc.x + (d.x * sv.x - d.y * sv.y), acc.y + (d.x * sv.y + d.y * sv.x));
+    }
+    X[(w + r) * TI_B + cc] = (r < rows) ? mk(-acc.x, -acc.y) : mk(0.0, 0.0);
+    __syncthreads();
+  }
+  // Binv[:, perm[q]] = X[:, q] (zeros above the block column)
+  for (int e = tid; e < n * TI_B; e += 256) {
+    const int row = e / TI_B, q = c0 + (e % TI_B);
+    if (q >= n) continue;
+    Binv[(int64_t)row * n + perm[q]] = (row < c0) ? mk(0.0, 0.0) : X[(row - c0) * TI_B + (q - c0)];
+  }
+}
+
+}  // namespace d3m
+
+// blocked L^-1 P + D^-1 coefficients for n <= 256 (-22 above)
+extern "C" int d3m_tri_inv_blocked_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef,
+                                          int n, void* stream) {
+  using namespace d3m;
+  if (n <= 0) return 0;
+  if (n > TI_NMAX) return -22;
+  static cplx* dinv = nullptr;
+  static bool cfg = false;
+  if (!dinv) {
+    if (cudaMalloc(&dinv, sizeof(cplx) * TI_NMAX * TI_B) != cudaSuccess) return 2;
+  }
+  if (!cfg) {
+    cudaFuncSetAttribute(tri_inv_cols16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTiSmem);
+    cfg = true;
+  }
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  const int nbk = (n + TI_B - 1) / TI_B;
+  auto Fp = static_cast<const cplx*>(F);
+  auto tp = static_cast<const int8_t*>(tags);
+  tri_inv_diag16<<<nbk, 64, 0, s>>>(Fp, tp, dinv, static_cast<cplx*>(coef), n);
+  tri_inv_cols16<<<nbk, 256, kTiSmem, s>>>(Fp, static_cast<const int64_t*>(perm), tp, dinv, static_cast<cplx*>(Binv), n);
+  return (int)cudaGetLastError();
+}
+
 // warp-per-column inverse for n <= 512 (returns -22 above: use d3m_tri_inv_launch)
 extern "C" int d3m_tri_inv_warp_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef,
                                        int n, void* stream) {
