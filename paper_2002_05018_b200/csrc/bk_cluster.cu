@@ -666,11 +666,20 @@ static int bkc_launch(BkArgs* a, int batch, cudaStream_t s) {
 
 // Bit-exact BK of `batch` blocks, one cluster each.  Returns -22 when the
 // block does not fit the cluster's shared memory (caller falls back).
+extern "C" int d3m_bk_cluster_launch_cs(d3m::BkArgs* a, int batch, int cs, void* stream);
+
 extern "C" int d3m_bk_cluster_launch(d3m::BkArgs* a, int batch, void* stream) {
+  return d3m_bk_cluster_launch_cs(a, batch, 0, stream);
+}
+
+// cs: cluster size (2, 4 or 8); 0 = D3M_BKC_CS or 8
+extern "C" int d3m_bk_cluster_launch_cs(d3m::BkArgs* a, int batch, int cs, void* stream) {
   using namespace d3m;
   if (batch <= 0 || a->n <= 0) return 0;
-  int cs = 8;
-  if (const char* env = getenv("D3M_BKC_CS")) cs = atoi(env);
+  if (cs == 0) {
+    cs = 8;
+    if (const char* env = getenv("D3M_BKC_CS")) cs = atoi(env);
+  }
   auto s = reinterpret_cast<cudaStream_t>(stream);
   int rc = -22;
   switch (cs) {

@@ -444,6 +444,11 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
   // diagonal BK kernel for supernodes > kExactBkMax: 0 cluster (default), 1 blocked
   const char* dbk = getenv("D3M_DIAG_BK");
   const int diag_bk_mode = (dbk && dbk[0] == 'b') ? 1 : 0;
+  // rest-update tiles above which a column's diagonal BK runs on a 4-CTA cluster (D3M_BKC4_TILES)
+  static const int64_t bkc4_tiles = [] {
+    const char* e = getenv("D3M_BKC4_TILES");
+    return e ? (int64_t)atoll(e) : (int64_t)8000;
+  }();
   // Streams: the caller's stream hands over to a high-priority critical
   // stream (BK -> L^-1 -> panel GEMM -> D^-1 -> next-column update) and a
   // low-priority bulk stream (the rest of each column's trailing update).
@@ -509,7 +514,10 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
       D3M_TRY(launch(kClsBk, s0, [&] {
         if (nj <= kExactBkMax) return d3m_bk_launch(&a, 1, s0);
         if (diag_bk_mode != 1) {          // cluster-resident exact BK (bk_cluster.cu)
-          const int rc = d3m_bk_cluster_launch(&a, 1, s0);
+          // 4-CTA clusters while the column's bulk update is long enough to hide the slower BK
+          // (frees 4 SMs for the update GEMMs), 8-CTA clusters on the exposed chain at the ends
+          const int cs = (lookahead && h_tiles_rest[j] >= bkc4_tiles) ? 4 : 0;
+          const int rc = d3m_bk_cluster_launch_cs(&a, 1, cs, s0);
           if (rc != -22) return rc;
         }
         const int rc = d3m_bk_blocked_launch(&a, 1, s0);
