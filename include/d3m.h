@@ -193,6 +193,13 @@ int d3m_block_solve_dataflow(int nb, const void* d_plan, const void* d_items, in
                              const void* d_pool, const void* d_binv, const void* d_tags, void* d_b, void* d_u,
                              void* d_x, void* d_part, int nrhs, void* stream);
 
+/* Rows where each coupling block has entries (ABI v7): D is B x n x m
+ * complex128 (device); flag: B*n int8 scratch; idx: B*n int64, block b's
+ * nonzero rows ascending in idx[b*n ...], -1 after count[b] (int32 x B).
+ * Feeds the row list of d3m_schur_reduce_batched (D^T X over those rows,
+ * subdomain.py:181). */
+int d3m_nonzero_rows(int B, int n, int m, const void* D, void* flag, void* idx, void* count, void* stream);
+
 /* Block residual r -= K x for iterative refinement of block_solve (ABI v7).
  * K's stored blocks (original numbering) stay in device buffers h_abase[l];
  * x and r are N x cols in plan-order rows.  Launch l is a grouped GEMM

@@ -28,6 +28,7 @@ _SIGNATURES = {
     "d3m_zgemm_grouped": [I32, I32, P, P, P, P, I32, P, P],
     "d3m_gemm_set_form": [I32],
     "d3m_block_residual": [I32, P, P, P, P, P, P, P, P, P],
+    "d3m_nonzero_rows": [I32, I32, I32, P, P, P, P, P],
     "d3m_block_solve_dataflow": [I32, P, P, I32, P, P, P, I32, P, P, P, P, P, P, P, P, I32, P],
     "d3m_schur_reduce_batched": [I32, I32, I32, I32, P, P, P, F64] + [P] * 14 + [P, I32, P, I32, P],
     "d3m_block_copy": [P, P, P, I32, I64, P],

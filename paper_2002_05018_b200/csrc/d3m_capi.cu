@@ -402,6 +402,12 @@ int d3m_block_residual(int nlaunch, const int32_t* h_ta, const int32_t* h_ntasks
   return 0;
 }
 
+int d3m_nonzero_rows(int B, int n, int m, const void* D, void* flag, void* idx, void* count, void* stream) {
+  if (B < 0 || n < 0 || m < 0) return fail(-22, "d3m_nonzero_rows: bad shape");
+  D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_nonzero_rows_launch(B, n, m, D, flag, idx, count, stream); }));
+  return 0;
+}
+
 int d3m_gather_rows(const void* src, const void* idx, void* out, int64_t nrows, int cols, void* stream) {
   D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_gather_index_launch(src, idx, out, nrows, cols, stream); }));
   return 0;

@@ -80,6 +80,7 @@ int d3m_tri_inv_launch(const void* F, int64_t stride_f, const void* perm, int64_
                        int64_t stride_t, void* Binv, int64_t stride_b, int n, int batch, void* stream);
 int d3m_dinv_rows_launch(const void* X, void* P, int64_t R, int n, const void* F, const void* tags, void* stream);
 int d3m_dinv_left_copy_launch(const void* Z, void* U, int n, int m, const void* F, const void* tags, void* stream);
+int d3m_nonzero_rows_launch(int B, int n, int m, const void* D, void* flag, void* idx, void* count, void* stream);
 int d3m_tri_inv_blocked_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef, int n,
                                void* stream);
 int d3m_tri_inv_warp_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef, int n,

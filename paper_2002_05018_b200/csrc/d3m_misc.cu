@@ -216,3 +216,71 @@ extern "C" int d3m_sym_exact_launch(const void* pool, const void* off, const voi
       static_cast<int*>(flag));
   return (int)cudaGetLastError();
 }
+
+// Nonzero rows of each coupling block D_b (B x n x m, row-major): one warp per
+// row sets flag[b*n + i] when any entry is nonzero; one CTA per block then
+// compacts the flagged rows in ascending order into idx[b*n + 0..count[b])
+// (the rest -1).  Replaces the row scan of D^T X over the rows where D has
+// entries (subdomain.py:181's product, ABI v3 row list).
+__global__ void nz_flag_kernel(const double2* __restrict__ D, int64_t rows_total, int m, int8_t* flag) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows_total) return;
+  const double2* p = D + row * m;
+  bool nz = false;
+  for (int c0 = 0; c0 < m; c0 += 32) {        // warp-uniform trip count; stop at the first nonzero
+    const int c = c0 + lane;
+    if (c < m) {
+      const double2 v = p[c];
+      nz = v.x != 0.0 || v.y != 0.0;
+    }
+    if (__any_sync(0xffffffffu, nz)) break;
+  }
+  nz = __any_sync(0xffffffffu, nz);
+  if (lane == 0) flag[row] = nz ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(1024) nz_compact_kernel(const int8_t* __restrict__ flag, int n, int64_t* idx,
+                                                          int* count) {
+  __shared__ int wsum[32];
+  __shared__ int base;
+  const int b = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int8_t* f = flag + (int64_t)b * n;
+  int64_t* out = idx + (int64_t)b * n;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < n; c0 += 1024) {
+    const int i = c0 + threadIdx.x;
+    const int v = (i < n && f[i]) ? 1 : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, v);
+    const int pre = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < warp; ++w) off += wsum[w];
+    const int b0 = base;
+    if (v) out[b0 + off + pre] = i;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w = 0; w < 32; ++w) tot += wsum[w];
+      base = b0 + tot;
+    }
+    __syncthreads();
+  }
+  const int cnt = base;
+  for (int i = cnt + threadIdx.x; i < n; i += 1024) out[i] = -1;
+  if (threadIdx.x == 0) count[b] = cnt;
+}
+
+extern "C" int d3m_nonzero_rows_launch(int B, int n, int m, const void* D, void* flag, void* idx, void* count,
+                                       void* stream) {
+  if (B <= 0 || n <= 0) return 0;
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t rows = (int64_t)B * n;
+  nz_flag_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(static_cast<const double2*>(D), rows, m,
+                                                             static_cast<int8_t*>(flag));
+  nz_compact_kernel<<<B, 1024, 0, s>>>(static_cast<const int8_t*>(flag), n, static_cast<int64_t*>(idx),
+                                       static_cast<int*>(count));
+  return (int)cudaGetLastError();
+}

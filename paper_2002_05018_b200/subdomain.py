@@ -308,20 +308,20 @@ def _nonzero_rows(D, n):
     """Rows where each domain's coupling block D_d (the filled device batch
     B x n x m) has nonzeros, ascending and -1 padded to the batch maximum,
     for D^T X over those rows only; (None, 0) when the couplings are dense
-    enough that the full product is as cheap.  One pass over D, one sync."""
+    enough that the full product is as cheap.  One device pass over D
+    (d3m_nonzero_rows), one sync for the counts."""
     t = require_cuda()
-    B = D.shape[0]
-    if D.shape[2] == 0 or n == 0:
+    B, m = int(D.shape[0]), int(D.shape[2])
+    if m == 0 or n == 0 or B == 0:
         return None, 0
-    nz = t.view_as_real(D).reshape(B, n, -1).ne(0).any(dim=2)             # B x n
-    nrows = int(nz.sum(dim=1).max().item())
+    flag = t.empty(B * n, dtype=t.int8, device="cuda")
+    idx = t.empty((B, n), dtype=t.int64, device="cuda")
+    cnt = t.empty(B, dtype=t.int32, device="cuda")
+    _lib.call("d3m_nonzero_rows", B, n, m, _P(D), _P(flag), _P(idx), _P(cnt), stream_ptr())
+    nrows = int(cnt.cpu().numpy().max())
     if nrows == 0 or nrows > 0.6 * n:
         return None, 0
-    ar = t.arange(n, device=D.device, dtype=t.int64)
-    key = t.where(nz, ar, ar + n)                                          # nonzero rows first, ascending
-    idx = t.sort(key, dim=1).values[:, :nrows]
-    idx = t.where(idx < n, idx, t.full_like(idx, -1)).contiguous()
-    return idx, nrows
+    return idx[:, :nrows].contiguous(), nrows
 
 
 def _fill(dst, src, shape):
