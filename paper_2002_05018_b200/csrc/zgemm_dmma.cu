@@ -54,6 +54,28 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// CTA-scope mbarriers for the 3M kernel's ring (no CTA-wide barrier per k-slice)
+__device__ __forceinline__ unsigned smaddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smaddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smaddr(b)) : "memory");
+}
+// arrives once this thread's earlier cp.async copies have landed (count pre-set by mb_init)
+__device__ __forceinline__ void mb_cp_arrive(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smaddr(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, unsigned parity) {
+  for (unsigned it = 0;; ++it) {
+    unsigned ok;
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok) : "r"(smaddr(b)), "r"(parity) : "memory");
+    if (ok) return;
+    if (it > (1u << 28)) __trap();
+  }
+}
+
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(c0), "+d"(c1)
@@ -121,7 +143,7 @@ __device__ __forceinline__ int find_task(const GemmTask* __restrict__ tasks, int
 // is normwise stable (each entry's error is bounded by eps times
 // (|a_re|+|a_im|)(|b_re|+|b_im|) summed over k, against the 4M product's
 // eps |a||b|), so the results stay within rounding of the reference's ZGEMM.
-template <bool TA, bool TB, bool G3>
+template <bool TA, bool TB, bool G3, bool MB = false>
 __global__ void __launch_bounds__(G3 ? 2 * NTHREADS : NTHREADS, 2)
 zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bbase, cplx* Cbase,
                      const GemmTask* __restrict__ tasks, int ntasks, unsigned long long* tmax) {
@@ -165,13 +187,30 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
           acc_x[i][j][1] = 0.0;
 
   const int ktiles = (K + BKC - 1) / BKC;
+  // MB: the ring is tracked by mbarriers -- full[s] completes when every
+  // thread's copies of the stage in slot s have landed, empty[s] when all
+  // warps have consumed it -- so a warp waits only for the data it reads and,
+  // before refilling a slot, for the slowest warp of the PREVIOUS k-slice
+  // (instead of a CTA barrier at every k-slice).
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  if constexpr (MB) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s) {
+        mb_init(&full_bar[s], NT);
+        mb_init(&empty_bar[s], NT / 32);
+      }
+    }
+    __syncthreads();
+  }
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < ktiles) {
       load_tile<TA, NT>(st[s].a, A, tk.lda, m0, M, s * BKC, K);
       load_tile<TB, NT>(st[s].b, B, tk.ldb, n0, N, s * BKC, K);
+      if constexpr (MB) mb_cp_arrive(&full_bar[s]);
     }
-    cp_commit();
+    if constexpr (!MB) cp_commit();
   }
   // C prefetch (C -= / += AB targets without mirrored writes): the last STAGES-1 iterations issue
   // no A/B loads, so each frees one ring slot; chunk c of the C tile (rows
@@ -182,9 +221,13 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
   const bool cpre = (!sym || (tk.flags & kGemmLowerOnly)) && mode != kGemmStore && ktiles >= STAGES;
 
   for (int kt = 0; kt < ktiles; ++kt) {
-    cp_wait<STAGES - 2>();
-    __syncthreads();
-    {
+    if constexpr (MB) {
+      mb_wait(&full_bar[kt % STAGES], (unsigned)(kt / STAGES) & 1u);
+    } else {
+      cp_wait<STAGES - 2>();
+      __syncthreads();
+    }
+    if constexpr (!MB) {
       const int nk = kt + STAGES - 1;
       if (nk < ktiles) {
         const int slot = nk % STAGES;
@@ -228,6 +271,30 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
           for (int j = 0; j < WJ; ++j) dmma(acc_x[i][j][0], acc_x[i][j][1], asum, bsum[j]);
         }
       }
+      if constexpr (MB) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mb_arrive(&empty_bar[slot]);
+        const int nk = kt + STAGES - 1;
+        const int slot2 = nk % STAGES;
+        if (nk < ktiles || cpre) {
+          // slot2 last held stage nk - STAGES (= kt - 1): wait until every warp consumed it
+          if (nk >= STAGES) mb_wait(&empty_bar[slot2], (unsigned)((nk - STAGES) / STAGES) & 1u);
+          if (nk < ktiles) {
+            load_tile<TA, NT>(st[slot2].a, A, tk.lda, m0, M, nk * BKC, K);
+            load_tile<TB, NT>(st[slot2].b, B, tk.ldb, n0, N, nk * BKC, K);
+            mb_cp_arrive(&full_bar[slot2]);
+          } else {
+            const int ch = nk - ktiles, r0 = ch * CP_ROWS;
+            const int rows = min(CP_ROWS, BM - r0);
+            cplx* dst = reinterpret_cast<cplx*>(&st[slot2]);
+            for (int e = threadIdx.x; e < rows * BN; e += NT) {
+              const int r = e / BN, c = e - r * BN;
+              const bool ok = m0 + r0 + r < M && n0 + c < N;
+              cp_async16(dst + r * CP_PITCH + c, ok ? C + (int64_t)(m0 + r0 + r) * tk.ldc + n0 + c : C, ok);
+            }
+          }
+        }
+      }
     } else {
 #pragma unroll
       for (int kk = 0; kk < BKC / 4; ++kk) {
@@ -266,6 +333,7 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
       }
     }
   }
+  if constexpr (MB) cp_commit();        // the C chunks of the MB path are not in a committed group yet
   cp_wait<0>();
   if constexpr (G3) {
 #pragma unroll
@@ -513,17 +581,17 @@ constexpr size_t kGemmSmem = sizeof(cplx) * STAGES * (BM + BN) * PITCH;
 
 static unsigned long long* g_tmax = nullptr;   // set per launch by d3m_gemm_launch_tm
 
-template <bool TA, bool TB, bool G3>
+template <bool TA, bool TB, bool G3, bool MB = false>
 static int launch_g(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
                     cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(zgemm_grouped_kernel<TA, TB, G3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(zgemm_grouped_kernel<TA, TB, G3, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kGemmSmem);
     configured = true;
   }
-  zgemm_grouped_kernel<TA, TB, G3><<<ntiles, G3 ? 2 * NTHREADS : NTHREADS, kGemmSmem, s>>>(A, B, C, tasks,
-                                                                                           ntasks, g_tmax);
+  zgemm_grouped_kernel<TA, TB, G3, MB><<<ntiles, G3 ? 2 * NTHREADS : NTHREADS, kGemmSmem, s>>>(A, B, C, tasks,
+                                                                                               ntasks, g_tmax);
   return (int)cudaGetLastError();
 }
 
@@ -541,8 +609,10 @@ static bool use_3m() {
 template <bool TA, bool TB>
 static int launch_t(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
                     cudaStream_t s) {
-  return use_3m() ? launch_g<TA, TB, true>(A, B, C, tasks, ntasks, ntiles, s)
-                  : launch_g<TA, TB, false>(A, B, C, tasks, ntasks, ntiles, s);
+  static const int mb = [] { const char* e = getenv("D3M_GEMM_MB"); return e ? atoi(e) : 1; }();
+  if (!use_3m()) return launch_g<TA, TB, false>(A, B, C, tasks, ntasks, ntiles, s);
+  return mb ? launch_g<TA, TB, true, true>(A, B, C, tasks, ntasks, ntiles, s)
+            : launch_g<TA, TB, true, false>(A, B, C, tasks, ntasks, ntiles, s);
 }
 
 }  // namespace d3m
