@@ -47,8 +47,8 @@ __device__ __forceinline__ void sn_dmma(double& c0, double& c1, double a, double
 
 // one warp stages A(16 rows x 8 k) and B(8 k x 16 RHS): 4 + 4 chunks per lane
 template <bool TA>
-__device__ __forceinline__ void sn_load(SnWarpSmem& S, int st, const cplx* A, int lda, int M, const cplx* B, int ldb,
-                                        const int64_t* bmap, int N, int m0, int k0, int kend, int lane) {
+__device__ __forceinline__ void sn_load_a(SnWarpSmem& S, int st, const cplx* A, int lda, int M, int m0, int k0,
+                                          int kend, int lane) {
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     const int e = p * 32 + lane;
@@ -59,6 +59,9 @@ __device__ __forceinline__ void sn_load(SnWarpSmem& S, int st, const cplx* A, in
     const cplx* g = TA ? A + (int64_t)(k0 + k) * lda + m0 + r : A + (int64_t)(m0 + r) * lda + k0 + k;
     sn_cp16(&S.A[st][r][k], ok ? g : A, ok);
   }
+}
+__device__ __forceinline__ void sn_load_b(SnWarpSmem& S, int st, const cplx* B, int ldb, const int64_t* bmap, int N,
+                                          int k0, int kend, int lane) {
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     const int e = p * 32 + lane, k = e >> 4, c = e & 15;
@@ -67,6 +70,16 @@ __device__ __forceinline__ void sn_load(SnWarpSmem& S, int st, const cplx* A, in
     sn_cp16(&S.B[st][k][c], ok ? B + row * ldb + c : B, ok);
   }
 }
+template <bool TA>
+__device__ __forceinline__ void sn_load(SnWarpSmem& S, int st, const cplx* A, int lda, int M, const cplx* B, int ldb,
+                                        const int64_t* bmap, int N, int m0, int k0, int kend, int lane) {
+  sn_load_a<TA>(S, st, A, lda, M, m0, k0, kend, lane);
+  sn_load_b(S, st, B, ldb, bmap, N, k0, kend, lane);
+}
+
+struct SnNoWait {
+  __device__ void operator()() const {}
+};
 
 // mode: 0 store, 1 subtract, 2 partial (part[(chunk * M + r) * N + c])
 // CTA: 16 rows x 16 RHS over K rows [kbeg, kbeg + 256 * passes) of its chunk;
@@ -74,11 +87,15 @@ __device__ __forceinline__ void sn_load(SnWarpSmem& S, int st, const cplx* A, in
 // in warp order at the end (fixed order, independent of N).
 // One CTA tile (rows [m0, m0+16), K rows [kbeg, kend) of chunk `chunk`);
 // shared by the per-product kernel below and the persistent block solve.
-template <bool TA>
+// `wait` runs between the prefetch of the first stages' A (factor data, never
+// produced in-kernel) and the loads of B (the vectors another CTA may still
+// be producing): the dataflow solve waits for its inputs there, so the A
+// latency overlaps the dependency wait.  It is called by every thread.
+template <bool TA, class W = SnNoWait>
 __device__ __forceinline__ void sn_tile(const cplx* __restrict__ A, int lda, int M, const cplx* __restrict__ B,
                                         int ldb, const int64_t* __restrict__ bmap, int N, cplx* C, int ldc,
                                         const int64_t* __restrict__ cmap, int mode, int m0, int chunk, int kbeg,
-                                        int kend, unsigned char* sn_smem) {
+                                        int kend, unsigned char* sn_smem, W wait = W()) {
   SnWarpSmem* ws = reinterpret_cast<SnWarpSmem*>(sn_smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int fr = lane >> 2, fc = lane & 3;
@@ -94,9 +111,16 @@ __device__ __forceinline__ void sn_tile(const cplx* __restrict__ A, int lda, int
   const int my_slices = nslice > warp ? (nslice - warp + SN_NW - 1) / SN_NW : 0;
   const int ktiles = my_slices * tiles_per_slice;
   auto tile_k0 = [&](int t) { return kbeg + ((t / tiles_per_slice) * SN_NW + warp) * SN_KW + (t % tiles_per_slice) * SN_BK; };
+  // A of stages 0..ST-2 as one group, then B of each stage as its own group:
+  // with ST-2 groups in flight the main loop's waits see A_s and B_s landed
+#pragma unroll
+  for (int s = 0; s < SN_ST - 1; ++s)
+    if (s < ktiles) sn_load_a<TA>(S, s, A, lda, M, m0, tile_k0(s), kend, lane);
+  asm volatile("cp.async.commit_group;\n" ::);
+  wait();
 #pragma unroll
   for (int s = 0; s < SN_ST - 1; ++s) {
-    if (s < ktiles) sn_load<TA>(S, s, A, lda, M, B, ldb, bmap, N, m0, tile_k0(s), kend, lane);
+    if (s < ktiles) sn_load_b(S, s, B, ldb, bmap, N, tile_k0(s), kend, lane);
     asm volatile("cp.async.commit_group;\n" ::);
   }
   for (int kt = 0; kt < ktiles; ++kt) {
@@ -334,26 +358,31 @@ block_solve_dataflow(SolvePlanDev p, const FlowItem* __restrict__ items, int nit
     if (idx >= nitems) break;
     const FlowItem it = items[idx];
     if (trace && threadIdx.x == 0) trace[3 * (int64_t)idx] = gtimer();
-    if (threadIdx.x == 0) {
-      for (int d = 0; d < it.dep_cnt; ++d) {
-        const int2 dp = deps[it.dep_off + d];
-        for (unsigned spin = 0; ld_acquire(cnt + dp.x) < dp.y; ++spin) {
-          if (spin > (1u << 28)) __trap();
-          if (spin > 64) __nanosleep(32);
+    // inputs ready: thread 0 polls the item's counters, then a CTA barrier;
+    // the tile items run it inside sn_tile, after their A prefetch
+    auto waitdeps = [&]() {
+      if (threadIdx.x == 0) {
+        for (int d = 0; d < it.dep_cnt; ++d) {
+          const int2 dp = deps[it.dep_off + d];
+          for (unsigned spin = 0; ld_acquire(cnt + dp.x) < dp.y; ++spin) {
+            if (spin > (1u << 28)) __trap();
+            if (spin > 64) __nanosleep(32);
+          }
         }
+        if (trace) trace[3 * (int64_t)idx + 1] = gtimer();
       }
-    }
-    __syncthreads();
-    if (trace && threadIdx.x == 0) trace[3 * (int64_t)idx + 1] = gtimer();
+      __syncthreads();
+    };
     const int j = it.j;
     const int nj = (int)p.sizes[j];
     const int64_t ro = p.row_off[j];
     switch (it.type) {
       case kFA:
         sn_tile<false>(p.binv + p.binv_off[j], nj, nj, p.b + ro * ld + p.c0, ld, nullptr, N, p.x + ro * ld + p.c0, ld,
-                       nullptr, 0, it.p0 * SN_BM, 0, 0, nj, sn_smem);
+                       nullptr, 0, it.p0 * SN_BM, 0, 0, nj, sn_smem, waitdeps);
         break;
       case kFD: {      // rows [p0, p1) (a 2x2 pair belongs to the piece of its first row)
+        waitdeps();
         const cplx* F = p.pool + p.diag_off[j];
         const int8_t* tg = p.tags + p.piv_off[j];
         const cplx* z = p.x + ro * ld + p.c0;
@@ -374,15 +403,16 @@ block_solve_dataflow(SolvePlanDev p, const FlowItem* __restrict__ items, int nit
       }
       case kFB:
         sn_tile<false>(p.pool + p.panel_off[j] + (int64_t)it.p0 * nj, nj, it.p1, p.x + ro * ld + p.c0, ld, nullptr, N,
-                       p.b + p.c0, ld, p.gidx + p.gptr[j] + it.p0, 1, 0, 0, 0, nj, sn_smem);
+                       p.b + p.c0, ld, p.gidx + p.gptr[j] + it.p0, 1, 0, 0, 0, nj, sn_smem, waitdeps);
         break;
       case kBC: {
         const int R = (int)p.panel_rows[j], ch = it.p0;
         sn_tile<true>(p.pool + p.panel_off[j], nj, nj, p.x + p.c0, ld, p.gidx + p.gptr[j], N, p.part + part_off[j], N,
-                      nullptr, 2, it.p1 * SN_BM, ch, ch * KCH, min(R, ch * KCH + KCH), sn_smem);
+                      nullptr, 2, it.p1 * SN_BM, ch, ch * KCH, min(R, ch * KCH + KCH), sn_smem, waitdeps);
         break;
       }
       case kBR: {      // rows [p0, p1); partials loaded 16 chunks ahead, summed in chunk order
+        waitdeps();
         const int R = (int)p.panel_rows[j];
         const int nch = R > 0 ? (R + KCH - 1) / KCH : 0;
         const int64_t len = (int64_t)nj * N;
@@ -407,7 +437,7 @@ block_solve_dataflow(SolvePlanDev p, const FlowItem* __restrict__ items, int nit
       }
       default:   // kBE
         sn_tile<true>(p.binv + p.binv_off[j], nj, nj, p.u + ro * ld + p.c0, ld, nullptr, N, p.x + ro * ld + p.c0, ld,
-                      nullptr, 0, it.p0 * SN_BM, 0, 0, nj, sn_smem);
+                      nullptr, 0, it.p0 * SN_BM, 0, 0, nj, sn_smem, waitdeps);
         break;
     }
     __threadfence();
