@@ -60,6 +60,8 @@ COPY_TASK = np.dtype([("src_off", "<i8"), ("dst_off", "<i8"), ("rows", "<i4"), (
 assert COPY_TASK.itemsize == 40
 
 GEMM_SUB, GEMM_STORE, GEMM_ADD, GEMM_SYM = 0, 1, 2, 4
+GEMM_TRIGATHER = 32       # csrc/d3m_gemm.h kGemmTriGather
+TRSM_TRI_MAX = 512        # d3m_capi.cu kTrsmTriMax
 COPY_STORE, COPY_ADD, COPY_ZERO_ADD = 0, 1, 2
 GEMM_BM = GEMM_BN = 64
 PANEL_BK_MIN = 512        # d3m_capi.cu kPanelBkMin

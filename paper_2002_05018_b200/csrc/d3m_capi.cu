@@ -43,6 +43,9 @@ int fail(int code, const char* what) {
 // is on, each launch is bracketed by a pair of events on its own stream and
 // the elapsed times are summed per class at d3m_counters_read().
 enum { kClsBk = 0, kClsTrsm = 1, kClsGemm = 2, kClsSolve = 3, kClsMisc = 4, kNumCls = 5 };
+// supernodes up to this order get the unpermuted L^-1 from the triangular-inverse kernels and the
+// gathered / triangular panel TRSM (factor.py sets kGemmTriGather on exactly these TRSM tasks)
+constexpr int kTrsmTriMax = 512;
 std::atomic<long long> g_launches{0};
 bool g_timing = false;
 struct TimedRec { int cls; cudaEvent_t a, b; };
@@ -493,6 +496,23 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
     if (cudaMalloc(&coef_buf, coef_bytes) != cudaSuccess) return fail(-12, "d3m_block_ldlt_exec: coef alloc");
     coef_cap = coef_bytes;
   }
+  // unpermuted L_jj^-1 of every column (same layout as binv), for the triangular panel TRSM
+  static cplx* linv = nullptr;
+  static int64_t linv_cap = 0;
+  static const bool trsm_tri = [] { const char* e = getenv("D3M_TRSM_TRI"); return !(e && e[0] == '0'); }();
+  cplx* linv_use = nullptr;
+  if (trsm_tri) {
+    const int64_t need = h_binv_off[nb];
+    if (need > linv_cap) {
+      if (linv) cudaFree(linv);
+      linv = nullptr;
+      linv_cap = 0;
+      if (cudaMalloc(&linv, sizeof(cplx) * (size_t)std::max<int64_t>(need, 1)) != cudaSuccess)
+        return fail(-12, "d3m_block_ldlt_exec: linv alloc");
+      linv_cap = need;
+    }
+    linv_use = linv;
+  }
   bool rest_pending = false;
   for (int j = 0; j < nb; ++j) {
     // blocks of K still being uploaded: column j waits for the chunks it is
@@ -535,14 +555,19 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
         // D3M_TRI_INV=w forces the warp kernel (A/B measurements)
         static const char* ti_env = getenv("D3M_TRI_INV");
         int rc = -22;
-        if (!(ti_env && ti_env[0] == 'w')) rc = d3m_tri_inv_blocked_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, s0);
-        if (rc == -22) rc = d3m_tri_inv_warp_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, s0);
+        cplx* lj = linv_use ? linv_use + h_binv_off[j] : nullptr;   // unpermuted L^-1 for the panel TRSM
+        if (!(ti_env && ti_env[0] == 'w')) rc = d3m_tri_inv_blocked_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, lj, s0);
+        if (rc == -22) rc = d3m_tri_inv_warp_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, s0, lj);
         return rc == -22 ? d3m_tri_inv_launch(diag, 0, perm, 0, tags, 0, binv + h_binv_off[j], 0, nj, 1, s0) : rc;
       }));
     }
     if (R > 0) {
       // X_ij = K_ij P^T L_jj^-T = panel * Binv^T on DMMA, then L_ij = X_ij D_jj^-1
       D3M_TRY(launch(kClsTrsm, s0, [&] {
+        // nj <= kTrsmTriMax: X = (K P^T) L^-T with the column gather and the triangular K cut
+        // (the task carries kGemmTriGather, factor.py); else X = K Binv^T
+        if (linv_use && nj <= kTrsmTriMax)
+          return d3m_gemm_launch_perm(pool, linv_use, xbuf, ttasks + j, 1, (int)h_tiles_trsm[j], d_perm, s0);
         return d3m_gemm_launch(0, 0, pool, binv, xbuf, ttasks + j, 1, (int)h_tiles_trsm[j], s0);
       }));
       D3M_TRY(launch(kClsTrsm, s0, [&] {

@@ -12,6 +12,9 @@ enum : int32_t {
   kGemmSym = 4,        // symmetric diagonal target: lower tiles, mirrored write
   kGemmLowerOnly = 8,  // with kGemmSym: write the lower triangle only (no mirror)
   kGemmTrackMax = 16,  // atomically max |C|^2 of written entries into tmax[pad_]
+  kGemmTriGather = 32, // A(r, k) = A[r*lda + gperm[pad_ + k]] (column gather) and B lower
+                       // triangular (B_eff[c][k] = 0 for k > c): output column tile tn
+                       // needs k < (tn + 1) * 64 only (the panel TRSM X = K P^T L^-T)
 };
 
 // One GEMM of a grouped launch.  Offsets are in complex elements relative to

@@ -82,9 +82,11 @@ int d3m_dinv_rows_launch(const void* X, void* P, int64_t R, int n, const void* F
 int d3m_dinv_left_copy_launch(const void* Z, void* U, int n, int m, const void* F, const void* tags, void* stream);
 int d3m_nonzero_rows_launch(int B, int n, int m, const void* D, void* flag, void* idx, void* count, void* stream);
 int d3m_tri_inv_blocked_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef, int n,
-                               void* stream);
+                               void* Linv, void* stream);
+int d3m_gemm_launch_perm(const void* A, const void* B, void* C, const void* dtasks, int ntasks, int ntiles,
+                         const void* gperm, void* stream);
 int d3m_tri_inv_warp_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef, int n,
-                            void* stream);
+                            void* stream, void* Linv = nullptr);
 int d3m_dinv_rows_coef_launch(const void* X, void* P, int64_t R, int n, const void* tags, const void* coef,
                               void* stream);
 int d3m_diag_block_launch(int fwd, const void* F, int64_t stride_f, const void* tags, int64_t stride_t, void* Z,

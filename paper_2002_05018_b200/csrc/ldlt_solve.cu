@@ -355,7 +355,7 @@ namespace d3m {
 template <int NPER>
 __global__ void __launch_bounds__(256)
 tri_inv_warp_kernel(const cplx* __restrict__ F, const int64_t* __restrict__ perm, const int8_t* __restrict__ tags,
-                    cplx* Binv, cplx* coef, int n) {
+                    cplx* Binv, cplx* coef, int n, cplx* Linv) {
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (q >= n) return;
@@ -395,7 +395,10 @@ tri_inv_warp_kernel(const cplx* __restrict__ F, const int64_t* __restrict__ perm
 #pragma unroll
   for (int t = 0; t < NPER; ++t) {
     const int row = lane + 32 * t;
-    if (row < n) Binv[(int64_t)row * n + pc] = row < q ? mk(0.0, 0.0) : y[t];
+    if (row < n) {
+      Binv[(int64_t)row * n + pc] = row < q ? mk(0.0, 0.0) : y[t];
+      if (Linv) Linv[(int64_t)row * n + q] = row < q ? mk(0.0, 0.0) : y[t];
+    }
   }
   if (lane == 0 && coef != nullptr) {
     const int8_t tg = tags[q];
@@ -508,7 +511,7 @@ __device__ __forceinline__ void ti_cp16(void* smem, const void* gmem) {
 
 __global__ void __launch_bounds__(256) tri_inv_cols16(const cplx* __restrict__ F, const int64_t* __restrict__ perm,
                                                       const int8_t* __restrict__ tags, const cplx* __restrict__ Dinv,
-                                                      cplx* Binv, int n) {
+                                                      cplx* Binv, cplx* Linv, int n) {
   extern __shared__ __align__(16) unsigned char ti_smem[];
   cplx* X = reinterpret_cast<cplx*>(ti_smem);                 // rows 16k.. of block column k, 16 wide
   cplx* Lb = X + (size_t)TI_NMAX * TI_B;                      // 2 x [16][16(i-k)] L row panels
@@ -563,11 +566,13 @@ __global__ void __launch_bounds__(256) tri_inv_cols16(const cplx* __restrict__ F
     X[(w + r) * TI_B + cc] = (r < rows) ? mk(-acc.x, -acc.y) : mk(0.0, 0.0);
     __syncthreads();
   }
-  // Binv[:, perm[q]] = X[:, q] (zeros above the block column)
+  // Binv[:, perm[q]] = X[:, q] (zeros above the block column); Linv[:, q] = X[:, q]
   for (int e = tid; e < n * TI_B; e += 256) {
     const int row = e / TI_B, q = c0 + (e % TI_B);
     if (q >= n) continue;
-    Binv[(int64_t)row * n + perm[q]] = (row < c0) ? mk(0.0, 0.0) : X[(row - c0) * TI_B + (q - c0)];
+    const cplx v = (row < c0) ? mk(0.0, 0.0) : X[(row - c0) * TI_B + (q - c0)];
+    Binv[(int64_t)row * n + perm[q]] = v;
+    if (Linv) Linv[(int64_t)row * n + q] = v;
   }
 }
 
@@ -575,7 +580,7 @@ __global__ void __launch_bounds__(256) tri_inv_cols16(const cplx* __restrict__ F
 
 // blocked L^-1 P + D^-1 coefficients for n <= 256 (-22 above)
 extern "C" int d3m_tri_inv_blocked_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef,
-                                          int n, void* stream) {
+                                          int n, void* Linv, void* stream) {
   using namespace d3m;
   if (n <= 0) return 0;
   if (n > TI_NMAX) return -22;
@@ -593,13 +598,14 @@ extern "C" int d3m_tri_inv_blocked_launch(const void* F, const void* perm, const
   auto Fp = static_cast<const cplx*>(F);
   auto tp = static_cast<const int8_t*>(tags);
   tri_inv_diag16<<<nbk, 64, 0, s>>>(Fp, tp, dinv, static_cast<cplx*>(coef), n);
-  tri_inv_cols16<<<nbk, 256, kTiSmem, s>>>(Fp, static_cast<const int64_t*>(perm), tp, dinv, static_cast<cplx*>(Binv), n);
+  tri_inv_cols16<<<nbk, 256, kTiSmem, s>>>(Fp, static_cast<const int64_t*>(perm), tp, dinv, static_cast<cplx*>(Binv),
+                                           static_cast<cplx*>(Linv), n);
   return (int)cudaGetLastError();
 }
 
 // warp-per-column inverse for n <= 512 (returns -22 above: use d3m_tri_inv_launch)
 extern "C" int d3m_tri_inv_warp_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef,
-                                       int n, void* stream) {
+                                       int n, void* stream, void* Linv) {
   using namespace d3m;
   if (n <= 0) return 0;
   const dim3 grid((n + 7) / 8);
@@ -607,8 +613,10 @@ extern "C" int d3m_tri_inv_warp_launch(const void* F, const void* perm, const vo
   auto Fp = static_cast<const cplx*>(F);
   auto pp = static_cast<const int64_t*>(perm);
   auto tp = static_cast<const int8_t*>(tags);
-  if (n <= 256) tri_inv_warp_kernel<8><<<grid, 256, 0, s>>>(Fp, pp, tp, static_cast<cplx*>(Binv), static_cast<cplx*>(coef), n);
-  else if (n <= 512) tri_inv_warp_kernel<16><<<grid, 256, 0, s>>>(Fp, pp, tp, static_cast<cplx*>(Binv), static_cast<cplx*>(coef), n);
+  if (n <= 256) tri_inv_warp_kernel<8><<<grid, 256, 0, s>>>(Fp, pp, tp, static_cast<cplx*>(Binv), static_cast<cplx*>(coef), n,
+                                                static_cast<cplx*>(Linv));
+  else if (n <= 512) tri_inv_warp_kernel<16><<<grid, 256, 0, s>>>(Fp, pp, tp, static_cast<cplx*>(Binv), static_cast<cplx*>(coef), n,
+                                                 static_cast<cplx*>(Linv));
   else return -22;
   return (int)cudaGetLastError();
 }

@@ -87,15 +87,17 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // NT threads (128 or 256) cover the 512 16-byte elements of a stage slice.
 template <bool TRANS, int NT = NTHREADS>
 __device__ __forceinline__ void load_tile(cplx (*S)[PITCH], const cplx* P, int ld, int r0, int rows,
-                                          int k0, int kdim) {
+                                          int k0, int kdim, const int64_t* gcol = nullptr) {
   const int t = threadIdx.x;
   if (!TRANS) {
-    // 8 threads cover one 128-byte row segment; NT/8 rows per pass
+    // 8 threads cover one 128-byte row segment; NT/8 rows per pass (gcol: column gather)
+    const int kq = t & 7;
+    const int64_t col = (k0 + kq < kdim) ? (gcol ? gcol[k0 + kq] : (int64_t)(k0 + kq)) : 0;
 #pragma unroll
     for (int p = 0; p < 512 / NT; ++p) {
-      const int r = p * (NT / 8) + (t >> 3), k = t & 7;
+      const int r = p * (NT / 8) + (t >> 3), k = kq;
       const bool ok = (r0 + r < rows) && (k0 + k < kdim);
-      const cplx* g = ok ? P + (int64_t)(r0 + r) * ld + (k0 + k) : P;
+      const cplx* g = ok ? P + (int64_t)(r0 + r) * ld + col : P;
       cp_async16(&S[r][k], g, ok);
     }
   } else {
@@ -146,7 +148,8 @@ __device__ __forceinline__ int find_task(const GemmTask* __restrict__ tasks, int
 template <bool TA, bool TB, bool G3, bool MB = false>
 __global__ void __launch_bounds__(G3 ? 2 * NTHREADS : NTHREADS, 2)
 zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bbase, cplx* Cbase,
-                     const GemmTask* __restrict__ tasks, int ntasks, unsigned long long* tmax) {
+                     const GemmTask* __restrict__ tasks, int ntasks, unsigned long long* tmax,
+                     const int64_t* __restrict__ gperm) {
   constexpr int NT = G3 ? 2 * NTHREADS : NTHREADS;
   constexpr int WJ = G3 ? 2 : 4;             // 8-column DMMA sub-tiles per warp tile
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -186,7 +189,13 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
       acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = acc_x[i][j][0] =
           acc_x[i][j][1] = 0.0;
 
-  const int ktiles = (K + BKC - 1) / BKC;
+  // TriGather: gathered A columns, K cut at the end of the triangular B's
+  // nonzero columns for this output column tile (the skipped products are
+  // exact zeros: the sum is bitwise that of the full range)
+  const bool trig = (tk.flags & kGemmTriGather) != 0 && gperm != nullptr;
+  const int64_t* gcol = trig ? gperm + tk.pad_ : nullptr;
+  const int Keff = trig ? min(K, n0 + BN) : K;
+  const int ktiles = (Keff + BKC - 1) / BKC;
   // MB: the ring is tracked by mbarriers -- full[s] completes when every
   // thread's copies of the stage in slot s have landed, empty[s] when all
   // warps have consumed it -- so a warp waits only for the data it reads and,
@@ -206,7 +215,7 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < ktiles) {
-      load_tile<TA, NT>(st[s].a, A, tk.lda, m0, M, s * BKC, K);
+      load_tile<TA, NT>(st[s].a, A, tk.lda, m0, M, s * BKC, K, gcol);
       load_tile<TB, NT>(st[s].b, B, tk.ldb, n0, N, s * BKC, K);
       if constexpr (MB) mb_cp_arrive(&full_bar[s]);
     }
@@ -231,7 +240,7 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
       const int nk = kt + STAGES - 1;
       if (nk < ktiles) {
         const int slot = nk % STAGES;
-        load_tile<TA, NT>(st[slot].a, A, tk.lda, m0, M, nk * BKC, K);
+        load_tile<TA, NT>(st[slot].a, A, tk.lda, m0, M, nk * BKC, K, gcol);
         load_tile<TB, NT>(st[slot].b, B, tk.ldb, n0, N, nk * BKC, K);
       } else if (cpre) {
         const int ch = nk - ktiles, r0 = ch * CP_ROWS;
@@ -280,7 +289,7 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
           // slot2 last held stage nk - STAGES (= kt - 1): wait until every warp consumed it
           if (nk >= STAGES) mb_wait(&empty_bar[slot2], (unsigned)((nk - STAGES) / STAGES) & 1u);
           if (nk < ktiles) {
-            load_tile<TA, NT>(st[slot2].a, A, tk.lda, m0, M, nk * BKC, K);
+            load_tile<TA, NT>(st[slot2].a, A, tk.lda, m0, M, nk * BKC, K, gcol);
             load_tile<TB, NT>(st[slot2].b, B, tk.ldb, n0, N, nk * BKC, K);
             mb_cp_arrive(&full_bar[slot2]);
           } else {
@@ -580,6 +589,7 @@ zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
 constexpr size_t kGemmSmem = sizeof(cplx) * STAGES * (BM + BN) * PITCH;
 
 static unsigned long long* g_tmax = nullptr;   // set per launch by d3m_gemm_launch_tm
+static const int64_t* g_gperm = nullptr;        // set per launch by d3m_gemm_launch_perm
 
 template <bool TA, bool TB, bool G3, bool MB = false>
 static int launch_g(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
@@ -591,7 +601,7 @@ static int launch_g(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks
     configured = true;
   }
   zgemm_grouped_kernel<TA, TB, G3, MB><<<ntiles, G3 ? 2 * NTHREADS : NTHREADS, kGemmSmem, s>>>(A, B, C, tasks,
-                                                                                               ntasks, g_tmax);
+                                                                                               ntasks, g_tmax, g_gperm);
   return (int)cudaGetLastError();
 }
 
@@ -645,6 +655,15 @@ extern "C" int d3m_gemm_set_form(int form) {
 extern "C" int d3m_gemm_launch(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
                                int ntasks, int ntiles, void* stream) {
   return d3m_gemm_launch_tm(ta, tb, A, B, C, dtasks, ntasks, ntiles, nullptr, stream);
+}
+
+// Launch with a column-gather permutation for kGemmTriGather tasks (A not transposed).
+extern "C" int d3m_gemm_launch_perm(const void* A, const void* B, void* C, const void* dtasks, int ntasks, int ntiles,
+                                    const void* gperm, void* stream) {
+  d3m::g_gperm = static_cast<const int64_t*>(gperm);
+  const int rc = d3m_gemm_launch_tm(0, 0, A, B, C, dtasks, ntasks, ntiles, nullptr, stream);
+  d3m::g_gperm = nullptr;
+  return rc;
 }
 
 extern "C" int d3m_gemm_launch_tm(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,

@@ -343,7 +343,11 @@ class _Schedule:
         tt["b_off"] = self.binv_off[:nb]
         tt["m"] = self.panel_rows
         tt["n"] = tt["k"] = tt["lda"] = tt["ldb"] = tt["ldc"] = sizes
-        tt["flags"] = _lib.GEMM_STORE
+        # X = (K_panel P^T) L^-T for supernodes <= 512 (d3m_capi.cu kTrsmTriMax): gathered A
+        # columns (perm at the column's pivot offset), triangular K range per output tile
+        tri = sizes <= _lib.TRSM_TRI_MAX
+        tt["flags"] = _lib.GEMM_STORE | np.where(tri, _lib.GEMM_TRIGATHER, 0)
+        tt["pad"] = np.where(tri, self.row_off[:nb], 0)
         tt["tiles_n"] = (sizes + bm - 1) // bm
         self.tiles_trsm = (((self.panel_rows + bm - 1) // bm) * ((sizes + bm - 1) // bm)).astype(np.int64)
         self.d_trsm_tasks = upload_bytes(tt)
