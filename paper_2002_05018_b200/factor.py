@@ -888,7 +888,9 @@ def block_solve(F: BlockFactor, g: list, refine: int = 0) -> list:
     ``g`` is a block vector in the original block numbering, each block 1-D
     or a matrix of RHS columns.  All columns go through one device pass, each
     computed independently, so k-RHS results equal k single solves bit for
-    bit.  Device-resident inputs give device-resident outputs.
+    bit.  Device-resident inputs give device-resident outputs; host torch
+    tensors give host torch tensors (views of one pinned copy), numpy gives
+    numpy.
 
     ``refine`` (not in the reference, default 0 = the reference's algorithm):
     steps of fixed-precision iterative refinement, x += solve(g - K x), with
@@ -903,7 +905,10 @@ def block_solve(F: BlockFactor, g: list, refine: int = 0) -> list:
         return []
     perm = F.plan.order.perm
     sizes = F.plan.sizes_perm
-    device_in = all(isinstance(b, DeviceArray) or _is_tensor(b) for b in g)
+    # host torch tensors (e.g. pinned RHS) take the host path and get host
+    # tensors back: one staged H2D copy in, one D2H copy out
+    cpu_t = all(_is_tensor(b) and not b.is_cuda for b in g)
+    device_in = not cpu_t and all(isinstance(b, DeviceArray) or _is_tensor(b) for b in g)
     shapes = [tuple(b.shape) for b in g]
     one_d = all(len(s) == 1 for s in shapes)
     cols = None
@@ -925,6 +930,12 @@ def block_solve(F: BlockFactor, g: list, refine: int = 0) -> list:
     if device_in:
         parts = [to_device(g[int(perm[j])]).reshape(int(sizes[j]), cols) for j in range(nb)]
         b = t.cat(parts, dim=0).contiguous()
+    elif cpu_t:
+        hp = t.empty((N, cols), dtype=t.complex128, pin_memory=True)
+        host = hp.numpy()
+        for j in range(nb):
+            host[sched.row_off[j]:sched.row_off[j + 1]] = g[int(perm[j])].numpy().reshape(int(sizes[j]), cols)
+        b = hp.to("cuda", non_blocking=True)
     else:
         host = np.empty((N, cols), dtype=np.complex128)
         for j in range(nb):
@@ -979,6 +990,13 @@ def block_solve(F: BlockFactor, g: list, refine: int = 0) -> list:
         for j in range(nb):
             blk = x[sched.row_off[j]:sched.row_off[j + 1]]
             out[int(perm[j])] = DeviceArray(blk[:, 0] if one_d else blk)
+        return out
+    if cpu_t:
+        xo = t.empty((N, cols), dtype=t.complex128, pin_memory=True)
+        xo.copy_(x)                                   # one D2H copy (synchronous: the result is ready)
+        for j in range(nb):
+            blk = xo[int(sched.row_off[j]):int(sched.row_off[j + 1])]
+            out[int(perm[j])] = blk[:, 0] if one_d else blk
         return out
     xh = x.cpu().numpy()
     for j in range(nb):
