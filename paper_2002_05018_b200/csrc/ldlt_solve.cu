@@ -502,7 +502,8 @@ __global__ void __launch_bounds__(64) tri_inv_diag16(const cplx* __restrict__ F,
 }
 
 constexpr int TI_NMAX = 256;
-constexpr size_t kTiSmem = sizeof(cplx) * ((size_t)TI_NMAX * TI_B + 2 * (size_t)TI_B * TI_NMAX + TI_B * TI_B);
+constexpr size_t kTiSmem = sizeof(cplx) * ((size_t)TI_NMAX * TI_B + 2 * (size_t)TI_B * TI_NMAX + TI_B * TI_B +
+                                          2 * TI_B * TI_B);
 
 __device__ __forceinline__ void ti_cp16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -516,6 +517,7 @@ __global__ void __launch_bounds__(256) tri_inv_cols16(const cplx* __restrict__ F
   cplx* X = reinterpret_cast<cplx*>(ti_smem);                 // rows 16k.. of block column k, 16 wide
   cplx* Lb = X + (size_t)TI_NMAX * TI_B;                      // 2 x [16][16(i-k)] L row panels
   cplx* S = Lb + 2 * (size_t)TI_B * TI_NMAX;                  // 16 x 16
+  cplx* Ds = S + TI_B * TI_B;                                 // 2 x Dinv_i (16 x 16), with the L rows
   const int k = blockIdx.x, nbk = (n + TI_B - 1) / TI_B, c0 = k * TI_B;
   const int tid = threadIdx.x, r = tid >> 4, cc = tid & 15;
   auto fetch = [&](int i, int buf) {      // L rows [16i, 16i+16) x cols [c0, 16i) -> Lb[buf]
@@ -525,6 +527,7 @@ __global__ void __launch_bounds__(256) tri_inv_cols16(const cplx* __restrict__ F
       const int rr = e / w, m = e - rr * w;
       ti_cp16(dst + rr * w + m, F + (int64_t)(i * TI_B + rr) * n + c0 + m);
     }
+    ti_cp16(Ds + buf * TI_B * TI_B + tid, Dinv + (int64_t)i * TI_B * TI_B + tid);     // 256 entries
     asm volatile("cp.async.commit_group;\n" ::);
   };
   if (k + 1 < nbk) fetch(k + 1, 0);
@@ -539,25 +542,31 @@ __global__ void __launch_bounds__(256) tri_inv_cols16(const cplx* __restrict__ F
     }
     __syncthreads();
     const cplx* Lr = Lb + (size_t)buf * TI_B * TI_NMAX;
-    // S = L_i,[k,i) X_[k,i),k  (two partial sums shorten the dependent chain)
-    cplx a0 = mk(0.0, 0.0), a1 = mk(0.0, 0.0);
+    // S = L_i,[k,i) X_[k,i),k: 16 columns per iteration, loads first, four
+    // partial sums (w is a multiple of 16)
+    cplx a[4] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
     if (r < rows) {
       const bool zr = r == 0 && tags[i * TI_B - 1] == 2;     // L[16i, 16i-1] of a 2x2 pivot
-      for (int m = 0; m < w; m += 2) {
-        const cplx l0 = Lr[r * w + m];                        // m even: never column w-1
-        const cplx x0 = X[m * TI_B + cc];
-        a0 = mk(a0.x + (l0.x * x0.x - l0.y * x0.y), a0.y + (l0.x * x0.y + l0.y * x0.x));
-        cplx l1 = Lr[r * w + m + 1];
-        if (zr && m + 1 == w - 1) l1 = mk(0.0, 0.0);
-        const cplx x1 = X[(m + 1) * TI_B + cc];
-        a1 = mk(a1.x + (l1.x * x1.x - l1.y * x1.y), a1.y + (l1.x * x1.y + l1.y * x1.x));
+      for (int m0 = 0; m0 < w; m0 += 16) {
+        cplx l[16], x[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          l[q] = Lr[r * w + m0 + q];
+          x[q] = X[(m0 + q) * TI_B + cc];
+        }
+        if (zr && m0 + 16 == w) l[15] = mk(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          cplx& t = a[q & 3];
+          t = mk(t.x + (l[q].x * x[q].x - l[q].y * x[q].y), t.y + (l[q].x * x[q].y + l[q].y * x[q].x));
+        }
       }
     }
-    S[r * TI_B + cc] = c_add(a0, a1);
+    S[r * TI_B + cc] = c_add(c_add(a[0], a[1]), c_add(a[2], a[3]));
     __syncthreads();
     // X_ik = -Dinv_i S
     cplx acc = mk(0.0, 0.0);
-    const cplx* Di = Dinv + (int64_t)i * TI_B * TI_B;
+    const cplx* Di = Ds + buf * TI_B * TI_B;
 #pragma unroll
     for (int c = 0; c < TI_B; ++c) {
       const cplx d = Di[r * TI_B + c], sv = S[c * TI_B + cc];
