@@ -241,3 +241,33 @@ def test_fem_pipeline_vs_reference_goldens(cuda, case):
     assert np.linalg.norm(lam_c - g[f"c{case}_lam"]) <= 1e-9 * np.linalg.norm(g[f"c{case}_lam"])
     sol = np.asarray(d.recover_primal(systems, lam))
     assert np.linalg.norm(sol - g[f"c{case}_sol"]) <= 1e-9 * np.linalg.norm(g[f"c{case}_sol"])
+
+
+@pytest.mark.parametrize("n,m,B", [(1, 1, 1), (37, 5, 3), (700, 45, 4), (2100, 300, 2)])
+def test_nonzero_rows_vs_numpy(cuda, n, m, B):
+    """d3m_nonzero_rows (the DᵀX row list): every domain's nonzero rows in
+    ascending order, -1 padded to the batch maximum; an all-zero domain and
+    rows whose only nonzero is the last column or has a zero real part are
+    included."""
+    from paper_2002_05018_b200.subdomain import _nonzero_rows
+    from paper_2002_05018_b200.device import to_device
+    rng = np.random.default_rng(n + m + B)
+    D = np.zeros((B, n, m), dtype=np.complex128)
+    for b in range(1, B):                     # domain 0 stays all-zero
+        rows = rng.choice(n, size=max(1, n // 7), replace=False)
+        for r in rows:
+            c = int(rng.integers(0, m))
+            D[b, r, c] = rng.choice([1.0, -1.0, 1j])
+        D[b, rows[0], m - 1] = 1j
+    idx, nrows = _nonzero_rows(to_device(D), n)
+    expect = [np.flatnonzero(np.any(D[b] != 0, axis=1)) for b in range(B)]
+    mx = max(len(e) for e in expect)
+    if mx == 0 or mx > 0.6 * n:
+        assert idx is None and nrows == 0
+        return
+    assert nrows == mx
+    got = idx.cpu().numpy()
+    for b in range(B):
+        want = np.full(mx, -1, dtype=np.int64)
+        want[:len(expect[b])] = expect[b]
+        assert np.array_equal(got[b], want), b
