@@ -466,10 +466,22 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
           else own = aw;
         }
         BKC_MARK(0, 5);
-        warp_argmax(v, vi);
-        own = warp_max(own);
+        // one butterfly for the exact argmax, the owner's modulus and the
+        // update maximum (independent shuffles per round; max and
+        // first-index argmax are order-free, so the results are unchanged)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+          const int i2 = __shfl_xor_sync(0xffffffffu, vi, o);
+          const double own2 = __shfl_xor_sync(0xffffffffu, own, o);
+          const double sq2 = __shfl_xor_sync(0xffffffffu, step_sq, o);
+          argmax_merge(v, vi, v2, i2);
+          own = fmax(own, own2);
+          step_sq = fmax(step_sq, sq2);
+        }
+      } else {
+        step_sq = warp_max(step_sq);
       }
-      step_sq = warp_max(step_sq);
       if (lane == 0) rst[s & 1][0] = step_sq;
       xpost<CS>(inbox[nb], rank, xslot(v, own, up, vi), &mbar[nb]);
       BKC_MARK(0, 6);
