@@ -616,11 +616,219 @@ static bool use_3m() {
   return g_form == 3;
 }
 
+// ---- 3M on half tiles: three CTAs per SM -------------------------------------
+// Each 64 x 64 task tile runs as two 64 x 32 CTAs (blockIdx.x = 2 * tile +
+// half; the task tile maps are unchanged) of 4 warps with the same 32 x 16
+// warp tiles: at three 128-thread CTAs per SM the register cap is 170 instead
+// of 128, so the A fragments need not reuse the registers of the DMMAs in
+// flight.  Per-element accumulation order and form are those of the 64 x 64
+// 3M kernel (bitwise equal results).  Non-transposed operands only.
+constexpr int HN = 32, HNT = 128;
+struct HStage {
+  cplx a[BM][PITCH];
+  cplx b[HN][PITCH];
+};
+constexpr int HCP_PITCH = HN + 1;
+static_assert(32 * HCP_PITCH <= (int)(sizeof(HStage) / sizeof(cplx)), "a 32-row C chunk fits a freed stage");
+constexpr size_t kHSmem = sizeof(HStage) * STAGES;
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(HNT, 3)
+zgemm3m_half_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bbase, cplx* Cbase,
+                    const GemmTask* __restrict__ tasks, int ntasks, unsigned long long* tmax,
+                    const int64_t* __restrict__ gperm) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  HStage* st = reinterpret_cast<HStage*>(smem_raw);
+  const int tile = blockIdx.x >> 1, half = blockIdx.x & 1;
+  const GemmTask tk = tasks[find_task(tasks, ntasks, tile)];
+  int local = tile - tk.tile_start, tm, tn;
+  const bool sym = (tk.flags & kGemmSym) != 0;
+  if (sym) {
+    tm = (int)((sqrt(8.0 * local + 1.0) - 1.0) * 0.5);
+    while ((tm + 1) * (tm + 2) / 2 <= local) ++tm;
+    while (tm * (tm + 1) / 2 > local) --tm;
+    tn = local - tm * (tm + 1) / 2;
+  } else {
+    tm = local / tk.tiles_n;
+    tn = local - tm * tk.tiles_n;
+  }
+  const int M = tk.m, N = tk.n, K = tk.k;
+  const int m0 = tm * BM, n0 = tn * BN + half * HN;
+  if (m0 >= M || n0 >= N) return;
+  const cplx* A = Abase + tk.a_off;
+  const cplx* B = Bbase + tk.b_off;
+  cplx* C = Cbase + tk.c_off;
+  const bool trig = (tk.flags & kGemmTriGather) != 0 && gperm != nullptr;
+  const int64_t* gcol = trig ? gperm + tk.pad_ : nullptr;
+  const int Keff = trig ? min(K, n0 + HN) : K;
+  const int ktiles = (Keff + BKC - 1) / BKC;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 16;
+  const int fr = lane >> 2, fc = lane & 3;
+  auto load_stage = [&](int slot, int k0) {
+    const int kq = t & 7;
+    const int64_t acol = (k0 + kq < K) ? (gcol ? gcol[k0 + kq] : (int64_t)(k0 + kq)) : 0;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {       // A: 64 rows, 16 per pass
+      const int r = p * 16 + (t >> 3);
+      const bool ok = (m0 + r < M) && (k0 + kq < K);
+      cp_async16(&st[slot].a[r][kq], ok ? A + (int64_t)(m0 + r) * tk.lda + acol : A, ok);
+    }
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {       // B: 32 rows
+      const int r = p * 16 + (t >> 3);
+      const bool ok = (n0 + r < N) && (k0 + kq < K);
+      cp_async16(&st[slot].b[r][kq], ok ? B + (int64_t)(n0 + r) * tk.ldb + k0 + kq : B, ok);
+    }
+  };
+  double P3[4][2][2], Q3[4][2][2], R3[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) P3[i][j][0] = P3[i][j][1] = Q3[i][j][0] = Q3[i][j][1] = R3[i][j][0] = R3[i][j][1] = 0.0;
+  const int mode = tk.flags & kGemmModeMask;
+  const bool cpre = (!sym || (tk.flags & kGemmLowerOnly)) && mode != kGemmStore && ktiles >= STAGES;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load_stage(s, s * BKC);
+    cp_commit();
+  }
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    const int nk = kt + STAGES - 1;
+    if (nk < ktiles) {
+      load_stage(nk % STAGES, nk * BKC);
+    } else if (cpre && nk - ktiles < 2) {          // C rows [32c, 32c+32) into the freed stage
+      const int ch = nk - ktiles;
+      cplx* dst = reinterpret_cast<cplx*>(&st[nk % STAGES]);
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int e = p * HNT + t, r = e >> 5, c = e & 31;
+        const int gr = m0 + ch * 32 + r;
+        const bool ok = gr < M && n0 + c < N;
+        cp_async16(dst + r * HCP_PITCH + c, ok ? C + (int64_t)gr * tk.ldc + n0 + c : C, ok);
+      }
+    }
+    cp_commit();
+    const HStage& S = st[kt % STAGES];
+#pragma unroll
+    for (int kk = 0; kk < BKC / 4; ++kk) {
+      double bre[2], bim[2], bsum[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const cplx b = S.b[wn + j * 8 + fr][kk * 4 + fc];
+        bre[j] = b.x;
+        bim[j] = b.y;
+        bsum[j] = b.x + b.y;
+      }
+      cplx a[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = S.a[wm + i * 8 + fr][kk * 4 + fc];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double asum = a[i].x + a[i].y;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(P3[i][j][0], P3[i][j][1], a[i].x, bre[j]);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(Q3[i][j][0], Q3[i][j][1], a[i].y, bim[j]);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(R3[i][j][0], R3[i][j][1], asum, bsum[j]);
+      }
+    }
+  }
+  cp_wait<0>();
+  const bool mirror = sym && !(tk.flags & kGemmLowerOnly);
+  const bool track = (tk.flags & kGemmTrackMax) != 0 && tmax != nullptr;
+  double tm2 = 0.0;
+  const int ldc = tk.ldc;
+  if (cpre) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rl = wm + i * 8 + fr, r = m0 + rl, ch = rl >> 5;
+      const cplx* crow = reinterpret_cast<const cplx*>(&st[(ktiles + ch) % STAGES]) + (rl & 31) * HCP_PITCH;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cl = wn + j * 8 + fc * 2 + h, c = n0 + cl;
+          if (r >= M || c >= N || (sym && c > r)) continue;
+          const double p = P3[i][j][h], q = Q3[i][j][h];
+          const cplx u = mk(p - q, (R3[i][j][h] - p) - q);
+          const cplx w = mode == kGemmSub ? c_sub(crow[cl], u) : c_add(crow[cl], u);
+          C[(int64_t)r * ldc + c] = w;
+          if (track) tm2 = fmax(tm2, w.x * w.x + w.y * w.y);
+        }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = m0 + wm + i * 8 + fr;
+      cplx cv[2][2], cq[2][2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = n0 + wn + j * 8 + fc * 2 + h;
+          const bool ok = r < M && c < N && (!sym || c <= r);
+          cv[j][h] = mk(0.0, 0.0);
+          cq[j][h] = mk(0.0, 0.0);
+          if (ok && mode != kGemmStore) cv[j][h] = C[(int64_t)r * ldc + c];
+          if (ok && mirror && c < r) cq[j][h] = C[(int64_t)c * ldc + r];
+        }
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = n0 + wn + j * 8 + fc * 2 + h;
+          if (r >= M || c >= N) continue;
+          const double p = P3[i][j][h], q = Q3[i][j][h];
+          const cplx u = mk(p - q, (R3[i][j][h] - p) - q);
+          if (sym) {
+            if (c > r) continue;
+            const cplx w = c_sub(cv[j][h], u);
+            C[(int64_t)r * ldc + c] = w;
+            if (track) tm2 = fmax(tm2, w.x * w.x + w.y * w.y);
+            if (mirror && c < r) C[(int64_t)c * ldc + r] = c_sub(cq[j][h], u);
+          } else {
+            cplx* pc = C + (int64_t)r * ldc + c;
+            if (mode == kGemmSub) *pc = c_sub(cv[j][h], u);
+            else if (mode == kGemmStore) *pc = u;
+            else *pc = c_add(cv[j][h], u);
+          }
+        }
+    }
+  }
+  if (track) {   // non-negative doubles order like their bit patterns: integer max is exact
+    tm2 = warp_max(tm2);
+    if (lane == 0) atomicMax(tmax + tk.pad_, (unsigned long long)__double_as_longlong(tm2));
+  }
+}
+
+static int launch_half(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
+                       cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(zgemm3m_half_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHSmem);
+    configured = true;
+  }
+  zgemm3m_half_kernel<false, false><<<2 * ntiles, HNT, kHSmem, s>>>(A, B, C, tasks, ntasks, g_tmax, g_gperm);
+  return (int)cudaGetLastError();
+}
+
 template <bool TA, bool TB>
 static int launch_t(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
                     cudaStream_t s) {
   static const int mb = [] { const char* e = getenv("D3M_GEMM_MB"); return e ? atoi(e) : 1; }();
+  static const int hk = [] { const char* e = getenv("D3M_GEMM_HALF"); return e ? atoi(e) : 1; }();
   if (!use_3m()) return launch_g<TA, TB, false>(A, B, C, tasks, ntasks, ntiles, s);
+  if constexpr (!TA && !TB) {
+    // not for the batched panel updates (max-tracking, device-built tasks with a
+    // padded tile budget): there the doubled grid of mostly empty CTAs cost more
+    // than the faster tiles gained (config 3: 96 -> 119 ms)
+    if (hk && g_tmax == nullptr) return launch_half(A, B, C, tasks, ntasks, ntiles, s);
+  }
   return mb ? launch_g<TA, TB, true, true>(A, B, C, tasks, ntasks, ntiles, s)
             : launch_g<TA, TB, true, false>(A, B, C, tasks, ntasks, ntiles, s);
 }
