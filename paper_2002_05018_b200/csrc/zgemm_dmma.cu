@@ -622,7 +622,7 @@ static bool use_3m() {
 // warp tiles: at three 128-thread CTAs per SM the register cap is 170 instead
 // of 128, so the A fragments need not reuse the registers of the DMMAs in
 // flight.  Per-element accumulation order and form are those of the 64 x 64
-// 3M kernel (bitwise equal results).  Non-transposed operands only.
+// 3M kernel (bitwise equal results).
 constexpr int HN = 32, HNT = 128;
 struct HStage {
   cplx a[BM][PITCH];
@@ -666,19 +666,38 @@ zgemm3m_half_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 16;
   const int fr = lane >> 2, fc = lane & 3;
   auto load_stage = [&](int slot, int k0) {
-    const int kq = t & 7;
-    const int64_t acol = (k0 + kq < K) ? (gcol ? gcol[k0 + kq] : (int64_t)(k0 + kq)) : 0;
+    if constexpr (!TA) {
+      const int kq = t & 7;
+      const int64_t acol = (k0 + kq < K) ? (gcol ? gcol[k0 + kq] : (int64_t)(k0 + kq)) : 0;
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {       // A: 64 rows, 16 per pass
-      const int r = p * 16 + (t >> 3);
-      const bool ok = (m0 + r < M) && (k0 + kq < K);
-      cp_async16(&st[slot].a[r][kq], ok ? A + (int64_t)(m0 + r) * tk.lda + acol : A, ok);
+      for (int p = 0; p < 4; ++p) {     // A: 64 rows, 16 per pass (8 threads per 128-byte row segment)
+        const int r = p * 16 + (t >> 3);
+        const bool ok = (m0 + r < M) && (k0 + kq < K);
+        cp_async16(&st[slot].a[r][kq], ok ? A + (int64_t)(m0 + r) * tk.lda + acol : A, ok);
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {     // A stored K x M: 64 threads per 1 KB row of the stored operand
+        const int r = t & 63, k = p * 2 + (t >> 6);
+        const bool ok = (m0 + r < M) && (k0 + k < K);
+        cp_async16(&st[slot].a[r][k], ok ? A + (int64_t)(k0 + k) * tk.lda + m0 + r : A, ok);
+      }
     }
+    if constexpr (!TB) {
+      const int kq = t & 7;
 #pragma unroll
-    for (int p = 0; p < 2; ++p) {       // B: 32 rows
-      const int r = p * 16 + (t >> 3);
-      const bool ok = (n0 + r < N) && (k0 + kq < K);
-      cp_async16(&st[slot].b[r][kq], ok ? B + (int64_t)(n0 + r) * tk.ldb + k0 + kq : B, ok);
+      for (int p = 0; p < 2; ++p) {     // B: 32 rows
+        const int r = p * 16 + (t >> 3);
+        const bool ok = (n0 + r < N) && (k0 + kq < K);
+        cp_async16(&st[slot].b[r][kq], ok ? B + (int64_t)(n0 + r) * tk.ldb + k0 + kq : B, ok);
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {     // B stored K x N: 32 threads per 512-byte row segment
+        const int r = t & 31, k = p * 4 + (t >> 5);
+        const bool ok = (n0 + r < N) && (k0 + k < K);
+        cp_async16(&st[slot].b[r][k], ok ? B + (int64_t)(k0 + k) * tk.ldb + n0 + r : B, ok);
+      }
     }
   };
   double P3[4][2][2], Q3[4][2][2], R3[4][2][2];
@@ -806,14 +825,15 @@ zgemm3m_half_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
   }
 }
 
+template <bool TA, bool TB>
 static int launch_half(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
                        cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(zgemm3m_half_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHSmem);
+    cudaFuncSetAttribute(zgemm3m_half_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHSmem);
     configured = true;
   }
-  zgemm3m_half_kernel<false, false><<<2 * ntiles, HNT, kHSmem, s>>>(A, B, C, tasks, ntasks, g_tmax, g_gperm);
+  zgemm3m_half_kernel<TA, TB><<<2 * ntiles, HNT, kHSmem, s>>>(A, B, C, tasks, ntasks, g_tmax, g_gperm);
   return (int)cudaGetLastError();
 }
 
@@ -823,11 +843,13 @@ static int launch_t(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks
   static const int mb = [] { const char* e = getenv("D3M_GEMM_MB"); return e ? atoi(e) : 1; }();
   static const int hk = [] { const char* e = getenv("D3M_GEMM_HALF"); return e ? atoi(e) : 1; }();
   if (!use_3m()) return launch_g<TA, TB, false>(A, B, C, tasks, ntasks, ntiles, s);
+  // non-transposed operands only, and not for the batched panel updates
+  // (max-tracking, device-built tasks with a padded tile budget): there the
+  // doubled grid of mostly empty CTAs cost more than the faster tiles gained
+  // (config 3: 96 -> 119 ms); the transposed launches of the subdomain solves
+  // ran 9% slower on half tiles (config 5 GEMM class 6.40 -> 6.96 s)
   if constexpr (!TA && !TB) {
-    // not for the batched panel updates (max-tracking, device-built tasks with a
-    // padded tile budget): there the doubled grid of mostly empty CTAs cost more
-    // than the faster tiles gained (config 3: 96 -> 119 ms)
-    if (hk && g_tmax == nullptr) return launch_half(A, B, C, tasks, ntasks, ntiles, s);
+    if (hk && g_tmax == nullptr) return launch_half<TA, TB>(A, B, C, tasks, ntasks, ntiles, s);
   }
   return mb ? launch_g<TA, TB, true, true>(A, B, C, tasks, ntasks, ntiles, s)
             : launch_g<TA, TB, true, false>(A, B, C, tasks, ntasks, ntiles, s);
