@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define D3M_ABI_VERSION 7
+#define D3M_ABI_VERSION 8
 
 int d3m_abi_version(void);
 const char* d3m_last_error(void);
@@ -136,6 +136,15 @@ int d3m_zero(void* p, int64_t n, void* stream);
  * blocks stay exactly symmetric through the factorisation. */
 int d3m_diag_sym_exact(const void* pool, const void* off, const void* n, int nb, void* flag, void* stream);
 
+/* Per-block version (ABI v8): CTA b checks diagonal block idx[b] (int64
+ * device list of count blocks) and writes flags[idx[b]] = 2 (bitwise
+ * symmetric) or 1 (int32 device array, one per block).  With the chunked
+ * upload every chunk flags the diagonal blocks it carries, and
+ * d3m_block_ldlt_exec's d_check_sym makes each column's BK read its own flag
+ * on the device (no host sync on the whole of K's diagonal). */
+int d3m_diag_sym_flags(const void* pool, const void* off, const void* n, const void* idx, int count, void* flags,
+                       void* stream);
+
 /* Test hook: hyp[i] = glibc-hypot modulus (numba abs, kernels.py:50-77) and
  * npabs[i] = numpy np.abs modulus (factor.py:94-96) of z[i], as computed by
  * the device code that makes the pivot decisions. */
@@ -160,7 +169,9 @@ int d3m_modulus_probe(const void* z, void* hyp, void* npabs, int64_t n, void* st
  * xbuf: X scratch (2 x max R_j n_j with lookahead).
  * nwait / h_wait_col / h_wait_ev (ABI v6; 0 / NULL / NULL = none): cudaEvent_t
  * handles; before column h_wait_col[w] the critical stream waits on
- * h_wait_ev[w] (blocks of K still being uploaded on a copy stream). */
+ * h_wait_ev[w] (blocks of K still being uploaded on a copy stream).
+ * d_check_sym (ABI v8; NULL = use check_sym): nb int32 device flags, column
+ * j's BK reads d_check_sym[j] (d3m_diag_sym_flags) instead of check_sym. */
 int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_off, const int64_t* h_panel_off,
                         const int64_t* h_panel_rows, const int64_t* h_piv_off, const int64_t* h_binv_off,
                         const int64_t* h_task_ptr, const int64_t* h_task_next, const int64_t* h_tiles_next,
@@ -168,7 +179,8 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                         const void* d_trsm_tasks, void* d_pool, void* d_binv, void* d_xbuf, int64_t xbuf_elems,
                         void* d_perm, void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale,
                         void* d_asym, void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead,
-                        int nwait, const int64_t* h_wait_col, void* const* h_wait_ev, void* stream);
+                        int nwait, const int64_t* h_wait_col, void* const* h_wait_ev, const void* d_check_sym,
+                        void* stream);
 
 /* n asynchronous copies dst + dst_off[i] <- src + src_off[i] (bytes, kind a
  * cudaMemcpyKind) on `stream`: the chunked upload of K's blocks from pinned

@@ -54,6 +54,7 @@ __device__ __forceinline__ void bargmax(double& v, int& idx, double* vs, int* is
 
 template <int NB, int NT>
 __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
+  const int csym = a.check_sym_dev ? *a.check_sym_dev : a.check_sym;   // per-block device flag (block_ldlt)
 #ifdef D3M_BK_PROFILE
   double prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long prof_t = clock64();
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
   // LDL^T diagonal targets: symmetric K blocks + mirrored updates), so the
   // scale is the max over the lower triangle and asym is 0 -- row-wise,
   // coalesced reads of half the matrix
-  const bool lower_only = a.check_sym == 2;
+  const bool lower_only = csym == 2;
   double p_all = 0.0, p_asy = 0.0, tm2 = 0.0;
   // pass 1 over the lower triangle incl. diagonal, row segments, 8 loads in
   // flight per lane: proxies of |W_ij|, |W_ij - W_ji| and the trailing max
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
           const double q = x_abs2(z[u]), qt = x_abs2(zt[u]);
           p_all = fmax(p_all, fmax(q, qt));
           tm2 = fmax(tm2, q);
-          if (a.check_sym && j < i) p_asy = fmax(p_asy, x_abs2(x_sub(z[u], zt[u])));
+          if (csym && j < i) p_asy = fmax(p_asy, x_abs2(x_sub(z[u], zt[u])));
         }
       }
     }
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
           if (j <= i) {
             if (x_abs2(z[u]) >= ta) scale = fmax(scale, np_abs(z[u]));
             if (x_abs2(zt[u]) >= ta) scale = fmax(scale, np_abs(zt[u]));
-            if (a.check_sym && j < i) {
+            if (csym && j < i) {
               const cplx dz = x_sub(z[u], zt[u]);
               if (x_abs2(dz) >= tb) asym = fmax(asym, np_abs(dz));
             }
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(NT) bk_blocked_kernel(BkArgs a) {
     asym = bmax<NT>(asym, ra);
   }
   if (tid == 0) { a.scale[b] = scale; a.asym[b] = asym; }
-  if (a.check_sym && n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) {
+  if (csym && n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) {
     if (tid == 0) { a.info[b] = -2; a.n2x2[b] = 0; a.growth[b] = 1.0; }
     return;
   }

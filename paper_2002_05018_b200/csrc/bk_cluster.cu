@@ -198,6 +198,7 @@ __host__ __device__ inline int64_t bkc_entries(int n) {    // per-CTA capacity (
 // follows the end of its step s-2 bulk update.
 template <int CS>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_kernel(BkArgs a) {
+  const int csym = a.check_sym_dev ? *a.check_sym_dev : a.check_sym;   // per-block device flag (block_ldlt)
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char bkc_smem[];
   __shared__ double rv[BKC_NT / 32];
@@ -240,12 +241,12 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     const int i = rank + q * CS;
     const cplx* row = W + (int64_t)i * lda;
     cplx* dst = Rl + bkc_off<CS>(i);
-    const int jend = a.check_sym == 2 ? i + 1 : n;     // 2: verified exactly symmetric (lower suffices)
+    const int jend = csym == 2 ? i + 1 : n;     // 2: verified exactly symmetric (lower suffices)
     for (int j = lane; j < jend; j += 32) {
       const cplx z = row[j];
       scale = fmax(scale, np_abs(z));
       if (j <= i) { tm2 = fmax(tm2, x_abs2(z)); dst[j] = z; }
-      if (a.check_sym == 1 && j < i) asym = fmax(asym, np_abs(x_sub(z, W[(int64_t)j * lda + i])));
+      if (csym == 1 && j < i) asym = fmax(asym, np_abs(x_sub(z, W[(int64_t)j * lda + i])));
     }
   }
   for (int i = tid; i < n; i += BKC_NT) { perm_s[i] = (short)i; tags_s[i] = 0; }
@@ -261,7 +262,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     tm2 = m.aux2;
   }
   if (lead) { a.scale[b] = scale; a.asym[b] = asym; }
-  if (a.check_sym == 1 && n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) {
+  if (csym == 1 && n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) {
     if (lead) {
       a.info[b] = -2; a.n2x2[b] = 0; a.growth[b] = 1.0;
       for (int i = 0; i < n; ++i) { a.perm[(int64_t)b * n + i] = i; a.tags[(int64_t)b * n + i] = 0; }

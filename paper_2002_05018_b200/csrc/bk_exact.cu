@@ -52,6 +52,7 @@ __device__ __forceinline__ void block_argmax(double& v, int& idx, double* vslots
 
 template <int NT>
 __global__ void __launch_bounds__(NT) bk_exact_kernel(BkArgs a, int use_smem) {
+  const int csym = a.check_sym_dev ? *a.check_sym_dev : a.check_sym;   // per-block device flag (block_ldlt)
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ double red_a[NT / 32], red_b[NT / 32], red_c[NT / 32], red_d[NT / 32];
   __shared__ int red_ai[NT / 32];
@@ -78,13 +79,13 @@ __global__ void __launch_bounds__(NT) bk_exact_kernel(BkArgs a, int use_smem) {
     const cplx z = W[(int64_t)i * lda + j];
     scale = fmax(scale, np_abs(z));
     if (j <= i) tm2 = fmax(tm2, x_abs2(z));
-    if (a.check_sym && j < i) asym = fmax(asym, np_abs(x_sub(z, W[(int64_t)j * lda + i])));
+    if (csym && j < i) asym = fmax(asym, np_abs(x_sub(z, W[(int64_t)j * lda + i])));
   }
   scale = block_max<NT>(scale, red_a);
   asym = block_max<NT>(asym, red_b);
   tm2 = block_max<NT>(tm2, red_c);
   if (tid == 0) { a.scale[b] = scale; a.asym[b] = asym; }
-  if (a.check_sym && n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) {
+  if (csym && n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) {
     if (tid == 0) { a.info[b] = -2; a.n2x2[b] = 0; a.growth[b] = 1.0; }
     return;
   }

@@ -421,6 +421,12 @@ int d3m_ordered_average(const void* E, const void* ptr, const void* src, void* o
   return 0;
 }
 
+int d3m_diag_sym_flags(const void* pool, const void* off, const void* n, const void* idx, int count, void* flags,
+                       void* stream) {
+  D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_sym_flags_launch(pool, off, n, idx, count, flags, stream); }));
+  return 0;
+}
+
 int d3m_diag_sym_exact(const void* pool, const void* off, const void* n, int nb, void* flag, void* stream) {
   D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_sym_exact_launch(pool, off, n, nb, flag, stream); }));
   return 0;
@@ -449,7 +455,8 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                         const void* d_trsm_tasks, void* d_pool, void* d_binv, void* d_xbuf, int64_t xbuf_elems,
                         void* d_perm, void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale,
                         void* d_asym, void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead,
-                        int nwait, const int64_t* h_wait_col, void* const* h_wait_ev, void* stream) {
+                        int nwait, const int64_t* h_wait_col, void* const* h_wait_ev, const void* d_check_sym,
+                        void* stream) {
   // diagonal BK kernel for supernodes > kExactBkMax: 0 cluster (default), 1 blocked
   const char* dbk = getenv("D3M_DIAG_BK");
   const int diag_bk_mode = (dbk && dbk[0] == 'b') ? 1 : 0;
@@ -531,6 +538,7 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                   static_cast<int32_t*>(d_n2x2) + j, static_cast<double*>(d_growth) + j,
                   static_cast<int32_t*>(d_info) + j, static_cast<double*>(d_scale) + j,
                   static_cast<double*>(d_asym) + j, C(d_bk_scratch)};
+    if (d_check_sym) a.check_sym_dev = static_cast<const int*>(d_check_sym) + j;   // per-block flag (ABI v8)
     if (nj > 0) {
       // supernodes up to kExactBkMax use the bit-exact unblocked kernel (so a
       // one-block K factors exactly like dense_ldlt_bk, test_block_factor.py:

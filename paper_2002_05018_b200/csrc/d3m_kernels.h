@@ -22,6 +22,7 @@ struct BkArgs {
   double* scale;      // batch: np.abs(W).max()
   double* asym;       // batch: np.abs(W - W.T).max()
   cplx* scratch;      // batch x 4n, used when the staging does not fit smem
+  const int* check_sym_dev = nullptr;   // optional device copy of check_sym (read by the kernel, batch 1)
 };
 
 // Device-resident plan of the persistent block solve (skinny_dmma.cu)
@@ -80,6 +81,8 @@ int d3m_tri_inv_launch(const void* F, int64_t stride_f, const void* perm, int64_
                        int64_t stride_t, void* Binv, int64_t stride_b, int n, int batch, void* stream);
 int d3m_dinv_rows_launch(const void* X, void* P, int64_t R, int n, const void* F, const void* tags, void* stream);
 int d3m_dinv_left_copy_launch(const void* Z, void* U, int n, int m, const void* F, const void* tags, void* stream);
+int d3m_sym_flags_launch(const void* pool, const void* off, const void* n, const void* idx, int count, void* flags,
+                         void* stream);
 int d3m_nonzero_rows_launch(int B, int n, int m, const void* D, void* flag, void* idx, void* count, void* stream);
 int d3m_tri_inv_blocked_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef, int n,
                                void* Linv, void* stream);

@@ -284,3 +284,34 @@ extern "C" int d3m_nonzero_rows_launch(int B, int n, int m, const void* D, void*
                                        static_cast<int*>(count));
   return (int)cudaGetLastError();
 }
+
+// Per-block exact-symmetry flags for block_ldlt's diagonal BK: CTA b checks
+// diagonal block idx[b] (offset off[.], order n[.]) and writes flags[idx[b]]
+// = 2 (bitwise symmetric: the BK reads the lower triangle only) or 1 (the BK
+// runs the reference's full symmetry check).
+__global__ void sym_flags_kernel(const cplx* pool, const int64_t* off, const int64_t* nn, const int64_t* idx,
+                                 int* flags) {
+  const int64_t blk = idx[blockIdx.x];
+  const int n = (int)nn[blk];
+  const cplx* W = pool + off[blk];
+  int bad = 0;
+  for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    if (j < i) {
+      const cplx x = W[(int64_t)i * n + j], y = W[(int64_t)j * n + i];
+      bad |= (__double_as_longlong(x.x) != __double_as_longlong(y.x)) |
+             (__double_as_longlong(x.y) != __double_as_longlong(y.y));
+    }
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) flags[blk] = bad ? 1 : 2;
+}
+
+extern "C" int d3m_sym_flags_launch(const void* pool, const void* off, const void* n, const void* idx, int count,
+                                    void* flags, void* stream) {
+  if (count <= 0) return 0;
+  sym_flags_kernel<<<count, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const cplx*>(pool), static_cast<const int64_t*>(off), static_cast<const int64_t*>(n),
+      static_cast<const int64_t*>(idx), static_cast<int*>(flags));
+  return (int)cudaGetLastError();
+}

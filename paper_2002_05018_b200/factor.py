@@ -516,14 +516,28 @@ def _first_touch(sched: _Schedule) -> dict:
 
 def _upload_K_streamed(K: BlockSparseSym, sched: _Schedule, plan: EliminationPlan, pool, flag):
     """Chunked asynchronous upload of K when every block is a view of one
-    pinned host allocation: chunk 0 holds the diagonal blocks and the blocks
-    first touched by the first block columns; later chunks follow by first
-    touch (_CHUNK_COLS) on a copy stream, each with an event the executor
-    waits on before the first column that touches it (ABI v6).  The sym-check
-    flag is computed after chunk 0.  Returns (wait columns, events, keep-alive)
+    pinned host allocation: every block (diagonal ones included) goes in the
+    chunk of the first block column that touches it (_CHUNK_COLS) on a copy
+    stream, each chunk with an event the executor waits on before that column
+    (ABI v6), and each chunk flags the exact symmetry of its diagonal blocks
+    (ABI v8).  Returns (wait columns, events, keep-alive)
     or None when the inputs do not qualify."""
     t = require_cuda()
     items = list(K.blocks.items())
+    # the chunk plan depends only on the block layout: cached per schedule,
+    # keyed by every block's key and host address (repeated factorisations of
+    # one pinned K skip the validation and the record building, ~4 ms)
+    try:
+        sig = tuple((k, b.data_ptr()) for k, b in items)
+    except AttributeError:
+        return None
+    cache = getattr(sched, "upload_cache", None)
+    if cache is None:
+        cache = sched.upload_cache = {}
+    hit = cache.get(sig)
+    if hit is not None:
+        base, recs, d_rec, plan_chunks, o, kentries = hit
+        return _stream_chunks(sched, pool, flag, base, recs, d_rec, plan_chunks, o, kentries)
     base = None
     for _, b in items:
         if not (_is_tensor(b) and not b.is_cuda and b.is_contiguous() and b.dtype == t.complex128 and b.is_pinned()):
@@ -546,7 +560,7 @@ def _upload_K_streamed(K: BlockSparseSym, sched: _Schedule, plan: EliminationPla
         key = (a, c) if a >= c else (c, a)
         if key not in ft:
             raise FactorConsistencyError(f"block {key} outside the symbolic pattern")
-        ch = 0 if key[0] == key[1] else int(np.searchsorted(bounds, ft[key], side="right")) - 1
+        ch = int(np.searchsorted(bounds, ft[key], side="right")) - 1
         chunks[ch].append(((i, j), b))
     recs = np.zeros(len(items), dtype=_lib.COPY_TASK)
     plan_chunks, r, o = [], 0, 0
@@ -555,13 +569,14 @@ def _upload_K_streamed(K: BlockSparseSym, sched: _Schedule, plan: EliminationPla
         if not entries:
             continue
         r0, maxe = r, 1
-        doff, soff, nby = [], [], []
+        doff, soff, nby, diag = [], [], [], []
         for (i, j), b in entries:
             a, c = int(inv[i]), int(inv[j])
             ni, nj = int(sizes[i]), int(sizes[j])
             key, transpose = ((a, c), 0) if a >= c else ((c, a), 1)
             if key[0] == key[1]:
                 dst, ld = int(sched.diag_off[key[0]]), int(plan.sizes_perm[key[0]])
+                diag.append(key[0])
             else:
                 dst, _, ld = sched.loc[key]
             rows, cols = (ni, nj) if not transpose else (nj, ni)
@@ -574,9 +589,20 @@ def _upload_K_streamed(K: BlockSparseSym, sched: _Schedule, plan: EliminationPla
             o += ni * nj
             r += 1
         plan_chunks.append((bounds[ch], r0, r - r0, maxe, np.asarray(doff, np.int64), np.asarray(soff, np.int64),
-                            np.asarray(nby, np.int64)))
-    stage = empty(max(o, 1))
+                            np.asarray(nby, np.int64), upload_i64(np.asarray(diag, np.int64)) if diag else None,
+                            len(diag)))
     d_rec = upload_bytes(recs)
+    if len(cache) >= 4:
+        cache.clear()
+    cache[sig] = (base, recs, d_rec, plan_chunks, o, kentries)
+    return _stream_chunks(sched, pool, flag, base, recs, d_rec, plan_chunks, o, kentries)
+
+
+def _stream_chunks(sched, pool, flag, base, recs, d_rec, plan_chunks, o, kentries):
+    """Issue the chunked upload planned by _upload_K_streamed on the copy stream."""
+    t = require_cuda()
+    nb = sched.nb
+    stage = empty(max(o, 1))
     cur = t.cuda.current_stream()
     cs = getattr(sched, "copy_stream", None)
     if cs is None:
@@ -587,16 +613,17 @@ def _upload_K_streamed(K: BlockSparseSym, sched: _Schedule, plan: EliminationPla
     csp = _lib.ctypes.c_void_p(cs.cuda_stream)
     H = _lib.hptr
     waits, events = [], []
-    for n, (col, r0, cnt, maxe, doff, soff, nby) in enumerate(plan_chunks):
+    for n, (col, r0, cnt, maxe, doff, soff, nby, d_diag, ndiag) in enumerate(plan_chunks):
         _lib.call("d3m_memcpy_batch", _P(stage), _lib.ctypes.c_void_p(base), H(doff), H(soff), H(nby), cnt, 1, csp)
         _lib.call("d3m_block_copy", _P(stage), _P(pool), _lib.ctypes.c_void_p(d_rec.data_ptr() + r0 * recs.itemsize),
                   cnt, maxe, csp)
-        if n == 0:
-            _lib.call("d3m_diag_sym_exact", _P(pool), _P(sched.d_diag_off), _P(sched.d_sizes), nb, _P(flag), csp)
+        if ndiag:                          # exact-symmetry flags of the chunk's diagonal blocks (as uploaded)
+            _lib.call("d3m_diag_sym_flags", _P(pool), _P(sched.d_diag_off), _P(sched.d_sizes), _P(d_diag), ndiag,
+                      _P(flag), csp)
         ev = t.cuda.Event()
         ev.record(cs)
         if n == 0:
-            cur.wait_event(ev)             # the flag and the first columns' blocks
+            cur.wait_event(ev)             # the first columns' blocks and flags
         else:
             waits.append(col)
             events.append(ev)
@@ -632,11 +659,17 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
     _lib.call("d3m_zero", _P(pool), sched.pool_elems, stream_ptr())
     # exactly symmetric diagonal blocks stay exactly symmetric (mirrored SYM
     # updates): the diagonal BK then needs only the lower triangle
-    flag = t.ones(1, dtype=t.int32, device="cuda")
+    # per-block exact-symmetry flags (2: bitwise symmetric, the BK reads the
+    # lower triangle only; 1: full check), read by each column's BK on the
+    # device (ABI v8): no host sync on the upload of K's diagonal
+    flag = t.ones(max(nb, 1), dtype=t.int32, device="cuda")
     streamed = _upload_K_streamed(K, sched, plan, pool, flag)
     if streamed is None:
         kgroups = _upload_K(K, sched, plan, pool)
-        _lib.call("d3m_diag_sym_exact", _P(pool), _P(sched.d_diag_off), _P(sched.d_sizes), nb, _P(flag), stream_ptr())
+        if getattr(sched, "d_all_blocks", None) is None:
+            sched.d_all_blocks = upload_i64(np.arange(nb, dtype=np.int64))
+        _lib.call("d3m_diag_sym_flags", _P(pool), _P(sched.d_diag_off), _P(sched.d_sizes), _P(sched.d_all_blocks), nb,
+                  _P(flag), stream_ptr())
         wait_cols, wait_ev = np.zeros(1, np.int64), np.zeros(1, np.uint64)
         nwait = 0
     else:
@@ -645,7 +678,7 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
         wait_ev = np.asarray([e.cuda_event for e in events] or [0], dtype=np.uint64)
         if nwait == 0:
             wait_cols = np.zeros(1, np.int64)
-    check_sym = 2 if int(flag.item()) == 1 else 1
+    check_sym = 1                          # superseded per block by the device flags
     perm = t.empty(max(sched.piv_elems, 1), dtype=t.int64, device="cuda")
     tags = t.empty(max(sched.piv_elems, 1), dtype=t.int8, device="cuda")
     info = t.empty(nb, dtype=t.int32, device="cuda")
@@ -663,7 +696,7 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
               H(sched.tiles_next), H(sched.tiles_rest), H(sched.tiles_trsm), _P(sched.d_tasks),
               _P(sched.d_trsm_tasks), _P(pool), _P(binv), _P(xbuf), sched.xbuf_elems, _P(perm), _P(tags),
               _P(info), _P(n2), _P(gr), _P(sc), _P(asy), _P(scratch), float(pivot_tol), check_sym,
-              int(bool(lookahead)), nwait, H(wait_cols), H(wait_ev), stream_ptr())
+              int(bool(lookahead)), nwait, H(wait_cols), H(wait_ev), _P(flag), stream_ptr())
     info_h = info.cpu().numpy()
     bad = np.flatnonzero(info_h != -1)
     if bad.size:

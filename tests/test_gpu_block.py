@@ -367,3 +367,41 @@ def test_refined_solve(cuda, device_k):
         xc = d.block_solve(F, [b[:, c:c + 1] for b in rhs], refine=1)
         for a, b_ in zip(x1, xc):
             assert np.array_equal(a[:, c], b_[:, 0])
+
+
+def test_pinned_streamed_upload_and_host_tensor_solve(cuda):
+    """K given as views of one pinned host allocation takes the chunked,
+    first-touch streamed upload (twice: the second call reuses the cached
+    chunk plan); the factor equals the one from numpy blocks bit for bit, and
+    a solve with pinned host-tensor RHS returns host tensors equal to the
+    numpy-RHS solve."""
+    import torch
+    import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import workloads as wl
+    K, _ = wl.rand_block_system(131, max_blocks=14, max_size=40, density=0.5)
+    while K.nblocks < 10:
+        K, _ = wl.rand_block_system(int(K.nblocks) + 500, max_blocks=14, max_size=40, density=0.5)
+    plan = _plan(K)
+    F0 = d.block_ldlt(K, plan)
+    tot = sum(int(np.asarray(b).size) for b in K.blocks.values())
+    buf = torch.empty(tot, dtype=torch.complex128, pin_memory=True)
+    Kp = d.BlockSparseSym(K.sizes)
+    o = 0
+    for k, b in K.blocks.items():
+        b = np.ascontiguousarray(np.asarray(b, dtype=np.complex128))
+        v = buf[o:o + b.size].view(b.shape)
+        v.copy_(torch.from_numpy(b))
+        Kp.blocks[k] = v
+        o += b.size
+    sched = F0._sched
+    for rep in range(2):
+        F = d.block_ldlt(Kp, plan)
+        assert np.array_equal(F._pool.cpu().numpy(), F0._pool.cpu().numpy()), rep
+    assert len(getattr(sched, "upload_cache", {})) >= 1
+    rng = np.random.default_rng(7)
+    rhs = [rng.standard_normal((int(n), 3)) + 1j * rng.standard_normal((int(n), 3)) for n in K.sizes]
+    x0 = d.block_solve(F0, rhs)
+    xp = d.block_solve(F, [torch.from_numpy(r).pin_memory() for r in rhs])
+    for a, b in zip(x0, xp):
+        assert isinstance(b, torch.Tensor) and not b.is_cuda
+        assert np.array_equal(a, b.numpy())
