@@ -864,19 +864,26 @@ def flow_items(sizes, pattern, panel_rows):
 
 def _residual_launches(F: BlockFactor, cols: int):
     """Grouped-GEMM launches computing r -= K x over K's stored blocks
-    (include/d3m.h d3m_block_residual), cached per factor and RHS count.
+    (include/d3m.h d3m_block_residual), cached per block layout and RHS count.
 
     Stored block (i, j) contributes K_ij x_j to row block i and, off the
     diagonal, K_ij^T x_i to row block j (blockmat.py:93-101's symmetric
     scatter).  Contributions to one target are ordered by (source, term) and
     launch round t carries every target's t-th contribution, so no two tasks
     of a launch write the same rows and the sum order is fixed."""
-    cache = getattr(F, "_res_cache", None)
-    if cache is None:
-        cache = F._res_cache = {}
-    if cols in cache:
-        return cache[cols]
     sched, plan = F._sched, F.plan
+    # the task records depend only on the block layout (groups' entries) and
+    # the RHS count: cached per schedule; the groups' base pointers are
+    # refreshed per factor (a new upload staging buffer each call)
+    cache = getattr(sched, "res_cache", None)
+    if cache is None:
+        cache = sched.res_cache = {}
+    key = (cols, tuple(tuple(e) for _, e in F._kgroups))
+    hit = cache.get(key)
+    if hit is not None:
+        nl, ta, nt, tiles, toff, gidx, d_tasks = hit
+        base = np.asarray([F._kgroups[g][0].data_ptr() for g in gidx], np.uint64)
+        return nl, ta, nt, tiles, toff, base, d_tasks
     inv = plan.order.inverse()
     ks = F._ksizes
     row_off = sched.row_off
@@ -892,7 +899,7 @@ def _residual_launches(F: BlockFactor, cols: int):
     for a, lst in per_target.items():
         for t, (c, term, gi, off, m, k, ta, lda) in enumerate(sorted(lst)):
             rounds.setdefault((t, gi, ta), []).append((a, c, off, m, k, lda))
-    recs, ta_l, nt_l, tiles_l, off_l, base_l = [], [], [], [], [], []
+    recs, ta_l, nt_l, tiles_l, off_l, base_l, g_l = [], [], [], [], [], [], []
     for (t, gi, ta) in sorted(rounds):
         lst = rounds[(t, gi, ta)]
         rec = np.zeros(len(lst), dtype=_lib.GEMM_TASK)
@@ -908,11 +915,14 @@ def _residual_launches(F: BlockFactor, cols: int):
         nt_l.append(len(lst))
         tiles_l.append(tiles)
         base_l.append(F._kgroups[gi][0].data_ptr())
+        g_l.append(gi)
     d_tasks = upload_bytes(np.concatenate(recs))
-    entry = (len(recs), np.asarray(ta_l, np.int32), np.asarray(nt_l, np.int32), np.asarray(tiles_l, np.int32),
-             np.asarray(off_l, np.int64), np.asarray(base_l, np.uint64), d_tasks)
-    cache[cols] = entry
-    return entry
+    arrs = (len(recs), np.asarray(ta_l, np.int32), np.asarray(nt_l, np.int32), np.asarray(tiles_l, np.int32),
+            np.asarray(off_l, np.int64))
+    if len(cache) >= 8:
+        cache.clear()
+    cache[key] = arrs + (g_l, d_tasks)
+    return arrs + (np.asarray(base_l, np.uint64), d_tasks)
 
 
 def block_solve(F: BlockFactor, g: list, refine: int = 0) -> list:
