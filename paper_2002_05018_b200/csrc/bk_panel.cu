@@ -493,9 +493,9 @@ __global__ void bk_panel_finalize_kernel(BkArgs a, const BkState* st, int batch)
 }  // namespace d3m
 
 // Host driver: init, then per panel one panel launch + one grouped GEMM over
-// the batch.  workspace: batch * (n * 65 complex + 64 B state + 64 B task + 8 B + 64 B).
+// the batch.  workspace: batch * (n * 129 complex + 64 B state + 64 B task + 8 B + 64 B).
 namespace d3m {
-constexpr int kPanelLdwMax = 65;      // workspace row pitch for the widest panel (NB = 64)
+constexpr int kPanelLdwMax = 129;     // workspace row pitch for the widest panel (NB = 128)
 
 // Panel loop for one panel width (NB - 1 or NB columns per panel); the
 // rank-<= NB trailing updates of all matrices run on the small-K kernel
@@ -546,7 +546,7 @@ static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* task
       // into freed ring stages) is ~4% faster than the small-K kernel on
       // config 3 at NB = 64; D3M_PANEL_GEMM=s selects the small-K kernel
       static const char* pg = getenv("D3M_PANEL_GEMM");
-      const int rc = (NB == 64 && !(pg && pg[0] == 's'))
+      const int rc = (NB >= 64 && !(pg && pg[0] == 's'))
                          ? d3m_gemm_launch_tm(0, 0, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream)
                          : d3m_gemm_smallk_launch_k(NB, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream);
       if (rc) return rc;
@@ -564,8 +564,14 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
   // panel width 64: rank-<=64 trailing updates cut the trailing-matrix
   // traffic 4x against NB = 16 (config 5 BK: 20.7 s at NB 16, 15.6 s at 32,
   // 13.0 s at 64; configs 2/3: -21% / -17%)
-  int nb = 64;
-  if (const char* env = getenv("D3M_PANEL_NB")) nb = atoi(env) == 64 ? 64 : atoi(env) == 32 ? 32 : 16;
+  // NB = 128 for large subdomains (n >= 8192, config 5): the rank-128 updates
+  // halve the trailing-matrix traffic per flop again, and the longer panel
+  // steps are a small share there
+  int nb = n >= 8192 ? 128 : 64;
+  if (const char* env = getenv("D3M_PANEL_NB")) {
+    const int v = atoi(env);
+    nb = v == 128 ? 128 : v == 64 ? 64 : v == 32 ? 32 : 16;
+  }
   char* w = static_cast<char*>(workspace);
   cplx* Wp = reinterpret_cast<cplx*>(w);
   w += (size_t)batch * n * kPanelLdwMax * sizeof(cplx);
@@ -585,7 +591,8 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
   bk_panel_state_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, red, batch);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
-  const int rc = nb == 64 ? panel_run<64>(a, batch, st, Wp, tasks, tmax, s, stream)
+  const int rc = nb == 128 ? panel_run<128>(a, batch, st, Wp, tasks, tmax, s, stream)
+                 : nb == 64 ? panel_run<64>(a, batch, st, Wp, tasks, tmax, s, stream)
                  : nb == 32 ? panel_run<32>(a, batch, st, Wp, tasks, tmax, s, stream)
                             : panel_run<16>(a, batch, st, Wp, tasks, tmax, s, stream);
   if (rc) return rc;

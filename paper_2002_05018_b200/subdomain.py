@@ -163,7 +163,7 @@ def _domain_bytes(n: int, m: int, r: int) -> int:
     panel workspace)."""
     w = m + r
     # A, D, F, X, Z, C, K, G, the compact D rows of D^T X (<= 0.6 n), panel workspace
-    return 16 * (n * n + n * m + n * r + 2 * n * w + m * w + m * m + m * r + (6 * n * m) // 10) + 65 * 16 * n + 1024
+    return 16 * (n * n + n * m + n * r + 2 * n * w + m * w + m * m + m * r + (6 * n * m) // 10) + 129 * 16 * n + 1024
 
 
 def _free_bytes(t) -> int:

@@ -145,15 +145,20 @@ def test_config3_pivots_and_schur_vs_reference(cuda, keep):
             assert np.linalg.norm(KDh - ref) <= 1e-9 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("n,m,batch,cs", [(600, 40, 3, None), (1030, 17, 2, None), (600, 40, 3, "1"),
-                                          (777, 9, 2, "2"), (777, 9, 2, "4"), (1030, 17, 2, "8")])
-def test_large_subdomain_panel_bk_vs_oracle(cuda, oracle, monkeypatch, n, m, batch, cs):
+@pytest.mark.parametrize("n,m,batch,cs,nb", [(600, 40, 3, None, None), (1030, 17, 2, None, None),
+                                             (600, 40, 3, "1", None), (777, 9, 2, "2", None),
+                                             (777, 9, 2, "4", None), (1030, 17, 2, "8", None),
+                                             (1030, 17, 2, None, "128"), (777, 9, 2, "4", "128")])
+def test_large_subdomain_panel_bk_vs_oracle(cuda, oracle, monkeypatch, n, m, batch, cs, nb):
     """n > 512 takes the batched panel BK (grouped DMMA trailing updates) and
     the blocked solves: pivots bit-exact vs the oracle, K_D / g_d to 1e-10,
-    for every cluster size of the panel kernel (D3M_PANEL_CS)."""
+    for every cluster size of the panel kernel (D3M_PANEL_CS) and the 64- and
+    128-column panels (D3M_PANEL_NB; 128 is the default from n = 8192)."""
     import paper_2002_05018_b200 as d
     if cs is not None:
         monkeypatch.setenv("D3M_PANEL_CS", cs)
+    if nb is not None:
+        monkeypatch.setenv("D3M_PANEL_NB", nb)
     rng = np.random.default_rng(n + m)
     systems, ref = [], []
     for b in range(batch):
