@@ -27,6 +27,7 @@ not shard in this tier), value = all ranks' flops / max time.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -189,12 +190,18 @@ def run_ours(args):
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # timed regions run with the cyclic garbage collector paused (the timeit
+    # convention): a full collection over the plan's host objects costs ~80 ms
+    # and would land in a random step
+    gc.collect()
+    gc.disable()
     with ClockSampler(local) as clk:
         e0.record(s)
         for _ in range(args.steps):
             F, x = step_dev()
         e1.record(s)
         torch.cuda.synchronize()
+    gc.enable()
     _barrier(dist)
     ms_total = _max_over_ranks(dist, e0.elapsed_time(e1))
     ms_step = ms_total / args.steps
@@ -234,6 +241,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_steps = max(3, min(args.steps, 5))
     e2e_samples = []
+    gc.collect()
+    gc.disable()
     for _ in range(e2e_steps):
         t0 = time.perf_counter()
         Fh = d.block_ldlt(Kp, plan)
@@ -241,8 +250,9 @@ def run_ours(args):
         torch.cuda.synchronize()
         e2e_samples.append((time.perf_counter() - t0) * 1e3)
         del Fh                                       # the caller releases the factor before the next solve
-    # median of the samples (all are reported): one host-side hiccup (GC, a
-    # page-locking stall) in a few-sample run otherwise dominates the mean
+    gc.enable()
+    # median of the samples (all are reported): one host-side hiccup in a
+    # few-sample run otherwise dominates the mean
     e2e_ms = _max_over_ranks(dist, float(np.median(e2e_samples)))
     e2e_value = flops_step * ws / (e2e_ms * 1e-3) / 1e12
     del xh
