@@ -16,6 +16,7 @@
 // number of columns in the call (block_solve's k-RHS == k x 1-RHS property,
 // factor.py:271-279).  D^-1 uses the exact helpers (reference rounding).
 #include <algorithm>
+#include <cstdlib>
 #include "d3m_common.cuh"
 #include "d3m_kernels.h"
 
@@ -585,6 +586,63 @@ __global__ void __launch_bounds__(256) tri_inv_cols16(const cplx* __restrict__ F
   }
 }
 
+// One CTA per column q of X = L^-1 (n CTAs): the column's 16-row blocks
+// below the diagonal block are the dependent chain (at most 15 steps at
+// n = 256), each step a 16-row dot over the rows already solved (16 lanes per
+// row, butterfly) and the 16 x 16 product with Dinv_i.  Spreads the block
+// columns' work over n SMs instead of n/16.
+__global__ void __launch_bounds__(256) tri_inv_colq(const cplx* __restrict__ F, const int64_t* __restrict__ perm,
+                                                    const int8_t* __restrict__ tags, const cplx* __restrict__ Dinv,
+                                                    cplx* Binv, cplx* Linv, int n) {
+  __shared__ cplx xs[TI_NMAX];
+  __shared__ cplx sv[TI_B];
+  const int q = blockIdx.x, k = q / TI_B, c0 = k * TI_B, tid = threadIdx.x;
+  const int nbk = (n + TI_B - 1) / TI_B;
+  const int r = tid >> 4, l16 = tid & 15;
+  for (int i = tid; i < n; i += 256) xs[i] = mk(0.0, 0.0);
+  __syncthreads();
+  if (tid < TI_B && c0 + tid < n) xs[c0 + tid] = Dinv[((int64_t)k * TI_B + tid) * TI_B + (q - c0)];
+  __syncthreads();
+  for (int i = k + 1; i < nbk; ++i) {
+    const int row = i * TI_B + r, w = TI_B * (i - k);
+    cplx a = mk(0.0, 0.0);
+    if (row < n) {
+      const cplx* Lr = F + (int64_t)row * n + c0;
+      const bool zr = r == 0 && tags[i * TI_B - 1] == 2;     // L[16i, 16i-1] of a 2x2 pivot
+      for (int m = l16; m < w; m += 16) {
+        cplx l = Lr[m];
+        if (zr && m == w - 1) l = mk(0.0, 0.0);
+        const cplx x = xs[c0 + m];
+        a = mk(a.x + (l.x * x.x - l.y * x.y), a.y + (l.x * x.y + l.y * x.x));
+      }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+      a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+    }
+    if (l16 == 0) sv[r] = a;
+    __syncthreads();
+    if (tid < TI_B) {
+      const cplx* Di = Dinv + ((int64_t)i * TI_B + tid) * TI_B;
+      cplx acc = mk(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < TI_B; ++c) {
+        const cplx d = Di[c], t = sv[c];
+        acc = mk(acc.x + (d.x * t.x - d.y * t.y), acc.y + (d.x * t.y + d.y * t.x));
+      }
+      if (i * TI_B + tid < n) xs[i * TI_B + tid] = mk(-acc.x, -acc.y);
+    }
+    __syncthreads();
+  }
+  const int64_t pc = perm[q];
+  for (int row = tid; row < n; row += 256) {
+    const cplx v = xs[row];
+    Binv[(int64_t)row * n + pc] = v;
+    if (Linv) Linv[(int64_t)row * n + q] = v;
+  }
+}
+
 }  // namespace d3m
 
 // blocked L^-1 P + D^-1 coefficients for n <= 256 (-22 above)
@@ -607,8 +665,13 @@ extern "C" int d3m_tri_inv_blocked_launch(const void* F, const void* perm, const
   auto Fp = static_cast<const cplx*>(F);
   auto tp = static_cast<const int8_t*>(tags);
   tri_inv_diag16<<<nbk, 64, 0, s>>>(Fp, tp, dinv, static_cast<cplx*>(coef), n);
-  tri_inv_cols16<<<nbk, 256, kTiSmem, s>>>(Fp, static_cast<const int64_t*>(perm), tp, dinv, static_cast<cplx*>(Binv),
-                                           static_cast<cplx*>(Linv), n);
+  static const int colq = [] { const char* e = getenv("D3M_TRI_COLQ"); return e ? atoi(e) : 1; }();
+  if (colq)
+    tri_inv_colq<<<n, 256, 0, s>>>(Fp, static_cast<const int64_t*>(perm), tp, dinv, static_cast<cplx*>(Binv),
+                                   static_cast<cplx*>(Linv), n);
+  else
+    tri_inv_cols16<<<nbk, 256, kTiSmem, s>>>(Fp, static_cast<const int64_t*>(perm), tp, dinv,
+                                             static_cast<cplx*>(Binv), static_cast<cplx*>(Linv), n);
   return (int)cudaGetLastError();
 }
 
