@@ -198,6 +198,9 @@ __host__ __device__ inline int64_t bkc_entries(int n) {    // per-CTA capacity (
 // follows the end of its step s-2 bulk update.
 template <int CS>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_kernel(BkArgs a) {
+#ifdef D3M_BK_PROFILE
+  const long long t_entry = clock64();
+#endif
   const int csym = a.check_sym_dev ? *a.check_sym_dev : a.check_sym;   // per-block device flag (block_ldlt)
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char bkc_smem[];
@@ -308,6 +311,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     xpost<CS>(inbox[0], rank, xslot(v, own, -1.0, vi), &mbar[0]);
   }
 #ifdef D3M_BK_PROFILE
+  const long long t_loop0 = clock64();
   double pacc[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) pacc[i] = 0.0;
@@ -610,6 +614,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     const XSlot mf = xmerge<CS>(inbox[s % 3], &xmerged);
     if (gthread && s >= 2) grow(mf.aux, ks2, k02);
   }
+#ifdef D3M_BK_PROFILE
+  const long long t_loop1 = clock64();
+#endif
   // ---- write back: diagonal / D entries and the trailing part in place; the
   //      L entries of the columns of step t move by the interchanges of the
   //      steps after t (kernels.py:96-98), applied here in reverse order ------
@@ -659,6 +666,12 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     double* prof = reinterpret_cast<double*>(a.scratch);
 #pragma unroll
     for (int i = 0; i < 8; ++i) prof[(tid == 0 ? 0 : 8) + i] = pacc[(tid == 0 ? 0 : 8) + i];
+    if (tid == 0) {   // prologue, step loop, write-back (cycles)
+      const long long t_end = clock64();
+      prof[16] = (double)(t_loop0 - t_entry);
+      prof[17] = (double)(t_loop1 - t_loop0);
+      prof[18] = (double)(t_end - t_loop1);
+    }
   }
 #endif
   cl.sync();     // no CTA exits while a peer may still push into its shared memory

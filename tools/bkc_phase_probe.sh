@@ -25,7 +25,7 @@ for j in range(4):
     W = to_device(blk).clone()
     perm = torch.empty(n, dtype=torch.int64, device="cuda"); tags = torch.empty(n, dtype=torch.int8, device="cuda")
     z = lambda t: torch.zeros(1, dtype=t, device="cuda")
-    scr = torch.zeros(16, dtype=torch.float64, device="cuda")
+    scr = torch.zeros(32, dtype=torch.float64, device="cuda")
     rc = lib.d3m_bk_blocked_factor(1, n, _lib.ptr(W), n*n, n, ctypes.c_double(1e-12), 1, _lib.ptr(perm), _lib.ptr(tags),
         _lib.ptr(z(torch.int32)), _lib.ptr(z(torch.float64)), _lib.ptr(z(torch.int32)), _lib.ptr(z(torch.float64)), _lib.ptr(z(torch.float64)), _lib.ptr(scr), stream_ptr())
     torch.cuda.synchronize()
@@ -33,5 +33,6 @@ for j in range(4):
     pn = ["wait", "merge", "decide+rowmax+swap", "arrive", "l0", "col-update+push+hypot", "argmax+post"]
     bn = ["wait", "merge", "refill+mult+arrive", "bulk"]
     print("pivot warp:", " ".join(f"{nm}={v/1e3:.0f}K" for nm, v in zip(pn, p[:7])), f"total={p[:8].sum()/1e6:.2f}M cycles")
-    print("bulk warps:", " ".join(f"{nm}={v/1e3:.0f}K" for nm, v in zip(bn, p[8:12])), f"total={p[8:].sum()/1e6:.2f}M cycles")
+    print("bulk warps:", " ".join(f"{nm}={v/1e3:.0f}K" for nm, v in zip(bn, p[8:12])), f"total={p[8:16].sum()/1e6:.2f}M cycles")
+    print(f"CTA 0: prologue {p[16]/1e3:.0f}K, step loop {p[17]/1e3:.0f}K, write-back {p[18]/1e3:.0f}K cycles")
 PY
