@@ -362,10 +362,10 @@ def _fem_secondary(which: str, reps: int) -> dict:
         for s in systems:
             s.factor, s._d3m_D, s._d3m_X = None, None, None
         timers = {}
+        # a collection before each run (not a paused collector: the pipeline's
+        # temporaries must be reclaimable, or the allocator grows instead of reusing)
         gc.collect()
-        gc.disable()
         sol, _, R, plan, F = fem3d.solve_d3m(model, rhs=None, keep="auto", timers=timers, systems=systems)
-        gc.enable()
         if (runs == 1 or i > 0) and (best is None or timers["d3m_total"] < best["d3m_total"]):
             best = timers
         keep = "solution" if systems[0].factor.released else "factor"
