@@ -609,8 +609,18 @@ __global__ void __launch_bounds__(256) tri_inv_colq(const cplx* __restrict__ F, 
     if (row < n) {
       const cplx* Lr = F + (int64_t)row * n + c0;
       const bool zr = r == 0 && tags[i * TI_B - 1] == 2;     // L[16i, 16i-1] of a 2x2 pivot
-      for (int m = l16; m < w; m += 16) {
-        cplx l = Lr[m];
+      // all of this lane's L loads first (one memory round trip per step), then the sum
+      cplx lv[TI_NMAX / TI_B];
+#pragma unroll
+      for (int j = 0; j < TI_NMAX / TI_B; ++j) {
+        const int m = l16 + TI_B * j;
+        lv[j] = m < w ? Lr[m] : mk(0.0, 0.0);
+      }
+#pragma unroll
+      for (int j = 0; j < TI_NMAX / TI_B; ++j) {
+        const int m = l16 + TI_B * j;
+        if (m >= w) break;
+        cplx l = lv[j];
         if (zr && m == w - 1) l = mk(0.0, 0.0);
         const cplx x = xs[c0 + m];
         a = mk(a.x + (l.x * x.x - l.y * x.y), a.y + (l.x * x.y + l.y * x.x));
