@@ -588,7 +588,8 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
     // them and targets columns >= j+2, so it may start now, concurrently with
     // the "next" update below (disjoint targets); the side stream keeps the
     // rest updates of consecutive columns in order.
-    if (lookahead && t1 > tn) cudaEventRecord(ev_next, s0);
+    static const int rest_after_next = [] { const char* e = getenv("D3M_REST_AFTER_NEXT"); return e ? atoi(e) : 1; }();
+    if (lookahead && t1 > tn && !rest_after_next) cudaEventRecord(ev_next, s0);
     if (rest_pending) {          // next-targets of column j+1 were also rest-targets of j-1
       cudaStreamWaitEvent(s0, ev_rest, 0);
       rest_pending = false;
@@ -597,6 +598,9 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
       D3M_TRY(launch(kClsGemm, s0, [&] {
         return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + t0, (int)(tn - t0), (int)h_tiles_next[j], s0);
       }));
+    // (default; D3M_REST_AFTER_NEXT=0 starts it beside the next update) the bulk update starts only after the next-column
+    // update, which then has the SMs to itself)
+    if (lookahead && t1 > tn && rest_after_next) cudaEventRecord(ev_next, s0);
     if (t1 > tn) {
       if (lookahead) {
         cudaStreamWaitEvent(side, ev_next, 0);
