@@ -585,9 +585,10 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
     }
     const int64_t t0 = h_task_ptr[j], tn = h_task_next[j], t1 = h_task_ptr[j + 1];
     // X_j / L_j are ready: the bulk ("rest") update of column j only reads
-    // them and targets columns >= j+2, so it may start now, concurrently with
-    // the "next" update below (disjoint targets); the side stream keeps the
-    // rest updates of consecutive columns in order.
+    // them and targets columns >= j+2, so it could start now, beside the
+    // "next" update below (disjoint targets); by default it waits for the next
+    // update (below).  The side stream keeps the rest updates of consecutive
+    // columns in order.
     static const int rest_after_next = [] { const char* e = getenv("D3M_REST_AFTER_NEXT"); return e ? atoi(e) : 1; }();
     if (lookahead && t1 > tn && !rest_after_next) cudaEventRecord(ev_next, s0);
     if (rest_pending) {          // next-targets of column j+1 were also rest-targets of j-1
@@ -598,8 +599,8 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
       D3M_TRY(launch(kClsGemm, s0, [&] {
         return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + t0, (int)(tn - t0), (int)h_tiles_next[j], s0);
       }));
-    // (default; D3M_REST_AFTER_NEXT=0 starts it beside the next update) the bulk update starts only after the next-column
-    // update, which then has the SMs to itself)
+    // default: the bulk update starts once the next-column update has finished,
+    // which then has the SMs to itself (D3M_REST_AFTER_NEXT=0: it starts beside it)
     if (lookahead && t1 > tn && rest_after_next) cudaEventRecord(ev_next, s0);
     if (t1 > tn) {
       if (lookahead) {
