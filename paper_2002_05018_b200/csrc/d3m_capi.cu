@@ -463,7 +463,7 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
   // rest-update tiles above which a column's diagonal BK runs on a 4-CTA cluster (D3M_BKC4_TILES)
   static const int64_t bkc4_tiles = [] {
     const char* e = getenv("D3M_BKC4_TILES");
-    return e ? (int64_t)atoll(e) : (int64_t)8000;
+    return e ? (int64_t)atoll(e) : (int64_t)5000;
   }();
   // Streams: the caller's stream hands over to a high-priority critical
   // stream (BK -> L^-1 -> panel GEMM -> D^-1 -> next-column update) and a
