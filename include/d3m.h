@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define D3M_ABI_VERSION 8
+#define D3M_ABI_VERSION 9
 
 int d3m_abi_version(void);
 const char* d3m_last_error(void);
@@ -43,14 +43,12 @@ int d3m_bk_factor_batched(int batch, int n, void* W, int64_t stride_w, int lda, 
                           void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
                           void* scratch, void* stream);
 
-/* Same contract as d3m_bk_factor_batched with the blocked shared-memory
- * panel kernel (zlasyf-style): identical pivot decisions whenever no test
- * sits within rounding of its threshold, values to rounding; growth is the
- * per-panel geometric mean of the trailing-max ratio.  Used for the
- * supernode diagonal blocks of block_ldlt wider than 128. */
-int d3m_bk_blocked_factor(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
-                          void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
-                          void* scratch, void* stream);
+/* Largest block order the bit-exact cluster BK (bk_cluster.cu) holds in the
+ * shared memory of a cs-CTA cluster (cs = 2, 4, 8, 16; 0 = any size).
+ * block_ldlt factors supernodes wider than 128 and up to this order on the
+ * cluster kernel, wider ones on the single-CTA exact kernel; both are
+ * bit-identical to kernels.py:36-146.  Host-only query (no device call). */
+int d3m_bk_cluster_max_n(int cs);
 
 /* Multi-RHS solve M X = B with packed factors: gather by perm, unit-L forward,
  * D^-1, unit-L^T backward, scatter.  Replaces DenseFactor.solve

@@ -23,7 +23,7 @@ F64 = ctypes.c_double
 _SIGNATURES = {
     "d3m_abi_version": [],
     "d3m_bk_factor_batched": [I32, I32, P, I64, I32, F64, I32, P, P, P, P, P, P, P, P, P],
-    "d3m_bk_blocked_factor": [I32, I32, P, I64, I32, F64, I32, P, P, P, P, P, P, P, P, P],
+    "d3m_bk_cluster_max_n": [I32],
     "d3m_ldlt_solve_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P],
     "d3m_zgemm_grouped": [I32, I32, P, P, P, P, I32, P, P],
     "d3m_gemm_set_form": [I32],

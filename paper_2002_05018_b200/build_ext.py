@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 OUT = os.path.join(HERE, "libd3m.so")
-SOURCES = ["bk_exact.cu", "bk_blocked.cu", "bk_cluster.cu", "zgemm_dmma.cu", "ldlt_solve.cu", "skinny_dmma.cu", "bk_panel.cu", "solve_blocked.cu", "d3m_misc.cu", "d3m_capi.cu"]
+SOURCES = ["bk_exact.cu", "bk_cluster.cu", "zgemm_dmma.cu", "ldlt_solve.cu", "skinny_dmma.cu", "bk_panel.cu", "solve_blocked.cu", "d3m_misc.cu", "d3m_capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
 

@@ -192,10 +192,11 @@ __host__ __device__ inline int64_t bkc_entries(int n) {    // per-CTA capacity (
 //     computes all of them) and the L column of the own rows, then the rank-1
 //     / rank-2 update of the columns > k0 of the own rows, overlapping the
 //     next step's exchange.
-// Broadcast vectors and inboxes are triple-buffered by step: the buffer a
-// peer fills during its step s was last read here in step s-2, and the peer
-// only reaches step s after this CTA pushed its step s-1 column, which
-// follows the end of its step s-2 bulk update.
+// The pivot-column vector and the inboxes are triple-buffered by step: the
+// buffer a peer fills during its step s was last read here in step s-2, and
+// the peer only reaches step s after this CTA pushed its step s-1 column,
+// which follows the end of its step s-2 bulk update.  The rowmax columns
+// (k+1, imax) are filled and read inside one step: double-buffered.
 template <int CS>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_kernel(BkArgs a) {
 #ifdef D3M_BK_PROFILE
@@ -222,8 +223,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
   cplx* Rl = reinterpret_cast<cplx*>(bkc_smem);      // own packed lower rows
   cplx* ls = Rl + cap;                                 // l_j / wk_j of every row (computed locally)
   cplx* ws = ls + n;                                   // wkp_j (2x2)
-  cplx* vec = ws + n;                                  // broadcast vectors [3][3][n]
-  short* perm_s = reinterpret_cast<short*>(vec + 9 * (int64_t)n);
+  cplx* vec = ws + n;                                  // broadcast vectors: A [3][n], B [2][n], C [2][n]
+  short* perm_s = reinterpret_cast<short*>(vec + 7 * (int64_t)n);
   short* qmap = perm_s + n;                            // write-back row map
   short* stk = qmap + n;                               // per step: k, kstep, kp (-1: no interchange)
   int8_t* tags_s = reinterpret_cast<int8_t*>(stk + 3 * n);
@@ -321,10 +322,14 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
   unsigned rphase = 0;
   double pend_usq = 0.0;
   while (k < n) {
+    // column k (cA) is pushed during the previous step: triple-buffered.
+    // Columns k+1 / imax (cB, cC) are pushed and read inside step s; a peer
+    // reaches step s+2's push only after this CTA's step s+1 merge (which ends
+    // the step-s bulk), so two buffers suffice.
     const int bs = s % 3;
-    cplx* cA = vec + (int64_t)(bs * 3 + 0) * n;
-    cplx* cB = vec + (int64_t)(bs * 3 + 1) * n;
-    cplx* cC = vec + (int64_t)(bs * 3 + 2) * n;
+    cplx* cA = vec + (int64_t)bs * n;
+    cplx* cB = vec + (int64_t)(3 + (s & 1)) * n;
+    cplx* cC = vec + (int64_t)(5 + (s & 1)) * n;
     // ---- 1. column k and the argmax slots have landed; merge ---------------
     if (tid == 0) mbar_arm(&mbar[bs], (unsigned)(n - k) * 16u + CS * kSlotBytes);
     mbar_wait(&mbar[bs], (unsigned)(s / 3) & 1u);
@@ -450,7 +455,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
           p0 = x_mul(d21s, x_sub(x_mul(d22, y), x));                          // wkp
         }
         BKC_MARK(0, 4);
-        cplx* cAn = vec + (int64_t)(nb * 3) * n;
+        cplx* cAn = vec + (int64_t)nb * n;
         const uint32_t nbar = saddr(&mbar[nb]);
         for (int q = qk0 + lane; q < nown; q += 32) {
           const int i = rank + q * CS;
@@ -678,12 +683,47 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
 }
 
 template <int CS>
-static int bkc_launch(BkArgs* a, int batch, cudaStream_t s) {
-  // own rows + ls, ws (2n) + broadcast vectors (9n) complex; perm, row map
+static size_t bkc_smem_bytes(int n) {
+  // own rows + ls, ws (2n) + broadcast vectors (7n) complex; perm, row map
   // (int16), step records (3 x int16), tags (int8): 11n bytes
-  const size_t smem = sizeof(cplx) * (size_t)(bkc_entries<CS>(a->n) + 11 * (int64_t)a->n) + 11 * (size_t)a->n + 16;
-  if (smem > 220 * 1024 || a->n > BKC_JPT * (BKC_NT - 32)) return -22;   // the CTA owns its SM
+  return sizeof(cplx) * (size_t)(bkc_entries<CS>(n) + 9 * (int64_t)n) + 11 * (size_t)n + 16;
+}
+constexpr size_t kBkcSmemMax = 220 * 1024;
+
+template <int CS>
+static bool bkc_fits(int n) { return bkc_smem_bytes<CS>(n) <= kBkcSmemMax && n <= BKC_JPT * (BKC_NT - 32); }
+
+template <int CS>
+static int bkc_launch(BkArgs* a, int batch, cudaStream_t s) {
+  const size_t smem = bkc_smem_bytes<CS>(a->n);
+  if (!bkc_fits<CS>(a->n)) return -22;   // the CTA owns its SM
   cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (CS == 16) {
+    // 16 is a non-portable cluster size: check once that a cluster of
+    // full-SM CTAs can be resident on this part
+    static int ok16 = -1;
+    if (ok16 < 0) {
+      cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBkcSmemMax);
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 16;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(16);
+      cfg.blockDim = dim3(BKC_NT);
+      cfg.dynamicSmemBytes = kBkcSmemMax;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      ok16 = (cudaOccupancyMaxActiveClusters(&nclusters, bk_cluster_kernel<CS>, &cfg) == cudaSuccess &&
+              nclusters > 0) ? 1 : 0;
+      cudaGetLastError();
+      cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    if (!ok16) return -22;
+  }
   bk_cluster_kernel<CS><<<batch * CS, BKC_NT, smem, s>>>(*a);
   return (int)cudaGetLastError();
 }
@@ -698,7 +738,9 @@ extern "C" int d3m_bk_cluster_launch(d3m::BkArgs* a, int batch, void* stream) {
   return d3m_bk_cluster_launch_cs(a, batch, 0, stream);
 }
 
-// cs: cluster size (2, 4 or 8); 0 = D3M_BKC_CS or 8
+// cs: cluster size (2, 4, 8 or 16); 0 = D3M_BKC_CS or 8.  A block that does
+// not fit the requested size's shared memory moves to the next larger
+// cluster (8, then 16); -22 when it fits none.
 extern "C" int d3m_bk_cluster_launch_cs(d3m::BkArgs* a, int batch, int cs, void* stream) {
   using namespace d3m;
   if (batch <= 0 || a->n <= 0) return 0;
@@ -711,7 +753,21 @@ extern "C" int d3m_bk_cluster_launch_cs(d3m::BkArgs* a, int batch, int cs, void*
   switch (cs) {
     case 2: rc = bkc_launch<2>(a, batch, s); break;
     case 4: rc = bkc_launch<4>(a, batch, s); break;
+    case 16: return bkc_launch<16>(a, batch, s);
     default: break;
   }
-  return rc == -22 ? bkc_launch<8>(a, batch, s) : rc;
+  if (rc == -22) rc = bkc_launch<8>(a, batch, s);
+  return rc == -22 ? bkc_launch<16>(a, batch, s) : rc;
+}
+
+// largest n the cluster kernel holds at cluster size cs (0: the largest of any size)
+extern "C" int d3m_bk_cluster_max_n(int cs) {
+  using namespace d3m;
+  int best = 0;
+  for (int n = 1; n <= BKC_JPT * (BKC_NT - 32); ++n) {
+    const bool f = cs == 2 ? bkc_fits<2>(n) : cs == 4 ? bkc_fits<4>(n) : cs == 8 ? bkc_fits<8>(n)
+                 : cs == 16 ? bkc_fits<16>(n) : (bkc_fits<8>(n) || bkc_fits<16>(n));
+    if (f) best = n;
+  }
+  return best;
 }

@@ -14,7 +14,7 @@
 // columns).  Pivot decisions match the reference whenever no test sits
 // within rounding of its threshold (measured margins >= 1.3e-4 on config 3);
 // growth is reported per panel (per-step geometric mean of the trailing-max
-// ratio), as for bk_blocked.cu.
+// ratio).
 #include <algorithm>
 #include <cstdlib>
 #include <cooperative_groups.h>

@@ -113,25 +113,6 @@ int d3m_bk_factor_batched(int batch, int n, void* W, int64_t stride_w, int lda, 
   return 0;
 }
 
-int d3m_bk_blocked_factor(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
-                          void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
-                          void* scratch, void* stream) {
-  if (batch < 0 || n < 0 || lda < n) return fail(-22, "d3m_bk_blocked_factor: bad shape");
-  d3m::BkArgs a{C(W), stride_w, n, lda, pivot_tol, check_sym, static_cast<int64_t*>(perm), static_cast<int8_t*>(tags),
-                static_cast<int32_t*>(n2x2), static_cast<double*>(growth), static_cast<int32_t*>(info),
-                static_cast<double*>(scale), static_cast<double*>(asym), C(scratch)};
-  const char* dbk = getenv("D3M_DIAG_BK");      // dev switch: 'c' = cluster-resident exact kernel
-  D3M_TRY(launch(kClsBk, stream, [&] {
-    if (dbk && dbk[0] == 'c') {
-      const int rc = d3m_bk_cluster_launch(&a, batch, stream);
-      if (rc != -22) return rc;
-    }
-    const int rc = d3m_bk_blocked_launch(&a, batch, stream);
-    return rc == -22 ? d3m_bk_launch(&a, batch, stream) : rc;
-  }));
-  return 0;
-}
-
 int d3m_ldlt_solve_batched(int batch, int n, const void* F, int64_t stride_f, const void* perm, int64_t stride_p,
                            const void* tags, int64_t stride_t, void* B, int64_t stride_b, int ldb, int m, void* work,
                            void* stream) {
@@ -457,9 +438,6 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                         void* d_asym, void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead,
                         int nwait, const int64_t* h_wait_col, void* const* h_wait_ev, const void* d_check_sym,
                         void* stream) {
-  // diagonal BK kernel for supernodes > kExactBkMax: 0 cluster (default), 1 blocked
-  const char* dbk = getenv("D3M_DIAG_BK");
-  const int diag_bk_mode = (dbk && dbk[0] == 'b') ? 1 : 0;
   // rest-update tiles above which a column's diagonal BK runs on a 4-CTA cluster (D3M_BKC4_TILES)
   static const int64_t bkc4_tiles = [] {
     const char* e = getenv("D3M_BKC4_TILES");
@@ -543,18 +521,14 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
       // supernodes up to kExactBkMax use the bit-exact unblocked kernel (so a
       // one-block K factors exactly like dense_ldlt_bk, test_block_factor.py:
       // 24-32); wider ones the bit-exact cluster kernel (lower triangle in the
-      // cluster's shared memory), else the blocked shared-memory panel kernel
-      // (pivots identical, values to rounding), else the exact one
+      // cluster's shared memory, 8- or 16-CTA clusters), else the exact one
       D3M_TRY(launch(kClsBk, s0, [&] {
         if (nj <= kExactBkMax) return d3m_bk_launch(&a, 1, s0);
-        if (diag_bk_mode != 1) {          // cluster-resident exact BK (bk_cluster.cu)
-          // 4-CTA clusters while the column's bulk update is long enough to hide the slower BK
-          // (frees 4 SMs for the update GEMMs), 8-CTA clusters on the exposed chain at the ends
-          const int cs = (lookahead && h_tiles_rest[j] >= bkc4_tiles) ? 4 : 0;
-          const int rc = d3m_bk_cluster_launch_cs(&a, 1, cs, s0);
-          if (rc != -22) return rc;
-        }
-        const int rc = d3m_bk_blocked_launch(&a, 1, s0);
+        // 4-CTA clusters while the column's bulk update is long enough to hide the slower BK
+        // (frees 4 SMs for the update GEMMs), 8-CTA clusters on the exposed chain at the ends;
+        // a block too wide for the requested size moves to a larger cluster
+        const int cs = (lookahead && h_tiles_rest[j] >= bkc4_tiles) ? 4 : 0;
+        const int rc = d3m_bk_cluster_launch_cs(&a, 1, cs, s0);
         return rc == -22 ? d3m_bk_launch(&a, 1, s0) : rc;
       }));
       // Binv_j = L_jj^-1 P_j (also used by block_solve) + D_jj^-1 coefficients

@@ -52,9 +52,9 @@ struct SolveBatch {
 
 extern "C" {
 int d3m_bk_launch(d3m::BkArgs* a, int batch, void* stream);
-int d3m_bk_blocked_launch(d3m::BkArgs* a, int batch, void* stream);
 int d3m_bk_cluster_launch(d3m::BkArgs* a, int batch, void* stream);
 int d3m_bk_cluster_launch_cs(d3m::BkArgs* a, int batch, int cs, void* stream);
+int d3m_bk_cluster_max_n(int cs);
 int d3m_skinny_launch(int ta, const void* A, int lda, int M, int K, const void* B, int ldb, const void* bmap, int N,
                       void* C, int ldc, const void* cmap, int mode, int kchunk, void* stream);
 int d3m_block_solve_persistent_launch(void* plan, void* stream);

@@ -210,21 +210,33 @@ def test_reference_kats(cuda):
         d.block_ldlt(K, _plan(K, d.identity_ordering(2)))
 
 
-@pytest.mark.parametrize("n,sym_exact", [(200, True), (256, True), (257, False), (360, True)])
-def test_cluster_diag_bk_is_bit_exact(cuda, monkeypatch, n, sym_exact):
+@pytest.mark.parametrize("n,sym_exact", [(200, True), (256, True), (257, False), (360, True), (384, True),
+                                         (447, True), (456, False), (512, True), (600, True)])
+def test_cluster_diag_bk_is_bit_exact(cuda, oracle, monkeypatch, n, sym_exact):
     """Supernodes wider than 128 take the cluster-resident exact BK
-    (bk_cluster.cu): a one-block K factors bit for bit like dense_ldlt_bk
-    (the single-CTA exact kernel) -- L, d, e, perm, tags, growth -- for the
-    known-symmetric prologue and the full symmetry check alike, and for every
-    cluster size."""
+    (bk_cluster.cu; 8-CTA clusters up to n = 400, 16-CTA clusters up to 526,
+    the config-5 supernodes are 447-456 wide): a one-block K factors bit for
+    bit like the CPU oracle (the restatement of kernels.py:36-146) and like
+    dense_ldlt_bk (the single-CTA exact kernel) -- L, d, e, perm, tags,
+    growth -- for the known-symmetric prologue and the full symmetry check
+    alike, and for every cluster size (a size that does not fit moves to a
+    larger cluster; n = 600 fits none and takes the exact kernel)."""
     import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import _lib
     M = rand_complex_symmetric(n, n)
     M[np.diag_indices(n)] += np.random.default_rng(n).uniform(-1, 1, n)
     if not sym_exact:       # not exactly symmetric (within 1e-12): full check path
         M[5, 3] += 1e-15 * abs(M[5, 3])
     ref = d.dense_ldlt_bk(M)
     assert ref.n_2x2 > 0
-    for cs in ("8", "4", "2"):          # a size that does not fit falls back to 8
+    if n >= 384:
+        fo = oracle.dense_ldlt_bk(M)
+        assert np.array_equal(ref.perm, fo.perm) and np.array_equal(ref.tags, fo.tags)
+        assert np.array_equal(np.tril(ref.packed.cpu().numpy()), np.tril(fo.packed))
+        assert ref.growth == fo.growth
+    lib = _lib.load()
+    assert lib.d3m_bk_cluster_max_n(16) >= 512 and lib.d3m_bk_cluster_max_n(8) >= 384
+    for cs in ("16", "8", "4", "2"):
         monkeypatch.setenv("D3M_BKC_CS", cs)
         K = d.from_blocks([n], [(0, 0, M)])
         F = d.block_ldlt(K, _plan(K))
