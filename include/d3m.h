@@ -38,10 +38,19 @@ const char* d3m_last_error(void);
  * W: batch x (n x lda) with stride_w elements between matrices.
  * Outputs per matrix: perm[n] int64, tags[n] int8, n2x2 int32, growth f64,
  * info int32, scale f64, asym f64.  scratch: batch*4*n complex, needed only
- * when 64*n bytes exceed the shared-memory staging (n > 3200). */
+ * when 64*n bytes exceed the shared-memory staging (n > 3200).
+ * margin (ABI v9; NULL = not tracked): batch x 2 f64 pivot-decision
+ * diagnostics -- [0] the minimum over all steps of the relative distance of
+ * every evaluated BK test (kernels.py:59-77: singularity, alpha colmax,
+ * alpha colmax^2 / rowmax, alpha rowmax) to its threshold, [1] the minimum
+ * relative gap between the colmax argmax winner and the runner-up.  A kernel
+ * whose arithmetic differs from the reference's by rounding takes the
+ * reference's decisions whenever both stay well above ~1e-14.  The same
+ * argument on d3m_bk_panel_batched, d3m_schur_reduce_batched and
+ * (per block column) d3m_block_ldlt_exec. */
 int d3m_bk_factor_batched(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
                           void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
-                          void* scratch, void* stream);
+                          void* scratch, void* margin, void* stream);
 
 /* Largest block order the bit-exact cluster BK (bk_cluster.cu) holds in the
  * shared memory of a cs-CTA cluster (cs = 2, 4, 8, 16; 0 = any size).
@@ -67,7 +76,7 @@ int d3m_ldlt_solve_batched(int batch, int n, const void* F, int64_t stride_f, co
  * bytes.  Used by d3m_schur_reduce_batched for n > 512. */
 int d3m_bk_panel_batched(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
                          void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
-                         void* workspace, void* stream);
+                         void* workspace, void* margin, void* stream);
 size_t d3m_bk_panel_workspace(int n, int batch);
 
 /* Blocked multi-RHS solve (64-row diagonal blocks in shared memory +
@@ -109,7 +118,8 @@ int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const v
                              double pivot_tol,
                              void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
                              void* K_out, void* g_out, void* work_z, void* work_x, void* work_c, void* bk_scratch,
-                             void* d_tasks, const void* rows, int nrows, void* work_d, int flags, void* stream);
+                             void* d_tasks, const void* rows, int nrows, void* work_d, int flags, void* margin,
+                             void* stream);
 
 /* Grouped block copy / ordered accumulate (40-byte CopyTask records, see
  * d3m_misc.h).  Used for factor._permute_blocks (factor.py:139-151) and the
@@ -178,7 +188,7 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                         void* d_perm, void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale,
                         void* d_asym, void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead,
                         int nwait, const int64_t* h_wait_col, void* const* h_wait_ev, const void* d_check_sym,
-                        void* stream);
+                        void* d_margin, void* stream);
 
 /* n asynchronous copies dst + dst_off[i] <- src + src_off[i] (bytes, kind a
  * cudaMemcpyKind) on `stream`: the chunked upload of K's blocks from pinned

@@ -71,14 +71,27 @@ static inline double c_abs2(cplx z) { return z.re * z.re + z.im * z.im; }
 /* (1+sqrt(17))/8, kernels.py:33 */
 double d3m_oracle_bk_alpha(void) { return (1.0 + sqrt(17.0)) / 8.0; }
 
+/* Relative distance of a pivot test lhs >= rhs to its threshold (the
+ * margin diagnostic of the GPU kernels, d3m_common.cuh test_margin). */
+static double test_margin(double lhs, double rhs) {
+  double m = lhs > rhs ? lhs : rhs;
+  return m > 0.0 ? fabs(lhs - rhs) / m : 1.0;
+}
+static double fmin2(double a, double b) { return a < b ? a : b; }
+
 /*
  * Bunch-Kaufman LDL^T, kernels.py:36-146.  Returns info (-1 = success,
  * else the failing elimination step); perm/tags/n2x2/growth as the reference.
+ * margin (NULL = not tracked): [0] the minimum relative distance of every
+ * evaluated test of kernels.py:59-77 to its threshold, [1] the minimum
+ * relative gap of the colmax winner over the runner-up (checker of the GPU
+ * kernels' BkArgs::margin diagnostic).
  */
-int64_t d3m_oracle_bk_factor(cplx* W, int64_t n, int64_t lda, double tol_abs,
-                             int64_t* perm, int8_t* tags, int64_t* n2x2_out,
-                             double* growth_out) {
+int64_t d3m_oracle_bk_factor_m(cplx* W, int64_t n, int64_t lda, double tol_abs,
+                               int64_t* perm, int8_t* tags, int64_t* n2x2_out,
+                               double* growth_out, double* margin) {
   const double alpha = d3m_oracle_bk_alpha();
+  double mdec = 1.0, mgap = 1.0;
   int64_t n2x2 = 0, info = -1;
   double growth = 1.0;
   for (int64_t i = 0; i < n; ++i) { perm[i] = i; tags[i] = 0; }
@@ -93,13 +106,19 @@ int64_t d3m_oracle_bk_factor(cplx* W, int64_t n, int64_t lda, double tol_abs,
     int64_t kstep = 1, kp, imax = k;
     double absakk = c_abs(AT(W, k, k)), colmax = 0.0;
     if (k + 1 < n) {                     /* first maximiser (np.argmax) */
+      double second = -1.0;
       imax = k + 1; colmax = c_abs(AT(W, k + 1, k));
       for (int64_t i = k + 2; i < n; ++i) {
         double v = c_abs(AT(W, i, k));
-        if (v > colmax) { colmax = v; imax = i; }
+        if (v > colmax) { second = colmax; colmax = v; imax = i; }
+        else if (v > second) second = v;
       }
+      if (margin && colmax > 0.0 && second >= 0.0) mgap = fmin2(mgap, (colmax - second) / colmax);
     }
-    if ((absakk > colmax ? absakk : colmax) <= tol_abs) { info = k; break; }
+    double amax = absakk > colmax ? absakk : colmax;
+    if (margin) mdec = fmin2(mdec, test_margin(tol_abs, amax));
+    if (amax <= tol_abs) { info = k; break; }
+    if (margin) mdec = fmin2(mdec, test_margin(absakk, alpha * colmax));
     if (absakk >= alpha * colmax) {
       kp = k;
     } else {
@@ -110,9 +129,13 @@ int64_t d3m_oracle_bk_factor(cplx* W, int64_t n, int64_t lda, double tol_abs,
         for (int64_t i = imax + 2; i < n; ++i) { double v = c_abs(AT(W, i, imax)); if (v > v2) v2 = v; }
         if (v2 > rowmax) rowmax = v2;
       }
+      if (margin) mdec = fmin2(mdec, test_margin(absakk * rowmax, alpha * colmax * colmax));
       if (absakk * rowmax >= alpha * colmax * colmax) kp = k;
-      else if (c_abs(AT(W, imax, imax)) >= alpha * rowmax) kp = imax;
-      else { kp = imax; kstep = 2; }
+      else {
+        if (margin) mdec = fmin2(mdec, test_margin(c_abs(AT(W, imax, imax)), alpha * rowmax));
+        if (c_abs(AT(W, imax, imax)) >= alpha * rowmax) kp = imax;
+        else { kp = imax; kstep = 2; }
+      }
     }
     int64_t kk = k + kstep - 1;
     if (kp != kk) {                      /* kernels.py:79-101 */
@@ -171,7 +194,14 @@ int64_t d3m_oracle_bk_factor(cplx* W, int64_t n, int64_t lda, double tol_abs,
     k = kn;
   }
   *n2x2_out = n2x2; *growth_out = growth;
+  if (margin) { margin[0] = mdec; margin[1] = mgap; }
   return info;
+}
+
+int64_t d3m_oracle_bk_factor(cplx* W, int64_t n, int64_t lda, double tol_abs,
+                             int64_t* perm, int8_t* tags, int64_t* n2x2_out,
+                             double* growth_out) {
+  return d3m_oracle_bk_factor_m(W, n, lda, tol_abs, perm, tags, n2x2_out, growth_out, 0);
 }
 
 /* B <- L^{-1} B, unit lower (kernels.py:149-152).  B is n x m, ldb. */

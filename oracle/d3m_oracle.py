@@ -56,6 +56,8 @@ def lib():
         D = ctypes.c_double
         _lib.d3m_oracle_bk_factor.restype = I
         _lib.d3m_oracle_bk_factor.argtypes = [P, I, I, D, P, P, P, P]
+        _lib.d3m_oracle_bk_factor_m.restype = I
+        _lib.d3m_oracle_bk_factor_m.argtypes = [P, I, I, D, P, P, P, P, P]
         for nm in ("d3m_oracle_solve_unit_lower", "d3m_oracle_solve_unit_lower_t"):
             getattr(_lib, nm).restype = None
             getattr(_lib, nm).argtypes = [P, I, I, P, I, I]
@@ -78,17 +80,28 @@ def _ptr(a: np.ndarray):
 # L1 kernels (kernels.py:36-202), in-place like the reference.
 # --------------------------------------------------------------------------
 
-def bk_factor(W: np.ndarray, tol_abs: float):
-    """kernels.py:36-146 -> (perm, tags, n2x2, growth, info); W in place."""
+def bk_factor(W: np.ndarray, tol_abs: float, margin: np.ndarray | None = None):
+    """kernels.py:36-146 -> (perm, tags, n2x2, growth, info); W in place.
+    ``margin`` (2 doubles, optional) receives the pivot-decision margin and
+    the argmax gap (the GPU kernels' diagnostic, include/d3m.h)."""
     assert W.dtype == np.complex128 and W.flags.c_contiguous
     n = W.shape[0]
     perm = np.empty(n, dtype=np.int64)
     tags = np.empty(n, dtype=np.int8)
     n2 = ctypes.c_int64(0)
     gr = ctypes.c_double(1.0)
-    info = lib().d3m_oracle_bk_factor(_ptr(W), n, max(n, 1), float(tol_abs), _ptr(perm),
-                                      _ptr(tags), ctypes.byref(n2), ctypes.byref(gr))
+    info = lib().d3m_oracle_bk_factor_m(_ptr(W), n, max(n, 1), float(tol_abs), _ptr(perm),
+                                        _ptr(tags), ctypes.byref(n2), ctypes.byref(gr),
+                                        _ptr(margin) if margin is not None else None)
     return perm, tags, int(n2.value), float(gr.value), int(info)
+
+
+def bk_margins(M, pivot_tol=1e-12):
+    """(decision margin, argmax gap) of the reference BK on M (a copy)."""
+    W = np.array(M, dtype=np.complex128, order="C")
+    mg = np.ones(2)
+    bk_factor(W, pivot_tol * np.abs(W).max() if W.size else 0.0, mg)
+    return float(mg[0]), float(mg[1])
 
 
 def solve_unit_lower(L, B):

@@ -22,7 +22,7 @@ F64 = ctypes.c_double
 # name -> argtypes (restype int unless stated)
 _SIGNATURES = {
     "d3m_abi_version": [],
-    "d3m_bk_factor_batched": [I32, I32, P, I64, I32, F64, I32, P, P, P, P, P, P, P, P, P],
+    "d3m_bk_factor_batched": [I32, I32, P, I64, I32, F64, I32, P, P, P, P, P, P, P, P, P, P],
     "d3m_bk_cluster_max_n": [I32],
     "d3m_ldlt_solve_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P],
     "d3m_zgemm_grouped": [I32, I32, P, P, P, P, I32, P, P],
@@ -30,7 +30,7 @@ _SIGNATURES = {
     "d3m_block_residual": [I32, P, P, P, P, P, P, P, P, P],
     "d3m_nonzero_rows": [I32, I32, I32, P, P, P, P, P],
     "d3m_block_solve_dataflow": [I32, P, P, I32, P, P, P, I32, P, P, P, P, P, P, P, P, I32, P],
-    "d3m_schur_reduce_batched": [I32, I32, I32, I32, P, P, P, F64] + [P] * 14 + [P, I32, P, I32, P],
+    "d3m_schur_reduce_batched": [I32, I32, I32, I32, P, P, P, F64] + [P] * 14 + [P, I32, P, I32, P, P],
     "d3m_block_copy": [P, P, P, I32, I64, P],
     "d3m_gather_rows": [P, P, P, I64, I32, P],
     "d3m_ordered_average": [P, P, P, P, I64, P],
@@ -38,13 +38,13 @@ _SIGNATURES = {
     "d3m_diag_sym_exact": [P, P, P, I32, P, P],
     "d3m_modulus_probe": [P, P, P, I64, P],
     "d3m_block_ldlt_exec": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, P, P, P, P, P, P, P,
-                            P, F64, I32, I32, I32, P, P, P, P],
+                            P, F64, I32, I32, I32, P, P, P, P, P],
     "d3m_diag_sym_flags": [P, P, P, P, I32, P, P],
     "d3m_memcpy_batch": [P, P, P, P, P, I32, I32, P],
     "d3m_block_solve_exec": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, I32, P, P],
     "d3m_recover_batched": [I32, I32, I32, P, P, P, P, P, P, P, P, P, P, I64, P, P],
     "d3m_counters_read": [P, P, P],
-    "d3m_bk_panel_batched": [I32, I32, P, I64, I32, F64, I32, P, P, P, P, P, P, P, P, P],
+    "d3m_bk_panel_batched": [I32, I32, P, I64, I32, F64, I32, P, P, P, P, P, P, P, P, P, P],
     "d3m_ldlt_solve_blocked_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P, P],
 }
 _SIZE_T = {"d3m_bk_panel_workspace": [I32, I32]}

@@ -66,12 +66,14 @@ __device__ __forceinline__ BkcSlot bkc_merge(const BkcSlot* box, BkcSlot* out) {
   return *out;
 }
 
-// ---- step exchange slot: 32 bytes, two st.async.v2.f64 ---------------------
+// ---- step exchange slot: 48 bytes, three st.async.v2.f64 -------------------
 struct XSlot {
   double v;      // exact argmax value or -1
   double own;    // a modulus only the owner of a row can supply, else -1
   double aux;    // max-reduced payload (rowmax, update maximum)
   double i;      // argmax index (int bits)
+  double v2;     // runner-up of the argmax (margin diagnostic), else -1
+  double pad;
 };
 constexpr unsigned kSlotBytes = sizeof(XSlot);
 
@@ -113,23 +115,28 @@ __device__ __forceinline__ void xpost(const XSlot* box, int rank, const XSlot& x
     const uint32_t dst = mapa(saddr(box + rank), lane), rb = mapa(saddr(bar), lane);
     st_async(dst, x.v, x.own, rb);
     st_async(dst + 16, x.aux, x.i, rb);
+    st_async(dst + 32, x.v2, x.pad, rb);
   }
 }
 
-// merge of the CS slots of a local inbox (warp 0), broadcast through smem
+// merge of the CS slots of a local inbox (warp 0), broadcast through smem;
+// with `track`, also the cluster-wide runner-up of the argmax (v2)
 template <int CS>
-__device__ __forceinline__ XSlot xmerge(const XSlot* box, XSlot* out) {
+__device__ __forceinline__ XSlot xmerge(const XSlot* box, XSlot* out, bool track = false) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    double v = -1.0, own = -1.0, aux = -1.0;
+    double v = -1.0, own = -1.0, aux = -1.0, r2 = -1.0;
     int vi = 0x7fffffff;
     if (lane < CS) {
       const XSlot r = box[lane];
       v = r.v;
       own = r.own;
       aux = r.aux;
+      r2 = r.v2;
       vi = (int)__double_as_longlong(r.i);
     }
+    const double lv = v;
+    const int li = vi;
 #pragma unroll
     for (int o = CS / 2; o > 0; o >>= 1) {
       const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
@@ -138,14 +145,25 @@ __device__ __forceinline__ XSlot xmerge(const XSlot* box, XSlot* out) {
       aux = fmax(aux, __shfl_xor_sync(0xffffffffu, aux, o));
       argmax_merge(v, vi, v2, i2);
     }
-    if (lane == 0) *out = XSlot{v, own, aux, __longlong_as_double((long long)vi)};
+    if (track) {   // the winner's slot offers its own runner-up, every other slot its winner
+      double c = li == vi ? r2 : lv;
+#pragma unroll
+      for (int o = CS / 2; o > 0; o >>= 1) c = fmax(c, __shfl_xor_sync(0xffffffffu, c, o));
+      r2 = c;
+    }
+    if (lane == 0) *out = XSlot{v, own, aux, __longlong_as_double((long long)vi), r2, 0.0};
   }
   __syncthreads();
   return *out;
 }
 __device__ __forceinline__ int xidx(const XSlot& x) { return (int)__double_as_longlong(x.i); }
-__device__ __forceinline__ XSlot xslot(double v, double own, double aux, int i) {
-  return XSlot{v, own, aux, __longlong_as_double((long long)i)};
+__device__ __forceinline__ XSlot xslot(double v, double own, double aux, int i, double v2 = -1.0) {
+  return XSlot{v, own, aux, __longlong_as_double((long long)i), v2, 0.0};
+}
+// runner-up of a warp's first-index argmax: lanes hold their own top-2
+// (lv, li, lv2), (v, vi) is the warp winner
+__device__ __forceinline__ double warp_runner_up(double lv, int li, double lv2, int vi) {
+  return warp_max(li == vi ? lv2 : lv);
 }
 
 __device__ __forceinline__ double bkc_block_max(double v, double* slots) {
@@ -269,12 +287,15 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
   if (csym == 1 && n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) {
     if (lead) {
       a.info[b] = -2; a.n2x2[b] = 0; a.growth[b] = 1.0;
+      if (a.margin) { a.margin[2 * b] = 1.0; a.margin[2 * b + 1] = 1.0; }
       for (int i = 0; i < n; ++i) { a.perm[(int64_t)b * n + i] = i; a.tags[(int64_t)b * n + i] = 0; }
     }
     cl.sync();
     return;
   }
   const double tol_abs = __dmul_rn(a.pivot_tol, scale);
+  const bool track = a.margin != nullptr;      // pivot-decision margins (lead thread)
+  double mdec = 1.0, mgap = 1.0;
   // growth recurrence (kernels.py:135-144), run by gthread only: a step's
   // update maximum reaches every CTA two steps later, applied in step order
   double trail_max = __dsqrt_rn(tm2);
@@ -295,7 +316,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
 
   // ---- column 0, pushed by the pivot warps -----------------------------------
   if (pw) {
-    double v = -1.0, own = -1.0;
+    double v = -1.0, own = -1.0, v2 = -1.0;
     int vi = 0x7fffffff;
     for (int q = lane; q < nown; q += 32) {
       const int i = rank + q * CS;
@@ -304,12 +325,15 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
 #pragma unroll
       for (int c = 0; c < CS; ++c) st_async(mapa(src, c), z.x, z.y, mapa(sb, c));
       const double az = x_abs(z);
-      if (i > 0) argmax_merge(v, vi, az, i);
+      if (i > 0) top2_merge(v, vi, v2, az, i);
       else own = az;
     }
+    const double lv = v;
+    const int li = vi;
     warp_argmax(v, vi);
     own = warp_max(own);
-    xpost<CS>(inbox[0], rank, xslot(v, own, -1.0, vi), &mbar[0]);
+    if (track) v2 = warp_runner_up(lv, li, v2, vi);
+    xpost<CS>(inbox[0], rank, xslot(v, own, -1.0, vi, v2), &mbar[0]);
   }
 #ifdef D3M_BK_PROFILE
   const long long t_loop0 = clock64();
@@ -335,19 +359,28 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     mbar_wait(&mbar[bs], (unsigned)(s / 3) & 1u);
     BKC_MARK(0, 0);
     BKC_MARK(32, 8);
-    const XSlot m1 = xmerge<CS>(inbox[bs], &xmerged);   // its __syncthreads also ends the local bulk
+    const XSlot m1 = xmerge<CS>(inbox[bs], &xmerged, track);   // its __syncthreads also ends the local bulk
     BKC_MARK(0, 1);
     BKC_MARK(32, 9);
     pend_usq = m1.aux;                                       // step s-2's update maximum
     const double absakk = m1.own;                            // |W[k, k]|, from its owner
     double colmax = 0.0;
     int imax = k;
-    if (k + 1 < n) { colmax = m1.v; imax = xidx(m1); }
-    if (fmax(absakk, colmax) <= tol_abs) { info = k; break; }
+    if (k + 1 < n) {
+      colmax = m1.v;
+      imax = xidx(m1);
+      if (track && lead) mgap = fmin(mgap, argmax_gap(colmax, m1.v2));
+    }
+    if (fmax(absakk, colmax) <= tol_abs) {
+      if (track && lead) mdec = fmin(mdec, test_margin(tol_abs, fmax(absakk, colmax)));
+      info = k;
+      break;
+    }
 
     int kstep = 1, kp;
     if (absakk >= __dmul_rn(kBkcAlpha, colmax)) {
       kp = k;
+      if (track && lead) mdec = fmin(mdec, decision_margin(tol_abs, absakk, colmax, 0.0, 0.0, kBkcAlpha, 1));
     } else {
       // ---- 2. push column k+1 and the symmetric column imax; rowmax over
       //         W[imax, k:imax] and W[imax+1:, imax]; |W[imax, imax]| ----------
@@ -385,14 +418,18 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
       ++rphase;
       const XSlot m2 = xmerge<CS>(inboxR, &xmerged);
       const double rowmax = m2.aux, absimax = m2.own;
+      int stage = 3;
       if (__dmul_rn(absakk, rowmax) >= __dmul_rn(__dmul_rn(kBkcAlpha, colmax), colmax)) {
         kp = k;
+        stage = 2;
       } else if (absimax >= __dmul_rn(kBkcAlpha, rowmax)) {
         kp = imax;
       } else {
         kp = imax;
         kstep = 2;
       }
+      if (track && lead)
+        mdec = fmin(mdec, decision_margin(tol_abs, absakk, colmax, rowmax, absimax, kBkcAlpha, stage));
     }
     const int kk = k + kstep - 1, k0 = k + kstep;
     const cplx* cK = kstep == 1 ? cA : cB;          // column kk before the swap
@@ -442,7 +479,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
       // ---- 4P. update of column k0 of the own rows, push ------------------
       double up = -1.0;
       if (s >= 1) up = warp_max(lane < NW ? rst[(s - 1) & 1][lane] : 0.0);
-      double v = -1.0, own = -1.0;
+      double v = -1.0, own = -1.0, v2 = -1.0;
       int vi = 0x7fffffff;
       if (k0 < n) {
         // multipliers of row k0 (the bulk threads compute the same values for rows > k0)
@@ -472,28 +509,31 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
           for (int c = 0; c < CS; ++c) st_async(mapa(src, c), w.x, w.y, mapa(nbar, c));
           step_sq = fmax(step_sq, x_abs2(w));
           const double aw = x_abs(w);
-          if (i > k0) argmax_merge(v, vi, aw, i);
+          if (i > k0) top2_merge(v, vi, v2, aw, i);
           else own = aw;
         }
         BKC_MARK(0, 5);
+        const double lv = v;
+        const int li = vi;
         // one butterfly for the exact argmax, the owner's modulus and the
         // update maximum (independent shuffles per round; max and
         // first-index argmax are order-free, so the results are unchanged)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-          const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+          const double v2_ = __shfl_xor_sync(0xffffffffu, v, o);
           const int i2 = __shfl_xor_sync(0xffffffffu, vi, o);
           const double own2 = __shfl_xor_sync(0xffffffffu, own, o);
           const double sq2 = __shfl_xor_sync(0xffffffffu, step_sq, o);
-          argmax_merge(v, vi, v2, i2);
+          argmax_merge(v, vi, v2_, i2);
           own = fmax(own, own2);
           step_sq = fmax(step_sq, sq2);
         }
+        if (track) v2 = warp_runner_up(lv, li, v2, vi);
       } else {
         step_sq = warp_max(step_sq);
       }
       if (lane == 0) rst[s & 1][0] = step_sq;
-      xpost<CS>(inbox[nb], rank, xslot(v, own, up, vi), &mbar[nb]);
+      xpost<CS>(inbox[nb], rank, xslot(v, own, up, vi, v2), &mbar[nb]);
       BKC_MARK(0, 6);
       if (kstep == 2) ++n2x2;
     } else {
@@ -664,6 +704,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
   if (lead) {
     a.n2x2[b] = n2x2;
     a.info[b] = info;
+    if (track) { a.margin[2 * b] = mdec; a.margin[2 * b + 1] = mgap; }
   }
   if (rank == 0 && gthread) a.growth[b] = growth;
 #ifdef D3M_BK_PROFILE

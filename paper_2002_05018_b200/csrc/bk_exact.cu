@@ -86,13 +86,18 @@ __global__ void __launch_bounds__(NT) bk_exact_kernel(BkArgs a, int use_smem) {
   tm2 = block_max<NT>(tm2, red_c);
   if (tid == 0) { a.scale[b] = scale; a.asym[b] = asym; }
   if (csym && n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) {
-    if (tid == 0) { a.info[b] = -2; a.n2x2[b] = 0; a.growth[b] = 1.0; }
+    if (tid == 0) {
+      a.info[b] = -2; a.n2x2[b] = 0; a.growth[b] = 1.0;
+      if (a.margin) { a.margin[2 * b] = 1.0; a.margin[2 * b + 1] = 1.0; }
+    }
     return;
   }
   const double tol_abs = __dmul_rn(a.pivot_tol, scale);
   double trail_max = __dsqrt_rn(tm2);
   double growth = 1.0;
   int n2x2 = 0, info = -1;
+  const bool track = a.margin != nullptr;
+  double mdec = 1.0, mgap = 1.0;
   __syncthreads();
 
   int k = 0;
@@ -102,18 +107,30 @@ __global__ void __launch_bounds__(NT) bk_exact_kernel(BkArgs a, int use_smem) {
     double colmax = 0.0;
     int imax = k;
     if (k + 1 < n) {
-      double v = -1.0;
+      double v = -1.0, v2 = -1.0;
       int vi = 0x7fffffff;
-      for (int i = k + 1 + tid; i < n; i += NT) argmax_merge(v, vi, x_abs(W[(int64_t)i * lda + k]), i);
+      for (int i = k + 1 + tid; i < n; i += NT) top2_merge(v, vi, v2, x_abs(W[(int64_t)i * lda + k]), i);
+      const double tv = v;
+      const int ti = vi;
       block_argmax<NT>(v, vi, red_a, red_ai);
       colmax = v;
       imax = vi;
+      if (track) {   // runner-up: every thread's best other than the winner
+        __syncthreads();
+        const double r2 = block_max<NT>(ti == imax ? v2 : tv, red_c);
+        mgap = fmin(mgap, argmax_gap(colmax, r2));
+      }
     }
-    if (fmax(absakk, colmax) <= tol_abs) { info = k; break; }
+    if (fmax(absakk, colmax) <= tol_abs) {
+      if (track) mdec = fmin(mdec, test_margin(tol_abs, fmax(absakk, colmax)));
+      info = k;
+      break;
+    }
 
     int kstep = 1, kp;
     if (absakk >= __dmul_rn(kBkAlpha, colmax)) {
       kp = k;
+      if (track) mdec = fmin(mdec, decision_margin(tol_abs, absakk, colmax, 0.0, 0.0, kBkAlpha, 1));
     } else {
       // ---- 2. rowmax over W[imax, k:imax] and W[imax+1:, imax] -------------
       // every thread reads |W[imax, imax]| before the reduction's barrier, so
@@ -127,14 +144,17 @@ __global__ void __launch_bounds__(NT) bk_exact_kernel(BkArgs a, int use_smem) {
         rm = fmax(rm, x_abs(z));
       }
       const double rowmax = block_max<NT>(rm, red_b);
+      int stage = 3;
       if (__dmul_rn(absakk, rowmax) >= __dmul_rn(__dmul_rn(kBkAlpha, colmax), colmax)) {
         kp = k;
+        stage = 2;
       } else if (absimax >= __dmul_rn(kBkAlpha, rowmax)) {
         kp = imax;
       } else {
         kp = imax;
         kstep = 2;
       }
+      if (track) mdec = fmin(mdec, decision_margin(tol_abs, absakk, colmax, rowmax, absimax, kBkAlpha, stage));
     }
 
     // ---- 3. symmetric interchange kk <-> kp --------------------------------
@@ -228,6 +248,7 @@ __global__ void __launch_bounds__(NT) bk_exact_kernel(BkArgs a, int use_smem) {
     a.n2x2[b] = n2x2;
     a.growth[b] = growth;
     a.info[b] = info;
+    if (track) { a.margin[2 * b] = mdec; a.margin[2 * b + 1] = mgap; }
   }
 }
 

@@ -31,7 +31,7 @@ constexpr double kAlphaP = 0.6403882032022076;
 struct BkState {          // 64 bytes per matrix
   int32_t k, info, n2x2, npiv_last;
   double trail_max, growth, tol_abs, scale, asym;
-  int32_t pad[2];
+  float mdec, mgap;       // running pivot-decision margins (BkArgs::margin)
 };
 static_assert(sizeof(BkState) == 64, "BkState layout");
 
@@ -139,6 +139,8 @@ __global__ void bk_panel_state_kernel(BkArgs a, BkState* st, const unsigned long
   s.tol_abs = __dmul_rn(a.pivot_tol, scale);
   s.scale = scale;
   s.asym = asym;
+  s.mdec = 1.0f;
+  s.mgap = 1.0f;
   st[b] = s;
   a.scale[b] = scale;
   a.asym[b] = asym;
@@ -211,14 +213,22 @@ __device__ __forceinline__ void panel_gemv(const cplx* __restrict__ W, int lda, 
 // candidate sets contains every global maximiser, so merging the local exact
 // results with argmax_merge gives the reference's np.argmax(abs(...)).
 // Returns ev = -1, ei = INT_MAX for an empty range.
+// With `ev2` (margin diagnostic), also the modulus of the local runner-up
+// (largest |col[i]| of any other row, from the |z|^2 proxies; -1: none).
 template <int NT>
 __device__ __forceinline__ void local_exact_argmax(const cplx* col, int ldw, int r0, int r1, int skip, double& ev,
-                                                   int& ei, double* vs, int* is) {
-  double pv = -1.0;
+                                                   int& ei, double* vs, int* is, double* ev2 = nullptr) {
+  double pv = -1.0, pv2 = -1.0;
   int pi = 0x7fffffff;
   for (int i = r0 + (int)threadIdx.x; i < r1; i += NT)
-    if (i != skip) argmax_merge(pv, pi, x_abs2(col[(int64_t)i * ldw]), i);
+    if (i != skip) top2_merge(pv, pi, pv2, x_abs2(col[(int64_t)i * ldw]), i);
+  const double tv = pv;
+  const int ti = pi;
   pargmax_red<NT>(pv, pi, vs, is);
+  if (ev2) {
+    const double r2 = pmax_red<NT>(ti == pi ? pv2 : tv, vs);
+    *ev2 = r2 >= 0.0 ? sqrt(r2) : -1.0;
+  }
   if (pi == 0x7fffffff) { ev = -1.0; ei = pi; return; }
   const double thr = pv * (1.0 - 1e-14);
   int amb = 0;
@@ -244,6 +254,7 @@ __device__ __forceinline__ void local_exact_argmax(const cplx* col, int ldw, int
 struct ClSlot {       // one CTA's contribution to a cluster-wide pivot search
   double ev;          // local exact max over the local candidates (-1: none)
   double own;         // modulus of the published diagonal-ish entry (-1: not owned)
+  double ev2;         // local runner-up (margin diagnostic, -1: none / not tracked)
   int ei;             // first index of ev
   int pad;
 };
@@ -251,17 +262,20 @@ struct ClSlot {       // one CTA's contribution to a cluster-wide pivot search
 // Gather the CS slots (DSMEM) after a cluster barrier; every CTA merges in the
 // same order, so all CTAs hold bitwise-identical decisions.
 template <int CS>
-__device__ __forceinline__ ClSlot cl_merge(cg::cluster_group& cl, ClSlot* slot, ClSlot* out) {
+__device__ __forceinline__ ClSlot cl_merge(cg::cluster_group& cl, ClSlot* slot, ClSlot* out, bool track = false) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    double ev = -1.0, own = -1.0;
+    double ev = -1.0, own = -1.0, r2 = -1.0;
     int ei = 0x7fffffff;
     if (lane < CS) {
       const ClSlot* p = cl.map_shared_rank(slot, lane);
       ev = p->ev;
       own = p->own;
+      r2 = p->ev2;
       ei = p->ei;
     }
+    const double lv = ev;
+    const int li = ei;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double ev2 = __shfl_xor_sync(0xffffffffu, ev, o);
@@ -269,7 +283,8 @@ __device__ __forceinline__ ClSlot cl_merge(cg::cluster_group& cl, ClSlot* slot, 
       own = fmax(own, __shfl_xor_sync(0xffffffffu, own, o));
       argmax_merge(ev, ei, ev2, ei2);
     }
-    if (lane == 0) { out->ev = ev; out->own = own; out->ei = ei; }
+    if (track) r2 = warp_max(li == ei ? r2 : lv);   // the winner's runner-up, every other CTA's winner
+    if (lane == 0) { out->ev = ev; out->own = own; out->ei = ei; out->ev2 = r2; }
   }
   __syncthreads();
   return *out;
@@ -318,6 +333,8 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
   const int ch = (n - k0 + CS - 1) / CS;
   const int lo = min(n, k0 + rank * ch), hi = min(n, lo + ch);
   int k = k0, kw = 0, npiv = 0, info = -1, n2x2 = s.n2x2, par = 0;
+  const bool track = a.margin != nullptr;     // pivot-decision margins (uniform over the cluster)
+  double mdec = s.mdec, mgap = s.mgap;
   // a step starts only while kw <= NB-2, so a panel is NB-1 or NB columns
   // (zlasyf's exit rule) and the trailing update has K <= NB = 16
   while (kw < NB - 1 && k < n) {
@@ -326,27 +343,38 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
     panel_gemv<NB, CNT>(W, lda, max(k, lo), hi, k0, kw, k, Wp, k, Wp + kw);
     __syncthreads();
     {
-      double ev;
+      double ev, ev2 = -1.0;
       int ei;
-      local_exact_argmax<CNT>(Wp + kw, LDW, max(k + 1, lo), hi, -1, ev, ei, ra, rai);
+      local_exact_argmax<CNT>(Wp + kw, LDW, max(k + 1, lo), hi, -1, ev, ei, ra, rai, track ? &ev2 : nullptr);
       if (tid == 0) {
         ClSlot& sl = slots[par];
         sl.ev = ev;
+        sl.ev2 = ev2;
         sl.ei = ei;
         sl.own = (k >= lo && k < hi) ? x_abs(Wp[(int64_t)k * LDW + kw]) : -1.0;
       }
     }
     cl.sync();
-    const ClSlot m1 = cl_merge<CS>(cl, &slots[par], &merged);
+    const ClSlot m1 = cl_merge<CS>(cl, &slots[par], &merged, track);
     par ^= 1;
     const double absakk = m1.own;
     double colmax = 0.0;
     int imax = k;
-    if (k + 1 < n) { imax = m1.ei; colmax = m1.ev; }
-    if (fmax(absakk, colmax) <= s.tol_abs) { info = k; break; }
+    if (k + 1 < n) {
+      imax = m1.ei;
+      colmax = m1.ev;
+      if (track) mgap = fmin(mgap, argmax_gap(colmax, m1.ev2));
+    }
+    if (fmax(absakk, colmax) <= s.tol_abs) {
+      if (track) mdec = fmin(mdec, test_margin(s.tol_abs, fmax(absakk, colmax)));
+      info = k;
+      break;
+    }
     int kstep = 1, kp = k;
     bool copy = false;
-    if (!(absakk >= __dmul_rn(kAlphaP, colmax))) {
+    if (absakk >= __dmul_rn(kAlphaP, colmax)) {
+      if (track) mdec = fmin(mdec, decision_margin(s.tol_abs, absakk, colmax, 0.0, 0.0, kAlphaP, 1));
+    } else {
       // -- C: column imax up to date into Wp[:, kw+1], then the cluster's
       //    exact rowmax (diagonal entry imax excluded) and |a_imax,imax|
       panel_gemv<NB, CNT>(W, lda, max(k, lo), hi, k0, kw, imax, Wp, imax, Wp + kw + 1);
@@ -367,8 +395,10 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
       par ^= 1;
       const double rowmax = fmax(0.0, m2.ev);
       const double absimax = m2.own;
+      int stage = 3;
       if (__dmul_rn(absakk, rowmax) >= __dmul_rn(__dmul_rn(kAlphaP, colmax), colmax)) {
         kp = k;
+        stage = 2;
       } else if (absimax >= __dmul_rn(kAlphaP, rowmax)) {
         kp = imax;
         copy = true;                       // column kw := column kw+1
@@ -376,6 +406,7 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
         kp = imax;
         kstep = 2;
       }
+      if (track) mdec = fmin(mdec, decision_margin(s.tol_abs, absakk, colmax, rowmax, absimax, kAlphaP, stage));
     }
     const int kk = k + kstep - 1, kkw = kw + kstep - 1;
     if (copy)   // own rows; rows kk / kp are moved by the interchange below
@@ -459,6 +490,8 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
     s.k = k;
     s.info = info;
     s.n2x2 = n2x2;
+    s.mdec = (float)mdec;
+    s.mgap = (float)mgap;
     s.npiv_last = (info < 0 && k < n) ? npiv : 0;
     st[b] = s;
     if (info < 0 && k < n) {
@@ -488,6 +521,7 @@ __global__ void bk_panel_finalize_kernel(BkArgs a, const BkState* st, int batch)
   a.info[b] = s.info;
   a.n2x2[b] = s.n2x2;
   a.growth[b] = s.growth;
+  if (a.margin) { a.margin[2 * b] = s.mdec; a.margin[2 * b + 1] = s.mgap; }
 }
 
 }  // namespace d3m

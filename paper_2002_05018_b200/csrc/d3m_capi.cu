@@ -95,7 +95,7 @@ extern "C" {
 int d3m_abi_version(void) { return D3M_ABI_VERSION; }
 int d3m_bk_panel_batched(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
                          void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
-                         void* workspace, void* stream);
+                         void* workspace, void* margin, void* stream);
 int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stride_f, const void* perm,
                                    int64_t stride_p, const void* tags, int64_t stride_t, void* B, int64_t stride_b,
                                    int ldb, int m, void* work, void* d_tasks, void* stream);
@@ -104,11 +104,12 @@ const char* d3m_last_error(void) { return g_err.c_str(); }
 
 int d3m_bk_factor_batched(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
                           void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
-                          void* scratch, void* stream) {
+                          void* scratch, void* margin, void* stream) {
   if (batch < 0 || n < 0 || lda < n) return fail(-22, "d3m_bk_factor_batched: bad shape");
   d3m::BkArgs a{C(W), stride_w, n, lda, pivot_tol, check_sym, static_cast<int64_t*>(perm), static_cast<int8_t*>(tags),
                 static_cast<int32_t*>(n2x2), static_cast<double*>(growth), static_cast<int32_t*>(info),
                 static_cast<double*>(scale), static_cast<double*>(asym), C(scratch)};
+  a.margin = static_cast<double*>(margin);
   D3M_TRY(launch(kClsBk, stream, [&] { return d3m_bk_launch(&a, batch, stream); }));
   return 0;
 }
@@ -231,11 +232,12 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
 
 int d3m_bk_panel_batched(int batch, int n, void* W, int64_t stride_w, int lda, double pivot_tol, int check_sym,
                          void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
-                         void* workspace, void* stream) {
+                         void* workspace, void* margin, void* stream) {
   if (batch < 0 || n < 0 || lda < n) return fail(-22, "d3m_bk_panel_batched: bad shape");
   d3m::BkArgs a{C(W), stride_w, n, lda, pivot_tol, check_sym, static_cast<int64_t*>(perm), static_cast<int8_t*>(tags),
                 static_cast<int32_t*>(n2x2), static_cast<double*>(growth), static_cast<int32_t*>(info),
                 static_cast<double*>(scale), static_cast<double*>(asym), nullptr};
+  a.margin = static_cast<double*>(margin);
   D3M_TRY(launch(kClsBk, stream, [&] { return d3m_bk_panel_batched_launch(&a, batch, workspace, stream); }));
   return 0;
 }
@@ -258,7 +260,7 @@ int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const v
                              double pivot_tol, void* perm, void* tags, void* n2x2, void* growth, void* info,
                              void* scale, void* asym, void* K_out, void* g_out, void* work_z, void* work_x,
                              void* work_c, void* bk_scratch, void* d_tasks, const void* rows, int nrows,
-                             void* work_d, int flags, void* stream) {
+                             void* work_d, int flags, void* margin, void* stream) {
   // A: batch x n x n (factored in place -> packed factor); D: batch x n x m;
   // F: batch x n x nrhs; work_z, work_x: batch x n x (m+nrhs); work_c: batch x m x (m+nrhs)
   if (batch < 0 || n < 0 || m < 0 || nrhs < 0) return fail(-22, "d3m_schur_reduce_batched: bad shape");
@@ -271,10 +273,10 @@ int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const v
   // the unblocked bit-exact kernel
   if (big)
     D3M_TRY(d3m_bk_panel_batched(batch, n, A, nn, n, pivot_tol, 1, perm, tags, n2x2, growth, info, scale, asym,
-                                 bk_scratch, stream));
+                                 bk_scratch, margin, stream));
   else
     D3M_TRY(d3m_bk_factor_batched(batch, n, A, nn, n, pivot_tol, 1, perm, tags, n2x2, growth, info, scale, asym,
-                                  bk_scratch, stream));
+                                  bk_scratch, margin, stream));
   if (n == 0 || w == 0) return 0;
   // RHS = [D | F]  (subdomain.py:177-179)
   D3M_TRY(launch(kClsMisc, stream, [&] {
@@ -437,7 +439,7 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                         void* d_perm, void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale,
                         void* d_asym, void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead,
                         int nwait, const int64_t* h_wait_col, void* const* h_wait_ev, const void* d_check_sym,
-                        void* stream) {
+                        void* d_margin, void* stream) {
   // rest-update tiles above which a column's diagonal BK runs on a 4-CTA cluster (D3M_BKC4_TILES)
   static const int64_t bkc4_tiles = [] {
     const char* e = getenv("D3M_BKC4_TILES");
@@ -517,6 +519,7 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                   static_cast<int32_t*>(d_info) + j, static_cast<double*>(d_scale) + j,
                   static_cast<double*>(d_asym) + j, C(d_bk_scratch)};
     if (d_check_sym) a.check_sym_dev = static_cast<const int*>(d_check_sym) + j;   // per-block flag (ABI v8)
+    if (d_margin) a.margin = static_cast<double*>(d_margin) + 2 * j;               // decision margins (ABI v9)
     if (nj > 0) {
       // supernodes up to kExactBkMax use the bit-exact unblocked kernel (so a
       // one-block K factors exactly like dense_ldlt_bk, test_block_factor.py:

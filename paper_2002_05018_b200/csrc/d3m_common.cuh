@@ -177,4 +177,38 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// ---- pivot-decision margins (diagnostic, BkArgs::margin) --------------------
+// Relative distance of a pivot test "lhs >= rhs" (kernels.py:59-77) to its
+// threshold: |lhs - rhs| / max(lhs, rhs); 1 when both sides are 0.  A kernel
+// whose arithmetic differs from the reference's by rounding (FMA, another
+// update order) takes the same decision whenever this is well above the
+// relative rounding of the operands (~1e-15).
+__device__ __forceinline__ double test_margin(double lhs, double rhs) {
+  const double m = fmax(lhs, rhs);
+  return m > 0.0 ? fabs(lhs - rhs) / m : 1.0;
+}
+// The per-step margins of one pivot decision, in the reference's test order:
+// the singularity test, |a_kk| >= alpha colmax, then (rowmax path)
+// |a_kk| rowmax >= alpha colmax^2 and |a_imax,imax| >= alpha rowmax as far as
+// they are evaluated.  stage: 1 = decided by the first test, 2 = by the
+// second, 3 = by the third (or the 2x2 fall-through).
+__device__ __forceinline__ double decision_margin(double tol_abs, double absakk, double colmax, double rowmax,
+                                                  double absimax, double alpha, int stage) {
+  double m = test_margin(tol_abs, fmax(absakk, colmax));
+  m = fmin(m, test_margin(absakk, alpha * colmax));
+  if (stage >= 2) m = fmin(m, test_margin(absakk * rowmax, alpha * colmax * colmax));
+  if (stage >= 3) m = fmin(m, test_margin(absimax, alpha * rowmax));
+  return m;
+}
+// Running top-2 of a first-index argmax: (v, i) the winner, v2 the largest
+// value of any other index (ties with the winner give v2 == v: gap 0).
+__device__ __forceinline__ void top2_merge(double& v, int& i, double& v2, double w, int wi) {
+  if (w > v || (w == v && wi < i)) { v2 = fmax(v2, v); v = w; i = wi; }
+  else v2 = fmax(v2, w);
+}
+// relative gap of the argmax winner v1 over the runner-up v2
+__device__ __forceinline__ double argmax_gap(double v1, double v2) {
+  return (v1 > 0.0 && v2 >= 0.0) ? (v1 - v2) / v1 : 1.0;
+}
+
 }  // namespace d3m

@@ -23,6 +23,10 @@ struct BkArgs {
   double* asym;       // batch: np.abs(W - W.T).max()
   cplx* scratch;      // batch x 4n, used when the staging does not fit smem
   const int* check_sym_dev = nullptr;   // optional device copy of check_sym (read by the kernel, batch 1)
+  // optional pivot-decision diagnostic, batch x 2 doubles: [0] the minimum
+  // decision_margin over all steps, [1] the minimum argmax_gap of the colmax
+  // searches (d3m_common.cuh); nullptr = not tracked
+  double* margin = nullptr;
 };
 
 // Device-resident plan of the persistent block solve (skinny_dmma.cu)

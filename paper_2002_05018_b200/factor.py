@@ -70,6 +70,11 @@ class DenseFactor:
         self.n_2x2 = int(n_2x2)
         self._n = int(perm_dev.shape[0])
         self._host = None
+        # (decision margin, argmax gap) of the pivot sequence when the
+        # factorisation tracked them (margins=True), else None: the minimum
+        # relative distance of any BK test of kernels.py:59-77 to its
+        # threshold and of the colmax winner to the runner-up
+        self.margin = None
 
     @property
     def n(self) -> int:
@@ -155,7 +160,7 @@ def _is_tensor(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
-def dense_ldlt_bk(M, pivot_tol: float = DEFAULT_PIVOT_TOL) -> DenseFactor:
+def dense_ldlt_bk(M, pivot_tol: float = DEFAULT_PIVOT_TOL, margins: bool = False) -> DenseFactor:
     """Bunch-Kaufman LDL^T of a complex symmetric matrix on the GPU.
 
     factor.py:83-116: rejects non-square input (ValueError), checks symmetry
@@ -169,10 +174,10 @@ def dense_ldlt_bk(M, pivot_tol: float = DEFAULT_PIVOT_TOL) -> DenseFactor:
     n = int(shape[0])
     t = require_cuda()
     W = to_device(M).clone() if n else t.zeros((0, 0), dtype=t.complex128, device="cuda")
-    return _factor_batch(W.reshape(1, n, n), pivot_tol, labels=None)[0]
+    return _factor_batch(W.reshape(1, n, n), pivot_tol, labels=None, margins=margins)[0]
 
 
-def _factor_batch(W, pivot_tol, labels, check_sym=True, scratch=None):
+def _factor_batch(W, pivot_tol, labels, check_sym=True, scratch=None, margins=False):
     """Factor a (batch, n, n) device tensor in place; returns DenseFactors
     or raises for the first failing matrix (``labels`` customises errors)."""
     t = require_cuda()
@@ -186,12 +191,13 @@ def _factor_batch(W, pivot_tol, labels, check_sym=True, scratch=None):
     asy = t.empty(batch, dtype=t.float64, device="cuda")
     if scratch is None and 64 * n > 200 * 1024:
         scratch = empty((batch, 4 * n))
+    mg = t.empty((batch, 2), dtype=t.float64, device="cuda") if margins else None
     _lib.call("d3m_bk_factor_batched", batch, n, _P(W), n * n, max(n, 1), float(pivot_tol), int(check_sym),
-              _P(perm), _P(tags), _P(n2), _P(gr), _P(info), _P(sc), _P(asy), _P(scratch), stream_ptr())
-    return _collect(W, perm, tags, n2, info, gr, sc, asy, pivot_tol, labels)
+              _P(perm), _P(tags), _P(n2), _P(gr), _P(info), _P(sc), _P(asy), _P(scratch), _P(mg), stream_ptr())
+    return _collect(W, perm, tags, n2, info, gr, sc, asy, pivot_tol, labels, margin=mg)
 
 
-def _collect(W, perm, tags, n2, info, gr, sc, asy, pivot_tol, labels, wrap=None):
+def _collect(W, perm, tags, n2, info, gr, sc, asy, pivot_tol, labels, wrap=None, margin=None):
     info_h = info.cpu().numpy()
     sc_h = sc.cpu().numpy()
     bad = np.flatnonzero(info_h != -1)
@@ -204,7 +210,11 @@ def _collect(W, perm, tags, n2, info, gr, sc, asy, pivot_tol, labels, wrap=None)
             raise wrap(b, msg)
         raise SingularBlockError(msg)
     gr_h, n2_h = gr.cpu().numpy(), n2.cpu().numpy()
-    return [DenseFactor(W[b], perm[b], tags[b], float(gr_h[b]), int(n2_h[b])) for b in range(W.shape[0])]
+    facs = [DenseFactor(W[b], perm[b], tags[b], float(gr_h[b]), int(n2_h[b])) for b in range(W.shape[0])]
+    if margin is not None:
+        for f, mrow in zip(facs, margin.cpu().numpy()):
+            f.margin = (float(mrow[0]), float(mrow[1]))
+    return facs
 
 
 # ---------------------------------------------------------------------------
@@ -218,6 +228,9 @@ class FactorStats:
     peak_bytes: int = 0
     growth_factor: float = 1.0
     n_2x2_pivots: int = 0
+    # pivot-decision diagnostics (block_ldlt(margins=True); not in the reference)
+    decision_margin: float | None = None
+    argmax_gap: float | None = None
 
 
 class _OffDiag(Mapping):
@@ -633,7 +646,7 @@ def _stream_chunks(sched, pool, flag, base, recs, d_rec, plan_chunks, o, kentrie
 
 
 def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFAULT_PIVOT_TOL,
-               lookahead: bool = True) -> BlockFactor:
+               lookahead: bool = True, margins: bool = False) -> BlockFactor:
     """Right-looking block LDL^T of ``K`` following ``plan`` on one GPU.
 
     factor.py:154-240: per block column j, Bunch-Kaufman of the diagonal
@@ -642,6 +655,11 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
     pattern pairs i >= k on the DMMA tensor pipe (diagonal targets
     symmetrised from the lower half).  The next column's factorisation
     overlaps the current column's trailing update (lookahead).
+
+    ``margins`` (an extension; the reference has no such output) tracks the
+    pivot-decision margins of every diagonal block: each DenseFactor gets
+    ``margin`` = (decision margin, argmax gap) and ``stats`` the minima over
+    the blocks (FactorStats.decision_margin / argmax_gap).
     """
     nb = K.nblocks
     if plan.nblocks != nb:
@@ -690,13 +708,14 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
     binv = empty(max(int(sched.binv_off[-1]), 1))
     nmax = int(sched.sizes.max())
     scratch = empty(4 * nmax) if 64 * nmax > 200 * 1024 else None
+    mg = t.empty((nb, 2), dtype=t.float64, device="cuda") if margins else None
     H = _lib.hptr
     _lib.call("d3m_block_ldlt_exec", nb, H(sched.sizes), H(sched.diag_off), H(sched.panel_off),
               H(sched.panel_rows), H(sched.row_off), H(sched.binv_off), H(sched.task_ptr), H(sched.task_next),
               H(sched.tiles_next), H(sched.tiles_rest), H(sched.tiles_trsm), _P(sched.d_tasks),
               _P(sched.d_trsm_tasks), _P(pool), _P(binv), _P(xbuf), sched.xbuf_elems, _P(perm), _P(tags),
               _P(info), _P(n2), _P(gr), _P(sc), _P(asy), _P(scratch), float(pivot_tol), check_sym,
-              int(bool(lookahead)), nwait, H(wait_cols), H(wait_ev), _P(flag), stream_ptr())
+              int(bool(lookahead)), nwait, H(wait_cols), H(wait_ev), _P(flag), _P(mg), stream_ptr())
     info_h = info.cpu().numpy()
     bad = np.flatnonzero(info_h != -1)
     if bad.size:
@@ -714,6 +733,11 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
                                 float(gr_h[j]), int(n2_h[j])))
     stats = FactorStats(stored, flops, peak, float(max(gr_h.max(), 1.0)) if nb else 1.0, int(n2_h.sum()))
     stats.growth_factor = float(max((f.growth for f in diag), default=1.0))
+    if mg is not None:
+        mh = mg.cpu().numpy()
+        for f, mrow in zip(diag, mh):
+            f.margin = (float(mrow[0]), float(mrow[1]))
+        stats.decision_margin, stats.argmax_gap = float(mh[:, 0].min()), float(mh[:, 1].min())
     F = BlockFactor(plan, diag, _OffDiag(sched, pool), stats, sched, pool, perm, tags)
     F._binv = binv
     # device copy of K's stored blocks (the upload staging buffer or the

@@ -422,14 +422,16 @@ def interpolate_einc(model: FemModel, rhs: int = 0) -> np.ndarray:
 
 
 def solve_d3m(model: FemModel, rhs: int | None = 0, ordering: str = "builtin", timers: dict | None = None,
-              keep: str = "auto", systems: list | None = None):
+              keep: str = "auto", systems: list | None = None, margins: bool = False):
     """Full D3M pipeline of the hot path on the GPU (driver.run_pipeline:103-142
     analog): reduce -> assemble -> ordering / symbolic -> block LDL^T -> block
     solve -> recover, for RHS column ``rhs`` or, with rhs=None, all RHS
     columns at once (one factorisation, n x r solves).  Returns the global
     edge solution (host numpy, n_edges or n_edges x r) and fills ``timers``
     (seconds, wall clock with device synchronisation) when given.  ``keep``
-    is passed to reduce_domains; prebuilt ``systems`` skip the front end."""
+    is passed to reduce_domains; prebuilt ``systems`` skip the front end.
+    ``margins`` tracks the pivot-decision margins of every subdomain and
+    diagonal-block factorisation (DenseFactor.margin, FactorStats)."""
     import time
 
     import torch
@@ -445,14 +447,14 @@ def solve_d3m(model: FemModel, rhs: int | None = 0, ordering: str = "builtin", t
     if systems is None:
         systems = subdomain_systems(model, rhs)
     t1 = tick()
-    red = subdomain.reduce_domains(systems, keep=keep)
+    red = subdomain.reduce_domains(systems, keep=keep, margins=margins)
     t2 = tick()
     R = subdomain.assemble_reduced(red, model)
     g = blockmat.clique_graph(R.K)
     order = ordm.reorder(g, R.K.sizes) if ordering == "builtin" else ordm.identity_ordering(R.K.nblocks)
     plan = symbolic.symbolic_factor(g, order, R.K.sizes)
     t3 = tick()
-    F = factor.block_ldlt(R.K, plan)
+    F = factor.block_ldlt(R.K, plan, margins=margins)
     t4 = tick()
     lam = factor.block_solve(F, R.g)
     t5 = tick()

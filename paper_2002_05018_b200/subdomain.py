@@ -172,7 +172,7 @@ def _free_bytes(t) -> int:
 
 
 def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PIVOT_TOL, keep: str = "factor",
-                   max_batch_bytes: int | None = None) -> list:
+                   max_batch_bytes: int | None = None, margins: bool = False) -> list:
     """Batched reduce_domain (subdomain.py:166-184): subdomains of equal order n
     are factored and reduced together (BK -> multi-RHS solve -> D^T X on DMMA
     -> symmetrisation), in batches sized to the free device memory (or
@@ -189,7 +189,10 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
     device memory.  keep="schur" keeps the factor but forms only the Schur
     blocks, as K = Z_D^T D^-1 Z with Z = L^-1 P [D | F] (A^-1 = P^T L^-T D^-1
     L^-1 P): no backward sweep, no X (recover_primal then solves with the
-    factor) -- for reductions whose primal recovery is not needed (config 3)."""
+    factor) -- for reductions whose primal recovery is not needed (config 3).
+
+    ``margins`` tracks each subdomain factorisation's pivot-decision margins
+    (DenseFactor.margin; include/d3m.h d3m_bk_factor_batched)."""
     t = require_cuda()
     if keep not in ("factor", "solution", "auto", "schur"):
         raise ValueError(f"keep must be 'factor', 'solution', 'auto' or 'schur', not {keep!r}")
@@ -223,7 +226,7 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
             cap = max(1, budget // _domain_bytes(n, m, r))
             chunk = members[pos:pos + cap]
             pos += len(chunk)
-            err = _reduce_chunk(systems, chunk, n, m, r, ms, pivot_tol, keep, vec, out)
+            err = _reduce_chunk(systems, chunk, n, m, r, ms, pivot_tol, keep, vec, out, margins)
             if err is not None and (first_error is None or err[0] < first_error[0]):
                 first_error = err
     if first_error is not None:
@@ -231,7 +234,7 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
     return out
 
 
-def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out):
+def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, margins=False):
     t = require_cuda()
     B = len(members)
     A = empty((B, n, n))
@@ -270,15 +273,17 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out):
         d_tasks = t.empty(64 * B, dtype=t.uint8, device="cuda")
     rows, nrows = _nonzero_rows(D, n) if keep != "schur" else (None, 0)
     wd = empty((B, nrows, m)) if rows is not None else None
+    mg = t.empty((B, 2), dtype=t.float64, device="cuda") if margins else None
     _lib.call("d3m_schur_reduce_batched", B, n, m, r, _P(A), _P(D), _P(f), float(pivot_tol), _P(perm),
               _P(tags), _P(n2), _P(gr), _P(info), _P(sc), _P(asy), _P(K), _P(g), _P(wz), _P(wx), _P(wc),
-              _P(scratch), _P(d_tasks), _P(rows), int(nrows), _P(wd), 1 if keep == "schur" else 0, stream_ptr())
+              _P(scratch), _P(d_tasks), _P(rows), int(nrows), _P(wd), 1 if keep == "schur" else 0, _P(mg),
+              stream_ptr())
     del wd, rows
     del wz, scratch, wc
     try:
         facs = _collect(A, perm, tags, n2, info, gr, sc, asy, pivot_tol, None,
                         wrap=lambda b, msg: SingularDomainError(
-                            f"domain {systems[members[b]].domain} is singular: {msg}"))
+                            f"domain {systems[members[b]].domain} is singular: {msg}"), margin=mg)
     except (SingularDomainError, ValueError) as err:
         return (members[int(_first_bad(info))], err)
     for i, idx in enumerate(members):
