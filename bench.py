@@ -16,8 +16,13 @@ flops are not counted).  One step = block_ldlt + block_solve.
   roofline : the trailing-update DMMA GEMM (dominant kernel) -- its
           algorithmic flops / its summed CUDA-event time in the timed region,
           against the FP64 DMMA peak measured live at start-up
-  cpu_baseline : the CPU oracle port (oracle/) on a bounded sample (the
-          first block columns of the same factorisation) on the host cores
+  cpu_baseline : the CPU oracle port (oracle/: the C restatement of the
+          reference's numba kernels + numpy/OpenBLAS block drivers) running
+          the SAME full step (block LDL^T of K + the 16-RHS solve) on the
+          host cores, timed once; the secondaries carry same-run CPU timings
+          of the subdomain reductions (configs 1 and 3, process pools)
+  secondary : configs 1, 2, 3 and 5 (BASELINE configs[0], [1], [2], [4]),
+          each with time, rate, roofline fraction and pivot-decision margins
 
 `--impl reference` runs only the CPU oracle port on the same metric.
 N > 1 (torchrun): independent replicas per GPU (the block LDL^T chain does
@@ -225,6 +230,12 @@ def run_ours(args):
     # residual check of the last step (untimed)
     res = _residual(K, rhs, [np.asarray(v) for v in x])
     refined = _refine_leg(d, F, K, rhs, rhs_d)
+    # pivot-decision margins of the 144 diagonal blocks (one extra, untimed factorisation)
+    del F, x
+    Fm = d.block_ldlt(Kd, plan, margins=True)
+    margins_cfg4 = {"decision_margin": Fm.stats.decision_margin, "argmax_gap": Fm.stats.argmax_gap}
+    del Fm
+    x = None
 
     # ---- e2e: public API with host buffers ------------------------------------
     # inputs in pinned host memory (K's blocks as views of one pinned
@@ -233,7 +244,6 @@ def run_ours(args):
     Kp, rhs_p = _pinned_inputs(K, rhs)
     h2d = 16 * sum(int(np.asarray(b).size) for b in K.blocks.values()) + 16 * sum(b.size for b in rhs)
     d2h = 16 * sum(b.size for b in rhs)
-    del F, x                                         # one factor alive at a time, as a caller would
     Fh = d.block_ldlt(Kp, plan)                     # untimed e2e warm-up step
     xh = [np.asarray(v) for v in d.block_solve(Fh, rhs_p, refine=REFINE)]
     del Fh, xh
@@ -255,6 +265,29 @@ def run_ours(args):
     # few-sample run otherwise dominates the mean
     e2e_ms = _max_over_ranks(dist, float(np.median(e2e_samples)))
     e2e_value = flops_step * ws / (e2e_ms * 1e-3) / 1e12
+    del xh
+    # the same with plain numpy inputs (a ddsolve caller's K.blocks / RHS
+    # arrays): pageable host memory, staged by the library
+    Fh = d.block_ldlt(K, plan)
+    xh = [np.asarray(v) for v in d.block_solve(Fh, rhs, refine=REFINE)]
+    del Fh, xh
+    torch.cuda.synchronize()
+    np_samples = []
+    gc.collect()
+    gc.disable()
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        Fh = d.block_ldlt(K, plan)
+        xh = [np.asarray(v) for v in d.block_solve(Fh, rhs, refine=REFINE)]
+        torch.cuda.synchronize()
+        np_samples.append((time.perf_counter() - t0) * 1e3)
+        del Fh
+    gc.enable()
+    np_ms = _max_over_ranks(dist, float(np.median(np_samples)))
+    e2e_numpy = {"value": round(flops_step * ws / (np_ms * 1e-3) / 1e12, 4), "unit": "TFLOP/s",
+                 "ms_per_step": round(np_ms, 3), "samples_ms": [round(v, 1) for v in np_samples],
+                 "statistic": "median", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                 "inputs": "numpy complex128 arrays (pageable host memory), as the reference API takes them"}
     del xh
 
     if rank != 0:
@@ -306,18 +339,25 @@ def run_ours(args):
                 "samples_ms": [round(v, 1) for v in e2e_samples], "statistic": "median"},
         "residual": res,
         "refined": refined,
+        "margins": margins_cfg4,
         "clocks": clk.summary(),
     }
+    line["e2e_numpy"] = e2e_numpy
     sec = {}
     if not args.no_cfg3:
-        sec["cfg3"] = _cfg3_secondary(max(2, min(args.steps, 3)))
-    for which in (["cfg1", "cfg2"] if not args.no_fem else []) + (["cfg5"] if args.cfg5 else []):
-        sec[which] = _fem_secondary(which, 1 if which == "cfg5" else 2)
-    # the CPU leg runs last: OpenBLAS worker threads keep spinning after a
+        sec["cfg3"] = _cfg3_secondary(max(2, min(args.steps, 3)), peak)
+    for which in (["cfg1", "cfg2"] if not args.no_fem else []) + (["cfg5"] if not args.no_cfg5 else []):
+        sec[which] = _fem_secondary(which, 1 if which == "cfg5" else 2, peak)
+    # the CPU legs run last: OpenBLAS worker threads keep spinning after a
     # call and would slow the host-side launches of the GPU legs
-    cpu = _cpu_sample(plan, K, rank, args.cpu_sample_columns) if not args.no_cpu else None
-    if cpu is not None:
-        line["cpu_baseline"] = cpu
+    if not args.no_cpu:
+        del Kd, rhs_d
+        line["cpu_baseline"] = _cpu_full_cfg4(plan, K, rhs, flops_step, ms_step)
+        if "cfg1" in sec:
+            sec["cfg1"]["cpu_reduce"] = _cpu_reduce_pool("cfg1", [0, 1], sec["cfg1"]["stage_ms"]["reduce"])
+        if "cfg3" in sec:
+            sec["cfg3"]["cpu_reduce"] = _cpu_reduce_pool("cfg3", list(range(8)), sec["cfg3"]["ms_per_step"],
+                                                         total=64)
     if sec:
         line["secondary"] = sec
     print(json.dumps(line), flush=True)
@@ -343,21 +383,23 @@ def _pinned_inputs(K, rhs):
     return Kp, rhs_p
 
 
-def _fem_secondary(which: str, reps: int) -> dict:
+def _fem_secondary(which: str, reps: int, peak: float) -> dict:
     """BASELINE configs[0] / [1] / [4]: the full D3M pipeline on the 3-D
     Nedelec FEM problems (fem3d.py; all RHS columns at once), from the
     host-built subdomain systems (sparse A_d / D_d) to the recovered global
     solution on the host: reduce (incl. H2D) -> assemble -> block LDL^T ->
     block solve -> recover (incl. D2H).  The mesh / element front end is
     excluded (it is not part of the path).  Best of ``reps`` timed runs after
-    one warm-up run (config 5: a single run, first call included)."""
+    one warm-up run (config 5: a single run, first call included).  The
+    pivot-decision margins of every subdomain and diagonal-block
+    factorisation are tracked in the first run (config 5: its only run)."""
     import torch
     from paper_2002_05018_b200 import fem3d
     cfg = {"cfg1": fem3d.config1, "cfg2": fem3d.config2, "cfg5": fem3d.config5}[which]()
     model = fem3d.build_model(cfg)
     systems = fem3d.subdomain_systems(model, rhs=None)
     runs = reps if which == "cfg5" else reps + 1
-    best, keep = None, None
+    best, keep, margins = None, None, None
     for i in range(runs):
         for s in systems:
             s.factor, s._d3m_D, s._d3m_X = None, None, None
@@ -365,7 +407,14 @@ def _fem_secondary(which: str, reps: int) -> dict:
         # a collection before each run (not a paused collector: the pipeline's
         # temporaries must be reclaimable, or the allocator grows instead of reusing)
         gc.collect()
-        sol, _, R, plan, F = fem3d.solve_d3m(model, rhs=None, keep="auto", timers=timers, systems=systems)
+        sol, _, R, plan, F = fem3d.solve_d3m(model, rhs=None, keep="auto", timers=timers, systems=systems,
+                                             margins=(i == 0))
+        if i == 0:
+            sub = [s.factor.margin for s in systems]
+            margins = {"subdomain_decision_margin": min(m[0] for m in sub),
+                       "subdomain_argmax_gap": min(m[1] for m in sub),
+                       "k_decision_margin": F.stats.decision_margin, "k_argmax_gap": F.stats.argmax_gap,
+                       "tracked_in": "the timed run" if runs == 1 else "the warm-up run"}
         if (runs == 1 or i > 0) and (best is None or timers["d3m_total"] < best["d3m_total"]):
             best = timers
         keep = "solution" if systems[0].factor.released else "factor"
@@ -377,11 +426,17 @@ def _fem_secondary(which: str, reps: int) -> dict:
     # algorithmic: complex symmetric LDL^T 4n^3/3 + the (m+r)-RHS solves 8n^2(m+r);
     # D^T X is a sparse product (D = s M_Gamma on interface rows) and not counted
     flops_sub = sum(4 * s.n_dofs ** 3 // 3 + 8 * s.n_dofs ** 2 * (m + r) for s, m in zip(systems, ms_sub))
+    sub_tf = flops_sub / best["reduce"] / 1e12
     out = {"workload": f"{which}: {cfg.cells}^3 hex x6 tets Nedelec, {cfg.parts} subdomains, "
                        f"{model.mesh.n_edges} edges, lambda={int(R.interface_sizes.sum())}, {r} RHS",
            "d3m_ms": round(best["d3m_total"] * 1e3, 1),
            "stage_ms": {k: round(v * 1e3, 1) for k, v in best.items() if k not in ("front_end", "d3m_total")},
-           "subdomain_tflops": round(flops_sub / best["reduce"] / 1e12, 2),
+           "subdomain_tflops": round(sub_tf, 2),
+           "roofline": {"bound": "tensor", "stage": "reduce (subdomain BK + solves, incl. H2D)",
+                        "achieved": round(sub_tf, 2), "peak": round(peak, 2), "unit": "TFLOP/s",
+                        "frac": round(sub_tf / peak, 4),
+                        "note": "algorithmic flops (4n^3/3 + 8n^2(m+r)) over the reduce stage's wall time"},
+           "margins": margins,
            "subdomain_flops": int(flops_sub), "n_subdomain": sorted({s.n_dofs for s in systems}),
            "keep": keep, "residual": res,
            "note": "wall clock with device syncs; reduce includes the sparse-block H2D, recover the D2H"}
@@ -389,7 +444,7 @@ def _fem_secondary(which: str, reps: int) -> dict:
     return out
 
 
-def _cfg3_secondary(steps: int) -> dict:
+def _cfg3_secondary(steps: int, peak: float) -> dict:
     """BASELINE configs[2]: batched Schur complement of 64 subdomains
     (n = 2048, m = 384); the workload's output is K_D / g_d only, so the
     reduction runs in its Schur-only form (keep="schur": forward sweep,
@@ -444,18 +499,20 @@ def _cfg3_secondary(steps: int) -> dict:
     e2e_ms = (time.perf_counter() - t0) * 1e3
     gc.enable()
     h2d = 16 * sum(s.A.size + s.f.size + sum(c.D.size for c in s.couplings) for s in host)
+    for s in dev:
+        s.factor = None
+        s._d3m_D = None
+    d.reduce_domains(dev, keep="schur", margins=True)            # untimed: pivot-decision margins
+    mg = [s.factor.margin for s in dev]
+    value = flops / (ms * 1e-3) / 1e12
     out = {"workload": "cfg3: 64 subdomains, n=2048, m=384 (A_i=(M+M^T)/2, D_i one +-1 per column), K_D and g_d",
-           "ms_per_step": round(ms, 3), "value": round(flops / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+           "ms_per_step": round(ms, 3), "value": round(value, 3), "unit": "TFLOP/s",
+           "roofline": {"bound": "tensor", "achieved": round(value, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
+                        "frac": round(value / peak, 4),
+                        "note": "effective: the reference algorithm's flops (4n^3/3 + 8n^2(m+1)) / device time"},
+           "margins": {"decision_margin": min(m[0] for m in mg), "argmax_gap": min(m[1] for m in mg)},
            "flops_per_step": flops, "e2e": {"ms_per_step": round(e2e_ms, 1), "h2d_bytes_per_step": int(h2d),
                                              "d2h_bytes_per_step": int(16 * B * m * (m + 1))}}
-    try:
-        import json as _j
-        g = np.load(os.path.join(ROOT, "tests", "golden", "cfg3.npz"))
-        out["cpu_reference_s_per_subdomain"] = round(float(g["time0"]), 1)
-        out["cpu_reference_note"] = ("reference reduce_domain (numba JIT) timed in the build container "
-                                     "(8-core Xeon) by tools/gen_golden.py; 64 subdomains ~ 64x serial")
-    except Exception:
-        pass
     del red, red_h, host_p, outs
     return out
 
@@ -502,32 +559,98 @@ def _residual(K, rhs, x) -> float:
     return float((num / den).max())
 
 
-def _cpu_sample(plan, K, rank, columns):
-    """Oracle port (oracle/d3m_oracle.py + C kernels, OpenBLAS ZGEMM on all
-    host threads) timed on the first `columns` block columns of the same
-    factorisation.  Returns the cpu_baseline object."""
+def _column_flops(sizes, pattern, columns) -> int:
+    """Algorithmic flops of the first `columns` block columns, counted as the
+    GPU side counts them (factor._Schedule): BK 4n^3/3 (complex symmetric
+    LDL^T), panel TRSM 4 R_j n_j^2, trailing updates 8 n_i n_k n_j (4 n_i^2 n_j
+    for diagonal targets)."""
+    fl = 0
+    for j in range(columns):
+        nj = int(sizes[j])
+        rows = [int(i) for i in pattern[j]]
+        fl += 4 * nj ** 3 // 3 + 4 * sum(int(sizes[i]) for i in rows) * nj * nj
+        for a, i in enumerate(rows):
+            for kk in rows[:a + 1]:
+                fl += (8 if i != kk else 4) * int(sizes[i]) * int(sizes[kk]) * nj
+    return fl
+
+
+def _cpu_full_cfg4(plan, K, rhs, flops_step, gpu_ms):
+    """The oracle port (C restatement of the reference's numba kernels +
+    numpy/OpenBLAS ZGEMM on all host threads, the reference's own algorithm
+    and drivers) running the SAME step as the GPU: the full block LDL^T of
+    config 4 and the 16-RHS block solve, timed once on the host cores."""
     from oracle import d3m_oracle as O
     adj = O.clique_adjacency(K.nblocks, K.blocks.keys())
     oplan = O.symbolic_factor(adj, plan.order.perm, K.sizes)
     blocks = {k: np.asarray(v) for k, v in K.blocks.items()}
     O.block_ldlt(blocks, oplan, columns=1)          # warm (loads the C kernels)
     t0 = time.perf_counter()
-    F = O.block_ldlt(blocks, oplan, columns=columns)
-    dt = time.perf_counter() - t0
-    sizes = oplan["sizes_perm"]
-    fl = 0
-    for j in range(columns):
-        nj = int(sizes[j])
-        rows = [int(i) for i in oplan["pattern"][j]]
-        fl += 8 * nj ** 3 // 3 + 4 * sum(int(sizes[i]) for i in rows) * nj * nj
-        for a, i in enumerate(rows):
-            for kk in rows[:a + 1]:
-                fl += (8 if i != kk else 4) * int(sizes[i]) * int(sizes[kk]) * nj
+    F = O.block_ldlt(blocks, oplan)
+    t1 = time.perf_counter()
+    O.block_solve(F, rhs)
+    t2 = time.perf_counter()
     del F
-    return {"value": round(fl / dt / 1e12, 6), "unit": "TFLOP/s", "cores": os.cpu_count(),
-            "kind": "port", "seconds": round(dt, 3),
-            "sample": f"first {columns} of 144 block columns of the cfg4 block LDL^T (BK + TRSM + trailing "
-                      f"updates, {fl / 1e9:.2f} GFLOP), oracle port with OpenBLAS ZGEMM on all host threads"}
+    dt = t2 - t0
+    return {"value": round(flops_step / dt / 1e12, 6), "unit": "TFLOP/s", "cores": os.cpu_count(),
+            "kind": "port", "seconds": round(dt, 2), "factor_s": round(t1 - t0, 2), "solve_s": round(t2 - t1, 2),
+            "gpu_speedup_device_resident": round(dt / (gpu_ms * 1e-3), 1),
+            "sample": "the full cfg4 step (block LDL^T of all 144 block columns + 16-RHS block solve, "
+                      f"{flops_step / 1e12:.2f} TFLOP counted as the GPU counts them), oracle port with OpenBLAS "
+                      "ZGEMM on all host threads, one run"}
+
+
+def _cpu_reduce_worker(job):
+    """One subdomain's reduce_domain (subdomain.py:166-184) by the oracle
+    port, in a spawned process (OpenBLAS single-threaded)."""
+    cfg, idx = job
+    sys.path.insert(0, ROOT)
+    from oracle import d3m_oracle as O
+    if cfg == "cfg3":
+        from paper_2002_05018_b200 import workloads as wl
+        A, D, f = wl.config3_domain(idx)
+    else:
+        from paper_2002_05018_b200 import fem3d
+        model = fem3d.build_model(getattr(fem3d, "config1" if cfg == "cfg1" else "config2")())
+        s = fem3d.subdomain_systems(model, rhs=0, sparse=False)[idx]
+        A, f = np.asarray(s.A), np.asarray(s.f)
+        D = np.concatenate([np.asarray(c.D) for c in s.couplings], axis=1)
+    O.dense_ldlt_bk(np.eye(2, dtype=complex))       # load the C kernels
+    t0 = time.perf_counter()
+    O.reduce_domain(A, D, f)
+    return time.perf_counter() - t0
+
+
+def _cpu_reduce_pool(cfg, indices, gpu_ms, total=None):
+    """Same-run CPU timing of the subdomain reduction: the
+    oracle port's reduce_domain on `indices` subdomains in a pool of
+    single-threaded processes (subdomains are independent),
+    extrapolated to all `total` subdomains at the same pool width."""
+    import multiprocessing as mp
+    procs = max(1, min(len(indices), os.cpu_count() or 1))
+    old = os.environ.get("OPENBLAS_NUM_THREADS")
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    try:
+        with mp.get_context("spawn").Pool(procs) as pool:
+            t0 = time.perf_counter()
+            secs = pool.map(_cpu_reduce_worker, [(cfg, i) for i in indices])
+            wall = time.perf_counter() - t0
+    finally:
+        if old is None:
+            os.environ.pop("OPENBLAS_NUM_THREADS", None)
+        else:
+            os.environ["OPENBLAS_NUM_THREADS"] = old
+    total = total or len(indices)
+    per = float(np.mean(secs))
+    waves = -(-total // procs)
+    est = waves * max(secs) if total != len(indices) else max(secs)
+    return {"kind": "port", "procs": procs, "cores": os.cpu_count(), "subdomains_timed": len(indices),
+            "s_per_subdomain": round(per, 2), "wall_s": round(wall, 2),
+            "all_subdomains_s": round(est, 1), "extrapolated": total != len(indices),
+            "gpu_speedup": round(est / (gpu_ms * 1e-3), 1),
+            "note": f"oracle reduce_domain per subdomain in {procs} single-threaded processes"
+                    + (f"; {total} subdomains = {waves} waves of the slowest timed one" if total != len(indices)
+                       else "")}
 
 
 def run_reference(args):
@@ -541,15 +664,7 @@ def run_reference(args):
     oplan = O.symbolic_factor(adj, plan.order.perm, K.sizes)
     blocks = {k: np.asarray(v) for k, v in K.blocks.items()}
     cols = args.cpu_sample_columns
-    sizes = oplan["sizes_perm"]
-    fl = 0
-    for j in range(cols):
-        nj = int(sizes[j])
-        rows = [int(i) for i in oplan["pattern"][j]]
-        fl += 8 * nj ** 3 // 3 + 4 * sum(int(sizes[i]) for i in rows) * nj * nj
-        for a, i in enumerate(rows):
-            for kk in rows[:a + 1]:
-                fl += (8 if i != kk else 4) * int(sizes[i]) * int(sizes[kk]) * nj
+    fl = _column_flops(oplan["sizes_perm"], oplan["pattern"], cols)
     for _ in range(args.warmup):
         O.block_ldlt(blocks, oplan, columns=cols)
     t0 = time.perf_counter()
@@ -577,10 +692,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-columns", type=int, default=CPU_SAMPLE_COLUMNS)
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU legs (cpu_baseline, cfg1/cfg3 CPU reduce)")
     ap.add_argument("--no-cfg3", action="store_true", help="skip the secondary config-3 measurement")
     ap.add_argument("--no-fem", action="store_true", help="skip the FEM config-1/2 secondaries")
-    ap.add_argument("--cfg5", action="store_true", help="also run FEM config 5 (~60 s, ~157 GB HBM)")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip FEM config 5 (~30 s, ~150 GB HBM)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

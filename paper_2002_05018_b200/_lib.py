@@ -24,6 +24,7 @@ _SIGNATURES = {
     "d3m_abi_version": [],
     "d3m_bk_factor_batched": [I32, I32, P, I64, I32, F64, I32, P, P, P, P, P, P, P, P, P, P],
     "d3m_bk_cluster_max_n": [I32],
+    "d3m_plan_flow_items": [I32, P, P, P, P, P, I64, P, I64, P, P],
     "d3m_ldlt_solve_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P],
     "d3m_zgemm_grouped": [I32, I32, P, P, P, P, I32, P, P],
     "d3m_gemm_set_form": [I32],
@@ -48,7 +49,8 @@ _SIGNATURES = {
     "d3m_ldlt_solve_blocked_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P, P],
 }
 _SIZE_T = {"d3m_bk_panel_workspace": [I32, I32]}
-_INT64 = {"d3m_timing_intervals": [P, I64]}
+_INT64 = {"d3m_timing_intervals": [P, I64],
+          "d3m_plan_gemm_tasks": [I32, P, P, P, P, P, P, I64, P, P, P, P, P]}
 _VOID = {"d3m_set_timing": [I32], "d3m_counters_reset": []}
 
 # GemmTask / CopyTask records (csrc/d3m_gemm.h, csrc/d3m_misc.h)
@@ -79,8 +81,13 @@ class D3MError(RuntimeError):
 _lib = None
 
 
+ABI_VERSION = 9          # include/d3m.h D3M_ABI_VERSION this binding is written for
+
+
 def load():
-    """Load libd3m.so (building it first if the sources are newer)."""
+    """Load libd3m.so (built by build_ext / __graft_entry__.build; there is no
+    implicit rebuild).  A library of another ABI version is rejected: an old
+    build would take the new argument lists silently."""
     global _lib
     if _lib is not None:
         return _lib
@@ -89,6 +96,11 @@ def load():
             f"{LIB_PATH} is missing; build it with `python -m paper_2002_05018_b200.build_ext` "
             "(the D3M path has no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
+    lib.d3m_abi_version.restype = ctypes.c_int
+    lib.d3m_abi_version.argtypes = []
+    if lib.d3m_abi_version() != ABI_VERSION:
+        raise D3MUnavailable(f"{LIB_PATH} has ABI version {lib.d3m_abi_version()}, this binding needs "
+                             f"{ABI_VERSION}; rebuild it with `python -m paper_2002_05018_b200.build_ext --force`")
     for name, args in _SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = args

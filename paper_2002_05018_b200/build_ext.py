@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 OUT = os.path.join(HERE, "libd3m.so")
-SOURCES = ["bk_exact.cu", "bk_cluster.cu", "zgemm_dmma.cu", "ldlt_solve.cu", "skinny_dmma.cu", "bk_panel.cu", "solve_blocked.cu", "d3m_misc.cu", "d3m_capi.cu"]
+SOURCES = ["bk_exact.cu", "bk_cluster.cu", "zgemm_dmma.cu", "ldlt_solve.cu", "skinny_dmma.cu", "bk_panel.cu", "solve_blocked.cu", "d3m_misc.cu", "d3m_capi.cu", "d3m_plan.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
 
@@ -29,12 +29,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     objdir = os.path.join(HERE, "_obj")
     os.makedirs(objdir, exist_ok=True)
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".cu")]
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith((".cu", ".cpp"))]
     headers.append(os.path.join(INCLUDE, "d3m.h"))
     hdr_t = max(os.path.getmtime(h) for h in headers)
     objs, cmds = [], []
     for src in SOURCES:
-        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
         objs.append(obj)
         srcp = os.path.join(CSRC, src)
         if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(srcp)):

@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib
+from . import _lib, planner
 from .blockmat import BlockSparseSym
 from .device import DeviceArray, empty, require_cuda, stream_ptr, to_device, upload_bytes, upload_i64
 from .symbolic import EliminationPlan
@@ -312,42 +312,13 @@ class _Schedule:
         self.offdiag_keys = sorted(self.loc, key=lambda ij: (ij[1], ij[0]))
         self.piv_elems = int(self.row_off[-1])
         # trailing-update GEMM tasks, "next" (targets in column j+1) first
-        recs, ptr, nxt, tiles_n, tiles_r = [], [0], [], [], []
+        # (native planner, csrc/d3m_plan.cpp d3m_plan_gemm_tasks)
         bm = _lib.GEMM_BM
-        for j in range(nb):
-            nj = int(sizes[j])
-            rows = [int(i) for i in pattern[j]]
-            prow = np.concatenate([[0], np.cumsum(sizes[rows])]).astype(np.int64) if rows else [0]
-            nxt_recs, rest_recs = [], []
-            for a, i in enumerate(rows):
-                for b in range(a + 1):
-                    kk = rows[b]
-                    ni, nk = int(sizes[i]), int(sizes[kk])
-                    if i == kk:
-                        c_off, ldc, flags = int(self.diag_off[i]), ni, _lib.GEMM_SUB | _lib.GEMM_SYM
-                        tm = (ni + bm - 1) // bm
-                        tiles = tm * (tm + 1) // 2
-                    else:
-                        if (i, kk) not in self.rowpos:
-                            raise FactorConsistencyError(f"update targets block {(i, kk)} outside pattern")
-                        c_off, ldc, flags = int(self.panel_off[kk]) + self.rowpos[(i, kk)] * nk, nk, _lib.GEMM_SUB
-                        tiles = ((ni + bm - 1) // bm) * ((nk + bm - 1) // bm)
-                    rec = (int(prow[a]) * nj, int(self.panel_off[j]) + int(prow[b]) * nj, c_off, ni, nk, nj,
-                           nj, nj, ldc, flags, tiles, (nk + bm - 1) // bm)
-                    (nxt_recs if kk == j + 1 else rest_recs).append(rec)
-            for group, tl in ((nxt_recs, tiles_n), (rest_recs, tiles_r)):
-                start = 0
-                for rec in group:
-                    recs.append(rec[:10] + (start, rec[11], 0))
-                    start += rec[10]
-                tl.append(start)
-            nxt.append(ptr[-1] + len(nxt_recs))
-            ptr.append(ptr[-1] + len(nxt_recs) + len(rest_recs))
-        tasks = np.zeros(len(recs), dtype=_lib.GEMM_TASK)
-        if recs:
-            arr = np.array(recs, dtype=np.int64)
-            for c, name in enumerate(_lib.GEMM_TASK.names):
-                tasks[name] = arr[:, c]
+        try:
+            tasks, ptr, nxt, tiles_n, tiles_r, self.flops_update = planner.gemm_tasks(
+                sizes, pattern, self.diag_off, self.panel_off)
+        except ValueError as err:
+            raise FactorConsistencyError(str(err)) from None
         self.tasks = tasks
         # panel TRSM as one GEMM per column: X = panel * Binv_j^T
         self.binv_off = np.concatenate([[0], np.cumsum(sizes * sizes)]).astype(np.int64)
@@ -367,10 +338,10 @@ class _Schedule:
         self.d_diag_off = upload_i64(self.diag_off if nb else np.zeros(1, np.int64))
         self.d_sizes = upload_i64(sizes if nb else np.zeros(1, np.int64))
         self.part_rows = int(max([len(p) * int(sizes[j]) for j, p in enumerate(pattern)] + [1]))
-        self.task_ptr = np.asarray(ptr, dtype=np.int64)
-        self.task_next = np.asarray(nxt if nxt else [0], dtype=np.int64)
-        self.tiles_next = np.asarray(tiles_n if tiles_n else [0], dtype=np.int64)
-        self.tiles_rest = np.asarray(tiles_r if tiles_r else [0], dtype=np.int64)
+        self.task_ptr = ptr
+        self.task_next = nxt
+        self.tiles_next = tiles_n
+        self.tiles_rest = tiles_r
         self.d_tasks = upload_bytes(tasks) if len(tasks) else t.zeros(64, dtype=t.uint8, device="cuda")
         self.xbuf_elems = 2 * max(1, int((self.panel_rows * sizes).max()) if nb else 1)
         # block_solve backward gather: global plan-order rows of every panel
@@ -381,9 +352,6 @@ class _Schedule:
             gptr.append(gptr[-1] + int(self.panel_rows[j]))
         self.gptr = np.asarray(gptr, dtype=np.int64)
         self.d_gidx = upload_i64(np.concatenate(gidx) if gidx else np.zeros(1, np.int64))
-        self.flops_update = int(sum(8 * int(sizes[i]) * int(sizes[kk]) * int(sizes[j]) if i != kk else
-                                    4 * int(sizes[i]) ** 2 * int(sizes[j])
-                                    for j in range(nb) for a, i in enumerate(pattern[j]) for kk in pattern[j][:a + 1]))
         self.flops_trsm = int(sum(4 * int(self.panel_rows[j]) * int(sizes[j]) ** 2 for j in range(nb)))
         self.flops_bk = int(sum(4 * int(s) ** 3 // 3 for s in sizes))     # complex LDL^T: 4n^3/3
         self.stats_cache = {}
@@ -783,107 +751,12 @@ def _solve_flow(sched: _Schedule):
 
 
 def flow_items(sizes, pattern, panel_rows):
-    """Host part of _solve_flow (pure numpy; tests/test_solve_flow.py checks
-    that the list is a topological order).  Returns (items int32 [n, 8],
-    deps int32 [m, 2], part_off int64 [nb], counter count, partial elems)."""
-    nb = len(sizes)
-    sizes = [int(v) for v in sizes]
-    T = [(n + 15) // 16 for n in sizes]
-    pat = [[int(i) for i in p] for p in pattern]
-    prow = [dict() for _ in range(nb)]                 # panel row offset of target block i in panel j
-    for j in range(nb):
-        r = 0
-        for i in pat[j]:
-            prow[j][i] = r
-            r += sizes[i]
-    ZC, BLK, UC, CC, RC, XC = (k * nb for k in range(6))
-    seq_base = np.concatenate([[6 * nb], 6 * nb + np.cumsum(T)]).astype(np.int64)
-    ncnt = int(seq_base[-1]) + 1                       # + queue head
-    items, deps = [], []
-
-    def add(typ, j, p0, p1, dl, inc0, inc1=-1):
-        items.append((typ, j, p0, p1, len(deps), len(dl), inc0, inc1))
-        deps.extend(dl)
-
-    n_into = [0] * nb                                  # FB tile items into each block
-    for j in range(nb):
-        for i in pat[j]:
-            n_into[i] += T[i]
-    seq_k = [[0] * T[i] for i in range(nb)]
-
-    def update(j, i):
-        for t in range(T[i]):
-            rows = min(16, sizes[i] - 16 * t)
-            add(_FB, j, prow[j][i] + 16 * t, rows, [(ZC + j, T[j]), (int(seq_base[i]) + t, seq_k[i][t])],
-                int(seq_base[i]) + t, BLK + i)
-            seq_k[i][t] += 1
-
-    pending = [[] for _ in range(nb)]                  # deferred updates (column j) per target block, FIFO
-
-    def flush(i, upto=None):
-        while pending[i] and (upto is None or pending[i][0] <= upto):
-            update(pending[i].pop(0), i)
-
-    for j in range(nb):
-        if sizes[j]:
-            for t in range(T[j]):
-                add(_FA, j, t, 0, [(BLK + j, n_into[j])] if n_into[j] else [], ZC + j)
-            for r0 in range(0, sizes[j], _FD_ROWS):
-                add(_FD, j, r0, min(sizes[j], r0 + _FD_ROWS), [(ZC + j, T[j])], UC + j)
-        if pat[j]:
-            par = pat[j][0]
-            flush(par)
-            update(j, par)
-        if j >= 1:
-            for i in pat[j - 1][1:]:
-                flush(i, upto=j - 1)
-        for i in pat[j][1:]:
-            pending[i].append(j)
-    for i in range(nb):
-        flush(i)
-    # backward
-    nch = [(int(panel_rows[j]) + _KCH - 1) // _KCH for j in range(nb)]
-
-    def chunk_blocks(j, ch):
-        lo, hi = ch * _KCH, min(int(panel_rows[j]), ch * _KCH + _KCH)
-        return [i for i in pat[j] if prow[j][i] < hi and prow[j][i] + sizes[i] > lo and sizes[i]]
-
-    def parent_chunk(j, ch):
-        return bool(pat[j]) and pat[j][0] in chunk_blocks(j, ch)
-
-    done_far = [False] * nb
-
-    def chunks(j, far):
-        for ch in range(nch[j]):
-            if parent_chunk(j, ch) != far:
-                for mt in range(T[j]):
-                    add(_BC, j, ch, mt, [(XC + i, T[i]) for i in chunk_blocks(j, ch)], CC + j)
-
-    for j in range(nb - 1, -1, -1):
-        if not sizes[j]:
-            continue
-        if not done_far[j]:
-            chunks(j, True)
-            done_far[j] = True
-        chunks(j, False)
-        npc = (sizes[j] + _BR_ROWS - 1) // _BR_ROWS
-        nfd = (sizes[j] + _FD_ROWS - 1) // _FD_ROWS
-        for pc in range(npc):
-            add(_BR, j, _BR_ROWS * pc, min(sizes[j], _BR_ROWS * pc + _BR_ROWS), [(CC + j, nch[j] * T[j]), (UC + j, nfd)],
-                RC + j)
-        for t in range(T[j]):
-            add(_BE, j, t, 0, [(RC + j, npc)], XC + j)
-        if j >= 1 and sizes[j - 1] and not done_far[j - 1]:
-            chunks(j - 1, True)
-            done_far[j - 1] = True
-    part_off = np.zeros(max(nb, 1), dtype=np.int64)
-    acc = 0
-    for j in range(nb):
-        part_off[j] = acc
-        acc += nch[j] * sizes[j] * 16
-    it = np.ascontiguousarray(np.asarray(items, dtype=np.int32).reshape(-1, 8))
-    dp = np.ascontiguousarray(np.asarray(deps, dtype=np.int32).reshape(-1, 2) if deps else np.zeros((1, 2), np.int32))
-    return it, dp, part_off, ncnt, max(acc, 1)
+    """Work list of the dataflow block solve, built by the native planner
+    (csrc/d3m_plan.cpp d3m_plan_flow_items; tests/test_solve_flow.py checks
+    it is a topological order and equals the Python restatement).  Returns
+    (items int32 [n, 8], deps int32 [m, 2], part_off int64 [nb], counter
+    count, partial elems)."""
+    return planner.flow_items(sizes, pattern, panel_rows)
 
 
 def _residual_launches(F: BlockFactor, cols: int):

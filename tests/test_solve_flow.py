@@ -1,15 +1,19 @@
-"""Host checks of the dataflow block-solve work list (factor.flow_items):
-every item's dependencies are satisfied by the items before it (so the
-device queue, which hands items out in list order, cannot deadlock), each
-16-row tile receives its updates in ascending column order, and every
-counter reaches the value the later items wait for."""
+"""Host checks of the native planner (csrc/d3m_plan.cpp, no GPU needed).
+
+The dataflow block-solve work list (factor.flow_items): every item's
+dependencies are satisfied by the items before it (so the device queue,
+which hands items out in list order, cannot deadlock), each 16-row tile
+receives its updates in ascending column order, every counter reaches the
+value the later items wait for, and the list equals the pure-Python
+restatement (tests/ref/flow_ref.py).  The block_ldlt GEMM task table equals
+its Python restatement (tests/ref/schedule_ref.py) record for record."""
 
 from __future__ import annotations
 
 import numpy as np
 import pytest
 
-from paper_2002_05018_b200 import workloads as wl
+from paper_2002_05018_b200 import planner, workloads as wl
 from paper_2002_05018_b200.blockmat import clique_graph
 from paper_2002_05018_b200.factor import _BC, _BE, _BR, _FA, _FB, _FD, flow_items
 from paper_2002_05018_b200.ordering import identity_ordering, reorder
@@ -21,6 +25,11 @@ def _check(plan):
     pattern = [np.asarray(p, dtype=np.int64) for p in plan.pattern]
     panel_rows = np.array([int(sizes[p].sum()) for p in pattern], dtype=np.int64)
     items, deps, part_off, ncnt, part_elems = flow_items(sizes, pattern, panel_rows)
+    from ref.flow_ref import flow_items_ref
+    ref = flow_items_ref(sizes, pattern, panel_rows)
+    assert np.array_equal(items, ref[0]) and np.array_equal(deps, ref[1]) and np.array_equal(part_off, ref[2])
+    assert (ncnt, part_elems) == ref[3:]
+    _check_tasks(sizes, pattern)
     cnt = np.zeros(ncnt, dtype=np.int64)
     upd_order = {}
     for idx, (typ, j, p0, p1, doff, dcnt, inc0, inc1) in enumerate(items):
@@ -52,6 +61,32 @@ def _check(plan):
         seen[(i, t)] = j
     assert part_elems >= 1 and len(part_off) >= 1
     return items
+
+
+def _check_tasks(sizes, pattern):
+    from ref.schedule_ref import gemm_tasks_ref
+    nb = len(sizes)
+    diag_off = np.zeros(nb, dtype=np.int64)
+    panel_off = np.zeros(nb, dtype=np.int64)
+    off = 0
+    for j in range(nb):
+        diag_off[j] = off
+        off += int(sizes[j]) ** 2
+        panel_off[j] = off
+        off += int(sizes[pattern[j]].sum()) * int(sizes[j])
+    got = planner.gemm_tasks(sizes, pattern, diag_off, panel_off)
+    want = gemm_tasks_ref(sizes, pattern, diag_off, panel_off)
+    assert got[0].tobytes() == want[0].tobytes()
+    for a, b in zip(got[1:5], want[1:5]):
+        assert np.array_equal(a, b)
+    assert got[5] == want[5]
+
+
+def test_gemm_tasks_reject_targets_outside_pattern():
+    sizes = np.array([2, 3, 4], dtype=np.int64)
+    pattern = [np.array([1, 2]), np.array([], dtype=np.int64), np.array([], dtype=np.int64)]   # (2, 1) missing
+    with pytest.raises(ValueError, match="outside the pattern"):
+        planner.gemm_tasks(sizes, pattern, np.zeros(3, np.int64), np.zeros(3, np.int64))
 
 
 def test_flow_list_config4():
