@@ -390,15 +390,14 @@ def _fem_secondary(which: str, reps: int, peak: float) -> dict:
     solution on the host: reduce (incl. H2D) -> assemble -> block LDL^T ->
     block solve -> recover (incl. D2H).  The mesh / element front end is
     excluded (it is not part of the path).  Best of ``reps`` timed runs after
-    one warm-up run (config 5: a single run, first call included).  The
-    pivot-decision margins of every subdomain and diagonal-block
-    factorisation are tracked in the first run (config 5: its only run)."""
+    one warm-up run; the warm-up run tracks the pivot-decision margins of
+    every subdomain and diagonal-block factorisation (the timed runs do not)."""
     import torch
     from paper_2002_05018_b200 import fem3d
     cfg = {"cfg1": fem3d.config1, "cfg2": fem3d.config2, "cfg5": fem3d.config5}[which]()
     model = fem3d.build_model(cfg)
     systems = fem3d.subdomain_systems(model, rhs=None)
-    runs = reps if which == "cfg5" else reps + 1
+    runs = reps + 1
     best, keep, margins = None, None, None
     for i in range(runs):
         for s in systems:
@@ -414,8 +413,8 @@ def _fem_secondary(which: str, reps: int, peak: float) -> dict:
             margins = {"subdomain_decision_margin": min(m[0] for m in sub),
                        "subdomain_argmax_gap": min(m[1] for m in sub),
                        "k_decision_margin": F.stats.decision_margin, "k_argmax_gap": F.stats.argmax_gap,
-                       "tracked_in": "the timed run" if runs == 1 else "the warm-up run"}
-        if (runs == 1 or i > 0) and (best is None or timers["d3m_total"] < best["d3m_total"]):
+                       "tracked_in": "the warm-up run"}
+        if i > 0 and (best is None or timers["d3m_total"] < best["d3m_total"]):
             best = timers
         keep = "solution" if systems[0].factor.released else "factor"
         del F

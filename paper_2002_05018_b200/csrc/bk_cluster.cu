@@ -75,7 +75,8 @@ struct XSlot {
   double v2;     // runner-up of the argmax (margin diagnostic), else -1
   double pad;
 };
-constexpr unsigned kSlotBytes = sizeof(XSlot);
+constexpr unsigned kSlotBytesMin = 32;          // v, own, aux, i (v2 only when margins are tracked)
+__device__ __forceinline__ unsigned slot_bytes(bool track) { return track ? (unsigned)sizeof(XSlot) : kSlotBytesMin; }
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t mapa(uint32_t a, int rank) {
@@ -107,15 +108,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
   }
 }
 
-// one slot to CTA `lane` (lanes < CS of the calling warp; all lanes hold x)
+// one slot to CTA `lane` (lanes < CS of the calling warp; all lanes hold x);
+// the runner-up v2 travels only when margins are tracked (slot_bytes)
 template <int CS>
-__device__ __forceinline__ void xpost(const XSlot* box, int rank, const XSlot& x, uint64_t* bar) {
+__device__ __forceinline__ void xpost(const XSlot* box, int rank, const XSlot& x, uint64_t* bar, bool track) {
   const int lane = threadIdx.x & 31;
   if (lane < CS) {
     const uint32_t dst = mapa(saddr(box + rank), lane), rb = mapa(saddr(bar), lane);
     st_async(dst, x.v, x.own, rb);
     st_async(dst + 16, x.aux, x.i, rb);
-    st_async(dst + 32, x.v2, x.pad, rb);
+    if (track) st_async(dst + 32, x.v2, x.pad, rb);
   }
 }
 
@@ -325,7 +327,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
 #pragma unroll
       for (int c = 0; c < CS; ++c) st_async(mapa(src, c), z.x, z.y, mapa(sb, c));
       const double az = x_abs(z);
-      if (i > 0) top2_merge(v, vi, v2, az, i);
+      if (i > 0) {
+        if (track) top2_merge(v, vi, v2, az, i);
+        else argmax_merge(v, vi, az, i);
+      }
       else own = az;
     }
     const double lv = v;
@@ -333,7 +338,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     warp_argmax(v, vi);
     own = warp_max(own);
     if (track) v2 = warp_runner_up(lv, li, v2, vi);
-    xpost<CS>(inbox[0], rank, xslot(v, own, -1.0, vi, v2), &mbar[0]);
+    xpost<CS>(inbox[0], rank, xslot(v, own, -1.0, vi, v2), &mbar[0], track);
   }
 #ifdef D3M_BK_PROFILE
   const long long t_loop0 = clock64();
@@ -355,7 +360,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     cplx* cB = vec + (int64_t)(3 + (s & 1)) * n;
     cplx* cC = vec + (int64_t)(5 + (s & 1)) * n;
     // ---- 1. column k and the argmax slots have landed; merge ---------------
-    if (tid == 0) mbar_arm(&mbar[bs], (unsigned)(n - k) * 16u + CS * kSlotBytes);
+    if (tid == 0) mbar_arm(&mbar[bs], (unsigned)(n - k) * 16u + CS * slot_bytes(track));
     mbar_wait(&mbar[bs], (unsigned)(s / 3) & 1u);
     BKC_MARK(0, 0);
     BKC_MARK(32, 8);
@@ -384,7 +389,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     } else {
       // ---- 2. push column k+1 and the symmetric column imax; rowmax over
       //         W[imax, k:imax] and W[imax+1:, imax]; |W[imax, imax]| ----------
-      if (tid == 0) mbar_arm(&mbarR, (unsigned)(2 * (n - k) - 1) * 16u + CS * kSlotBytes);
+      if (tid == 0) mbar_arm(&mbarR, (unsigned)(2 * (n - k) - 1) * 16u + CS * slot_bytes(track));
       const uint32_t rb = saddr(&mbarR);
       double rm = 0.0, aim = -1.0;
       if (imax % CS == rank) {
@@ -413,7 +418,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
       }
       rm = bkc_block_max(rm, rv);
       aim = bkc_block_max(aim, rv);
-      if (pw) xpost<CS>(inboxR, rank, xslot(-1.0, aim, rm, 0x7fffffff), &mbarR);
+      if (pw) xpost<CS>(inboxR, rank, xslot(-1.0, aim, rm, 0x7fffffff), &mbarR, track);
       mbar_wait(&mbarR, rphase & 1u);
       ++rphase;
       const XSlot m2 = xmerge<CS>(inboxR, &xmerged);
@@ -509,7 +514,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
           for (int c = 0; c < CS; ++c) st_async(mapa(src, c), w.x, w.y, mapa(nbar, c));
           step_sq = fmax(step_sq, x_abs2(w));
           const double aw = x_abs(w);
-          if (i > k0) top2_merge(v, vi, v2, aw, i);
+          if (i > k0) {
+            if (track) top2_merge(v, vi, v2, aw, i);
+            else argmax_merge(v, vi, aw, i);
+          }
           else own = aw;
         }
         BKC_MARK(0, 5);
@@ -533,7 +541,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
         step_sq = warp_max(step_sq);
       }
       if (lane == 0) rst[s & 1][0] = step_sq;
-      xpost<CS>(inbox[nb], rank, xslot(v, own, up, vi, v2), &mbar[nb]);
+      xpost<CS>(inbox[nb], rank, xslot(v, own, up, vi, v2), &mbar[nb], track);
       BKC_MARK(0, 6);
       if (kstep == 2) ++n2x2;
     } else {
@@ -640,10 +648,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
   if (info >= 0) {
     // stopped at the top of step s: step s-1's maximum is in rst, not pushed
     if (s >= 1) {
-      if (tid == 0) mbar_arm(&mbarR, CS * kSlotBytes);
+      if (tid == 0) mbar_arm(&mbarR, CS * slot_bytes(track));
       if (pw) {
         const double up = warp_max(lane < NW ? rst[(s - 1) & 1][lane] : 0.0);
-        xpost<CS>(inboxR, rank, xslot(-1.0, -1.0, up, 0x7fffffff), &mbarR);
+        xpost<CS>(inboxR, rank, xslot(-1.0, -1.0, up, 0x7fffffff), &mbarR, track);
       }
       mbar_wait(&mbarR, rphase & 1u);
       const XSlot mf = xmerge<CS>(inboxR, &xmerged);
@@ -654,7 +662,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     }
   } else {
     // ran to the end: the last step's push carried step s-2's maximum
-    if (tid == 0) mbar_arm(&mbar[s % 3], (unsigned)(n - k) * 16u + CS * kSlotBytes);
+    if (tid == 0) mbar_arm(&mbar[s % 3], (unsigned)(n - k) * 16u + CS * slot_bytes(track));
     mbar_wait(&mbar[s % 3], (unsigned)(s / 3) & 1u);
     const XSlot mf = xmerge<CS>(inbox[s % 3], &xmerged);
     if (gthread && s >= 2) grow(mf.aux, ks2, k02);
@@ -740,10 +748,13 @@ static int bkc_launch(BkArgs* a, int batch, cudaStream_t s) {
   if (!bkc_fits<CS>(a->n)) return -22;   // the CTA owns its SM
   cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (CS == 16) {
-    // 16 is a non-portable cluster size: check once that a cluster of
-    // full-SM CTAs can be resident on this part
-    static int ok16 = -1;
-    if (ok16 < 0) {
+    // 16 is a non-portable cluster size: check once per device that a
+    // cluster of full-SM CTAs can be resident on this part
+    static PerDeviceOnce checked;
+    static std::atomic<unsigned long long> yes16{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (checked.first()) {
       cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBkcSmemMax);
       cudaLaunchConfig_t cfg = {};
@@ -758,12 +769,12 @@ static int bkc_launch(BkArgs* a, int batch, cudaStream_t s) {
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       int nclusters = 0;
-      ok16 = (cudaOccupancyMaxActiveClusters(&nclusters, bk_cluster_kernel<CS>, &cfg) == cudaSuccess &&
-              nclusters > 0) ? 1 : 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, bk_cluster_kernel<CS>, &cfg) == cudaSuccess && nclusters > 0)
+        yes16.fetch_or(1ull << (dev & 63));
       cudaGetLastError();
       cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
-    if (!ok16) return -22;
+    if (!(yes16.load() & (1ull << (dev & 63)))) return -22;
   }
   bk_cluster_kernel<CS><<<batch * CS, BKC_NT, smem, s>>>(*a);
   return (int)cudaGetLastError();

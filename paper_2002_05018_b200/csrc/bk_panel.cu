@@ -532,8 +532,7 @@ namespace d3m {
 constexpr int kPanelLdwMax = 129;     // workspace row pitch for the widest panel (NB = 128)
 
 // Panel loop for one panel width (NB - 1 or NB columns per panel); the
-// rank-<= NB trailing updates of all matrices run on the small-K kernel
-// (C tile staged with A and B, shared-memory epilogue).
+// rank-<= NB trailing updates of all matrices run as one grouped GEMM launch.
 template <int NB>
 static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* tasks, unsigned long long* tmax,
                      cudaStream_t s, void* stream) {
@@ -544,8 +543,13 @@ static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* task
   int cs = batch * 16 <= 296 ? 16 : batch * 8 <= 296 ? 8 : batch * 4 <= 296 ? 4 : batch * 2 <= 296 ? 2 : 1;
   if (const char* env = getenv("D3M_PANEL_CS")) cs = atoi(env);
   if (cs != 1 && cs != 2 && cs != 4 && cs != 8 && cs != 16) cs = 1;
-  static int ok16 = -1;          // can this device keep a 16-CTA cluster of the panel kernel resident?
-  if (cs == 16 && ok16 < 0) {
+  // can this device keep a 16-CTA cluster of the panel kernel resident?
+  // (per device: bit d of ok16 set = checked, of yes16 = resident)
+  static std::atomic<unsigned long long> ok16{0}, yes16{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long dbit = 1ull << (dev & 63);
+  if (cs == 16 && !(ok16.load() & dbit)) {
     cudaFuncSetAttribute(bk_panel_kernel<NB, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -558,11 +562,12 @@ static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* task
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    ok16 = (cudaOccupancyMaxActiveClusters(&nclusters, bk_panel_kernel<NB, 16>, &cfg) == cudaSuccess &&
-            nclusters > 0) ? 1 : 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, bk_panel_kernel<NB, 16>, &cfg) == cudaSuccess && nclusters > 0)
+      yes16.fetch_or(dbit);
     cudaGetLastError();
+    ok16.fetch_or(dbit);
   }
-  if (cs == 16 && ok16 == 0) cs = 8;
+  if (cs == 16 && !(yes16.load() & dbit)) cs = 8;
   for (int p = 0; p * (NB - 1) < n; ++p) {
     const int mrem = n - (p + 1) * (NB - 1);           // rows left after this panel (upper bound)
     const int tm = mrem > 0 ? (mrem + 63) / 64 : 0;
@@ -576,13 +581,10 @@ static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* task
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
     if (maxtiles > 0) {
-      // rank-<=NB trailing update: the pipelined grouped kernel (C prefetched
-      // into freed ring stages) is ~4% faster than the small-K kernel on
-      // config 3 at NB = 64; D3M_PANEL_GEMM=s selects the small-K kernel
-      static const char* pg = getenv("D3M_PANEL_GEMM");
-      const int rc = (NB >= 64 && !(pg && pg[0] == 's'))
-                         ? d3m_gemm_launch_tm(0, 0, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream)
-                         : d3m_gemm_smallk_launch_k(NB, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream);
+      // rank-<=NB trailing update on the pipelined grouped kernel (C
+      // prefetched into freed ring stages; 4% faster on config 3 than a
+      // small-K kernel that staged C with A and B, since removed)
+      const int rc = d3m_gemm_launch_tm(0, 0, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream);
       if (rc) return rc;
     }
   }
@@ -597,15 +599,12 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
   const int n = a->n;
   // panel width 64: rank-<=64 trailing updates cut the trailing-matrix
   // traffic 4x against NB = 16 (config 5 BK: 20.7 s at NB 16, 15.6 s at 32,
-  // 13.0 s at 64; configs 2/3: -21% / -17%)
+  // 13.0 s at 64; configs 2/3: -21% / -17%; the narrow panels are gone)
   // NB = 128 for large subdomains (n >= 8192, config 5): the rank-128 updates
   // halve the trailing-matrix traffic per flop again, and the longer panel
-  // steps are a small share there
+  // steps are a small share there.  D3M_PANEL_NB=64|128 overrides (tests).
   int nb = n >= 8192 ? 128 : 64;
-  if (const char* env = getenv("D3M_PANEL_NB")) {
-    const int v = atoi(env);
-    nb = v == 128 ? 128 : v == 64 ? 64 : v == 32 ? 32 : 16;
-  }
+  if (const char* env = getenv("D3M_PANEL_NB")) nb = atoi(env) == 128 ? 128 : 64;
   char* w = static_cast<char*>(workspace);
   cplx* Wp = reinterpret_cast<cplx*>(w);
   w += (size_t)batch * n * kPanelLdwMax * sizeof(cplx);
@@ -626,9 +625,7 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
   const int rc = nb == 128 ? panel_run<128>(a, batch, st, Wp, tasks, tmax, s, stream)
-                 : nb == 64 ? panel_run<64>(a, batch, st, Wp, tasks, tmax, s, stream)
-                 : nb == 32 ? panel_run<32>(a, batch, st, Wp, tasks, tmax, s, stream)
-                            : panel_run<16>(a, batch, st, Wp, tasks, tmax, s, stream);
+                            : panel_run<64>(a, batch, st, Wp, tasks, tmax, s, stream);
   if (rc) return rc;
   bk_panel_finalize_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, batch);
   return (int)cudaGetLastError();

@@ -10,6 +10,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -46,14 +49,17 @@ enum { kClsBk = 0, kClsTrsm = 1, kClsGemm = 2, kClsSolve = 3, kClsMisc = 4, kNum
 // supernodes up to this order get the unpermuted L^-1 from the triangular-inverse kernels and the
 // gathered / triangular panel TRSM (factor.py sets kGemmTriGather on exactly these TRSM tasks)
 constexpr int kTrsmTriMax = 512;
+// The counters are process-wide (a measurement facility of bench.py and the
+// tools); the timing records are guarded by g_tmu.
 std::atomic<long long> g_launches{0};
-bool g_timing = false;
+std::atomic<bool> g_timing{false};
+std::mutex g_tmu;
 struct TimedRec { int cls; cudaEvent_t a, b; };
 std::vector<TimedRec> g_pending;
 std::vector<cudaEvent_t> g_free_ev;
 double g_ms[kNumCls] = {0, 0, 0, 0, 0};
 double g_union[kNumCls] = {0, 0, 0, 0, 0};
-long long g_cnt[kNumCls] = {0, 0, 0, 0, 0};
+std::atomic<long long> g_cnt[kNumCls];
 cudaEvent_t g_ref = nullptr;          // common origin for interval unions
 std::vector<double> g_iv;             // (class, start ms, end ms) of the last d3m_counters_read
 
@@ -71,13 +77,19 @@ cudaEvent_t take_event() {
 template <typename Fn>
 int launch(int cls, void* stream, Fn fn) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  g_cnt[cls] += 1;
-  if (!g_timing) return fn();
+  g_cnt[cls].fetch_add(1, std::memory_order_relaxed);
+  if (!g_timing.load(std::memory_order_relaxed)) return fn();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  TimedRec r{cls, take_event(), take_event()};
+  TimedRec r{cls, nullptr, nullptr};
+  {
+    std::lock_guard<std::mutex> g(g_tmu);
+    r.a = take_event();
+    r.b = take_event();
+  }
   cudaEventRecord(r.a, s);
   const int rc = fn();
   cudaEventRecord(r.b, s);
+  std::lock_guard<std::mutex> g(g_tmu);
   g_pending.push_back(r);
   return rc;
 }
@@ -87,6 +99,45 @@ constexpr int kExactBkMax = 128;    // supernodes up to this use the bit-exact B
 constexpr int kPanelBkMin = 512;    // subdomains above this use the batched panel BK + blocked solves
 inline cplx* C(void* p) { return static_cast<cplx*>(p); }
 inline const cplx* CC(const void* p) { return static_cast<const cplx*>(p); }
+
+// Per-device state of the block LDL^T executor: the critical / bulk streams
+// and their events, the D^-1 coefficient buffer, the unpermuted L^-1 of every
+// column and the diagonal-inverse scratch.  One context per device, created
+// on first use on that device; calls on a device serialise on its mutex.
+struct ExecCtx {
+  std::mutex mu;
+  cudaStream_t crit = nullptr, side = nullptr;
+  cudaEvent_t ev_next = nullptr, ev_rest = nullptr, ev_in = nullptr, ev_out = nullptr;
+  void* coef_buf = nullptr;
+  size_t coef_cap = 0;
+  cplx* linv = nullptr;
+  int64_t linv_cap = 0;
+  cplx* dinv = nullptr;               // 256 x 16 complex: tri_inv_diag16 output
+};
+
+ExecCtx* exec_ctx() {
+  static std::mutex m;
+  static std::map<int, std::unique_ptr<ExecCtx>> ctxs;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> g(m);
+  std::unique_ptr<ExecCtx>& p = ctxs[dev];
+  if (!p) {
+    auto c = std::make_unique<ExecCtx>();
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&c->crit, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_next, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_rest, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMalloc(&c->dinv, sizeof(cplx) * 256 * 16) != cudaSuccess)
+      return nullptr;
+    p = std::move(c);
+  }
+  return p.get();
+}
 
 }  // namespace
 
@@ -445,160 +496,162 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
     const char* e = getenv("D3M_BKC4_TILES");
     return e ? (int64_t)atoll(e) : (int64_t)5000;
   }();
+  static const bool trsm_tri = [] { const char* e = getenv("D3M_TRSM_TRI"); return !(e && e[0] == '0'); }();
+  // default: the bulk update starts once the next-column update has finished,
+  // which then has the SMs to itself (D3M_REST_AFTER_NEXT=0: it starts beside it)
+  static const int rest_after_next = [] { const char* e = getenv("D3M_REST_AFTER_NEXT"); return e ? atoi(e) : 1; }();
+  // every column's X panel must fit its half of xbuf: checked before anything is launched
+  for (int j = 0; j < nb; ++j)
+    if (h_panel_rows[j] * h_sizes[j] > (lookahead ? xbuf_elems / 2 : xbuf_elems))
+      return fail(-22, "d3m_block_ldlt_exec: xbuf too small");
+  ExecCtx* ctx = exec_ctx();
+  if (!ctx) return fail(-12, "d3m_block_ldlt_exec: stream/event/scratch creation");
+  // calls on one device share its streams and buffers: they enqueue one at a
+  // time (stream order then keeps their kernels apart)
+  std::lock_guard<std::mutex> guard(ctx->mu);
+  int64_t nmax = 0;
+  for (int j = 0; j < nb; ++j) nmax = std::max<int64_t>(nmax, h_sizes[j]);
+  // D^-1 coefficients of the current column (3 complex per pivot column);
+  // double-buffered with the column parity like xbuf
+  const size_t coef_bytes = (size_t)2 * 3 * std::max<int64_t>(nmax, 1) * sizeof(cplx);
+  if (coef_bytes > ctx->coef_cap) {
+    if (ctx->coef_buf) cudaFree(ctx->coef_buf);      // synchronising: no earlier call still reads it
+    ctx->coef_buf = nullptr;
+    ctx->coef_cap = 0;
+    if (cudaMalloc(&ctx->coef_buf, coef_bytes) != cudaSuccess) return fail(-12, "d3m_block_ldlt_exec: coef alloc");
+    ctx->coef_cap = coef_bytes;
+  }
+  // unpermuted L_jj^-1 of every column (same layout as binv), for the triangular panel TRSM
+  cplx* linv_use = nullptr;
+  if (trsm_tri) {
+    const int64_t need = h_binv_off[nb];
+    if (need > ctx->linv_cap) {
+      if (ctx->linv) cudaFree(ctx->linv);
+      ctx->linv = nullptr;
+      ctx->linv_cap = 0;
+      if (cudaMalloc(&ctx->linv, sizeof(cplx) * (size_t)std::max<int64_t>(need, 1)) != cudaSuccess)
+        return fail(-12, "d3m_block_ldlt_exec: linv alloc");
+      ctx->linv_cap = need;
+    }
+    linv_use = ctx->linv;
+  }
   // Streams: the caller's stream hands over to a high-priority critical
   // stream (BK -> L^-1 -> panel GEMM -> D^-1 -> next-column update) and a
   // low-priority bulk stream (the rest of each column's trailing update).
-  static cudaStream_t crit = nullptr, side = nullptr;
-  static cudaEvent_t ev_next = nullptr, ev_rest = nullptr, ev_in = nullptr, ev_out = nullptr;
-  if (!crit) {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if (cudaStreamCreateWithPriority(&crit, cudaStreamNonBlocking, hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev_next, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming) != cudaSuccess)
-      return fail(-12, "d3m_block_ldlt_exec: stream/event creation");
-  }
   cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
+  cudaStream_t crit = ctx->crit, side = ctx->side;
   cudaStream_t s0 = lookahead ? crit : user;
   if (lookahead) {
-    cudaEventRecord(ev_in, user);
-    cudaStreamWaitEvent(crit, ev_in, 0);
+    cudaEventRecord(ctx->ev_in, user);
+    cudaStreamWaitEvent(crit, ctx->ev_in, 0);
+    cudaStreamWaitEvent(side, ctx->ev_in, 0);
   }
   auto* tasks = static_cast<const d3m::GemmTask*>(d_tasks);
   auto* ttasks = static_cast<const d3m::GemmTask*>(d_trsm_tasks);
   cplx* pool = C(d_pool);
   cplx* binv = C(d_binv);
-  // D^-1 coefficients of the current column (3 complex per pivot column);
-  // double-buffered with the column parity like xbuf
-  static void* coef_buf = nullptr;
-  static size_t coef_cap = 0;
-  int64_t nmax = 0;
-  for (int j = 0; j < nb; ++j) nmax = std::max<int64_t>(nmax, h_sizes[j]);
-  const size_t coef_bytes = (size_t)2 * 3 * std::max<int64_t>(nmax, 1) * sizeof(cplx);
-  if (coef_bytes > coef_cap) {
-    if (coef_buf) cudaFree(coef_buf);
-    if (cudaMalloc(&coef_buf, coef_bytes) != cudaSuccess) return fail(-12, "d3m_block_ldlt_exec: coef alloc");
-    coef_cap = coef_bytes;
-  }
-  // unpermuted L_jj^-1 of every column (same layout as binv), for the triangular panel TRSM
-  static cplx* linv = nullptr;
-  static int64_t linv_cap = 0;
-  static const bool trsm_tri = [] { const char* e = getenv("D3M_TRSM_TRI"); return !(e && e[0] == '0'); }();
-  cplx* linv_use = nullptr;
-  if (trsm_tri) {
-    const int64_t need = h_binv_off[nb];
-    if (need > linv_cap) {
-      if (linv) cudaFree(linv);
-      linv = nullptr;
-      linv_cap = 0;
-      if (cudaMalloc(&linv, sizeof(cplx) * (size_t)std::max<int64_t>(need, 1)) != cudaSuccess)
-        return fail(-12, "d3m_block_ldlt_exec: linv alloc");
-      linv_cap = need;
-    }
-    linv_use = linv;
-  }
-  bool rest_pending = false;
-  for (int j = 0; j < nb; ++j) {
-    // blocks of K still being uploaded: column j waits for the chunks it is
-    // the first to touch (the side stream follows s0 through ev_next)
-    for (int w = 0; w < nwait; ++w)
-      if (h_wait_col[w] == j) cudaStreamWaitEvent(s0, static_cast<cudaEvent_t>(h_wait_ev[w]), 0);
-    const int nj = (int)h_sizes[j];
-    const int64_t R = h_panel_rows[j];
-    cplx* xbuf = C(d_xbuf) + (lookahead ? (j & 1) * (xbuf_elems / 2) : 0);
-    if (R * nj > (lookahead ? xbuf_elems / 2 : xbuf_elems)) return fail(-22, "d3m_block_ldlt_exec: xbuf too small");
-    int64_t* perm = static_cast<int64_t*>(d_perm) + h_piv_off[j];
-    int8_t* tags = static_cast<int8_t*>(d_tags) + h_piv_off[j];
-    cplx* diag = pool + h_diag_off[j];
-    cplx* coef = static_cast<cplx*>(coef_buf) + (size_t)(j & 1) * 3 * nmax;
-    d3m::BkArgs a{diag, 0, nj, nj, pivot_tol, check_sym, perm, tags,
-                  static_cast<int32_t*>(d_n2x2) + j, static_cast<double*>(d_growth) + j,
-                  static_cast<int32_t*>(d_info) + j, static_cast<double*>(d_scale) + j,
-                  static_cast<double*>(d_asym) + j, C(d_bk_scratch)};
-    if (d_check_sym) a.check_sym_dev = static_cast<const int*>(d_check_sym) + j;   // per-block flag (ABI v8)
-    if (d_margin) a.margin = static_cast<double*>(d_margin) + 2 * j;               // decision margins (ABI v9)
-    if (nj > 0) {
-      // supernodes up to kExactBkMax use the bit-exact unblocked kernel (so a
-      // one-block K factors exactly like dense_ldlt_bk, test_block_factor.py:
-      // 24-32); wider ones the bit-exact cluster kernel (lower triangle in the
-      // cluster's shared memory, 8- or 16-CTA clusters), else the exact one
-      D3M_TRY(launch(kClsBk, s0, [&] {
-        if (nj <= kExactBkMax) return d3m_bk_launch(&a, 1, s0);
-        // 4-CTA clusters while the column's bulk update is long enough to hide the slower BK
-        // (frees 4 SMs for the update GEMMs), 8-CTA clusters on the exposed chain at the ends;
-        // a block too wide for the requested size moves to a larger cluster
-        const int cs = (lookahead && h_tiles_rest[j] >= bkc4_tiles) ? 4 : 0;
-        const int rc = d3m_bk_cluster_launch_cs(&a, 1, cs, s0);
-        return rc == -22 ? d3m_bk_launch(&a, 1, s0) : rc;
-      }));
-      // Binv_j = L_jj^-1 P_j (also used by block_solve) + D_jj^-1 coefficients
-      D3M_TRY(launch(kClsTrsm, s0, [&] {
-        // blocked 16 x 16 inverse (n <= 256), else warp per column (n <= 512), else the generic kernel;
-        // D3M_TRI_INV=w forces the warp kernel (A/B measurements)
-        static const char* ti_env = getenv("D3M_TRI_INV");
-        int rc = -22;
-        cplx* lj = linv_use ? linv_use + h_binv_off[j] : nullptr;   // unpermuted L^-1 for the panel TRSM
-        if (!(ti_env && ti_env[0] == 'w')) rc = d3m_tri_inv_blocked_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, lj, s0);
-        if (rc == -22) rc = d3m_tri_inv_warp_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, s0, lj);
-        return rc == -22 ? d3m_tri_inv_launch(diag, 0, perm, 0, tags, 0, binv + h_binv_off[j], 0, nj, 1, s0) : rc;
-      }));
-    }
-    if (R > 0) {
-      // X_ij = K_ij P^T L_jj^-T = panel * Binv^T on DMMA, then L_ij = X_ij D_jj^-1
-      D3M_TRY(launch(kClsTrsm, s0, [&] {
-        // nj <= kTrsmTriMax: X = (K P^T) L^-T with the column gather and the triangular K cut
-        // (the task carries kGemmTriGather, factor.py); else X = K Binv^T
-        if (linv_use && nj <= kTrsmTriMax)
-          return d3m_gemm_launch_perm(pool, linv_use, xbuf, ttasks + j, 1, (int)h_tiles_trsm[j], d_perm, s0);
-        return d3m_gemm_launch(0, 0, pool, binv, xbuf, ttasks + j, 1, (int)h_tiles_trsm[j], s0);
-      }));
-      D3M_TRY(launch(kClsTrsm, s0, [&] {
-        return nj <= 512 ? d3m_dinv_rows_coef_launch(xbuf, pool + h_panel_off[j], R, nj, tags, coef, s0)
-                         : d3m_dinv_rows_launch(xbuf, pool + h_panel_off[j], R, nj, diag, tags, s0);
-      }));
-    }
-    const int64_t t0 = h_task_ptr[j], tn = h_task_next[j], t1 = h_task_ptr[j + 1];
-    // X_j / L_j are ready: the bulk ("rest") update of column j only reads
-    // them and targets columns >= j+2, so it could start now, beside the
-    // "next" update below (disjoint targets); by default it waits for the next
-    // update (below).  The side stream keeps the rest updates of consecutive
-    // columns in order.
-    static const int rest_after_next = [] { const char* e = getenv("D3M_REST_AFTER_NEXT"); return e ? atoi(e) : 1; }();
-    if (lookahead && t1 > tn && !rest_after_next) cudaEventRecord(ev_next, s0);
-    if (rest_pending) {          // next-targets of column j+1 were also rest-targets of j-1
-      cudaStreamWaitEvent(s0, ev_rest, 0);
-      rest_pending = false;
-    }
-    if (tn > t0)
-      D3M_TRY(launch(kClsGemm, s0, [&] {
-        return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + t0, (int)(tn - t0), (int)h_tiles_next[j], s0);
-      }));
-    // default: the bulk update starts once the next-column update has finished,
-    // which then has the SMs to itself (D3M_REST_AFTER_NEXT=0: it starts beside it)
-    if (lookahead && t1 > tn && rest_after_next) cudaEventRecord(ev_next, s0);
-    if (t1 > tn) {
-      if (lookahead) {
-        cudaStreamWaitEvent(side, ev_next, 0);
-        D3M_TRY(launch(kClsGemm, side, [&] {
-          return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], side);
+  // all columns; an early return (a failed launch) still reaches the join below
+  auto columns = [&]() -> int {
+    bool rest_pending = false;
+    for (int j = 0; j < nb; ++j) {
+      // blocks of K still being uploaded: column j waits for the chunks it is
+      // the first to touch (the side stream follows s0 through ev_next)
+      for (int w = 0; w < nwait; ++w)
+        if (h_wait_col[w] == j) cudaStreamWaitEvent(s0, static_cast<cudaEvent_t>(h_wait_ev[w]), 0);
+      const int nj = (int)h_sizes[j];
+      const int64_t R = h_panel_rows[j];
+      cplx* xbuf = C(d_xbuf) + (lookahead ? (j & 1) * (xbuf_elems / 2) : 0);
+      int64_t* perm = static_cast<int64_t*>(d_perm) + h_piv_off[j];
+      int8_t* tags = static_cast<int8_t*>(d_tags) + h_piv_off[j];
+      cplx* diag = pool + h_diag_off[j];
+      cplx* coef = static_cast<cplx*>(ctx->coef_buf) + (size_t)(j & 1) * 3 * nmax;
+      d3m::BkArgs a{diag, 0, nj, nj, pivot_tol, check_sym, perm, tags,
+                    static_cast<int32_t*>(d_n2x2) + j, static_cast<double*>(d_growth) + j,
+                    static_cast<int32_t*>(d_info) + j, static_cast<double*>(d_scale) + j,
+                    static_cast<double*>(d_asym) + j, C(d_bk_scratch)};
+      if (d_check_sym) a.check_sym_dev = static_cast<const int*>(d_check_sym) + j;   // per-block flag (ABI v8)
+      if (d_margin) a.margin = static_cast<double*>(d_margin) + 2 * j;               // decision margins (ABI v9)
+      if (nj > 0) {
+        // supernodes up to kExactBkMax use the bit-exact unblocked kernel (so a
+        // one-block K factors exactly like dense_ldlt_bk, test_block_factor.py:
+        // 24-32); wider ones the bit-exact cluster kernel (lower triangle in the
+        // cluster's shared memory, 8- or 16-CTA clusters), else the exact one
+        D3M_TRY(launch(kClsBk, s0, [&] {
+          if (nj <= kExactBkMax) return d3m_bk_launch(&a, 1, s0);
+          // 4-CTA clusters while the column's bulk update is long enough to hide the slower BK
+          // (frees 4 SMs for the update GEMMs), 8-CTA clusters on the exposed chain at the ends;
+          // a block too wide for the requested size moves to a larger cluster
+          const int cs = (lookahead && h_tiles_rest[j] >= bkc4_tiles) ? 4 : 0;
+          const int rc = d3m_bk_cluster_launch_cs(&a, 1, cs, s0);
+          return rc == -22 ? d3m_bk_launch(&a, 1, s0) : rc;
         }));
-        cudaEventRecord(ev_rest, side);
-        rest_pending = true;
-      } else {
-        D3M_TRY(launch(kClsGemm, s0, [&] {
-          return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], s0);
+        // Binv_j = L_jj^-1 P_j (also used by block_solve) + D_jj^-1 coefficients
+        D3M_TRY(launch(kClsTrsm, s0, [&] {
+          // blocked 16 x 16 inverse (n <= 256), else warp per column (n <= 512), else the generic kernel
+          cplx* lj = linv_use ? linv_use + h_binv_off[j] : nullptr;   // unpermuted L^-1 for the panel TRSM
+          int rc = d3m_tri_inv_blocked_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, lj, ctx->dinv, s0);
+          if (rc == -22) rc = d3m_tri_inv_warp_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, s0, lj);
+          return rc == -22 ? d3m_tri_inv_launch(diag, 0, perm, 0, tags, 0, binv + h_binv_off[j], 0, nj, 1, s0) : rc;
         }));
       }
+      if (R > 0) {
+        // X_ij = K_ij P^T L_jj^-T = panel * Binv^T on DMMA, then L_ij = X_ij D_jj^-1
+        D3M_TRY(launch(kClsTrsm, s0, [&] {
+          // nj <= kTrsmTriMax: X = (K P^T) L^-T with the column gather and the triangular K cut
+          // (the task carries kGemmTriGather, factor.py); else X = K Binv^T
+          if (linv_use && nj <= kTrsmTriMax)
+            return d3m_gemm_launch_perm(pool, linv_use, xbuf, ttasks + j, 1, (int)h_tiles_trsm[j], d_perm, s0);
+          return d3m_gemm_launch(0, 0, pool, binv, xbuf, ttasks + j, 1, (int)h_tiles_trsm[j], s0);
+        }));
+        D3M_TRY(launch(kClsTrsm, s0, [&] {
+          return nj <= 512 ? d3m_dinv_rows_coef_launch(xbuf, pool + h_panel_off[j], R, nj, tags, coef, s0)
+                           : d3m_dinv_rows_launch(xbuf, pool + h_panel_off[j], R, nj, diag, tags, s0);
+        }));
+      }
+      const int64_t t0 = h_task_ptr[j], tn = h_task_next[j], t1 = h_task_ptr[j + 1];
+      // X_j / L_j are ready: the bulk ("rest") update of column j only reads
+      // them and targets columns >= j+2, so it could start now, beside the
+      // "next" update below (disjoint targets); by default it waits for the
+      // next update.  The side stream keeps the rest updates of consecutive
+      // columns in order.
+      if (lookahead && t1 > tn && !rest_after_next) cudaEventRecord(ctx->ev_next, s0);
+      if (rest_pending) {          // next-targets of column j+1 were also rest-targets of j-1
+        cudaStreamWaitEvent(s0, ctx->ev_rest, 0);
+        rest_pending = false;
+      }
+      if (tn > t0)
+        D3M_TRY(launch(kClsGemm, s0, [&] {
+          return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + t0, (int)(tn - t0), (int)h_tiles_next[j], s0);
+        }));
+      if (lookahead && t1 > tn && rest_after_next) cudaEventRecord(ctx->ev_next, s0);
+      if (t1 > tn) {
+        if (lookahead) {
+          cudaStreamWaitEvent(side, ctx->ev_next, 0);
+          D3M_TRY(launch(kClsGemm, side, [&] {
+            return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], side);
+          }));
+          cudaEventRecord(ctx->ev_rest, side);
+          rest_pending = true;
+        } else {
+          D3M_TRY(launch(kClsGemm, s0, [&] {
+            return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], s0);
+          }));
+        }
+      }
     }
-  }
-  if (rest_pending) cudaStreamWaitEvent(s0, ev_rest, 0);
+    return 0;
+  };
+  const int rc = columns();
+  // join, on success and on failure alike: the caller's stream waits for
+  // everything enqueued on the critical and bulk streams, so buffers it frees
+  // after a raised error are not still in use
   if (lookahead) {
-    cudaEventRecord(ev_out, s0);
-    cudaStreamWaitEvent(user, ev_out, 0);
+    cudaEventRecord(ctx->ev_rest, side);
+    cudaStreamWaitEvent(crit, ctx->ev_rest, 0);
+    cudaEventRecord(ctx->ev_out, crit);
+    cudaStreamWaitEvent(user, ctx->ev_out, 0);
   }
+  if (rc != 0) return rc;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail((int)e, "d3m_block_ldlt_exec: launch");
   return 0;
@@ -772,8 +825,9 @@ int d3m_recover_batched(int batch, int n, int m, const void* F, const void* perm
 }
 
 void d3m_set_timing(int on) {
+  std::lock_guard<std::mutex> g(g_tmu);
   g_timing = on != 0;
-  if (g_timing) {
+  if (on) {
     if (!g_ref) cudaEventCreate(&g_ref);
     cudaDeviceSynchronize();
     cudaEventRecord(g_ref, 0);
@@ -781,6 +835,7 @@ void d3m_set_timing(int on) {
 }
 
 void d3m_counters_reset(void) {
+  std::lock_guard<std::mutex> g(g_tmu);
   for (auto& r : g_pending) {
     cudaEventSynchronize(r.b);
     g_free_ev.push_back(r.a);
@@ -794,6 +849,7 @@ void d3m_counters_reset(void) {
 // launches: total kernel launches since reset; ms[5] / n[5]: summed event
 // time and launch count per class (bk, trsm, gemm-update, solve, misc).
 int d3m_counters_read(int64_t* launches, double* ms, int64_t* n) {
+  std::lock_guard<std::mutex> g(g_tmu);
   std::vector<std::pair<double, double>> iv[kNumCls];
   g_iv.clear();
   for (auto& r : g_pending) {
@@ -836,6 +892,7 @@ int d3m_counters_read(int64_t* launches, double* ms, int64_t* n) {
 // Diagnostics: the timed launch intervals collected by the last
 // d3m_counters_read, as (class, start_ms, end_ms) triplets; returns the count.
 int64_t d3m_timing_intervals(double* out, int64_t max_triplets) {
+  std::lock_guard<std::mutex> g(g_tmu);
   const int64_t n = (int64_t)g_iv.size() / 3;
   if (out) std::memcpy(out, g_iv.data(), sizeof(double) * 3 * (size_t)std::min(n, max_triplets));
   return n;

@@ -14,10 +14,24 @@
 //  * plain operators for the tensor-core / FMA paths (GEMM, TRSM, solves),
 //    whose parity with the reference is to tolerance.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace d3m {
+
+// Host: true the first time first() is called for the current device (one
+// instance per call site, e.g. a kernel's shared-memory attribute, which is
+// per device); thread-safe.
+struct PerDeviceOnce {
+  std::atomic<unsigned long long> done{0};
+  bool first() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    return !(done.fetch_or(bit) & bit);
+  }
+};
 
 using cplx = double2;
 

@@ -89,7 +89,7 @@ int d3m_sym_flags_launch(const void* pool, const void* off, const void* n, const
                          void* stream);
 int d3m_nonzero_rows_launch(int B, int n, int m, const void* D, void* flag, void* idx, void* count, void* stream);
 int d3m_tri_inv_blocked_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef, int n,
-                               void* Linv, void* stream);
+                               void* Linv, void* dinv, void* stream);
 int d3m_gemm_launch_perm(const void* A, const void* B, void* C, const void* dtasks, int ntasks, int ntiles,
                          const void* gperm, void* stream);
 int d3m_tri_inv_warp_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef, int n,
@@ -107,7 +107,3 @@ size_t d3m_bk_panel_workspace_bytes(int n, int batch);
 extern "C" int d3m_gemm_prepare_tasks(d3m::GemmTask* tasks, int ntasks);
 extern "C" int d3m_gemm_launch_tm(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
                                   int ntasks, int ntiles, void* tmax, void* stream);
-extern "C" int d3m_gemm_smallk_launch_k(int kt, const void* A, const void* B, void* C, const void* dtasks, int ntasks,
-                                        int ntiles, void* tmax, void* stream);
-extern "C" int d3m_gemm_smallk_launch_tm(const void* A, const void* B, void* C, const void* dtasks, int ntasks,
-                                         int ntiles, void* tmax, void* stream);

@@ -447,9 +447,10 @@ namespace d3m {
 // each (~150 us at n = 256); here the chain is n/16 block steps:
 //   tri_inv_diag16:  Dinv_i = L_ii^-1 of every 16 x 16 diagonal block (+ the
 //                    D^-1 coefficients, as the warp kernel)
-//   tri_inv_cols16:  CTA k owns block column k of X = L^-1:
-//                    X_kk = Dinv_k;  X_ik = -Dinv_i (sum_{k<=m<i} L_im X_mk),
-//                    the L rows of the next step prefetched by cp.async.
+//   tri_inv_colq:    one CTA per column q of X = L^-1:
+//                    X_kk = Dinv_k;  X_ik = -Dinv_i (sum_{k<=m<i} L_im X_mk)
+//                    (a per-block-column CTA version, 2x slower on the
+//                    critical chain, was removed)
 // L(i, j) is the packed factor's strict lower part with the sub-diagonal of
 // every 2 x 2 pivot read as zero (kernels.py:123-125 stores e there).
 // -------------------------------------------------------------------------
@@ -503,89 +504,6 @@ __global__ void __launch_bounds__(64) tri_inv_diag16(const cplx* __restrict__ F,
 }
 
 constexpr int TI_NMAX = 256;
-constexpr size_t kTiSmem = sizeof(cplx) * ((size_t)TI_NMAX * TI_B + 2 * (size_t)TI_B * TI_NMAX + TI_B * TI_B +
-                                          2 * TI_B * TI_B);
-
-__device__ __forceinline__ void ti_cp16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-
-__global__ void __launch_bounds__(256) tri_inv_cols16(const cplx* __restrict__ F, const int64_t* __restrict__ perm,
-                                                      const int8_t* __restrict__ tags, const cplx* __restrict__ Dinv,
-                                                      cplx* Binv, cplx* Linv, int n) {
-  extern __shared__ __align__(16) unsigned char ti_smem[];
-  cplx* X = reinterpret_cast<cplx*>(ti_smem);                 // rows 16k.. of block column k, 16 wide
-  cplx* Lb = X + (size_t)TI_NMAX * TI_B;                      // 2 x [16][16(i-k)] L row panels
-  cplx* S = Lb + 2 * (size_t)TI_B * TI_NMAX;                  // 16 x 16
-  cplx* Ds = S + TI_B * TI_B;                                 // 2 x Dinv_i (16 x 16), with the L rows
-  const int k = blockIdx.x, nbk = (n + TI_B - 1) / TI_B, c0 = k * TI_B;
-  const int tid = threadIdx.x, r = tid >> 4, cc = tid & 15;
-  auto fetch = [&](int i, int buf) {      // L rows [16i, 16i+16) x cols [c0, 16i) -> Lb[buf]
-    const int w = TI_B * (i - k), rows = min(TI_B, n - i * TI_B);
-    cplx* dst = Lb + (size_t)buf * TI_B * TI_NMAX;
-    for (int e = tid; e < rows * w; e += 256) {
-      const int rr = e / w, m = e - rr * w;
-      ti_cp16(dst + rr * w + m, F + (int64_t)(i * TI_B + rr) * n + c0 + m);
-    }
-    ti_cp16(Ds + buf * TI_B * TI_B + tid, Dinv + (int64_t)i * TI_B * TI_B + tid);     // 256 entries
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
-  if (k + 1 < nbk) fetch(k + 1, 0);
-  X[r * TI_B + cc] = (c0 + r < n && c0 + cc < n) ? Dinv[((int64_t)k * TI_B + r) * TI_B + cc] : mk(0.0, 0.0);
-  for (int i = k + 1; i < nbk; ++i) {
-    const int buf = (i - k - 1) & 1, w = TI_B * (i - k), rows = min(TI_B, n - i * TI_B);
-    if (i + 1 < nbk) {
-      fetch(i + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;\n" ::);
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-    }
-    __syncthreads();
-    const cplx* Lr = Lb + (size_t)buf * TI_B * TI_NMAX;
-    // S = L_i,[k,i) X_[k,i),k: 16 columns per iteration, loads first, four
-    // partial sums (w is a multiple of 16)
-    cplx a[4] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
-    if (r < rows) {
-      const bool zr = r == 0 && tags[i * TI_B - 1] == 2;     // L[16i, 16i-1] of a 2x2 pivot
-      for (int m0 = 0; m0 < w; m0 += 16) {
-        cplx l[16], x[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          l[q] = Lr[r * w + m0 + q];
-          x[q] = X[(m0 + q) * TI_B + cc];
-        }
-        if (zr && m0 + 16 == w) l[15] = mk(0.0, 0.0);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          cplx& t = a[q & 3];
-          t = mk(t.x + (l[q].x * x[q].x - l[q].y * x[q].y), t.y + (l[q].x * x[q].y + l[q].y * x[q].x));
-        }
-      }
-    }
-    S[r * TI_B + cc] = c_add(c_add(a[0], a[1]), c_add(a[2], a[3]));
-    __syncthreads();
-    // X_ik = -Dinv_i S
-    cplx acc = mk(0.0, 0.0);
-    const cplx* Di = Ds + buf * TI_B * TI_B;
-#pragma unroll
-    for (int c = 0; c < TI_B; ++c) {
-      const cplx d = Di[r * TI_B + c], sv = S[c * TI_B + cc];
-      acc = mk(acc.x + (d.x * sv.x - d.y * sv.y), acc.y + (d.x * sv.y + d.y * sv.x));
-    }
-    X[(w + r) * TI_B + cc] = (r < rows) ? mk(-acc.x, -acc.y) : mk(0.0, 0.0);
-    __syncthreads();
-  }
-  // Binv[:, perm[q]] = X[:, q] (zeros above the block column); Linv[:, q] = X[:, q]
-  for (int e = tid; e < n * TI_B; e += 256) {
-    const int row = e / TI_B, q = c0 + (e % TI_B);
-    if (q >= n) continue;
-    const cplx v = (row < c0) ? mk(0.0, 0.0) : X[(row - c0) * TI_B + (q - c0)];
-    Binv[(int64_t)row * n + perm[q]] = v;
-    if (Linv) Linv[(int64_t)row * n + q] = v;
-  }
-}
-
 // One CTA per column q of X = L^-1 (n CTAs): the column's 16-row blocks
 // below the diagonal block are the dependent chain (at most 15 steps at
 // n = 256), each step a 16-row dot over the rows already solved (16 lanes per
@@ -655,33 +573,22 @@ __global__ void __launch_bounds__(256) tri_inv_colq(const cplx* __restrict__ F, 
 
 }  // namespace d3m
 
-// blocked L^-1 P + D^-1 coefficients for n <= 256 (-22 above)
+// blocked L^-1 P + D^-1 coefficients for n <= 256 (-22 above); dinv: scratch
+// of 256 x 16 complex (the 16 x 16 diagonal-block inverses), owned by the
+// caller's per-device context
 extern "C" int d3m_tri_inv_blocked_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef,
-                                          int n, void* Linv, void* stream) {
+                                          int n, void* Linv, void* dinv, void* stream) {
   using namespace d3m;
   if (n <= 0) return 0;
-  if (n > TI_NMAX) return -22;
-  static cplx* dinv = nullptr;
-  static bool cfg = false;
-  if (!dinv) {
-    if (cudaMalloc(&dinv, sizeof(cplx) * TI_NMAX * TI_B) != cudaSuccess) return 2;
-  }
-  if (!cfg) {
-    cudaFuncSetAttribute(tri_inv_cols16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTiSmem);
-    cfg = true;
-  }
+  if (n > TI_NMAX || dinv == nullptr) return -22;
   auto s = reinterpret_cast<cudaStream_t>(stream);
   const int nbk = (n + TI_B - 1) / TI_B;
   auto Fp = static_cast<const cplx*>(F);
   auto tp = static_cast<const int8_t*>(tags);
-  tri_inv_diag16<<<nbk, 64, 0, s>>>(Fp, tp, dinv, static_cast<cplx*>(coef), n);
-  static const int colq = [] { const char* e = getenv("D3M_TRI_COLQ"); return e ? atoi(e) : 1; }();
-  if (colq)
-    tri_inv_colq<<<n, 256, 0, s>>>(Fp, static_cast<const int64_t*>(perm), tp, dinv, static_cast<cplx*>(Binv),
-                                   static_cast<cplx*>(Linv), n);
-  else
-    tri_inv_cols16<<<nbk, 256, kTiSmem, s>>>(Fp, static_cast<const int64_t*>(perm), tp, dinv,
-                                             static_cast<cplx*>(Binv), static_cast<cplx*>(Linv), n);
+  auto Dp = static_cast<cplx*>(dinv);
+  tri_inv_diag16<<<nbk, 64, 0, s>>>(Fp, tp, Dp, static_cast<cplx*>(coef), n);
+  tri_inv_colq<<<n, 256, 0, s>>>(Fp, static_cast<const int64_t*>(perm), tp, Dp, static_cast<cplx*>(Binv),
+                                 static_cast<cplx*>(Linv), n);
   return (int)cudaGetLastError();
 }
 

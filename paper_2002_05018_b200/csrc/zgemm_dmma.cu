@@ -429,191 +429,39 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
   }
 }
 
-// ---- small-K variant (K <= 16 or 32): the rank-<=NB trailing updates of the
-// batched panel BK (bk_panel.cu; NB = 32 by default: 140 KB, one CTA per SM).  At K = 16 a 64x64 tile does 0.5 MFLOP
-// against 128 KB of C traffic (4 flop/B), so the tile is HBM/latency bound:
-// the C tile is fetched by cp.async into shared memory together with A and B
-// (all 96 KB of the tile's traffic in flight at once), updated there by the
-// DMMA fragments and written back with coalesced 16-byte stores.
-constexpr int SK_PC = BN + 1;
-template <int KT>
-constexpr size_t sk_smem() { return sizeof(cplx) * ((BM + BN) * (KT + 4) + BM * SK_PC); }
-
-constexpr int SK_NT = 256;      // 8 warps: 2 x 4 warp grid of 32 x 16 tiles
-
-template <int KT>
-__global__ void __launch_bounds__(SK_NT, KT <= 16 ? 2 : 1)
-zgemm_smallk_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bbase, cplx* Cbase,
-                    const GemmTask* __restrict__ tasks, int ntasks, unsigned long long* tmax) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  constexpr int SK_K = KT, SK_PA = KT + 4;
-  cplx(*As)[SK_PA] = reinterpret_cast<cplx(*)[SK_PA]>(smem_raw);
-  cplx(*Bs)[SK_PA] = reinterpret_cast<cplx(*)[SK_PA]>(smem_raw + sizeof(cplx) * BM * SK_PA);
-  cplx(*Cs)[SK_PC] = reinterpret_cast<cplx(*)[SK_PC]>(smem_raw + sizeof(cplx) * (BM + BN) * SK_PA);
-  const int tile = blockIdx.x;
-  const GemmTask tk = tasks[find_task(tasks, ntasks, tile)];
-  int local = tile - tk.tile_start, tm, tn;
-  const bool sym = (tk.flags & kGemmSym) != 0;
-  if (sym) {
-    tm = (int)((sqrt(8.0 * local + 1.0) - 1.0) * 0.5);
-    while ((tm + 1) * (tm + 2) / 2 <= local) ++tm;
-    while (tm * (tm + 1) / 2 > local) --tm;
-    tn = local - tm * (tm + 1) / 2;
-  } else {
-    tm = local / tk.tiles_n;
-    tn = local - tm * tk.tiles_n;
-  }
-  const cplx* A = Abase + tk.a_off;
-  const cplx* B = Bbase + tk.b_off;
-  cplx* C = Cbase + tk.c_off;
-  const int M = tk.m, N = tk.n, K = tk.k, ldc = tk.ldc;
-  const int m0 = tm * BM, n0 = tn * BN;
-  if (m0 >= M || n0 >= N) return;
-  const int mode = tk.flags & kGemmModeMask;
-  const int t = threadIdx.x;
-  // ---- staging: A and B in k-chunks of 16 (one cp.async group each), then the
-  // C tile; the DMMAs of chunk c start as soon as chunk c has landed, while
-  // the later chunks and C are still in flight
-  constexpr int NCH = SK_K / 16;
-#pragma unroll
-  for (int ch = 0; ch < NCH; ++ch) {
-#pragma unroll
-    for (int p = 0; p < 2 * BM * 16 / SK_NT; ++p) {       // A then B: 64 rows x 16 k each
-      const int e = p * SK_NT + t, r = (e >> 4) & 63, k = ch * 16 + (e & 15);
-      const bool isb = e >= BM * 16;
-      const int rows = isb ? N : M, r0 = isb ? n0 : m0;
-      const bool ok = (r0 + r < rows) && (k < K);
-      const cplx* g = isb ? B + (int64_t)(n0 + r) * tk.ldb + k : A + (int64_t)(m0 + r) * tk.lda + k;
-      cplx* d = isb ? &Bs[r][k] : &As[r][k];
-      cp_async16(d, ok ? g : Abase, ok);
-    }
-    cp_commit();
-  }
-  if (mode != kGemmStore) {
-#pragma unroll 8
-    for (int p = 0; p < BM * BN / SK_NT; ++p) {
-      const int e = p * SK_NT + t, r = e >> 6, c = e & 63;
-      const bool ok = (m0 + r < M) && (n0 + c < N) && (!sym || n0 + c <= m0 + r);
-      cp_async16(&Cs[r][c], ok ? C + (int64_t)(m0 + r) * ldc + n0 + c : Cbase, ok);
-    }
-  }
-  cp_commit();
-
-  const int lane = t & 31, warp = t >> 5;
-  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
-  const int fr = lane >> 2, fc = lane & 3;
-  double acc_re[4][2][2], acc_im[4][2][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
-#pragma unroll
-  for (int ch = 0; ch < NCH; ++ch) {
-    // groups still allowed in flight: the later A/B chunks and C
-    switch (NCH - ch) {
-      case 4: cp_wait<4>(); break;
-      case 3: cp_wait<3>(); break;
-      case 2: cp_wait<2>(); break;
-      default: cp_wait<1>(); break;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kq = 0; kq < 4; ++kq) {
-      const int kk = ch * 4 + kq;
-      double are[4], aim[4], anim[4], bre[2], bim[2];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const cplx a = As[wm + i * 8 + fr][kk * 4 + fc];
-        are[i] = a.x;
-        aim[i] = a.y;
-        anim[i] = -a.y;
-      }
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const cplx b = Bs[wn + j * 8 + fr][kk * 4 + fc];
-        bre[j] = b.x;
-        bim[j] = b.y;
-      }
-      // four passes over all sub-tiles: dependent DMMAs on one accumulator are
-      // 16 instructions apart (per-accumulator order unchanged: bitwise same)
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
-    }
-  }
-  cp_wait<0>();               // the C tile
-  __syncthreads();
-  // ---- epilogue in shared memory, then coalesced stores
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = wm + i * 8 + fr, c = wn + j * 8 + fc * 2 + h;
-        const cplx u = mk(acc_re[i][j][h], acc_im[i][j][h]);
-        cplx& w = Cs[r][c];
-        w = mode == kGemmSub ? c_sub(w, u) : mode == kGemmStore ? u : c_add(w, u);
-      }
-  __syncthreads();
-  const bool track = (tk.flags & kGemmTrackMax) != 0 && tmax != nullptr;
-  double tm2 = 0.0;
-#pragma unroll 8
-  for (int p = 0; p < BM * BN / SK_NT; ++p) {
-    const int e = p * SK_NT + t, r = e >> 6, c = e & 63;
-    if ((m0 + r < M) && (n0 + c < N) && (!sym || n0 + c <= m0 + r)) {
-      const cplx w = Cs[r][c];
-      C[(int64_t)(m0 + r) * ldc + n0 + c] = w;
-      if (track) tm2 = fmax(tm2, w.x * w.x + w.y * w.y);
-    }
-  }
-  if (track) {
-    tm2 = warp_max(tm2);
-    if (lane == 0) atomicMax(tmax + tk.pad_, (unsigned long long)__double_as_longlong(tm2));
-  }
-}
-
 constexpr size_t kGemmSmem = sizeof(cplx) * STAGES * (BM + BN) * PITCH;
 
-static unsigned long long* g_tmax = nullptr;   // set per launch by d3m_gemm_launch_tm
-static const int64_t* g_gperm = nullptr;        // set per launch by d3m_gemm_launch_perm
+// Optional per-launch operands: tmax (kGemmTrackMax targets) and gperm (the
+// column gather of kGemmTriGather tasks), passed with every launch.
+struct LaunchExtra {
+  unsigned long long* tmax;
+  const int64_t* gperm;
+};
 
 template <bool TA, bool TB, bool G3, bool MB = false>
 static int launch_g(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
-                    cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+                    const LaunchExtra& x, cudaStream_t s) {
+  static PerDeviceOnce configured;
+  if (configured.first())
     cudaFuncSetAttribute(zgemm_grouped_kernel<TA, TB, G3, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kGemmSmem);
-    configured = true;
-  }
   zgemm_grouped_kernel<TA, TB, G3, MB><<<ntiles, G3 ? 2 * NTHREADS : NTHREADS, kGemmSmem, s>>>(A, B, C, tasks,
-                                                                                               ntasks, g_tmax, g_gperm);
+                                                                                               ntasks, x.tmax, x.gperm);
   return (int)cudaGetLastError();
 }
 
-// Complex product form of the grouped GEMM: 3M (default) or 4M, chosen once
-// per process by D3M_ZGEMM=3m|4m, or per call chain by d3m_gemm_set_form.
-static int g_form = -1;
+// Complex product form of the grouped GEMM: 3M (default) or 4M, a process-wide
+// setting (D3M_ZGEMM=3m|4m at the first launch, or d3m_gemm_set_form).
+static std::atomic<int> g_form{-1};
 static bool use_3m() {
-  if (g_form < 0) {
+  int f = g_form.load();
+  if (f < 0) {
     const char* e = getenv("D3M_ZGEMM");
-    g_form = (e && (e[0] == '4')) ? 4 : 3;
+    int expect = -1;
+    g_form.compare_exchange_strong(expect, (e && (e[0] == '4')) ? 4 : 3);
+    f = g_form.load();
   }
-  return g_form == 3;
+  return f == 3;
 }
 
 // ---- 3M on half tiles: three CTAs per SM -------------------------------------
@@ -827,32 +675,29 @@ zgemm3m_half_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bba
 
 template <bool TA, bool TB>
 static int launch_half(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
-                       cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+                       const LaunchExtra& x, cudaStream_t s) {
+  static PerDeviceOnce configured;
+  if (configured.first())
     cudaFuncSetAttribute(zgemm3m_half_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHSmem);
-    configured = true;
-  }
-  zgemm3m_half_kernel<TA, TB><<<2 * ntiles, HNT, kHSmem, s>>>(A, B, C, tasks, ntasks, g_tmax, g_gperm);
+  zgemm3m_half_kernel<TA, TB><<<2 * ntiles, HNT, kHSmem, s>>>(A, B, C, tasks, ntasks, x.tmax, x.gperm);
   return (int)cudaGetLastError();
 }
 
 template <bool TA, bool TB>
 static int launch_t(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
-                    cudaStream_t s) {
-  static const int mb = [] { const char* e = getenv("D3M_GEMM_MB"); return e ? atoi(e) : 1; }();
+                    const LaunchExtra& x, cudaStream_t s) {
+  // D3M_GEMM_HALF=0: the 64 x 64 3M kernel for every launch (A/B measurements)
   static const int hk = [] { const char* e = getenv("D3M_GEMM_HALF"); return e ? atoi(e) : 1; }();
-  if (!use_3m()) return launch_g<TA, TB, false>(A, B, C, tasks, ntasks, ntiles, s);
+  if (!use_3m()) return launch_g<TA, TB, false>(A, B, C, tasks, ntasks, ntiles, x, s);
   // non-transposed operands only, and not for the batched panel updates
   // (max-tracking, device-built tasks with a padded tile budget): there the
   // doubled grid of mostly empty CTAs cost more than the faster tiles gained
   // (config 3: 96 -> 119 ms); the transposed launches of the subdomain solves
   // ran 9% slower on half tiles (config 5 GEMM class 6.40 -> 6.96 s)
   if constexpr (!TA && !TB) {
-    if (hk && g_tmax == nullptr) return launch_half<TA, TB>(A, B, C, tasks, ntasks, ntiles, s);
+    if (hk && x.tmax == nullptr) return launch_half<TA, TB>(A, B, C, tasks, ntasks, ntiles, x, s);
   }
-  return mb ? launch_g<TA, TB, true, true>(A, B, C, tasks, ntasks, ntiles, s)
-            : launch_g<TA, TB, true, false>(A, B, C, tasks, ntasks, ntiles, s);
+  return launch_g<TA, TB, true, true>(A, B, C, tasks, ntasks, ntiles, x, s);   // mbarrier ring
 }
 
 }  // namespace d3m
@@ -871,76 +716,45 @@ extern "C" int d3m_gemm_prepare_tasks(d3m::GemmTask* tasks, int ntasks) {
   return total;
 }
 
-extern "C" int d3m_gemm_launch_tm(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
-                                  int ntasks, int ntiles, void* tmax, void* stream);
+namespace {
+int gemm_launch_x(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks, int ntasks, int ntiles,
+                  const d3m::LaunchExtra& x, void* stream) {
+  using namespace d3m;
+  if (ntiles <= 0 || ntasks <= 0) return 0;
+  auto a = static_cast<const cplx*>(A);
+  auto b = static_cast<const cplx*>(B);
+  auto c = static_cast<cplx*>(C);
+  auto t = static_cast<const GemmTask*>(dtasks);
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  if (!ta && !tb) return launch_t<false, false>(a, b, c, t, ntasks, ntiles, x, s);
+  if (!ta && tb) return launch_t<false, true>(a, b, c, t, ntasks, ntiles, x, s);
+  if (ta && !tb) return launch_t<true, false>(a, b, c, t, ntasks, ntiles, x, s);
+  return launch_t<true, true>(a, b, c, t, ntasks, ntiles, x, s);
+}
+}  // namespace
 
 // Select the complex product form of the grouped GEMM: 3 (Gauss 3M) or 4 (4M).
 // Returns the form in effect before the call; 0 only queries.
 extern "C" int d3m_gemm_set_form(int form) {
   const int prev = d3m::use_3m() ? 3 : 4;
-  if (form == 3 || form == 4) d3m::g_form = form;
+  if (form == 3 || form == 4) d3m::g_form.store(form);
   return prev;
 }
 
 extern "C" int d3m_gemm_launch(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
                                int ntasks, int ntiles, void* stream) {
-  return d3m_gemm_launch_tm(ta, tb, A, B, C, dtasks, ntasks, ntiles, nullptr, stream);
+  return gemm_launch_x(ta, tb, A, B, C, dtasks, ntasks, ntiles, d3m::LaunchExtra{nullptr, nullptr}, stream);
 }
 
 // Launch with a column-gather permutation for kGemmTriGather tasks (A not transposed).
 extern "C" int d3m_gemm_launch_perm(const void* A, const void* B, void* C, const void* dtasks, int ntasks, int ntiles,
                                     const void* gperm, void* stream) {
-  d3m::g_gperm = static_cast<const int64_t*>(gperm);
-  const int rc = d3m_gemm_launch_tm(0, 0, A, B, C, dtasks, ntasks, ntiles, nullptr, stream);
-  d3m::g_gperm = nullptr;
-  return rc;
+  return gemm_launch_x(0, 0, A, B, C, dtasks, ntasks, ntiles,
+                       d3m::LaunchExtra{nullptr, static_cast<const int64_t*>(gperm)}, stream);
 }
 
 extern "C" int d3m_gemm_launch_tm(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
                                   int ntasks, int ntiles, void* tmax, void* stream) {
-  using namespace d3m;
-  if (ntiles <= 0 || ntasks <= 0) return 0;
-  g_tmax = static_cast<unsigned long long*>(tmax);
-  auto a = static_cast<const cplx*>(A);
-  auto b = static_cast<const cplx*>(B);
-  auto c = static_cast<cplx*>(C);
-  auto t = static_cast<const GemmTask*>(dtasks);
-  auto s = reinterpret_cast<cudaStream_t>(stream);
-  if (!ta && !tb) return launch_t<false, false>(a, b, c, t, ntasks, ntiles, s);
-  if (!ta && tb) return launch_t<false, true>(a, b, c, t, ntasks, ntiles, s);
-  if (ta && !tb) return launch_t<true, false>(a, b, c, t, ntasks, ntiles, s);
-  return launch_t<true, true>(a, b, c, t, ntasks, ntiles, s);
-}
-
-// Grouped small-K launch (every task K <= 16; SYM tasks must be LowerOnly).
-extern "C" int d3m_gemm_smallk_launch_k(int kt, const void* A, const void* B, void* C, const void* dtasks, int ntasks,
-                                        int ntiles, void* tmax, void* stream);
-
-extern "C" int d3m_gemm_smallk_launch_tm(const void* A, const void* B, void* C, const void* dtasks, int ntasks,
-                                         int ntiles, void* tmax, void* stream) {
-  return d3m_gemm_smallk_launch_k(16, A, B, C, dtasks, ntasks, ntiles, tmax, stream);
-}
-
-// Grouped small-K launch: every task K <= kt (16 or 32); SYM tasks must be LowerOnly.
-extern "C" int d3m_gemm_smallk_launch_k(int kt, const void* A, const void* B, void* C, const void* dtasks, int ntasks,
-                                        int ntiles, void* tmax, void* stream) {
-  using namespace d3m;
-  if (ntiles <= 0 || ntasks <= 0) return 0;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(zgemm_smallk_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sk_smem<16>());
-    cudaFuncSetAttribute(zgemm_smallk_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sk_smem<32>());
-    cudaFuncSetAttribute(zgemm_smallk_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sk_smem<64>());
-    configured = true;
-  }
-  auto s = reinterpret_cast<cudaStream_t>(stream);
-  auto a = static_cast<const cplx*>(A);
-  auto b = static_cast<const cplx*>(B);
-  auto c = static_cast<cplx*>(C);
-  auto t = static_cast<const GemmTask*>(dtasks);
-  auto tm = static_cast<unsigned long long*>(tmax);
-  if (kt <= 16) zgemm_smallk_kernel<16><<<ntiles, SK_NT, sk_smem<16>(), s>>>(a, b, c, t, ntasks, tm);
-  else if (kt <= 32) zgemm_smallk_kernel<32><<<ntiles, SK_NT, sk_smem<32>(), s>>>(a, b, c, t, ntasks, tm);
-  else zgemm_smallk_kernel<64><<<ntiles, SK_NT, sk_smem<64>(), s>>>(a, b, c, t, ntasks, tm);
-  return (int)cudaGetLastError();
+  return gemm_launch_x(ta, tb, A, B, C, dtasks, ntasks, ntiles,
+                       d3m::LaunchExtra{static_cast<unsigned long long*>(tmax), nullptr}, stream);
 }

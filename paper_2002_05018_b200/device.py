@@ -48,12 +48,18 @@ def zeros(shape, dtype="complex128"):
 
 
 def to_device(a, dtype=np.complex128):
-    """Host array / DeviceArray / tensor -> contiguous CUDA tensor."""
+    """Host array / DeviceArray / tensor -> contiguous CUDA tensor of `dtype`
+    (the kernels read raw complex128 / int64 memory, so a tensor of another
+    dtype is converted like np.asarray(a, dtype) would convert it; a tensor
+    that already matches is passed through without a copy)."""
     t = require_cuda()
     if isinstance(a, DeviceArray):
-        return a.tensor
+        a = a.tensor
     if isinstance(a, t.Tensor):
-        return a.contiguous() if a.is_cuda else a.to("cuda").contiguous()
+        tdt = t.from_numpy(np.empty(0, dtype=dtype)).dtype
+        if a.is_complex() and not tdt.is_complex:
+            raise TypeError(f"cannot convert a {a.dtype} tensor to {np.dtype(dtype)}")
+        return a.to(device="cuda", dtype=tdt).contiguous()
     arr = np.ascontiguousarray(np.asarray(a, dtype=dtype))
     return t.from_numpy(arr).to("cuda", non_blocking=False)
 

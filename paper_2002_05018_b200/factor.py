@@ -413,7 +413,16 @@ def _upload_K(K: BlockSparseSym, sched: _Schedule, plan: EliminationPlan, pool):
     t = require_cuda()
     inv = plan.order.inverse()
     sizes = K.sizes
-    items = list(K.blocks.items())
+    items = []
+    for k, b in K.blocks.items():
+        # device blocks must be complex128 (the copy kernel reads raw memory):
+        # CUDA tensors and DeviceArrays of another dtype are converted first
+        if _is_tensor(b) and b.is_cuda:
+            b = DeviceArray(to_device(b))
+        elif isinstance(b, DeviceArray) and b.tensor.dtype != t.complex128:
+            b = DeviceArray(to_device(b))
+        items.append((k, b))
+
     def cpu_view(b):
         return _is_tensor(b) and not b.is_cuda and b.is_contiguous() and b.dtype == t.complex128
 

@@ -417,3 +417,64 @@ def test_pinned_streamed_upload_and_host_tensor_solve(cuda):
     for a, b in zip(x0, xp):
         assert isinstance(b, torch.Tensor) and not b.is_cuda
         assert np.array_equal(a, b.numpy())
+
+
+def test_concurrent_block_ldlt_from_two_threads(cuda):
+    """libd3m keeps its executor state per device and serialises the enqueue
+    of concurrent calls (d3m_capi.cu ExecCtx): two host threads factoring and
+    solving at once (ctypes releases the GIL) get the bitwise results of the
+    sequential calls."""
+    import threading
+
+    import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import workloads as wl
+    K, _ = wl.rand_block_system(97, max_blocks=8, max_size=300)
+    plan = _plan(K)
+    rng = np.random.default_rng(98)
+    B = [rng.standard_normal((int(s), 3)) + 1j * rng.standard_normal((int(s), 3)) for s in K.sizes]
+    F0 = d.block_ldlt(K, plan)
+    x0 = [np.asarray(v) for v in d.block_solve(F0, B)]
+    out, errs = {}, []
+
+    def work(tag):
+        try:
+            for it in range(3):
+                F = d.block_ldlt(K, plan)
+                out[(tag, it)] = ([f.perm for f in F.diag], [np.asarray(v) for v in d.block_solve(F, B)])
+        except Exception as e:          # noqa: BLE001  (reported below)
+            errs.append(e)
+    th = [threading.Thread(target=work, args=(t,)) for t in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for (perms, x) in out.values():
+        for p, f in zip(perms, F0.diag):
+            assert np.array_equal(p, f.perm)
+        for a, b in zip(x, x0):
+            assert np.array_equal(a, b)
+
+
+def test_real_and_single_precision_tensor_inputs_are_converted(cuda):
+    """A torch RHS of another dtype (float64, complex64) is converted like
+    np.asarray(b, complex128) would convert it, not reinterpreted."""
+    import torch
+
+    import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import workloads as wl
+    K, _ = wl.rand_block_system(55, max_blocks=5, max_size=20)
+    F = d.block_ldlt(K, _plan(K))
+    rng = np.random.default_rng(56)
+    Br = [rng.standard_normal(int(s)) for s in K.sizes]
+    want = [np.asarray(v) for v in d.block_solve(F, [b.astype(complex) for b in Br])]
+    for conv in (lambda b: torch.from_numpy(b).cuda(), lambda b: torch.from_numpy(b)):
+        got = [np.asarray(v) for v in d.block_solve(F, [conv(b) for b in Br])]
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
+    B64 = [torch.from_numpy(b.astype(np.complex64)).cuda() for b in Br]
+    got = [np.asarray(v) for v in d.block_solve(F, B64)]
+    for a, b in zip(got, want):
+        assert np.abs(a - b).max() <= 1e-5 * max(np.abs(b).max(), 1.0)
+    f = d.dense_ldlt_bk(torch.eye(4, dtype=torch.float64, device="cuda"))
+    assert np.array_equal(f.d, np.ones(4, dtype=complex))
