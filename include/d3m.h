@@ -190,6 +190,21 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                         int nwait, const int64_t* h_wait_col, void* const* h_wait_ev, const void* d_check_sym,
                         void* d_margin, void* stream);
 
+/* Host-staged upload of pageable inputs (ABI v9): a native host thread copies
+ * chunk c's blocks (blocks [chunk_ptr[c], chunk_ptr[c+1]) of the n copies
+ * src[i] -> dst + dst_off[i], nbytes[i] bytes; dst is pinned host memory)
+ * with up to nthreads threads, then stores c + 1 into the pinned int *flag.
+ * The sources must stay alive until d3m_host_stage_join.  Returns a handle,
+ * NULL on failure.  Used by block_ldlt for numpy K blocks (the reference
+ * API's inputs) so the H2D transfer of later chunks overlaps the first
+ * columns' factorisation. */
+void* d3m_host_stage_start(int nchunks, const int64_t* chunk_ptr, int n, const void* const* src,
+                           const int64_t* dst_off, const int64_t* nbytes, void* dst, void* flag, int nthreads);
+/* Join the host thread of d3m_host_stage_start and free its handle. */
+int d3m_host_stage_join(void* handle);
+/* Make `stream` wait until the pinned host int *flag >= value. */
+int d3m_stream_wait_flag(const void* flag, int value, void* stream);
+
 /* n asynchronous copies dst + dst_off[i] <- src + src_off[i] (bytes, kind a
  * cudaMemcpyKind) on `stream`: the chunked upload of K's blocks from pinned
  * host memory. */

@@ -24,6 +24,8 @@ _SIGNATURES = {
     "d3m_abi_version": [],
     "d3m_bk_factor_batched": [I32, I32, P, I64, I32, F64, I32, P, P, P, P, P, P, P, P, P, P],
     "d3m_bk_cluster_max_n": [I32],
+    "d3m_host_stage_join": [P],
+    "d3m_stream_wait_flag": [P, I32, P],
     "d3m_plan_flow_items": [I32, P, P, P, P, P, I64, P, I64, P, P],
     "d3m_ldlt_solve_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P],
     "d3m_zgemm_grouped": [I32, I32, P, P, P, P, I32, P, P],
@@ -49,6 +51,7 @@ _SIGNATURES = {
     "d3m_ldlt_solve_blocked_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P, P],
 }
 _SIZE_T = {"d3m_bk_panel_workspace": [I32, I32]}
+_PTR = {"d3m_host_stage_start": [I32, P, I32, P, P, P, P, P, I32]}
 _INT64 = {"d3m_timing_intervals": [P, I64],
           "d3m_plan_gemm_tasks": [I32, P, P, P, P, P, P, I64, P, P, P, P, P]}
 _VOID = {"d3m_set_timing": [I32], "d3m_counters_reset": []}
@@ -115,6 +118,10 @@ def load():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = ctypes.c_size_t
+    for name, args in _PTR.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_void_p
     for name, args in _VOID.items():
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -124,7 +131,7 @@ def load():
 
 
 def exported_symbols() -> list[str]:
-    return list(_SIGNATURES) + list(_VOID) + list(_SIZE_T) + list(_INT64) + ["d3m_last_error"]
+    return list(_SIGNATURES) + list(_VOID) + list(_SIZE_T) + list(_INT64) + list(_PTR) + ["d3m_last_error"]
 
 
 CLASSES = ("bk", "trsm", "gemm", "solve", "misc")

@@ -217,7 +217,9 @@ __host__ __device__ inline int64_t bkc_entries(int n) {    // per-CTA capacity (
 // the peer only reaches step s after this CTA pushed its step s-1 column,
 // which follows the end of its step s-2 bulk update.  The rowmax columns
 // (k+1, imax) are filled and read inside one step: double-buffered.
-template <int CS>
+// TRACK: the margin diagnostic (BkArgs::margin) is compiled in only in the
+// TRACK instance, so the production kernel keeps its registers.
+template <int CS, bool TRACK>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_kernel(BkArgs a) {
 #ifdef D3M_BK_PROFILE
   const long long t_entry = clock64();
@@ -296,7 +298,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     return;
   }
   const double tol_abs = __dmul_rn(a.pivot_tol, scale);
-  const bool track = a.margin != nullptr;      // pivot-decision margins (lead thread)
+  constexpr bool track = TRACK;                // pivot-decision margins (lead thread)
   double mdec = 1.0, mgap = 1.0;
   // growth recurrence (kernels.py:135-144), run by gthread only: a step's
   // update maximum reaches every CTA two steps later, applied in step order
@@ -742,11 +744,11 @@ constexpr size_t kBkcSmemMax = 220 * 1024;
 template <int CS>
 static bool bkc_fits(int n) { return bkc_smem_bytes<CS>(n) <= kBkcSmemMax && n <= BKC_JPT * (BKC_NT - 32); }
 
-template <int CS>
-static int bkc_launch(BkArgs* a, int batch, cudaStream_t s) {
+template <int CS, bool TRACK>
+static int bkc_launch_t(BkArgs* a, int batch, cudaStream_t s) {
   const size_t smem = bkc_smem_bytes<CS>(a->n);
   if (!bkc_fits<CS>(a->n)) return -22;   // the CTA owns its SM
-  cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(bk_cluster_kernel<CS, TRACK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (CS == 16) {
     // 16 is a non-portable cluster size: check once per device that a
     // cluster of full-SM CTAs can be resident on this part
@@ -755,8 +757,9 @@ static int bkc_launch(BkArgs* a, int batch, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (checked.first()) {
-      cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBkcSmemMax);
+      cudaFuncSetAttribute(bk_cluster_kernel<CS, TRACK>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(bk_cluster_kernel<CS, TRACK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kBkcSmemMax);
       cudaLaunchConfig_t cfg = {};
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -769,15 +772,21 @@ static int bkc_launch(BkArgs* a, int batch, cudaStream_t s) {
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       int nclusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&nclusters, bk_cluster_kernel<CS>, &cfg) == cudaSuccess && nclusters > 0)
+      if (cudaOccupancyMaxActiveClusters(&nclusters, bk_cluster_kernel<CS, TRACK>, &cfg) == cudaSuccess &&
+          nclusters > 0)
         yes16.fetch_or(1ull << (dev & 63));
       cudaGetLastError();
-      cudaFuncSetAttribute(bk_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(bk_cluster_kernel<CS, TRACK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     if (!(yes16.load() & (1ull << (dev & 63)))) return -22;
   }
-  bk_cluster_kernel<CS><<<batch * CS, BKC_NT, smem, s>>>(*a);
+  bk_cluster_kernel<CS, TRACK><<<batch * CS, BKC_NT, smem, s>>>(*a);
   return (int)cudaGetLastError();
+}
+
+template <int CS>
+static int bkc_launch(BkArgs* a, int batch, cudaStream_t s) {
+  return a->margin ? bkc_launch_t<CS, true>(a, batch, s) : bkc_launch_t<CS, false>(a, batch, s);
 }
 
 }  // namespace d3m

@@ -14,6 +14,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "d3m_common.cuh"
@@ -913,3 +914,89 @@ int d3m_memcpy_batch(void* dst, const void* src, const int64_t* dst_off, const i
   }
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// Host-staged upload of pageable inputs (block_ldlt with numpy K blocks).
+//
+// A host thread copies the blocks of chunk c into a pinned staging buffer
+// (nthreads-way parallel memcpy) and then publishes the chunk by storing
+// c + 1 into a pinned flag; on the copy stream, d3m_stream_wait_flag holds
+// chunk c's H2D copy until the flag reaches c + 1.  The factorisation's
+// first columns start as soon as their chunk is staged, while the host is
+// still copying the later ones.
+// ---------------------------------------------------------------------------
+namespace {
+struct HostStage {
+  std::thread th;
+  std::atomic<int> err{0};
+};
+
+void host_stage_run(HostStage* h, int nchunks, std::vector<int64_t> chunk_ptr, std::vector<const char*> src,
+                    std::vector<int64_t> dst_off, std::vector<int64_t> nbytes, char* dst, int* flag, int nthreads) {
+  std::vector<std::thread> pool;
+  for (int c = 0; c < nchunks; ++c) {
+    const int64_t b0 = chunk_ptr[c], b1 = chunk_ptr[c + 1];
+    int64_t tot = 0;
+    for (int64_t b = b0; b < b1; ++b) tot += nbytes[b];
+    // split the chunk's bytes evenly over the threads (each copies a
+    // contiguous byte range of the concatenated blocks)
+    const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads, tot >> 22));   // >= 4 MB per thread
+    auto copy_range = [&](int64_t lo, int64_t hi) {
+      int64_t pos = 0;
+      for (int64_t b = b0; b < b1 && pos < hi; ++b) {
+        const int64_t s0 = std::max(lo, pos), s1 = std::min(hi, pos + nbytes[b]);
+        if (s1 > s0) std::memcpy(dst + dst_off[b] + (s0 - pos), src[b] + (s0 - pos), (size_t)(s1 - s0));
+        pos += nbytes[b];
+      }
+    };
+    pool.clear();
+    for (int t = 1; t < nt; ++t) pool.emplace_back(copy_range, tot * t / nt, tot * (t + 1) / nt);
+    copy_range(0, tot / nt);
+    for (auto& th : pool) th.join();
+    __atomic_store_n(flag, c + 1, __ATOMIC_RELEASE);
+  }
+}
+}  // namespace
+
+extern "C" {
+
+// Start the host thread: nchunks chunks, chunk c = blocks [chunk_ptr[c],
+// chunk_ptr[c+1]) of the n block copies src[i] -> dst + dst_off[i] (nbytes[i]
+// bytes; dst a pinned buffer, flag a pinned int).  The source arrays must stay
+// alive until d3m_host_stage_join.  Returns a handle (NULL on failure).
+void* d3m_host_stage_start(int nchunks, const int64_t* chunk_ptr, int n, const void* const* src,
+                           const int64_t* dst_off, const int64_t* nbytes, void* dst, void* flag, int nthreads) {
+  try {
+    auto* h = new HostStage;
+    std::vector<int64_t> cp(chunk_ptr, chunk_ptr + nchunks + 1);
+    std::vector<const char*> sv(n);
+    for (int i = 0; i < n; ++i) sv[i] = static_cast<const char*>(src[i]);
+    std::vector<int64_t> doff(dst_off, dst_off + n), nb(nbytes, nbytes + n);
+    h->th = std::thread(host_stage_run, h, nchunks, std::move(cp), std::move(sv), std::move(doff), std::move(nb),
+                        static_cast<char*>(dst), static_cast<int*>(flag), std::max(1, nthreads));
+    return h;
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+// Wait for the host thread and release the handle; 0 on success.
+int d3m_host_stage_join(void* handle) {
+  if (!handle) return fail(-22, "d3m_host_stage_join: null handle");
+  auto* h = static_cast<HostStage*>(handle);
+  h->th.join();
+  const int e = h->err.load();
+  delete h;
+  return e;
+}
+
+// The stream waits until the pinned host int *flag >= value (a one-thread
+// kernel polling the mapped host memory; traps after ~60 s instead of
+// hanging the stream when the host side never publishes).
+int d3m_stream_wait_flag(const void* flag, int value, void* stream) {
+  return launch(kClsMisc, stream, [&] {
+    return d3m_wait_flag_launch(static_cast<const int*>(flag), value, stream);
+  });
+}
+
+}  // extern "C"

@@ -88,6 +88,7 @@ int d3m_dinv_left_copy_launch(const void* Z, void* U, int n, int m, const void* 
 int d3m_sym_flags_launch(const void* pool, const void* off, const void* n, const void* idx, int count, void* flags,
                          void* stream);
 int d3m_nonzero_rows_launch(int B, int n, int m, const void* D, void* flag, void* idx, void* count, void* stream);
+int d3m_wait_flag_launch(const int* flag, int value, void* stream);
 int d3m_tri_inv_blocked_launch(const void* F, const void* perm, const void* tags, void* Binv, void* coef, int n,
                                void* Linv, void* dinv, void* stream);
 int d3m_gemm_launch_perm(const void* A, const void* B, void* C, const void* dtasks, int ntasks, int ntiles,

@@ -315,3 +315,24 @@ extern "C" int d3m_sym_flags_launch(const void* pool, const void* off, const voi
       static_cast<const int64_t*>(idx), static_cast<int*>(flags));
   return (int)cudaGetLastError();
 }
+
+// One thread polls a pinned (mapped) host int until it reaches `value`
+// (system-scope acquire loads, backing off with nanosleep); a host side that
+// never publishes ends in a trap after ~60 s rather than a hung stream.
+__global__ void wait_flag_kernel(const int* flag, int value) {
+  unsigned ns = 256;
+  const long long t0 = clock64();
+  for (;;) {
+    int v;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];\n" : "=r"(v) : "l"(flag) : "memory");
+    if (v >= value) return;
+    __nanosleep(ns);
+    if (ns < 8192) ns <<= 1;
+    if (clock64() - t0 > 120000000000LL) __trap();     // ~60 s at 2 GHz
+  }
+}
+
+extern "C" int d3m_wait_flag_launch(const int* flag, int value, void* stream) {
+  wait_flag_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flag, value);
+  return (int)cudaGetLastError();
+}

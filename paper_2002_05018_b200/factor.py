@@ -622,6 +622,146 @@ def _stream_chunks(sched, pool, flag, base, recs, d_rec, plan_chunks, o, kentrie
     return np.asarray(waits, dtype=np.int64), events, (stage, d_rec), [(stage, kentries)]
 
 
+def _host_layout(K: BlockSparseSym, sched: _Schedule, plan: EliminationPlan):
+    """Chunk layout of a host-staged upload (_upload_K_hoststaged): cached per
+    schedule and block-key set.  Blocks go in the chunk of the first block
+    column that touches them (_CHUNK_COLS), in staging order; returns
+    (keys, copy records, device records, chunks, staged elements, kentries)
+    with chunks = [(first column, record start, count, max entries,
+    item indices, staging offsets, diag device array, diag count)]."""
+    keys = tuple(K.blocks)
+    cache = getattr(sched, "host_layout", None)
+    if cache is None:
+        cache = sched.host_layout = {}
+    hit = cache.get(keys)
+    if hit is not None:
+        return hit
+    nb = plan.nblocks
+    inv = plan.order.inverse()
+    sizes = K.sizes
+    ft = _first_touch(sched)
+    bounds = [0] + [c for c in _CHUNK_COLS if c < nb] + [nb]
+    chunks = [[] for _ in range(len(bounds) - 1)]
+    for idx, (i, j) in enumerate(keys):
+        a, c = int(inv[i]), int(inv[j])
+        key = (a, c) if a >= c else (c, a)
+        if key not in ft:
+            raise FactorConsistencyError(f"block {key} outside the symbolic pattern")
+        chunks[int(np.searchsorted(bounds, ft[key], side="right")) - 1].append(idx)
+    recs = np.zeros(len(keys), dtype=_lib.COPY_TASK)
+    out_chunks, r, o, kentries = [], 0, 0, []
+    for ch, members in enumerate(chunks):
+        if not members:
+            continue
+        r0, maxe, offs, diag = r, 1, [], []
+        for idx in members:
+            i, j = keys[idx]
+            a, c = int(inv[i]), int(inv[j])
+            ni, nj = int(sizes[i]), int(sizes[j])
+            key, transpose = ((a, c), 0) if a >= c else ((c, a), 1)
+            if key[0] == key[1]:
+                dst, ld = int(sched.diag_off[key[0]]), int(plan.sizes_perm[key[0]])
+                diag.append(key[0])
+            else:
+                dst, _, ld = sched.loc[key]
+            rows, cols = (ni, nj) if not transpose else (nj, ni)
+            recs[r] = (o, dst, rows, cols, nj, ld, transpose, _lib.COPY_STORE)
+            kentries.append((o, (i, j)))
+            maxe = max(maxe, rows * cols)
+            offs.append(o)
+            o += ni * nj
+            r += 1
+        out_chunks.append((bounds[ch], r0, r - r0, maxe, members, offs,
+                           upload_i64(np.asarray(diag, np.int64)) if diag else None, len(diag)))
+    hit = (keys, recs, upload_bytes(recs), out_chunks, o, kentries)
+    if len(cache) >= 4:
+        cache.clear()
+    cache[keys] = hit
+    return hit
+
+
+def _upload_K_hoststaged(K: BlockSparseSym, sched: _Schedule, plan: EliminationPlan, pool, flag):
+    """Chunked upload of K from pageable host arrays (numpy blocks, as the
+    reference API takes them).  A native host thread (d3m_host_stage_start)
+    copies chunk after chunk into a pinned staging buffer, cached on the
+    schedule, and publishes each chunk through a pinned flag; the copy stream
+    holds each chunk's H2D copy until its flag (d3m_stream_wait_flag), so the
+    first columns' factorisation starts while the host is still staging the
+    later blocks.  Returns (wait columns, events, keep-alive, kgroups, handle)
+    or None when a block is on the device."""
+    t = require_cuda()
+    items = list(K.blocks.items())
+    if not items or any(isinstance(b, DeviceArray) or (_is_tensor(b) and b.is_cuda) for _, b in items):
+        return None
+    keys, recs, d_rec, chunks, o, kentries = _host_layout(K, sched, plan)
+    # sources: C-contiguous complex128 host arrays, alive until the join
+    src = []
+    for _, b in items:
+        a = b.numpy() if _is_tensor(b) else b
+        src.append(np.ascontiguousarray(np.asarray(a, dtype=np.complex128)))
+    for (i, j), a in zip(keys, src):
+        if a.size != int(K.sizes[i]) * int(K.sizes[j]):
+            raise ValueError(f"block {(i, j)} has shape {a.shape}, expected {(int(K.sizes[i]), int(K.sizes[j]))}")
+    prev = getattr(sched, "pin_busy", None)
+    if prev is not None:
+        prev.synchronize()                 # the last upload's copies out of the staging buffer are done
+    pin = getattr(sched, "pin_stage", None)
+    if pin is None or pin.numel() < o:
+        pin = sched.pin_stage = t.empty(max(o, 1), dtype=t.complex128, pin_memory=True)
+        sched.pin_flag = t.zeros(1, dtype=t.int32, pin_memory=True)
+    pflag = sched.pin_flag
+    pflag.numpy()[0] = 0
+    stage = empty(max(o, 1))
+    cur = t.cuda.current_stream()
+    cs = getattr(sched, "copy_stream", None)
+    if cs is None:
+        cs = sched.copy_stream = t.cuda.Stream()
+    ready = t.cuda.Event()
+    ready.record(cur)                      # pool zeroed, flag / staging allocated
+    cs.wait_event(ready)
+    csp = _lib.ctypes.c_void_p(cs.cuda_stream)
+    H = _lib.hptr
+    fptr = _lib.ctypes.c_void_p(pflag.data_ptr())
+    waits, events = [], []
+    chunk_ptr, order, dst_off, nbytes = [0], [], [], []
+    for n, (col, r0, cnt, maxe, members, offs, d_diag, ndiag) in enumerate(chunks):
+        lo, hi = offs[0], offs[-1] + src[members[-1]].size
+        _lib.call("d3m_stream_wait_flag", fptr, n + 1, csp)
+        _lib.call("d3m_memcpy_batch", _P(stage), _lib.ctypes.c_void_p(pin.data_ptr()),
+                  H(np.array([16 * lo], np.int64)), H(np.array([16 * lo], np.int64)),
+                  H(np.array([16 * (hi - lo)], np.int64)), 1, 1, csp)
+        _lib.call("d3m_block_copy", _P(stage), _P(pool), _lib.ctypes.c_void_p(d_rec.data_ptr() + r0 * recs.itemsize),
+                  cnt, maxe, csp)
+        if ndiag:                          # exact-symmetry flags of the chunk's diagonal blocks (as uploaded)
+            _lib.call("d3m_diag_sym_flags", _P(pool), _P(sched.d_diag_off), _P(sched.d_sizes), _P(d_diag), ndiag,
+                      _P(flag), csp)
+        ev = t.cuda.Event()
+        ev.record(cs)
+        if n == 0:
+            cur.wait_event(ev)             # the first columns' blocks and flags
+        else:
+            waits.append(col)
+            events.append(ev)
+        for m, off in zip(members, offs):
+            order.append(m)
+            dst_off.append(16 * off)
+            nbytes.append(16 * src[m].size)
+        chunk_ptr.append(len(order))
+    sched.pin_busy = events[-1] if events else ev
+    stage.record_stream(cs)
+    d_rec.record_stream(cs)
+    srcp = (_lib.ctypes.c_void_p * max(len(order), 1))(*[src[m].ctypes.data for m in order])
+    handle = _lib.load().d3m_host_stage_start(len(chunks), H(np.asarray(chunk_ptr, np.int64)), len(order), srcp,
+                                              H(np.asarray(dst_off, np.int64)), H(np.asarray(nbytes, np.int64)),
+                                              _lib.ctypes.c_void_p(pin.data_ptr()), fptr,
+                                              min(8, _os.cpu_count() or 1))
+    if not handle:
+        pflag.numpy()[0] = len(chunks)     # release the waiting copy stream, then fail
+        raise _lib.D3MError("d3m_host_stage_start failed")
+    return (np.asarray(waits, dtype=np.int64), events, (stage, d_rec, src, pin), [(stage, kentries)],
+            _lib.ctypes.c_void_p(handle))
+
+
 def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFAULT_PIVOT_TOL,
                lookahead: bool = True, margins: bool = False) -> BlockFactor:
     """Right-looking block LDL^T of ``K`` following ``plan`` on one GPU.
@@ -659,6 +799,22 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
     # device (ABI v8): no host sync on the upload of K's diagonal
     flag = t.ones(max(nb, 1), dtype=t.int32, device="cuda")
     streamed = _upload_K_streamed(K, sched, plan, pool, flag)
+    stage_handle = None
+    if streamed is None:
+        hs = _upload_K_hoststaged(K, sched, plan, pool, flag)
+        if hs is not None:
+            *streamed, stage_handle = hs
+    try:
+        return _block_ldlt_run(K, plan, pivot_tol, lookahead, margins, sched, pool, flag, streamed, stored, flops,
+                               peak, inv)
+    finally:
+        if stage_handle is not None:       # the host thread reads the caller's arrays until here
+            _lib.call("d3m_host_stage_join", stage_handle)
+
+
+def _block_ldlt_run(K, plan, pivot_tol, lookahead, margins, sched, pool, flag, streamed, stored, flops, peak, inv):
+    t = require_cuda()
+    nb = K.nblocks
     if streamed is None:
         kgroups = _upload_K(K, sched, plan, pool)
         if getattr(sched, "d_all_blocks", None) is None:

@@ -13,7 +13,7 @@ from conftest import ROOT
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "d3m.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(d3m_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|void\*?|const char\*)\s+(d3m_\w+)\s*\(", src, re.M)))
 
 
 def test_header_declares_entry_points():
