@@ -184,10 +184,13 @@ def ptr(t) -> ctypes.c_void_p:
     if t is None:
         return ctypes.c_void_p(0)
     if isinstance(t, np.ndarray):
-        return ctypes.c_void_p(t.ctypes.data)
+        return t.ctypes.data_as(ctypes.c_void_p)      # keeps the array alive with the pointer
     return ctypes.c_void_p(t.data_ptr())
 
 
 def hptr(a: np.ndarray) -> ctypes.c_void_p:
+    """Host pointer of a C-contiguous array; the returned object holds a
+    reference to the array, so a temporary (hptr(np.asarray(...))) stays
+    alive until the call that receives the pointer has returned."""
     assert a.flags.c_contiguous
-    return ctypes.c_void_p(a.ctypes.data)
+    return a.ctypes.data_as(ctypes.c_void_p)
