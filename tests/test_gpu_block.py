@@ -489,10 +489,10 @@ def test_host_staged_upload_matches_device_inputs(cuda):
     import paper_2002_05018_b200 as d
     from paper_2002_05018_b200 import workloads as wl
     from paper_2002_05018_b200.factor import to_device_blocks
-    K, _ = wl.rand_block_system(123, max_blocks=40, max_size=48, density=0.3)
+    K = wl.config4_matrix(seed=123, grid=(3, 3, 3), n=24)               # 54 faces: several chunks
     k0 = next(k for k in K.blocks if k[0] != k[1])
     K.blocks[k0] = np.asfortranarray(np.asarray(K.blocks[k0]).real)      # float64, F-order
-    plan = _plan(K)
+    plan = _plan(K, d.identity_ordering(K.nblocks))
     assert plan.nblocks > 16                                              # several upload chunks
     Fd = d.block_ldlt(to_device_blocks(K), plan)
     rng = np.random.default_rng(124)
