@@ -219,6 +219,28 @@ def gen_cfg3(domains=(0, 1)):
     np.savez_compressed(os.path.join(OUT, "cfg3.npz"), domains=np.array(domains), **recs)
 
 
+def gen_blk():
+    """A "D3M-BLK v1" dump written by the REFERENCE's save_blk (the golden-K
+    exchange format, blockmat.py:132-146) of a small config-4-shaped K, and
+    the reference's block_ldlt pivots / 1-RHS solution of the loaded K."""
+    K = wl.config4_matrix(seed=21, grid=(2, 2, 3), n=12)
+    Kr = rb.from_blocks(K.sizes, [(i, j, np.asarray(b)) for (i, j), b in K.blocks.items()])
+    path = os.path.join(OUT, "k_small.blk")
+    rb.save_blk(path, Kr)
+    Kl = rb.load_blk(path)
+    g = rb.clique_graph(Kl)
+    order = ro.reorder(g, Kl.sizes)
+    plan = rsym.symbolic_factor(g, order, Kl.sizes)
+    F = rf.block_ldlt(Kl, plan)
+    rng = np.random.default_rng(22)
+    b = [rng.standard_normal(int(s)) + 1j * rng.standard_normal(int(s)) for s in Kl.sizes]
+    x = rf.block_solve(F, b)
+    np.savez_compressed(os.path.join(OUT, "k_small.npz"), order=order.perm,
+                        perm=np.concatenate([f.perm for f in F.diag]), tags=np.concatenate([f.tags for f in F.diag]),
+                        x=np.concatenate(x), b=np.concatenate(b))
+    print("blk fixture written")
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
@@ -230,3 +252,5 @@ if __name__ == "__main__":
         gen_cfg4()
     if what in ("cfg3", "all"):
         gen_cfg3()
+    if what in ("blk", "all"):
+        gen_blk()
