@@ -174,7 +174,19 @@ int d3m_modulus_probe(const void* z, void* hyp, void* npabs, int64_t n, void* st
  * h_piv_off[j]; info/n2x2/growth/scale/asym are nb-long device arrays.
  * check_sym: 1 = full numpy-style symmetry check per diagonal block,
  * 2 = blocks known exactly symmetric (d3m_diag_sym_exact).
- * xbuf: X scratch (2 x max R_j n_j with lookahead).
+ * xbuf: X scratch (4 x max R_j n_j with lookahead: a ring of X panels of
+ * the columns in flight).  bk_scratch (only for supernodes > 3200): 4 x 4 x
+ * max n_j complex, one per critical stream.
+ * lookahead 0: every launch in column order on `stream`.  lookahead 1
+ * (etree-parallel, ABI v9): each column's critical chain (BK -> L^-1 ->
+ * panel TRSM -> D^-1 -> update of column j+1) runs on one of 4 high-priority
+ * streams, h_sched[3j] (independent subtrees of the elimination tree
+ * overlap); the bulk trailing updates run in column order on one
+ * low-priority stream, so every block receives its updates in ascending
+ * source-column order and the factor is bitwise that of lookahead 0.
+ * h_sched[3j+1] / [3j+2]: the last column k < j whose bulk update writes
+ * column j / column j+1 (-1: none), the events column j's BK / its update
+ * of column j+1 wait for (planner.etree_schedule).
  * nwait / h_wait_col / h_wait_ev (ABI v6; 0 / NULL / NULL = none): cudaEvent_t
  * handles; before column h_wait_col[w] the critical stream waits on
  * h_wait_ev[w] (blocks of K still being uploaded on a copy stream).
@@ -188,7 +200,7 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                         void* d_perm, void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale,
                         void* d_asym, void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead,
                         int nwait, const int64_t* h_wait_col, void* const* h_wait_ev, const void* d_check_sym,
-                        void* d_margin, void* stream);
+                        void* d_margin, const int32_t* h_sched, void* stream);
 
 /* Host-staged upload of pageable inputs (ABI v9): a native host thread copies
  * chunk c's blocks (blocks [chunk_ptr[c], chunk_ptr[c+1]) of the n copies

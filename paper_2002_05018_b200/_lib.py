@@ -41,7 +41,7 @@ _SIGNATURES = {
     "d3m_diag_sym_exact": [P, P, P, I32, P, P],
     "d3m_modulus_probe": [P, P, P, I64, P],
     "d3m_block_ldlt_exec": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, P, P, P, P, P, P, P,
-                            P, F64, I32, I32, I32, P, P, P, P, P],
+                            P, F64, I32, I32, I32, P, P, P, P, P, P],
     "d3m_diag_sym_flags": [P, P, P, P, I32, P, P],
     "d3m_memcpy_batch": [P, P, P, P, P, I32, I32, P],
     "d3m_block_solve_exec": [I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, I32, P, P],

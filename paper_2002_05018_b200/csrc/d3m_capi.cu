@@ -105,15 +105,29 @@ inline const cplx* CC(const void* p) { return static_cast<const cplx*>(p); }
 // and their events, the D^-1 coefficient buffer, the unpermuted L^-1 of every
 // column and the diagonal-inverse scratch.  One context per device, created
 // on first use on that device; calls on a device serialise on its mutex.
+constexpr int kCritStreams = 4;       // critical streams of the etree-parallel executor
+constexpr int kXSlots = 4;            // X-panel / D^-1-coefficient ring slots (columns in flight)
 struct ExecCtx {
   std::mutex mu;
-  cudaStream_t crit = nullptr, side = nullptr;
-  cudaEvent_t ev_next = nullptr, ev_rest = nullptr, ev_in = nullptr, ev_out = nullptr;
+  cudaStream_t crit[kCritStreams] = {}, side = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  std::vector<cudaEvent_t> ev_col, ev_rest;   // per block column: critical work done / bulk update done
   void* coef_buf = nullptr;
   size_t coef_cap = 0;
   cplx* linv = nullptr;
   int64_t linv_cap = 0;
-  cplx* dinv = nullptr;               // 256 x 16 complex: tri_inv_diag16 output
+  cplx* dinv[kCritStreams] = {};      // 256 x 16 complex each: tri_inv_diag16 output, one per stream
+  bool grow_events(size_t nb) {
+    while (ev_col.size() < nb) {
+      cudaEvent_t a, b;
+      if (cudaEventCreateWithFlags(&a, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&b, cudaEventDisableTiming) != cudaSuccess)
+        return false;
+      ev_col.push_back(a);
+      ev_rest.push_back(b);
+    }
+    return true;
+  }
 };
 
 ExecCtx* exec_ctx() {
@@ -127,13 +141,13 @@ ExecCtx* exec_ctx() {
     auto c = std::make_unique<ExecCtx>();
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if (cudaStreamCreateWithPriority(&c->crit, cudaStreamNonBlocking, hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_next, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_rest, cudaEventDisableTiming) != cudaSuccess ||
+    for (int q = 0; q < kCritStreams; ++q)
+      if (cudaStreamCreateWithPriority(&c->crit[q], cudaStreamNonBlocking, hi) != cudaSuccess ||
+          cudaMalloc(&c->dinv[q], sizeof(cplx) * 256 * 16) != cudaSuccess)
+        return nullptr;
+    if (cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) != cudaSuccess ||
-        cudaMalloc(&c->dinv, sizeof(cplx) * 256 * 16) != cudaSuccess)
+        cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) != cudaSuccess)
       return nullptr;
     p = std::move(c);
   }
@@ -491,30 +505,29 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
                         void* d_perm, void* d_tags, void* d_info, void* d_n2x2, void* d_growth, void* d_scale,
                         void* d_asym, void* d_bk_scratch, double pivot_tol, int check_sym, int lookahead,
                         int nwait, const int64_t* h_wait_col, void* const* h_wait_ev, const void* d_check_sym,
-                        void* d_margin, void* stream) {
+                        void* d_margin, const int32_t* h_sched, void* stream) {
   // rest-update tiles above which a column's diagonal BK runs on a 4-CTA cluster (D3M_BKC4_TILES)
   static const int64_t bkc4_tiles = [] {
     const char* e = getenv("D3M_BKC4_TILES");
     return e ? (int64_t)atoll(e) : (int64_t)5000;
   }();
   static const bool trsm_tri = [] { const char* e = getenv("D3M_TRSM_TRI"); return !(e && e[0] == '0'); }();
-  // default: the bulk update starts once the next-column update has finished,
-  // which then has the SMs to itself (D3M_REST_AFTER_NEXT=0: it starts beside it)
-  static const int rest_after_next = [] { const char* e = getenv("D3M_REST_AFTER_NEXT"); return e ? atoi(e) : 1; }();
-  // every column's X panel must fit its half of xbuf: checked before anything is launched
+  // every column's X panel must fit its xbuf slot: checked before anything is launched
+  const int nslots = lookahead ? kXSlots : 1;
+  const int64_t slot_elems = xbuf_elems / nslots;
   for (int j = 0; j < nb; ++j)
-    if (h_panel_rows[j] * h_sizes[j] > (lookahead ? xbuf_elems / 2 : xbuf_elems))
-      return fail(-22, "d3m_block_ldlt_exec: xbuf too small");
+    if (h_panel_rows[j] * h_sizes[j] > slot_elems) return fail(-22, "d3m_block_ldlt_exec: xbuf too small");
+  if (lookahead && !h_sched) return fail(-22, "d3m_block_ldlt_exec: etree schedule missing");
   ExecCtx* ctx = exec_ctx();
   if (!ctx) return fail(-12, "d3m_block_ldlt_exec: stream/event/scratch creation");
   // calls on one device share its streams and buffers: they enqueue one at a
   // time (stream order then keeps their kernels apart)
   std::lock_guard<std::mutex> guard(ctx->mu);
+  if (!ctx->grow_events((size_t)nb)) return fail(-12, "d3m_block_ldlt_exec: event creation");
   int64_t nmax = 0;
   for (int j = 0; j < nb; ++j) nmax = std::max<int64_t>(nmax, h_sizes[j]);
-  // D^-1 coefficients of the current column (3 complex per pivot column);
-  // double-buffered with the column parity like xbuf
-  const size_t coef_bytes = (size_t)2 * 3 * std::max<int64_t>(nmax, 1) * sizeof(cplx);
+  // D^-1 coefficients of the columns in flight (3 complex per pivot column), one ring slot per column
+  const size_t coef_bytes = (size_t)nslots * 3 * std::max<int64_t>(nmax, 1) * sizeof(cplx);
   if (coef_bytes > ctx->coef_cap) {
     if (ctx->coef_buf) cudaFree(ctx->coef_buf);      // synchronising: no earlier call still reads it
     ctx->coef_buf = nullptr;
@@ -536,40 +549,88 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
     }
     linv_use = ctx->linv;
   }
-  // Streams: the caller's stream hands over to a high-priority critical
-  // stream (BK -> L^-1 -> panel GEMM -> D^-1 -> next-column update) and a
-  // low-priority bulk stream (the rest of each column's trailing update).
+  // Streams.  lookahead = 0: everything in order on the caller's stream.
+  // lookahead = 1 (etree-parallel): the critical chain of column j (BK ->
+  // L^-1 -> panel TRSM -> D^-1 -> the "next" update into column j+1) runs on
+  // one of kCritStreams high-priority streams, h_sched[3j] (the stream of
+  // its last child, so a chain stays on one stream and independent subtrees
+  // of the elimination tree overlap); the bulk ("rest") updates of every
+  // column run on ONE low-priority stream in column order, so every target
+  // block receives its updates in ascending source-column order and the
+  // factor is bitwise that of the sequential executor.  Cross-stream
+  // dependencies are events:
+  //   BK(j)        after the bulk update of h_sched[3j+1] = the last column
+  //                k < j-1 whose bulk update writes column j (the side stream
+  //                is ordered, so all earlier ones are done too), and after
+  //                column j-1's critical work when it updates column j;
+  //   next(j)      after the bulk update of h_sched[3j+2] = the last k < j
+  //                whose bulk update writes column j+1 (ascending order);
+  //   TRSM(j)      after the readers of its X ring slot, column j - kXSlots
+  //                (its next and bulk updates);
+  //   rest(j)      after column j's critical work.
+  // Waits a stream already implies (an earlier wait on a later bulk event, or
+  // its own earlier work) are skipped, so a chain-shaped plan (natural order)
+  // enqueues exactly the lookahead-1 pipeline.
   cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
-  cudaStream_t crit = ctx->crit, side = ctx->side;
-  cudaStream_t s0 = lookahead ? crit : user;
+  cudaStream_t side = ctx->side;
+  int rest_waited[kCritStreams];                      // largest bulk-event column each stream has waited on
+  bool used[kCritStreams] = {};
+  for (int q = 0; q < kCritStreams; ++q) rest_waited[q] = -1;
   if (lookahead) {
     cudaEventRecord(ctx->ev_in, user);
-    cudaStreamWaitEvent(crit, ctx->ev_in, 0);
+    for (int q = 0; q < kCritStreams; ++q) cudaStreamWaitEvent(ctx->crit[q], ctx->ev_in, 0);
     cudaStreamWaitEvent(side, ctx->ev_in, 0);
   }
+  std::vector<int> col_stream(nb, 0);
+  std::vector<char> has_rest(nb, 0);
   auto* tasks = static_cast<const d3m::GemmTask*>(d_tasks);
   auto* ttasks = static_cast<const d3m::GemmTask*>(d_trsm_tasks);
   cplx* pool = C(d_pool);
   cplx* binv = C(d_binv);
+  auto wait_rest = [&](int q, cudaStream_t st, int k) {     // stream q waits for the bulk update of column k
+    if (k < 0 || k <= rest_waited[q]) return;
+    // the latest bulk update at or before k that exists (columns without one recorded nothing)
+    while (k >= 0 && !has_rest[k]) --k;
+    if (k < 0 || k <= rest_waited[q]) return;
+    cudaStreamWaitEvent(st, ctx->ev_rest[k], 0);
+    rest_waited[q] = k;
+  };
   // all columns; an early return (a failed launch) still reaches the join below
   auto columns = [&]() -> int {
-    bool rest_pending = false;
     for (int j = 0; j < nb; ++j) {
+      const int q = lookahead ? std::min(std::max(h_sched[3 * j], 0), kCritStreams - 1) : 0;
+      cudaStream_t s0 = lookahead ? ctx->crit[q] : user;
+      col_stream[j] = q;
+      used[q] = true;
       // blocks of K still being uploaded: column j waits for the chunks it is
-      // the first to touch (the side stream follows s0 through ev_next)
+      // the first to touch
       for (int w = 0; w < nwait; ++w)
         if (h_wait_col[w] == j) cudaStreamWaitEvent(s0, static_cast<cudaEvent_t>(h_wait_ev[w]), 0);
+      if (lookahead) {
+        wait_rest(q, s0, h_sched[3 * j + 1]);
+        // column j-1's next update writes column j (j = parent(j-1)): on another stream, wait for it
+        if (j > 0 && h_task_next[j - 1] > h_task_ptr[j - 1] && col_stream[j - 1] != q)
+          cudaStreamWaitEvent(s0, ctx->ev_col[j - 1], 0);
+        // the X / coefficient ring slot of column j was last used by column j - nslots
+        const int o = j - nslots;
+        if (o >= 0) {
+          if (col_stream[o] != q) cudaStreamWaitEvent(s0, ctx->ev_col[o], 0);
+          wait_rest(q, s0, has_rest[o] ? o : -1);
+        }
+      }
       const int nj = (int)h_sizes[j];
       const int64_t R = h_panel_rows[j];
-      cplx* xbuf = C(d_xbuf) + (lookahead ? (j & 1) * (xbuf_elems / 2) : 0);
+      const int slot = j % nslots;
+      cplx* xbuf = C(d_xbuf) + slot * slot_elems;
       int64_t* perm = static_cast<int64_t*>(d_perm) + h_piv_off[j];
       int8_t* tags = static_cast<int8_t*>(d_tags) + h_piv_off[j];
       cplx* diag = pool + h_diag_off[j];
-      cplx* coef = static_cast<cplx*>(ctx->coef_buf) + (size_t)(j & 1) * 3 * nmax;
+      cplx* coef = static_cast<cplx*>(ctx->coef_buf) + (size_t)slot * 3 * nmax;
       d3m::BkArgs a{diag, 0, nj, nj, pivot_tol, check_sym, perm, tags,
                     static_cast<int32_t*>(d_n2x2) + j, static_cast<double*>(d_growth) + j,
                     static_cast<int32_t*>(d_info) + j, static_cast<double*>(d_scale) + j,
-                    static_cast<double*>(d_asym) + j, C(d_bk_scratch)};
+                    static_cast<double*>(d_asym) + j,
+                    d_bk_scratch ? C(d_bk_scratch) + (size_t)q * 4 * nmax : nullptr};
       if (d_check_sym) a.check_sym_dev = static_cast<const int*>(d_check_sym) + j;   // per-block flag (ABI v8)
       if (d_margin) a.margin = static_cast<double*>(d_margin) + 2 * j;               // decision margins (ABI v9)
       if (nj > 0) {
@@ -590,7 +651,7 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
         D3M_TRY(launch(kClsTrsm, s0, [&] {
           // blocked 16 x 16 inverse (n <= 256), else warp per column (n <= 512), else the generic kernel
           cplx* lj = linv_use ? linv_use + h_binv_off[j] : nullptr;   // unpermuted L^-1 for the panel TRSM
-          int rc = d3m_tri_inv_blocked_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, lj, ctx->dinv, s0);
+          int rc = d3m_tri_inv_blocked_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, lj, ctx->dinv[q], s0);
           if (rc == -22) rc = d3m_tri_inv_warp_launch(diag, perm, tags, binv + h_binv_off[j], coef, nj, s0, lj);
           return rc == -22 ? d3m_tri_inv_launch(diag, 0, perm, 0, tags, 0, binv + h_binv_off[j], 0, nj, 1, s0) : rc;
         }));
@@ -610,33 +671,26 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
         }));
       }
       const int64_t t0 = h_task_ptr[j], tn = h_task_next[j], t1 = h_task_ptr[j + 1];
-      // X_j / L_j are ready: the bulk ("rest") update of column j only reads
-      // them and targets columns >= j+2, so it could start now, beside the
-      // "next" update below (disjoint targets); by default it waits for the
-      // next update.  The side stream keeps the rest updates of consecutive
-      // columns in order.
-      if (lookahead && t1 > tn && !rest_after_next) cudaEventRecord(ctx->ev_next, s0);
-      if (rest_pending) {          // next-targets of column j+1 were also rest-targets of j-1
-        cudaStreamWaitEvent(s0, ctx->ev_rest, 0);
-        rest_pending = false;
-      }
-      if (tn > t0)
+      // next update (targets in column j+1): after every earlier bulk update into column j+1
+      if (tn > t0) {
+        if (lookahead) wait_rest(q, s0, h_sched[3 * j + 2]);
         D3M_TRY(launch(kClsGemm, s0, [&] {
           return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + t0, (int)(tn - t0), (int)h_tiles_next[j], s0);
         }));
-      if (lookahead && t1 > tn && rest_after_next) cudaEventRecord(ctx->ev_next, s0);
+      }
+      if (lookahead) cudaEventRecord(ctx->ev_col[j], s0);
+      // the bulk ("rest") update of column j targets columns >= j+2 and only
+      // reads X_j / L_j: it starts once column j's critical work (including
+      // the next update, which then has the SMs to itself) is done
       if (t1 > tn) {
+        cudaStream_t sb = lookahead ? side : s0;
+        if (lookahead) cudaStreamWaitEvent(side, ctx->ev_col[j], 0);
+        D3M_TRY(launch(kClsGemm, sb, [&] {
+          return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], sb);
+        }));
         if (lookahead) {
-          cudaStreamWaitEvent(side, ctx->ev_next, 0);
-          D3M_TRY(launch(kClsGemm, side, [&] {
-            return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], side);
-          }));
-          cudaEventRecord(ctx->ev_rest, side);
-          rest_pending = true;
-        } else {
-          D3M_TRY(launch(kClsGemm, s0, [&] {
-            return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], s0);
-          }));
+          cudaEventRecord(ctx->ev_rest[j], side);
+          has_rest[j] = 1;
         }
       }
     }
@@ -647,10 +701,13 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
   // everything enqueued on the critical and bulk streams, so buffers it frees
   // after a raised error are not still in use
   if (lookahead) {
-    cudaEventRecord(ctx->ev_rest, side);
-    cudaStreamWaitEvent(crit, ctx->ev_rest, 0);
-    cudaEventRecord(ctx->ev_out, crit);
+    cudaEventRecord(ctx->ev_out, side);
     cudaStreamWaitEvent(user, ctx->ev_out, 0);
+    for (int q = 0; q < kCritStreams; ++q)
+      if (used[q]) {
+        cudaEventRecord(ctx->ev_out, ctx->crit[q]);
+        cudaStreamWaitEvent(user, ctx->ev_out, 0);
+      }
   }
   if (rc != 0) return rc;
   const cudaError_t e = cudaGetLastError();

@@ -343,7 +343,9 @@ class _Schedule:
         self.tiles_next = tiles_n
         self.tiles_rest = tiles_r
         self.d_tasks = upload_bytes(tasks) if len(tasks) else t.zeros(64, dtype=t.uint8, device="cuda")
-        self.xbuf_elems = 2 * max(1, int((self.panel_rows * sizes).max()) if nb else 1)
+        # X panels of the columns in flight: a ring of 4 slots (d3m_capi.cu kXSlots)
+        self.xbuf_elems = 4 * max(1, int((self.panel_rows * sizes).max()) if nb else 1)
+        self.etree_sched = planner.etree_schedule(plan.etree_parent, pattern)
         # block_solve backward gather: global plan-order rows of every panel
         gidx, gptr = [], [0]
         for j in range(nb):
@@ -840,7 +842,7 @@ def _block_ldlt_run(K, plan, pivot_tol, lookahead, margins, sched, pool, flag, s
     xbuf = empty(sched.xbuf_elems)
     binv = empty(max(int(sched.binv_off[-1]), 1))
     nmax = int(sched.sizes.max())
-    scratch = empty(4 * nmax) if 64 * nmax > 200 * 1024 else None
+    scratch = empty(4 * 4 * nmax) if 64 * nmax > 200 * 1024 else None      # one per critical stream
     mg = t.empty((nb, 2), dtype=t.float64, device="cuda") if margins else None
     H = _lib.hptr
     _lib.call("d3m_block_ldlt_exec", nb, H(sched.sizes), H(sched.diag_off), H(sched.panel_off),
@@ -848,7 +850,8 @@ def _block_ldlt_run(K, plan, pivot_tol, lookahead, margins, sched, pool, flag, s
               H(sched.tiles_next), H(sched.tiles_rest), H(sched.tiles_trsm), _P(sched.d_tasks),
               _P(sched.d_trsm_tasks), _P(pool), _P(binv), _P(xbuf), sched.xbuf_elems, _P(perm), _P(tags),
               _P(info), _P(n2), _P(gr), _P(sc), _P(asy), _P(scratch), float(pivot_tol), check_sym,
-              int(bool(lookahead)), nwait, H(wait_cols), H(wait_ev), _P(flag), _P(mg), stream_ptr())
+              int(bool(lookahead)), nwait, H(wait_cols), H(wait_ev), _P(flag), _P(mg), H(sched.etree_sched),
+              stream_ptr())
     info_h = info.cpu().numpy()
     bad = np.flatnonzero(info_h != -1)
     if bad.size:

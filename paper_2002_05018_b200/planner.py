@@ -76,3 +76,43 @@ def flow_items(sizes, pattern, panel_rows):
     if rc != 0:
         raise RuntimeError(f"d3m_plan_flow_items returned {rc}")
     return items, deps, part_off, int(out[2]), int(out[3])
+
+
+N_CRIT_STREAMS = 4          # d3m_capi.cu kCritStreams
+
+
+def etree_schedule(parent, pattern, nstreams: int = N_CRIT_STREAMS) -> np.ndarray:
+    """Per block column j (plan order) the int32 triple the etree-parallel
+    executor (include/d3m.h d3m_block_ldlt_exec, h_sched) needs:
+
+    * the critical stream: the stream of j's last child, so a chain of the
+      elimination tree stays on one stream; a leaf takes the stream whose
+      last column is the oldest, so independent subtrees spread out;
+    * the last column k < j whose bulk ("rest") update writes column j:
+      max{k : j in pattern(k), j != k + 1} (-1: none; column k+1 is
+      written by k's "next" update instead);
+    * the last column k < j whose bulk update writes column j+1.
+    """
+    nb = len(pattern)
+    out = np.full((max(nb, 1), 3), -1, dtype=np.int32)
+    last_child = np.full(max(nb, 1), -1, dtype=np.int64)
+    for j in range(nb):
+        p = int(parent[j])
+        if p >= 0:
+            last_child[p] = max(last_child[p], j)
+    last_use = np.full(nstreams, -1, dtype=np.int64)
+    dep = np.full(nb + 1, -1, dtype=np.int64)          # last rest-writer seen so far, per target column
+    for j in range(nb):
+        c = int(last_child[j])
+        q = int(out[c, 0]) if c >= 0 else int(np.argmin(last_use))
+        out[j, 0] = q
+        last_use[q] = j
+        out[j, 1] = dep[j]
+        out[j, 2] = dep[j + 1] if j + 1 <= nb else -1
+        for t in pattern[j]:
+            t = int(t)
+            if t != j + 1:
+                dep[t] = j
+    if nb == 0:
+        out[0] = (0, -1, -1)
+    return np.ascontiguousarray(out.reshape(-1))

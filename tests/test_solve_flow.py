@@ -109,3 +109,22 @@ def test_flow_list_random_plans(seed):
     g = clique_graph(K)
     for order in (reorder(g, K.sizes), identity_ordering(K.nblocks)):
         _check(symbolic_factor(g, order, K.sizes))
+
+
+def test_etree_schedule_dependencies():
+    """planner.etree_schedule: a chain stays on one stream; in a forest the
+    leaves of different subtrees take different streams; the recorded bulk
+    writers are the last earlier columns whose pattern holds the column."""
+    from paper_2002_05018_b200 import planner
+    parent = np.array([1, 2, 3, -1])
+    pattern = [np.array([1, 3]), np.array([2, 3]), np.array([3]), np.array([], dtype=np.int64)]
+    s = planner.etree_schedule(parent, pattern).reshape(-1, 3)
+    assert set(s[:, 0]) == {0}
+    assert list(s[:, 1]) == [-1, -1, -1, 1]          # column 3: written by the rest updates of 0 and 1
+    assert list(s[:, 2]) == [-1, -1, 1, -1]          # column 2 updates 3 after 1's rest update
+    parent = np.array([2, 2, 5, 5, 5, -1])            # subtrees {0,1,2} and {3,4}
+    pattern = [np.array([2, 5]), np.array([2]), np.array([5]), np.array([5]), np.array([5]),
+               np.array([], dtype=np.int64)]
+    s = planner.etree_schedule(parent, pattern).reshape(-1, 3)
+    assert s[0, 0] != s[1, 0] and s[2, 0] == s[1, 0] and s[3, 0] != s[2, 0]
+    assert s[5, 1] == 3                               # 4 -> 5 is a next update; 3 is the last rest writer
