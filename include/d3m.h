@@ -188,8 +188,9 @@ int d3m_modulus_probe(const void* z, void* hyp, void* npabs, int64_t n, void* st
  * column j / column j+1 (-1: none), the events column j's BK / its update
  * of column j+1 wait for (planner.etree_schedule).
  * nwait / h_wait_col / h_wait_ev (ABI v6; 0 / NULL / NULL = none): cudaEvent_t
- * handles; before column h_wait_col[w] the critical stream waits on
- * h_wait_ev[w] (blocks of K still being uploaded on a copy stream).
+ * handles, h_wait_col ascending; a stream about to run a column >=
+ * h_wait_col[w] first waits on h_wait_ev[w] (blocks of K still being
+ * uploaded on a copy stream).
  * d_check_sym (ABI v8; NULL = use check_sym): nb int32 device flags, column
  * j's BK reads d_check_sym[j] (d3m_diag_sym_flags) instead of check_sym. */
 int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_off, const int64_t* h_panel_off,

@@ -574,6 +574,7 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
   cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
   cudaStream_t side = ctx->side;
   int rest_waited[kCritStreams];                      // largest bulk-event column each stream has waited on
+  int chunk_waited[kCritStreams] = {};                // upload chunks each stream has waited on
   bool used[kCritStreams] = {};
   for (int q = 0; q < kCritStreams; ++q) rest_waited[q] = -1;
   if (lookahead) {
@@ -602,10 +603,11 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
       cudaStream_t s0 = lookahead ? ctx->crit[q] : user;
       col_stream[j] = q;
       used[q] = true;
-      // blocks of K still being uploaded: column j waits for the chunks it is
-      // the first to touch
-      for (int w = 0; w < nwait; ++w)
-        if (h_wait_col[w] == j) cudaStreamWaitEvent(s0, static_cast<cudaEvent_t>(h_wait_ev[w]), 0);
+      // blocks of K still being uploaded: before column j its stream waits
+      // for every chunk first touched at or before column j that it has not
+      // waited for yet (the chunks' columns ascend)
+      while (chunk_waited[q] < nwait && h_wait_col[chunk_waited[q]] <= j)
+        cudaStreamWaitEvent(s0, static_cast<cudaEvent_t>(h_wait_ev[chunk_waited[q]++]), 0);
       if (lookahead) {
         wait_rest(q, s0, h_sched[3 * j + 1]);
         // column j-1's next update writes column j (j = parent(j-1)): on another stream, wait for it
