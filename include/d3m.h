@@ -39,6 +39,9 @@ const char* d3m_last_error(void);
  * Outputs per matrix: perm[n] int64, tags[n] int8, n2x2 int32, growth f64,
  * info int32, scale f64, asym f64.  scratch: batch*4*n complex, needed only
  * when 64*n bytes exceed the shared-memory staging (n > 3200).
+ * check_sym bit 2 (value 4, ABI v9): pivot_tol is the absolute threshold
+ * itself (kernels.bk_factor(W, tol_abs) semantics); otherwise the threshold
+ * is pivot_tol * scale.  Bits 0-1: 0 no symmetry check, 1 numpy-style check.
  * margin (ABI v9; NULL = not tracked): batch x 2 f64 pivot-decision
  * diagnostics -- [0] the minimum over all steps of the relative distance of
  * every evaluated BK test (kernels.py:59-77: singularity, alpha colmax,

@@ -297,7 +297,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     cl.sync();
     return;
   }
-  const double tol_abs = __dmul_rn(a.pivot_tol, scale);
+  const double tol_abs = bk_threshold(a.pivot_tol, scale, a.abs_tol);
   constexpr bool track = TRACK;                // pivot-decision margins (lead thread)
   double mdec = 1.0, mgap = 1.0;
   // growth recurrence (kernels.py:135-144), run by gthread only: a step's

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(NT) bk_exact_kernel(BkArgs a, int use_smem) {
     }
     return;
   }
-  const double tol_abs = __dmul_rn(a.pivot_tol, scale);
+  const double tol_abs = bk_threshold(a.pivot_tol, scale, a.abs_tol);
   double trail_max = __dsqrt_rn(tm2);
   double growth = 1.0;
   int n2x2 = 0, info = -1;

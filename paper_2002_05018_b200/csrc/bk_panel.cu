@@ -136,7 +136,7 @@ __global__ void bk_panel_state_kernel(BkArgs a, BkState* st, const unsigned long
   s.info = (a.check_sym && a.n > 0 && scale > 0.0 && asym > __dmul_rn(1e-12, scale)) ? -2 : -1;
   s.trail_max = sqrt(as_pos(rb[2]));
   s.growth = 1.0;
-  s.tol_abs = __dmul_rn(a.pivot_tol, scale);
+  s.tol_abs = bk_threshold(a.pivot_tol, scale, a.abs_tol);
   s.scale = scale;
   s.asym = asym;
   s.mdec = 1.0f;

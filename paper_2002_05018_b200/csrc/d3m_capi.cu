@@ -172,10 +172,13 @@ int d3m_bk_factor_batched(int batch, int n, void* W, int64_t stride_w, int lda, 
                           void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
                           void* scratch, void* margin, void* stream) {
   if (batch < 0 || n < 0 || lda < n) return fail(-22, "d3m_bk_factor_batched: bad shape");
+  const bool abs_tol = (check_sym & 4) != 0;
+  check_sym &= 3;
   d3m::BkArgs a{C(W), stride_w, n, lda, pivot_tol, check_sym, static_cast<int64_t*>(perm), static_cast<int8_t*>(tags),
                 static_cast<int32_t*>(n2x2), static_cast<double*>(growth), static_cast<int32_t*>(info),
                 static_cast<double*>(scale), static_cast<double*>(asym), C(scratch)};
   a.margin = static_cast<double*>(margin);
+  a.abs_tol = abs_tol;
   D3M_TRY(launch(kClsBk, stream, [&] { return d3m_bk_launch(&a, batch, stream); }));
   return 0;
 }

@@ -191,6 +191,15 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// Pivot threshold of a BK factorisation: pivot_tol * scale (factor.py:99,
+// scale = np.abs(W).max() computed on the device), or pivot_tol itself when
+// it is an absolute threshold (BkArgs::abs_tol: kernels.bk_factor(W, tol_abs)
+// bindings pass the caller's tol_abs unchanged instead of round-tripping it
+// through tol_abs / scale * scale, which can move it by an ulp).
+__device__ __forceinline__ double bk_threshold(double pivot_tol, double scale, bool abs_tol) {
+  return abs_tol ? pivot_tol : __dmul_rn(pivot_tol, scale);
+}
+
 // ---- pivot-decision margins (diagnostic, BkArgs::margin) --------------------
 // Relative distance of a pivot test "lhs >= rhs" (kernels.py:59-77) to its
 // threshold: |lhs - rhs| / max(lhs, rhs); 1 when both sides are 0.  A kernel

@@ -27,6 +27,7 @@ struct BkArgs {
   // decision_margin over all steps, [1] the minimum argmax_gap of the colmax
   // searches (d3m_common.cuh); nullptr = not tracked
   double* margin = nullptr;
+  bool abs_tol = false;               // pivot_tol is the absolute threshold (d3m_bk_factor_batched check_sym bit 2)
 };
 
 // Device-resident plan of the persistent block solve (skinny_dmma.cu)

@@ -102,10 +102,13 @@ _FP_MAX_BYTES = 256 << 20
 
 def _fingerprint(a):
     """CRC-32 of a host array's bytes (numpy, CPU tensor or SparseBlock), or
-    None for device arrays and arrays above _FP_MAX_BYTES: recover_primal
-    reuses X = A^-1 [D | F] only while the loads and couplings it was formed
-    from are unchanged (identity AND content, so in-place edits are seen);
-    device and very large couplings are checked by identity only."""
+    None for device arrays and arrays above _FP_MAX_BYTES.  recover_primal
+    reuses X = A^-1 [D | F] only while the loads it was formed from are the
+    same objects with the same content (an in-place edit of f, e.g. a new
+    excitation, is seen) and the couplings are the same objects.  Couplings
+    are not content-hashed: they are geometry (config 5 carries 1.9 GB of
+    them, ~0.4 s of CRC per call) and must not be edited in place after
+    reduce_domains -- reduce again instead."""
     if isinstance(a, SparseBlock):
         if a.keys.nbytes + a.vals.nbytes > _FP_MAX_BYTES:
             return None
@@ -319,8 +322,7 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, marg
         else:
             s._d3m_X = wx[i]
             s._d3m_Xm = m
-            s._d3m_src = (s.f, tuple(c.D for c in s.couplings), _fingerprint(s.f),
-                          tuple(_fingerprint(c.D) for c in s.couplings))
+            s._d3m_src = (s.f, tuple(c.D for c in s.couplings), _fingerprint(s.f))
         if keep in ("factor", "schur"):
             s.factor = facs[i]
             s._d3m_D = D[i, :, :mr]
@@ -536,8 +538,7 @@ def _local_E(systems, lam):
         src = getattr(s, "_d3m_src", None)
         return (getattr(s, "_d3m_X", None) is not None and src is not None and src[0] is s.f
                 and len(src[1]) == len(s.couplings) and all(a is c.D for a, c in zip(src[1], s.couplings))
-                and src[2] == _fingerprint(s.f)
-                and all(fp == _fingerprint(c.D) for fp, c in zip(src[3], s.couplings)))
+                and src[2] == _fingerprint(s.f))
 
     use_x = []
     for s in systems:

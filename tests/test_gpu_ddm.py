@@ -276,3 +276,25 @@ def test_nonzero_rows_vs_numpy(cuda, n, m, B):
         want = np.full(mx, -1, dtype=np.int64)
         want[:len(expect[b])] = expect[b]
         assert np.array_equal(got[b], want), b
+
+
+def test_recover_sees_in_place_load_edits(cuda):
+    """recover_primal reuses X = A^-1 [D | F] only while the loads are
+    unchanged: an in-place edit of f (same object) falls back to the factor
+    solve and gives the recovery of the new load."""
+    import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import workloads as wl
+    systems, part, _ = wl.synthetic_d3m((2, 2, 1), 10, 4, 3)
+    red = d.reduce_domains(systems, keep="factor")
+    R = d.assemble_reduced(red, part)
+    gr = d.clique_graph(R.K)
+    F = d.block_ldlt(R.K, d.symbolic_factor(gr, d.reorder(gr, R.K.sizes), R.K.sizes))
+    lam = d.block_solve(F, R.g)
+    before = np.asarray(d.recover_primal(systems, lam))
+    systems[1].f[:] *= 2.0                       # in place: same object, new content
+    after = np.asarray(d.recover_primal(systems, lam))
+    fresh = [d.SubdomainSystem(s.domain, s.A, s.f.copy(), s.dof_map, s.couplings) for s in systems]
+    d.reduce_domains(fresh, keep="factor")
+    want = np.asarray(d.recover_primal(fresh, lam))
+    assert not np.allclose(after, before)
+    assert np.linalg.norm(after - want) <= 1e-10 * np.linalg.norm(want)

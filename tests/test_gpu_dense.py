@@ -157,3 +157,41 @@ def test_deterministic(cuda):
     assert np.array_equal(a.packed.cpu().numpy(), b.packed.cpu().numpy())
     B = np.ones((150, 3), dtype=complex)
     assert np.array_equal(a.solve(B), b.solve(B))
+
+
+def test_bk_factor_binding_with_absolute_threshold(cuda, oracle):
+    """The kernels.bk_factor(W, tol_abs) binding of INTEGRATION.md: check_sym
+    bit 2 makes pivot_tol the absolute threshold, so a threshold placed
+    exactly at a column maximum (where tol_abs / scale * scale could move by
+    an ulp) decides like the reference: info and pivots equal the oracle's."""
+    import torch
+    from paper_2002_05018_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(77)
+    n = 40
+    G = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    M = (G + G.T) / 2
+    M[20:, 20:] *= 1e-9                               # a numerically small trailing block
+    W0 = np.ascontiguousarray(M)
+    Wo = W0.copy()
+    ref = oracle.bk_factor(Wo, 0.0)
+    for tol_abs in (0.0, 1e-12, np.abs(Wo[25:, 25]).max(), 1e-7, 10.0):
+        Wo = W0.copy()
+        want = oracle.bk_factor(Wo, float(tol_abs))
+        d = torch.from_numpy(W0.copy()).cuda()
+        perm = torch.empty(n, dtype=torch.int64, device="cuda")
+        tags = torch.empty(n, dtype=torch.int8, device="cuda")
+        i32 = lambda: torch.empty(1, dtype=torch.int32, device="cuda")
+        f64 = lambda: torch.empty(1, dtype=torch.float64, device="cuda")
+        n2, info, gr, sc, asy = i32(), i32(), f64(), f64(), f64()
+        P = _lib.ctypes.c_void_p
+        rc = lib.d3m_bk_factor_batched(1, n, P(d.data_ptr()), n * n, n, float(tol_abs), 4, P(perm.data_ptr()),
+                                       P(tags.data_ptr()), P(n2.data_ptr()), P(gr.data_ptr()), P(info.data_ptr()),
+                                       P(sc.data_ptr()), P(asy.data_ptr()), None, None,
+                                       P(torch.cuda.current_stream().cuda_stream))
+        assert rc == 0
+        assert int(info.item()) == want[4], tol_abs
+        if want[4] < 0:
+            assert np.array_equal(perm.cpu().numpy(), want[0]) and np.array_equal(tags.cpu().numpy(), want[1])
+            assert np.array_equal(np.tril(d.cpu().numpy()), np.tril(Wo))
+    assert ref[4] == -1
