@@ -19,13 +19,14 @@
 #include <vector>
 
 #include "d3m_gemm.h"
+#include "../../include/d3m.h"
 
 namespace {
 
 constexpr int kBM = 64;                   // GEMM output tile (zgemm_dmma.cu)
 constexpr int kKCH = 256;                 // backward split-K chunk (panel rows), skinny_dmma.cu
 constexpr int kFdRows = 32, kBrRows = 16;  // rows per D^-1 / reduce work item
-enum { FA = 0, FD = 1, FB = 2, BC = 3, BR = 4, BE = 5 };   // skinny_dmma.cu FlowItem types
+enum { FA = 0, FD = 1, FB = 2, BC = 3, BR = 4, BE = 5, FA2 = 6, BE2 = 7 };   // skinny_dmma.cu FlowItem types
 
 struct Pattern {
   int nb;
@@ -72,9 +73,10 @@ extern "C" {
 // the "next" group), tiles_next[nb], tiles_rest[nb].  flops[0] = the
 // algorithmic update flops (8 n_i n_k n_j, 4 n_i^2 n_j for diagonal targets).
 int64_t d3m_plan_gemm_tasks(int nb, const int64_t* sizes, const int64_t* pat_ptr, const int64_t* pat_idx,
-                            const int64_t* diag_off, const int64_t* panel_off, d3m::GemmTask* tasks, int64_t cap,
+                            const int64_t* diag_off, const int64_t* panel_off, void* tasks_v, int64_t cap,
                             int64_t* task_ptr, int64_t* task_next, int64_t* tiles_next, int64_t* tiles_rest,
                             int64_t* flops) {
+  auto* tasks = static_cast<d3m::GemmTask*>(tasks_v);
   const Pattern P{nb, sizes, pat_ptr, pat_idx};
   const std::vector<int64_t> prow = panel_row_offsets(P);
   int64_t count = 0, fl = 0;
@@ -156,9 +158,18 @@ int64_t d3m_plan_gemm_tasks(int nb, const int64_t* sizes, const int64_t* pat_ptr
 // count only).  out[0..3] = item count, dependency count, counter count
 // (+1 for the queue head), partial-sum elements; part_off[nb] (>= 1 entry).
 // Returns 0, or -2 when a capacity is too small.
+//
+// fold != 0 (parent[nb] = elimination-tree parents): the chain-folded list.
+// The update of the parent block p by its last child c is folded into p's
+// z tiles (FA2: z_p = Binv_p b_p - G_c z_c with G_c = Binv_p L_pc, built by
+// the solve's precompute), and the parent term of every column's backward
+// sum into its x tiles (BE2: x_j = Binv_j^T w_j - H_j^T x_p with H_j =
+// L_pj Binv_j); the split-K chunks of column j then start after the parent
+// block (row n_p of the panel).  Each block column's critical chain is one
+// item per sweep instead of a z -> update -> z hand-off.
 int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, const int64_t* pat_idx,
                         const int64_t* panel_rows, int32_t* items, int64_t cap_items, int32_t* deps,
-                        int64_t cap_deps, int64_t* part_off, int64_t* out) {
+                        int64_t cap_deps, int64_t* part_off, int64_t* out, int fold, const int64_t* parent) {
   const Pattern P{nb, sizes, pat_ptr, pat_idx};
   const std::vector<int64_t> prow = panel_row_offsets(P);
   std::vector<int64_t> T(nb);
@@ -209,9 +220,15 @@ int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, co
   };
 
   // ---- forward -------------------------------------------------------------
+  std::vector<int> last_child(nb, -1);                  // folded child of each block (fold mode)
+  if (fold && parent)
+    for (int j = 0; j < nb; ++j)
+      if (parent[j] >= 0) last_child[parent[j]] = std::max(last_child[parent[j]], j);
+  auto folded = [&](int j, int i) { return fold && last_child[i] == j; };   // update j -> i folded away
   std::vector<int64_t> n_into(nb, 0);                   // FB tile items into each block
   for (int j = 0; j < nb; ++j)
-    for (int a = 0; a < P.len(j); ++a) n_into[P.at(j, a)] += T[P.at(j, a)];
+    for (int a = 0; a < P.len(j); ++a)
+      if (!folded(j, P.at(j, a))) n_into[P.at(j, a)] += T[P.at(j, a)];
   std::vector<int64_t> seq_k(seq_base[nb] - seq_base[0], 0);
   auto update = [&](int j, int i) {
     const int64_t rp = P.rowpos(j, i, prow);
@@ -232,9 +249,16 @@ int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, co
   };
   for (int j = 0; j < nb; ++j) {
     if (P.size(j)) {
+      const int c = last_child[j];
       for (int64_t t = 0; t < T[j]; ++t) {
-        if (n_into[j]) add(FA, j, t, 0, {{BLK + j, n_into[j]}}, ZC + j, -1);
-        else add(FA, j, t, 0, {}, ZC + j, -1);
+        if (c >= 0) {
+          if (n_into[j]) add(FA2, j, t, 0, {{BLK + j, n_into[j]}, {ZC + c, T[c]}}, ZC + j, -1);
+          else add(FA2, j, t, 0, {{ZC + c, T[c]}}, ZC + j, -1);
+        } else if (n_into[j]) {
+          add(FA, j, t, 0, {{BLK + j, n_into[j]}}, ZC + j, -1);
+        } else {
+          add(FA, j, t, 0, {}, ZC + j, -1);
+        }
       }
       for (int64_t r0 = 0; r0 < P.size(j); r0 += kFdRows)
         add(FD, j, r0, std::min<int64_t>(P.size(j), r0 + kFdRows), {{ZC + j, T[j]}}, UC + j, -1);
@@ -242,7 +266,7 @@ int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, co
     if (P.len(j)) {
       const int par = P.at(j, 0);
       flush(par, -1);
-      update(j, par);
+      if (!folded(j, par)) update(j, par);
     }
     if (j >= 1)
       for (int a = 1; a < P.len(j - 1); ++a) flush(P.at(j - 1, a), j - 1);
@@ -251,12 +275,17 @@ int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, co
   for (int i = 0; i < nb; ++i) flush(i, -1);
 
   // ---- backward ------------------------------------------------------------
-  std::vector<int64_t> nch(nb);
-  for (int j = 0; j < nb; ++j) nch[j] = (panel_rows[j] + kKCH - 1) / kKCH;
+  // fold: column j's split-K chunks start after its parent block (rows
+  // [0, n_p) of the panel), whose term the fused BE2 item adds
+  std::vector<int64_t> nch(nb), coff(nb, 0);
+  for (int j = 0; j < nb; ++j) {
+    if (fold && parent && parent[j] >= 0) coff[j] = P.size((int)parent[j]);
+    nch[j] = (panel_rows[j] - coff[j] + kKCH - 1) / kKCH;
+  }
   // blocks of pattern(j) overlapping panel rows of chunk ch (non-empty blocks)
   auto chunk_blocks = [&](int j, int64_t ch, std::vector<int>& out_blocks) {
     out_blocks.clear();
-    const int64_t lo = ch * kKCH, hi = std::min<int64_t>(panel_rows[j], ch * kKCH + kKCH);
+    const int64_t lo = coff[j] + ch * kKCH, hi = std::min<int64_t>(panel_rows[j], coff[j] + ch * kKCH + kKCH);
     for (int a = 0; a < P.len(j); ++a) {
       const int i = P.at(j, a);
       const int64_t r = prow[P.ptr[j] + a];
@@ -292,7 +321,11 @@ int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, co
     for (int64_t pc = 0; pc < npc; ++pc)
       add(BR, j, kBrRows * pc, std::min<int64_t>(P.size(j), kBrRows * pc + kBrRows),
           {{CC + j, nch[j] * T[j]}, {UC + j, nfd}}, RC + j, -1);
-    for (int64_t t = 0; t < T[j]; ++t) add(BE, j, t, 0, {{RC + j, npc}}, XC + j, -1);
+    const bool be2 = fold && parent && parent[j] >= 0;
+    for (int64_t t = 0; t < T[j]; ++t) {
+      if (be2) add(BE2, j, t, 0, {{RC + j, npc}, {XC + parent[j], T[parent[j]]}}, XC + j, -1);
+      else add(BE, j, t, 0, {{RC + j, npc}}, XC + j, -1);
+    }
     if (j >= 1 && P.size(j - 1) && !done_far[j - 1]) {
       chunks(j - 1, true);
       done_far[j - 1] = 1;

@@ -6,12 +6,12 @@ from __future__ import annotations
 
 import numpy as np
 
-_FA, _FB, _FD, _BC, _BR, _BE = 0, 2, 1, 3, 4, 5      # skinny_dmma.cu FlowItem types
+_FA, _FB, _FD, _BC, _BR, _BE, _FA2, _BE2 = 0, 2, 1, 3, 4, 5, 6, 7      # skinny_dmma.cu FlowItem types
 _KCH = 256
 _FD_ROWS, _BR_ROWS = 32, 16
 
 
-def flow_items_ref(sizes, pattern, panel_rows):
+def flow_items_ref(sizes, pattern, panel_rows, fold=False, parent=None):
     """Host part of _solve_flow (pure numpy; tests/test_solve_flow.py checks
     that the list is a topological order).  Returns (items int32 [n, 8],
     deps int32 [m, 2], part_off int64 [nb], counter count, partial elems)."""
@@ -34,10 +34,20 @@ def flow_items_ref(sizes, pattern, panel_rows):
         items.append((typ, j, p0, p1, len(deps), len(dl), inc0, inc1))
         deps.extend(dl)
 
+    last_child = [-1] * nb
+    if fold:
+        for j in range(nb):
+            if parent[j] >= 0:
+                last_child[int(parent[j])] = max(last_child[int(parent[j])], j)
+
+    def folded(j, i):
+        return fold and last_child[i] == j
+
     n_into = [0] * nb                                  # FB tile items into each block
     for j in range(nb):
         for i in pat[j]:
-            n_into[i] += T[i]
+            if not folded(j, i):
+                n_into[i] += T[i]
     seq_k = [[0] * T[i] for i in range(nb)]
 
     def update(j, i):
@@ -55,14 +65,20 @@ def flow_items_ref(sizes, pattern, panel_rows):
 
     for j in range(nb):
         if sizes[j]:
+            c = last_child[j]
             for t in range(T[j]):
-                add(_FA, j, t, 0, [(BLK + j, n_into[j])] if n_into[j] else [], ZC + j)
+                dl = [(BLK + j, n_into[j])] if n_into[j] else []
+                if c >= 0:
+                    add(_FA2, j, t, 0, dl + [(ZC + c, T[c])], ZC + j)
+                else:
+                    add(_FA, j, t, 0, dl, ZC + j)
             for r0 in range(0, sizes[j], _FD_ROWS):
                 add(_FD, j, r0, min(sizes[j], r0 + _FD_ROWS), [(ZC + j, T[j])], UC + j)
         if pat[j]:
             par = pat[j][0]
             flush(par)
-            update(j, par)
+            if not folded(j, par):
+                update(j, par)
         if j >= 1:
             for i in pat[j - 1][1:]:
                 flush(i, upto=j - 1)
@@ -71,10 +87,11 @@ def flow_items_ref(sizes, pattern, panel_rows):
     for i in range(nb):
         flush(i)
     # backward
-    nch = [(int(panel_rows[j]) + _KCH - 1) // _KCH for j in range(nb)]
+    coff = [sizes[int(parent[j])] if fold and parent[j] >= 0 else 0 for j in range(nb)]
+    nch = [(int(panel_rows[j]) - coff[j] + _KCH - 1) // _KCH for j in range(nb)]
 
     def chunk_blocks(j, ch):
-        lo, hi = ch * _KCH, min(int(panel_rows[j]), ch * _KCH + _KCH)
+        lo, hi = coff[j] + ch * _KCH, min(int(panel_rows[j]), coff[j] + ch * _KCH + _KCH)
         return [i for i in pat[j] if prow[j][i] < hi and prow[j][i] + sizes[i] > lo and sizes[i]]
 
     def parent_chunk(j, ch):
@@ -101,7 +118,11 @@ def flow_items_ref(sizes, pattern, panel_rows):
             add(_BR, j, _BR_ROWS * pc, min(sizes[j], _BR_ROWS * pc + _BR_ROWS), [(CC + j, nch[j] * T[j]), (UC + j, nfd)],
                 RC + j)
         for t in range(T[j]):
-            add(_BE, j, t, 0, [(RC + j, npc)], XC + j)
+            if fold and parent[j] >= 0:
+                p = int(parent[j])
+                add(_BE2, j, t, 0, [(RC + j, npc), (XC + p, T[p])], XC + j)
+            else:
+                add(_BE, j, t, 0, [(RC + j, npc)], XC + j)
         if j >= 1 and sizes[j - 1] and not done_far[j - 1]:
             chunks(j - 1, True)
             done_far[j - 1] = True
