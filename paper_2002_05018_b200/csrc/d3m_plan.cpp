@@ -161,12 +161,15 @@ int64_t d3m_plan_gemm_tasks(int nb, const int64_t* sizes, const int64_t* pat_ptr
 //
 // fold != 0 (parent[nb] = elimination-tree parents): the chain-folded list.
 // The update of the parent block p by its last child c is folded into p's
-// z tiles (FA2: z_p = Binv_p b_p - G_c z_c with G_c = Binv_p L_pc, built by
-// the solve's precompute), and the parent term of every column's backward
-// sum into its x tiles (BE2: x_j = Binv_j^T w_j - H_j^T x_p with H_j =
-// L_pj Binv_j); the split-K chunks of column j then start after the parent
-// block (row n_p of the panel).  Each block column's critical chain is one
-// item per sweep instead of a z -> update -> z hand-off.
+// z tiles: FA(p) forms Binv_p b_p from the other updates early, then FA2(p)
+// subtracts G_c z_c (G_c = Binv_p L_pc, built by the solve's precompute) as
+// soon as z_c is known.  Backward, BE(j) forms Binv_j^T w_j without the
+// parent term and BE2(j) subtracts H_j^T x_p (H_j = L_pj Binv_j) once x_p is
+// known; column j's split-K chunks then start after the parent block (row
+// n_p of the panel).  The critical chain of a block column is one K = n
+// tile product per sweep instead of z -> update -> z (forward) and
+// partial -> reduce -> x (backward).  Extra counters: ZA (Binv_p b_p done),
+// XA (Binv_j^T w_j done).
 int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, const int64_t* pat_idx,
                         const int64_t* panel_rows, int32_t* items, int64_t cap_items, int32_t* deps,
                         int64_t cap_deps, int64_t* part_off, int64_t* out, int fold, const int64_t* parent) {
@@ -175,9 +178,9 @@ int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, co
   std::vector<int64_t> T(nb);
   for (int j = 0; j < nb; ++j) T[j] = (P.size(j) + 15) / 16;
   const int64_t ZC = 0, BLK = nb, UC = 2 * (int64_t)nb, CC = 3 * (int64_t)nb, RC = 4 * (int64_t)nb,
-                XC = 5 * (int64_t)nb;
+                XC = 5 * (int64_t)nb, ZA = 6 * (int64_t)nb, XA = 7 * (int64_t)nb;
   std::vector<int64_t> seq_base(nb + 1);
-  seq_base[0] = 6 * (int64_t)nb;
+  seq_base[0] = (fold ? 8 : 6) * (int64_t)nb;
   for (int j = 0; j < nb; ++j) seq_base[j + 1] = seq_base[j] + T[j];
   const int64_t ncnt = seq_base[nb] + 1;            // + queue head
   int64_t ni = 0, nd = 0;
@@ -250,16 +253,13 @@ int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, co
   for (int j = 0; j < nb; ++j) {
     if (P.size(j)) {
       const int c = last_child[j];
+      const int64_t zinc = c >= 0 ? ZA + j : ZC + j;     // folded: z_j is done after FA2
       for (int64_t t = 0; t < T[j]; ++t) {
-        if (c >= 0) {
-          if (n_into[j]) add(FA2, j, t, 0, {{BLK + j, n_into[j]}, {ZC + c, T[c]}}, ZC + j, -1);
-          else add(FA2, j, t, 0, {{ZC + c, T[c]}}, ZC + j, -1);
-        } else if (n_into[j]) {
-          add(FA, j, t, 0, {{BLK + j, n_into[j]}}, ZC + j, -1);
-        } else {
-          add(FA, j, t, 0, {}, ZC + j, -1);
-        }
+        if (n_into[j]) add(FA, j, t, 0, {{BLK + j, n_into[j]}}, zinc, -1);
+        else add(FA, j, t, 0, {}, zinc, -1);
       }
+      if (c >= 0)
+        for (int64_t t = 0; t < T[j]; ++t) add(FA2, j, t, 0, {{ZA + j, T[j]}, {ZC + c, T[c]}}, ZC + j, -1);
       for (int64_t r0 = 0; r0 < P.size(j); r0 += kFdRows)
         add(FD, j, r0, std::min<int64_t>(P.size(j), r0 + kFdRows), {{ZC + j, T[j]}}, UC + j, -1);
     }
@@ -322,9 +322,14 @@ int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, co
       add(BR, j, kBrRows * pc, std::min<int64_t>(P.size(j), kBrRows * pc + kBrRows),
           {{CC + j, nch[j] * T[j]}, {UC + j, nfd}}, RC + j, -1);
     const bool be2 = fold && parent && parent[j] >= 0;
-    for (int64_t t = 0; t < T[j]; ++t) {
-      if (be2) add(BE2, j, t, 0, {{RC + j, npc}, {XC + parent[j], T[parent[j]]}}, XC + j, -1);
-      else add(BE, j, t, 0, {{RC + j, npc}}, XC + j, -1);
+    if (be2) {
+      // BE overwrites z_j (kept in x_j's rows): every reader of z_j (the
+      // parent's FA2 or its update into the parent) precedes z_p
+      const int64_t pp = parent[j];
+      for (int64_t t = 0; t < T[j]; ++t) add(BE, j, t, 0, {{RC + j, npc}, {ZC + pp, T[pp]}}, XA + j, -1);
+      for (int64_t t = 0; t < T[j]; ++t) add(BE2, j, t, 0, {{XA + j, T[j]}, {XC + pp, T[pp]}}, XC + j, -1);
+    } else {
+      for (int64_t t = 0; t < T[j]; ++t) add(BE, j, t, 0, {{RC + j, npc}}, XC + j, -1);
     }
     if (j >= 1 && P.size(j - 1) && !done_far[j - 1]) {
       chunks(j - 1, true);

@@ -194,119 +194,6 @@ __device__ __forceinline__ void sn_tile(const cplx* __restrict__ A, int lda, int
   __syncthreads();                 // the staging memory is reused by the next tile
 }
 
-// Two-segment tile for the chain-folded solve (FA2 / BE2 items):
-//   C[r][c] = sum_k A1(r, k) B1[k][c] - sum_k A2(r, k) B2[k][c]   (K1, K2 rows)
-// over a virtual K of roundup(K1, SN_KW) + K2 rows: every 8-row k-tile lies
-// in one segment, segment 2's A values enter the DMMAs negated.  Same warp
-// split, ring and warp-order reduction as sn_tile; the summation order of
-// an output entry depends only on K1 and K2 (k-RHS == k x 1-RHS bitwise).
-// mode 0 (store) only; A1 / A2 accessed as in sn_tile for TA.
-template <bool TA, class W = SnNoWait>
-__device__ __forceinline__ void sn_tile2(const cplx* __restrict__ A1, int lda1, int K1, const cplx* __restrict__ B1,
-                                         int ldb1, const cplx* __restrict__ A2, int lda2, int K2,
-                                         const cplx* __restrict__ B2, int ldb2, int M, int N, cplx* C, int ldc, int m0,
-                                         unsigned char* sn_smem, W wait = W()) {
-  SnWarpSmem* ws = reinterpret_cast<SnWarpSmem*>(sn_smem);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int fr = lane >> 2, fc = lane & 3;
-  SnWarpSmem& S = ws[warp];
-  double acc_re[2][2][2], acc_im[2][2][2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
-  const int K1p = (K1 + SN_KW - 1) / SN_KW * SN_KW;
-  const int kend = K1p + K2;
-  const int tiles_per_slice = SN_KW / SN_BK;
-  const int nslice = (kend + SN_KW - 1) / SN_KW;
-  const int my_slices = nslice > warp ? (nslice - warp + SN_NW - 1) / SN_NW : 0;
-  const int ktiles = my_slices * tiles_per_slice;
-  auto tile_k0 = [&](int t) { return ((t / tiles_per_slice) * SN_NW + warp) * SN_KW + (t % tiles_per_slice) * SN_BK; };
-  auto load_a = [&](int st, int k0) {
-    if (k0 < K1p) sn_load_a<TA>(S, st, A1, lda1, M, m0, k0, K1, lane);
-    else sn_load_a<TA>(S, st, A2, lda2, M, m0, k0 - K1p, K2, lane);
-  };
-  auto load_b = [&](int st, int k0) {
-    if (k0 < K1p) sn_load_b(S, st, B1, ldb1, nullptr, N, k0, K1, lane);
-    else sn_load_b(S, st, B2, ldb2, nullptr, N, k0 - K1p, K2, lane);
-  };
-#pragma unroll
-  for (int s = 0; s < SN_ST - 1; ++s)
-    if (s < ktiles) load_a(s, tile_k0(s));
-  asm volatile("cp.async.commit_group;\n" ::);
-  wait();
-#pragma unroll
-  for (int s = 0; s < SN_ST - 1; ++s) {
-    if (s < ktiles) load_b(s, tile_k0(s));
-    asm volatile("cp.async.commit_group;\n" ::);
-  }
-  for (int kt = 0; kt < ktiles; ++kt) {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(SN_ST - 2));
-    __syncwarp();
-    const int nk = kt + SN_ST - 1;
-    if (nk < ktiles) {
-      load_a(nk % SN_ST, tile_k0(nk));
-      load_b(nk % SN_ST, tile_k0(nk));
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-    const int st = kt % SN_ST;
-    const double sg = tile_k0(kt) < K1p ? 1.0 : -1.0;
-#pragma unroll
-    for (int kk = 0; kk < SN_BK / 4; ++kk) {
-      double are[2], aim[2], anim[2], bre[2], bim[2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const cplx a = S.A[st][i * 8 + fr][kk * 4 + fc];
-        are[i] = sg * a.x;
-        aim[i] = sg * a.y;
-        anim[i] = -aim[i];
-      }
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const cplx b = S.B[st][kk * 4 + fc][j * 8 + fr];
-        bre[j] = b.x;
-        bim[j] = b.y;
-      }
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) sn_dmma(acc_re[i][j][0], acc_re[i][j][1], are[i], bre[j]);
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) sn_dmma(acc_im[i][j][0], acc_im[i][j][1], are[i], bim[j]);
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) sn_dmma(acc_re[i][j][0], acc_re[i][j][1], anim[i], bim[j]);
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) sn_dmma(acc_im[i][j][0], acc_im[i][j][1], aim[i], bre[j]);
-    }
-    __syncwarp();
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::);
-  __syncthreads();
-  cplx (*red)[SN_BM][SN_BN] = reinterpret_cast<cplx (*)[SN_BM][SN_BN]>(sn_smem);
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) red[warp][i * 8 + fr][j * 8 + fc * 2 + h] = mk(acc_re[i][j][h], acc_im[i][j][h]);
-  __syncthreads();
-  for (int e = threadIdx.x; e < SN_BM * SN_BN; e += SN_NT) {
-    const int rr = e >> 4, c = e & 15, r = m0 + rr;
-    if (r >= M || c >= N) continue;
-    cplx v = red[0][rr][c];
-#pragma unroll
-    for (int w = 1; w < SN_NW; ++w) v = c_add(v, red[w][rr][c]);
-    C[(int64_t)r * ldc + c] = v;
-  }
-  __syncthreads();
-}
-
 template <bool TA>
 __global__ void __launch_bounds__(SN_NT)
 skinny_dmma_kernel(const cplx* __restrict__ A, int lda, int M, int K, const cplx* __restrict__ B, int ldb,
@@ -525,20 +412,18 @@ block_solve_dataflow(SolvePlanDev p, const FlowItem* __restrict__ items, int nit
                       nullptr, 2, it.p1 * SN_BM, ch, off + ch * KCH, min(R, off + ch * KCH + KCH), sn_smem, waitdeps);
         break;
       }
-      case kFA2: {     // z_p tile = Binv_p b_p - G_c z_c (c: the folded last child)
+      case kFA2: {     // folded: z_p tile -= G_c z_c (Binv_p b_p already in place, c: the last child)
         const int c = (int)p.fold[5 * j];
         const int nc = (int)p.sizes[c];
-        sn_tile2<false>(p.binv + p.binv_off[j], nj, nj, p.b + ro * ld + p.c0, ld, p.gh + p.fold[5 * j + 1], nc, nc,
-                        p.x + p.row_off[c] * ld + p.c0, ld, nj, N, p.x + ro * ld + p.c0, ld, it.p0 * SN_BM, sn_smem,
-                        waitdeps);
+        sn_tile<false>(p.gh + p.fold[5 * j + 1], nc, nj, p.x + p.row_off[c] * ld + p.c0, ld, nullptr, N,
+                       p.x + ro * ld + p.c0, ld, nullptr, 1, it.p0 * SN_BM, 0, 0, nc, sn_smem, waitdeps);
         break;
       }
-      case kBE2: {     // x_j tile = Binv_j^T w_j - H_j^T x_p (p: the parent)
+      case kBE2: {     // folded: x_j tile -= H_j^T x_p (Binv_j^T w_j already in place, p: the parent)
         const int pp = (int)p.fold[5 * j + 2];
         const int np_ = (int)p.sizes[pp];
-        sn_tile2<true>(p.binv + p.binv_off[j], nj, nj, p.u + ro * ld + p.c0, ld, p.gh + p.fold[5 * j + 3], nj, np_,
-                       p.x + p.row_off[pp] * ld + p.c0, ld, nj, N, p.x + ro * ld + p.c0, ld, it.p0 * SN_BM, sn_smem,
-                       waitdeps);
+        sn_tile<true>(p.gh + p.fold[5 * j + 3], nj, nj, p.x + p.row_off[pp] * ld + p.c0, ld, nullptr, N,
+                      p.x + ro * ld + p.c0, ld, nullptr, 1, it.p0 * SN_BM, 0, 0, np_, sn_smem, waitdeps);
         break;
       }
       case kBR: {      // rows [p0, p1); partials loaded 16 chunks ahead, summed in chunk order

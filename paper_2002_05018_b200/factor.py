@@ -900,7 +900,7 @@ _KCH = 256                                            # backward split-K chunk (
 _FD_ROWS, _BR_ROWS = 32, 16                           # rows per D^-1 / reduce work item
 
 
-def _solve_flow(sched: _Schedule):
+def _solve_flow(sched: _Schedule, fold: bool = False):
     """Work-item list of the dataflow block solve (include/d3m.h
     d3m_block_solve_dataflow), built once per plan.
 
@@ -912,7 +912,6 @@ def _solve_flow(sched: _Schedule):
     and the Binv^T tiles, the farther chunks of column j-1 right after.
     Updates of one 16-row tile stay in ascending column order (per-tile
     sequence counters), as in the barrier kernel's phases."""
-    fold = _solve_fold()
     cache = getattr(sched, "flow", None)
     if cache is None:
         cache = sched.flow = {}
@@ -924,10 +923,18 @@ def _solve_flow(sched: _Schedule):
     return fl
 
 
-def _solve_fold() -> bool:
-    """Chain-folded dataflow solve (default); D3M_SOLVE_FOLD=0 selects the
-    plain list, bitwise equal to the barrier kernel (tests)."""
-    return _os.environ.get("D3M_SOLVE_FOLD", "1") != "0"
+def _solve_fold(refine: int) -> bool:
+    """Whether block_solve runs the chain-folded dataflow list.  Folding the
+    parent updates through the precomputed G_c = Binv_p L_pc / H_j = L_pj
+    Binv_j shortens every block column's critical chain to one tile product
+    per sweep, at a slightly larger rounding error (config 4 unrefined:
+    7.1e-10 against 4.3e-10).  With refinement the result is the same
+    (2.3e-13), so it is used when refine >= 1; refine = 0 keeps the plain
+    list, bitwise equal to the barrier kernel.  D3M_SOLVE_FOLD=0/1 forces."""
+    env = _os.environ.get("D3M_SOLVE_FOLD", "")
+    if env in ("0", "1"):
+        return env == "1"
+    return refine >= 1
 
 
 def _fold_layout(sched: _Schedule):
@@ -1133,11 +1140,12 @@ def block_solve(F: BlockFactor, g: list, refine: int = 0) -> list:
     H = _lib.hptr
     if _SOLVE_MODE == "flow":
         # dataflow kernel: per-column partial storage, counters
-        d_items, nitems, d_deps, d_poff, ncnt, part_elems = _solve_flow(sched)
+        fold = _solve_fold(int(refine))
+        d_items, nitems, d_deps, d_poff, ncnt, part_elems = _solve_flow(sched, fold)
         part = empty(part_elems)
         counters = t.empty(ncnt, dtype=t.int32, device="cuda")
 
-        gh, d_tab = _fold_blocks(F) if _solve_fold() else (None, None)
+        gh, d_tab = _fold_blocks(F) if fold else (None, None)
 
         def solve(rhs, out):
             _lib.call("d3m_block_solve_dataflow", nb, _P(_solve_plan(sched)), _P(d_items), nitems, _P(d_deps),

@@ -25,8 +25,9 @@ def flow_items_ref(sizes, pattern, panel_rows, fold=False, parent=None):
         for i in pat[j]:
             prow[j][i] = r
             r += sizes[i]
-    ZC, BLK, UC, CC, RC, XC = (k * nb for k in range(6))
-    seq_base = np.concatenate([[6 * nb], 6 * nb + np.cumsum(T)]).astype(np.int64)
+    ZC, BLK, UC, CC, RC, XC, ZA, XA = (k * nb for k in range(8))
+    cb = (8 if fold else 6) * nb
+    seq_base = np.concatenate([[cb], cb + np.cumsum(T)]).astype(np.int64)
     ncnt = int(seq_base[-1]) + 1                       # + queue head
     items, deps = [], []
 
@@ -67,11 +68,10 @@ def flow_items_ref(sizes, pattern, panel_rows, fold=False, parent=None):
         if sizes[j]:
             c = last_child[j]
             for t in range(T[j]):
-                dl = [(BLK + j, n_into[j])] if n_into[j] else []
-                if c >= 0:
-                    add(_FA2, j, t, 0, dl + [(ZC + c, T[c])], ZC + j)
-                else:
-                    add(_FA, j, t, 0, dl, ZC + j)
+                add(_FA, j, t, 0, [(BLK + j, n_into[j])] if n_into[j] else [], ZA + j if c >= 0 else ZC + j)
+            if c >= 0:
+                for t in range(T[j]):
+                    add(_FA2, j, t, 0, [(ZA + j, T[j]), (ZC + c, T[c])], ZC + j)
             for r0 in range(0, sizes[j], _FD_ROWS):
                 add(_FD, j, r0, min(sizes[j], r0 + _FD_ROWS), [(ZC + j, T[j])], UC + j)
         if pat[j]:
@@ -117,11 +117,14 @@ def flow_items_ref(sizes, pattern, panel_rows, fold=False, parent=None):
         for pc in range(npc):
             add(_BR, j, _BR_ROWS * pc, min(sizes[j], _BR_ROWS * pc + _BR_ROWS), [(CC + j, nch[j] * T[j]), (UC + j, nfd)],
                 RC + j)
-        for t in range(T[j]):
-            if fold and parent[j] >= 0:
-                p = int(parent[j])
-                add(_BE2, j, t, 0, [(RC + j, npc), (XC + p, T[p])], XC + j)
-            else:
+        if fold and parent[j] >= 0:
+            p = int(parent[j])
+            for t in range(T[j]):
+                add(_BE, j, t, 0, [(RC + j, npc), (ZC + p, T[p])], XA + j)
+            for t in range(T[j]):
+                add(_BE2, j, t, 0, [(XA + j, T[j]), (XC + p, T[p])], XC + j)
+        else:
+            for t in range(T[j]):
                 add(_BE, j, t, 0, [(RC + j, npc)], XC + j)
         if j >= 1 and sizes[j - 1] and not done_far[j - 1]:
             chunks(j - 1, True)
