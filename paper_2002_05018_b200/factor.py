@@ -16,6 +16,7 @@ Device layout of a BlockFactor (one HBM pool, complex128):
 
 from __future__ import annotations
 
+import threading
 from collections.abc import Mapping
 from dataclasses import dataclass, field
 
@@ -347,6 +348,7 @@ class _Schedule:
         self.xbuf_elems = 4 * max(1, int((self.panel_rows * sizes).max()) if nb else 1)
         self.etree_sched = planner.etree_schedule(plan.etree_parent, pattern)
         self.parent = np.asarray(plan.etree_parent, dtype=np.int64)
+        self.stage_lock = threading.Lock()     # the host-staged upload's pinned ring (one upload at a time)
         # block_solve backward gather: global plan-order rows of every panel
         gidx, gptr = [], [0]
         for j in range(nb):
@@ -683,6 +685,12 @@ def _host_layout(K: BlockSparseSym, sched: _Schedule, plan: EliminationPlan):
     return hit
 
 
+def _host_stageable(K: BlockSparseSym) -> bool:
+    """All blocks on the host (numpy arrays or CPU tensors): the host-staged upload applies."""
+    items = list(K.blocks.values())
+    return bool(items) and not any(isinstance(b, DeviceArray) or (_is_tensor(b) and b.is_cuda) for b in items)
+
+
 def _upload_K_hoststaged(K: BlockSparseSym, sched: _Schedule, plan: EliminationPlan, pool, flag):
     """Chunked upload of K from pageable host arrays (numpy blocks, as the
     reference API takes them).  A native host thread (d3m_host_stage_start)
@@ -690,12 +698,10 @@ def _upload_K_hoststaged(K: BlockSparseSym, sched: _Schedule, plan: EliminationP
     schedule, and publishes each chunk through a pinned flag; the copy stream
     holds each chunk's H2D copy until its flag (d3m_stream_wait_flag), so the
     first columns' factorisation starts while the host is still staging the
-    later blocks.  Returns (wait columns, events, keep-alive, kgroups, handle)
-    or None when a block is on the device."""
+    later blocks.  Returns (wait columns, events, keep-alive, kgroups, handle);
+    the caller holds sched.stage_lock until the join."""
     t = require_cuda()
     items = list(K.blocks.items())
-    if not items or any(isinstance(b, DeviceArray) or (_is_tensor(b) and b.is_cuda) for _, b in items):
-        return None
     keys, recs, d_rec, chunks, o, kentries = _host_layout(K, sched, plan)
     # sources: C-contiguous complex128 host arrays, alive until the join
     src = []
@@ -803,16 +809,27 @@ def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFA
     flag = t.ones(max(nb, 1), dtype=t.int32, device="cuda")
     streamed = _upload_K_streamed(K, sched, plan, pool, flag)
     stage_handle = None
-    if streamed is None:
-        hs = _upload_K_hoststaged(K, sched, plan, pool, flag)
-        if hs is not None:
-            *streamed, stage_handle = hs
+    staged = False
+    if streamed is None and _host_stageable(K):
+        # the plan's pinned staging ring and flag serve one upload at a time
+        # (another thread factoring with the same plan waits here)
+        sched.stage_lock.acquire()
+        staged = True
+        try:
+            *streamed, stage_handle = _upload_K_hoststaged(K, sched, plan, pool, flag)
+        except BaseException:
+            sched.stage_lock.release()
+            raise
     try:
         return _block_ldlt_run(K, plan, pivot_tol, lookahead, margins, sched, pool, flag, streamed, stored, flops,
                                peak, inv)
     finally:
-        if stage_handle is not None:       # the host thread reads the caller's arrays until here
-            _lib.call("d3m_host_stage_join", stage_handle)
+        try:
+            if stage_handle is not None:   # the host thread reads the caller's arrays until here
+                _lib.call("d3m_host_stage_join", stage_handle)
+        finally:
+            if staged:
+                sched.stage_lock.release()
 
 
 def _block_ldlt_run(K, plan, pivot_tol, lookahead, margins, sched, pool, flag, streamed, stored, flops, peak, inv):
