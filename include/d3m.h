@@ -219,13 +219,12 @@ int64_t d3m_plan_gemm_tasks(int nb, const int64_t* sizes, const int64_t* pat_ptr
                             int64_t* flops);
 /* Work items (int32 x 8) and dependency pairs (int32 x 2) of
  * d3m_block_solve_dataflow (factor.py:243-310 as tiles), a topological order
- * with each column's critical items first.  fold != 0 with the etree
- * parent[nb]: the chain-folded list (FA2 / BE2 items, needs the solve's
- * G / H precompute).  Two-pass (items = NULL counts); out[0..3] = items,
- * deps, counters, partial elements; part_off[nb].  0, or -2 on overflow. */
+ * with each column's critical items first.  Two-pass (items = NULL
+ * counts); out[0..3] = items, deps, counters, partial elements;
+ * part_off[nb].  0, or -2 on overflow. */
 int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, const int64_t* pat_idx,
                         const int64_t* panel_rows, int32_t* items, int64_t cap_items, int32_t* deps,
-                        int64_t cap_deps, int64_t* part_off, int64_t* out, int fold, const int64_t* parent);
+                        int64_t cap_deps, int64_t* part_off, int64_t* out);
 
 /* Host-staged upload of pageable inputs (ABI v9): a native host thread copies
  * chunk c's blocks (blocks [chunk_ptr[c], chunk_ptr[c+1]) of the n copies
@@ -259,18 +258,11 @@ int d3m_memcpy_batch(void* dst, const void* src, const int64_t* dst_off, const i
  * ceil(R_j/256) * n_j * 16 complex); d_counters: ncounters int32 scratch
  * (zeroed here before every pass; the last one is the queue head).  The item
  * list is built by the host (factor.py _solve_flow).  Replaces the
- * substitutions of factor.py:271-310 like d3m_block_solve_exec.
- * d_fold / d_gh (ABI v9; NULL / NULL = the plain list): the chain-folded
- * list of d3m_plan_flow_items(fold=1) with its per-column table (int64 x 5:
- * folded child c, offset of G_c = Binv_p L_pc in d_gh, parent p, offset of
- * H_j = L_pj Binv_j in d_gh, first split-K panel row) and the G / H blocks
- * (complex128, built once per factor): one dependent item per block column
- * and sweep on the critical chain.  Equal to the plain list to rounding. */
+ * substitutions of factor.py:271-310 like d3m_block_solve_exec. */
 int d3m_block_solve_dataflow(int nb, const void* d_plan, const void* d_items, int nitems, const void* d_deps,
                              const void* d_part_off, void* d_counters, int ncounters, const void* d_gidx,
                              const void* d_pool, const void* d_binv, const void* d_tags, void* d_b, void* d_u,
-                             void* d_x, void* d_part, int nrhs, const void* d_fold, const void* d_gh,
-                             void* stream);
+                             void* d_x, void* d_part, int nrhs, void* stream);
 
 /* Rows where each coupling block has entries (ABI v7): D is B x n x m
  * complex128 (device); flag: B*n int8 scratch; idx: B*n int64, block b's

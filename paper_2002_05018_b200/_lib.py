@@ -26,13 +26,13 @@ _SIGNATURES = {
     "d3m_bk_cluster_max_n": [I32],
     "d3m_host_stage_join": [P],
     "d3m_stream_wait_flag": [P, I32, P],
-    "d3m_plan_flow_items": [I32, P, P, P, P, P, I64, P, I64, P, P, I32, P],
+    "d3m_plan_flow_items": [I32, P, P, P, P, P, I64, P, I64, P, P],
     "d3m_ldlt_solve_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P],
     "d3m_zgemm_grouped": [I32, I32, P, P, P, P, I32, P, P],
     "d3m_gemm_set_form": [I32],
     "d3m_block_residual": [I32, P, P, P, P, P, P, P, P, P],
     "d3m_nonzero_rows": [I32, I32, I32, P, P, P, P, P],
-    "d3m_block_solve_dataflow": [I32, P, P, I32, P, P, P, I32, P, P, P, P, P, P, P, P, I32, P, P, P],
+    "d3m_block_solve_dataflow": [I32, P, P, I32, P, P, P, I32, P, P, P, P, P, P, P, P, I32, P],
     "d3m_schur_reduce_batched": [I32, I32, I32, I32, P, P, P, F64] + [P] * 14 + [P, I32, P, I32, P, P],
     "d3m_block_copy": [P, P, P, I32, I64, P],
     "d3m_gather_rows": [P, P, P, I64, I32, P],

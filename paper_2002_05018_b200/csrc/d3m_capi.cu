@@ -732,7 +732,7 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
 int d3m_block_solve_dataflow(int nb, const void* d_plan, const void* d_items, int nitems, const void* d_deps,
                              const void* d_part_off, void* d_counters, int ncounters, const void* d_gidx,
                              const void* d_pool, const void* d_binv, const void* d_tags, void* d_b, void* d_u,
-                             void* d_x, void* d_part, int nrhs, const void* d_fold, const void* d_gh, void* stream) {
+                             void* d_x, void* d_part, int nrhs, void* stream) {
   if (nb <= 0 || nrhs <= 0) return 0;
   if (!d_plan || !d_items || nitems <= 0 || ncounters <= 0) return fail(-22, "d3m_block_solve_dataflow: empty plan");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -745,9 +745,6 @@ int d3m_block_solve_dataflow(int nb, const void* d_plan, const void* d_items, in
   pl.tags = static_cast<const int8_t*>(d_tags);
   pl.b = C(d_b); pl.u = C(d_u); pl.x = C(d_x); pl.tmp = nullptr; pl.part = C(d_part);
   pl.nb = nb; pl.ldn = nrhs;
-  pl.fold = static_cast<const int64_t*>(d_fold);
-  pl.gh = CC(d_gh);
-  if (pl.fold && !pl.gh) return fail(-22, "d3m_block_solve_dataflow: folded plan without G / H");
   for (int c0 = 0; c0 < nrhs; c0 += 16) {
     pl.c0 = c0;
     pl.N = std::min(16, nrhs - c0);

@@ -39,11 +39,6 @@ struct SolvePlanDev {
   cplx *b, *u, *x, *tmp, *part;
   int nb, N;                       // N: RHS columns of this pass (<= 16), leading dimension ldn
   int ldn, c0;                     // row stride of b / u / x and the pass's first column
-  // chain-folded dataflow (optional): per column j, fold[5j..5j+4] = folded
-  // last child c (-1), offset of G_c = Binv_j L_jc in gh, parent p (-1),
-  // offset of H_j = L_pj Binv_j in gh, first split-K panel row (n_p or 0)
-  const int64_t* fold = nullptr;
-  const cplx* gh = nullptr;
 };
 
 

@@ -26,7 +26,7 @@ namespace {
 constexpr int kBM = 64;                   // GEMM output tile (zgemm_dmma.cu)
 constexpr int kKCH = 256;                 // backward split-K chunk (panel rows), skinny_dmma.cu
 constexpr int kFdRows = 32, kBrRows = 16;  // rows per D^-1 / reduce work item
-enum { FA = 0, FD = 1, FB = 2, BC = 3, BR = 4, BE = 5, FA2 = 6, BE2 = 7 };   // skinny_dmma.cu FlowItem types
+enum { FA = 0, FD = 1, FB = 2, BC = 3, BR = 4, BE = 5 };   // skinny_dmma.cu FlowItem types
 
 struct Pattern {
   int nb;
@@ -158,29 +158,17 @@ int64_t d3m_plan_gemm_tasks(int nb, const int64_t* sizes, const int64_t* pat_ptr
 // count only).  out[0..3] = item count, dependency count, counter count
 // (+1 for the queue head), partial-sum elements; part_off[nb] (>= 1 entry).
 // Returns 0, or -2 when a capacity is too small.
-//
-// fold != 0 (parent[nb] = elimination-tree parents): the chain-folded list.
-// The update of the parent block p by its last child c is folded into p's
-// z tiles: FA(p) forms Binv_p b_p from the other updates early, then FA2(p)
-// subtracts G_c z_c (G_c = Binv_p L_pc, built by the solve's precompute) as
-// soon as z_c is known.  Backward, BE(j) forms Binv_j^T w_j without the
-// parent term and BE2(j) subtracts H_j^T x_p (H_j = L_pj Binv_j) once x_p is
-// known; column j's split-K chunks then start after the parent block (row
-// n_p of the panel).  The critical chain of a block column is one K = n
-// tile product per sweep instead of z -> update -> z (forward) and
-// partial -> reduce -> x (backward).  Extra counters: ZA (Binv_p b_p done),
-// XA (Binv_j^T w_j done).
 int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, const int64_t* pat_idx,
                         const int64_t* panel_rows, int32_t* items, int64_t cap_items, int32_t* deps,
-                        int64_t cap_deps, int64_t* part_off, int64_t* out, int fold, const int64_t* parent) {
+                        int64_t cap_deps, int64_t* part_off, int64_t* out) {
   const Pattern P{nb, sizes, pat_ptr, pat_idx};
   const std::vector<int64_t> prow = panel_row_offsets(P);
   std::vector<int64_t> T(nb);
   for (int j = 0; j < nb; ++j) T[j] = (P.size(j) + 15) / 16;
   const int64_t ZC = 0, BLK = nb, UC = 2 * (int64_t)nb, CC = 3 * (int64_t)nb, RC = 4 * (int64_t)nb,
-                XC = 5 * (int64_t)nb, ZA = 6 * (int64_t)nb, XA = 7 * (int64_t)nb;
+                XC = 5 * (int64_t)nb;
   std::vector<int64_t> seq_base(nb + 1);
-  seq_base[0] = (fold ? 8 : 6) * (int64_t)nb;
+  seq_base[0] = 6 * (int64_t)nb;
   for (int j = 0; j < nb; ++j) seq_base[j + 1] = seq_base[j] + T[j];
   const int64_t ncnt = seq_base[nb] + 1;            // + queue head
   int64_t ni = 0, nd = 0;
@@ -223,15 +211,9 @@ int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, co
   };
 
   // ---- forward -------------------------------------------------------------
-  std::vector<int> last_child(nb, -1);                  // folded child of each block (fold mode)
-  if (fold && parent)
-    for (int j = 0; j < nb; ++j)
-      if (parent[j] >= 0) last_child[parent[j]] = std::max(last_child[parent[j]], j);
-  auto folded = [&](int j, int i) { return fold && last_child[i] == j; };   // update j -> i folded away
   std::vector<int64_t> n_into(nb, 0);                   // FB tile items into each block
   for (int j = 0; j < nb; ++j)
-    for (int a = 0; a < P.len(j); ++a)
-      if (!folded(j, P.at(j, a))) n_into[P.at(j, a)] += T[P.at(j, a)];
+    for (int a = 0; a < P.len(j); ++a) n_into[P.at(j, a)] += T[P.at(j, a)];
   std::vector<int64_t> seq_k(seq_base[nb] - seq_base[0], 0);
   auto update = [&](int j, int i) {
     const int64_t rp = P.rowpos(j, i, prow);
@@ -252,21 +234,17 @@ int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, co
   };
   for (int j = 0; j < nb; ++j) {
     if (P.size(j)) {
-      const int c = last_child[j];
-      const int64_t zinc = c >= 0 ? ZA + j : ZC + j;     // folded: z_j is done after FA2
       for (int64_t t = 0; t < T[j]; ++t) {
-        if (n_into[j]) add(FA, j, t, 0, {{BLK + j, n_into[j]}}, zinc, -1);
-        else add(FA, j, t, 0, {}, zinc, -1);
+        if (n_into[j]) add(FA, j, t, 0, {{BLK + j, n_into[j]}}, ZC + j, -1);
+        else add(FA, j, t, 0, {}, ZC + j, -1);
       }
-      if (c >= 0)
-        for (int64_t t = 0; t < T[j]; ++t) add(FA2, j, t, 0, {{ZA + j, T[j]}, {ZC + c, T[c]}}, ZC + j, -1);
       for (int64_t r0 = 0; r0 < P.size(j); r0 += kFdRows)
         add(FD, j, r0, std::min<int64_t>(P.size(j), r0 + kFdRows), {{ZC + j, T[j]}}, UC + j, -1);
     }
     if (P.len(j)) {
       const int par = P.at(j, 0);
       flush(par, -1);
-      if (!folded(j, par)) update(j, par);
+      update(j, par);
     }
     if (j >= 1)
       for (int a = 1; a < P.len(j - 1); ++a) flush(P.at(j - 1, a), j - 1);
@@ -275,17 +253,12 @@ int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, co
   for (int i = 0; i < nb; ++i) flush(i, -1);
 
   // ---- backward ------------------------------------------------------------
-  // fold: column j's split-K chunks start after its parent block (rows
-  // [0, n_p) of the panel), whose term the fused BE2 item adds
-  std::vector<int64_t> nch(nb), coff(nb, 0);
-  for (int j = 0; j < nb; ++j) {
-    if (fold && parent && parent[j] >= 0) coff[j] = P.size((int)parent[j]);
-    nch[j] = (panel_rows[j] - coff[j] + kKCH - 1) / kKCH;
-  }
+  std::vector<int64_t> nch(nb);
+  for (int j = 0; j < nb; ++j) nch[j] = (panel_rows[j] + kKCH - 1) / kKCH;
   // blocks of pattern(j) overlapping panel rows of chunk ch (non-empty blocks)
   auto chunk_blocks = [&](int j, int64_t ch, std::vector<int>& out_blocks) {
     out_blocks.clear();
-    const int64_t lo = coff[j] + ch * kKCH, hi = std::min<int64_t>(panel_rows[j], coff[j] + ch * kKCH + kKCH);
+    const int64_t lo = ch * kKCH, hi = std::min<int64_t>(panel_rows[j], ch * kKCH + kKCH);
     for (int a = 0; a < P.len(j); ++a) {
       const int i = P.at(j, a);
       const int64_t r = prow[P.ptr[j] + a];
@@ -321,16 +294,7 @@ int d3m_plan_flow_items(int nb, const int64_t* sizes, const int64_t* pat_ptr, co
     for (int64_t pc = 0; pc < npc; ++pc)
       add(BR, j, kBrRows * pc, std::min<int64_t>(P.size(j), kBrRows * pc + kBrRows),
           {{CC + j, nch[j] * T[j]}, {UC + j, nfd}}, RC + j, -1);
-    const bool be2 = fold && parent && parent[j] >= 0;
-    if (be2) {
-      // BE overwrites z_j (kept in x_j's rows): every reader of z_j (the
-      // parent's FA2 or its update into the parent) precedes z_p
-      const int64_t pp = parent[j];
-      for (int64_t t = 0; t < T[j]; ++t) add(BE, j, t, 0, {{RC + j, npc}, {ZC + pp, T[pp]}}, XA + j, -1);
-      for (int64_t t = 0; t < T[j]; ++t) add(BE2, j, t, 0, {{XA + j, T[j]}, {XC + pp, T[pp]}}, XC + j, -1);
-    } else {
-      for (int64_t t = 0; t < T[j]; ++t) add(BE, j, t, 0, {{RC + j, npc}}, XC + j, -1);
-    }
+    for (int64_t t = 0; t < T[j]; ++t) add(BE, j, t, 0, {{RC + j, npc}}, XC + j, -1);
     if (j >= 1 && P.size(j - 1) && !done_far[j - 1]) {
       chunks(j - 1, true);
       done_far[j - 1] = 1;

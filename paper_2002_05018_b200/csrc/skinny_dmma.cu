@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(SN_NT, 2) block_solve_persistent(SolvePlanDev 
 struct FlowItem {
   int type, j, p0, p1, dep_off, dep_cnt, inc0, inc1;
 };
-enum { kFA = 0, kFD = 1, kFB = 2, kBC = 3, kBR = 4, kBE = 5, kFA2 = 6, kBE2 = 7 };
+enum { kFA = 0, kFD = 1, kFB = 2, kBC = 3, kBR = 4, kBE = 5 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -405,32 +405,16 @@ block_solve_dataflow(SolvePlanDev p, const FlowItem* __restrict__ items, int nit
         sn_tile<false>(p.pool + p.panel_off[j] + (int64_t)it.p0 * nj, nj, it.p1, p.x + ro * ld + p.c0, ld, nullptr, N,
                        p.b + p.c0, ld, p.gidx + p.gptr[j] + it.p0, 1, 0, 0, 0, nj, sn_smem, waitdeps);
         break;
-      case kBC: {      // chunk ch of the panel rows after the column's chunk offset (folded parent)
+      case kBC: {
         const int R = (int)p.panel_rows[j], ch = it.p0;
-        const int off = p.fold ? (int)p.fold[5 * j + 4] : 0;
         sn_tile<true>(p.pool + p.panel_off[j], nj, nj, p.x + p.c0, ld, p.gidx + p.gptr[j], N, p.part + part_off[j], N,
-                      nullptr, 2, it.p1 * SN_BM, ch, off + ch * KCH, min(R, off + ch * KCH + KCH), sn_smem, waitdeps);
-        break;
-      }
-      case kFA2: {     // folded: z_p tile -= G_c z_c (Binv_p b_p already in place, c: the last child)
-        const int c = (int)p.fold[5 * j];
-        const int nc = (int)p.sizes[c];
-        sn_tile<false>(p.gh + p.fold[5 * j + 1], nc, nj, p.x + p.row_off[c] * ld + p.c0, ld, nullptr, N,
-                       p.x + ro * ld + p.c0, ld, nullptr, 1, it.p0 * SN_BM, 0, 0, nc, sn_smem, waitdeps);
-        break;
-      }
-      case kBE2: {     // folded: x_j tile -= H_j^T x_p (Binv_j^T w_j already in place, p: the parent)
-        const int pp = (int)p.fold[5 * j + 2];
-        const int np_ = (int)p.sizes[pp];
-        sn_tile<true>(p.gh + p.fold[5 * j + 3], nj, nj, p.x + p.row_off[pp] * ld + p.c0, ld, nullptr, N,
-                      p.x + ro * ld + p.c0, ld, nullptr, 1, it.p0 * SN_BM, 0, 0, np_, sn_smem, waitdeps);
+                      nullptr, 2, it.p1 * SN_BM, ch, ch * KCH, min(R, ch * KCH + KCH), sn_smem, waitdeps);
         break;
       }
       case kBR: {      // rows [p0, p1); partials loaded 16 chunks ahead, summed in chunk order
         waitdeps();
         const int R = (int)p.panel_rows[j];
-        const int off = p.fold ? (int)p.fold[5 * j + 4] : 0;
-        const int nch = R > off ? (R - off + KCH - 1) / KCH : 0;
+        const int nch = R > 0 ? (R + KCH - 1) / KCH : 0;
         const int64_t len = (int64_t)nj * N;
         const cplx* part = p.part + part_off[j];
         cplx* uj = p.u + ro * ld + p.c0;

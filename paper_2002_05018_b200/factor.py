@@ -347,7 +347,6 @@ class _Schedule:
         # X panels of the columns in flight: a ring of 4 slots (d3m_capi.cu kXSlots)
         self.xbuf_elems = 4 * max(1, int((self.panel_rows * sizes).max()) if nb else 1)
         self.etree_sched = planner.etree_schedule(plan.etree_parent, pattern)
-        self.parent = np.asarray(plan.etree_parent, dtype=np.int64)
         self.stage_lock = threading.Lock()     # the host-staged upload's pinned ring (one upload at a time)
         # block_solve backward gather: global plan-order rows of every panel
         gidx, gptr = [], [0]
@@ -917,7 +916,7 @@ _KCH = 256                                            # backward split-K chunk (
 _FD_ROWS, _BR_ROWS = 32, 16                           # rows per D^-1 / reduce work item
 
 
-def _solve_flow(sched: _Schedule, fold: bool = False):
+def _solve_flow(sched: _Schedule):
     """Work-item list of the dataflow block solve (include/d3m.h
     d3m_block_solve_dataflow), built once per plan.
 
@@ -929,95 +928,11 @@ def _solve_flow(sched: _Schedule, fold: bool = False):
     and the Binv^T tiles, the farther chunks of column j-1 right after.
     Updates of one 16-row tile stay in ascending column order (per-tile
     sequence counters), as in the barrier kernel's phases."""
-    cache = getattr(sched, "flow", None)
-    if cache is None:
-        cache = sched.flow = {}
-    fl = cache.get(fold)
+    fl = getattr(sched, "flow", None)
     if fl is None:
-        it, dp, part_off, ncnt, part_elems = planner.flow_items(sched.sizes, sched.pattern, sched.panel_rows, fold,
-                                                                sched.parent)
-        fl = cache[fold] = (upload_bytes(it), len(it), upload_bytes(dp), upload_i64(part_off), ncnt, part_elems)
+        it, dp, part_off, ncnt, part_elems = flow_items(sched.sizes, sched.pattern, sched.panel_rows)
+        fl = sched.flow = (upload_bytes(it), len(it), upload_bytes(dp), upload_i64(part_off), ncnt, part_elems)
     return fl
-
-
-def _solve_fold(refine: int) -> bool:
-    """Whether block_solve runs the chain-folded dataflow list.  Folding the
-    parent updates through the precomputed G_c = Binv_p L_pc / H_j = L_pj
-    Binv_j shortens every block column's critical chain to one tile product
-    per sweep, at a slightly larger rounding error (config 4 unrefined:
-    7.1e-10 against 4.3e-10).  With refinement the result is the same
-    (2.3e-13), so it is used when refine >= 1; refine = 0 keeps the plain
-    list, bitwise equal to the barrier kernel.  D3M_SOLVE_FOLD=0/1 forces."""
-    env = _os.environ.get("D3M_SOLVE_FOLD", "")
-    if env in ("0", "1"):
-        return env == "1"
-    return refine >= 1
-
-
-def _fold_layout(sched: _Schedule):
-    """Per-column table of the chain-folded solve (include/d3m.h
-    d3m_block_solve_dataflow d_fold) and the G / H layout, once per plan:
-    G_c = Binv_p L_pc (n_p x n_c) for each column p with children (c: the
-    last child), H_j = L_pj Binv_j (n_p x n_j) for each column with a parent."""
-    lay = getattr(sched, "fold_layout", None)
-    if lay is None:
-        nb, sizes, par = sched.nb, sched.sizes, sched.parent
-        last = np.full(nb, -1, dtype=np.int64)
-        for j in range(nb):
-            if par[j] >= 0:
-                last[par[j]] = max(last[par[j]], j)
-        tab = np.full((nb, 5), -1, dtype=np.int64)
-        tab[:, 4] = 0
-        off = 0
-        for p in range(nb):
-            c = int(last[p])
-            if c >= 0:
-                tab[p, 0], tab[p, 1] = c, off
-                off += int(sizes[p]) * int(sizes[c])
-        for j in range(nb):
-            p = int(par[j])
-            if p >= 0:
-                tab[j, 2], tab[j, 3], tab[j, 4] = p, off, int(sizes[p])
-                off += int(sizes[p]) * int(sizes[j])
-        lay = sched.fold_layout = (tab, upload_i64(tab.reshape(-1)), off)
-    return lay
-
-
-def _fold_blocks(F: "BlockFactor"):
-    """The G / H blocks of the chain-folded solve for factor F (two grouped
-    DMMA launches, cached on F): G_c = Binv_p L_pc from the stored panel of
-    c (its parent block is the panel's first block) and H_j = L_pj Binv_j."""
-    gh = getattr(F, "_gh", None)
-    if gh is not None:
-        return gh
-    sched = F._sched
-    tab, d_tab, total = _fold_layout(sched)
-    gh = empty(max(total, 1))
-    sizes, t = sched.sizes, require_cuda()
-    g_tasks, h_tasks = [], []
-    for j in range(sched.nb):
-        c, goff, p, hoff = (int(v) for v in tab[j, :4])
-        nj = int(sizes[j])
-        if c >= 0:     # G_c (n_j x n_c) = Binv_j (n_j x n_j) . L_jc, L_jc = rows [0, n_j) of panel c
-            nc = int(sizes[c])
-            g_tasks.append((int(sched.binv_off[j]), int(sched.panel_off[c]), goff, nj, nc, nj, nj, nc, nc,
-                            _lib.GEMM_STORE, 0, 0, 0))
-        if p >= 0:     # H_j (n_p x n_j) = L_pj (rows [0, n_p) of panel j) . Binv_j
-            np_ = int(sizes[p])
-            h_tasks.append((int(sched.panel_off[j]), int(sched.binv_off[j]), hoff, np_, nj, nj, nj, nj, nj,
-                            _lib.GEMM_STORE, 0, 0, 0))
-    for recs, A, B in ((g_tasks, F._binv, F._pool), (h_tasks, F._pool, F._binv)):
-        if not recs:
-            continue
-        tk = np.zeros(len(recs), dtype=_lib.GEMM_TASK)
-        arr = np.asarray(recs, dtype=np.int64)
-        for col, name in enumerate(_lib.GEMM_TASK.names):
-            tk[name] = arr[:, col]
-        d_tk = t.empty(64 * len(recs), dtype=t.uint8, device="cuda")
-        # C = A . B^T with B^T = the right factor: B(n, k) = right[k * ldb + n] (tb = 1)
-        _lib.call("d3m_zgemm_grouped", 0, 1, _P(A), _P(B), _P(gh), _lib.hptr(tk), len(recs), _P(d_tk), stream_ptr())
-    F._gh = (gh, d_tab)
-    return F._gh
 
 
 def flow_items(sizes, pattern, panel_rows):
@@ -1157,17 +1072,14 @@ def block_solve(F: BlockFactor, g: list, refine: int = 0) -> list:
     H = _lib.hptr
     if _SOLVE_MODE == "flow":
         # dataflow kernel: per-column partial storage, counters
-        fold = _solve_fold(int(refine))
-        d_items, nitems, d_deps, d_poff, ncnt, part_elems = _solve_flow(sched, fold)
+        d_items, nitems, d_deps, d_poff, ncnt, part_elems = _solve_flow(sched)
         part = empty(part_elems)
         counters = t.empty(ncnt, dtype=t.int32, device="cuda")
-
-        gh, d_tab = _fold_blocks(F) if fold else (None, None)
 
         def solve(rhs, out):
             _lib.call("d3m_block_solve_dataflow", nb, _P(_solve_plan(sched)), _P(d_items), nitems, _P(d_deps),
                       _P(d_poff), _P(counters), ncnt, _P(sched.d_gidx), _P(F._pool), _P(F._binv), _P(F._tags),
-                      _P(rhs), _P(u), _P(out), _P(part), int(cols), _P(d_tab), _P(gh), stream_ptr())
+                      _P(rhs), _P(u), _P(out), _P(part), int(cols), stream_ptr())
     else:
         tmp = empty((int(sched.sizes.max()), cols))
         # split-K partials of the backward L^T x products: ceil(R_j / 256) chunks x n_j x 16 RHS (one pass)

@@ -53,11 +53,9 @@ def gemm_tasks(sizes, pattern, diag_off, panel_off):
     return tasks, task_ptr, task_next, tiles_next, tiles_rest, int(flops[0])
 
 
-def flow_items(sizes, pattern, panel_rows, fold: bool = False, parent=None):
+def flow_items(sizes, pattern, panel_rows):
     """-> (items int32 [n, 8], deps int32 [m, 2] (>= 1 row), part_off int64
-    [max(nb, 1)], counter count, partial-sum elements).  ``fold`` (with the
-    elimination-tree ``parent``) gives the chain-folded list of
-    csrc/d3m_plan.cpp (FA2 / BE2 items)."""
+    [max(nb, 1)], counter count, partial-sum elements)."""
     lib = _lib.load()
     nb = len(sizes)
     sizes = np.ascontiguousarray(sizes, dtype=np.int64)
@@ -67,17 +65,14 @@ def flow_items(sizes, pattern, panel_rows, fold: bool = False, parent=None):
     null = _lib.ctypes.c_void_p(0)
     out = np.zeros(4, dtype=np.int64)
     part_off = np.zeros(max(nb, 1), dtype=np.int64)
-    par = np.ascontiguousarray(parent if (fold and nb) else np.full(max(nb, 1), -1), dtype=np.int64)
-    fl = 1 if fold else 0
-    rc = lib.d3m_plan_flow_items(nb, H(sizes), H(ptr), H(idx), H(panel_rows), null, 0, null, 0, null, H(out), fl,
-                                 H(par))
+    rc = lib.d3m_plan_flow_items(nb, H(sizes), H(ptr), H(idx), H(panel_rows), null, 0, null, 0, null, H(out))
     if rc != 0:
         raise RuntimeError(f"d3m_plan_flow_items returned {rc}")
     ni, nd = int(out[0]), int(out[1])
     items = np.zeros((ni, 8), dtype=np.int32)
     deps = np.zeros((max(nd, 1), 2), dtype=np.int32)
     rc = lib.d3m_plan_flow_items(nb, H(sizes), H(ptr), H(idx), H(panel_rows), H(items), ni, H(deps), nd,
-                                 H(part_off), H(out), fl, H(par))
+                                 H(part_off), H(out))
     if rc != 0:
         raise RuntimeError(f"d3m_plan_flow_items returned {rc}")
     return items, deps, part_off, int(out[2]), int(out[3])

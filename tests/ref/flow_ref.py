@@ -6,12 +6,12 @@ from __future__ import annotations
 
 import numpy as np
 
-_FA, _FB, _FD, _BC, _BR, _BE, _FA2, _BE2 = 0, 2, 1, 3, 4, 5, 6, 7      # skinny_dmma.cu FlowItem types
+_FA, _FB, _FD, _BC, _BR, _BE = 0, 2, 1, 3, 4, 5      # skinny_dmma.cu FlowItem types
 _KCH = 256
 _FD_ROWS, _BR_ROWS = 32, 16
 
 
-def flow_items_ref(sizes, pattern, panel_rows, fold=False, parent=None):
+def flow_items_ref(sizes, pattern, panel_rows):
     """Host part of _solve_flow (pure numpy; tests/test_solve_flow.py checks
     that the list is a topological order).  Returns (items int32 [n, 8],
     deps int32 [m, 2], part_off int64 [nb], counter count, partial elems)."""
@@ -25,9 +25,8 @@ def flow_items_ref(sizes, pattern, panel_rows, fold=False, parent=None):
         for i in pat[j]:
             prow[j][i] = r
             r += sizes[i]
-    ZC, BLK, UC, CC, RC, XC, ZA, XA = (k * nb for k in range(8))
-    cb = (8 if fold else 6) * nb
-    seq_base = np.concatenate([[cb], cb + np.cumsum(T)]).astype(np.int64)
+    ZC, BLK, UC, CC, RC, XC = (k * nb for k in range(6))
+    seq_base = np.concatenate([[6 * nb], 6 * nb + np.cumsum(T)]).astype(np.int64)
     ncnt = int(seq_base[-1]) + 1                       # + queue head
     items, deps = [], []
 
@@ -35,20 +34,10 @@ def flow_items_ref(sizes, pattern, panel_rows, fold=False, parent=None):
         items.append((typ, j, p0, p1, len(deps), len(dl), inc0, inc1))
         deps.extend(dl)
 
-    last_child = [-1] * nb
-    if fold:
-        for j in range(nb):
-            if parent[j] >= 0:
-                last_child[int(parent[j])] = max(last_child[int(parent[j])], j)
-
-    def folded(j, i):
-        return fold and last_child[i] == j
-
     n_into = [0] * nb                                  # FB tile items into each block
     for j in range(nb):
         for i in pat[j]:
-            if not folded(j, i):
-                n_into[i] += T[i]
+            n_into[i] += T[i]
     seq_k = [[0] * T[i] for i in range(nb)]
 
     def update(j, i):
@@ -66,19 +55,14 @@ def flow_items_ref(sizes, pattern, panel_rows, fold=False, parent=None):
 
     for j in range(nb):
         if sizes[j]:
-            c = last_child[j]
             for t in range(T[j]):
-                add(_FA, j, t, 0, [(BLK + j, n_into[j])] if n_into[j] else [], ZA + j if c >= 0 else ZC + j)
-            if c >= 0:
-                for t in range(T[j]):
-                    add(_FA2, j, t, 0, [(ZA + j, T[j]), (ZC + c, T[c])], ZC + j)
+                add(_FA, j, t, 0, [(BLK + j, n_into[j])] if n_into[j] else [], ZC + j)
             for r0 in range(0, sizes[j], _FD_ROWS):
                 add(_FD, j, r0, min(sizes[j], r0 + _FD_ROWS), [(ZC + j, T[j])], UC + j)
         if pat[j]:
             par = pat[j][0]
             flush(par)
-            if not folded(j, par):
-                update(j, par)
+            update(j, par)
         if j >= 1:
             for i in pat[j - 1][1:]:
                 flush(i, upto=j - 1)
@@ -87,11 +71,10 @@ def flow_items_ref(sizes, pattern, panel_rows, fold=False, parent=None):
     for i in range(nb):
         flush(i)
     # backward
-    coff = [sizes[int(parent[j])] if fold and parent[j] >= 0 else 0 for j in range(nb)]
-    nch = [(int(panel_rows[j]) - coff[j] + _KCH - 1) // _KCH for j in range(nb)]
+    nch = [(int(panel_rows[j]) + _KCH - 1) // _KCH for j in range(nb)]
 
     def chunk_blocks(j, ch):
-        lo, hi = coff[j] + ch * _KCH, min(int(panel_rows[j]), coff[j] + ch * _KCH + _KCH)
+        lo, hi = ch * _KCH, min(int(panel_rows[j]), ch * _KCH + _KCH)
         return [i for i in pat[j] if prow[j][i] < hi and prow[j][i] + sizes[i] > lo and sizes[i]]
 
     def parent_chunk(j, ch):
@@ -117,15 +100,8 @@ def flow_items_ref(sizes, pattern, panel_rows, fold=False, parent=None):
         for pc in range(npc):
             add(_BR, j, _BR_ROWS * pc, min(sizes[j], _BR_ROWS * pc + _BR_ROWS), [(CC + j, nch[j] * T[j]), (UC + j, nfd)],
                 RC + j)
-        if fold and parent[j] >= 0:
-            p = int(parent[j])
-            for t in range(T[j]):
-                add(_BE, j, t, 0, [(RC + j, npc), (ZC + p, T[p])], XA + j)
-            for t in range(T[j]):
-                add(_BE2, j, t, 0, [(XA + j, T[j]), (XC + p, T[p])], XC + j)
-        else:
-            for t in range(T[j]):
-                add(_BE, j, t, 0, [(RC + j, npc)], XC + j)
+        for t in range(T[j]):
+            add(_BE, j, t, 0, [(RC + j, npc)], XC + j)
         if j >= 1 and sizes[j - 1] and not done_far[j - 1]:
             chunks(j - 1, True)
             done_far[j - 1] = True

@@ -262,11 +262,10 @@ def test_multi_rhs_equals_single_rhs_bitwise(cuda):
 
 @pytest.mark.parametrize("seed,max_blocks,max_size", [(91, 7, 60), (93, 6, 300), (95, 12, 20)])
 def test_solve_kernels_bitwise_equal(cuda, monkeypatch, seed, max_blocks, max_size):
-    """The plain dataflow block solve (D3M_SOLVE_FOLD=0), the grid-barrier
-    persistent kernel (ABI v5) and the per-product launch sequence give
-    bitwise equal solutions, over two passes of RHS (20 columns); the
-    chain-folded dataflow (default) agrees to rounding; columns solved alone
-    equal the multi-RHS solve bitwise in both dataflow forms."""
+    """The dataflow block solve (default), the grid-barrier persistent kernel
+    (ABI v5) and the per-product launch sequence give bitwise equal
+    solutions, over two passes of RHS (20 columns); columns solved alone
+    equal the multi-RHS solve bitwise."""
     import paper_2002_05018_b200 as d
     from paper_2002_05018_b200 import factor as fac
     from paper_2002_05018_b200 import workloads as wl
@@ -275,16 +274,7 @@ def test_solve_kernels_bitwise_equal(cuda, monkeypatch, seed, max_blocks, max_si
     rng = np.random.default_rng(seed + 1)
     B = [rng.standard_normal((int(s), 20)) + 1j * rng.standard_normal((int(s), 20)) for s in K.sizes]
     assert fac._SOLVE_MODE == "flow"
-    Xf = d.block_solve(F, B)
-    for c in (0, 15, 16, 19):
-        Xc = d.block_solve(F, [b[:, c:c + 1] for b in B])
-        for i in range(K.nblocks):
-            assert np.array_equal(np.asarray(Xf[i])[:, c:c + 1], np.asarray(Xc[i]))
-    monkeypatch.setenv("D3M_SOLVE_FOLD", "0")
     X0 = d.block_solve(F, B)
-    for i in range(K.nblocks):
-        a, b = np.asarray(Xf[i]), np.asarray(X0[i])
-        assert np.abs(a - b).max() <= 1e-12 * max(np.abs(b).max(), 1e-300)
     monkeypatch.setattr(fac, "_SOLVE_MODE", "barrier")
     X1 = d.block_solve(F, B)
     monkeypatch.setattr(fac, "_solve_plan", lambda sched: None)
@@ -293,7 +283,6 @@ def test_solve_kernels_bitwise_equal(cuda, monkeypatch, seed, max_blocks, max_si
         assert np.array_equal(X0[i], X1[i])
         assert np.array_equal(X1[i], X2[i])
     monkeypatch.undo()
-    monkeypatch.setenv("D3M_SOLVE_FOLD", "0")
     for c in (0, 15, 16, 19):
         Xc = d.block_solve(F, [b[:, c:c + 1] for b in B])
         for i in range(K.nblocks):

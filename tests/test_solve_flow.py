@@ -20,14 +20,13 @@ from paper_2002_05018_b200.ordering import identity_ordering, reorder
 from paper_2002_05018_b200.symbolic import symbolic_factor
 
 
-def _check(plan, fold=False):
+def _check(plan):
     sizes = np.asarray(plan.sizes_perm, dtype=np.int64)
     pattern = [np.asarray(p, dtype=np.int64) for p in plan.pattern]
     panel_rows = np.array([int(sizes[p].sum()) for p in pattern], dtype=np.int64)
-    parent = np.asarray(plan.etree_parent, dtype=np.int64)
-    items, deps, part_off, ncnt, part_elems = planner.flow_items(sizes, pattern, panel_rows, fold, parent)
+    items, deps, part_off, ncnt, part_elems = flow_items(sizes, pattern, panel_rows)
     from ref.flow_ref import flow_items_ref
-    ref = flow_items_ref(sizes, pattern, panel_rows, fold, parent)
+    ref = flow_items_ref(sizes, pattern, panel_rows)
     assert np.array_equal(items, ref[0]) and np.array_equal(deps, ref[1]) and np.array_equal(part_off, ref[2])
     assert (ncnt, part_elems) == ref[3:]
     _check_tasks(sizes, pattern)
@@ -45,18 +44,10 @@ def _check(plan, fold=False):
     T = (sizes + 15) // 16
     assert np.array_equal(cnt[:nb], np.where(sizes > 0, T, 0))                   # z tiles
     assert np.array_equal(cnt[5 * nb:6 * nb], np.where(sizes > 0, T, 0))         # x tiles
-    # every update tile of every column appears exactly once (fold: the update
-    # of each parent by its last child is folded into the parent's z tiles)
+    # every update tile of every column appears exactly once
     fb = items[items[:, 0] == _FB]
-    last = {}
-    for j in range(nb):
-        if parent[j] >= 0:
-            last[int(parent[j])] = max(last.get(int(parent[j]), -1), j)
-    expect = sum(int(T[i]) for j in range(nb) for i in pattern[j] if not (fold and last.get(int(i)) == j))
+    expect = sum(int(T[i]) for j in range(nb) for i in pattern[j])
     assert len(fb) == expect
-    if fold:
-        assert (items[:, 0] == 6).sum() == sum(int(T[p]) for p in last)          # FA2 tiles
-        assert (items[:, 0] == 7).sum() == sum(int(T[j]) for j in range(nb) if parent[j] >= 0)   # BE2
     # per target tile: ascending columns
     seen = {}
     for typ, j, p0, p1, *_ in items:
@@ -110,7 +101,6 @@ def test_flow_list_config4():
     plan = symbolic_factor(clique_graph(K1), identity_ordering(len(faces)), [256] * len(faces))
     items = _check(plan)
     assert len(items) > 100_000
-    _check(plan, fold=True)
 
 
 @pytest.mark.parametrize("seed", range(12))
@@ -118,9 +108,7 @@ def test_flow_list_random_plans(seed):
     K, _ = wl.rand_block_system(seed + 200, max_blocks=14, max_size=40, density=0.35)
     g = clique_graph(K)
     for order in (reorder(g, K.sizes), identity_ordering(K.nblocks)):
-        plan = symbolic_factor(g, order, K.sizes)
-        _check(plan)
-        _check(plan, fold=True)
+        _check(symbolic_factor(g, order, K.sizes))
 
 
 def test_etree_schedule_dependencies():
