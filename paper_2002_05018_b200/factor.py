@@ -697,8 +697,10 @@ def _upload_K_hoststaged(K: BlockSparseSym, sched: _Schedule, plan: EliminationP
     schedule, and publishes each chunk through a pinned flag; the copy stream
     holds each chunk's H2D copy until its flag (d3m_stream_wait_flag), so the
     first columns' factorisation starts while the host is still staging the
-    later blocks.  Returns (wait columns, events, keep-alive, kgroups, handle);
-    the caller holds sched.stage_lock until the join."""
+    later blocks.  The host thread starts before the waits are enqueued, so
+    blocking launches (CUDA_LAUNCH_BLOCKING=1, profilers) cannot deadlock.
+    Returns (wait columns, events, keep-alive, kgroups, handle); the caller
+    holds sched.stage_lock until the join."""
     t = require_cuda()
     items = list(K.blocks.items())
     keys, recs, d_rec, chunks, o, kentries = _host_layout(K, sched, plan)
@@ -719,55 +721,59 @@ def _upload_K_hoststaged(K: BlockSparseSym, sched: _Schedule, plan: EliminationP
         sched.pin_flag = t.zeros(1, dtype=t.int32, pin_memory=True)
     pflag = sched.pin_flag
     pflag.numpy()[0] = 0
-    stage = empty(max(o, 1))
-    cur = t.cuda.current_stream()
-    cs = getattr(sched, "copy_stream", None)
-    if cs is None:
-        cs = sched.copy_stream = t.cuda.Stream()
-    ready = t.cuda.Event()
-    ready.record(cur)                      # pool zeroed, flag / staging allocated
-    cs.wait_event(ready)
-    csp = _lib.ctypes.c_void_p(cs.cuda_stream)
     H = _lib.hptr
     fptr = _lib.ctypes.c_void_p(pflag.data_ptr())
-    waits, events = [], []
     chunk_ptr, order, dst_off, nbytes = [0], [], [], []
-    for n, (col, r0, cnt, maxe, members, offs, d_diag, ndiag) in enumerate(chunks):
-        lo, hi = offs[0], offs[-1] + src[members[-1]].size
-        _lib.call("d3m_stream_wait_flag", fptr, n + 1, csp)
-        _lib.call("d3m_memcpy_batch", _P(stage), _lib.ctypes.c_void_p(pin.data_ptr()),
-                  H(np.array([16 * lo], np.int64)), H(np.array([16 * lo], np.int64)),
-                  H(np.array([16 * (hi - lo)], np.int64)), 1, 1, csp)
-        _lib.call("d3m_block_copy", _P(stage), _P(pool), _lib.ctypes.c_void_p(d_rec.data_ptr() + r0 * recs.itemsize),
-                  cnt, maxe, csp)
-        if ndiag:                          # exact-symmetry flags of the chunk's diagonal blocks (as uploaded)
-            _lib.call("d3m_diag_sym_flags", _P(pool), _P(sched.d_diag_off), _P(sched.d_sizes), _P(d_diag), ndiag,
-                      _P(flag), csp)
-        ev = t.cuda.Event()
-        ev.record(cs)
-        if n == 0:
-            cur.wait_event(ev)             # the first columns' blocks and flags
-        else:
-            waits.append(col)
-            events.append(ev)
+    for (col, r0, cnt, maxe, members, offs, d_diag, ndiag) in chunks:
         for m, off in zip(members, offs):
             order.append(m)
             dst_off.append(16 * off)
             nbytes.append(16 * src[m].size)
         chunk_ptr.append(len(order))
-    sched.pin_busy = events[-1] if events else ev
-    stage.record_stream(cs)
-    d_rec.record_stream(cs)
     srcp = (_lib.ctypes.c_void_p * max(len(order), 1))(*[src[m].ctypes.data for m in order])
     handle = _lib.load().d3m_host_stage_start(len(chunks), H(np.asarray(chunk_ptr, np.int64)), len(order), srcp,
                                               H(np.asarray(dst_off, np.int64)), H(np.asarray(nbytes, np.int64)),
                                               _lib.ctypes.c_void_p(pin.data_ptr()), fptr,
                                               min(8, _os.cpu_count() or 1))
     if not handle:
-        pflag.numpy()[0] = len(chunks)     # release the waiting copy stream, then fail
         raise _lib.D3MError("d3m_host_stage_start failed")
-    return (np.asarray(waits, dtype=np.int64), events, (stage, d_rec, src, pin), [(stage, kentries)],
-            _lib.ctypes.c_void_p(handle))
+    handle = _lib.ctypes.c_void_p(handle)
+    try:
+        stage = empty(max(o, 1))
+        cur = t.cuda.current_stream()
+        cs = getattr(sched, "copy_stream", None)
+        if cs is None:
+            cs = sched.copy_stream = t.cuda.Stream()
+        ready = t.cuda.Event()
+        ready.record(cur)                  # pool zeroed, flag / staging allocated
+        cs.wait_event(ready)
+        csp = _lib.ctypes.c_void_p(cs.cuda_stream)
+        waits, events = [], []
+        for n, (col, r0, cnt, maxe, members, offs, d_diag, ndiag) in enumerate(chunks):
+            lo, hi = offs[0], offs[-1] + src[members[-1]].size
+            _lib.call("d3m_stream_wait_flag", fptr, n + 1, csp)
+            _lib.call("d3m_memcpy_batch", _P(stage), _lib.ctypes.c_void_p(pin.data_ptr()),
+                      H(np.array([16 * lo], np.int64)), H(np.array([16 * lo], np.int64)),
+                      H(np.array([16 * (hi - lo)], np.int64)), 1, 1, csp)
+            _lib.call("d3m_block_copy", _P(stage), _P(pool),
+                      _lib.ctypes.c_void_p(d_rec.data_ptr() + r0 * recs.itemsize), cnt, maxe, csp)
+            if ndiag:                      # exact-symmetry flags of the chunk's diagonal blocks (as uploaded)
+                _lib.call("d3m_diag_sym_flags", _P(pool), _P(sched.d_diag_off), _P(sched.d_sizes), _P(d_diag), ndiag,
+                          _P(flag), csp)
+            ev = t.cuda.Event()
+            ev.record(cs)
+            if n == 0:
+                cur.wait_event(ev)         # the first columns' blocks and flags
+            else:
+                waits.append(col)
+                events.append(ev)
+        sched.pin_busy = events[-1] if events else ev
+        stage.record_stream(cs)
+        d_rec.record_stream(cs)
+    except BaseException:
+        _lib.load().d3m_host_stage_join(handle)
+        raise
+    return (np.asarray(waits, dtype=np.int64), events, (stage, d_rec, src, pin), [(stage, kentries)], handle)
 
 
 def block_ldlt(K: BlockSparseSym, plan: EliminationPlan, pivot_tol: float = DEFAULT_PIVOT_TOL,

@@ -535,3 +535,24 @@ def test_etree_parallel_executor_bitwise_equals_sequential(cuda, grid, n, order)
     B = [rng.standard_normal((int(s), 2)) + 1j * rng.standard_normal((int(s), 2)) for s in K.sizes]
     for a, b in zip(d.block_solve(F0, B), d.block_solve(F1, B)):
         assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
+def test_host_staged_upload_under_blocking_launches(cuda):
+    """With CUDA_LAUNCH_BLOCKING=1 (or a profiler serialising launches) every
+    launch returns only once its kernel has finished: the staging thread must
+    already be running when the copy stream's flag waits are enqueued, or the
+    first wait never ends.  A subprocess factors a numpy K that way."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "import paper_2002_05018_b200 as d\n"
+            "from paper_2002_05018_b200 import workloads as wl\n"
+            "K = wl.config4_matrix(seed=5, grid=(3, 3, 2), n=16)\n"
+            "plan = d.symbolic_factor(d.clique_graph(K), d.identity_ordering(K.nblocks), K.sizes)\n"
+            "for _ in range(2):\n"
+            "    F = d.block_ldlt(K, plan)\n"
+            "print('ok', F.stats.n_2x2_pivots)\n") % ROOT
+    env = dict(__import__("os").environ, CUDA_LAUNCH_BLOCKING="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stderr[-2000:]
