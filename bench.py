@@ -195,18 +195,16 @@ def run_ours(args):
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # timed regions run with the cyclic garbage collector paused (the timeit
-    # convention): a full collection over the plan's host objects costs ~80 ms
-    # and would land in a random step
+    # a collection before each timed region; the collector stays on (the plan's
+    # tables are numpy arrays built by the native planner, so a full collection
+    # has little to walk)
     gc.collect()
-    gc.disable()
     with ClockSampler(local) as clk:
         e0.record(s)
         for _ in range(args.steps):
             F, x = step_dev()
         e1.record(s)
         torch.cuda.synchronize()
-    gc.enable()
     _barrier(dist)
     ms_total = _max_over_ranks(dist, e0.elapsed_time(e1))
     ms_step = ms_total / args.steps
@@ -252,7 +250,6 @@ def run_ours(args):
     e2e_steps = max(3, min(args.steps, 5))
     e2e_samples = []
     gc.collect()
-    gc.disable()
     for _ in range(e2e_steps):
         t0 = time.perf_counter()
         Fh = d.block_ldlt(Kp, plan)
@@ -260,7 +257,6 @@ def run_ours(args):
         torch.cuda.synchronize()
         e2e_samples.append((time.perf_counter() - t0) * 1e3)
         del Fh                                       # the caller releases the factor before the next solve
-    gc.enable()
     # median of the samples (all are reported): one host-side hiccup in a
     # few-sample run otherwise dominates the mean
     e2e_ms = _max_over_ranks(dist, float(np.median(e2e_samples)))
@@ -274,7 +270,6 @@ def run_ours(args):
     torch.cuda.synchronize()
     np_samples = []
     gc.collect()
-    gc.disable()
     for _ in range(e2e_steps):
         t0 = time.perf_counter()
         Fh = d.block_ldlt(K, plan)
@@ -282,7 +277,6 @@ def run_ours(args):
         torch.cuda.synchronize()
         np_samples.append((time.perf_counter() - t0) * 1e3)
         del Fh
-    gc.enable()
     np_ms = _max_over_ranks(dist, float(np.median(np_samples)))
     e2e_numpy = {"value": round(flops_step * ws / (np_ms * 1e-3) / 1e12, 4), "unit": "TFLOP/s",
                  "ms_per_step": round(np_ms, 3), "samples_ms": [round(v, 1) for v in np_samples],
@@ -470,7 +464,6 @@ def _cfg3_secondary(steps: int, peak: float) -> dict:
     s0 = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     gc.collect()
-    gc.disable()
     e0.record(s0)
     for _ in range(steps):
         for s in dev:
@@ -479,7 +472,6 @@ def _cfg3_secondary(steps: int, peak: float) -> dict:
         red = d.reduce_domains(dev, keep="schur")
     e1.record(s0)
     torch.cuda.synchronize()
-    gc.enable()
     ms = e0.elapsed_time(e1) / steps
     # e2e: pinned host inputs (A, D, f as pinned torch CPU tensors), copied
     # inside the timed region; all K_D / g_d read back to numpy
@@ -490,13 +482,11 @@ def _cfg3_secondary(steps: int, peak: float) -> dict:
     d.reduce_domains(host_p, keep="schur")
     torch.cuda.synchronize()
     gc.collect()
-    gc.disable()
     t0 = time.perf_counter()
     red_h = d.reduce_domains(host_p, keep="schur")
     outs = [(np.asarray(K_), np.asarray(g_)) for K_, g_ in red_h]
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3
-    gc.enable()
     h2d = 16 * sum(s.A.size + s.f.size + sum(c.D.size for c in s.couplings) for s in host)
     for s in dev:
         s.factor = None
