@@ -58,10 +58,10 @@ def timed(n, cs, reps=20):
     return c["ms"]["bk"] / c["n"]["bk"]
 
 
-for n in (32, 64, 96, 128):
+for n in (() if os.environ.get("NO_EXACT") else (32, 64, 96, 128)):
     ms = timed(n, 0)
     print(f"exact  n={n:4d}: {ms * 1e3:8.1f} us  {ms * 1e3 / n:6.2f} us/step", flush=True)
-for cs in (8, 4):
+for cs in tuple(int(c) for c in os.environ.get("CS_LIST", "8,4").split(",")):
     for n in (130, 192, 256):
         ms = timed(n, cs)
         print(f"cluster{cs} n={n:4d}: {ms * 1e3:8.1f} us  {ms * 1e3 / n:6.2f} us/step", flush=True)
