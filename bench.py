@@ -20,7 +20,8 @@ flops are not counted).  One step = block_ldlt + block_solve.
           reference's numba kernels + numpy/OpenBLAS block drivers) running
           the SAME full step (block LDL^T of K + the 16-RHS solve) on the
           host cores, timed once; the secondaries carry same-run CPU timings
-          of the subdomain reductions (configs 1 and 3, process pools)
+          of the subdomain reductions (configs 1, 2 and 3, process pools;
+          config 5's ~20 CPU-minutes per subdomain are out of a bench's reach)
   secondary : configs 1, 2, 3 and 5 (BASELINE configs[0], [1], [2], [4]),
           each with time, rate, roofline fraction and pivot-decision margins
 
@@ -349,6 +350,8 @@ def run_ours(args):
         line["cpu_baseline"] = _cpu_full_cfg4(plan, K, rhs, flops_step, ms_step)
         if "cfg1" in sec:
             sec["cfg1"]["cpu_reduce"] = _cpu_reduce_pool("cfg1", [0, 1], sec["cfg1"]["stage_ms"]["reduce"])
+        if "cfg2" in sec:
+            sec["cfg2"]["cpu_reduce"] = _cpu_reduce_pool("cfg2", list(range(8)), sec["cfg2"]["stage_ms"]["reduce"])
         if "cfg3" in sec:
             sec["cfg3"]["cpu_reduce"] = _cpu_reduce_pool("cfg3", list(range(8)), sec["cfg3"]["ms_per_step"],
                                                          total=64)

@@ -34,7 +34,7 @@ int fail(int code, const char* what) {
   do {                                                                       \
     int _rc = (expr);                                                        \
     if (_rc != 0) {                                                          \
-      char _b[256];                                                          \
+      char _b[1024];                                                          \
       snprintf(_b, sizeof(_b), "%s failed with %d (%s)", #expr, _rc,        \
                _rc > 0 ? cudaGetErrorString((cudaError_t)_rc) : "invalid"); \
       g_err = _b;                                                            \

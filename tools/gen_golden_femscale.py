@@ -10,10 +10,12 @@ REFERENCE implementation (numba JIT backend) in the build container.
   SPEC.md:176).  Stored: every subdomain's pivot sequence (perm, tags, n2x2),
   K_D (cfg1 full; cfg2 the first 64 rows plus the Frobenius norm), g_d, the
   reduced system's order and block pivots, lambda and the recovered field.
+* ``cfg3_all.npz`` (``cfg3all``): the reference's reduce_domain on all 64
+  config-3 subdomains: pivot sequences, K_D norms and first rows.
 * ``cfg4_x16.npz``: the config-4 solution for all 16 RHS columns on a fixed
   row sample (rows 0..4095 and 2048 seeded random rows) plus column norms.
 
-    NUMBA_CACHE_DIR=/tmp/numba_cache python tools/gen_golden_femscale.py [cfg1|cfg2|cfg4|all]
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tools/gen_golden_femscale.py [cfg1|cfg2|cfg4|all|cfg3all]
 """
 
 from __future__ import annotations
@@ -129,6 +131,34 @@ def gen_cfg4_x16():
     print(f"cfg4 x16: factor {t1 - t0:.1f}s, 16-RHS solve {t2 - t1:.1f}s", flush=True)
 
 
+def _cfg3_one(i):
+    from ddsolve import subdomain as rs
+    from paper_2002_05018_b200 import workloads as wl
+    A, D, f = wl.config3_domain(i)
+    s = rs.SubdomainSystem(i, A, f, np.arange(A.shape[0]), [rs.Coupling(0, D, 1)])
+    t0 = time.perf_counter()
+    KD, gd = rs.reduce_domain(s)
+    dt = time.perf_counter() - t0
+    print(f"cfg3 domain {i}: {dt:.1f}s n2x2 {s.factor.n_2x2}", flush=True)
+    return (i, s.factor.perm.astype(np.int16), s.factor.tags, s.factor.n_2x2, s.factor.growth,
+            float(np.linalg.norm(KD)), KD[:8].copy(), dt)
+
+
+def gen_cfg3_all(workers: int = 8):
+    """BASELINE configs[2]: the reference's reduce_domain on all 64
+    subdomains (process pool): every pivot sequence, K_D norms and the first
+    8 rows of every K_D (cfg3_all.npz; cfg3.npz keeps two full K_D)."""
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=workers) as ex:
+        res = sorted(ex.map(_cfg3_one, range(64)), key=lambda r: r[0])
+    np.savez_compressed(os.path.join(OUT, "cfg3_all.npz"),
+                        perm=np.stack([r[1] for r in res]), tags=np.stack([r[2] for r in res]),
+                        n2x2=np.array([r[3] for r in res]), growth=np.array([r[4] for r in res]),
+                        KDnorm=np.array([r[5] for r in res]), KDrows=np.stack([r[6] for r in res]),
+                        t_each=np.array([r[7] for r in res]), t_wall=np.array(time.perf_counter() - t0))
+    print(f"cfg3 all 64: {time.perf_counter() - t0:.1f}s wall", flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what in ("cfg1", "all"):
@@ -137,3 +167,5 @@ if __name__ == "__main__":
         gen_fem("cfg2")
     if what in ("cfg4", "all"):
         gen_cfg4_x16()
+    if what == "cfg3all":
+        gen_cfg3_all()
