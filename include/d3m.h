@@ -72,8 +72,10 @@ int d3m_ldlt_solve_batched(int batch, int n, const void* F, int64_t stride_f, co
                            void* stream);
 
 /* Batched blocked Bunch-Kaufman for large dense matrices (zlasyf form): per
- * panel of 16 columns one CTA per matrix (panel in L2) + one grouped DMMA
- * GEMM for all trailing updates.  Same outputs as d3m_bk_factor_batched;
+ * panel of 63-64 columns (127-128 from n = 8192) a thread-block cluster of
+ * 1-16 CTAs per matrix (contiguous row slices, pivot searches merged through
+ * distributed shared memory) + one grouped DMMA GEMM for all matrices'
+ * trailing updates.  Same outputs as d3m_bk_factor_batched;
  * identical pivot decisions whenever no test sits within rounding of its
  * threshold, values to rounding.  workspace: d3m_bk_panel_workspace(n, batch)
  * bytes.  Used by d3m_schur_reduce_batched for n > 512. */

@@ -4,8 +4,9 @@
 // The reference factors A_d with the unblocked right-looking kernel
 // (kernels.py:36-146), which rewrites the whole trailing triangle per step.
 // Here (LAPACK zlasyf, lower) every matrix of the batch advances one panel of
-// NB columns per launch of bk_panel_kernel (one CTA per matrix, panel and the
-// X = L D workspace in L2-resident global memory), applying the reference's
+// NB columns per launch of bk_panel_kernel (a cluster of CS CTAs per matrix,
+// each owning a contiguous slice of the active rows; the panel and the
+// X = L D workspace in global memory), applying the reference's
 // decision rules (glibc-hypot modulus, alpha, first-index argmax, "<= tol"),
 // its symmetric interchanges including the L rows of all previous columns,
 // and storing L/D in the reference's packed layout.  The trailing rank-NB
