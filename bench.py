@@ -170,7 +170,7 @@ def run_ours(args):
     from paper_2002_05018_b200.device import DeviceArray, to_device
 
     dist, rank, ws = _dist()
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     K, plan, rhs = _cfg4_host()
     # device-resident copies (value leg)
