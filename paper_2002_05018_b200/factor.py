@@ -17,6 +17,7 @@ Device layout of a BlockFactor (one HBM pool, complex128):
 from __future__ import annotations
 
 import threading
+from collections import OrderedDict
 from collections.abc import Mapping
 from dataclasses import dataclass, field
 
@@ -361,16 +362,34 @@ class _Schedule:
         self.stats_cache = {}
 
 
+_SCHED_CACHE: "OrderedDict[tuple, _Schedule]" = OrderedDict()
+_SCHED_LOCK = threading.Lock()
+_SCHED_KEEP = 2
+
+
 def _schedule(plan: EliminationPlan) -> _Schedule:
+    """The device layout / task tables of a plan, cached by plan STRUCTURE
+    (supernode sizes and block pattern), so a new plan object of the same
+    structure (a new solve_d3m run) reuses them; the last _SCHED_KEEP
+    structures are kept."""
     sched = getattr(plan, "_d3m_schedule", None)
     key = (tuple(int(s) for s in plan.sizes_perm), tuple(tuple(int(i) for i in p) for p in plan.pattern))
-    if sched is None or sched[0] != key:
-        sched = (key, _Schedule(plan))
-        try:
-            plan._d3m_schedule = sched
-        except AttributeError:
-            pass
-    return sched[1]
+    if sched is not None and sched[0] == key:
+        return sched[1]
+    with _SCHED_LOCK:
+        hit = _SCHED_CACHE.get(key)
+        if hit is None:
+            hit = _Schedule(plan)
+            _SCHED_CACHE[key] = hit
+            while len(_SCHED_CACHE) > _SCHED_KEEP:
+                _SCHED_CACHE.popitem(last=False)
+        else:
+            _SCHED_CACHE.move_to_end(key)
+    try:
+        plan._d3m_schedule = (key, hit)
+    except AttributeError:
+        pass
+    return hit
 
 
 def _reference_stats(K_keys, sizes_orig, plan: EliminationPlan, inv) -> tuple[int, int, int]:
