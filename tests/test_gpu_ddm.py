@@ -298,3 +298,24 @@ def test_recover_sees_in_place_load_edits(cuda):
     want = np.asarray(d.recover_primal(fresh, lam))
     assert not np.allclose(after, before)
     assert np.linalg.norm(after - want) <= 1e-10 * np.linalg.norm(want)
+
+
+def test_config3_all_64_subdomains_vs_reference(cuda):
+    """BASELINE configs[2] in full: all 64 subdomains (n = 2048, m = 384)
+    reduced in one batch (panel BK, Schur-only form as the bench runs it):
+    every pivot sequence (perm, tags, n2x2) equals the reference's
+    (tools/gen_golden_femscale.py cfg3all, the reference's reduce_domain on
+    each subdomain), K_D norms and first rows within 1e-10."""
+    import paper_2002_05018_b200 as d
+    from paper_2002_05018_b200 import workloads as wl
+    g = golden("cfg3_all.npz")
+    systems = wl.config3_systems(64)
+    red = d.reduce_domains(systems, keep="schur", margins=True)
+    for i, s in enumerate(systems):
+        assert np.array_equal(s.factor.perm, g["perm"][i].astype(np.int64)), i
+        assert np.array_equal(s.factor.tags, g["tags"][i]), i
+        assert s.factor.n_2x2 == int(g["n2x2"][i]), i
+        KD = np.asarray(red[i][0])
+        assert abs(np.linalg.norm(KD) - g["KDnorm"][i]) <= 1e-10 * g["KDnorm"][i], i
+        assert np.linalg.norm(KD[:8] - g["KDrows"][i]) <= 1e-10 * np.linalg.norm(g["KDrows"][i]), i
+    assert min(s.factor.margin[0] for s in systems) > 1e-10
