@@ -195,7 +195,9 @@ __host__ __device__ inline int64_t bkc_entries(int n) {    // per-CTA capacity (
 
 #ifdef D3M_BK_PROFILE
 // per-role phase clocks of CTA 0: slots 0-7 the pivot warp (lane 0), 8-15 the
-// first bulk thread; accumulated in registers, written once at the end
+// first bulk thread; accumulated in registers, written once at the end into
+// g_bkc_prof (read by d3m_bkc_prof_read; profiling builds only)
+__device__ double g_bkc_prof[32];
 #define BKC_MARK(who, slot) do { if (rank == 0 && tid == (who)) { long long t_ = clock64(); \
     pacc[slot] += (double)(t_ - prof_t); prof_t = t_; } } while (0)
 #else
@@ -525,25 +527,22 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
         BKC_MARK(0, 5);
         const double lv = v;
         const int li = vi;
-        // one butterfly for the exact argmax, the owner's modulus and the
-        // update maximum (independent shuffles per round; max and
-        // first-index argmax are order-free, so the results are unchanged)
+        // the critical butterfly carries only the exact argmax (first-index,
+        // order-free); the owner's modulus |W[k0, k0]| comes from lane 0
+        // (row k0 is the first own row >= k0), and the update maximum is
+        // reduced after the push, off the chain
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           const double v2_ = __shfl_xor_sync(0xffffffffu, v, o);
           const int i2 = __shfl_xor_sync(0xffffffffu, vi, o);
-          const double own2 = __shfl_xor_sync(0xffffffffu, own, o);
-          const double sq2 = __shfl_xor_sync(0xffffffffu, step_sq, o);
           argmax_merge(v, vi, v2_, i2);
-          own = fmax(own, own2);
-          step_sq = fmax(step_sq, sq2);
         }
+        own = __shfl_sync(0xffffffffu, own, 0);
         if (track) v2 = warp_runner_up(lv, li, v2, vi);
-      } else {
-        step_sq = warp_max(step_sq);
       }
-      if (lane == 0) rst[s & 1][0] = step_sq;
       xpost<CS>(inbox[nb], rank, xslot(v, own, up, vi, v2), &mbar[nb], track);
+      step_sq = warp_max(step_sq);
+      if (lane == 0) rst[s & 1][0] = step_sq;
       BKC_MARK(0, 6);
       if (kstep == 2) ++n2x2;
     } else {
@@ -719,7 +718,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
   if (rank == 0 && gthread) a.growth[b] = growth;
 #ifdef D3M_BK_PROFILE
   if (rank == 0 && (tid == 0 || tid == 32)) {
-    double* prof = reinterpret_cast<double*>(a.scratch);
+    double* prof = g_bkc_prof;
 #pragma unroll
     for (int i = 0; i < 8; ++i) prof[(tid == 0 ? 0 : 8) + i] = pacc[(tid == 0 ? 0 : 8) + i];
     if (tid == 0) {   // prologue, step loop, write-back (cycles)
@@ -832,3 +831,10 @@ extern "C" int d3m_bk_cluster_max_n(int cs) {
   }
   return best;
 }
+
+#ifdef D3M_BK_PROFILE
+// profiling builds (-DD3M_BK_PROFILE, tools/bkc_profile.sh): the phase clocks of the last cluster BK
+extern "C" int d3m_bkc_prof_read(double* host32) {
+  return (int)cudaMemcpyFromSymbol(host32, d3m::g_bkc_prof, sizeof(double) * 32);
+}
+#endif
