@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define D3M_ABI_VERSION 9
+#define D3M_ABI_VERSION 10
 
 int d3m_abi_version(void);
 const char* d3m_last_error(void);
@@ -249,6 +249,10 @@ int d3m_stream_wait_flag(const void* flag, int value, void* stream);
 int d3m_memcpy_batch(void* dst, const void* src, const int64_t* dst_off, const int64_t* src_off,
                      const int64_t* nbytes, int n, int kind, void* stream);
 
+/* Scheduler scratch the dataflow solve keeps after the planner's counters
+ * (ABI v10): d_counters holds (planner count + D3M_FLOW_EXTRA_COUNTERS) ints. */
+#define D3M_FLOW_EXTRA_COUNTERS 2052
+
 /* Block substitution as a dataflow of work items (ABI v7): the products of
  * d3m_block_solve_exec (same tiles and summation order, so bitwise equal to
  * it), taken from an atomic queue by one resident grid per pass of <= 16 RHS
@@ -258,10 +262,14 @@ int d3m_memcpy_batch(void* dst, const void* src, const int64_t* dst_off, const i
  * d_deps: int32 pairs {counter, target}; d_part_off: per-column int64 offset
  * of its split-K partials in d_part (sum over columns of
  * ceil(R_j/256) * n_j * 16 complex); d_counters: ncounters int32 scratch
- * (zeroed here before every pass; the last one is the queue head).  The item
- * list is built by the host (factor.py _solve_flow).  Replaces the
- * substitutions of factor.py:271-310 like d3m_block_solve_exec. */
-int d3m_block_solve_dataflow(int nb, const void* d_plan, const void* d_items, int nitems, const void* d_deps,
+ * (zeroed here before every pass; the last D3M_FLOW_EXTRA_COUNTERS are the
+ * queues').  ABI v10: the first nchain items are the critical chain (each
+ * column's z_j, parent update, parent-chunk partials, reduce and x_j), run
+ * by CTAs that own their SM; the others by the rest of the grid; each part
+ * keeps the planner's (topological) order.  The item list is built by the
+ * host (factor.py _solve_flow).  Replaces the substitutions of
+ * factor.py:271-310 like d3m_block_solve_exec. */
+int d3m_block_solve_dataflow(int nb, const void* d_plan, const void* d_items, int nitems, int nchain, const void* d_deps,
                              const void* d_part_off, void* d_counters, int ncounters, const void* d_gidx,
                              const void* d_pool, const void* d_binv, const void* d_tags, void* d_b, void* d_u,
                              void* d_x, void* d_part, int nrhs, void* stream);

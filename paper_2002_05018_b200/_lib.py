@@ -32,7 +32,7 @@ _SIGNATURES = {
     "d3m_gemm_set_form": [I32],
     "d3m_block_residual": [I32, P, P, P, P, P, P, P, P, P],
     "d3m_nonzero_rows": [I32, I32, I32, P, P, P, P, P],
-    "d3m_block_solve_dataflow": [I32, P, P, I32, P, P, P, I32, P, P, P, P, P, P, P, P, I32, P],
+    "d3m_block_solve_dataflow": [I32, P, P, I32, I32, P, P, P, I32, P, P, P, P, P, P, P, P, I32, P],
     "d3m_schur_reduce_batched": [I32, I32, I32, I32, P, P, P, F64] + [P] * 14 + [P, I32, P, I32, P, P],
     "d3m_block_copy": [P, P, P, I32, I64, P],
     "d3m_gather_rows": [P, P, P, I64, I32, P],
@@ -84,7 +84,8 @@ class D3MError(RuntimeError):
 _lib = None
 
 
-ABI_VERSION = 9          # include/d3m.h D3M_ABI_VERSION this binding is written for
+FLOW_EXTRA_COUNTERS = 2052  # include/d3m.h D3M_FLOW_EXTRA_COUNTERS
+ABI_VERSION = 10         # include/d3m.h D3M_ABI_VERSION this binding is written for
 
 
 def load():

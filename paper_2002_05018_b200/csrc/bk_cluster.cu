@@ -387,6 +387,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     }
 
     int kstep = 1, kp;
+#ifdef D3M_BK_PROFILE
+    bool prof_rm = false;
+#endif
     if (absakk >= __dmul_rn(kBkcAlpha, colmax)) {
       kp = k;
       if (track && lead) mdec = fmin(mdec, decision_margin(tol_abs, absakk, colmax, 0.0, 0.0, kBkcAlpha, 1));
@@ -394,6 +397,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
       // ---- 2. push column k+1 and the symmetric column imax; rowmax over
       //         W[imax, k:imax] and W[imax+1:, imax]; |W[imax, imax]| ----------
       if (tid == 0) mbar_arm(&mbarR, (unsigned)(2 * (n - k) - 1) * 16u + CS * slot_bytes(track));
+#ifdef D3M_BK_PROFILE
+      if (rank == 0 && tid == 0) pacc[13] += 1.0;
+      prof_rm = true;
+#endif
       const uint32_t rb = saddr(&mbarR);
       double rm = 0.0, aim = -1.0;
       if (imax % CS == rank) {
@@ -441,6 +448,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
         mdec = fmin(mdec, decision_margin(tol_abs, absakk, colmax, rowmax, absimax, kBkcAlpha, stage));
     }
     const int kk = k + kstep - 1, k0 = k + kstep;
+#ifdef D3M_BK_PROFILE
+    if (rank == 0 && tid == 0) { pacc[14] += kp != kk ? 1.0 : 0.0; pacc[15] += kstep == 2 ? 1.0 : 0.0; }
+#endif
     const cplx* cK = kstep == 1 ? cA : cB;          // column kk before the swap
     // post-interchange columns k (X) and k+1 (Y) at row i >= k0: sigma swaps kk, kp
     auto Xc = [&](int i) -> cplx {
@@ -461,6 +471,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
     const int nb = (s + 1) % 3;
     const int qk0 = first_q(k0);
     double step_sq = 0.0;
+#ifdef D3M_BK_PROFILE
+    BKC_MARK(0, prof_rm ? 12 : 3);
+#endif
 
     if (pw) {
       // ---- 3P. interchange of the own rows i > kp: W[i, kk] <-> W[i, kp] ----
@@ -484,10 +497,13 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
       }
       __syncwarp();
       asm volatile("bar.arrive 1, %0;\n" ::"n"(BKC_NT) : "memory");   // the bulk may read the swapped rows
-      BKC_MARK(0, 2);
+#ifdef D3M_BK_PROFILE
+      BKC_MARK(0, prof_rm ? 12 : 2);
+#endif
       // ---- 4P. update of column k0 of the own rows, push ------------------
       double up = -1.0;
       if (s >= 1) up = warp_max(lane < NW ? rst[(s - 1) & 1][lane] : 0.0);
+      BKC_MARK(0, 7);
       double v = -1.0, own = -1.0, v2 = -1.0;
       int vi = 0x7fffffff;
       if (k0 < n) {
@@ -726,6 +742,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(BKC_NT) bk_cluster_
       prof[16] = (double)(t_loop0 - t_entry);
       prof[17] = (double)(t_loop1 - t_loop0);
       prof[18] = (double)(t_end - t_loop1);
+      prof[19] = pacc[13];     // steps with the rowmax exchange
+      prof[20] = pacc[14];     // steps with an interchange
+      prof[21] = pacc[15];     // 2x2 pivots
+      prof[22] = (double)s;    // steps
+      prof[23] = pacc[12];     // decide + rowmax + interchange cycles of the rowmax steps
     }
   }
 #endif

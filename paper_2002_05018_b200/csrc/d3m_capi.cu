@@ -729,12 +729,13 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
 //   b, u, x : N x nrhs plan order (b consumed);  tmp: max n_j x nrhs;
 //   part    : partial sums, part_elems complex
 // ---------------------------------------------------------------------------
-int d3m_block_solve_dataflow(int nb, const void* d_plan, const void* d_items, int nitems, const void* d_deps,
+int d3m_block_solve_dataflow(int nb, const void* d_plan, const void* d_items, int nitems, int nchain, const void* d_deps,
                              const void* d_part_off, void* d_counters, int ncounters, const void* d_gidx,
                              const void* d_pool, const void* d_binv, const void* d_tags, void* d_b, void* d_u,
                              void* d_x, void* d_part, int nrhs, void* stream) {
   if (nb <= 0 || nrhs <= 0) return 0;
-  if (!d_plan || !d_items || nitems <= 0 || ncounters <= 0) return fail(-22, "d3m_block_solve_dataflow: empty plan");
+  if (!d_plan || !d_items || nitems <= 0 || ncounters <= D3M_FLOW_EXTRA_COUNTERS || nchain < 0 || nchain > nitems)
+    return fail(-22, "d3m_block_solve_dataflow: empty plan or counters without the scheduler scratch");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t* d_arr = static_cast<const int64_t*>(d_plan);
   d3m::SolvePlanDev pl{};
@@ -749,7 +750,7 @@ int d3m_block_solve_dataflow(int nb, const void* d_plan, const void* d_items, in
     pl.c0 = c0;
     pl.N = std::min(16, nrhs - c0);
     const int rc = launch(kClsSolve, s, [&] {
-      return d3m_block_solve_flow_launch(&pl, d_items, nitems, d_deps, d_part_off, d_counters, ncounters, s);
+      return d3m_block_solve_flow_launch(&pl, d_items, nitems, nchain, d_deps, d_part_off, d_counters, ncounters, s);
     });
     if (rc != 0) return fail(rc, "d3m_block_solve_dataflow: launch");
   }

@@ -63,7 +63,7 @@ int d3m_bk_cluster_max_n(int cs);
 int d3m_skinny_launch(int ta, const void* A, int lda, int M, int K, const void* B, int ldb, const void* bmap, int N,
                       void* C, int ldc, const void* cmap, int mode, int kchunk, void* stream);
 int d3m_block_solve_persistent_launch(void* plan, void* stream);
-int d3m_block_solve_flow_launch(void* plan, const void* items, int nitems, const void* deps, const void* part_off,
+int d3m_block_solve_flow_launch(void* plan, const void* items, int nitems, int nchain, const void* deps, const void* part_off,
                                 void* cnt, int ncounters, void* stream);
 int d3m_skinny_reduce_launch(const void* base, int ldb, const void* part, int nch, int M, int np, double sign,
                              void* out, int ldo, void* stream);

@@ -22,10 +22,11 @@
 #include <cooperative_groups.h>
 #include "d3m_common.cuh"
 #include "d3m_kernels.h"
+#include "../../include/d3m.h"
 
 namespace d3m {
 
-constexpr int SN_BM = 16, SN_BN = 16, SN_BK = 8, SN_ST = 4, SN_PA = SN_BK + 4, SN_PB = SN_BN + 2, SN_NT = 128;
+constexpr int SN_BM = 16, SN_BN = 16, SN_BK = 8, SN_ST = 3, SN_PA = SN_BK + 4, SN_PB = SN_BN + 2, SN_NT = 128;
 constexpr int SN_NW = SN_NT / 32;
 constexpr int SN_KW = 64;                  // K rows per warp and CTA pass (a CTA covers 256 K rows)
 
@@ -338,24 +339,61 @@ __device__ __forceinline__ long long gtimer() {
   return t;
 }
 
-__global__ void __launch_bounds__(SN_NT, 2)
-block_solve_dataflow(SolvePlanDev p, const FlowItem* __restrict__ items, int nitems, const int2* __restrict__ deps,
-                     const int64_t* __restrict__ part_off, int* cnt, int* next, long long* trace) {
+// Two queues: the chain items (items[0, nchain): z_j, the parent block's
+// update, the parent chunk's partials, the reduce and x_j -- the critical
+// path of both sweeps) go to the "chain" CTAs, one per SM on the first
+// chain_sms SMs to arrive (the other CTA of such an SM exits), so they never
+// share an SM's DMMA pipe; every other CTA takes the rest, items[nchain,
+// nitems).  Each list is a subsequence of one topological order, so the
+// smallest unfinished item is always held by a CTA of its class that can
+// run it: no deadlock.  sched: [0] chain head, [1] bulk head, [2] chain CTA
+// count, [4, 4 + kFlowSms) SM tickets, [4 + kFlowSms, 4 + 2 kFlowSms) SM roles.
+constexpr int kFlowSms = 1024;
+
+__global__ void __launch_bounds__(SN_NT, 3)
+block_solve_dataflow(SolvePlanDev p, const FlowItem* __restrict__ items, int nitems, int nchain, int chain_sms,
+                     const int2* __restrict__ deps, const int64_t* __restrict__ part_off, int* cnt, int* sched,
+                     long long* trace) {
   extern __shared__ __align__(128) unsigned char sn_smem[];
-  __shared__ int s_idx;
+  __shared__ int s_idx, s_role;
   const int N = p.N, ld = p.ldn;
   constexpr int KCH = 256;
   __shared__ int s_next;
-  if (threadIdx.x == 0) s_next = atomicAdd(next, 1);
+  if (threadIdx.x == 0) {
+    int role = 0;                                    // 0 rest, 1 chain, 2 exit
+    if (nchain > 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
+      smid &= kFlowSms - 1;
+      int* role_of = sched + 4 + kFlowSms;
+      if (atomicAdd(sched + 4 + smid, 1) == 0) {
+        role = atomicAdd(sched + 2, 1) < chain_sms ? 1 : 0;
+        atomicExch(role_of + smid, role + 1);
+      } else {
+        int r;
+        for (unsigned spin = 0; (r = ld_acquire(role_of + smid)) == 0; ++spin)
+          if (spin > (1u << 26)) __trap();
+        role = r == 2 ? 2 : 0;
+      }
+    }
+    s_role = role;
+  }
+  __syncthreads();
+  if (s_role == 2) return;
+  const bool chain = s_role == 1;
+  const int q0 = chain ? 0 : nchain;
+  const int qn = chain ? nchain : nitems;
+  int* next = sched + (chain ? 0 : 1);
+  if (threadIdx.x == 0) s_next = q0 + atomicAdd(next, 1);
   for (;;) {
     // the queue index of the item after this one is taken while this one runs
     if (threadIdx.x == 0) {
       s_idx = s_next;
-      if (s_idx < nitems) s_next = atomicAdd(next, 1);
+      if (s_idx < qn) s_next = q0 + atomicAdd(next, 1);
     }
     __syncthreads();
     const int idx = s_idx;
-    if (idx >= nitems) break;
+    if (idx >= qn) break;
     const FlowItem it = items[idx];
     if (trace && threadIdx.x == 0) trace[3 * (int64_t)idx] = gtimer();
     // inputs ready: thread 0 polls the item's counters, then a CTA barrier;
@@ -464,9 +502,9 @@ extern "C" int d3m_flow_trace(void* host, int max_items) {
 }
 
 // Dataflow block solve (one cooperative launch per pass of <= 16 RHS; the
-// caller zeroes `cnt` (ncounters ints, the last one the queue head) before
-// each pass).  Returns -22 when the grid cannot be co-resident.
-extern "C" int d3m_block_solve_flow_launch(void* plan, const void* items, int nitems, const void* deps,
+// launcher zeroes `cnt` (ncounters ints, the last D3M_FLOW_EXTRA_COUNTERS
+// the scheduler's) before each pass).  Returns -22 when the grid cannot be co-resident.
+extern "C" int d3m_block_solve_flow_launch(void* plan, const void* items, int nitems, int nchain, const void* deps,
                                            const void* part_off, void* cnt, int ncounters, void* stream) {
   using namespace d3m;
   static int grid = -1;
@@ -476,7 +514,7 @@ extern "C" int d3m_block_solve_flow_launch(void* plan, const void* items, int ni
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, block_solve_dataflow, SN_NT, kSnSmem);
-    grid = sms * std::min(per, 2);
+    grid = sms * std::min(per, 3);      // three CTAs per SM (two: +0.4-0.8 ms per pass)
     if (grid <= 0) grid = 0;
   }
   if (grid == 0) return -22;
@@ -488,7 +526,7 @@ extern "C" int d3m_block_solve_flow_launch(void* plan, const void* items, int ni
   const int2* dp = static_cast<const int2*>(deps);
   const int64_t* po = static_cast<const int64_t*>(part_off);
   int* c = static_cast<int*>(cnt);
-  int* nx = c + ncounters - 1;
+  int* sc = c + ncounters - D3M_FLOW_EXTRA_COUNTERS;          // scheduler scratch (see block_solve_dataflow)
   // D3M_FLOW_TRACE=1 (dev aid): per-item globaltimer stamps (taken, inputs
   // ready, done) of the last pass, read back by d3m_flow_trace
   static long long* trace = nullptr;
@@ -505,7 +543,10 @@ extern "C" int d3m_block_solve_flow_launch(void* plan, const void* items, int ni
     g_flow_trace = trace;
     g_flow_trace_n = nitems;
   }
-  void* args[] = {const_cast<SolvePlanDev*>(pl), &it, &nitems, &dp, &po, &c, &nx, &tr};
+  // chain SMs: 24 (A/B on config 4, three CTAs per SM elsewhere: 16 7.24,
+  // 24 6.78, 32 6.80 ms per 16-RHS pass; one queue on two CTAs per SM 7.4)
+  int csms = 24;
+  void* args[] = {const_cast<SolvePlanDev*>(pl), &it, &nitems, &nchain, &csms, &dp, &po, &c, &sc, &tr};
   e = cudaLaunchCooperativeKernel((void*)block_solve_dataflow, dim3(grid), dim3(SN_NT), args, kSnSmem, s);
   return (int)e;
 }

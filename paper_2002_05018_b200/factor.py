@@ -952,12 +952,38 @@ def _solve_flow(sched: _Schedule):
     partials of the chunks holding the parent block come before the reduce
     and the Binv^T tiles, the farther chunks of column j-1 right after.
     Updates of one 16-row tile stay in ascending column order (per-tile
-    sequence counters), as in the barrier kernel's phases."""
+    sequence counters), as in the barrier kernel's phases.
+
+    The list is then split (``chain_split``): the critical chain first (its
+    own queue, run by CTAs that own their SM), the rest after, each part in
+    this order.  Returns (items, nitems, nchain, deps, part_off, counter
+    count incl. the scheduler scratch, partial elements)."""
     fl = getattr(sched, "flow", None)
     if fl is None:
         it, dp, part_off, ncnt, part_elems = flow_items(sched.sizes, sched.pattern, sched.panel_rows)
-        fl = sched.flow = (upload_bytes(it), len(it), upload_bytes(dp), upload_i64(part_off), ncnt, part_elems)
+        it, nchain = chain_split(it, sched.sizes, sched.pattern)
+        fl = sched.flow = (upload_bytes(it), len(it), nchain, upload_bytes(dp), upload_i64(part_off),
+                           ncnt + _lib.FLOW_EXTRA_COUNTERS, part_elems)
     return fl
+
+
+def chain_split(items, sizes, pattern):
+    """(items reordered: critical chain first, nchain).  Chain items: z_j
+    (FA), the reduce and x_j (BR, BE), the updates of the parent block's
+    rows (FB with panel row < n_parent; the parent is the first pattern
+    block) and the partials of the chunks holding them (BC with 256 chunk <
+    n_parent).  D^-1 (FD, needed only by the backward sweep) and the farther
+    updates / partials run on the other CTAs.  Stable: each part keeps the
+    planner's topological order."""
+    items = np.asarray(items)
+    nb = len(sizes)
+    npar = np.array([int(sizes[int(p[0])]) if len(p) else 0 for p in pattern] + [0], dtype=np.int64)
+    typ, j, p0 = items[:, 0], items[:, 1], items[:, 2].astype(np.int64)
+    jn = np.where((j >= 0) & (j < nb), j, nb)
+    crit = ((typ == _FA) | (typ == _BR) | (typ == _BE) | ((typ == _FB) & (p0 < npar[jn]))
+            | ((typ == _BC) & (p0 * _KCH < npar[jn])))
+    order = np.concatenate([np.nonzero(crit)[0], np.nonzero(~crit)[0]])
+    return np.ascontiguousarray(items[order]), int(crit.sum())
 
 
 def flow_items(sizes, pattern, panel_rows):
@@ -1097,12 +1123,12 @@ def block_solve(F: BlockFactor, g: list, refine: int = 0) -> list:
     H = _lib.hptr
     if _SOLVE_MODE == "flow":
         # dataflow kernel: per-column partial storage, counters
-        d_items, nitems, d_deps, d_poff, ncnt, part_elems = _solve_flow(sched)
+        d_items, nitems, nchain, d_deps, d_poff, ncnt, part_elems = _solve_flow(sched)
         part = empty(part_elems)
         counters = t.empty(ncnt, dtype=t.int32, device="cuda")
 
         def solve(rhs, out):
-            _lib.call("d3m_block_solve_dataflow", nb, _P(_solve_plan(sched)), _P(d_items), nitems, _P(d_deps),
+            _lib.call("d3m_block_solve_dataflow", nb, _P(_solve_plan(sched)), _P(d_items), nitems, nchain, _P(d_deps),
                       _P(d_poff), _P(counters), ncnt, _P(sched.d_gidx), _P(F._pool), _P(F._binv), _P(F._tags),
                       _P(rhs), _P(u), _P(out), _P(part), int(cols), stream_ptr())
     else:

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     from paper_2002_05018_b200 import _lib
     assert set(_declared()) <= set(_lib.exported_symbols())
-    assert lib.d3m_abi_version() == 9
+    assert lib.d3m_abi_version() == _lib.ABI_VERSION == 10
 
 
 def test_gpu_path_fails_loudly_without_device():
@@ -43,3 +43,10 @@ def test_gpu_path_fails_loudly_without_device():
     from paper_2002_05018_b200 import D3MUnavailable, dense_ldlt_bk
     with pytest.raises(D3MUnavailable):
         dense_ldlt_bk(np.eye(3, dtype=complex))
+
+
+def test_flow_extra_counters_match_header():
+    import re
+    from paper_2002_05018_b200 import _lib
+    hdr = open(os.path.join(ROOT, "include", "d3m.h")).read()
+    assert int(re.search(r"#define D3M_FLOW_EXTRA_COUNTERS (\d+)", hdr).group(1)) == _lib.FLOW_EXTRA_COUNTERS

@@ -128,3 +128,21 @@ def test_etree_schedule_dependencies():
     s = planner.etree_schedule(parent, pattern).reshape(-1, 3)
     assert s[0, 0] != s[1, 0] and s[2, 0] == s[1, 0] and s[3, 0] != s[2, 0]
     assert s[5, 1] == 3                               # 4 -> 5 is a next update; 3 is the last rest writer
+
+
+def test_chain_split_keeps_order_and_picks_the_critical_items():
+    from paper_2002_05018_b200.factor import chain_split
+    sizes = np.array([256, 200, 256, 130, 256, 64], dtype=np.int64)
+    pattern = [np.array([1, 2, 4]), np.array([2, 5]), np.array([3, 4, 5]), np.array([4]), np.array([5]), np.array([])]
+    panel_rows = np.array([int(sizes[p].sum()) if len(p) else 0 for p in pattern], dtype=np.int64)
+    items = flow_items(sizes, pattern, panel_rows)[0]
+    split, nchain = chain_split(items, sizes, pattern)
+    assert len(split) == len(items) and 0 < nchain < len(items)
+    key = {tuple(r): i for i, r in enumerate(items)}
+    pos = np.array([key[tuple(r)] for r in split])
+    assert np.all(np.diff(pos[:nchain]) > 0) and np.all(np.diff(pos[nchain:]) > 0)    # stable parts
+    for r in split[:nchain]:
+        typ, j, p0 = int(r[0]), int(r[1]), int(r[2])
+        npar = int(sizes[pattern[j][0]]) if len(pattern[j]) else 0
+        assert typ in (_FA, _BR, _BE) or (typ == _FB and p0 < npar) or (typ == _BC and 256 * p0 < npar)
+    assert not np.any(split[nchain:, 0] == _FA) and np.all(split[:nchain, 0] != _FD)

@@ -4,6 +4,7 @@
 set -e
 cd "$(dirname "$0")/.."
 D=/tmp/bkcprof; mkdir -p $D
+if [ -z "$SKIP_BUILD" ]; then
 SRCS=$(python -c "import sys; sys.path.insert(0, 'paper_2002_05018_b200'); import build_ext; print(' '.join(build_ext.SOURCES))")
 for f in $SRCS; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -DD3M_BK_PROFILE --expt-relaxed-constexpr \
@@ -11,7 +12,8 @@ for f in $SRCS; do
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $D/libd3m.so $D/*.o -lcudart
-D3M_LIB=$D/libd3m.so python - <<'PY'
+fi
+D3M_LIB=${D3M_LIB:-$D/libd3m.so} python - <<'PY'
 import ctypes, os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
@@ -29,12 +31,13 @@ for cs in (os.environ.get("CS_LIST", "8,4").split(",")):
         torch.cuda.synchronize()
         p = np.zeros(32)
         lib.d3m_bkc_prof_read(p.ctypes.data_as(ctypes.c_void_p))
-        pn = ["wait", "merge", "decide+rowmax+swap", "arrive", "l0", "col-update+push+hypot", "argmax+post"]
+        pn = ["wait", "merge", "3P-swap+arrive", "decide", "l0", "col-update+push+hypot", "argmax+post", "up"]
         bn = ["wait", "merge", "refill+mult+arrive", "bulk"]
-        print(f"CS={cs} block {j}: pivot warp:", " ".join(f"{nm}={v/1e3:.0f}K" for nm, v in zip(pn, p[:7])),
+        print(f"CS={cs} block {j}: pivot warp:", " ".join(f"{nm}={v/1e3:.0f}K" for nm, v in zip(pn, p[:8])),
               f"total={p[:8].sum()/1e6:.3f}M cycles")
         print(f"CS={cs} block {j}: bulk warps:", " ".join(f"{nm}={v/1e3:.0f}K" for nm, v in zip(bn, p[8:12])),
               f"total={p[8:16].sum()/1e6:.3f}M")
         print(f"CS={cs} block {j}: CTA 0: prologue {p[16]/1e3:.0f}K, step loop {p[17]/1e3:.0f}K, "
-              f"write-back {p[18]/1e3:.0f}K cycles", flush=True)
+              f"write-back {p[18]/1e3:.0f}K cycles; steps {p[22]:.0f}: rowmax {p[19]:.0f}, interchange {p[20]:.0f}, "
+              f"2x2 {p[21]:.0f}; decide phase: plain steps {(p[2]+p[3])/max(1, p[22]-p[19]):.0f}, rowmax steps {p[23]/max(1, p[19]):.0f} cycles/step", flush=True)
 PY

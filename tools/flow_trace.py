@@ -19,7 +19,8 @@ torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); x = d.block_solve(F, rhs); e1.record(); torch.cuda.synchronize()
 print(f"solve {e0.elapsed_time(e1):.2f} ms")
-items = fac.flow_items(F._sched.sizes, F._sched.pattern, F._sched.panel_rows)[0]
+items = fac.chain_split(fac.flow_items(F._sched.sizes, F._sched.pattern, F._sched.panel_rows)[0],
+                        F._sched.sizes, F._sched.pattern)[0]
 n = len(items)
 buf = np.zeros(3 * n, dtype=np.int64)
 lib = _lib.load()
