@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define D3M_ABI_VERSION 10
+#define D3M_ABI_VERSION 11
 
 int d3m_abi_version(void);
 const char* d3m_last_error(void);
@@ -83,6 +83,27 @@ int d3m_bk_panel_batched(int batch, int n, void* W, int64_t stride_w, int lda, d
                          void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
                          void* workspace, void* margin, void* stream);
 size_t d3m_bk_panel_workspace(int n, int batch);
+/* check_sym bit 3 (value 8, ABI v11) on d3m_bk_panel_batched: the scale is
+ * np.abs(tril(W)).max() and the upper triangle is never read (no symmetry
+ * check) -- the split upload of host matrices, where the upper halves are
+ * still in flight when the factorisation starts; the caller checks symmetry
+ * and the full scale with d3m_sym_scan_batched on an intact copy and
+ * refactors when the full scale differs (an inexactly symmetric input). */
+
+/* scale[b] = np.abs(W_b).max(), asym[b] = np.abs(W_b - W_b.T).max()
+ * (factor.py:94-98) exactly as the factorisation kernels compute them.
+ * workspace: >= 64 * batch bytes.  (ABI v11) */
+int d3m_sym_scan_batched(int batch, int n, const void* W, int64_t stride_w, int lda, void* scale, void* asym,
+                         void* workspace, void* stream);
+
+/* Row-block pieces of row-major n x n complex128 matrices src[b] (leading
+ * dimension src_ld) into dst + b * dst_stride (leading dimension dst_ld):
+ * part 0 = rows [r0, r0+128) x columns [0, r0+128) of every 128-row block
+ * (the lower triangle and the diagonal blocks), part 1 = the remainder
+ * (strict upper triangle outside the diagonal blocks).  kind is a
+ * cudaMemcpyKind (1 host->device, 3 device->device).  (ABI v11) */
+int d3m_copy_triangle(int batch, const void* const* src, int64_t src_ld, void* dst, int64_t dst_stride,
+                      int64_t dst_ld, int n, int part, int kind, void* stream);
 
 /* Blocked multi-RHS solve (64-row diagonal blocks in shared memory +
  * right-looking DMMA GEMM updates), same contract as d3m_ldlt_solve_batched;
@@ -116,6 +137,8 @@ int d3m_gemm_set_form(int form);
  * work_z is reused for the gathered X rows).  rows = NULL: dense product.
  * flags (ABI v4): bit 0 = Schur only -- forward sweep Z = L^-1 P [D | F]
  * and K = Z_D^T D^-1 Z (no backward sweep; work_x does not hold X then).
+ * Bit 1 (ABI v11): A already holds the packed factor and perm/tags/... are
+ * filled (the caller ran d3m_bk_panel_batched itself); the BK is skipped.
  * n <= 512: exact BK + chain solves (bk_scratch: batch*4n complex if n>3200);
  * n > 512: panel BK + blocked solves (bk_scratch: d3m_bk_panel_workspace
  * bytes, d_tasks: max(batch, 2 ceil(n/64) batch) records). */

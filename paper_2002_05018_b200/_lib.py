@@ -49,6 +49,8 @@ _SIGNATURES = {
     "d3m_counters_read": [P, P, P],
     "d3m_bk_panel_batched": [I32, I32, P, I64, I32, F64, I32, P, P, P, P, P, P, P, P, P, P],
     "d3m_ldlt_solve_blocked_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P, P],
+    "d3m_sym_scan_batched": [I32, I32, P, I64, I32, P, P, P, P],
+    "d3m_copy_triangle": [I32, P, I64, P, I64, I64, I32, I32, I32, P],
 }
 _SIZE_T = {"d3m_bk_panel_workspace": [I32, I32]}
 _PTR = {"d3m_host_stage_start": [I32, P, I32, P, P, P, P, P, I32]}
@@ -85,7 +87,7 @@ _lib = None
 
 
 FLOW_EXTRA_COUNTERS = 2052  # include/d3m.h D3M_FLOW_EXTRA_COUNTERS
-ABI_VERSION = 10         # include/d3m.h D3M_ABI_VERSION this binding is written for
+ABI_VERSION = 11         # include/d3m.h D3M_ABI_VERSION this binding is written for
 
 
 def load():

@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(256) bk_scan_kernel(BkArgs a, unsigned long lo
       const int i = ti * 32 + r, j = tj * 32 + tx;
       Ta[r][tx] = (i < n && j < n) ? W[(int64_t)i * lda + j] : mk(0.0, 0.0);        // block (ti, tj)
       const int i2 = tj * 32 + r, j2 = ti * 32 + tx;
-      Tb[r][tx] = (i2 < n && j2 < n) ? W[(int64_t)i2 * lda + j2] : mk(0.0, 0.0);    // block (tj, ti)
+      // block (tj, ti); not read in lower_only mode
+      Tb[r][tx] = (i2 < n && j2 < n && !a.lower_only) ? W[(int64_t)i2 * lda + j2] : mk(0.0, 0.0);
     }
     __syncthreads();
     for (int r = ty; r < 32; r += 8) {
@@ -101,12 +102,12 @@ __global__ void __launch_bounds__(256) bk_scan_kernel(BkArgs a, unsigned long lo
       const cplx z = Ta[r][tx], zt = Tb[tx][r];     // W[i][j], W[j][i]
       if (pass == 0) {
         const double q = x_abs2(z);
-        v0 = fmax(v0, fmax(q, x_abs2(zt)));
+        v0 = fmax(v0, a.lower_only ? q : fmax(q, x_abs2(zt)));
         v2 = fmax(v2, q);
         if (a.check_sym && j < i) v1 = fmax(v1, x_abs2(x_sub(z, zt)));
       } else {
         if (x_abs2(z) >= ta) v0 = fmax(v0, np_abs(z));
-        if (x_abs2(zt) >= ta) v0 = fmax(v0, np_abs(zt));
+        if (!a.lower_only && x_abs2(zt) >= ta) v0 = fmax(v0, np_abs(zt));
         if (a.check_sym && j < i) {
           const cplx dz = x_sub(z, zt);
           if (x_abs2(dz) >= tb) v1 = fmax(v1, np_abs(dz));
@@ -629,6 +630,35 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
                             : panel_run<64>(a, batch, st, Wp, tasks, tmax, s, stream);
   if (rc) return rc;
   bk_panel_finalize_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, batch);
+  return (int)cudaGetLastError();
+}
+
+namespace d3m {
+__global__ void sym_scan_store_kernel(const unsigned long long* red, double* scale, double* asym, int batch) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  scale[b] = as_pos(red[8 * b + 3]);
+  asym[b] = as_pos(red[8 * b + 4]);
+}
+}  // namespace d3m
+
+// The prologue scan alone over full matrices: scale = np.abs(W).max() and
+// asym = np.abs(W - W.T).max() per matrix (factor.py:94-98), exactly as the
+// factorisation kernels compute them.  red: >= 64 * batch bytes.
+extern "C" int d3m_sym_scan_batched_launch(d3m::BkArgs* a, int batch, void* red_ws, void* stream) {
+  using namespace d3m;
+  if (batch <= 0 || a->n <= 0) return 0;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  auto* red = static_cast<unsigned long long*>(red_ws);
+  cudaMemsetAsync(red, 0, (size_t)batch * 8 * sizeof(unsigned long long), s);
+  const int nt = (a->n + 31) / 32, ntile = nt * (nt + 1) / 2;
+  const dim3 sgrid(std::min(ntile, 256), batch);
+  BkArgs x = *a;
+  x.check_sym = 1;
+  x.lower_only = false;
+  bk_scan_kernel<<<sgrid, 256, 0, s>>>(x, red, 0);
+  bk_scan_kernel<<<sgrid, 256, 0, s>>>(x, red, 1);
+  sym_scan_store_kernel<<<(batch + 127) / 128, 128, 0, s>>>(red, a->scale, a->asym, batch);
   return (int)cudaGetLastError();
 }
 

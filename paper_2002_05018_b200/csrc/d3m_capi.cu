@@ -303,15 +303,54 @@ int d3m_bk_panel_batched(int batch, int n, void* W, int64_t stride_w, int lda, d
                          void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
                          void* workspace, void* margin, void* stream) {
   if (batch < 0 || n < 0 || lda < n) return fail(-22, "d3m_bk_panel_batched: bad shape");
+  const bool lower_only = (check_sym & 8) != 0;      // ABI v11: scale from the lower triangle only
+  check_sym = lower_only ? 0 : (check_sym & 3);
   d3m::BkArgs a{C(W), stride_w, n, lda, pivot_tol, check_sym, static_cast<int64_t*>(perm), static_cast<int8_t*>(tags),
                 static_cast<int32_t*>(n2x2), static_cast<double*>(growth), static_cast<int32_t*>(info),
                 static_cast<double*>(scale), static_cast<double*>(asym), nullptr};
   a.margin = static_cast<double*>(margin);
+  a.lower_only = lower_only;
   D3M_TRY(launch(kClsBk, stream, [&] { return d3m_bk_panel_batched_launch(&a, batch, workspace, stream); }));
   return 0;
 }
 
 size_t d3m_bk_panel_workspace(int n, int batch) { return d3m_bk_panel_workspace_bytes(n, batch); }
+
+int d3m_sym_scan_batched(int batch, int n, const void* W, int64_t stride_w, int lda, void* scale, void* asym,
+                         void* workspace, void* stream) {
+  if (batch < 0 || n < 0 || lda < n) return fail(-22, "d3m_sym_scan_batched: bad shape");
+  d3m::BkArgs a{C(const_cast<void*>(W)), stride_w, n, lda, 0.0, 1, nullptr, nullptr, nullptr, nullptr, nullptr,
+                static_cast<double*>(scale), static_cast<double*>(asym), nullptr};
+  D3M_TRY(launch(kClsMisc, stream, [&] { return d3m_sym_scan_batched_launch(&a, batch, workspace, stream); }));
+  return 0;
+}
+
+// Row-block pieces of square row-major n x n matrices (16-byte elements):
+// part 0 copies rows [r0, r1) x columns [0, r1) of each 128-row block -- the
+// lower triangle plus the upper triangles inside the diagonal blocks (53% of
+// the bytes at n = 2048) -- and part 1 the rest, rows [r0, r1) x [r1, n).
+// One cudaMemcpy2DAsync per piece; kind is a cudaMemcpyKind.
+int d3m_copy_triangle(int batch, const void* const* src, int64_t src_ld, void* dst, int64_t dst_stride,
+                      int64_t dst_ld, int n, int part, int kind, void* stream) {
+  if (batch < 0 || n < 0 || src_ld < n || dst_ld < n || (part != 0 && part != 1))
+    return fail(-22, "d3m_copy_triangle: bad arguments");
+  constexpr int kRb = 128;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  for (int b = 0; b < batch; ++b) {
+    const char* sb = static_cast<const char*>(src[b]);
+    char* db = static_cast<char*>(dst) + (size_t)b * dst_stride * 16;
+    for (int r0 = 0; r0 < n; r0 += kRb) {
+      const int r1 = std::min(n, r0 + kRb);
+      const int c0 = part == 0 ? 0 : r1, c1 = part == 0 ? r1 : n;
+      if (c1 <= c0) continue;
+      cudaError_t e = cudaMemcpy2DAsync(db + ((size_t)r0 * dst_ld + c0) * 16, (size_t)dst_ld * 16,
+                                        sb + ((size_t)r0 * src_ld + c0) * 16, (size_t)src_ld * 16,
+                                        (size_t)(c1 - c0) * 16, (size_t)(r1 - r0), (cudaMemcpyKind)kind, s);
+      if (e != cudaSuccess) return fail((int)e, "d3m_copy_triangle: cudaMemcpy2DAsync");
+    }
+  }
+  return 0;
+}
 
 int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* Cm, void* h_tasks, int ntasks,
                       void* d_tasks, void* stream) {
@@ -339,11 +378,13 @@ int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const v
   const bool big = n > kPanelBkMin;
   // large subdomains: batched blocked BK (panel kernel + grouped DMMA trailing
   // updates, bk_scratch >= d3m_bk_panel_workspace(n, batch) bytes); small:
-  // the unblocked bit-exact kernel
-  if (big)
+  // the unblocked bit-exact kernel.  flags bit 1: A already holds the factor
+  // (the caller ran the BK itself, e.g. on a split upload)
+  const bool factored = (flags & 2) != 0;
+  if (big && !factored)
     D3M_TRY(d3m_bk_panel_batched(batch, n, A, nn, n, pivot_tol, 1, perm, tags, n2x2, growth, info, scale, asym,
                                  bk_scratch, margin, stream));
-  else
+  else if (!factored)
     D3M_TRY(d3m_bk_factor_batched(batch, n, A, nn, n, pivot_tol, 1, perm, tags, n2x2, growth, info, scale, asym,
                                   bk_scratch, margin, stream));
   if (n == 0 || w == 0) return 0;

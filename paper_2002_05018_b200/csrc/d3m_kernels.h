@@ -28,6 +28,11 @@ struct BkArgs {
   // searches (d3m_common.cuh); nullptr = not tracked
   double* margin = nullptr;
   bool abs_tol = false;               // pivot_tol is the absolute threshold (d3m_bk_factor_batched check_sym bit 2)
+  // panel BK only (d3m_bk_panel_batched check_sym bit 3): the scale is the
+  // maximum over the lower triangle and the upper triangle is never read --
+  // the split upload, where the upper half is still in flight and the
+  // symmetry check / full scale run separately (d3m_sym_scan_batched)
+  bool lower_only = false;
 };
 
 // Device-resident plan of the persistent block solve (skinny_dmma.cu)
@@ -103,6 +108,7 @@ int d3m_diag_block_launch(int fwd, const void* F, int64_t stride_f, const void* 
 int d3m_diag_block_rows();
 int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* workspace, void* stream);
 size_t d3m_bk_panel_workspace_bytes(int n, int batch);
+int d3m_sym_scan_batched_launch(d3m::BkArgs* a, int batch, void* red_ws, void* stream);
 }
 
 #include "d3m_gemm.h"

@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib
 from .blockmat import BlockSparseSym
-from .device import DeviceArray, empty, require_cuda, stream_ptr, to_device, upload_bytes, upload_i64
+from .device import BatchHost, DeviceArray, empty, require_cuda, stream_ptr, to_device, upload_bytes, upload_i64
 from .factor import DEFAULT_PIVOT_TOL, DenseFactor, SolverStateError, _collect, _singular_msg
 
 _P = _lib.ptr
@@ -248,7 +248,10 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
         while pos < len(members):
             m = ms[members[pos]]
             budget = max_batch_bytes if max_batch_bytes is not None else int(0.8 * _free_bytes(t))
-            cap = max(1, budget // _domain_bytes(n, m, r))
+            # the split upload of dense host matrices keeps an intact copy A0
+            per = _domain_bytes(n, m, r) + (16 * n * n if n > _lib.PANEL_BK_MIN and _host_dense(systems[members[pos]].A)
+                                            else 0)
+            cap = max(1, budget // per)
             chunk = members[pos:pos + cap]
             pos += len(chunk)
             err = _reduce_chunk(systems, chunk, n, m, r, ms, pivot_tol, keep, vec, out, margins)
@@ -259,16 +262,51 @@ def reduce_domains(systems: list[SubdomainSystem], pivot_tol: float = DEFAULT_PI
     return out
 
 
-def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, margins=False):
+def _host_dense(a) -> bool:
+    """A dense host matrix (numpy array or CPU torch tensor)."""
+    if isinstance(a, (SparseBlock, DeviceArray)):
+        return False
+    if type(a).__module__.startswith("torch"):
+        return not a.is_cuda
+    return isinstance(a, np.ndarray)
+
+
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(t):
+    dev = t.cuda.current_device()
+    if dev not in _COPY_STREAMS:
+        _COPY_STREAMS[dev] = t.cuda.Stream()
+    return _COPY_STREAMS[dev]
+
+
+def _host_matrix_ptrs(systems, members, n):
+    """Contiguous complex128 host views of the members' A and a ctypes array
+    of their data pointers (the views are returned so they outlive the copies)."""
     t = require_cuda()
-    B = len(members)
-    A = empty((B, n, n))
-    D = t.zeros((B, n, m), dtype=t.complex128, device="cuda")
-    f = empty((B, n, r))
+    views, ptrs = [], []
+    for idx in members:
+        a = systems[idx].A
+        if type(a).__module__.startswith("torch"):
+            a = a.to(dtype=t.complex128).contiguous()
+            p = a.data_ptr()
+        else:
+            a = np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+            p = a.ctypes.data
+        if tuple(a.shape) != (n, n):
+            raise ValueError(f"domain {systems[idx].domain}: A must be {n} x {n}")
+        views.append(a)
+        ptrs.append(p)
+    return views, (_lib.ctypes.c_void_p * len(ptrs))(*ptrs)
+
+
+def _fill_inputs(systems, members, n, ms, A, D, f):
     for i, idx in enumerate(members):
         s = systems[idx]
         mr = ms[idx]
-        _fill(A[i], s.A, (n, n))
+        if A is not None:
+            _fill(A[i], s.A, (n, n))
         if mr:
             if _dev_D(s):
                 D[i, :, :mr].copy_(s._d3m_D)
@@ -276,7 +314,29 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, marg
                 _fill(D[i, :, :mr], s.couplings[0].D, (n, mr))
             else:
                 _fill(D[i, :, :mr], _coupling_matrix(s), (n, mr))
-        _fill(f[i], s.f, (n, r))
+        _fill(f[i], s.f, (n, f.shape[2]))
+
+
+def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, margins=False, A_dev=None):
+    """One batch of equal-order subdomains through d3m_schur_reduce_batched.
+
+    Dense host matrices on the panel-BK path (n > 512) take the split upload:
+    the lower row blocks of every A_d go first (d3m_copy_triangle part 0, on
+    the compute stream) and are duplicated device-side into an intact copy
+    A0; the panel BK starts on them at once (it reads nothing else: scale
+    over the lower triangle, d3m_bk_panel_batched check_sym bit 3) while a
+    copy stream uploads D, F and the upper remainder into A0 and runs the
+    symmetry check and full scale there (d3m_sym_scan_batched,
+    factor.py:94-98).  An input whose full scale differs from the lower
+    triangle's, or that fails the check, is reduced again from A0 by the
+    one-pass path, which applies the reference's check and threshold
+    exactly.  ``A_dev``: device matrices already in place (that re-run)."""
+    t = require_cuda()
+    B = len(members)
+    split = A_dev is None and n > _lib.PANEL_BK_MIN and all(_host_dense(systems[i].A) for i in members)
+    A = empty((B, n, n)) if A_dev is None else A_dev
+    D = t.zeros((B, n, m), dtype=t.complex128, device="cuda")
+    f = empty((B, n, r))
     perm = t.empty((B, n), dtype=t.int64, device="cuda")
     tags = t.empty((B, n), dtype=t.int8, device="cuda")
     n2 = t.empty(B, dtype=t.int32, device="cuda")
@@ -296,13 +356,44 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, marg
     else:
         scratch = empty((B, 4 * n)) if 64 * n > 200 * 1024 else None
         d_tasks = t.empty(64 * B, dtype=t.uint8, device="cuda")
+    mg = t.empty((B, 2), dtype=t.float64, device="cuda") if margins else None
+    flags = 1 if keep == "schur" else 0
+    if split:
+        S, cs = t.cuda.current_stream(), _copy_stream(t)
+        views, hptr = _host_matrix_ptrs(systems, members, n)
+        _lib.call("d3m_copy_triangle", B, hptr, n, _P(A), n * n, n, n, 0, 1, stream_ptr())
+        A0 = A.clone()             # one flat D2D copy (the upper halves are overwritten below)
+        cs.wait_event(S.record_event())
+        _lib.call("d3m_bk_panel_batched", B, n, _P(A), n * n, n, float(pivot_tol), 8, _P(perm), _P(tags), _P(n2),
+                  _P(gr), _P(info), _P(sc), _P(asy), _P(scratch), _P(mg), stream_ptr())
+        flags |= 2
+        sc_full = t.empty(B, dtype=t.float64, device="cuda")
+        asy_full = t.empty(B, dtype=t.float64, device="cuda")
+        red = t.empty(8 * B, dtype=t.float64, device="cuda")
+        with t.cuda.stream(cs):
+            _fill_inputs(systems, members, n, ms, None, D, f)
+            ev_df = cs.record_event()
+            cstream = _lib.ctypes.c_void_p(cs.cuda_stream)
+            _lib.call("d3m_copy_triangle", B, hptr, n, _P(A0), n * n, n, n, 1, 1, cstream)
+            _lib.call("d3m_sym_scan_batched", B, n, _P(A0), n * n, n, _P(sc_full), _P(asy_full), _P(red), cstream)
+            ev_scan = cs.record_event()
+        S.wait_event(ev_df)
+    else:
+        _fill_inputs(systems, members, n, ms, A if A_dev is None else None, D, f)
     rows, nrows = _nonzero_rows(D, n) if keep != "schur" else (None, 0)
     wd = empty((B, nrows, m)) if rows is not None else None
-    mg = t.empty((B, 2), dtype=t.float64, device="cuda") if margins else None
     _lib.call("d3m_schur_reduce_batched", B, n, m, r, _P(A), _P(D), _P(f), float(pivot_tol), _P(perm),
               _P(tags), _P(n2), _P(gr), _P(info), _P(sc), _P(asy), _P(K), _P(g), _P(wz), _P(wx), _P(wc),
-              _P(scratch), _P(d_tasks), _P(rows), int(nrows), _P(wd), 1 if keep == "schur" else 0, _P(mg),
-              stream_ptr())
+              _P(scratch), _P(d_tasks), _P(rows), int(nrows), _P(wd), flags, _P(mg), stream_ptr())
+    if split:
+        S.wait_event(ev_scan)
+        sc_h, full_h, asy_h = sc.cpu().numpy(), sc_full.cpu().numpy(), asy_full.cpu().numpy()
+        del views
+        if not np.array_equal(sc_h, full_h) or bool(np.any(asy_h > 1e-12 * full_h)):
+            del A, D, f, wz, wx, wc, K, g, scratch, wd, rows
+            return _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, margins, A_dev=A0)
+        asy.copy_(asy_full)
+        del A0
     del wd, rows
     del wz, scratch, wc
     try:
@@ -311,6 +402,7 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, marg
                             f"domain {systems[members[b]].domain} is singular: {msg}"), margin=mg)
     except (SingularDomainError, ValueError) as err:
         return (members[int(_first_bad(info))], err)
+    kh, gh = BatchHost(K), BatchHost(g)
     for i, idx in enumerate(members):
         s = systems[idx]
         mr = ms[idx]
@@ -329,8 +421,9 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, marg
         else:
             s.factor = facs[i].release()
             s._d3m_D = None
-        gi = g[i, :mr, 0] if vec else g[i, :mr, :]
-        out[idx] = (DeviceArray(K[i, :mr, :mr]), DeviceArray(gi))
+        gidx = (i, slice(0, mr), 0) if vec else (i, slice(0, mr), slice(None))
+        out[idx] = (DeviceArray(K[i, :mr, :mr], (kh, (i, slice(0, mr), slice(0, mr)))),
+                    DeviceArray(g[gidx], (gh, gidx)))
     return None
 
 
