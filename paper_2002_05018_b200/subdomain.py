@@ -393,6 +393,10 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, marg
             del A, D, f, wz, wx, wc, K, g, scratch, wd, rows
             return _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, margins, A_dev=A0)
         asy.copy_(asy_full)
+        # the reference leaves the input's upper triangle in `packed`
+        # (kernels.py:18): bring it over from the intact copy (device to device)
+        dptr = (_lib.ctypes.c_void_p * B)(*[A0.data_ptr() + 16 * n * n * b for b in range(B)])
+        _lib.call("d3m_copy_triangle", B, dptr, n, _P(A), n * n, n, n, 1, 3, stream_ptr())
         del A0
     del wd, rows
     del wz, scratch, wc

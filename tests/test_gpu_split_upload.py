@@ -44,6 +44,21 @@ def _run(systems, keep):
     return [(np.asarray(K), np.asarray(g), s.factor.perm, s.factor.tags) for (K, g), s in zip(red, systems)]
 
 
+def test_split_upload_packed_factor_keeps_the_input_upper_triangle(cuda):
+    """`packed` is the one-pass path's bit for bit: the factor below the
+    diagonal and, above it, the input's entries (kernels.py:18, "only the
+    lower triangle is read or written")."""
+    import paper_2002_05018_b200 as d
+    systems = _systems(3, 640, 40, 15)
+    dev = _device_copy(systems)
+    d.reduce_domains(systems, keep="factor")
+    d.reduce_domains(dev, keep="factor")
+    for s, s0 in zip(systems, dev):
+        P, P0 = s.factor.packed.cpu().numpy(), s0.factor.packed.cpu().numpy()
+        assert np.array_equal(P, P0)
+        assert np.array_equal(np.triu(P, 1), np.triu(np.asarray(s.A), 1))
+
+
 @pytest.mark.parametrize("host,keep", [("numpy", "factor"), ("pinned", "schur"), ("numpy", "solution")])
 def test_split_upload_bitwise_equals_device_inputs(cuda, host, keep):
     systems = _systems(3, 640, 40, 11, host)
