@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define D3M_ABI_VERSION 11
+#define D3M_ABI_VERSION 12
 
 int d3m_abi_version(void);
 const char* d3m_last_error(void);
@@ -119,6 +119,17 @@ int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stri
  * factor.py:215, subdomain.py:181,183,233. */
 int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* C, void* h_tasks, int ntasks,
                       void* d_tasks, void* stream);
+
+/* The TMA-staged update GEMM of d3m_block_ldlt_exec on one panel pair (ABI
+ * v12): X (rows_x x n) and L (rows_l x n) are contiguous row-major panels,
+ * every task has lda = ldb = k = n, a_off relative to X, b_off relative to L,
+ * and the flags of a trailing update (C -= A B^T, optionally the symmetric
+ * diagonal target).  Tile operands are staged by cp.async.bulk.tensor from
+ * tensor maps over the panels.  Results are bitwise those of
+ * d3m_zgemm_grouped(0, 0, ...).  h_tasks / d_tasks as d3m_zgemm_grouped.
+ * Replaces factor.py:215. */
+int d3m_zgemm_tma_panels(const void* X, int64_t rows_x, const void* L, int64_t rows_l, int n, void* C, void* h_tasks,
+                         int ntasks, void* d_tasks, void* stream);
 
 /* Complex product form of every grouped GEMM launched afterwards in this
  * process: 3 = Gauss 3M (three real DMMA products per complex product, the

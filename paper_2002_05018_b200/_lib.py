@@ -29,6 +29,7 @@ _SIGNATURES = {
     "d3m_plan_flow_items": [I32, P, P, P, P, P, I64, P, I64, P, P],
     "d3m_ldlt_solve_batched": [I32, I32, P, I64, P, I64, P, I64, P, I64, I32, I32, P, P],
     "d3m_zgemm_grouped": [I32, I32, P, P, P, P, I32, P, P],
+    "d3m_zgemm_tma_panels": [P, I64, P, I64, I32, P, P, I32, P, P],
     "d3m_gemm_set_form": [I32],
     "d3m_block_residual": [I32, P, P, P, P, P, P, P, P, P],
     "d3m_nonzero_rows": [I32, I32, I32, P, P, P, P, P],
@@ -87,7 +88,7 @@ _lib = None
 
 
 FLOW_EXTRA_COUNTERS = 2052  # include/d3m.h D3M_FLOW_EXTRA_COUNTERS
-ABI_VERSION = 11         # include/d3m.h D3M_ABI_VERSION this binding is written for
+ABI_VERSION = 12         # include/d3m.h D3M_ABI_VERSION this binding is written for
 
 
 def load():

@@ -364,6 +364,27 @@ int d3m_zgemm_grouped(int ta, int tb, const void* A, const void* B, void* Cm, vo
   return 0;
 }
 
+int d3m_zgemm_tma_panels(const void* X, int64_t rows_x, const void* L, int64_t rows_l, int n, void* Cm,
+                         void* h_tasks, int ntasks, void* d_tasks, void* stream) {
+  if (ntasks <= 0) return 0;
+  if (rows_x <= 0 || rows_l <= 0 || n <= 0) return fail(-22, "d3m_zgemm_tma_panels: bad shape");
+  auto* t = static_cast<d3m::GemmTask*>(h_tasks);
+  for (int i = 0; i < ntasks; ++i)
+    if (t[i].lda != n || t[i].ldb != n || t[i].k != n || t[i].a_off % n || t[i].b_off % n ||
+        (t[i].flags & ~(d3m::kGemmModeMask | d3m::kGemmSym | d3m::kGemmLowerOnly)))
+      return fail(-22, "d3m_zgemm_tma_panels: task does not fit the panel form");
+  const int tiles = d3m_gemm_prepare_tasks(t, ntasks);
+  cudaError_t e = cudaMemcpyAsync(d_tasks, t, sizeof(d3m::GemmTask) * ntasks, cudaMemcpyHostToDevice,
+                                  reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail((int)e, "d3m_zgemm_tma_panels: task upload");
+  alignas(64) unsigned char maps[256];
+  const int prc = d3m_gemm_tma_prepare(X, rows_x, L, rows_l, n, maps);
+  if (prc) return fail(prc, "d3m_zgemm_tma_panels: tensor map encoding");
+  D3M_TRY(launch(kClsGemm, stream,
+                 [&] { return d3m_gemm_tma_launch(maps, Cm, d_tasks, ntasks, tiles, 0, stream); }));
+  return 0;
+}
+
 int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const void* D, const void* f,
                              double pivot_tol, void* perm, void* tags, void* n2x2, void* growth, void* info,
                              void* scale, void* asym, void* K_out, void* g_out, void* work_z, void* work_x,
@@ -556,6 +577,8 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
     return e ? (int64_t)atoll(e) : (int64_t)5000;
   }();
   static const bool trsm_tri = [] { const char* e = getenv("D3M_TRSM_TRI"); return !(e && e[0] == '0'); }();
+  // update GEMM staging: 1 = TMA tensor copies (default), 0 = the cp.async kernel (D3M_GEMM_TMA, A/B runs)
+  static const int gemm_tma = [] { const char* e = getenv("D3M_GEMM_TMA"); return e ? atoi(e) : 1; }();
   // every column's X panel must fit its xbuf slot: checked before anything is launched
   const int nslots = lookahead ? kXSlots : 1;
   const int64_t slot_elems = xbuf_elems / nslots;
@@ -593,6 +616,7 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
     }
     linv_use = ctx->linv;
   }
+  int tma_mode = d3m_gemm_set_form(0) == 3 ? gemm_tma : 0;     // the TMA kernel is a 3M kernel
   // Streams.  lookahead = 0: everything in order on the caller's stream.
   // lookahead = 1 (etree-parallel): the critical chain of column j (BK ->
   // L^-1 -> panel TRSM -> D^-1 -> the "next" update into column j+1) runs on
@@ -717,10 +741,22 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
         }));
       }
       const int64_t t0 = h_task_ptr[j], tn = h_task_next[j], t1 = h_task_ptr[j + 1];
+      // the update launches of this column stage X_j / L_j tiles by TMA from tensor maps over the two panels
+      alignas(64) unsigned char maps[256];
+      bool col_tma = false;
+      if (tma_mode && R > 0 && t1 > t0) {
+        const int prc = d3m_gemm_tma_prepare(xbuf, R, pool + h_panel_off[j], R, nj, maps);
+        if (prc == -38) tma_mode = 0;                    // driver without tensor-map encoding: cp.async kernel
+        else if (prc) return fail(prc, "d3m_block_ldlt_exec: tensor map");
+        else col_tma = true;
+      }
       // next update (targets in column j+1): after every earlier bulk update into column j+1
       if (tn > t0) {
         if (lookahead) wait_rest(q, s0, h_sched[3 * j + 2]);
         D3M_TRY(launch(kClsGemm, s0, [&] {
+          if (col_tma)
+            return d3m_gemm_tma_launch(maps, pool, tasks + t0, (int)(tn - t0), (int)h_tiles_next[j], h_panel_off[j],
+                                       s0);
           return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + t0, (int)(tn - t0), (int)h_tiles_next[j], s0);
         }));
       }
@@ -732,6 +768,9 @@ int d3m_block_ldlt_exec(int nb, const int64_t* h_sizes, const int64_t* h_diag_of
         cudaStream_t sb = lookahead ? side : s0;
         if (lookahead) cudaStreamWaitEvent(side, ctx->ev_col[j], 0);
         D3M_TRY(launch(kClsGemm, sb, [&] {
+          if (col_tma)
+            return d3m_gemm_tma_launch(maps, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], h_panel_off[j],
+                                       sb);
           return d3m_gemm_launch(0, 0, xbuf, pool, pool, tasks + tn, (int)(t1 - tn), (int)h_tiles_rest[j], sb);
         }));
         if (lookahead) {

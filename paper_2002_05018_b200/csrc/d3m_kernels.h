@@ -109,6 +109,9 @@ int d3m_diag_block_rows();
 int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* workspace, void* stream);
 size_t d3m_bk_panel_workspace_bytes(int n, int batch);
 int d3m_sym_scan_batched_launch(d3m::BkArgs* a, int batch, void* red_ws, void* stream);
+int d3m_gemm_tma_prepare(const void* X, int64_t rows_x, const void* L, int64_t rows_l, int n, void* maps_out);
+int d3m_gemm_tma_launch(const void* maps, void* C, const void* dtasks, int ntasks, int ntiles, int64_t b_base,
+                        void* stream);
 }
 
 #include "d3m_gemm.h"

@@ -28,7 +28,9 @@
 #include "d3m_common.cuh"
 #include "d3m_gemm.h"
 #include "d3m_kernels.h"
+#include <algorithm>
 #include <cstdlib>
+#include <cuda.h>
 
 namespace d3m {
 
@@ -683,6 +685,235 @@ static int launch_half(const cplx* A, const cplx* B, cplx* C, const GemmTask* ta
   return (int)cudaGetLastError();
 }
 
+// ---- 3M half tiles staged by TMA ----------------------------------------------
+// The trailing updates of block LDL^T read whole panels (X_j in the xbuf ring,
+// L_j in the pool; lda = ldb = K = n_j), so one 2-D tensor map per panel
+// describes every task's operand tile: a task's A tile is the box at (k0,
+// a_off / lda + m0).  One elected thread issues the stage's two bulk tensor
+// copies (cp.async.bulk.tensor.2d, SASS UTMALDG) against a per-stage mbarrier;
+// the other 127 threads issue no staging instructions at all (the cp.async
+// ring spends 6 LDGSTS plus their address / predicate math per thread and
+// k-slice).  Rows past a task's block are whatever follows in the panel (they
+// only feed accumulator rows that are never written); rows past the panel and
+// k >= n_j are zero-filled by TMA.  The per-element product order is that of
+// zgemm3m_half_kernel, so the results are bitwise equal.
+//
+// Shared-memory layout per stage (tile bases 1024-byte aligned):
+//   a  64 x 8 complex, 128-byte rows, SWIZZLE_128B: 16-byte chunk c of row r at chunk c ^ (r & 7)
+//   b  32 x 8 complex, same
+// A DMMA fragment row fr (lane >> 2) is mapped to tile row pr = (fr >> 1) |
+// ((fr & 1) << 2) of its 8-row group: a quarter warp's LDS.128 then covers the
+// rows {q, q + 4} x 4 chunks, which the swizzle puts in different 64-byte
+// halves (conflict-free).  The same map applies to B's rows, i.e. to the
+// columns of C: accumulator (i, j, h) of a lane is C(wm + 8i + pr, wn + 8j +
+// fc + 4h), so a store instruction writes 64 contiguous bytes per row.
+struct alignas(1024) TStage {
+  cplx a[BM][BKC];
+  cplx b[HN][BKC];
+  cplx pad_[(32 * HCP_PITCH > (BM + HN) * BKC) ? 32 * HCP_PITCH - (BM + HN) * BKC : 0];   // room for a 32-row C chunk
+};
+static_assert(32 * HCP_PITCH * sizeof(cplx) <= sizeof(TStage), "a 32-row C chunk fits a freed stage");
+constexpr size_t kTSmem = sizeof(TStage) * STAGES + 1024;      // + manual 1024-byte alignment
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smaddr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smaddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smaddr(b)), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(HNT, 3)
+zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, cplx* Cbase,
+                   const GemmTask* __restrict__ tasks, int ntasks, int64_t b_base) {
+  extern __shared__ unsigned char smem_dyn[];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  TStage* st = reinterpret_cast<TStage*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mb_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  const int tile = blockIdx.x >> 1, half = blockIdx.x & 1;
+  const GemmTask tk = tasks[find_task(tasks, ntasks, tile)];      // (its barrier publishes the mbarrier inits)
+  int local = tile - tk.tile_start, tm, tn;
+  const bool sym = (tk.flags & kGemmSym) != 0;
+  if (sym) {
+    tm = (int)((sqrt(8.0 * local + 1.0) - 1.0) * 0.5);
+    while ((tm + 1) * (tm + 2) / 2 <= local) ++tm;
+    while (tm * (tm + 1) / 2 > local) --tm;
+    tn = local - tm * (tm + 1) / 2;
+  } else {
+    tm = local / tk.tiles_n;
+    tn = local - tm * tk.tiles_n;
+  }
+  const int M = tk.m, N = tk.n, K = tk.k;
+  const int m0 = tm * BM, n0 = tn * BN + half * HN;
+  if (m0 >= M || n0 >= N) return;
+  cplx* C = Cbase + tk.c_off;
+  const int arow = (int)(tk.a_off / tk.lda) + m0;               // panel rows of the tile's first A / B row
+  const int brow = (int)((tk.b_off - b_base) / tk.ldb) + n0;
+  const int ktiles = (K + BKC - 1) / BKC;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 16;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int pr = (fr >> 1) | ((fr & 1) << 2);
+  constexpr unsigned kStageBytes = (unsigned)(sizeof(cplx) * (BM + HN) * BKC);
+  auto issue = [&](int slot, int kt) {                          // thread 0 only
+    mb_expect_tx(&full[slot], kStageBytes);
+    tma_load_2d(&st[slot].a[0][0], &mapA, 2 * kt * BKC, arow, &full[slot]);
+    tma_load_2d(&st[slot].b[0][0], &mapB, 2 * kt * BKC, brow, &full[slot]);
+  };
+  double P3[4][2][2], Q3[4][2][2], R3[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) P3[i][j][0] = P3[i][j][1] = Q3[i][j][0] = Q3[i][j][1] = R3[i][j][0] = R3[i][j][1] = 0.0;
+  const int mode = tk.flags & kGemmModeMask;
+  const bool cpre = (!sym || (tk.flags & kGemmLowerOnly)) && mode != kGemmStore && ktiles >= STAGES;
+  if (t == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s)
+      if (s < ktiles) issue(s, s);
+  }
+  const int ca0 = fc ^ pr, ca1 = (4 + fc) ^ pr;          // swizzled chunk of k = kk*4 + fc in this lane's rows
+  for (int kt = 0; kt < ktiles; ++kt) {
+    __syncthreads();                       // every warp is done with slot (kt - 1) % STAGES
+    const int nk = kt + STAGES - 1;
+    if (nk < ktiles) {
+      if (t == 0) issue(nk % STAGES, nk);
+    } else if (cpre && nk - ktiles < 2) {  // C rows [32c, 32c+32) into the freed stage
+      const int ch = nk - ktiles;
+      cplx* dst = reinterpret_cast<cplx*>(&st[nk % STAGES]);
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int e = p * HNT + t, r = e >> 5, c = e & 31;
+        const int gr = m0 + ch * 32 + r;
+        const bool ok = gr < M && n0 + c < N;
+        cp_async16(dst + r * HCP_PITCH + c, ok ? C + (int64_t)gr * tk.ldc + n0 + c : C, ok);
+      }
+      cp_commit();
+    }
+    mb_wait(&full[kt % STAGES], (unsigned)(kt / STAGES) & 1u);
+    const TStage& S = st[kt % STAGES];
+#pragma unroll
+    for (int kk = 0; kk < BKC / 4; ++kk) {
+      const int ca = kk ? ca1 : ca0;
+      double bre[2], bim[2], bsum[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const cplx b = S.b[wn + j * 8 + pr][ca];
+        bre[j] = b.x;
+        bim[j] = b.y;
+        bsum[j] = b.x + b.y;
+      }
+      cplx a[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = S.a[wm + i * 8 + pr][ca];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double asum = a[i].x + a[i].y;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(P3[i][j][0], P3[i][j][1], a[i].x, bre[j]);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(Q3[i][j][0], Q3[i][j][1], a[i].y, bim[j]);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(R3[i][j][0], R3[i][j][1], asum, bsum[j]);
+      }
+    }
+  }
+  cp_wait<0>();
+  const bool mirror = sym && !(tk.flags & kGemmLowerOnly);
+  const int ldc = tk.ldc;
+  if (cpre) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rl = wm + i * 8 + pr, r = m0 + rl, ch = rl >> 5;
+      const cplx* crow = reinterpret_cast<const cplx*>(&st[(ktiles + ch) % STAGES]) + (rl & 31) * HCP_PITCH;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cl = wn + j * 8 + fc + 4 * h, c = n0 + cl;
+          if (r >= M || c >= N || (sym && c > r)) continue;
+          const double p = P3[i][j][h], q = Q3[i][j][h];
+          const cplx u = mk(p - q, (R3[i][j][h] - p) - q);
+          C[(int64_t)r * ldc + c] = mode == kGemmSub ? c_sub(crow[cl], u) : c_add(crow[cl], u);
+        }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = m0 + wm + i * 8 + pr;
+      cplx cv[2][2], cq[2][2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = n0 + wn + j * 8 + fc + 4 * h;
+          const bool ok = r < M && c < N && (!sym || c <= r);
+          cv[j][h] = mk(0.0, 0.0);
+          cq[j][h] = mk(0.0, 0.0);
+          if (ok && mode != kGemmStore) cv[j][h] = C[(int64_t)r * ldc + c];
+          if (ok && mirror && c < r) cq[j][h] = C[(int64_t)c * ldc + r];
+        }
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = n0 + wn + j * 8 + fc + 4 * h;
+          if (r >= M || c >= N) continue;
+          const double p = P3[i][j][h], q = Q3[i][j][h];
+          const cplx u = mk(p - q, (R3[i][j][h] - p) - q);
+          if (sym) {
+            if (c > r) continue;
+            C[(int64_t)r * ldc + c] = c_sub(cv[j][h], u);
+            if (mirror && c < r) C[(int64_t)c * ldc + r] = c_sub(cq[j][h], u);
+          } else {
+            cplx* pc = C + (int64_t)r * ldc + c;
+            if (mode == kGemmSub) *pc = c_sub(cv[j][h], u);
+            else if (mode == kGemmStore) *pc = u;
+            else *pc = c_add(cv[j][h], u);
+          }
+        }
+    }
+  }
+}
+
+using TmapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TmapEncodeFn tmap_encoder() {
+  static const TmapEncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<TmapEncodeFn>(p);
+  }();
+  return fn;
+}
+
+// 2-D map over `rows` rows of `cols` doubles (row pitch `pitch_bytes`), box box_cols x box_rows
+static int tmap_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t pitch_bytes, int box_cols,
+                   int box_rows, CUtensorMapSwizzle sw) {
+  const TmapEncodeFn enc = tmap_encoder();
+  if (!enc) return -38;
+  const cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t gstr[1] = {(cuuint64_t)pitch_bytes};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t est[2] = {1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), gdim, gstr, box, est,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -22;
+}
+
 template <bool TA, bool TB>
 static int launch_t(const cplx* A, const cplx* B, cplx* C, const GemmTask* tasks, int ntasks, int ntiles,
                     const LaunchExtra& x, cudaStream_t s) {
@@ -744,6 +975,37 @@ extern "C" int d3m_gemm_set_form(int form) {
 extern "C" int d3m_gemm_launch(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
                                int ntasks, int ntiles, void* stream) {
   return gemm_launch_x(ta, tb, A, B, C, dtasks, ntasks, ntiles, d3m::LaunchExtra{nullptr, nullptr}, stream);
+}
+
+// ---- TMA-staged trailing updates (zgemm3m_tma_kernel) -------------------------
+// d3m_gemm_tma_prepare: encode the tensor maps of the panels X (rows_x x n,
+// contiguous rows) and L (rows_l x n) into maps_out (host memory, 2 x
+// sizeof(CUtensorMap) = 256 bytes).  Returns -38 when the driver has no
+// cuTensorMapEncodeTiled (the caller then uses the cp.async kernel).
+extern "C" int d3m_gemm_tma_prepare(const void* X, int64_t rows_x, const void* L, int64_t rows_l, int n,
+                                    void* maps_out) {
+  using namespace d3m;
+  if (rows_x <= 0 || rows_l <= 0 || n <= 0) return -22;
+  auto* m = static_cast<CUtensorMap*>(maps_out);
+  int rc = tmap_2d(&m[0], X, rows_x, 2 * (int64_t)n, (int64_t)n * 16, 2 * BKC, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = tmap_2d(&m[1], L, rows_l, 2 * (int64_t)n, (int64_t)n * 16, 2 * BKC, HN, CU_TENSOR_MAP_SWIZZLE_128B);
+  return rc;
+}
+
+// Launch the tasks (kGemmSub / kGemmSym targets, a_off relative to X, b_off
+// relative to Bbase with the L panel at b_base; lda = ldb = k = n of the
+// prepared panels) on the TMA kernel.
+extern "C" int d3m_gemm_tma_launch(const void* maps, void* C, const void* dtasks, int ntasks, int ntiles,
+                                   int64_t b_base, void* stream) {
+  using namespace d3m;
+  if (ntiles <= 0 || ntasks <= 0) return 0;
+  auto* m = static_cast<const CUtensorMap*>(maps);
+  static PerDeviceOnce configured;
+  if (configured.first())
+    cudaFuncSetAttribute(zgemm3m_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
+  zgemm3m_tma_kernel<<<2 * ntiles, HNT, kTSmem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      m[0], m[1], static_cast<cplx*>(C), static_cast<const GemmTask*>(dtasks), ntasks, b_base);
+  return (int)cudaGetLastError();
 }
 
 // Launch with a column-gather permutation for kGemmTriGather tasks (A not transposed).
