@@ -312,7 +312,7 @@ def run_ours(args):
                           "executes 6, so this is an effective fraction" if form == 3 else
                           "value counts algorithmic flops (8 per complex FMA, executed as 4 real DMMA products)"),
         "gemm_form": f"{form}m",
-        "roofline": {"bound": "tensor", "kernel": ("zgemm3m_half_kernel (3M, 64x32 half tiles" if form == 3 else "zgemm_grouped_kernel (4M")
+        "roofline": {"bound": "tensor", "kernel": ("zgemm3m_tma_kernel (3M, 64x32 half tiles, TMA-staged" if form == 3 else "zgemm_grouped_kernel (4M")
                                + "; trailing Schur updates, DMMA)",
                      "timing": "EXECUTED update DMMA flops (algorithmic x form/4) / union of the update-GEMM "
                                "CUDA-event intervals in the instrumented timed region (2)",
@@ -321,10 +321,10 @@ def run_ours(args):
                      "peak_source": "live DMMA m8n8k4 probe (tools/fp64_peak.cu)" if peak_live else
                      "profiles/fp64_peak_r01.txt (measured DMMA burst)",
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if achieved else None,
-                     "traffic": 1.664e9,
-                     "traffic_note": "DRAM bytes per launch of a representative 11,628-tile rest-update launch "
-                                     "(ncu --set full, profiles/ncu_gemm3m_half_cfg4_r01o_summary.txt, 3M half "
-                                     "tiles); algorithmic C traffic of that launch 1.524e9 B (1.09x)"},
+                     "traffic": 7.616e8,
+                     "traffic_note": "DRAM bytes per launch of a representative 5,460-tile rest-update launch "
+                                     "(ncu --set full, profiles/ncu_gemm_tma_cfg4_r02_summary.txt); algorithmic C "
+                                     "traffic of that launch 7.157e8 B (1.06x)"},
         "instrumented_ms_per_step": round(ms_step_instr, 3),
         "stage_ms_per_step": {k: round(v / args.steps, 3) for k, v in cnt["union_ms"].items()},
         "stage_ms_summed_per_step": {k: round(v / args.steps, 3) for k, v in cnt["ms"].items()},

@@ -89,6 +89,88 @@ __global__ void __launch_bounds__(128, 3) mix(double* out, int iters) {
   if (s == 12345.0) out[0] = s;
 }
 
+
+// Issue-order variants of the kernel's mix (LDS + DADD + DMMA), DMMAs in volatile asm so their order is the source's:
+// ORDER 0: per fragment row i: sum, P, Q, R (the kernel's order)
+// ORDER 1: all six sums at the top of the step, then all P, all Q, all R (R products >= 16 DMMAs behind their sums)
+// ORDER 2: the sums of step s+1 are formed at the end of step s from prefetched fragments (one step ahead)
+template <int ORDER>
+__global__ void __launch_bounds__(128, 3) mixo(double* out, int iters) {
+  __shared__ double2 sa[64][12], sb[32][12];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int e = t; e < 64 * 12; e += 128) sa[e / 12][e % 12] = make_double2(1.0 + e * 1e-9, 1.0 - e * 1e-9);
+  for (int e = t; e < 32 * 12; e += 128) sb[e / 12][e % 12] = make_double2(1.0 - e * 1e-9, 1.0 + e * 1e-9);
+  __syncthreads();
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 16, fr = lane >> 2, fc = lane & 3;
+  double P[4][2][2] = {}, Q[4][2][2] = {}, R[4][2][2] = {};
+  double2 a[4], b[2];
+  double as[4], bs[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) { b[j] = sb[wn + j * 8 + fr][fc]; bs[j] = b[j].x + b[j].y; }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { a[i] = sa[wm + i * 8 + fr][fc]; as[i] = a[i].x + a[i].y; }
+  for (int it = 0; it < 2 * iters; ++it) {
+    const int ko = (fc + 4 * it + (it >> 1)) & 7;
+    double2 an[4], bn[2];
+    if (ORDER == 2) {                       // prefetch the next step's fragments
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bn[j] = sb[wn + j * 8 + fr][ko];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) an[i] = sa[wm + i * 8 + fr][ko];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = sb[wn + j * 8 + fr][ko];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = sa[wm + i * 8 + fr][ko];
+    }
+    if (ORDER == 0) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bs[j] = b[j].x + b[j].y;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double asum = a[i].x + a[i].y;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(P[i][j][0], P[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(Q[i][j][0], Q[i][j][1], a[i].y, b[j].y);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(R[i][j][0], R[i][j][1], asum, bs[j]);
+      }
+    } else {
+      if (ORDER == 1) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) bs[j] = b[j].x + b[j].y;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) as[i] = a[i].x + a[i].y;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(P[i][j][0], P[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(Q[i][j][0], Q[i][j][1], a[i].y, b[j].y);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(R[i][j][0], R[i][j][1], as[i], bs[j]);
+      if (ORDER == 2) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) { b[j] = bn[j]; bs[j] = bn[j].x + bn[j].y; }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { a[i] = an[i]; as[i] = an[i].x + an[i].y; }
+      }
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) s += P[i][j][0] + P[i][j][1] + Q[i][j][0] + Q[i][j][1] + R[i][j][0] + R[i][j][1];
+  if (s == 12345.0) out[0] = s;
+}
+
 template <typename F>
 float timeit(F f) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -113,6 +195,9 @@ int main() {
   ms = timeit([&] { mix<2><<<blocks, 128>>>(out, iters); }); printf("DMMA + LDS                : %6.2f TFLOP/s\n", flops / ms / 1e9);
   ms = timeit([&] { mix<3><<<blocks, 128>>>(out, iters); }); printf("DMMA + LDS + DADD (kernel): %6.2f TFLOP/s\n", flops / ms / 1e9);
   ms = timeit([&] { mix<4><<<blocks, 128>>>(out, iters); }); printf("DMMA + LDS + sum plane    : %6.2f TFLOP/s\n", flops / ms / 1e9);
+  ms = timeit([&] { mixo<0><<<blocks, 128>>>(out, iters); }); printf("order 0 (kernel: sum,P,Q,R per row)   : %6.2f TFLOP/s\n", flops / ms / 1e9);
+  ms = timeit([&] { mixo<1><<<blocks, 128>>>(out, iters); }); printf("order 1 (sums first, P*,Q*,R*)        : %6.2f TFLOP/s\n", flops / ms / 1e9);
+  ms = timeit([&] { mixo<2><<<blocks, 128>>>(out, iters); }); printf("order 2 (sums one step ahead)         : %6.2f TFLOP/s\n", flops / ms / 1e9);
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
