@@ -36,6 +36,19 @@ struct BkState {          // 64 bytes per matrix
 };
 static_assert(sizeof(BkState) == 64, "BkState layout");
 
+#ifdef D3M_PANEL_PROFILE
+// phase clocks of matrix 0's rank-0 CTA (thread 0), summed over the panel launches (profiling builds only;
+// tools/panel_profile.sh): 0 gemv(k) 1 argmax(k) 2 cluster merge 3 gemv(imax) 4 argmax + merge (imax)
+// 5 interchange 6 L store 7 loop top; 8 steps 9 rowmax steps 10 interchanges
+__device__ double g_panel_prof[16];
+#define PANEL_MARK(slot) do { if (prof_on) { long long t_ = clock64(); pacc[slot] += (double)(t_ - prof_t); \
+    prof_t = t_; } } while (0)
+#define PANEL_COUNT(slot) do { if (prof_on) pacc[slot] += 1.0; } while (0)
+#else
+#define PANEL_MARK(slot) do { } while (0)
+#define PANEL_COUNT(slot) do { } while (0)
+#endif
+
 template <int NT>
 __device__ __forceinline__ double pmax_red(double v, double* slots) {
   v = warp_max(v);
@@ -339,11 +352,19 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
   double mdec = s.mdec, mgap = s.mgap;
   // a step starts only while kw <= NB-2, so a panel is NB-1 or NB columns
   // (zlasyf's exit rule) and the trailing update has K <= NB = 16
+#ifdef D3M_PANEL_PROFILE
+  const bool prof_on = blockIdx.x == 0 && tid == 0;
+  double pacc[16] = {};
+  long long prof_t = clock64();
+#endif
   while (kw < NB - 1 && k < n) {
+    PANEL_MARK(7);
+    PANEL_COUNT(8);
     // -- A: column k up to date into Wp[:, kw] for the own rows, then the
     //    cluster's exact colmax / imax below the diagonal and |a_kk|
     panel_gemv<NB, CNT>(W, lda, max(k, lo), hi, k0, kw, k, Wp, k, Wp + kw);
     __syncthreads();
+    PANEL_MARK(0);
     {
       double ev, ev2 = -1.0;
       int ei;
@@ -356,8 +377,10 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
         sl.own = (k >= lo && k < hi) ? x_abs(Wp[(int64_t)k * LDW + kw]) : -1.0;
       }
     }
+    PANEL_MARK(1);
     cl.sync();
     const ClSlot m1 = cl_merge<CS>(cl, &slots[par], &merged, track);
+    PANEL_MARK(2);
     par ^= 1;
     const double absakk = m1.own;
     double colmax = 0.0;
@@ -379,8 +402,10 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
     } else {
       // -- C: column imax up to date into Wp[:, kw+1], then the cluster's
       //    exact rowmax (diagonal entry imax excluded) and |a_imax,imax|
+      PANEL_COUNT(9);
       panel_gemv<NB, CNT>(W, lda, max(k, lo), hi, k0, kw, imax, Wp, imax, Wp + kw + 1);
       __syncthreads();
+      PANEL_MARK(3);
       {
         double ev;
         int ei;
@@ -394,6 +419,7 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
       }
       cl.sync();
       const ClSlot m2 = cl_merge<CS>(cl, &slots[par], &merged);
+      PANEL_MARK(4);
       par ^= 1;
       const double rowmax = fmax(0.0, m2.ev);
       const double absimax = m2.own;
@@ -442,6 +468,8 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
     } else {
       __syncthreads();
     }
+    if (kp != kk) PANEL_COUNT(10);
+    PANEL_MARK(5);
     // -- E: store D and the L column(s) of the own rows (packed layout,
     //    kernels.py:7-22)
     if (kstep == 1) {
@@ -485,9 +513,14 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
     }
     ++npiv;
     __syncthreads();
+    PANEL_MARK(6);
     k += kstep;
     kw += kstep;
   }
+#ifdef D3M_PANEL_PROFILE
+  if (prof_on)
+    for (int i = 0; i < 16; ++i) atomicAdd(&g_panel_prof[i], pacc[i]);
+#endif
   if (lead) {
     s.k = k;
     s.info = info;
@@ -661,6 +694,18 @@ extern "C" int d3m_sym_scan_batched_launch(d3m::BkArgs* a, int batch, void* red_
   sym_scan_store_kernel<<<(batch + 127) / 128, 128, 0, s>>>(red, a->scale, a->asym, batch);
   return (int)cudaGetLastError();
 }
+
+#ifdef D3M_PANEL_PROFILE
+extern "C" int d3m_panel_prof_read(double* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, d3m::g_panel_prof, sizeof(double) * 16);
+  if (reset) {
+    double z[16] = {};
+    cudaMemcpyToSymbol(d3m::g_panel_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 extern "C" size_t d3m_bk_panel_workspace_bytes(int n, int batch) {
   return (size_t)batch * ((size_t)n * d3m::kPanelLdwMax * 16 + 64 + 64 + 8 + 64) + 256;
