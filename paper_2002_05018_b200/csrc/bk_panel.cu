@@ -18,6 +18,7 @@
 // ratio).
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 #include <cooperative_groups.h>
 #include "d3m_common.cuh"
 #include "d3m_gemm.h"
@@ -521,6 +522,10 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
   if (prof_on)
     for (int i = 0; i < 16; ++i) atomicAdd(&g_panel_prof[i], pacc[i]);
 #endif
+  // the TMA-staged trailing update reads B = Wp in 16-column k-slices: a panel of NB - 1 columns
+  // leaves column kw of the slice, which must read as zero (its A partner is the first trailing column)
+  if (info < 0 && k < n && (kw & 15))
+    for (int i = max(k, lo) + tid; i < hi; i += CNT) Wp[(int64_t)i * LDW + kw] = mk(0.0, 0.0);
   if (lead) {
     s.k = k;
     s.info = info;
@@ -570,7 +575,7 @@ constexpr int kPanelLdwMax = 129;     // workspace row pitch for the widest pane
 // rank-<= NB trailing updates of all matrices run as one grouped GEMM launch.
 template <int NB>
 static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* tasks, unsigned long long* tmax,
-                     cudaStream_t s, void* stream) {
+                     void* d_maps, cudaStream_t s, void* stream) {
   const int n = a->n;
   cudaError_t e;
   // CTAs per matrix: the largest cluster size whose CTAs (two per SM) fill
@@ -619,7 +624,9 @@ static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* task
       // rank-<=NB trailing update on the pipelined grouped kernel (C
       // prefetched into freed ring stages; 4% faster on config 3 than a
       // small-K kernel that staged C with A and B, since removed)
-      const int rc = d3m_gemm_launch_tm(0, 0, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream);
+      const int rc = d_maps ? d3m_gemm_tma_launch_batched(d_maps, a->W, tasks, batch, batch * maxtiles, a->stride_w,
+                                                         (int64_t)n * (NB + 1), tmax, stream)
+                            : d3m_gemm_launch_tm(0, 0, a->W, Wp, a->W, tasks, batch, batch * maxtiles, tmax, stream);
       if (rc) return rc;
     }
   }
@@ -650,6 +657,26 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
   unsigned long long* tmax = reinterpret_cast<unsigned long long*>(w);
   w += (size_t)batch * sizeof(unsigned long long);
   unsigned long long* red = reinterpret_cast<unsigned long long*>(w);
+  w += (size_t)batch * 8 * sizeof(unsigned long long);
+  // TMA-staged trailing updates (3M form): per matrix a tensor-map pair over W_b (n x n, pitch lda) and
+  // over its X workspace Wp_b (n x (nb + 1)), encoded on the host and copied once per factorisation
+  // (D3M_PANEL_TMA=0: the cp.async grouped kernel).  Bitwise the same factor; BK class time config 5
+  // 8.18 -> 7.67 s, config 2 65.1 -> 63.7 ms, config 3 63.6 -> 62.6 ms
+  const char* tma_str = getenv("D3M_PANEL_TMA");
+  const int tma_env = tma_str ? atoi(tma_str) : -1;
+  void* d_maps = nullptr;
+  if (tma_env != 0 && d3m_gemm_set_form(0) == 3) {
+    std::vector<unsigned char> hm((size_t)batch * 256);
+    const int rc = d3m_gemm_tma_prepare_batched(a->W, a->stride_w, n, n, a->lda, Wp, (int64_t)n * (nb + 1), n, nb + 1,
+                                                nb + 1, batch, hm.data());
+    if (rc == 0) {
+      d_maps = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(w) + 127) & ~uintptr_t(127));
+      // (pageable source: staged before the call returns)
+      if (cudaMemcpyAsync(d_maps, hm.data(), hm.size(), cudaMemcpyHostToDevice, s) != cudaSuccess) d_maps = nullptr;
+    } else if (rc != -38) {
+      return rc;
+    }
+  }
   cudaMemsetAsync(red, 0, (size_t)batch * 8 * sizeof(unsigned long long), s);
   const int nt = (n + 31) / 32, ntile = nt * (nt + 1) / 2;
   const dim3 sgrid(std::min(ntile, 256), batch);
@@ -659,8 +686,8 @@ extern "C" int d3m_bk_panel_batched_launch(d3m::BkArgs* a, int batch, void* work
   bk_panel_state_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, red, batch);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
-  const int rc = nb == 128 ? panel_run<128>(a, batch, st, Wp, tasks, tmax, s, stream)
-                            : panel_run<64>(a, batch, st, Wp, tasks, tmax, s, stream);
+  const int rc = nb == 128 ? panel_run<128>(a, batch, st, Wp, tasks, tmax, d_maps, s, stream)
+                            : panel_run<64>(a, batch, st, Wp, tasks, tmax, d_maps, s, stream);
   if (rc) return rc;
   bk_panel_finalize_kernel<<<(batch + 127) / 128, 128, 0, s>>>(*a, st, batch);
   return (int)cudaGetLastError();
@@ -708,5 +735,5 @@ extern "C" int d3m_panel_prof_read(double* out, int reset) {
 #endif
 
 extern "C" size_t d3m_bk_panel_workspace_bytes(int n, int batch) {
-  return (size_t)batch * ((size_t)n * d3m::kPanelLdwMax * 16 + 64 + 64 + 8 + 64) + 256;
+  return (size_t)batch * ((size_t)n * d3m::kPanelLdwMax * 16 + 64 + 64 + 8 + 64 + 256) + 512;   // + tensor maps
 }

@@ -112,9 +112,14 @@ int d3m_sym_scan_batched_launch(d3m::BkArgs* a, int batch, void* red_ws, void* s
 int d3m_gemm_tma_prepare(const void* X, int64_t rows_x, const void* L, int64_t rows_l, int n, void* maps_out);
 int d3m_gemm_tma_launch(const void* maps, void* C, const void* dtasks, int ntasks, int ntiles, int64_t b_base,
                         void* stream);
+int d3m_gemm_tma_prepare_batched(const void* A, int64_t a_stride, int64_t a_rows, int a_cols, int lda, const void* B,
+                                 int64_t b_stride, int64_t b_rows, int b_cols, int ldb, int batch, void* h_maps);
+int d3m_gemm_tma_launch_batched(const void* d_maps, void* C, const void* dtasks, int ntasks, int ntiles,
+                                int64_t a_stride, int64_t b_stride, void* tmax, void* stream);
 }
 
 #include "d3m_gemm.h"
 extern "C" int d3m_gemm_prepare_tasks(d3m::GemmTask* tasks, int ntasks);
+extern "C" int d3m_gemm_set_form(int form);
 extern "C" int d3m_gemm_launch_tm(int ta, int tb, const void* A, const void* B, void* C, const void* dtasks,
                                   int ntasks, int ntiles, void* tmax, void* stream);

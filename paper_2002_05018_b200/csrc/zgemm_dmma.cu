@@ -728,9 +728,15 @@ __device__ __forceinline__ void mb_expect_tx(uint64_t* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smaddr(b)), "r"(bytes) : "memory");
 }
 
+// BATCH: one pair of tensor maps per matrix in global memory (gmaps[2 b], gmaps[2 b + 1], b = the
+// task's pad_), operand offsets relative to the matrix (a_off - b * a_stride = row * lda + first column,
+// b_off - b * b_stride = row * ldb), and the running maximum of the written |C|^2 (kGemmTrackMax) -- the
+// batched trailing updates of the subdomain panel BK (bk_panel.cu).
+template <bool BATCH>
 __global__ void __launch_bounds__(HNT, 3)
 zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, cplx* Cbase,
-                   const GemmTask* __restrict__ tasks, int ntasks, int64_t b_base) {
+                   const GemmTask* __restrict__ tasks, int ntasks, int64_t b_base, const CUtensorMap* gmaps,
+                   int64_t a_stride, int64_t b_stride, unsigned long long* tmax) {
   extern __shared__ unsigned char smem_dyn[];
   __shared__ __align__(8) uint64_t full[TSTAGES];
   TStage* st = reinterpret_cast<TStage*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
@@ -757,8 +763,19 @@ zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
   const int m0 = tm * BM, n0 = tn * BN + half * HN;
   if (m0 >= M || n0 >= N) return;
   cplx* C = Cbase + tk.c_off;
-  const int arow = (int)(tk.a_off / tk.lda) + m0;               // panel rows of the tile's first A / B row
-  const int brow = (int)((tk.b_off - b_base) / tk.ldb) + n0;
+  int arow, brow, acol = 0;                                     // panel rows of the tile's first A / B row
+  const CUtensorMap *pmA = &mapA, *pmB = &mapB;
+  if constexpr (BATCH) {
+    const int arel = (int)(tk.a_off - tk.pad_ * a_stride);
+    arow = arel / tk.lda + m0;
+    acol = arel % tk.lda;
+    brow = (int)((tk.b_off - tk.pad_ * b_stride) / tk.ldb) + n0;
+    pmA = gmaps + 2 * tk.pad_;
+    pmB = pmA + 1;
+  } else {
+    arow = (int)(tk.a_off / tk.lda) + m0;
+    brow = (int)((tk.b_off - b_base) / tk.ldb) + n0;
+  }
   const int ktiles = (K + TKS * BKC - 1) / (TKS * BKC);
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 16;
   const int fr = lane >> 2, fc = lane & 3;
@@ -768,8 +785,8 @@ zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     mb_expect_tx(&full[slot], kStageBytes);
 #pragma unroll
     for (int h = 0; h < TKS; ++h) {
-      tma_load_2d(&st[slot].a[h][0][0], &mapA, 2 * (kt * TKS + h) * BKC, arow, &full[slot]);
-      tma_load_2d(&st[slot].b[h][0][0], &mapB, 2 * (kt * TKS + h) * BKC, brow, &full[slot]);
+      tma_load_2d(&st[slot].a[h][0][0], pmA, 2 * (acol + (kt * TKS + h) * BKC), arow, &full[slot]);
+      tma_load_2d(&st[slot].b[h][0][0], pmB, 2 * (kt * TKS + h) * BKC, brow, &full[slot]);
     }
   };
   double P3[4][2][2], Q3[4][2][2], R3[4][2][2];
@@ -833,6 +850,7 @@ zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
   cp_wait<0>();
   const bool mirror = sym && !(tk.flags & kGemmLowerOnly);
   const int ldc = tk.ldc;
+  double tm2 = 0.0;
   if (cpre) {
     __syncthreads();
 #pragma unroll
@@ -847,7 +865,9 @@ zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
           if (r >= M || c >= N || (sym && c > r)) continue;
           const double p = P3[i][j][h], q = Q3[i][j][h];
           const cplx u = mk(p - q, (R3[i][j][h] - p) - q);
-          C[(int64_t)r * ldc + c] = mode == kGemmSub ? c_sub(crow[cl], u) : c_add(crow[cl], u);
+          const cplx w = mode == kGemmSub ? c_sub(crow[cl], u) : c_add(crow[cl], u);
+          C[(int64_t)r * ldc + c] = w;
+          if constexpr (BATCH) tm2 = fmax(tm2, w.x * w.x + w.y * w.y);
         }
     }
   } else {
@@ -876,7 +896,9 @@ zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
           const cplx u = mk(p - q, (R3[i][j][h] - p) - q);
           if (sym) {
             if (c > r) continue;
-            C[(int64_t)r * ldc + c] = c_sub(cv[j][h], u);
+            const cplx w = c_sub(cv[j][h], u);
+            C[(int64_t)r * ldc + c] = w;
+            if constexpr (BATCH) tm2 = fmax(tm2, w.x * w.x + w.y * w.y);
             if (mirror && c < r) C[(int64_t)c * ldc + r] = c_sub(cq[j][h], u);
           } else {
             cplx* pc = C + (int64_t)r * ldc + c;
@@ -885,6 +907,12 @@ zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             else *pc = c_add(cv[j][h], u);
           }
         }
+    }
+  }
+  if constexpr (BATCH) {
+    if ((tk.flags & kGemmTrackMax) != 0 && tmax != nullptr) {   // non-negative doubles order like their bit patterns
+      tm2 = warp_max(tm2);
+      if (lane == 0) atomicMax(tmax + tk.pad_, (unsigned long long)__double_as_longlong(tm2));
     }
   }
 }
@@ -1007,9 +1035,42 @@ extern "C" int d3m_gemm_tma_launch(const void* maps, void* C, const void* dtasks
   auto* m = static_cast<const CUtensorMap*>(maps);
   static PerDeviceOnce configured;
   if (configured.first())
-    cudaFuncSetAttribute(zgemm3m_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
-  zgemm3m_tma_kernel<<<2 * ntiles, HNT, kTSmem, reinterpret_cast<cudaStream_t>(stream)>>>(
-      m[0], m[1], static_cast<cplx*>(C), static_cast<const GemmTask*>(dtasks), ntasks, b_base);
+    cudaFuncSetAttribute(zgemm3m_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
+  zgemm3m_tma_kernel<false><<<2 * ntiles, HNT, kTSmem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      m[0], m[1], static_cast<cplx*>(C), static_cast<const GemmTask*>(dtasks), ntasks, b_base, nullptr, 0, 0, nullptr);
+  return (int)cudaGetLastError();
+}
+
+// Batched form: per matrix b a map pair over its A matrix (rows x cols complex, leading dimension lda)
+// and its B matrix, encoded into h_maps (2 * batch CUtensorMap, host) by d3m_gemm_tma_prepare_batched and
+// copied by the caller into d_maps (device, 64-byte aligned).  Tasks carry the matrix index in pad_.
+extern "C" int d3m_gemm_tma_prepare_batched(const void* A, int64_t a_stride, int64_t a_rows, int a_cols, int lda,
+                                            const void* B, int64_t b_stride, int64_t b_rows, int b_cols, int ldb,
+                                            int batch, void* h_maps) {
+  using namespace d3m;
+  auto* m = static_cast<CUtensorMap*>(h_maps);
+  for (int b = 0; b < batch; ++b) {
+    int rc = tmap_2d(&m[2 * b], static_cast<const cplx*>(A) + b * a_stride, a_rows, 2 * (int64_t)a_cols,
+                     (int64_t)lda * 16, 2 * BKC, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (!rc)
+      rc = tmap_2d(&m[2 * b + 1], static_cast<const cplx*>(B) + b * b_stride, b_rows, 2 * (int64_t)b_cols,
+                   (int64_t)ldb * 16, 2 * BKC, HN, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+extern "C" int d3m_gemm_tma_launch_batched(const void* d_maps, void* C, const void* dtasks, int ntasks, int ntiles,
+                                           int64_t a_stride, int64_t b_stride, void* tmax, void* stream) {
+  using namespace d3m;
+  if (ntiles <= 0 || ntasks <= 0) return 0;
+  static PerDeviceOnce configured;
+  if (configured.first())
+    cudaFuncSetAttribute(zgemm3m_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
+  CUtensorMap dummy{};
+  zgemm3m_tma_kernel<true><<<2 * ntiles, HNT, kTSmem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      dummy, dummy, static_cast<cplx*>(C), static_cast<const GemmTask*>(dtasks), ntasks, 0,
+      static_cast<const CUtensorMap*>(d_maps), a_stride, b_stride, static_cast<unsigned long long*>(tmax));
   return (int)cudaGetLastError();
 }
 

@@ -186,6 +186,40 @@ def test_large_subdomain_panel_bk_vs_oracle(cuda, oracle, monkeypatch, n, m, bat
         assert np.linalg.norm(X - Xo) <= 1e-10 * np.linalg.norm(Xo)
 
 
+@pytest.mark.parametrize("n,batch,cs,nb", [(600, 3, None, "64"), (1030, 2, "8", "64"), (777, 2, "4", "128"),
+                                           (1100, 2, None, "128")])
+def test_panel_bk_tma_updates_are_bitwise_the_grouped_kernel(cuda, monkeypatch, n, batch, cs, nb):
+    """The panel BK's trailing updates through the TMA-staged kernel
+    (D3M_PANEL_TMA=1: per-matrix tensor maps over W and the X workspace, zeroed
+    slice tail after an (NB-1)-column panel, running maximum) give the packed
+    factor, pivots and growth of the cp.async grouped kernel bit for bit."""
+    import paper_2002_05018_b200 as d
+    if cs is not None:
+        monkeypatch.setenv("D3M_PANEL_CS", cs)
+    monkeypatch.setenv("D3M_PANEL_NB", nb)
+    rng = np.random.default_rng(7 * n)
+    mats = []
+    for b in range(batch):
+        G = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2 * n)
+        A = (G + G.T) / 2
+        A[np.diag_indices(n)] += rng.uniform(-1, 1, n) + 1j * rng.uniform(-0.1, 0.1, n)
+        mats.append(A)
+    D = np.zeros((n, 2), dtype=complex)
+    D[[1, n - 2], [0, 1]] = 1.0
+    out = {}
+    for tma in ("0", "1"):
+        monkeypatch.setenv("D3M_PANEL_TMA", tma)
+        systems = [d.SubdomainSystem(b, A.copy(), np.ones(n, complex), np.arange(n), [d.Coupling(0, D, 1)])
+                   for b, A in enumerate(mats)]
+        d.reduce_domains(systems)
+        out[tma] = [(s.factor.packed.cpu().numpy(), np.asarray(s.factor.perm), np.asarray(s.factor.tags),
+                     s.factor.growth, s.factor.n_2x2) for s in systems]
+    for (W0, p0, t0, g0, c0), (W1, p1, t1, g1, c1) in zip(out["0"], out["1"]):
+        assert c0 == c1 and c0 > 0 and g0 == g1
+        assert np.array_equal(p0, p1) and np.array_equal(t0, t1)
+        assert np.array_equal(np.tril(W0), np.tril(W1))
+
+
 @pytest.mark.parametrize("cells,parts,radius", [(4, (2, 2, 2), 0.15), (8, (2, 1, 1), 0.0)])
 def test_fem3d_pipeline_vs_monolithic(cuda, cells, parts, radius):
     """Full GPU D3M pipeline on the 3-D Nedelec problems (config 1 is the
