@@ -321,10 +321,10 @@ def run_ours(args):
                      "peak_source": "live DMMA m8n8k4 probe (tools/fp64_peak.cu)" if peak_live else
                      "profiles/fp64_peak_r01.txt (measured DMMA burst)",
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if achieved else None,
-                     "traffic": 7.616e8,
+                     "traffic": 7.633e8,
                      "traffic_note": "DRAM bytes per launch of a representative 5,460-tile rest-update launch "
-                                     "(ncu --set full, profiles/ncu_gemm_tma_cfg4_r02_summary.txt); algorithmic C "
-                                     "traffic of that launch 7.157e8 B (1.06x)"},
+                                     "(ncu --set full, profiles/ncu_gemm_tma_cfg4_r02v_summary.txt); algorithmic C "
+                                     "traffic of that launch 7.157e8 B (1.07x)"},
         "instrumented_ms_per_step": round(ms_step_instr, 3),
         "stage_ms_per_step": {k: round(v / args.steps, 3) for k, v in cnt["union_ms"].items()},
         "stage_ms_summed_per_step": {k: round(v / args.steps, 3) for k, v in cnt["ms"].items()},

@@ -36,6 +36,10 @@ namespace d3m {
 
 constexpr int BM = 64, BN = 64, BKC = 8, STAGES = 4, PITCH = BKC + 4;
 constexpr int NTHREADS = 128;
+// k-major pitch of a transposed operand's stage slice: 66 = 2 mod 8, so a quarter warp's fragment
+// LDS.128 (4 k-rows x 2 consecutive elements) covers the eight 16-byte bank groups once
+constexpr int TPITCH = BM + 2;
+static_assert(BKC * TPITCH <= BM * PITCH, "a k-major slice fits the stage's operand slot");
 // One ring stage: the A and B k-slices side by side, so a freed stage is one
 // contiguous 24 KB block (the epilogue's C prefetch reuses freed stages).
 struct GemmStage {
@@ -103,13 +107,17 @@ __device__ __forceinline__ void load_tile(cplx (*S)[PITCH], const cplx* P, int l
       cp_async16(&S[r][k], g, ok);
     }
   } else {
-    // 64 threads cover one contiguous 1 KB row of the stored operand
+    // 64 threads cover one contiguous 1 KB row of the stored operand, and the stage keeps it k-major
+    // (St[k][r], pitch TPITCH): the 64 threads' 16-byte shared-memory writes are contiguous.  (Written
+    // as S[r][k] at the 192-byte row pitch they fell into two bank groups -- a 16-way conflict per
+    // warp, which bound the transposed launches of the subdomain solves.)
+    cplx* St = &S[0][0];
 #pragma unroll
     for (int p = 0; p < 512 / NT; ++p) {
       const int r = t & 63, k = p * (NT / 64) + (t >> 6);
       const bool ok = (r0 + r < rows) && (k0 + k < kdim);
       const cplx* g = ok ? P + (int64_t)(k0 + k) * ld + (r0 + r) : P;
-      cp_async16(&S[r][k], g, ok);
+      cp_async16(St + k * TPITCH + r, g, ok);
     }
   }
 }
@@ -257,13 +265,22 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
       cp_commit();
     }
     const int slot = kt % STAGES;
+    // fragment element (tile row r, k) of a staged operand: row-major slices, k-major when transposed
+    auto fa = [&](int r, int k) -> cplx {
+      if constexpr (TA) return (&st[slot].a[0][0])[k * TPITCH + r];
+      else return st[slot].a[r][k];
+    };
+    auto fb = [&](int r, int k) -> cplx {
+      if constexpr (TB) return (&st[slot].b[0][0])[k * TPITCH + r];
+      else return st[slot].b[r][k];
+    };
     if constexpr (G3) {
 #pragma unroll
       for (int kk = 0; kk < BKC / 4; ++kk) {
         double bre[WJ], bim[WJ], bsum[WJ];
 #pragma unroll
         for (int j = 0; j < WJ; ++j) {
-          const cplx b = st[slot].b[wn + j * 8 + fr][kk * 4 + fc];
+          const cplx b = fb(wn + j * 8 + fr, kk * 4 + fc);
           bre[j] = b.x;
           bim[j] = b.y;
           bsum[j] = b.x + b.y;
@@ -272,7 +289,7 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
         // accumulator is touched once per k-step (24 DMMAs apart)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const cplx a = st[slot].a[wm + i * 8 + fr][kk * 4 + fc];
+          const cplx a = fa(wm + i * 8 + fr, kk * 4 + fc);
           const double asum = a.x + a.y;
 #pragma unroll
           for (int j = 0; j < WJ; ++j) dmma(acc_re[i][j][0], acc_re[i][j][1], a.x, bre[j]);
@@ -312,14 +329,14 @@ zgemm_grouped_kernel(const cplx* __restrict__ Abase, const cplx* __restrict__ Bb
         double are[4], aim[4], anim[4], bre[4], bim[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const cplx a = st[slot].a[wm + i * 8 + fr][kk * 4 + fc];
+          const cplx a = fa(wm + i * 8 + fr, kk * 4 + fc);
           are[i] = a.x;
           aim[i] = a.y;
           anim[i] = -a.y;
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const cplx b = st[slot].b[wn + j * 8 + fr][kk * 4 + fc];
+          const cplx b = fb(wn + j * 8 + fr, kk * 4 + fc);
           bre[j] = b.x;
           bim[j] = b.y;
         }
