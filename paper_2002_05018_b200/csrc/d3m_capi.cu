@@ -252,6 +252,7 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
         f.m = n - R1; f.k = R1 - R0;
       }
       f.n = m; f.lda = n; f.ldb = m; f.ldc = m; f.flags = d3m::kGemmSub;
+      f.pad_ = b;             // matrix index (the TMA kernel's per-matrix tensor maps)
       d3m::GemmTask& g = t[(size_t)(nblk + ib) * batch + b];
       if (r0 > R0) {          // Z[R0:r0] -= L[r0:r1, R0:r0]^T Z[r0:r1]
         g.a_off = b * stride_f + (int64_t)r0 * n + R0;
@@ -265,6 +266,7 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
         g.m = R0; g.k = R1 - R0;
       }
       g.n = m; g.lda = n; g.ldb = m; g.ldc = m; g.flags = d3m::kGemmSub;
+      g.pad_ = b;
     }
     tiles[ib] = d3m_gemm_prepare_tasks(&t[(size_t)ib * batch], batch);
     tiles[nblk + ib] = d3m_gemm_prepare_tasks(&t[(size_t)(nblk + ib) * batch], batch);
@@ -272,6 +274,38 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
   cudaError_t e = cudaMemcpyAsync(d_tasks, t.data(), sizeof(d3m::GemmTask) * t.size(), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return fail((int)e, "d3m_ldlt_solve_blocked_batched: task upload");
   auto* dt = static_cast<const d3m::GemmTask*>(d_tasks);
+  // TMA-staged updates (3M form; D3M_SOLVE_TMA=0: the cp.async grouped kernel): per matrix tensor maps over
+  // the factor and the work array, kept in a per-device buffer.  A launch qualifies when its k range is a
+  // multiple of 16 (all but a ragged last block): rows past K inside the matrices are data, not zeros.
+  const char* tma_str = getenv("D3M_SOLVE_TMA");
+  const void* d_maps = nullptr;
+  if (!(tma_str && atoi(tma_str) == 0) && d3m_gemm_set_form(0) == 3 ) {
+    std::vector<unsigned char> hm((size_t)batch * 4 * 128);
+    const int rc = d3m_gemm_tma_prepare_solve(F, stride_f, n, work, sz, m, batch, hm.data());
+    if (rc == 0) {
+      static std::mutex mu;
+      static std::map<int, std::pair<void*, size_t>> bufs;     // per device, grow-only
+      int dev = 0;
+      cudaGetDevice(&dev);
+      std::lock_guard<std::mutex> g(mu);
+      auto& bf = bufs[dev];
+      if (bf.second < hm.size()) {
+        if (bf.first) { cudaStreamSynchronize(s); cudaFree(bf.first); }
+        bf = {nullptr, 0};
+        if (cudaMalloc(&bf.first, hm.size()) == cudaSuccess) bf.second = hm.size();
+        else cudaGetLastError();
+      }
+      // (pageable source: staged before the call returns; the buffer's previous reader is earlier on
+      // this stream or on a stream the caller has already ordered before it)
+      if (bf.first && cudaMemcpyAsync(bf.first, hm.data(), hm.size(), cudaMemcpyHostToDevice, s) == cudaSuccess)
+        d_maps = bf.first;
+    } else if (rc != -38) {
+      return fail(rc, "d3m_ldlt_solve_blocked_batched: tensor map");
+    }
+  }
+  const char* d_fwd_maps = static_cast<const char*>(d_maps);
+  const char* d_bwd_maps = d_fwd_maps ? d_fwd_maps + (size_t)batch * 2 * 128 : nullptr;
+  auto tma_ok = [&](int task_row) { return d_maps && (t[(size_t)task_row * batch].k % 16) == 0; };
   D3M_TRY(launch(kClsSolve, stream, [&] { return d3m_solve_phase_launch(0, &sb, batch, stream); }));   // Z = B[perm]
   for (int ib = 0; ib < nblk; ++ib) {
     const int r0 = ib * DBR;
@@ -280,6 +314,9 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
     }));
     if (tiles[ib] > 0)
       D3M_TRY(launch(kClsGemm, stream, [&] {
+        if (tma_ok(ib))
+          return d3m_gemm_tma_launch_batched_t(0, d_fwd_maps, work, dt + (size_t)ib * batch, batch, tiles[ib], stride_f,
+                                               sz, stream);
         return d3m_gemm_launch(0, 1, F, work, work, dt + (size_t)ib * batch, batch, tiles[ib], stream);
       }));
   }
@@ -292,6 +329,9 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
     }));
     if (tiles[nblk + ib] > 0)
       D3M_TRY(launch(kClsGemm, stream, [&] {
+        if (tma_ok(nblk + ib))
+          return d3m_gemm_tma_launch_batched_t(1, d_bwd_maps, work, dt + (size_t)(nblk + ib) * batch, batch,
+                                               tiles[nblk + ib], stride_f, sz, stream);
         return d3m_gemm_launch(1, 1, F, work, work, dt + (size_t)(nblk + ib) * batch, batch, tiles[nblk + ib], stream);
       }));
   }

@@ -116,6 +116,10 @@ int d3m_gemm_tma_prepare_batched(const void* A, int64_t a_stride, int64_t a_rows
                                  int64_t b_stride, int64_t b_rows, int b_cols, int ldb, int batch, void* h_maps);
 int d3m_gemm_tma_launch_batched(const void* d_maps, void* C, const void* dtasks, int ntasks, int ntiles,
                                 int64_t a_stride, int64_t b_stride, void* tmax, void* stream);
+int d3m_gemm_tma_prepare_solve(const void* F, int64_t stride_f, int n, const void* Z, int64_t stride_z, int m,
+                               int batch, void* h_maps);
+int d3m_gemm_tma_launch_batched_t(int ta, const void* d_maps, void* C, const void* dtasks, int ntasks, int ntiles,
+                                  int64_t a_stride, int64_t b_stride, void* stream);
 }
 
 #include "d3m_gemm.h"

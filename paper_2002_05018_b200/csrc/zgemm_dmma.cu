@@ -749,7 +749,14 @@ __device__ __forceinline__ void mb_expect_tx(uint64_t* b, unsigned bytes) {
 // task's pad_), operand offsets relative to the matrix (a_off - b * a_stride = row * lda + first column,
 // b_off - b * b_stride = row * ldb), and the running maximum of the written |C|^2 (kGemmTrackMax) -- the
 // batched trailing updates of the subdomain panel BK (bk_panel.cu).
-template <bool BATCH>
+// TA / TB (BATCH only): the operand is stored K x M (K x N), as the subdomain solves read the factor and
+// the right-hand sides.  Its slice is staged as 8-column boxes of the stored rows: box q of a slice holds
+// k = 0..7 as 128-byte rows of the eight tile rows 8q..8q+7 (SWIZZLE_128B: row element e of k at chunk
+// e ^ k), so the fragment of tile row 8q + pr at k reads chunk pr ^ k of row k of box q -- the chunk index
+// of the row-major form, and as conflict-free (a quarter warp's rows {q, q + 4} x four k cover the
+// eight chunks once).  The k range of such a task must end on a 16-k boundary or at the operand's last
+// stored row (rows past the task's K inside the matrix are data, not zeros): the callers check.
+template <bool BATCH, bool TA = false, bool TB = false>
 __global__ void __launch_bounds__(HNT, 3)
 zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, cplx* Cbase,
                    const GemmTask* __restrict__ tasks, int ntasks, int64_t b_base, const CUtensorMap* gmaps,
@@ -782,11 +789,24 @@ zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
   cplx* C = Cbase + tk.c_off;
   int arow, brow, acol = 0;                                     // panel rows of the tile's first A / B row
   const CUtensorMap *pmA = &mapA, *pmB = &mapB;
+  int bcol = 0;
   if constexpr (BATCH) {
     const int arel = (int)(tk.a_off - tk.pad_ * a_stride);
-    arow = arel / tk.lda + m0;
-    acol = arel % tk.lda;
-    brow = (int)((tk.b_off - tk.pad_ * b_stride) / tk.ldb) + n0;
+    const int brel = (int)(tk.b_off - tk.pad_ * b_stride);
+    if constexpr (TA) {            // stored K x M: arow = first stored (k) row, acol = the tile's first column
+      arow = arel / tk.lda;
+      acol = arel % tk.lda + m0;
+    } else {
+      arow = arel / tk.lda + m0;
+      acol = arel % tk.lda;
+    }
+    if constexpr (TB) {
+      brow = brel / tk.ldb;
+      bcol = brel % tk.ldb + n0;
+    } else {
+      brow = brel / tk.ldb + n0;
+      bcol = brel % tk.ldb;
+    }
     pmA = gmaps + 2 * tk.pad_;
     pmB = pmA + 1;
   } else {
@@ -802,8 +822,21 @@ zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     mb_expect_tx(&full[slot], kStageBytes);
 #pragma unroll
     for (int h = 0; h < TKS; ++h) {
-      tma_load_2d(&st[slot].a[h][0][0], pmA, 2 * (acol + (kt * TKS + h) * BKC), arow, &full[slot]);
-      tma_load_2d(&st[slot].b[h][0][0], pmB, 2 * (kt * TKS + h) * BKC, brow, &full[slot]);
+      const int k0 = (kt * TKS + h) * BKC;
+      if constexpr (TA) {
+#pragma unroll
+        for (int q = 0; q < BM / 8; ++q)
+          tma_load_2d(&st[slot].a[h][q * 8][0], pmA, 2 * (acol + q * 8), arow + k0, &full[slot]);
+      } else {
+        tma_load_2d(&st[slot].a[h][0][0], pmA, 2 * (acol + k0), arow, &full[slot]);
+      }
+      if constexpr (TB) {
+#pragma unroll
+        for (int q = 0; q < HN / 8; ++q)
+          tma_load_2d(&st[slot].b[h][q * 8][0], pmB, 2 * (bcol + q * 8), brow + k0, &full[slot]);
+      } else {
+        tma_load_2d(&st[slot].b[h][0][0], pmB, 2 * (bcol + k0), brow, &full[slot]);
+      }
     }
   };
   double P3[4][2][2], Q3[4][2][2], R3[4][2][2];
@@ -841,17 +874,18 @@ zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
 #pragma unroll
     for (int kq = 0; kq < TKS * BKC / 4; ++kq) {
       const int ca = (kq & 1) ? ca1 : ca0, ks = kq >> 1;
+      const int k8 = (kq & 1) * 4 + fc;               // k within the slice (row of a k-major box)
       double bre[2], bim[2], bsum[2];
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const cplx b = S.b[ks][wn + j * 8 + pr][ca];
+        const cplx b = S.b[ks][TB ? wn + j * 8 + k8 : wn + j * 8 + pr][ca];
         bre[j] = b.x;
         bim[j] = b.y;
         bsum[j] = b.x + b.y;
       }
       cplx a[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = S.a[ks][wm + i * 8 + pr][ca];
+      for (int i = 0; i < 4; ++i) a[i] = S.a[ks][TA ? wm + i * 8 + k8 : wm + i * 8 + pr][ca];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const double asum = a[i].x + a[i].y;
@@ -1075,6 +1109,53 @@ extern "C" int d3m_gemm_tma_prepare_batched(const void* A, int64_t a_stride, int
     if (rc) return rc;
   }
   return 0;
+}
+
+// Map pairs of the blocked subdomain solves (ldlt_solve_blocked_impl): per matrix b
+//   forward  h_maps[2 b]                = F_b (n x n) row boxes (A = L[rows, block], not transposed),
+//            h_maps[2 b + 1]            = Z_b (n x m) k-major boxes (B = Z[block, :], stored K x N);
+//   backward h_maps[2 batch + 2 b]      = F_b k-major boxes (A = L[block, cols]^T, stored K x M),
+//            h_maps[2 batch + 2 b + 1]  = Z_b k-major boxes.
+extern "C" int d3m_gemm_tma_prepare_solve(const void* F, int64_t stride_f, int n, const void* Z, int64_t stride_z,
+                                          int m, int batch, void* h_maps) {
+  using namespace d3m;
+  auto* mp = static_cast<CUtensorMap*>(h_maps);
+  for (int b = 0; b < batch; ++b) {
+    const cplx* f = static_cast<const cplx*>(F) + b * stride_f;
+    const cplx* z = static_cast<const cplx*>(Z) + b * stride_z;
+    int rc = tmap_2d(&mp[2 * b], f, n, 2 * (int64_t)n, (int64_t)n * 16, 2 * BKC, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (!rc) rc = tmap_2d(&mp[2 * b + 1], z, n, 2 * (int64_t)m, (int64_t)m * 16, 16, 8, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (!rc)
+      rc = tmap_2d(&mp[2 * batch + 2 * b], f, n, 2 * (int64_t)n, (int64_t)n * 16, 16, 8, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    mp[2 * batch + 2 * b + 1] = mp[2 * b + 1];
+  }
+  return 0;
+}
+
+// ta = 0: A not transposed, B stored K x N (forward updates); ta = 1: both stored k-major (backward)
+extern "C" int d3m_gemm_tma_launch_batched_t(int ta, const void* d_maps, void* C, const void* dtasks, int ntasks,
+                                             int ntiles, int64_t a_stride, int64_t b_stride, void* stream) {
+  using namespace d3m;
+  if (ntiles <= 0 || ntasks <= 0) return 0;
+  static PerDeviceOnce configured;
+  if (configured.first()) {
+    cudaFuncSetAttribute(zgemm3m_tma_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kTSmem);
+    cudaFuncSetAttribute(zgemm3m_tma_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kTSmem);
+  }
+  CUtensorMap dummy{};
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  if (ta)
+    zgemm3m_tma_kernel<true, true, true><<<2 * ntiles, HNT, kTSmem, s>>>(
+        dummy, dummy, static_cast<cplx*>(C), static_cast<const GemmTask*>(dtasks), ntasks, 0,
+        static_cast<const CUtensorMap*>(d_maps), a_stride, b_stride, nullptr);
+  else
+    zgemm3m_tma_kernel<true, false, true><<<2 * ntiles, HNT, kTSmem, s>>>(
+        dummy, dummy, static_cast<cplx*>(C), static_cast<const GemmTask*>(dtasks), ntasks, 0,
+        static_cast<const CUtensorMap*>(d_maps), a_stride, b_stride, nullptr);
+  return (int)cudaGetLastError();
 }
 
 extern "C" int d3m_gemm_tma_launch_batched(const void* d_maps, void* C, const void* dtasks, int ntasks, int ntiles,

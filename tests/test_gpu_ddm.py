@@ -220,6 +220,41 @@ def test_panel_bk_tma_updates_are_bitwise_the_grouped_kernel(cuda, monkeypatch, 
         assert np.array_equal(np.tril(W0), np.tril(W1))
 
 
+@pytest.mark.parametrize("n,m,batch", [(600, 40, 3), (1030, 17, 2), (1296, 130, 2)])
+def test_blocked_solve_tma_updates_are_bitwise_the_grouped_kernel(cuda, monkeypatch, n, m, batch):
+    """The blocked subdomain solves' GEMM updates through the TMA-staged kernel
+    (factor rows as row boxes, the right-hand sides and the transposed factor
+    as k-major boxes; ragged last blocks stay on the cp.async kernel) give the
+    Schur blocks and the kept solution of D3M_SOLVE_TMA=0 bit for bit."""
+    import paper_2002_05018_b200 as d
+    rng = np.random.default_rng(11 * n + m)
+    mats = []
+    for b in range(batch):
+        G = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2 * n)
+        A = (G + G.T) / 2
+        A[np.diag_indices(n)] += rng.uniform(-1, 1, n) + 1j * rng.uniform(-0.1, 0.1, n)
+        D = np.zeros((n, m), dtype=complex)
+        D[rng.choice(n, m, replace=False), np.arange(m)] = rng.choice([-1.0, 1.0], m)
+        D[:, :2] += rng.standard_normal((n, 2)) * 0.1
+        mats.append((A, D, rng.standard_normal(n) + 1j * rng.standard_normal(n)))
+    out = {}
+    for tma in ("0", "1"):
+        monkeypatch.setenv("D3M_SOLVE_TMA", tma)
+        for keep in ("factor", "schur"):
+            systems = [d.SubdomainSystem(b, A.copy(), f.copy(), np.arange(n), [d.Coupling(0, D.copy(), 1)])
+                       for b, (A, D, f) in enumerate(mats)]
+            red = d.reduce_domains(systems, keep=keep)
+            out[tma, keep] = [(np.asarray(KD), np.asarray(gd)) for KD, gd in red]
+            if keep == "factor":
+                B = np.arange(n * 3, dtype=float).reshape(n, 3) / n + 0.5j
+                out[tma, "solve"] = [np.asarray(s.factor.solve(B)) for s in systems]
+    for keep in ("factor", "schur"):
+        for (K0, g0), (K1, g1) in zip(out["0", keep], out["1", keep]):
+            assert np.array_equal(K0, K1) and np.array_equal(g0, g1)
+    for X0, X1 in zip(out["0", "solve"], out["1", "solve"]):
+        assert np.array_equal(X0, X1)
+
+
 @pytest.mark.parametrize("cells,parts,radius", [(4, (2, 2, 2), 0.15), (8, (2, 1, 1), 0.0)])
 def test_fem3d_pipeline_vs_monolithic(cuda, cells, parts, radius):
     """Full GPU D3M pipeline on the 3-D Nedelec problems (config 1 is the
