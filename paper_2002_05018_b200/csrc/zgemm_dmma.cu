@@ -818,27 +818,30 @@ zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
   const int fr = lane >> 2, fc = lane & 3;
   const int pr = (fr >> 1) | ((fr & 1) << 2);
   constexpr unsigned kStageBytes = (unsigned)sizeof(TStage);
-  auto issue = [&](int slot, int kt) {                          // thread 0 only
-    mb_expect_tx(&full[slot], kStageBytes);
+  auto issue = [&](int slot, int kt) {
+    // lane 0 of every warp (with k-major operands the stage is up to 24 copies: each warp issues a
+    // quarter of the boxes); warp 0 arms the barrier and issues the row-major operands
+    if (warp == 0) mb_expect_tx(&full[slot], kStageBytes);
 #pragma unroll
     for (int h = 0; h < TKS; ++h) {
       const int k0 = (kt * TKS + h) * BKC;
       if constexpr (TA) {
 #pragma unroll
-        for (int q = 0; q < BM / 8; ++q)
-          tma_load_2d(&st[slot].a[h][q * 8][0], pmA, 2 * (acol + q * 8), arow + k0, &full[slot]);
+        for (int q = 0; q < BM / 8 / 4; ++q)
+          tma_load_2d(&st[slot].a[h][(4 * q + warp) * 8][0], pmA, 2 * (acol + (4 * q + warp) * 8), arow + k0,
+                      &full[slot]);
       } else {
-        tma_load_2d(&st[slot].a[h][0][0], pmA, 2 * (acol + k0), arow, &full[slot]);
+        if (warp == 0) tma_load_2d(&st[slot].a[h][0][0], pmA, 2 * (acol + k0), arow, &full[slot]);
       }
       if constexpr (TB) {
-#pragma unroll
-        for (int q = 0; q < HN / 8; ++q)
-          tma_load_2d(&st[slot].b[h][q * 8][0], pmB, 2 * (bcol + q * 8), brow + k0, &full[slot]);
+        tma_load_2d(&st[slot].b[h][warp * 8][0], pmB, 2 * (bcol + warp * 8), brow + k0, &full[slot]);
       } else {
-        tma_load_2d(&st[slot].b[h][0][0], pmB, 2 * (bcol + k0), brow, &full[slot]);
+        if (warp == 0) tma_load_2d(&st[slot].b[h][0][0], pmB, 2 * (bcol + k0), brow, &full[slot]);
       }
     }
   };
+  static_assert(HN / 8 == HNT / 32 && (BM / 8) % (HNT / 32) == 0, "k-major boxes split evenly over the warps");
+  const bool issuer = (TA || TB) ? lane == 0 : t == 0;
   double P3[4][2][2], Q3[4][2][2], R3[4][2][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -846,7 +849,7 @@ zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     for (int j = 0; j < 2; ++j) P3[i][j][0] = P3[i][j][1] = Q3[i][j][0] = Q3[i][j][1] = R3[i][j][0] = R3[i][j][1] = 0.0;
   const int mode = tk.flags & kGemmModeMask;
   const bool cpre = (!sym || (tk.flags & kGemmLowerOnly)) && mode != kGemmStore && ktiles >= TSTAGES;
-  if (t == 0) {
+  if (issuer) {
 #pragma unroll
     for (int s = 0; s < TSTAGES - 1; ++s)
       if (s < ktiles) issue(s, s);
@@ -856,7 +859,7 @@ zgemm3m_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     __syncthreads();                       // every warp is done with slot (kt - 1) % TSTAGES
     const int nk = kt + TSTAGES - 1;
     if (nk < ktiles) {
-      if (t == 0) issue(nk % TSTAGES, nk);
+      if (issuer) issue(nk % TSTAGES, nk);
     } else if (cpre && nk - ktiles < 2) {  // C rows [32c, 32c+32) into the freed stage
       const int ch = nk - ktiles;
       cplx* dst = reinterpret_cast<cplx*>(&st[nk % TSTAGES]);
