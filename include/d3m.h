@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define D3M_ABI_VERSION 12
+#define D3M_ABI_VERSION 13
 
 int d3m_abi_version(void);
 const char* d3m_last_error(void);
@@ -152,13 +152,17 @@ int d3m_gemm_set_form(int form);
  * filled (the caller ran d3m_bk_panel_batched itself); the BK is skipped.
  * n <= 512: exact BK + chain solves (bk_scratch: batch*4n complex if n>3200);
  * n > 512: panel BK + blocked solves (bk_scratch: d3m_bk_panel_workspace
- * bytes, d_tasks: max(batch, 2 ceil(n/64) batch) records). */
+ * bytes, d_tasks: max(batch, 4 ceil(n/64) batch) records).
+ * h_mcols (ABI v13, HOST int32[batch] or NULL): the coupling columns each
+ * domain really has when its D_d is zero-padded to m; the blocked solves'
+ * GEMM updates then skip the padded columns [h_mcols[b], m) (their solution
+ * is exactly zero, so every result is unchanged bit for bit). */
 int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const void* D, const void* f,
                              double pivot_tol,
                              void* perm, void* tags, void* n2x2, void* growth, void* info, void* scale, void* asym,
                              void* K_out, void* g_out, void* work_z, void* work_x, void* work_c, void* bk_scratch,
                              void* d_tasks, const void* rows, int nrows, void* work_d, int flags, void* margin,
-                             void* stream);
+                             const int32_t* h_mcols, void* stream);
 
 /* Grouped block copy / ordered accumulate (40-byte CopyTask records, see
  * d3m_misc.h).  Used for factor._permute_blocks (factor.py:139-151) and the

@@ -34,7 +34,7 @@ _SIGNATURES = {
     "d3m_block_residual": [I32, P, P, P, P, P, P, P, P, P],
     "d3m_nonzero_rows": [I32, I32, I32, P, P, P, P, P],
     "d3m_block_solve_dataflow": [I32, P, P, I32, I32, P, P, P, I32, P, P, P, P, P, P, P, P, I32, P],
-    "d3m_schur_reduce_batched": [I32, I32, I32, I32, P, P, P, F64] + [P] * 14 + [P, I32, P, I32, P, P],
+    "d3m_schur_reduce_batched": [I32, I32, I32, I32, P, P, P, F64] + [P] * 14 + [P, I32, P, I32, P, P, P],
     "d3m_block_copy": [P, P, P, I32, I64, P],
     "d3m_gather_rows": [P, P, P, I64, I32, P],
     "d3m_ordered_average": [P, P, P, P, I64, P],
@@ -88,7 +88,7 @@ _lib = None
 
 
 FLOW_EXTRA_COUNTERS = 2052  # include/d3m.h D3M_FLOW_EXTRA_COUNTERS
-ABI_VERSION = 12         # include/d3m.h D3M_ABI_VERSION this binding is written for
+ABI_VERSION = 13         # include/d3m.h D3M_ABI_VERSION this binding is written for
 
 
 def load():

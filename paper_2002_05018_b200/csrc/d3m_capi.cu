@@ -208,7 +208,8 @@ int d3m_ldlt_solve_batched(int batch, int n, const void* F, int64_t stride_f, co
 // batch GEMM records.
 static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stride_f, const void* perm,
                                    int64_t stride_p, const void* tags, int64_t stride_t, void* B, int64_t stride_b,
-                                   int ldb, int m, void* work, void* d_tasks, void* stream, bool fwd_only);
+                                   int ldb, int m, void* work, void* d_tasks, void* stream, bool fwd_only,
+                                   const int32_t* h_mcols = nullptr, int tail = 0);
 
 int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stride_f, const void* perm,
                                    int64_t stride_p, const void* tags, int64_t stride_t, void* B, int64_t stride_b,
@@ -219,9 +220,13 @@ int d3m_ldlt_solve_blocked_batched(int batch, int n, const void* F, int64_t stri
 
 // fwd_only: stop after Z = L^-1 P B (left in `work`, pivot order): the Schur
 // reduction K = Z^T D^-1 Z needs no backward sweep.
+// h_mcols / tail: matrix b's columns [h_mcols[b], m - tail) are zero right-hand sides (padding of the
+// coupling block): the GEMM updates run on [0, h_mcols[b]) and [m - tail, m) only -- up to two tasks per
+// matrix and block step (d_tasks: 4 * ceil(n/64) * batch records then).
 static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stride_f, const void* perm,
                                    int64_t stride_p, const void* tags, int64_t stride_t, void* B, int64_t stride_b,
-                                   int ldb, int m, void* work, void* d_tasks, void* stream, bool fwd_only) {
+                                   int ldb, int m, void* work, void* d_tasks, void* stream, bool fwd_only,
+                                   const int32_t* h_mcols, int tail) {
   if (batch < 0 || n < 0 || m < 0 || ldb < m) return fail(-22, "d3m_ldlt_solve_blocked_batched: bad shape");
   if (batch == 0 || n == 0 || m == 0) return 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -231,45 +236,59 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
   const int64_t sz = (int64_t)n * m;
   d3m::SolveBatch sb{CC(F), stride_f, static_cast<const int8_t*>(tags), stride_t, static_cast<const int64_t*>(perm),
                      stride_p, C(work), sz, nullptr, 0, CC(B), stride_b, n, m, m, ldb};
-  // GEMM task table: [fwd ib][b] then [bwd ib][b]
-  std::vector<d3m::GemmTask> t((size_t)2 * nblk * batch);
+  // column ranges with nonzero right-hand sides: (matrix, first column, count)
+  struct Range { int b, c0, nc; };
+  std::vector<Range> rg;
+  for (int b = 0; b < batch; ++b) {
+    const int mc = h_mcols ? std::max(0, std::min((int)h_mcols[b], m - tail)) : m - tail;
+    if (h_mcols && mc < m - tail) {
+      if (mc > 0) rg.push_back({b, 0, mc});
+      if (tail > 0) rg.push_back({b, m - tail, tail});
+    } else {
+      rg.push_back({b, 0, m});
+    }
+  }
+  const int T = (int)rg.size();          // tasks per block step and sweep
+  // GEMM task table: [fwd ib][q] then [bwd ib][q]
+  std::vector<d3m::GemmTask> t((size_t)2 * nblk * T);
   std::memset(t.data(), 0, sizeof(d3m::GemmTask) * t.size());
   std::vector<int> tiles(2 * nblk, 0);
   for (int ib = 0; ib < nblk; ++ib) {
     const int r0 = ib * DBR, r1 = std::min(n, r0 + DBR);
     const int R0 = (r0 / OBR) * OBR, R1 = std::min(n, R0 + OBR);
-    for (int b = 0; b < batch; ++b) {
-      d3m::GemmTask& f = t[(size_t)ib * batch + b];
+    for (int q = 0; q < T; ++q) {
+      const int b = rg[q].b, c0 = rg[q].c0, nc = rg[q].nc;
+      d3m::GemmTask& f = t[(size_t)ib * T + q];
       if (r1 < R1) {          // Z[r1:R1] -= L[r1:R1, r0:r1] Z[r0:r1]
         f.a_off = b * stride_f + (int64_t)r1 * n + r0;
-        f.b_off = b * sz + (int64_t)r0 * m;
-        f.c_off = b * sz + (int64_t)r1 * m;
+        f.b_off = b * sz + (int64_t)r0 * m + c0;
+        f.c_off = b * sz + (int64_t)r1 * m + c0;
         f.m = R1 - r1; f.k = r1 - r0;
       } else {                // Z[R1:] -= L[R1:, R0:R1] Z[R0:R1]
         f.a_off = b * stride_f + (int64_t)R1 * n + R0;
-        f.b_off = b * sz + (int64_t)R0 * m;
-        f.c_off = b * sz + (int64_t)R1 * m;
+        f.b_off = b * sz + (int64_t)R0 * m + c0;
+        f.c_off = b * sz + (int64_t)R1 * m + c0;
         f.m = n - R1; f.k = R1 - R0;
       }
-      f.n = m; f.lda = n; f.ldb = m; f.ldc = m; f.flags = d3m::kGemmSub;
+      f.n = nc; f.lda = n; f.ldb = m; f.ldc = m; f.flags = d3m::kGemmSub;
       f.pad_ = b;             // matrix index (the TMA kernel's per-matrix tensor maps)
-      d3m::GemmTask& g = t[(size_t)(nblk + ib) * batch + b];
+      d3m::GemmTask& g = t[(size_t)(nblk + ib) * T + q];
       if (r0 > R0) {          // Z[R0:r0] -= L[r0:r1, R0:r0]^T Z[r0:r1]
         g.a_off = b * stride_f + (int64_t)r0 * n + R0;
-        g.b_off = b * sz + (int64_t)r0 * m;
-        g.c_off = b * sz + (int64_t)R0 * m;
+        g.b_off = b * sz + (int64_t)r0 * m + c0;
+        g.c_off = b * sz + (int64_t)R0 * m + c0;
         g.m = r0 - R0; g.k = r1 - r0;
       } else {                // Z[:R0] -= L[R0:R1, :R0]^T Z[R0:R1]
         g.a_off = b * stride_f + (int64_t)R0 * n;
-        g.b_off = b * sz + (int64_t)R0 * m;
-        g.c_off = b * sz;
+        g.b_off = b * sz + (int64_t)R0 * m + c0;
+        g.c_off = b * sz + c0;
         g.m = R0; g.k = R1 - R0;
       }
-      g.n = m; g.lda = n; g.ldb = m; g.ldc = m; g.flags = d3m::kGemmSub;
+      g.n = nc; g.lda = n; g.ldb = m; g.ldc = m; g.flags = d3m::kGemmSub;
       g.pad_ = b;
     }
-    tiles[ib] = d3m_gemm_prepare_tasks(&t[(size_t)ib * batch], batch);
-    tiles[nblk + ib] = d3m_gemm_prepare_tasks(&t[(size_t)(nblk + ib) * batch], batch);
+    tiles[ib] = d3m_gemm_prepare_tasks(&t[(size_t)ib * T], T);
+    tiles[nblk + ib] = d3m_gemm_prepare_tasks(&t[(size_t)(nblk + ib) * T], T);
   }
   cudaError_t e = cudaMemcpyAsync(d_tasks, t.data(), sizeof(d3m::GemmTask) * t.size(), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return fail((int)e, "d3m_ldlt_solve_blocked_batched: task upload");
@@ -305,7 +324,7 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
   }
   const char* d_fwd_maps = static_cast<const char*>(d_maps);
   const char* d_bwd_maps = d_fwd_maps ? d_fwd_maps + (size_t)batch * 2 * 128 : nullptr;
-  auto tma_ok = [&](int task_row) { return d_maps && (t[(size_t)task_row * batch].k % 16) == 0; };
+  auto tma_ok = [&](int task_row) { return d_maps && (t[(size_t)task_row * T].k % 16) == 0; };
   D3M_TRY(launch(kClsSolve, stream, [&] { return d3m_solve_phase_launch(0, &sb, batch, stream); }));   // Z = B[perm]
   for (int ib = 0; ib < nblk; ++ib) {
     const int r0 = ib * DBR;
@@ -315,9 +334,9 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
     if (tiles[ib] > 0)
       D3M_TRY(launch(kClsGemm, stream, [&] {
         if (tma_ok(ib))
-          return d3m_gemm_tma_launch_batched_t(0, d_fwd_maps, work, dt + (size_t)ib * batch, batch, tiles[ib], stride_f,
-                                               sz, stream);
-        return d3m_gemm_launch(0, 1, F, work, work, dt + (size_t)ib * batch, batch, tiles[ib], stream);
+          return d3m_gemm_tma_launch_batched_t(0, d_fwd_maps, work, dt + (size_t)ib * T, T, tiles[ib], stride_f, sz,
+                                               stream);
+        return d3m_gemm_launch(0, 1, F, work, work, dt + (size_t)ib * T, T, tiles[ib], stream);
       }));
   }
   if (fwd_only) return 0;
@@ -330,9 +349,9 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
     if (tiles[nblk + ib] > 0)
       D3M_TRY(launch(kClsGemm, stream, [&] {
         if (tma_ok(nblk + ib))
-          return d3m_gemm_tma_launch_batched_t(1, d_bwd_maps, work, dt + (size_t)(nblk + ib) * batch, batch,
-                                               tiles[nblk + ib], stride_f, sz, stream);
-        return d3m_gemm_launch(1, 1, F, work, work, dt + (size_t)(nblk + ib) * batch, batch, tiles[nblk + ib], stream);
+          return d3m_gemm_tma_launch_batched_t(1, d_bwd_maps, work, dt + (size_t)(nblk + ib) * T, T, tiles[nblk + ib],
+                                               stride_f, sz, stream);
+        return d3m_gemm_launch(1, 1, F, work, work, dt + (size_t)(nblk + ib) * T, T, tiles[nblk + ib], stream);
       }));
   }
   D3M_TRY(launch(kClsSolve, stream, [&] { return d3m_solve_phase_launch(4, &sb, batch, stream); }));   // B[perm] = Z
@@ -429,7 +448,7 @@ int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const v
                              double pivot_tol, void* perm, void* tags, void* n2x2, void* growth, void* info,
                              void* scale, void* asym, void* K_out, void* g_out, void* work_z, void* work_x,
                              void* work_c, void* bk_scratch, void* d_tasks, const void* rows, int nrows,
-                             void* work_d, int flags, void* margin, void* stream) {
+                             void* work_d, int flags, void* margin, const int32_t* h_mcols, void* stream) {
   // A: batch x n x n (factored in place -> packed factor); D: batch x n x m;
   // F: batch x n x nrhs; work_z, work_x: batch x n x (m+nrhs); work_c: batch x m x (m+nrhs)
   if (batch < 0 || n < 0 || m < 0 || nrhs < 0) return fail(-22, "d3m_schur_reduce_batched: bad shape");
@@ -458,7 +477,7 @@ int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const v
     // (forward sweep only) C = Z_D^T D^-1 Z = D^T A^-1 [D | F]
     if (big)
       D3M_TRY(ldlt_solve_blocked_impl(batch, n, A, nn, perm, n, tags, n, work_x, nw, w, w, work_z, d_tasks, stream,
-                                      true));
+                                      true, h_mcols, nrhs));
     else {
       d3m::SolveBatch sf{CC(A), nn, static_cast<const int8_t*>(tags), n, static_cast<const int64_t*>(perm), n,
                          C(work_z), nw, nullptr, 0, CC(work_x), nw, n, w, w, w};
@@ -496,8 +515,8 @@ int d3m_schur_reduce_batched(int batch, int n, int m, int nrhs, void* A, const v
   }
   // X = A^-1 RHS (factor.py:52-66)
   if (big)
-    D3M_TRY(d3m_ldlt_solve_blocked_batched(batch, n, A, nn, perm, n, tags, n, work_x, nw, w, w, work_z, d_tasks,
-                                           stream));
+    D3M_TRY(ldlt_solve_blocked_impl(batch, n, A, nn, perm, n, tags, n, work_x, nw, w, w, work_z, d_tasks, stream,
+                                    false, h_mcols, nrhs));
   else
     D3M_TRY(d3m_ldlt_solve_batched(batch, n, A, nn, perm, n, tags, n, work_x, nw, w, w, work_z, stream));
   if (m == 0) return 0;

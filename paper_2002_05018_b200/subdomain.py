@@ -352,7 +352,7 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, marg
     if n > _lib.PANEL_BK_MIN:
         nbytes = int(_lib.load().d3m_bk_panel_workspace(n, B))
         scratch = t.empty((nbytes + 15) // 16, dtype=t.complex128, device="cuda")
-        d_tasks = t.empty(64 * max(B, 2 * ((n + 63) // 64) * B), dtype=t.uint8, device="cuda")
+        d_tasks = t.empty(64 * max(B, 4 * ((n + 63) // 64) * B), dtype=t.uint8, device="cuda")
     else:
         scratch = empty((B, 4 * n)) if 64 * n > 200 * 1024 else None
         d_tasks = t.empty(64 * B, dtype=t.uint8, device="cuda")
@@ -382,9 +382,13 @@ def _reduce_chunk(systems, members, n, m, r, ms, pivot_tol, keep, vec, out, marg
         _fill_inputs(systems, members, n, ms, A if A_dev is None else None, D, f)
     rows, nrows = _nonzero_rows(D, n) if keep != "schur" else (None, 0)
     wd = empty((B, nrows, m)) if rows is not None else None
+    # the coupling columns each domain really has (its D is zero-padded to the batch's m): the blocked
+    # solves skip the padded ones
+    mcols = np.array([ms[i] for i in members], dtype=np.int32)
     _lib.call("d3m_schur_reduce_batched", B, n, m, r, _P(A), _P(D), _P(f), float(pivot_tol), _P(perm),
               _P(tags), _P(n2), _P(gr), _P(info), _P(sc), _P(asy), _P(K), _P(g), _P(wz), _P(wx), _P(wc),
-              _P(scratch), _P(d_tasks), _P(rows), int(nrows), _P(wd), flags, _P(mg), stream_ptr())
+              _P(scratch), _P(d_tasks), _P(rows), int(nrows), _P(wd), flags, _P(mg),
+              _lib.hptr(mcols) if bool(np.any(mcols < m)) else None, stream_ptr())
     if split:
         S.wait_event(ev_scan)
         sc_h, full_h, asy_h = sc.cpu().numpy(), sc_full.cpu().numpy(), asy_full.cpu().numpy()

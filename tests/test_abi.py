@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     from paper_2002_05018_b200 import _lib
     assert set(_declared()) <= set(_lib.exported_symbols())
-    assert lib.d3m_abi_version() == _lib.ABI_VERSION == 12
+    assert lib.d3m_abi_version() == _lib.ABI_VERSION == 13
 
 
 def test_gpu_path_fails_loudly_without_device():

@@ -220,6 +220,35 @@ def test_panel_bk_tma_updates_are_bitwise_the_grouped_kernel(cuda, monkeypatch, 
         assert np.array_equal(np.tril(W0), np.tril(W1))
 
 
+def test_padded_coupling_columns_are_skipped_exactly(cuda, oracle):
+    """Domains of one batch with different coupling widths: the narrower D is
+    zero-padded to the batch's m and the blocked solves skip its padded
+    columns (d3m_schur_reduce_batched h_mcols, ABI v13) -- K_D, g_d and the
+    recovered field match the oracle as for an unpadded domain."""
+    import paper_2002_05018_b200 as d
+    n = 700
+    rng = np.random.default_rng(77)
+    systems, ref = [], []
+    for b, m in enumerate((70, 9, 33)):
+        G = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2 * n)
+        A = (G + G.T) / 2
+        A[np.diag_indices(n)] += rng.uniform(-1, 1, n) + 1j * rng.uniform(-0.1, 0.1, n)
+        D = np.zeros((n, m), dtype=complex)
+        D[rng.choice(n, m, replace=False), np.arange(m)] = rng.choice([-1.0, 1.0], m)
+        f = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        systems.append(d.SubdomainSystem(b, A, f, np.arange(n), [d.Coupling(b, D, 1)]))
+        ref.append(oracle.reduce_domain(A, D, f))
+    red = d.reduce_domains(systems)
+    for s, (KD, gd), (Ko, go, fo) in zip(systems, red, ref):
+        assert np.asarray(KD).shape == Ko.shape
+        assert np.array_equal(s.factor.perm, fo.perm) and np.array_equal(s.factor.tags, fo.tags)
+        assert np.linalg.norm(np.asarray(KD) - Ko) <= 1e-10 * np.linalg.norm(Ko)
+        assert np.linalg.norm(np.asarray(gd) - go) <= 1e-10 * np.linalg.norm(go)
+        X = np.asarray(s._d3m_X.cpu().numpy() if hasattr(s._d3m_X, "cpu") else s._d3m_X)
+        m = Ko.shape[0]
+        assert not np.any(X[:, m:-1])                       # padded columns: exactly zero
+
+
 @pytest.mark.parametrize("n,m,batch", [(600, 40, 3), (1030, 17, 2), (1296, 130, 2)])
 def test_blocked_solve_tma_updates_are_bitwise_the_grouped_kernel(cuda, monkeypatch, n, m, batch):
     """The blocked subdomain solves' GEMM updates through the TMA-staged kernel
