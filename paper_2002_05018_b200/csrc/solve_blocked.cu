@@ -17,6 +17,8 @@ namespace d3m {
 constexpr int DB = 64;           // diagonal block
 constexpr int DB_NC = 32;        // RHS columns per CTA
 constexpr int DB_THREADS = 256;
+constexpr int DB_CW = DB_NC / (DB_THREADS / 32);     // RHS columns per warp
+static_assert(DB == 64 && DB_CW * (DB_THREADS / 32) == DB_NC, "two rows per lane, whole columns per warp");
 
 // forward: Z[r0:r0+64] = L_bb^-1 Z[r0:r0+64]   (after the straddle fix)
 __global__ void __launch_bounds__(DB_THREADS)
@@ -47,13 +49,37 @@ diag_fwd_kernel(const cplx* Fbase, int64_t stride_f, const int8_t* tagsbase, int
     c_fma(Zs[0][threadIdx.x], e, Z[(int64_t)(r0 - 1) * m + c0 + threadIdx.x]);
   }
   __syncthreads();
-  for (int c = 0; c < nb - 1; ++c) {
-    for (int e = threadIdx.x; e < (nb - 1 - c) * DB_NC; e += DB_THREADS) {
-      const int r = c + 1 + e / DB_NC, cc = e % DB_NC;
-      c_fms(Zs[r][cc], Ls[r][c], Zs[c][cc]);
+  // substitution in registers: warp w owns the RHS columns 4w..4w+3, lane l their rows l and l + 32;
+  // the pivot row's values travel by shuffle (no CTA barrier per step).  Every element takes the updates
+  // z_r -= L_rc z_c in ascending c with the fused form of c_fms, as the barrier version did.
+  {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    cplx z0[DB_CW], z1[DB_CW];
+#pragma unroll
+    for (int q = 0; q < DB_CW; ++q) {
+      z0[q] = Zs[lane][w * DB_CW + q];
+      z1[q] = Zs[lane + 32][w * DB_CW + q];
     }
-    __syncthreads();
+    for (int c = 0; c < nb - 1; ++c) {
+      const cplx l0 = Ls[lane][c], l1 = Ls[lane + 32][c];
+      const bool hi = c >= 32;
+#pragma unroll
+      for (int q = 0; q < DB_CW; ++q) {
+        const cplx src = hi ? z1[q] : z0[q];
+        cplx zc;
+        zc.x = __shfl_sync(0xffffffffu, src.x, c & 31);
+        zc.y = __shfl_sync(0xffffffffu, src.y, c & 31);
+        if (lane > c) c_fms(z0[q], l0, zc);
+        if (lane + 32 > c) c_fms(z1[q], l1, zc);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < DB_CW; ++q) {
+      Zs[lane][w * DB_CW + q] = z0[q];
+      Zs[lane + 32][w * DB_CW + q] = z1[q];
+    }
   }
+  __syncthreads();
   for (int e = threadIdx.x; e < nb * DB_NC; e += DB_THREADS) {
     const int r = e / DB_NC, c = e % DB_NC;
     if (c0 + c < m) Z[(int64_t)(r0 + r) * m + c0 + c] = Zs[r][c];
@@ -90,13 +116,35 @@ diag_bwd_kernel(const cplx* Fbase, int64_t stride_f, const int8_t* tagsbase, int
     c_fma(Zs[nb - 1][threadIdx.x], e, Z[(int64_t)r1 * m + c0 + threadIdx.x]);
   }
   __syncthreads();
-  for (int c = nb - 1; c > 0; --c) {
-    for (int e = threadIdx.x; e < c * DB_NC; e += DB_THREADS) {
-      const int r = e / DB_NC, cc = e % DB_NC;   // rows r < c
-      c_fms(Zs[r][cc], Ls[c][r], Zs[c][cc]);
+  // (as the forward kernel: rows r < c take z_r -= L_cr z_c in descending c)
+  {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    cplx z0[DB_CW], z1[DB_CW];
+#pragma unroll
+    for (int q = 0; q < DB_CW; ++q) {
+      z0[q] = Zs[lane][w * DB_CW + q];
+      z1[q] = Zs[lane + 32][w * DB_CW + q];
     }
-    __syncthreads();
+    for (int c = nb - 1; c > 0; --c) {
+      const cplx l0 = Ls[c][lane], l1 = Ls[c][lane + 32];
+      const bool hi = c >= 32;
+#pragma unroll
+      for (int q = 0; q < DB_CW; ++q) {
+        const cplx src = hi ? z1[q] : z0[q];
+        cplx zc;
+        zc.x = __shfl_sync(0xffffffffu, src.x, c & 31);
+        zc.y = __shfl_sync(0xffffffffu, src.y, c & 31);
+        if (lane < c) c_fms(z0[q], l0, zc);
+        if (lane + 32 < c) c_fms(z1[q], l1, zc);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < DB_CW; ++q) {
+      Zs[lane][w * DB_CW + q] = z0[q];
+      Zs[lane + 32][w * DB_CW + q] = z1[q];
+    }
   }
+  __syncthreads();
   for (int e = threadIdx.x; e < nb * DB_NC; e += DB_THREADS) {
     const int r = e / DB_NC, c = e % DB_NC;
     if (c0 + c < m) Z[(int64_t)(r0 + r) * m + c0 + c] = Zs[r][c];
