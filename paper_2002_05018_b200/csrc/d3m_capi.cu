@@ -303,11 +303,13 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
     const int rc = d3m_gemm_tma_prepare_solve(F, stride_f, n, work, sz, m, batch, hm.data());
     if (rc == 0) {
       static std::mutex mu;
-      static std::map<int, std::pair<void*, size_t>> bufs;     // per device, grow-only
+      // per (device, stream), grow-only: calls on one stream reuse the buffer in stream order, calls on
+      // different streams (two host threads) never share one
+      static std::map<std::pair<int, void*>, std::pair<void*, size_t>> bufs;
       int dev = 0;
       cudaGetDevice(&dev);
       std::lock_guard<std::mutex> g(mu);
-      auto& bf = bufs[dev];
+      auto& bf = bufs[{dev, stream}];
       if (bf.second < hm.size()) {
         if (bf.first) { cudaStreamSynchronize(s); cudaFree(bf.first); }
         bf = {nullptr, 0};
@@ -315,7 +317,7 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
         else cudaGetLastError();
       }
       // (pageable source: staged before the call returns; the buffer's previous reader is earlier on
-      // this stream or on a stream the caller has already ordered before it)
+      // this stream)
       if (bf.first && cudaMemcpyAsync(bf.first, hm.data(), hm.size(), cudaMemcpyHostToDevice, s) == cudaSuccess)
         d_maps = bf.first;
     } else if (rc != -38) {
