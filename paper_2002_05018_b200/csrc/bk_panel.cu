@@ -312,7 +312,9 @@ __device__ __forceinline__ ClSlot cl_merge(cg::cluster_group& cl, ClSlot* slot, 
 // pivot searches meet in one cluster barrier each (DSMEM slots, double
 // buffered), and the symmetric interchange (global memory, any thread of the
 // cluster) is fenced by one more barrier when it moves data.
-template <int NB, int CS>
+// TRACK: the pivot-decision margin diagnostic (BkArgs::margin) is compiled only into the TRACK instance, so
+// the production kernel keeps its registers (it sits at the 128-register cap of two CTAs per SM).
+template <int NB, int CS, bool TRACK>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(CNT)
 bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned long long* tmax, int maxtiles) {
   cg::cluster_group cl = cg::this_cluster();
@@ -349,7 +351,7 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
   const int ch = (n - k0 + CS - 1) / CS;
   const int lo = min(n, k0 + rank * ch), hi = min(n, lo + ch);
   int k = k0, kw = 0, npiv = 0, info = -1, n2x2 = s.n2x2, par = 0;
-  const bool track = a.margin != nullptr;     // pivot-decision margins (uniform over the cluster)
+  constexpr bool track = TRACK;               // pivot-decision margins
   double mdec = s.mdec, mgap = s.mgap;
   // a step starts only while kw <= NB-2, so a panel is NB-1 or NB columns
   // (zlasyf's exit rule) and the trailing update has K <= NB = 16
@@ -590,7 +592,8 @@ static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* task
   cudaGetDevice(&dev);
   const unsigned long long dbit = 1ull << (dev & 63);
   if (cs == 16 && !(ok16.load() & dbit)) {
-    cudaFuncSetAttribute(bk_panel_kernel<NB, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(bk_panel_kernel<NB, 16, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(bk_panel_kernel<NB, 16, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -602,7 +605,7 @@ static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* task
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, bk_panel_kernel<NB, 16>, &cfg) == cudaSuccess && nclusters > 0)
+    if (cudaOccupancyMaxActiveClusters(&nclusters, bk_panel_kernel<NB, 16, false>, &cfg) == cudaSuccess && nclusters > 0)
       yes16.fetch_or(dbit);
     cudaGetLastError();
     ok16.fetch_or(dbit);
@@ -612,13 +615,17 @@ static int panel_run(BkArgs* a, int batch, BkState* st, cplx* Wp, GemmTask* task
     const int mrem = n - (p + 1) * (NB - 1);           // rows left after this panel (upper bound)
     const int tm = mrem > 0 ? (mrem + 63) / 64 : 0;
     const int maxtiles = tm * (tm + 1) / 2;
+#define D3M_PANEL_LAUNCH(CSV)                                                                                \
+  if (a->margin) bk_panel_kernel<NB, CSV, true><<<batch * CSV, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); \
+  else bk_panel_kernel<NB, CSV, false><<<batch * CSV, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles)
     switch (cs) {
-      case 16: bk_panel_kernel<NB, 16><<<batch * 16, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
-      case 8: bk_panel_kernel<NB, 8><<<batch * 8, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
-      case 4: bk_panel_kernel<NB, 4><<<batch * 4, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
-      case 2: bk_panel_kernel<NB, 2><<<batch * 2, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
-      default: bk_panel_kernel<NB, 1><<<batch, CNT, 0, s>>>(*a, st, Wp, tasks, tmax, maxtiles); break;
+      case 16: D3M_PANEL_LAUNCH(16); break;
+      case 8: D3M_PANEL_LAUNCH(8); break;
+      case 4: D3M_PANEL_LAUNCH(4); break;
+      case 2: D3M_PANEL_LAUNCH(2); break;
+      default: D3M_PANEL_LAUNCH(1); break;
     }
+#undef D3M_PANEL_LAUNCH
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
     if (maxtiles > 0) {
       // rank-<=NB trailing update on the pipelined grouped kernel (C
