@@ -556,3 +556,33 @@ def test_host_staged_upload_under_blocking_launches(cuda):
     env = dict(__import__("os").environ, CUDA_LAUNCH_BLOCKING="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.startswith("ok"), r.stderr[-2000:]
+
+
+def test_tma_and_cp_async_update_gemm_give_the_same_factor(cuda):
+    """block_ldlt with the update GEMMs on the TMA-staged kernel (default) and
+    on the cp.async kernel (D3M_GEMM_TMA=0, read once per process: two
+    subprocesses) produces the same factor pool, pivots and solution bit for
+    bit (ragged supernodes, builtin order, lookahead on)."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = ("import sys, hashlib; sys.path.insert(0, %r)\n"
+            "import numpy as np\n"
+            "import paper_2002_05018_b200 as d\n"
+            "from paper_2002_05018_b200 import workloads as wl\n"
+            "K = wl.config4_matrix(seed=7, grid=(3, 3, 2), n=150)\n"
+            "plan = d.symbolic_factor(d.clique_graph(K), d.reorder(d.clique_graph(K), K.sizes), K.sizes)\n"
+            "F = d.block_ldlt(K, plan)\n"
+            "rhs = wl.config4_rhs(K, nrhs=3)\n"
+            "x = d.block_solve(F, rhs)\n"
+            "h = hashlib.sha256()\n"
+            "h.update(F._pool.cpu().numpy().tobytes())\n"
+            "for b in x: h.update(np.ascontiguousarray(np.asarray(b)).tobytes())\n"
+            "print('sha', h.hexdigest(), F.stats.n_2x2_pivots)\n") % ROOT
+    out = []
+    for tma in ("1", "0"):
+        env = dict(__import__("os").environ, D3M_GEMM_TMA=tma)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0 and r.stdout.startswith("sha"), r.stderr[-2000:]
+        out.append(r.stdout.strip())
+    assert out[0] == out[1]
