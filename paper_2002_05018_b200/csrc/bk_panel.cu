@@ -178,7 +178,7 @@ __global__ void bk_perm_init_kernel(BkArgs a, int batch) {
 // G(i, col) for i >= col (stale column) or G(col, i) for i < col (its row
 // part), col = the target column.  The summation order per row is fixed (4
 // partial sums, butterfly).
-constexpr int PG_ROWS = 4;
+constexpr int PG_ROWS = 3;   // (4: 2-3% slower panels on every config, 2: slower again; r02 A/B)
 template <int NB, int NT>
 __device__ __forceinline__ void panel_gemv(const cplx* __restrict__ W, int lda, int r_lo, int r_hi, int k0, int kw,
                                            int col, const cplx* __restrict__ Wp, int src,
