@@ -234,6 +234,21 @@ __device__ __forceinline__ void panel_gemv(const cplx* __restrict__ W, int lda, 
 template <int NT>
 __device__ __forceinline__ void local_exact_argmax(const cplx* col, int ldw, int r0, int r1, int skip, double& ev,
                                                    int& ei, double* vs, int* is, double* ev2 = nullptr) {
+  if (!ev2 && r1 - r0 <= NT) {
+    // at most one row per thread: the exact moduli directly (one reduction; the proxy passes below
+    // cost two more barriers and two more reads of the column)
+    const int i = r0 + (int)threadIdx.x;
+    double v = -1.0;
+    int vi = 0x7fffffff;
+    if (i < r1 && i != skip) {
+      v = x_abs(col[(int64_t)i * ldw]);
+      vi = i;
+    }
+    pargmax_red<NT>(v, vi, vs, is);
+    ev = v;
+    ei = vi;
+    return;
+  }
   double pv = -1.0, pv2 = -1.0;
   int pi = 0x7fffffff;
   for (int i = r0 + (int)threadIdx.x; i < r1; i += NT)
