@@ -288,6 +288,7 @@ struct ClSlot {       // one CTA's contribution to a cluster-wide pivot search
   double ev2;         // local runner-up (margin diagnostic, -1: none / not tracked)
   int ei;             // first index of ev
   int pad;
+  double dre, dim;    // the published entry itself (owner only): the 1 x 1 pivot value when no rows move
 };
 
 // Gather the CS slots (DSMEM) after a cluster barrier; every CTA merges in the
@@ -296,7 +297,7 @@ template <int CS>
 __device__ __forceinline__ ClSlot cl_merge(cg::cluster_group& cl, ClSlot* slot, ClSlot* out, bool track = false) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    double ev = -1.0, own = -1.0, r2 = -1.0;
+    double ev = -1.0, own = -1.0, r2 = -1.0, dre = 0.0, dim = 0.0;
     int ei = 0x7fffffff;
     if (lane < CS) {
       const ClSlot* p = cl.map_shared_rank(slot, lane);
@@ -304,7 +305,14 @@ __device__ __forceinline__ ClSlot cl_merge(cg::cluster_group& cl, ClSlot* slot, 
       own = p->own;
       r2 = p->ev2;
       ei = p->ei;
+      dre = p->dre;
+      dim = p->dim;
     }
+    // the owner's entry (at most one CTA publishes own >= 0)
+    const unsigned ob = __ballot_sync(0xffffffffu, own >= 0.0);
+    const int ol = ob ? __ffs(ob) - 1 : 0;
+    dre = __shfl_sync(0xffffffffu, dre, ol);
+    dim = __shfl_sync(0xffffffffu, dim, ol);
     const double lv = ev;
     const int li = ei;
 #pragma unroll
@@ -315,7 +323,7 @@ __device__ __forceinline__ ClSlot cl_merge(cg::cluster_group& cl, ClSlot* slot, 
       argmax_merge(ev, ei, ev2, ei2);
     }
     if (track) r2 = warp_max(li == ei ? r2 : lv);   // the winner's runner-up, every other CTA's winner
-    if (lane == 0) { out->ev = ev; out->own = own; out->ei = ei; out->ev2 = r2; }
+    if (lane == 0) { out->ev = ev; out->own = own; out->ei = ei; out->ev2 = r2; out->dre = dre; out->dim = dim; }
   }
   __syncthreads();
   return *out;
@@ -336,6 +344,7 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
   __shared__ double ra[CNT / 32];
   __shared__ int rai[CNT / 32];
   __shared__ ClSlot slots[2], merged;
+  __shared__ double s_own[3];              // |entry|, re, im of the published entry (owner CTA)
   constexpr int LDW = NB + 1;
   const int rank = (int)cl.block_rank();
   const int b = blockIdx.x / CS, n = a.n, lda = a.lda, tid = threadIdx.x;
@@ -384,6 +393,19 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
     __syncthreads();
     PANEL_MARK(0);
     {
+      // the owner of row k publishes |a_kk| and a_kk: read by the last warp's first lane while the
+      // others search (the reductions' barriers publish s_own to thread 0)
+      if (tid == CNT - 32) {
+        cplx dk = mk(0.0, 0.0);
+        double ak = -1.0;
+        if (k >= lo && k < hi) {
+          dk = Wp[(int64_t)k * LDW + kw];
+          ak = x_abs(dk);
+        }
+        s_own[0] = ak;
+        s_own[1] = dk.x;
+        s_own[2] = dk.y;
+      }
       double ev, ev2 = -1.0;
       int ei;
       local_exact_argmax<CNT>(Wp + kw, LDW, max(k + 1, lo), hi, -1, ev, ei, ra, rai, track ? &ev2 : nullptr);
@@ -392,7 +414,9 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
         sl.ev = ev;
         sl.ev2 = ev2;
         sl.ei = ei;
-        sl.own = (k >= lo && k < hi) ? x_abs(Wp[(int64_t)k * LDW + kw]) : -1.0;
+        sl.own = s_own[0];
+        sl.dre = s_own[1];
+        sl.dim = s_own[2];
       }
     }
     PANEL_MARK(1);
@@ -433,6 +457,7 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
           sl.ev = ev;
           sl.ei = ei;
           sl.own = (imax >= lo && imax < hi) ? x_abs(Wp[(int64_t)imax * LDW + kw + 1]) : -1.0;
+          sl.dre = sl.dim = 0.0;
         }
       }
       cl.sync();
@@ -483,15 +508,16 @@ bk_panel_kernel(BkArgs a, BkState* st, cplx* Wp_base, GemmTask* tasks, unsigned 
       }
       if (lead) { const int64_t t0 = perm[kk]; perm[kk] = perm[kp]; perm[kp] = t0; }
       cl.sync();
-    } else {
-      __syncthreads();
     }
+    // (no barrier when no rows move: everything step E reads was written before the barriers of the
+    //  column updates and the pivot searches)
     if (kp != kk) PANEL_COUNT(10);
     PANEL_MARK(5);
     // -- E: store D and the L column(s) of the own rows (packed layout,
     //    kernels.py:7-22)
     if (kstep == 1) {
-      const cplx d = Wp[(int64_t)k * LDW + kw];
+      // the pivot: the owner published it with |a_kk| (no rows moved), else it moved into row k
+      const cplx d = kp == kk ? mk(m1.dre, m1.dim) : Wp[(int64_t)k * LDW + kw];
       const bool re_big = fabs(d.x) >= fabs(d.y);
       const double rat = re_big ? __ddiv_rn(d.y, d.x) : __ddiv_rn(d.x, d.y);
       const double scl = re_big ? __ddiv_rn(1.0, __dadd_rn(d.x, __dmul_rn(d.y, rat)))
