@@ -178,6 +178,10 @@ __global__ void bk_perm_init_kernel(BkArgs a, int batch) {
 // G(i, col) for i >= col (stale column) or G(col, i) for i < col (its row
 // part), col = the target column.  The summation order per row is fixed (4
 // partial sums, butterfly).
+#ifndef D3M_EXACT_ROWS
+#define D3M_EXACT_ROWS 2
+#endif
+constexpr int kExactRows = D3M_EXACT_ROWS;   // rows per thread up to which the pivot search takes exact moduli directly
 constexpr int PG_ROWS = 3;   // (4: 2-3% slower panels on every config, 2: slower again; r02 A/B)
 template <int NB, int NT>
 __device__ __forceinline__ void panel_gemv(const cplx* __restrict__ W, int lda, int r_lo, int r_hi, int k0, int kw,
@@ -234,16 +238,13 @@ __device__ __forceinline__ void panel_gemv(const cplx* __restrict__ W, int lda, 
 template <int NT>
 __device__ __forceinline__ void local_exact_argmax(const cplx* col, int ldw, int r0, int r1, int skip, double& ev,
                                                    int& ei, double* vs, int* is, double* ev2 = nullptr) {
-  if (!ev2 && r1 - r0 <= NT) {
-    // at most one row per thread: the exact moduli directly (one reduction; the proxy passes below
-    // cost two more barriers and two more reads of the column)
-    const int i = r0 + (int)threadIdx.x;
+  if (!ev2 && r1 - r0 <= kExactRows * NT) {
+    // few rows per thread: the exact moduli directly (one reduction; the proxy passes below cost two
+    // more barriers and two more reads of the column)
     double v = -1.0;
     int vi = 0x7fffffff;
-    if (i < r1 && i != skip) {
-      v = x_abs(col[(int64_t)i * ldw]);
-      vi = i;
-    }
+    for (int i = r0 + (int)threadIdx.x; i < r1; i += NT)
+      if (i != skip) argmax_merge(v, vi, x_abs(col[(int64_t)i * ldw]), i);
     pargmax_red<NT>(v, vi, vs, is);
     ev = v;
     ei = vi;
