@@ -477,7 +477,7 @@ def _cfg3_secondary(steps: int, peak: float) -> dict:
     # one event pair per step, median over the steps: single steps on this pool stall by 20-40 ms now
     # and then (host-side, with and without any of this round's kernels: tools/_sec2-style repeats)
     samples = []
-    for _ in range(max(steps, 5)):
+    for _ in range(max(steps, 9)):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         for s in dev:
             s.factor = None

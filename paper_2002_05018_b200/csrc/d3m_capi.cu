@@ -290,40 +290,70 @@ static int ldlt_solve_blocked_impl(int batch, int n, const void* F, int64_t stri
     tiles[ib] = d3m_gemm_prepare_tasks(&t[(size_t)ib * T], T);
     tiles[nblk + ib] = d3m_gemm_prepare_tasks(&t[(size_t)(nblk + ib) * T], T);
   }
-  cudaError_t e = cudaMemcpyAsync(d_tasks, t.data(), sizeof(d3m::GemmTask) * t.size(), cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return fail((int)e, "d3m_ldlt_solve_blocked_batched: task upload");
-  auto* dt = static_cast<const d3m::GemmTask*>(d_tasks);
+  // The task table and the tensor maps go up from a pinned, event-guarded staging buffer kept per
+  // (device, stream): a copy from pageable memory of this size would synchronise the stream first, i.e.
+  // hold the host until the factorisation before this solve has finished, and the solve's launches would
+  // then be enqueued with the GPU idle.
   // TMA-staged updates (3M form; D3M_SOLVE_TMA=0: the cp.async grouped kernel): per matrix tensor maps over
-  // the factor and the work array, kept in a per-device buffer.  A launch qualifies when its k range is a
-  // multiple of 16 (all but a ragged last block): rows past K inside the matrices are data, not zeros.
+  // the factor and the work array.  A launch qualifies when its k range is a multiple of 16 (all but a
+  // ragged last block): rows past K inside the matrices are data, not zeros.
+  const size_t task_bytes = sizeof(d3m::GemmTask) * t.size();
+  const size_t map_bytes = (size_t)batch * 4 * 128;
   const char* tma_str = getenv("D3M_SOLVE_TMA");
+  const bool want_tma = !(tma_str && atoi(tma_str) == 0) && d3m_gemm_set_form(0) == 3;
   const void* d_maps = nullptr;
-  if (!(tma_str && atoi(tma_str) == 0) && d3m_gemm_set_form(0) == 3 ) {
-    std::vector<unsigned char> hm((size_t)batch * 4 * 128);
-    const int rc = d3m_gemm_tma_prepare_solve(F, stride_f, n, work, sz, m, batch, hm.data());
-    if (rc == 0) {
-      static std::mutex mu;
-      // per (device, stream), grow-only: calls on one stream reuse the buffer in stream order, calls on
-      // different streams (two host threads) never share one
-      static std::map<std::pair<int, void*>, std::pair<void*, size_t>> bufs;
-      int dev = 0;
-      cudaGetDevice(&dev);
-      std::lock_guard<std::mutex> g(mu);
-      auto& bf = bufs[{dev, stream}];
-      if (bf.second < hm.size()) {
-        if (bf.first) { cudaStreamSynchronize(s); cudaFree(bf.first); }
-        bf = {nullptr, 0};
-        if (cudaMalloc(&bf.first, hm.size()) == cudaSuccess) bf.second = hm.size();
-        else cudaGetLastError();
-      }
-      // (pageable source: staged before the call returns; the buffer's previous reader is earlier on
-      // this stream)
-      if (bf.first && cudaMemcpyAsync(bf.first, hm.data(), hm.size(), cudaMemcpyHostToDevice, s) == cudaSuccess)
-        d_maps = bf.first;
-    } else if (rc != -38) {
-      return fail(rc, "d3m_ldlt_solve_blocked_batched: tensor map");
+  {
+    struct Stage {
+      void* host = nullptr;      // pinned: [tasks | maps]
+      size_t host_cap = 0;
+      void* dev_maps = nullptr;
+      size_t dev_cap = 0;
+      cudaEvent_t done = nullptr;
+    };
+    static std::mutex mu;
+    static std::map<std::pair<int, void*>, Stage> stages;      // grow-only
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    Stage& st = stages[{dev, stream}];
+    if (!st.done && cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming) != cudaSuccess)
+      return fail(-12, "d3m_ldlt_solve_blocked_batched: event");
+    cudaEventSynchronize(st.done);                             // the previous call's copies have left the buffer
+    const size_t need = task_bytes + map_bytes;
+    if (st.host_cap < need) {
+      if (st.host) cudaFreeHost(st.host);
+      st.host = nullptr;
+      st.host_cap = 0;
+      if (cudaMallocHost(&st.host, need) != cudaSuccess) return fail(-12, "d3m_ldlt_solve_blocked_batched: pinned staging");
+      st.host_cap = need;
     }
+    std::memcpy(st.host, t.data(), task_bytes);
+    unsigned char* hm = static_cast<unsigned char*>(st.host) + task_bytes;
+    bool maps_ok = false;
+    if (want_tma) {
+      const int rc = d3m_gemm_tma_prepare_solve(F, stride_f, n, work, sz, m, batch, hm);
+      if (rc == 0) {
+        if (st.dev_cap < map_bytes) {
+          if (st.dev_maps) { cudaStreamSynchronize(s); cudaFree(st.dev_maps); }
+          st.dev_maps = nullptr;
+          st.dev_cap = 0;
+          if (cudaMalloc(&st.dev_maps, map_bytes) == cudaSuccess) st.dev_cap = map_bytes;
+          else cudaGetLastError();
+        }
+        maps_ok = st.dev_maps != nullptr;
+      } else if (rc != -38) {
+        return fail(rc, "d3m_ldlt_solve_blocked_batched: tensor map");
+      }
+    }
+    cudaError_t e = cudaMemcpyAsync(d_tasks, st.host, task_bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && maps_ok) {
+      e = cudaMemcpyAsync(st.dev_maps, hm, map_bytes, cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) d_maps = st.dev_maps;
+    }
+    cudaEventRecord(st.done, s);
+    if (e != cudaSuccess) return fail((int)e, "d3m_ldlt_solve_blocked_batched: task upload");
   }
+  auto* dt = static_cast<const d3m::GemmTask*>(d_tasks);
   const char* d_fwd_maps = static_cast<const char*>(d_maps);
   const char* d_bwd_maps = d_fwd_maps ? d_fwd_maps + (size_t)batch * 2 * 128 : nullptr;
   auto tma_ok = [&](int task_row) { return d_maps && (t[(size_t)task_row * T].k % 16) == 0; };
