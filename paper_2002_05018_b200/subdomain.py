@@ -170,7 +170,10 @@ class SparseBlock:
         return self.toarray().T
 
     @staticmethod
-    def hconcat(blocks) -> "SparseBlock":
+    def hconcat(blocks, sort: bool = True) -> "SparseBlock":
+        """[D_1 | D_2 | ...] as one block.  ``sort=False`` skips the key sort
+        (the argsort is most of the cost, ~1.5 ms per config-2 domain): enough
+        for a device scatter, which takes the entries in any order."""
         n = blocks[0].shape[0]
         m = sum(b.shape[1] for b in blocks)
         keys, vals, off = [], [], 0
@@ -181,15 +184,17 @@ class SparseBlock:
             off += b.shape[1]
         k = np.concatenate(keys) if keys else np.zeros(0, np.int64)
         v = np.concatenate(vals) if vals else np.zeros(0, np.complex128)
-        o = np.argsort(k, kind="stable")
-        out = SparseBlock((n, m), k[o], v[o])
+        if sort:
+            o = np.argsort(k, kind="stable")
+            k, v = k[o], v[o]
+        out = SparseBlock((n, m), k, v)
         out._transient = True          # built per call: not worth page-locking
         return out
 
 
-def _coupling_matrix(sys: SubdomainSystem):
+def _coupling_matrix(sys: SubdomainSystem, sort: bool = True):
     if sys.couplings and all(isinstance(c.D, SparseBlock) for c in sys.couplings):
-        return SparseBlock.hconcat([c.D for c in sys.couplings])
+        return SparseBlock.hconcat([c.D for c in sys.couplings], sort=sort)
     if sys.couplings:
         return np.concatenate([np.asarray(c.D, dtype=np.complex128) for c in sys.couplings], axis=1)
     return np.zeros((sys.n_dofs, 0), dtype=np.complex128)
@@ -330,7 +335,7 @@ def _fill_inputs(systems, members, n, ms, A, D, f):
             elif len(s.couplings) == 1:
                 _fill(D[i, :, :mr], s.couplings[0].D, (n, mr))
             else:
-                _fill(D[i, :, :mr], _coupling_matrix(s), (n, mr))
+                _fill(D[i, :, :mr], _coupling_matrix(s, sort=False), (n, mr))     # scattered on the device
         _fill(f[i], s.f, (n, f.shape[2]))
 
 
