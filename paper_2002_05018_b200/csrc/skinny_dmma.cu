@@ -543,9 +543,15 @@ extern "C" int d3m_block_solve_flow_launch(void* plan, const void* items, int ni
     g_flow_trace = trace;
     g_flow_trace_n = nitems;
   }
-  // chain SMs: 24 (A/B on config 4, three CTAs per SM elsewhere: 16 7.24,
-  // 24 6.78, 32 6.80 ms per 16-RHS pass; one queue on two CTAs per SM 7.4)
-  int csms = 24;
+  // chain SMs: 32.  A block column of config 4 puts 48 items on the chain
+  // queue per sweep step (16 BC tiles, 16 BR pieces, 16 BE tiles).  With 24
+  // chain CTAs the rotation has two stable phases, picked by the start-up
+  // race: all 16 BC tiles held before x_{j+1} lands (5.97 ms per 16-RHS
+  // pass), or 8 of them taken one round late (7.55 ms, about 40% of the
+  // passes; tools/flow_modes.py, tools/solve_mode_probe.py).  32 chain CTAs
+  // always hold the 16 BC tiles in time: 5.94-6.06 ms, every pass (16 SMs x
+  // 2 CTAs: 6.03; 48: 6.19; 16 x 3: 6.21; 16 x 1: 7.24 ms).
+  int csms = 32;
   void* args[] = {const_cast<SolvePlanDev*>(pl), &it, &nitems, &nchain, &csms, &dp, &po, &c, &sc, &tr};
   e = cudaLaunchCooperativeKernel((void*)block_solve_dataflow, dim3(grid), dim3(SN_NT), args, kSnSmem, s);
   return (int)e;
